@@ -1,0 +1,353 @@
+"""bench.py — MCA attention-layer throughput on B200 (BASELINE.json metric).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config c2|c1|c3|c4] [--alpha A] [--dtype bf16|f32]
+
+One step = one MCA attention-layer forward (score pass + Eq. 9 budgets +
+sampled encoding + A.H~) over one batch of synthetic BERT-shaped inputs
+already resident in HBM. Default workload: BASELINE.json configs[1] — BERT-base
+(d=768, 12 heads of 64), B=64 sequences of n=512 per GPU, bf16, alpha=0.4.
+
+Multi-GPU (torchrun, one process per GPU): every rank runs its own B=64
+sequences with b_offset = rank*B (weak scaling; no collective in the hot
+path). Time = max over ranks of the device-timed total; NCCL is used only for
+the barrier/max and, after timing, to gather per-rank checksums for
+validation.
+
+The JSON line also carries:
+  e2e           the same metric through the C ABI with HOST buffers: pinned
+                H2D of q/k/x, forward, D2H of y inside the timed region
+  roofline      the dominant kernel's achieved algorithmic GB/s or TFLOP/s vs
+                MEASURED_PEAKS.json (DESIGN.md §7 defines the per-unit work)
+  cpu_baseline  the fp64 CPU oracle (the reference algorithm, test
+                infrastructure) on this host's cores, bounded sample
+  clocks        nvidia-smi samples taken while the benchmark ran
+`--impl reference` times the CPU reference path (the oracle port; the
+reference itself ships no definitions) on the same config, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MCA attn-layer tokens/sec @BERT-base/large 1/2/4/8 B200; HBM GB/s frac; FLOP cut"
+
+CONFIGS = {
+    # name: (B per GPU, n, d_in, heads, description)
+    "c1": (1, 128, 768, 12, "BERT-base MCA attention layer, B=1, n=128 (configs[0])"),
+    "c2": (64, 512, 768, 12, "BERT-base MCA attention layer, B=64, n=512, 1 B200 per 64 sequences (configs[1])"),
+    "c3": (128, 512, 1024, 16, "BERT-large MCA attention layer, B=128, n=512 (configs[2], one layer)"),
+    "c4": (16, 4096, 768, 12, "long-sequence BERT-base MCA layer, B=16, n=4096 (configs[3])"),
+}
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return {"hbm_gbs": p["hbm_gbs"], "bf16_tflops": p["bf16_tflops"], "src": "measured"}
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "src": "fallback"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms."""
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.sw_power_cap,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown")
+
+    def __init__(self, device_index: int):
+        self.idx = device_index
+        self.samples = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.samples.append(parts)
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+        time.sleep(0.05)
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        load = [v for v in sm if v > 0.5 * (max(sm) if sm else 1)]
+        names = ["sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------- CPU legs
+def cpu_reference_rate(cfg_name: str, alpha: float, budget_s: float, threads: int):
+    """Tokens/s of the fp64 CPU oracle (oracle/, the reference algorithm) on a
+    bounded sample of the workload: whole sequences until ~budget_s seconds."""
+    from oracle import oracle as orc
+    from paper_2201_12854_b200 import synthetic
+    B, n, d_in, H, _ = CONFIGS[cfg_name]
+    orc.set_threads(threads)
+    w = synthetic.make_weights(d_in, H).double().numpy()
+    done_tokens, t_total, b = 0, 0.0, 0
+    per = max(1, threads)  # sequences per call: keep every thread busy on (b, h) pairs
+    while t_total < budget_s and b < 4 * B:
+        inp = synthetic.make_inputs(per, n, d_in, H, seed=1234 + b)
+        q, k, x = (t.double().numpy() for t in (inp.q, inp.k, inp.x))
+        t0 = time.perf_counter()
+        orc.batched_forward(q, k, x, w, heads=H, alpha=alpha, seed=42, b_offset=b, want_h=False)
+        t_total += time.perf_counter() - t0
+        done_tokens += per * n
+        b += per
+    return done_tokens / t_total, f"{b} sequences of n={n} ({done_tokens} tokens), fp64, {threads} threads", t_total
+
+
+def run_reference(args, rank: int):
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    B, n, d_in, H, desc = CONFIGS[args.config]
+    per_step_budget = max(2.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
+    rates = []
+    for i in range(args.warmup + args.steps):
+        r, sample, _ = cpu_reference_rate(args.config, args.alpha, per_step_budget, threads)
+        if i >= args.warmup:
+            rates.append(r)
+    value = statistics.median(rates)
+    line = {"metric": METRIC, "impl": "reference", "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * B * n / value,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": desc, "B": B, "n": n, "d_in": d_in, "heads": H, "d_h": 64, "alpha": args.alpha,
+                       "seed": 42},
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "note": "reference ships declarations only (matrix.hpp); the CPU reference path is the fp64 SPEC "
+                    "restatement in oracle/ (OpenMP over (b, h)), timed on this host's cores"}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- GPU leg
+def algorithmic_work(B, n, d_in, H, elem):
+    dh = 64
+    flops_qk = 2.0 * B * H * n * n * dh
+    k3_bytes = B * n * d_in * elem + B * n * H * dh * elem + 4.0 * B * H * n + H * d_in * (dh * elem + 12)
+    k2_bytes = B * H * n * (8 + 4 + 1)
+    return {"score": ("tensor", flops_qk), "budgets": ("hbm", k2_bytes), "encode": ("hbm", k3_bytes),
+            "apply": ("tensor", flops_qk)}
+
+
+def run_ours(args, rank: int, world: int, local_rank: int):
+    import torch
+
+    import paper_2201_12854_b200 as mca
+    from paper_2201_12854_b200 import synthetic
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    B, n, d_in, H, desc = CONFIGS[args.config]
+    dtype = torch.bfloat16 if args.dtype == "bf16" else torch.float32
+    elem = 2 if dtype == torch.bfloat16 else 4
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+
+    w = synthetic.make_weights(d_in, H).to(dtype)
+    inp = synthetic.make_inputs(B, n, d_in, H, seed=1234 + rank)  # rank's own shard of the global batch
+    weights = mca.AttentionWeights(w.to(dev), heads=H)
+    q, k, x = (t.to(dtype).to(dev) for t in (inp.q, inp.k, inp.x))
+    y = torch.empty_like(q)
+    cfg = mca.McaConfig(alpha=args.alpha)
+    b_offset = rank * B
+    weights.reserve(B * n)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
+    stream = torch.cuda.current_stream()
+
+    def step():
+        mca.mca_forward(weights, q, k, x, cfg, seed=42, b_offset=b_offset, y=y)
+
+    out = mca.mca_forward(weights, q, k, x, cfg, seed=42, b_offset=b_offset, y=y, flops=True, return_plan=True)
+    flops_report = out.flops
+    launches_per_step = weights.last_launch_count()
+
+    sampler = ClockSampler(local_rank) if rank == 0 else None
+    if sampler:
+        sampler.start()
+    weights.set_timing(True)
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    stage_tot = [0.0, 0.0, 0.0, 0.0]
+    for i in range(args.steps):
+        flush.zero_()                                   # L2 flushed between timed steps (untimed)
+        starts[i].record(stream)
+        step()
+        ends[i].record(stream)
+        st = weights.last_stage_ms()                    # events on the forward's own stream
+        for s in range(len(st)):
+            stage_tot[s] += st[s]
+    torch.cuda.synchronize()
+    total_ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
+    if dist:
+        t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    weights.set_timing(False)
+    ms_per_step = total_ms / args.steps
+    value = world * B * n / (ms_per_step / 1e3)
+
+    # e2e: host buffers through the C ABI (pinned H2D + forward + D2H), same stream
+    hq, hk, hx = (t.to(dtype).pin_memory() for t in (inp.q, inp.k, inp.x))
+    hy = torch.empty(y.shape, dtype=dtype).pin_memory()
+    dq, dk, dx = torch.empty_like(q), torch.empty_like(k), torch.empty_like(x)
+
+    def e2e_step():
+        dq.copy_(hq, non_blocking=True)
+        dk.copy_(hk, non_blocking=True)
+        dx.copy_(hx, non_blocking=True)
+        mca.mca_forward(weights, dq, dk, dx, cfg, seed=42, b_offset=b_offset, y=y)
+        hy.copy_(y, non_blocking=True)
+
+    for _ in range(max(1, args.warmup)):
+        e2e_step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / args.steps
+    if dist:
+        t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    clocks = sampler.stop() if sampler else None
+
+    # validation gather (outside timing): per-rank checksums of y and the plan
+    chk = torch.tensor([float(y.double().sum()), float(out.budgets.double().sum())], device=dev, dtype=torch.float64)
+    if dist:
+        allc = [torch.empty_like(chk) for _ in range(world)]
+        dist.all_gather(allc, chk)
+        checksums = [c.tolist() for c in allc]
+    else:
+        checksums = [chk.tolist()]
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+
+    peaks = _peaks()
+    work = algorithmic_work(B, n, d_in, H, elem)
+    names = ["score", "budgets", "encode", "apply"]
+    stage_ms = {names[i]: stage_tot[i] / args.steps for i in range(4)}
+    dom = max(names, key=lambda s: stage_ms[s])
+    bound, amount = work[dom]
+    if bound == "tensor":
+        achieved = amount / (stage_ms[dom] / 1e3) / 1e12
+        roof = {"kernel": dom, "bound": "tensor", "achieved": achieved, "peak": peaks["bf16_tflops"],
+                "unit": "TFLOP/s", "frac": achieved / peaks["bf16_tflops"]}
+    else:
+        achieved = amount / (stage_ms[dom] / 1e3) / 1e9
+        roof = {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": achieved / peaks["hbm_gbs"]}
+    roof["peak_src"] = peaks["src"]
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get(dom)
+        except Exception:
+            traffic = None
+    roof["traffic"] = traffic
+    enc_gbs = work["encode"][1] / (stage_ms["encode"] / 1e3) / 1e9
+    gather_gbs = flops_report.samples * 64 * elem / (stage_ms["encode"] / 1e3) / 1e9
+
+    cpu = None
+    if not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        rate, sample, _ = cpu_reference_rate(args.config, args.alpha, args.cpu_seconds, threads)
+        cpu = {"value": rate, "unit": "tokens/s", "cores": threads, "kind": "port", "sample": sample}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
+        "config": {"workload": desc, "global_batch": world * B, "B_per_gpu": B, "seq_len": n, "d_in": d_in,
+                   "heads": H, "d_h": 64, "alpha": args.alpha, "seed": 42, "parallelism": f"dp{world} (batch shards)",
+                   "l2": "flushed (256 MB write) before every timed step"},
+        "e2e": {"value": world * B * n / (e2e_ms / 1e3), "unit": "tokens/s",
+                "h2d_bytes_per_step": int(3 * q.numel() * elem), "d2h_bytes_per_step": int(y.numel() * elem)},
+        "roofline": roof,
+        "stages_ms": stage_ms,
+        "encode": {"algorithmic_GBps": enc_gbs, "hbm_frac": enc_gbs / peaks["hbm_gbs"], "gather_GBps": gather_gbs,
+                   "samples_per_step": flops_report.samples, "exact_token_heads": flops_report.exact_tokens},
+        "flop_cut": {"reduction_factor": flops_report.reduction_factor,
+                     "total_reduction": flops_report.total_reduction},
+        "gpu_launches": launches_per_step * args.steps,
+        "cpu_baseline": cpu,
+        "clocks": clocks,
+        "validation": {"rank_checksums": checksums},
+    }
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--alpha", type=float, default=0.4)
+    ap.add_argument("--dtype", default="bf16", choices=["bf16", "f32"])
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank)
+    else:
+        run_ours(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

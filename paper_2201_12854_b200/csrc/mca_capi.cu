@@ -1,0 +1,452 @@
+// mca_capi.cu — host side of the C ABI (include/mca/mca_cuda.h).
+//
+// Owns the prepared weights and the forward's workspace, validates arguments
+// into SPEC error classes, and enqueues K0..K4 on the caller's stream. There
+// is no CPU compute path: every stage of the forward runs on the GPU, and a
+// missing device is reported as MCA_ERR_CUDA.
+//
+// Unity build: the kernel translation units are included here so one nvcc
+// invocation produces libmca_b200.so (no relocatable device code needed).
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "mca/mca_cuda.h"
+
+#include "k0_weights.cu"
+#include "k1_scores_simt.cu"
+// #include "k1_scores_tc.cu"
+#include "k2_budgets.cu"
+#include "k3_encode.cu"
+#include "k4_apply_simt.cu"
+// #include "k4_apply_tc.cu"
+
+using namespace mca_dev;
+
+namespace {
+
+thread_local std::string g_err;
+
+mca_status fail(mca_status s, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return s;
+}
+
+#define MCA_CUDA_TRY(expr)                                                                                   \
+    do {                                                                                                     \
+        cudaError_t e_ = (expr);                                                                             \
+        if (e_ != cudaSuccess)                                                                               \
+            return fail(MCA_ERR_CUDA, "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(e_), __FILE__, __LINE__); \
+    } while (0)
+
+#define MCA_LAUNCH_CHECK(name)                                                                               \
+    do {                                                                                                     \
+        cudaError_t e_ = cudaGetLastError();                                                                 \
+        if (e_ != cudaSuccess) return fail(MCA_ERR_CUDA, "launch of %s failed: %s", name, cudaGetErrorString(e_)); \
+        ++launches;                                                                                          \
+    } while (0)
+
+size_t dtype_size(mca_dtype t) { return t == MCA_BF16 ? 2 : 4; }
+
+int sm_count() {
+    static int c = 0;
+    if (!c) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&c, cudaDevAttrMultiProcessorCount, dev);
+        if (c <= 0) c = 148;
+    }
+    return c;
+}
+
+}  // namespace
+
+struct mca_weights {
+    int d_in = 0, heads = 0, dh = 0;
+    mca_dtype wdt = MCA_F32;
+    int device = 0;
+    void* w = nullptr;            // [d_in, heads*dh] copy of W_V
+    double* probs = nullptr;      // [heads, d_in]
+    double* cdf = nullptr;        // [heads, d_in]
+    uint64_t* thr = nullptr;      // [heads, d_in]
+    float* invp = nullptr;        // [heads, d_in]
+    uint16_t* guide = nullptr;    // [heads, kGuide]
+    // workspace (grown on demand)
+    long cap_tokens = 0;          // capacity in B*n tokens
+    float* lse = nullptr;                     // [B, H, n]
+    double* row_m = nullptr;                  // [B, H, n] row max of the scaled scores
+    double* row_l = nullptr;                  // [B, H, n] row sum of exp(t - m)
+    unsigned long long* colkey = nullptr;     // [B, H, n]
+    int32_t* budgets = nullptr;               // [B, H, n]
+    uint8_t* exact = nullptr;                 // [B, H, n]
+    void* hbuf = nullptr;                     // [B, n, H*dh]
+    unsigned long long* counters = nullptr;   // [8]
+    int* chunk_counter = nullptr;             // [heads]
+    // timing
+    bool timing = false;
+    cudaEvent_t ev[5] = {};
+    bool ev_valid = false;
+    int last_launches = 0;
+};
+
+namespace {
+
+void free_workspace(mca_weights* w) {
+    cudaFree(w->lse);
+    cudaFree(w->row_m);
+    cudaFree(w->row_l);
+    cudaFree(w->colkey);
+    cudaFree(w->budgets);
+    cudaFree(w->exact);
+    cudaFree(w->hbuf);
+    w->lse = nullptr;
+    w->row_m = nullptr;
+    w->row_l = nullptr;
+    w->colkey = nullptr;
+    w->budgets = nullptr;
+    w->exact = nullptr;
+    w->hbuf = nullptr;
+    w->cap_tokens = 0;
+}
+
+mca_status ensure_workspace(mca_weights* w, long tokens, mca_stream_t stream) {
+    if (tokens <= w->cap_tokens) return MCA_OK;
+    if (w->cap_tokens) MCA_CUDA_TRY(cudaStreamSynchronize(stream));  // old buffers may still be in use
+    free_workspace(w);
+    const size_t th = (size_t)tokens * w->heads;
+    if (cudaMalloc(&w->lse, th * sizeof(float)) != cudaSuccess ||
+        cudaMalloc(&w->row_m, th * sizeof(double)) != cudaSuccess ||
+        cudaMalloc(&w->row_l, th * sizeof(double)) != cudaSuccess ||
+        cudaMalloc(&w->colkey, th * sizeof(unsigned long long)) != cudaSuccess ||
+        cudaMalloc(&w->budgets, th * sizeof(int32_t)) != cudaSuccess ||
+        cudaMalloc(&w->exact, th * sizeof(uint8_t)) != cudaSuccess ||
+        cudaMalloc(&w->hbuf, th * w->dh * dtype_size(w->wdt)) != cudaSuccess) {
+        cudaGetLastError();
+        free_workspace(w);
+        return fail(MCA_ERR_ALLOC, "workspace allocation for %ld tokens failed", tokens);
+    }
+    w->cap_tokens = tokens;
+    return MCA_OK;
+}
+
+mca_status check_config(const mca_config* cfg, bool need_alpha) {
+    if (!cfg) return fail(MCA_ERR_NULL, "cfg is NULL");
+    if (cfg->mode != MCA_MODE_APPROX && cfg->mode != MCA_MODE_REGULAR)
+        return fail(MCA_ERR_CONFIG, "unknown mode %d", cfg->mode);
+    if (need_alpha && cfg->mode == MCA_MODE_APPROX && !(cfg->alpha > 0.0 && cfg->alpha <= 1.0))
+        return fail(MCA_ERR_DOMAIN, "alpha = %g is not in (0, 1] (SPEC.md:270, 353)", cfg->alpha);
+    if (cfg->min_samples < 1) return fail(MCA_ERR_DOMAIN, "min_samples = %d must be >= 1", cfg->min_samples);
+    return MCA_OK;
+}
+
+template <class T, class Acc>
+mca_status launch_k3(mca_weights* w, const void* x, int B, int n, long b_offset, uint32_t layer, uint64_t seed,
+                     void* hout, int32_t* draws, int draws_stride, mca_stream_t stream, int& launches) {
+    using Coef = typename CoefT<T>::type;
+    size_t smem = k3_smem_bytes(w->d_in, sizeof(T), sizeof(Coef), true);
+    bool wsmem = smem <= 200 * 1024;
+    if (!wsmem) smem = k3_smem_bytes(w->d_in, sizeof(T), sizeof(Coef), false);
+    auto kern = wsmem ? k3_encode<T, Acc, true> : k3_encode<T, Acc, false>;
+    MCA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int occ = 0;
+    MCA_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kK3Threads, smem));
+    if (occ < 1) occ = 1;
+    const int chunks = B * ((n + kChunk - 1) / kChunk);
+    int G = (sm_count() * occ + w->heads - 1) / w->heads;
+    if (G > chunks) G = chunks;
+    if (G < 1) G = 1;
+    kern<<<dim3(G, w->heads), kK3Threads, smem, stream>>>(
+        (const T*)x, (const T*)w->w, w->d_in, w->heads, n, B, b_offset, layer, seed, w->budgets, w->exact, w->thr,
+        w->guide, w->probs, w->invp, (T*)hout, draws, draws_stride, w->counters + 3, w->chunk_counter);
+    MCA_LAUNCH_CHECK("k3_encode");
+    return MCA_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* mca_last_error(void) { return g_err.c_str(); }
+const char* mca_version(void) { return "mca_b200 0.1 (sm_100a)"; }
+
+mca_status mca_prepare_weights(const void* w_v, mca_dtype wdt, int d_in, int heads, int d_h, mca_stream_t stream,
+                               mca_weights** out) {
+    if (!out || !w_v) return fail(MCA_ERR_NULL, "w_v / out is NULL");
+    *out = nullptr;
+    if (wdt != MCA_F32 && wdt != MCA_BF16) return fail(MCA_ERR_CONFIG, "unknown dtype %d", (int)wdt);
+    if (d_in <= 0 || heads <= 0 || d_h <= 0) return fail(MCA_ERR_SHAPE, "d_in, heads, d_h must be positive");
+    if (d_h != kDh) return fail(MCA_ERR_UNSUPPORTED, "d_h = %d: the sm_100a kernels implement d_h = 64", d_h);
+    if (d_in > 65535) return fail(MCA_ERR_UNSUPPORTED, "d_in = %d exceeds the 16-bit guide table", d_in);
+    int dev_count = 0;
+    if (cudaGetDeviceCount(&dev_count) != cudaSuccess || dev_count == 0) {
+        cudaGetLastError();
+        return fail(MCA_ERR_CUDA, "no CUDA device: the MCA forward has no CPU path");
+    }
+    mca_weights* w = new mca_weights();
+    w->d_in = d_in;
+    w->heads = heads;
+    w->dh = d_h;
+    w->wdt = wdt;
+    cudaGetDevice(&w->device);
+    const size_t wbytes = (size_t)d_in * heads * d_h * dtype_size(wdt);
+    const size_t hd = (size_t)heads * d_in;
+    double* sq = nullptr;
+    int* status = nullptr;
+    auto cleanup = [&](mca_status s) {
+        cudaFree(sq);
+        cudaFree(status);
+        if (s != MCA_OK) mca_weights_free(w);
+        return s;
+    };
+    if (cudaMalloc(&w->w, wbytes) != cudaSuccess || cudaMalloc(&w->probs, hd * 8) != cudaSuccess ||
+        cudaMalloc(&w->cdf, hd * 8) != cudaSuccess || cudaMalloc(&w->thr, hd * 8) != cudaSuccess ||
+        cudaMalloc(&w->invp, hd * 4) != cudaSuccess || cudaMalloc(&w->guide, (size_t)heads * kGuide * 2) != cudaSuccess ||
+        cudaMalloc(&w->counters, 8 * sizeof(unsigned long long)) != cudaSuccess ||
+        cudaMalloc(&w->chunk_counter, heads * sizeof(int)) != cudaSuccess || cudaMalloc(&sq, hd * 8) != cudaSuccess ||
+        cudaMalloc(&status, heads * sizeof(int)) != cudaSuccess) {
+        cudaGetLastError();
+        return cleanup(fail(MCA_ERR_ALLOC, "weight table allocation failed"));
+    }
+    if (cudaMemcpyAsync(w->w, w_v, wbytes, cudaMemcpyDeviceToDevice, stream) != cudaSuccess)
+        return cleanup(fail(MCA_ERR_CUDA, "copying w_v failed: %s", cudaGetErrorString(cudaGetLastError())));
+    const dim3 g0((d_in + 255) / 256, heads);
+    if (wdt == MCA_F32) k0_row_sq<float><<<g0, 256, 0, stream>>>((const float*)w->w, d_in, heads, sq);
+    else k0_row_sq<__nv_bfloat16><<<g0, 256, 0, stream>>>((const __nv_bfloat16*)w->w, d_in, heads, sq);
+    k0_dist<<<heads, 256, 0, stream>>>(sq, d_in, w->probs, w->cdf, w->thr, w->invp, w->guide, status);
+    std::vector<int> hs(heads);
+    if (cudaMemcpyAsync(hs.data(), status, heads * sizeof(int), cudaMemcpyDeviceToHost, stream) != cudaSuccess ||
+        cudaStreamSynchronize(stream) != cudaSuccess)
+        return cleanup(fail(MCA_ERR_CUDA, "K0 failed: %s", cudaGetErrorString(cudaGetLastError())));
+    for (int h = 0; h < heads; ++h)
+        if (hs[h]) return cleanup(fail(MCA_ERR_DEGENERATE, "head %d: W_h is zero or non-finite (SPEC.md:205)", h));
+    *out = w;
+    return cleanup(MCA_OK);
+}
+
+void mca_weights_free(mca_weights* w) {
+    if (!w) return;
+    free_workspace(w);
+    cudaFree(w->w);
+    cudaFree(w->probs);
+    cudaFree(w->cdf);
+    cudaFree(w->thr);
+    cudaFree(w->invp);
+    cudaFree(w->guide);
+    cudaFree(w->counters);
+    cudaFree(w->chunk_counter);
+    for (auto& e : w->ev)
+        if (e) cudaEventDestroy(e);
+    delete w;
+}
+
+mca_status mca_weights_export(const mca_weights* w, double* probs_host, double* cdf_host) {
+    if (!w) return fail(MCA_ERR_NULL, "weights is NULL");
+    const size_t hd = (size_t)w->heads * w->d_in * 8;
+    if (probs_host) MCA_CUDA_TRY(cudaMemcpy(probs_host, w->probs, hd, cudaMemcpyDeviceToHost));
+    if (cdf_host) MCA_CUDA_TRY(cudaMemcpy(cdf_host, w->cdf, hd, cudaMemcpyDeviceToHost));
+    return MCA_OK;
+}
+
+mca_status mca_reserve(mca_weights* w, long max_tokens, mca_stream_t stream) {
+    if (!w) return fail(MCA_ERR_NULL, "weights is NULL");
+    if (max_tokens < 0) return fail(MCA_ERR_SHAPE, "max_tokens < 0");
+    return ensure_workspace(w, max_tokens, stream);
+}
+
+mca_status mca_set_timing(mca_weights* w, int enable) {
+    if (!w) return fail(MCA_ERR_NULL, "weights is NULL");
+    w->timing = enable != 0;
+    if (w->timing && !w->ev[0])
+        for (auto& e : w->ev) MCA_CUDA_TRY(cudaEventCreate(&e));
+    w->ev_valid = false;
+    return MCA_OK;
+}
+
+int mca_last_stage_ms(const mca_weights* w, float* ms, int max_stages) {
+    if (!w || !w->timing || !w->ev_valid) return 0;
+    if (cudaEventSynchronize(w->ev[4]) != cudaSuccess) return 0;
+    int k = 0;
+    for (; k < 4 && k < max_stages; ++k)
+        if (cudaEventElapsedTime(&ms[k], w->ev[k], w->ev[k + 1]) != cudaSuccess) return k;
+    return k;
+}
+
+int mca_last_launch_count(const mca_weights* w) { return w ? w->last_launches : 0; }
+
+mca_status mca_stage_budgets(const double* cmax, long count, int n, int d, const mca_config* cfg, int32_t* budgets,
+                             uint8_t* exact, mca_stream_t stream) {
+    if (!cmax || !budgets || !exact) return fail(MCA_ERR_NULL, "cmax / budgets / exact is NULL");
+    if (mca_status s = check_config(cfg, true)) return s;
+    if (count < 0 || n <= 0 || d <= 0) return fail(MCA_ERR_SHAPE, "bad count / n / d");
+    if (count == 0) return MCA_OK;
+    int launches = 0;
+    const int grid = (int)std::min<long>((count + 255) / 256, 65535);
+    K2Args a{};
+    a.cmax_in = cmax;
+    a.count = count;
+    a.n = n;
+    a.heads = 1;
+    a.d = d;
+    a.dh = kDh;
+    a.min_samples = cfg->min_samples;
+    a.alpha = cfg->alpha;
+    a.budgets = budgets;
+    a.exact = exact;
+    k2_budgets<kGivenCmax, float><<<grid, 256, 0, stream>>>(a);
+    MCA_LAUNCH_CHECK("k2_budgets");
+    return MCA_OK;
+}
+
+mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const void* x, mca_dtype dt, int B, int n,
+                          long b_offset, uint32_t layer, const mca_config* cfg, uint64_t seed, void* y,
+                          int32_t* budgets_out, uint8_t* exact_out, mca_flops* flops_out, const mca_debug* dbg,
+                          mca_stream_t stream) {
+    if (!w) return fail(MCA_ERR_NULL, "weights is NULL");
+    if (mca_status s = check_config(cfg, true)) return s;
+    if (B < 0 || n <= 0) return fail(MCA_ERR_SHAPE, "B = %d, n = %d: need B >= 0, n >= 1", B, n);
+    if (dt != w->wdt) return fail(MCA_ERR_CONFIG, "activation dtype %d != weight dtype %d", (int)dt, (int)w->wdt);
+    if (b_offset < 0) return fail(MCA_ERR_SHAPE, "b_offset < 0");
+    const bool approx = cfg->mode == MCA_MODE_APPROX;
+    if (dbg && dbg->budgets_override && !dbg->exact_override)
+        return fail(MCA_ERR_NULL, "budgets_override needs exact_override");
+    if (flops_out) std::memset(flops_out, 0, sizeof(*flops_out));
+    if (B == 0) {
+        w->last_launches = 0;
+        return MCA_OK;
+    }
+    if (!q || !k || !x || !y) return fail(MCA_ERR_NULL, "q / k / x / y is NULL");
+    const long tokens = (long)B * n;
+    if (mca_status s = ensure_workspace(w, tokens, stream)) return s;
+    const int H = w->heads;
+    const long th = tokens * H;
+    const double scale = cfg->scale > 0.0 ? cfg->scale : 1.0 / std::sqrt((double)w->dh);
+    int launches = 0;
+
+    if (w->timing) MCA_CUDA_TRY(cudaEventRecord(w->ev[0], stream));
+    MCA_CUDA_TRY(cudaMemsetAsync(w->colkey, 0, th * sizeof(unsigned long long), stream));
+    MCA_CUDA_TRY(cudaMemsetAsync(w->counters, 0, 8 * sizeof(unsigned long long), stream));
+    MCA_CUDA_TRY(cudaMemsetAsync(w->chunk_counter, 0, H * sizeof(int), stream));
+
+    // K1: row statistics + column maxima
+    {
+        const dim3 grid((n + kQT - 1) / kQT, H, B);
+        if (dt == MCA_F32)
+            k1_scores_simt<float, double><<<grid, kThreads, 0, stream>>>((const float*)q, (const float*)k, n, H, scale,
+                                                                         w->row_m, w->row_l, w->lse, w->colkey);
+        else
+            k1_scores_simt<__nv_bfloat16, float><<<grid, kThreads, 0, stream>>>(
+                (const __nv_bfloat16*)q, (const __nv_bfloat16*)k, n, H, scale, w->row_m, w->row_l, w->lse,
+                w->colkey);
+        MCA_LAUNCH_CHECK("k1_scores");
+    }
+    if (w->timing) MCA_CUDA_TRY(cudaEventRecord(w->ev[1], stream));
+    // K2: Eq. 9 budgets
+    {
+        const int grid = (int)std::min<long>((th + 255) / 256, 4 * 148 * 8);
+        K2Args a{};
+        a.colkey = w->colkey;
+        a.cmax_in = dbg ? dbg->cmax_override : nullptr;
+        a.row_m = w->row_m;
+        a.row_l = w->row_l;
+        a.q = q;
+        a.k = k;
+        a.scale = scale;
+        a.count = th;
+        a.n = n;
+        a.heads = H;
+        a.d = w->d_in;
+        a.dh = w->dh;
+        a.min_samples = cfg->min_samples;
+        a.alpha = cfg->alpha;
+        a.force_exact = !approx;
+        a.budgets_override = dbg ? dbg->budgets_override : nullptr;
+        a.exact_override = dbg ? dbg->exact_override : nullptr;
+        a.budgets = w->budgets;
+        a.exact = w->exact;
+        a.cmax_out = dbg ? dbg->cmax_out : nullptr;
+        a.counters = w->counters;
+        if (a.cmax_in) k2_budgets<kGivenCmax, float><<<grid, 256, 0, stream>>>(a);
+        else if (dt == MCA_F32) k2_budgets<kKeyValue, float><<<grid, 256, 0, stream>>>(a);
+        else k2_budgets<kKeyArgmax, __nv_bfloat16><<<grid, 256, 0, stream>>>(a);
+        MCA_LAUNCH_CHECK("k2_budgets");
+    }
+    if (w->timing) MCA_CUDA_TRY(cudaEventRecord(w->ev[2], stream));
+    // K3: encoding
+    {
+        int32_t* draws = dbg ? dbg->draws_out : nullptr;
+        const int stride = dbg ? dbg->draws_stride : 0;
+        mca_status s = dt == MCA_F32
+                           ? launch_k3<float, double>(w, x, B, n, b_offset, layer, seed, w->hbuf, draws, stride,
+                                                      stream, launches)
+                           : launch_k3<__nv_bfloat16, float>(w, x, B, n, b_offset, layer, seed, w->hbuf, draws, stride,
+                                                             stream, launches);
+        if (s) return s;
+    }
+    if (w->timing) MCA_CUDA_TRY(cudaEventRecord(w->ev[3], stream));
+    // K4: y = A . H~
+    {
+        const dim3 grid((n + kQT4 - 1) / kQT4, H, B);
+        if (dt == MCA_F32)
+            k4_apply_simt<float><<<grid, kT4, 0, stream>>>((const float*)q, (const float*)k, (const float*)w->hbuf,
+                                                            w->lse, n, H, (float)scale, (float*)y);
+        else
+            k4_apply_simt<__nv_bfloat16><<<grid, kT4, 0, stream>>>(
+                (const __nv_bfloat16*)q, (const __nv_bfloat16*)k, (const __nv_bfloat16*)w->hbuf, w->lse, n, H,
+                (float)scale, (__nv_bfloat16*)y);
+        MCA_LAUNCH_CHECK("k4_apply");
+    }
+    if (w->timing) {
+        MCA_CUDA_TRY(cudaEventRecord(w->ev[4], stream));
+        w->ev_valid = true;
+    }
+    // optional outputs
+    if (budgets_out)
+        MCA_CUDA_TRY(cudaMemcpyAsync(budgets_out, w->budgets, th * sizeof(int32_t), cudaMemcpyDeviceToDevice, stream));
+    if (exact_out)
+        MCA_CUDA_TRY(cudaMemcpyAsync(exact_out, w->exact, th * sizeof(uint8_t), cudaMemcpyDeviceToDevice, stream));
+    if (dbg && dbg->lse_out)
+        MCA_CUDA_TRY(cudaMemcpyAsync(dbg->lse_out, w->lse, th * sizeof(float), cudaMemcpyDeviceToDevice, stream));
+    if (dbg && dbg->h_out)
+        MCA_CUDA_TRY(cudaMemcpyAsync(dbg->h_out, w->hbuf, th * w->dh * dtype_size(dt), cudaMemcpyDeviceToDevice,
+                                     stream));
+    w->last_launches = launches;
+    if (flops_out) {
+        unsigned long long c[8];
+        MCA_CUDA_TRY(cudaMemcpyAsync(c, w->counters, sizeof(c), cudaMemcpyDeviceToHost, stream));
+        MCA_CUDA_TRY(cudaStreamSynchronize(stream));
+        flops_out->exact_encoding = (uint64_t)th * 2ull * w->d_in * w->dh;
+        flops_out->approx_encoding = approx ? c[0] : flops_out->exact_encoding;
+        flops_out->aggregation = (uint64_t)B * H * 2ull * n * n * w->dh;
+        flops_out->samples = c[3];
+        flops_out->exact_tokens = c[2];
+        flops_out->reduction_factor = (double)flops_out->exact_encoding / (double)flops_out->approx_encoding;
+        flops_out->total_reduction = (double)(flops_out->exact_encoding + flops_out->aggregation) /
+                                     (double)(flops_out->approx_encoding + flops_out->aggregation);
+    }
+    return MCA_OK;
+}
+
+mca_status mca_forward(mca_weights* w, const void* q, const void* k, const void* x, mca_dtype dt, int B, int n,
+                       long b_offset, uint32_t layer, const mca_config* cfg, uint64_t seed, void* y,
+                       int32_t* budgets_out, uint8_t* exact_out, mca_flops* flops_out, mca_stream_t stream) {
+    return mca_forward_ex(w, q, k, x, dt, B, n, b_offset, layer, cfg, seed, y, budgets_out, exact_out, flops_out,
+                          nullptr, stream);
+}
+
+mca_status mca_regular_forward(mca_weights* w, const void* q, const void* k, const void* x, mca_dtype dt, int B,
+                               int n, double scale, void* y, mca_stream_t stream) {
+    mca_config cfg{1.0, scale, 1, MCA_MODE_REGULAR};
+    return mca_forward_ex(w, q, k, x, dt, B, n, 0, 0, &cfg, 0, y, nullptr, nullptr, nullptr, nullptr, stream);
+}
+
+}  // extern "C"

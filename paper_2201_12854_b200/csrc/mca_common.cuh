@@ -1,0 +1,118 @@
+// mca_common.cuh — device primitives shared by the MCA kernels (sm_100a).
+//
+// Philox4x32-10 here is the device generator; the fp64 oracle has its own,
+// independently written copy (oracle/sampling.cpp) and both are pinned to the
+// Random123 known-answer vectors, so index parity GPU-vs-oracle is a real check.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace mca_dev {
+
+constexpr int kDh = 64;            // head dimension the kernels implement (BERT base/large)
+constexpr int kGuideBits = 10;     // guide table: 1024 buckets over the 53-bit uniform
+constexpr int kGuide = 1 << kGuideBits;
+
+// ----------------------------------------------------------------- Philox
+__device__ __forceinline__ void philox4x32_10(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0,
+                                              uint32_t k1, uint32_t out[4]) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        if (r) {
+            k0 += 0x9E3779B9u;
+            k1 += 0xBB67AE85u;
+        }
+        const uint32_t lo0 = 0xD2511F53u * c0, hi0 = __umulhi(0xD2511F53u, c0);
+        const uint32_t lo1 = 0xCD9E8D57u * c2, hi1 = __umulhi(0xCD9E8D57u, c2);
+        const uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+        c0 = n0;
+        c1 = lo1;
+        c2 = n2;
+        c3 = lo0;
+    }
+    out[0] = c0;
+    out[1] = c1;
+    out[2] = c2;
+    out[3] = c3;
+}
+
+// Draws 2*blk and 2*blk+1 of stream (seed, stream_id, layer) as 53-bit integers
+// m (the uniform is m * 2^-53), DESIGN.md §3.
+__device__ __forceinline__ void philox_pair53(uint64_t seed, uint64_t stream_id, uint32_t layer, uint32_t blk,
+                                              uint64_t* m0, uint64_t* m1) {
+    uint32_t x[4];
+    philox4x32_10(blk, layer, (uint32_t)stream_id, (uint32_t)(stream_id >> 32), (uint32_t)seed,
+                  (uint32_t)(seed >> 32), x);
+    *m0 = ((((uint64_t)x[1]) << 32) | x[0]) >> 11;
+    *m1 = ((((uint64_t)x[3]) << 32) | x[2]) >> 11;
+}
+
+// Inverse CDF: first i with thr[i] > m, thr[i] = ceil(cdf[i] * 2^53). The guide
+// entry for m's top kGuideBits bits is a lower bound on the answer, so the
+// forward scan returns exactly std::upper_bound(cdf, m * 2^-53).
+__device__ __forceinline__ int sample_index(const uint64_t* __restrict__ thr, const uint16_t* __restrict__ guide,
+                                            uint64_t m) {
+    int i = guide[(uint32_t)(m >> (53 - kGuideBits))];
+    while (thr[i] <= m) ++i;
+    return i;
+}
+
+// ------------------------------------------------ order-preserving float keys
+__device__ __forceinline__ uint32_t float_to_ordered(float f) {
+    const uint32_t u = __float_as_uint(f);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float ordered_to_float(uint32_t u) {
+    return __uint_as_float((u & 0x80000000u) ? (u & 0x7FFFFFFFu) : ~u);
+}
+
+// ------------------------------------------------------------ dtype helpers
+template <class T>
+__device__ __forceinline__ float to_f32(T v);
+template <>
+__device__ __forceinline__ float to_f32<float>(float v) { return v; }
+template <>
+__device__ __forceinline__ float to_f32<__nv_bfloat16>(__nv_bfloat16 v) { return __bfloat162float(v); }
+
+template <class T>
+__device__ __forceinline__ T from_f32(float v);
+template <>
+__device__ __forceinline__ float from_f32<float>(float v) { return v; }
+template <>
+__device__ __forceinline__ __nv_bfloat16 from_f32<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
+
+// Load 8 consecutive elements as floats (16 B for bf16, 32 B for f32).
+__device__ __forceinline__ void load8(const __nv_bfloat16* p, float v[8]) {
+    const uint4 u = *reinterpret_cast<const uint4*>(p);
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        v[2 * i] = __uint_as_float(w[i] << 16);
+        v[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+    }
+}
+__device__ __forceinline__ void load8(const float* p, float v[8]) {
+    const float4 a = reinterpret_cast<const float4*>(p)[0];
+    const float4 b = reinterpret_cast<const float4*>(p)[1];
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+    v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+__device__ __forceinline__ void store8(__nv_bfloat16* p, const float v[8]) {
+    uint4 u;
+    uint32_t w[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+        w[i] = *reinterpret_cast<const uint32_t*>(&h);
+    }
+    u.x = w[0]; u.y = w[1]; u.z = w[2]; u.w = w[3];
+    *reinterpret_cast<uint4*>(p) = u;
+}
+__device__ __forceinline__ void store8(float* p, const float v[8]) {
+    reinterpret_cast<float4*>(p)[0] = make_float4(v[0], v[1], v[2], v[3]);
+    reinterpret_cast<float4*>(p)[1] = make_float4(v[4], v[5], v[6], v[7]);
+}
+
+}  // namespace mca_dev

@@ -1,0 +1,370 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the fp64 oracle.
+
+Contract:
+  (1) K0 tables: p(i) and cdf bitwise equal to the oracle's weight_probs.
+  (2) Eq. 9: oracle budgets(GPU cmax) == GPU budgets, bitwise, everywhere.
+  (3) Indices: for equal (seed, stream, layer, r) the device draws equal the
+      oracle's, bitwise (golden fixtures and full C1 dumps).
+  (4) H~ given equal budgets: per-row relative error <= 1e-5 (fp32) / 1e-2 (bf16).
+  (5) Y given equal budgets: per-row relative error <= 1e-5 (fp32) / 2e-2 (bf16),
+      against the oracle run on the same rounded inputs.
+  (6) End-to-end budgets vs the fp64 oracle: zero mismatches on C1 (fp32).
+  (7) Theorem 1: mean per-row error <= alpha*beta*||W_h||_F over 100 seeds; tail
+      fraction at delta = 0.1 <= 0.12.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+TOL_H = {torch.float32: 1e-5, torch.bfloat16: 1e-2}
+TOL_Y = {torch.float32: 1e-5, torch.bfloat16: 2e-2}
+
+
+@pytest.fixture(scope="module")
+def mca():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2201_12854_b200 as m
+    return m
+
+
+@pytest.fixture(scope="module")
+def syn():
+    from paper_2201_12854_b200 import synthetic
+    return synthetic
+
+
+def _np(t):
+    return t.detach().float().cpu().double().numpy() if t.dtype == torch.bfloat16 else t.detach().cpu().double().numpy()
+
+
+def _row_rel(a, b):
+    """max over rows of ||a_i - b_i|| / max(||b_i||, tiny) for [..., D] arrays."""
+    a = a.reshape(-1, a.shape[-1])
+    b = b.reshape(-1, b.shape[-1])
+    num = np.linalg.norm(a - b, axis=1)
+    den = np.maximum(np.linalg.norm(b, axis=1), 1e-30)
+    return float(np.max(num / den))
+
+
+def _setup(mca, syn, B, n, d_in, H, dtype, seed=1234):
+    w = syn.make_weights(d_in, H, seed=seed).to(dtype)
+    inp = syn.make_inputs(B, n, d_in, H, seed=seed)
+    q, k, x = (t.to(dtype).cuda() for t in (inp.q, inp.k, inp.x))
+    weights = mca.AttentionWeights(w.cuda(), heads=H)
+    return weights, w, q, k, x
+
+
+def _oracle(orc, w, q, k, x, H, **kw):
+    return orc.batched_forward(_np(q), _np(k), _np(x), _np(w), heads=H, **kw)
+
+
+# ------------------------------------------------------------------- (1) K0
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_k0_tables_bitwise(mca, syn, orc, dtype):
+    H, d_in = 12, 768
+    w = syn.make_weights(d_in, H).to(dtype)
+    w[5, :64] = 0.0                               # a zero row in head 0 -> p = 0, never drawn
+    weights = mca.AttentionWeights(w.cuda(), heads=H)
+    p, c = weights.distributions()
+    wn = _np(w)
+    for h in range(H):
+        d = orc.weight_probs(wn[:, h * 64:(h + 1) * 64])
+        assert np.array_equal(p[h].numpy(), d.probs), h
+        assert np.array_equal(c[h].numpy(), d.cdf), h
+    assert p[0, 5] == 0.0
+
+
+def test_k0_degenerate_head_raises(mca):
+    w = torch.randn(64, 128, device="cuda")
+    w[:, 64:] = 0.0
+    with pytest.raises(mca.DegenerateError):
+        mca.AttentionWeights(w, heads=2)
+
+
+def test_unsupported_head_dim(mca):
+    with pytest.raises(mca.UnsupportedError):
+        mca.AttentionWeights(torch.randn(64, 64, device="cuda"), heads=2, d_h=32)
+
+
+# ------------------------------------------------------------------ (2) Eq. 9
+def test_stage_budgets_bitwise(mca, orc):
+    rng = np.random.default_rng(0)
+    cm = np.concatenate([rng.uniform(0, 1, 20000), rng.uniform(0, 0.02, 20000), [0.0, 1.0, 1 / 512, 0.5, 1e-300]])
+    # values whose raw lands within an ulp of an integer: the discontinuity Eq. 9 has
+    target = rng.integers(1, 700, 2000).astype(np.float64)
+    cm = np.concatenate([cm, np.sqrt(target) * 0.4 / 512, np.nextafter(np.sqrt(target) * 0.4 / 512, 1.0)])
+    for n, alpha, mins, d in ((512, 0.4, 1, 768), (128, 0.2, 3, 768), (4096, 1.0, 1, 1024), (16, 0.05, 1, 128)):
+        b, e = mca.sample_budgets(torch.tensor(cm, device="cuda"), n, d, mca.McaConfig(alpha=alpha, min_samples=mins))
+        rb, re = orc.sample_budgets_from_cmax(cm, n, alpha, mins, d)
+        assert np.array_equal(b.cpu().numpy(), rb)
+        assert np.array_equal(e.cpu().numpy().astype(bool), re)
+
+
+def test_stage_budgets_golden(mca):
+    with open(os.path.join(GOLDEN, "budgets.json")) as f:
+        cases = json.load(f)["cases"]
+    for c in cases:
+        b, e = mca.sample_budgets(torch.tensor([c["cmax"]], dtype=torch.float64, device="cuda"), c["n"], c["d"],
+                                  mca.McaConfig(alpha=c["alpha"], min_samples=c["min_samples"]))
+        assert int(b.item()) == c["r"] and bool(e.item()) == c["exact"], c
+
+
+def test_invalid_alpha(mca):
+    cm = torch.zeros(4, dtype=torch.float64, device="cuda")
+    for a in (0.0, -0.1, 1.5):
+        with pytest.raises(mca.DomainError):
+            mca.sample_budgets(cm, 4, 64, mca.McaConfig(alpha=a))
+
+
+# ---------------------------------------------------------------- (3) draws
+def test_golden_draws_on_device(mca):
+    """The golden (seed, stream, layer) -> index dumps, reproduced by the
+    encoding kernel itself: W is zero-padded to d_h = 64 (same row norms ->
+    same p), n = 1 and b_offset = stream so token 0's stream id is `stream`."""
+    with open(os.path.join(GOLDEN, "draws.json")) as f:
+        cases = json.load(f)["cases"]
+    for c in cases:
+        w = np.array(c["w"])
+        d = w.shape[0]
+        wp = np.zeros((d, 64))
+        wp[:, : w.shape[1]] = w
+        weights = mca.AttentionWeights(torch.tensor(wp, dtype=torch.float32, device="cuda"), heads=1)
+        q = torch.zeros((1, 1, 64), device="cuda")
+        x = torch.ones((1, 1, d), device="cuda")
+        r = c["r"]
+        draws = torch.full((1, 1, 1, r), -7, dtype=torch.int32, device="cuda")
+        dbg = dict(draws_out=draws, draws_stride=r,
+                   budgets_override=torch.tensor([[[r]]], dtype=torch.int32, device="cuda"),
+                   exact_override=torch.zeros((1, 1, 1), dtype=torch.uint8, device="cuda"))
+        mca.mca_forward(weights, q, q, x, mca.McaConfig(alpha=1.0), seed=c["seed"], b_offset=c["stream"],
+                        layer=c["layer"], debug=dbg)
+        assert draws.view(-1).cpu().tolist() == c["indices"], c["stream"]
+
+
+# ------------------------------------------------------- C1 end to end (fp32)
+@pytest.fixture(scope="module")
+def c1_f32(mca, syn, orc):
+    """BASELINE.json configs[0]: B=1, n=128, d=768, 12 heads, fp32, alpha=0.4, seed 42."""
+    H, n, d_in = 12, 128, 768
+    weights, w, q, k, x = _setup(mca, syn, 1, n, d_in, H, torch.float32)
+    stride = d_in
+    dbg = dict(cmax_out=torch.zeros((1, H, n), dtype=torch.float64, device="cuda"),
+               lse_out=torch.zeros((1, H, n), device="cuda"), h_out=torch.zeros_like(q),
+               draws_out=torch.zeros((1, H, n, stride), dtype=torch.int32, device="cuda"), draws_stride=stride)
+    out = mca.mca_forward(weights, q, k, x, mca.McaConfig(alpha=0.4), seed=42, return_plan=True, flops=True,
+                          debug=dbg)
+    torch.cuda.synchronize()
+    ref = _oracle(orc, w, q, k, x, H, alpha=0.4, seed=42)
+    return dict(weights=weights, w=w, q=q, k=k, x=x, out=out, dbg=dbg, ref=ref, H=H, n=n, d_in=d_in)
+
+
+def test_c1_budgets_end_to_end_exact(c1_f32):
+    got = c1_f32["out"].budgets.cpu().numpy()
+    ex = c1_f32["out"].exact_mask.cpu().numpy().astype(bool)
+    assert np.array_equal(got, c1_f32["ref"].budgets)          # (6): zero mismatches on C1
+    assert np.array_equal(ex, c1_f32["ref"].exact)
+
+
+def test_c1_cmax_and_lse(c1_f32):
+    cm = c1_f32["dbg"]["cmax_out"].cpu().numpy()
+    np.testing.assert_allclose(cm, c1_f32["ref"].cmax, rtol=1e-12, atol=0)
+    np.testing.assert_allclose(c1_f32["dbg"]["lse_out"].cpu().numpy(), c1_f32["ref"].lse, rtol=1e-6, atol=1e-6)
+
+
+def test_c1_stage_isolated_budgets(c1_f32, orc):
+    cm = c1_f32["dbg"]["cmax_out"].cpu().numpy()
+    rb, re = orc.sample_budgets_from_cmax(cm, c1_f32["n"], 0.4, 1, c1_f32["d_in"])
+    assert np.array_equal(c1_f32["out"].budgets.cpu().numpy(), rb)
+
+
+def test_c1_draws_bitwise(c1_f32, orc):
+    draws = c1_f32["dbg"]["draws_out"].cpu().numpy()
+    budgets = c1_f32["out"].budgets.cpu().numpy()
+    exact = c1_f32["out"].exact_mask.cpu().numpy()
+    H, n = c1_f32["H"], c1_f32["n"]
+    wn = _np(c1_f32["w"])
+    checked = 0
+    for h in range(H):
+        dist = orc.weight_probs(wn[:, h * 64:(h + 1) * 64])
+        for j in range(n):
+            if exact[0, h, j]:
+                assert np.all(draws[0, h, j] == -1)
+                continue
+            r = int(budgets[0, h, j])
+            ref = orc.draw_indices(dist, r, 42, (0 * H + h) * n + j, 0)
+            assert np.array_equal(draws[0, h, j, :r], ref), (h, j)
+            assert np.all(draws[0, h, j, r:] == -1)
+            checked += 1
+    assert checked > 1000
+
+
+def test_c1_encodings_and_output(c1_f32):
+    ref = c1_f32["ref"]
+    assert _row_rel(_np(c1_f32["dbg"]["h_out"]), ref.h) <= TOL_H[torch.float32]
+    assert _row_rel(_np(c1_f32["out"].y), ref.y) <= TOL_Y[torch.float32]
+
+
+def test_c1_flops_counters(c1_f32):
+    f = c1_f32["out"].flops
+    ref = c1_f32["ref"].flops
+    b = c1_f32["out"].budgets.cpu().numpy()
+    e = c1_f32["out"].exact_mask.cpu().numpy().astype(bool)
+    assert f.exact_encoding == ref.exact_encoding
+    assert f.approx_encoding == ref.approx_encoding
+    assert f.aggregation == ref.aggregation
+    assert f.samples == int(b[~e].sum())                       # instrumented == model
+    assert f.exact_tokens == int(e.sum())
+    assert f.reduction_factor == pytest.approx(ref.reduction_factor, rel=1e-15)
+
+
+# ----------------------------------------------------------- bf16 parity
+@pytest.mark.parametrize("B,n", [(2, 128), (1, 512), (1, 77)])
+def test_bf16_parity(mca, syn, orc, B, n):
+    H, d_in = 12, 768
+    weights, w, q, k, x = _setup(mca, syn, B, n, d_in, H, torch.bfloat16, seed=7)
+    dbg = dict(cmax_out=torch.zeros((B, H, n), dtype=torch.float64, device="cuda"), h_out=torch.zeros_like(q),
+               draws_out=torch.zeros((B, H, n, 64), dtype=torch.int32, device="cuda"), draws_stride=64)
+    out = mca.mca_forward(weights, q, k, x, mca.McaConfig(alpha=0.4), seed=42, return_plan=True, flops=True,
+                          debug=dbg)
+    b = out.budgets.cpu().numpy()
+    e = out.exact_mask.cpu().numpy().astype(bool)
+    # (2) stage-isolated Eq. 9
+    rb, re = orc.sample_budgets_from_cmax(dbg["cmax_out"].cpu().numpy(), n, 0.4, 1, d_in)
+    assert np.array_equal(b, rb) and np.array_equal(e, re)
+    # (4)/(5) with the GPU's plan
+    ref = _oracle(orc, w, q, k, x, H, alpha=0.4, seed=42, budgets_override=b, exact_override=e)
+    assert _row_rel(_np(dbg["h_out"]), ref.h) <= TOL_H[torch.bfloat16]
+    assert _row_rel(_np(out.y), ref.y) <= TOL_Y[torch.bfloat16]
+    # (3) draws for a sample of token-heads
+    wn = _np(w)
+    draws = dbg["draws_out"].cpu().numpy()
+    rng = np.random.default_rng(1)
+    for _ in range(200):
+        bb, h, j = rng.integers(B), rng.integers(H), rng.integers(n)
+        if e[bb, h, j]:
+            continue
+        r = int(b[bb, h, j])
+        ref_idx = orc.draw_indices(orc.weight_probs(wn[:, h * 64:(h + 1) * 64]), min(r, 64), 42,
+                                   (bb * H + h) * n + j, 0)
+        assert np.array_equal(draws[bb, h, j, :min(r, 64)], ref_idx)
+    # end-to-end budget agreement with the fp64 oracle is reported, not required (bf16 scores)
+    full = _oracle(orc, w, q, k, x, H, alpha=0.4, seed=42)
+    mism = int((full.budgets != b).sum())
+    print(f"bf16 B={B} n={n}: {mism} / {b.size} budgets differ from the fp64 oracle end to end")
+    assert mism <= max(5, b.size // 100)
+
+
+# -------------------------------------------------------------- properties
+def test_regular_forward(mca, syn, orc):
+    H, n, d_in = 12, 128, 768
+    weights, w, q, k, x = _setup(mca, syn, 2, n, d_in, H, torch.float32)
+    y = mca.regular_forward(weights, q, k, x)
+    ref = _oracle(orc, w, q, k, x, H, mode="regular")
+    assert _row_rel(_np(y), ref.y) <= 1e-5
+
+
+def test_exact_clamp_equals_regular(mca, syn):
+    H, n, d_in = 12, 64, 768
+    weights, w, q, k, x = _setup(mca, syn, 1, n, d_in, H, torch.float32)
+    out = mca.mca_forward(weights, q, k, x, mca.McaConfig(alpha=1e-7), seed=3, return_plan=True)
+    assert bool(out.exact_mask.bool().all())
+    y = mca.regular_forward(weights, q, k, x)
+    assert _row_rel(_np(out.y), _np(y)) <= 1e-6
+
+
+def test_determinism_and_shard_invariance(mca, syn):
+    H, n, d_in = 12, 128, 768
+    weights, w, q, k, x = _setup(mca, syn, 4, n, d_in, H, torch.bfloat16)
+    cfg = mca.McaConfig(alpha=0.4)
+    a = mca.mca_forward(weights, q, k, x, cfg, seed=9).y.clone()
+    b = mca.mca_forward(weights, q, k, x, cfg, seed=9).y.clone()
+    assert torch.equal(a, b)
+    parts = [mca.mca_forward(weights, q[s:s + 2].contiguous(), k[s:s + 2].contiguous(), x[s:s + 2].contiguous(),
+                             cfg, seed=9, b_offset=s).y for s in (0, 2)]
+    assert torch.equal(torch.cat(parts), a)                     # batch shards reproduce the global run bitwise
+    c = mca.mca_forward(weights, q, k, x, cfg, seed=10).y
+    assert not torch.equal(a, c)
+
+
+def test_uniform_attention_alpha1_gives_one_sample(mca, syn):
+    H, n, d_in = 12, 256, 768
+    weights, w, q, k, x = _setup(mca, syn, 1, n, d_in, H, torch.float32)
+    qz = torch.zeros_like(q)                                    # uniform attention: every A[i, j] = 1/n
+    out = mca.mca_forward(weights, qz, qz, x, mca.McaConfig(alpha=1.0), seed=1, return_plan=True, flops=True)
+    assert bool((out.budgets == 1).all()) and not bool(out.exact_mask.bool().any())
+    assert out.flops.reduction_factor == pytest.approx(2 * 768 * 64 / (2 * 64 + 3))
+
+
+def test_edge_shapes(mca, syn, orc):
+    H, d_in = 12, 768
+    for B, n in ((1, 1), (3, 7), (1, 33), (2, 65)):
+        weights, w, q, k, x = _setup(mca, syn, B, n, d_in, H, torch.float32, seed=B * 100 + n)
+        out = mca.mca_forward(weights, q, k, x, mca.McaConfig(alpha=0.5), seed=5, return_plan=True)
+        ref = _oracle(orc, w, q, k, x, H, alpha=0.5, seed=5)
+        assert np.array_equal(out.budgets.cpu().numpy(), ref.budgets), (B, n)
+        assert _row_rel(_np(out.y), ref.y) <= 1e-5, (B, n)
+    # B = 0 is a no-op
+    weights, w, q, k, x = _setup(mca, syn, 1, 8, d_in, H, torch.float32)
+    e = q[:0]
+    out = mca.mca_forward(weights, e, e, x[:0], mca.McaConfig(), seed=1)
+    assert out.y.shape[0] == 0
+
+
+def test_input_validation(mca, syn):
+    H, n, d_in = 12, 16, 768
+    weights, w, q, k, x = _setup(mca, syn, 1, n, d_in, H, torch.float32)
+    with pytest.raises(mca.ConfigError):
+        mca.mca_forward(weights, q.bfloat16(), k.bfloat16(), x.bfloat16())
+    with pytest.raises(mca.ShapeError):
+        mca.mca_forward(weights, q, k, x[:, :, :100].contiguous())
+    with pytest.raises(mca.DomainError):
+        mca.mca_forward(weights, q, k, x, mca.McaConfig(alpha=0.0))
+
+
+def test_theorem1_bound_on_gpu(mca, syn):
+    """Theorem 1 on C1: for every head and output row, the
+    mean over 100 seeds of ||Y~[i] - Y[i]|| stays below alpha * beta * ||W_h||_F,
+    and the fraction above the bound / delta (delta = 0.1) is <= 0.12."""
+    H, n, d_in = 12, 128, 768
+    weights, w, q, k, x = _setup(mca, syn, 1, n, d_in, H, torch.float32)
+    y = mca.regular_forward(weights, q, k, x).double()
+    beta = x[0].double().norm(dim=1).mean()
+    for alpha in (0.2, 0.6):
+        errs = []
+        for s in range(100):
+            yt = mca.mca_forward(weights, q, k, x, mca.McaConfig(alpha=alpha), seed=1000 + s).y.double()
+            errs.append((yt - y).view(n, H, 64).norm(dim=2))   # [n, H]
+        errs = torch.stack(errs)                                # [T, n, H]
+        bound = alpha * beta * w.double().view(d_in, H, 64).norm(dim=(0, 2)).cuda()   # [H]
+        assert bool((errs.mean(dim=0) <= bound).all())
+        assert float((errs > bound / 0.1).float().mean(dim=0).max()) <= 0.12
+
+
+def test_c2_full_size_properties(mca, syn, orc):
+    """BASELINE.json configs[1] at full size (B=64, n=512, bf16): Eq. 9 parity
+    on all 393,216 token-heads, the FLOP counter, and oracle parity on two
+    whole sequences (size-independent checks plus a sampled full check)."""
+    H, n, d_in, B = 12, 512, 768, 64
+    weights, w, q, k, x = _setup(mca, syn, B, n, d_in, H, torch.bfloat16)
+    cm = torch.zeros((B, H, n), dtype=torch.float64, device="cuda")
+    out = mca.mca_forward(weights, q, k, x, mca.McaConfig(alpha=0.4), seed=42, return_plan=True, flops=True,
+                          debug=dict(cmax_out=cm))
+    b = out.budgets.cpu().numpy()
+    e = out.exact_mask.cpu().numpy().astype(bool)
+    rb, re = orc.sample_budgets_from_cmax(cm.cpu().numpy(), n, 0.4, 1, d_in)
+    assert np.array_equal(b, rb) and np.array_equal(e, re)
+    assert out.flops.samples == int(b[~e].sum())
+    assert torch.isfinite(out.y.float()).all()
+    for s in (0, 37):
+        sl = slice(s, s + 1)
+        ref = orc.batched_forward(_np(q[sl]), _np(k[sl]), _np(x[sl]), _np(w), heads=H, alpha=0.4, seed=42,
+                                  b_offset=s, budgets_override=b[sl], exact_override=e[sl])
+        assert _row_rel(_np(out.y[sl]), ref.y) <= TOL_Y[torch.bfloat16]
