@@ -1,0 +1,203 @@
+// k4_apply_tc.cu — K4 on the 5th-generation tensor cores: y = A . H~ for one
+// (b, h, 128-query tile) per CTA (matrix.hpp:33-34 `matmul`).
+//
+// A is never materialised. Per 128-key block:
+//   S  = Q K_blk^T                  tcgen05.mma M=128 N=128 K=64 -> TMEM (fp32)
+//   P  = exp(scale*S - lse)         4 softmax warps, 1 TMEM lane (= query row)
+//                                   each; lse from K1, so no online rescaling;
+//                                   P written bf16 into a 128B-swizzled K-major
+//                                   smem tile
+//   O += P H~_blk                   tcgen05.mma M=128 N=64 K=128 (H~ MN-major)
+// Warp roles (192 threads): warp 0 TMA producer (Q once, then a 3-stage ring of
+// K/H~ blocks), warp 1 TMEM allocator + single-thread MMA issuer, warps 2-5
+// softmax + epilogue. S is double-buffered in TMEM and P in smem, so the
+// tensor core computes S(kb+1) while the softmax warps exponentiate S(kb), and
+// P(kb) . H~(kb) overlaps the exponentials of block kb+1. TMEM: S0 [0,128),
+// S1 [128,256), O [256,320).
+#include "mca_common.cuh"
+#include "tc_common.cuh"
+
+namespace mca_dev {
+
+namespace k4tc {
+constexpr int kBM = 128, kBK = 128, kStages = 3;
+constexpr int kThreads = 192;
+constexpr uint32_t kTileBytes = kBK * kDh * 2;       // 16 KB: one 128 x 64 bf16 tile
+constexpr uint32_t kPBytes = kBM * kBK * 2;          // 32 KB: P tile (two 64-key swizzle atoms)
+constexpr uint32_t kSmemQ = 0;
+constexpr uint32_t kSmemK = kSmemQ + kTileBytes;                     // kStages tiles
+constexpr uint32_t kSmemH = kSmemK + kStages * kTileBytes;           // kStages tiles
+constexpr uint32_t kSmemP = kSmemH + kStages * kTileBytes;           // 2 P tiles
+constexpr uint32_t kSmemBar = kSmemP + 2 * kPBytes;
+constexpr uint32_t kSmemBytes = kSmemBar + 256 + 1024;               // + alignment slack
+constexpr uint32_t kIdescS = mca_tc::idesc_f16(1, 0, kBM, kBK);      // bf16, B K-major
+constexpr uint32_t kIdescO = mca_tc::idesc_f16(1, 1, kBM, kDh);      // bf16, B MN-major
+}  // namespace k4tc
+
+__global__ void __launch_bounds__(k4tc::kThreads, 1)
+    k4_apply_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                const __grid_constant__ CUtensorMap tm_h, const float* __restrict__ lse, int n, int heads,
+                float scale, __nv_bfloat16* __restrict__ y) {
+    using namespace k4tc;
+    using namespace mca_tc;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kSmemBar);
+    uint64_t* q_full = bars + 0;
+    uint64_t* kv_full = bars + 1;              // [kStages]
+    uint64_t* kv_empty = bars + 1 + kStages;   // [kStages]
+    uint64_t* s_full = bars + 1 + 2 * kStages; // [2]
+    uint64_t* s_empty = s_full + 2;            // [2]
+    uint64_t* p_full = s_full + 4;             // [2]
+    uint64_t* p_empty = s_full + 6;            // [2]
+    uint64_t* o_full = s_full + 8;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 9);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int b = blockIdx.z, h = blockIdx.y, m0 = blockIdx.x * kBM;
+    const int nkb = (n + kBK - 1) / kBK;
+
+    if (threadIdx.x == 0) {
+        mbar_init(q_full, 1);
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(kv_full + s, 1);
+            mbar_init(kv_empty + s, 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(s_full + i, 1);
+            mbar_init(s_empty + i, 128);
+            mbar_init(p_full + i, 128);
+            mbar_init(p_empty + i, 1);
+        }
+        mbar_init(o_full, 1);
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc<512>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {  // ---------------- TMA producer
+            tma_prefetch(&tm_q);
+            tma_prefetch(&tm_k);
+            tma_prefetch(&tm_h);
+            mbar_expect_tx(q_full, kTileBytes);
+            tma_load_3d(smem + kSmemQ, &tm_q, q_full, h * kDh, m0, b);
+            for (int kb = 0; kb < nkb; ++kb) {
+                const int s = kb % kStages;
+                mbar_wait(kv_empty + s, ((kb / kStages) & 1) ^ 1);
+                mbar_expect_tx(kv_full + s, 2 * kTileBytes);
+                tma_load_3d(smem + kSmemK + s * kTileBytes, &tm_k, kv_full + s, h * kDh, kb * kBK, b);
+                tma_load_3d(smem + kSmemH + s * kTileBytes, &tm_h, kv_full + s, h * kDh, kb * kBK, b);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // ---------------- MMA issuer
+            const uint32_t q_addr = smem_u32(smem + kSmemQ);
+            auto issue_pv = [&](int j) {
+                const int pb = j & 1, s = j % kStages;
+                mbar_wait(p_full + pb, (j >> 1) & 1);
+                tc_fence_after();
+                const uint32_t p_addr = smem_u32(smem + kSmemP + pb * kPBytes);
+                const uint32_t h_addr = smem_u32(smem + kSmemH + s * kTileBytes);
+#pragma unroll
+                for (int kk = 0; kk < kBK / 16; ++kk) {
+                    const uint64_t ad = sw128_desc(p_addr + (kk >> 2) * (kBM * 128) + (kk & 3) * 32, 16, 1024);
+                    const uint64_t bd = sw128_desc(h_addr + kk * 2048, kBK * 128, 1024);
+                    umma_f16(tmem + 256, ad, bd, kIdescO, (j > 0 || kk > 0) ? 1u : 0u);
+                }
+                umma_commit(p_empty + pb);
+                umma_commit(kv_empty + s);
+            };
+            mbar_wait(q_full, 0);
+            for (int kb = 0; kb < nkb; ++kb) {
+                const int s = kb % kStages, sb = kb & 1;
+                mbar_wait(kv_full + s, (kb / kStages) & 1);
+                mbar_wait(s_empty + sb, ((kb >> 1) & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t k_addr = smem_u32(smem + kSmemK + s * kTileBytes);
+#pragma unroll
+                for (int kk = 0; kk < kDh / 16; ++kk) {
+                    const uint64_t ad = sw128_desc(q_addr + kk * 32, 16, 1024);
+                    const uint64_t bd = sw128_desc(k_addr + kk * 32, 16, 1024);
+                    umma_f16(tmem + sb * kBK, ad, bd, kIdescS, kk > 0 ? 1u : 0u);
+                }
+                umma_commit(s_full + sb);
+                if (kb > 0) issue_pv(kb - 1);
+            }
+            issue_pv(nkb - 1);
+            umma_commit(o_full);
+        }
+    } else {  // ------------------------------- softmax + epilogue (warps 2..5)
+        const int quad = warp & 3;                 // TMEM lane quadrant this warp may access
+        const int row = quad * 32 + lane;          // query row within the tile
+        const uint32_t lane_base = tmem + ((uint32_t)(quad * 32) << 16);
+        const float c = scale * 1.4426950408889634f;
+        const int grow = m0 + row;
+        const float lse2 = grow < n ? lse[((size_t)b * heads + h) * n + grow] * 1.4426950408889634f : 0.0f;
+        for (int kb = 0; kb < nkb; ++kb) {
+            const int sb = kb & 1;
+            const uint32_t ph = (kb >> 1) & 1;
+            mbar_wait(s_full + sb, ph);
+            tc_fence_after();
+            uint32_t sv[4][32];
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4) tmem_ld32(lane_base + sb * kBK + q4 * 32, sv[q4]);
+            tmem_ld_wait();
+            tc_fence_before();
+            mbar_arrive(s_empty + sb);
+            mbar_wait(p_empty + sb, ph ^ 1);
+            uint8_t* pt = smem + kSmemP + sb * kPBytes;
+            const int kbase = kb * kBK;
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4) {
+#pragma unroll
+                for (int ch = 0; ch < 4; ++ch) {       // 16-byte chunks of 8 keys
+                    uint32_t pk[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const int col = q4 * 32 + ch * 8 + 2 * e;
+                        float p0 = ex2_approx(__uint_as_float(sv[q4][ch * 8 + 2 * e]) * c - lse2);
+                        float p1 = ex2_approx(__uint_as_float(sv[q4][ch * 8 + 2 * e + 1]) * c - lse2);
+                        if (kbase + col >= n) p0 = 0.0f;
+                        if (kbase + col + 1 >= n) p1 = 0.0f;
+                        pk[e] = pack_bf16x2(p0, p1);
+                    }
+                    const int key0 = q4 * 32 + ch * 8;                   // first key of the chunk
+                    const uint32_t off = (key0 >> 6) * (kBM * 128) + sw128_offset(row, (key0 & 63) * 2);
+                    *reinterpret_cast<uint4*>(pt + off) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                }
+            }
+            fence_proxy_async_smem();
+            mbar_arrive(p_full + sb);
+        }
+        // epilogue: O (fp32, TMEM cols 256..319) -> bf16 -> y
+        mbar_wait(o_full, 0);
+        tc_fence_after();
+        uint32_t ov[2][32];
+        tmem_ld32(lane_base + 256, ov[0]);
+        tmem_ld32(lane_base + 288, ov[1]);
+        tmem_ld_wait();
+        if (grow < n) {
+            __nv_bfloat16* dst = y + ((size_t)b * n + grow) * (size_t)heads * kDh + (size_t)h * kDh;
+#pragma unroll
+            for (int g = 0; g < 8; ++g) {
+                uint32_t pk[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int cidx = g * 8 + 2 * e;
+                    pk[e] = pack_bf16x2(__uint_as_float(ov[cidx >> 5][cidx & 31]),
+                                        __uint_as_float(ov[(cidx + 1) >> 5][(cidx + 1) & 31]));
+                }
+                reinterpret_cast<uint4*>(dst)[g] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) tmem_dealloc<512>(tmem);
+}
+
+}  // namespace mca_dev

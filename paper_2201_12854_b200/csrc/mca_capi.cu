@@ -7,6 +7,8 @@
 //
 // Unity build: the kernel translation units are included here so one nvcc
 // invocation produces libmca_b200.so (no relocatable device code needed).
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -20,11 +22,11 @@
 
 #include "k0_weights.cu"
 #include "k1_scores_simt.cu"
-// #include "k1_scores_tc.cu"
+#include "k1_scores_tc.cu"
 #include "k2_budgets.cu"
 #include "k3_encode.cu"
 #include "k4_apply_simt.cu"
-// #include "k4_apply_tc.cu"
+#include "k4_apply_tc.cu"
 
 using namespace mca_dev;
 
@@ -67,6 +69,43 @@ int sm_count() {
         if (c <= 0) c = 148;
     }
     return c;
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+// 3-D bf16 view [batch][rows][inner] with a {64, box_rows, 1} box and 128-byte
+// swizzle: the UMMA operand layout of tc_common.cuh. Rows past `rows` read as 0.
+bool make_tmap_bf16(CUtensorMap* m, const void* base, uint64_t inner, uint64_t rows, uint64_t batch,
+                    uint32_t box_rows) {
+    auto enc = tmap_encoder();
+    if (!enc) return false;
+    cuuint64_t dims[3] = {inner, rows, batch};
+    cuuint64_t strides[2] = {inner * 2, rows * inner * 2};
+    cuuint32_t box[3] = {64, box_rows, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+bool force_simt() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("MCA_FORCE_SIMT");
+        v = (e && e[0] == '1') ? 1 : 0;
+    }
+    return v == 1;
 }
 
 }  // namespace
@@ -343,10 +382,24 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
         if (dt == MCA_F32)
             k1_scores_simt<float, double><<<grid, kThreads, 0, stream>>>((const float*)q, (const float*)k, n, H, scale,
                                                                          w->row_m, w->row_l, w->lse, w->colkey);
-        else
+        else if (force_simt())
             k1_scores_simt<__nv_bfloat16, float><<<grid, kThreads, 0, stream>>>(
                 (const __nv_bfloat16*)q, (const __nv_bfloat16*)k, n, H, scale, w->row_m, w->row_l, w->lse,
                 w->colkey);
+        else {
+            CUtensorMap tq, tk;
+            if (!make_tmap_bf16(&tq, q, (uint64_t)H * kDh, n, B, 128) ||
+                !make_tmap_bf16(&tk, k, (uint64_t)H * kDh, n, B, 128))
+                return fail(MCA_ERR_CUDA, "cuTensorMapEncodeTiled failed for q/k");
+            static bool attr = false;
+            if (!attr) {
+                MCA_CUDA_TRY(cudaFuncSetAttribute(k1_scores_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  (int)k1tc::kSmemBytes));
+                attr = true;
+            }
+            k1_scores_tc<<<dim3((n + 127) / 128, H, B), k1tc::kThreads, k1tc::kSmemBytes, stream>>>(
+                tq, tk, n, H, (float)scale, w->row_m, w->row_l, w->lse, w->colkey);
+        }
         MCA_LAUNCH_CHECK("k1_scores");
     }
     if (w->timing) MCA_CUDA_TRY(cudaEventRecord(w->ev[1], stream));
@@ -399,10 +452,25 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
         if (dt == MCA_F32)
             k4_apply_simt<float><<<grid, kT4, 0, stream>>>((const float*)q, (const float*)k, (const float*)w->hbuf,
                                                             w->lse, n, H, (float)scale, (float*)y);
-        else
+        else if (force_simt())
             k4_apply_simt<__nv_bfloat16><<<grid, kT4, 0, stream>>>(
                 (const __nv_bfloat16*)q, (const __nv_bfloat16*)k, (const __nv_bfloat16*)w->hbuf, w->lse, n, H,
                 (float)scale, (__nv_bfloat16*)y);
+        else {
+            CUtensorMap tq, tk, th;
+            if (!make_tmap_bf16(&tq, q, (uint64_t)H * kDh, n, B, 128) ||
+                !make_tmap_bf16(&tk, k, (uint64_t)H * kDh, n, B, 128) ||
+                !make_tmap_bf16(&th, w->hbuf, (uint64_t)H * kDh, n, B, 128))
+                return fail(MCA_ERR_CUDA, "cuTensorMapEncodeTiled failed for q/k/h");
+            static bool attr = false;
+            if (!attr) {
+                MCA_CUDA_TRY(cudaFuncSetAttribute(k4_apply_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  (int)k4tc::kSmemBytes));
+                attr = true;
+            }
+            k4_apply_tc<<<dim3((n + 127) / 128, H, B), k4tc::kThreads, k4tc::kSmemBytes, stream>>>(
+                tq, tk, th, w->lse, n, H, (float)scale, (__nv_bfloat16*)y);
+        }
         MCA_LAUNCH_CHECK("k4_apply");
     }
     if (w->timing) {

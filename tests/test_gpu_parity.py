@@ -226,7 +226,7 @@ def test_c1_flops_counters(c1_f32):
 
 
 # ----------------------------------------------------------- bf16 parity
-@pytest.mark.parametrize("B,n", [(2, 128), (1, 512), (1, 77)])
+@pytest.mark.parametrize("B,n", [(2, 128), (1, 512), (1, 77), (1, 640), (2, 200)])
 def test_bf16_parity(mca, syn, orc, B, n):
     H, d_in = 12, 768
     weights, w, q, k, x = _setup(mca, syn, B, n, d_in, H, torch.bfloat16, seed=7)
