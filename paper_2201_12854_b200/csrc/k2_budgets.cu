@@ -1,4 +1,5 @@
-// k2_budgets.cu — K2: column maxima -> Eq. 9 sample budgets + FLOP accounting.
+// k2_budgets.cu — K2: column maxima -> Eq. 9 sample budgets, FLOP accounting,
+// and the per-head work lists the encoding kernels consume.
 //
 // sample_budgets:
 //   t = (n * cmax) / alpha;  raw = t * t;  c = ceil(raw)
@@ -13,8 +14,12 @@
 //               recomputed here in fp64 from the (bf16) inputs — products of
 //               bf16 values are exact in fp64 — and cmax = exp(t - m_i*) / l_i*,
 //               the oracle's softmax formula, with K1's row statistics.
-// The kernel also reduces flops_for_plan: approx cost, the
-// number of sampled draws and exact token-heads.
+//
+// Bucketing ("tokens bucketed by sample count"): a block covers
+// 256 tokens of ONE (b, h) row, so it histograms budgets per head in shared
+// memory; k2_scan turns the histograms into descending-budget offsets and
+// k2_scatter writes each head's sampled-token list sorted by budget (largest
+// first: LPT order for K3) and its exact-token list (for K3b).
 #include "mca_common.cuh"
 
 namespace mca_dev {
@@ -48,6 +53,7 @@ struct K2Args {
     const void* k;
     double scale;
     long count;                        // B*H*n
+    int row_len;                       // tokens per block row (= n in the forward)
     int n, heads, d, dh, min_samples;
     double alpha;
     bool force_exact;
@@ -57,13 +63,36 @@ struct K2Args {
     uint8_t* exact;
     double* cmax_out;
     unsigned long long* counters;      // [0] approx cost, [1] sampled draws, [2] exact token-heads
+    unsigned int* hist;                // [H, d + 1]: bins 1..d-1 sampled budgets, bin d = exact (nullable)
 };
 
+template <class T>
+__device__ __forceinline__ double dot64_f64(const T* a, const T* b) {
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int c = 0; c < kDh; c += 8) {
+        float va[8], vb[8];
+        load8(a + c, va);
+        load8(b + c, vb);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[e & 3] = fma((double)va[e], (double)vb[e], acc[e & 3]);
+    }
+    return (acc[0] + acc[1]) + (acc[2] + acc[3]);
+}
+
+// grid = (ceil(row_len / 256), B * H); block = 256 tokens of one (b, h).
 template <int kSrc, class T>
-__global__ void k2_budgets(K2Args a) {
+__global__ void __launch_bounds__(256) k2_budgets(K2Args a) {
+    __shared__ unsigned int s_hist[1025];
+    const bool use_hist = a.hist != nullptr && a.d <= 1024;
+    if (use_hist)
+        for (int i = threadIdx.x; i <= a.d; i += blockDim.x) s_hist[i] = 0;
+    __syncthreads();
+    const long bh = blockIdx.y;
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
     unsigned long long cost = 0, samples = 0, nexact = 0;
-    const unsigned long long exact_cost = 2ull * (unsigned long long)a.d * (unsigned long long)a.dh;
-    for (long t = blockIdx.x * (long)blockDim.x + threadIdx.x; t < a.count; t += (long)gridDim.x * blockDim.x) {
+    if (j < a.row_len) {
+        const long t = bh * a.row_len + j;
         int r;
         bool ex;
         if (a.force_exact) {
@@ -81,14 +110,11 @@ __global__ void k2_budgets(K2Args a) {
             } else {
                 const unsigned long long key = a.colkey[t];
                 const int i = (int)(0xFFFFFFFFu - (uint32_t)(key & 0xFFFFFFFFull));
-                const long bh = t / a.n;                 // b * H + h
-                const int j = (int)(t - bh * a.n);
                 const int b = (int)(bh / a.heads), h = (int)(bh - (long)b * a.heads);
                 const size_t HD = (size_t)a.heads * kDh;
                 const T* qi = reinterpret_cast<const T*>(a.q) + ((size_t)b * a.n + i) * HD + (size_t)h * kDh;
                 const T* kj = reinterpret_cast<const T*>(a.k) + ((size_t)b * a.n + j) * HD + (size_t)h * kDh;
-                double s = 0.0;
-                for (int c = 0; c < kDh; ++c) s = __dadd_rn(s, __dmul_rn((double)to_f32(qi[c]), (double)to_f32(kj[c])));
+                const double s = dot64_f64(qi, kj);
                 const size_t ri = (size_t)bh * a.n + i;
                 cm = __ddiv_rn(exp(__dsub_rn(__dmul_rn(a.scale, s), a.row_m[ri])), a.row_l[ri]);
             }
@@ -98,23 +124,93 @@ __global__ void k2_budgets(K2Args a) {
         a.budgets[t] = r;
         a.exact[t] = ex ? 1 : 0;
         if (ex) {
-            cost += exact_cost;
-            nexact += 1;
+            cost = 2ull * (unsigned long long)a.d * (unsigned long long)a.dh;
+            nexact = 1;
         } else {
-            cost += (unsigned long long)r * (2ull * a.dh + 3ull);
-            samples += (unsigned long long)r;
+            cost = (unsigned long long)r * (2ull * a.dh + 3ull);
+            samples = (unsigned long long)r;
+        }
+        // sort bin: budgets above d - 1 only occur through budgets_override (tests)
+        const int bin = ex ? a.d : min(r, a.d - 1);
+        if (use_hist) atomicAdd(&s_hist[bin], 1u);
+        else if (a.hist) atomicAdd(&a.hist[(size_t)(bh % a.heads) * (a.d + 1) + bin], 1u);
+    }
+    if (a.counters) {
+        for (int off = 16; off; off >>= 1) {  // warp reduce, one atomic per warp
+            cost += __shfl_xor_sync(0xffffffffu, cost, off);
+            samples += __shfl_xor_sync(0xffffffffu, samples, off);
+            nexact += __shfl_xor_sync(0xffffffffu, nexact, off);
+        }
+        if ((threadIdx.x & 31) == 0) {
+            if (cost) atomicAdd(a.counters + 0, cost);
+            if (samples) atomicAdd(a.counters + 1, samples);
+            if (nexact) atomicAdd(a.counters + 2, nexact);
         }
     }
-    if (!a.counters) return;
-    for (int off = 16; off; off >>= 1) {  // warp reduce, one atomic per warp
-        cost += __shfl_xor_sync(0xffffffffu, cost, off);
-        samples += __shfl_xor_sync(0xffffffffu, samples, off);
-        nexact += __shfl_xor_sync(0xffffffffu, nexact, off);
+    if (use_hist) {
+        __syncthreads();
+        const int h = (int)(bh % a.heads);
+        for (int i = threadIdx.x; i <= a.d; i += blockDim.x)
+            if (s_hist[i]) atomicAdd(&a.hist[(size_t)h * (a.d + 1) + i], s_hist[i]);
     }
-    if ((threadIdx.x & 31) == 0) {
-        if (cost) atomicAdd(a.counters + 0, cost);
-        if (samples) atomicAdd(a.counters + 1, samples);
-        if (nexact) atomicAdd(a.counters + 2, nexact);
+}
+
+// One block per head: cursor[h][bin] = start of `bin` in the head's sampled
+// list, bins in DESCENDING budget order; cursor[h][d] = 0 for the exact list.
+// counts[h] = {number of sampled tokens, number of exact tokens}.
+__global__ void __launch_bounds__(1024) k2_scan(const unsigned int* __restrict__ hist, int d,
+                                                unsigned int* __restrict__ cursor, int* __restrict__ counts) {
+    __shared__ unsigned int s[1024];
+    __shared__ unsigned int carry;
+    const int h = blockIdx.x;
+    const unsigned int* hh = hist + (size_t)h * (d + 1);
+    unsigned int* cc = cursor + (size_t)h * (d + 1);
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    // bins r = d-1, d-2, ..., 1 (descending), processed 1024 at a time
+    for (int base = 0; base < d - 1; base += 1024) {
+        const int idx = base + threadIdx.x;           // position in descending order
+        const int r = d - 1 - idx;
+        const unsigned int v = (idx < d - 1) ? hh[r] : 0u;
+        s[threadIdx.x] = v;
+        __syncthreads();
+        for (int off = 1; off < 1024; off <<= 1) {    // Hillis-Steele inclusive scan
+            const unsigned int add = threadIdx.x >= off ? s[threadIdx.x - off] : 0u;
+            __syncthreads();
+            s[threadIdx.x] += add;
+            __syncthreads();
+        }
+        if (idx < d - 1) cc[r] = carry + s[threadIdx.x] - v;
+        __syncthreads();
+        if (threadIdx.x == 1023) carry += s[1023];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        cc[d] = 0;
+        counts[2 * h + 0] = (int)carry;
+        counts[2 * h + 1] = (int)hh[d];
+    }
+}
+
+// Scatter token ids (b * n + j) into the per-head lists. Order inside a bin is
+// whatever the atomics give: it only changes which warp encodes a token, never
+// the token's result.
+__global__ void __launch_bounds__(256) k2_scatter(const int32_t* __restrict__ budgets,
+                                                  const uint8_t* __restrict__ exact, int n, int heads, int d,
+                                                  long tokens, unsigned int* __restrict__ cursor,
+                                                  int32_t* __restrict__ samp_list, int32_t* __restrict__ exact_list) {
+    const long bh = blockIdx.y;
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    const long t = bh * n + j;
+    const int b = (int)(bh / heads), h = (int)(bh - (long)b * heads);
+    const int tok = b * n + j;
+    if (exact[t]) {
+        const unsigned int pos = atomicAdd(&cursor[(size_t)h * (d + 1) + d], 1u);
+        exact_list[(size_t)h * tokens + pos] = tok;
+    } else {
+        const unsigned int pos = atomicAdd(&cursor[(size_t)h * (d + 1) + min(budgets[t], d - 1)], 1u);
+        samp_list[(size_t)h * tokens + pos] = tok;
     }
 }
 

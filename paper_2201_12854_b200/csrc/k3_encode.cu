@@ -1,33 +1,39 @@
-// k3_encode.cu — K3: the MCA value encoding (gather-scale-accumulate).
+// k3_encode.cu — K3: the MCA value encoding.
 //
 // For every token-head (b, j, h) with budget r_j:
-//   exact_mask: H~[j] = X[j] . W_h
-//   otherwise:  H~[j] = sum_k X[j, s_k] / (r_j p(s_k)) * W_h[s_k]
+//   exact_mask: H~[j] = X[j] . W_h  -> k3b_encode_exact
+//   otherwise:  H~[j] = sum_k X[j, s_k] / (r_j p(s_k)) * W_h[s_k] -> k3_encode_sampled
 // with s_k = first i such that thr_h[i] > m_k, m_k = draw k of Philox stream
 // ((b_offset + b) * heads + h) * n + j, layer `layer`.
 //
-// Layout / scheduling:
+// k3_encode_sampled (gather-scale-accumulate):
 //   - grid = (G, heads); a CTA owns one head: W_h (d_in x 64) is staged in
 //     shared memory once with 16-byte coalesced loads, together with the
 //     sampler tables (53-bit thresholds, 1024-entry guide table, 1/p).
-//   - CTAs pull 64-token chunks of their head from a per-head atomic counter.
-//     Each chunk is rank-sorted by budget (exact tokens first) so the four
-//     tokens a warp processes together have similar sample counts, and warps
-//     pull groups of 4 tokens in that order (LPT): tokens bucketed by sample
-//     count keep warps balanced.
+//   - Work comes from K2's per-head list, sorted by budget, largest first.
+//     Warps pull 4 consecutive tokens at a time from a per-head atomic cursor
+//     (LPT order: the expensive tokens start first, the cheap ones fill the
+//     tail), so the 4 tokens a warp encodes together have near-equal budgets
+//     and the warp's octets stay converged.
 //   - An octet of 8 lanes encodes one token; lane l owns output columns
 //     [8l, 8l+8). Per round the octet draws 16 samples (8 Philox calls, 2
-//     53-bit draws each), resolves them with the guide table, then all 8 lanes
-//     walk the 16 samples in draw order: one 16/32-byte shared-memory load of
-//     the sampled W_h row and 8 FMAs per lane per sample.
+//     53-bit draws each) and resolves them with the guide table; the next
+//     round's draws and X gathers are issued before the current round is
+//     accumulated (software pipelining), and the token's X row is prefetched
+//     into L1 when the token starts. Accumulation walks the 16 samples in draw
+//     order: one 16/32-byte shared-memory load of the sampled W_h row and 8 FMAs
+//     per lane per sample.
 // The fp32 path (Acc = double) forms each coefficient exactly as the oracle
 // does, x / (r * p) in binary64, and accumulates in fp64; the bf16 path uses
 // fp32 coefficients x * (1/p) * (1/r) and fp32 accumulation.
+//
+// k3b_encode_exact: exact token-heads (~6% of token-heads, but each costs a
+// full 768-long dot product per output) as a tiled GEMM over K2's per-head
+// exact list: 64 gathered tokens x 64 outputs per tile, K staged 32 at a time.
 #include "mca_common.cuh"
 
 namespace mca_dev {
 
-constexpr int kChunk = 64;   // tokens per chunk
 constexpr int kK3Threads = 256;
 
 template <class T>
@@ -37,42 +43,59 @@ struct CoefT<float> { using type = double; };          // p(i) in fp64 (exact or
 template <>
 struct CoefT<__nv_bfloat16> { using type = float; };   // 1/p(i) in fp32
 
-__device__ __forceinline__ void load8w(const __nv_bfloat16* p, float v[8]) { load8(p, v); }
-__device__ __forceinline__ void load8w(const float* p, float v[8]) { load8(p, v); }
+struct K3Args {
+    const void* x;             // [B, n, d_in]
+    const void* wv;            // [d_in, H*64]
+    int d_in, heads, n;
+    long tokens;               // B * n
+    long b_offset;
+    uint32_t layer;
+    uint64_t seed;
+    const int32_t* budgets;    // [B, H, n]
+    const uint64_t* thr;       // [H, d_in]
+    const uint16_t* guide;     // [H, kGuide]
+    const double* probs;       // [H, d_in]
+    const float* invp;         // [H, d_in]
+    void* h_out;               // [B, n, H*64]
+    int32_t* draws_out;
+    int draws_stride;
+    unsigned long long* sample_counter;
+    const int32_t* samp_list;  // [H, tokens]
+    const int32_t* exact_list; // [H, tokens]
+    const int* counts;         // [H, 2]: sampled, exact
+    int* task_cursor;          // [H]
+};
+
+size_t k3_smem_bytes(int d_in, size_t elem, size_t coef, bool wsmem) {
+    const size_t head = (((size_t)d_in * (8 + coef) + kGuide * 2) + 127) & ~(size_t)127;
+    return head + (wsmem ? (size_t)d_in * kDh * elem : 0);
+}
 
 template <class T, class Acc, bool kWSmem>
-__global__ void __launch_bounds__(kK3Threads) k3_encode(
-    const T* __restrict__ x, const T* __restrict__ wv, int d_in, int heads, int n, int B, long b_offset,
-    uint32_t layer, uint64_t seed, const int32_t* __restrict__ budgets, const uint8_t* __restrict__ exact,
-    const uint64_t* __restrict__ thr_all, const uint16_t* __restrict__ guide_all,
-    const double* __restrict__ probs_all, const float* __restrict__ invp_all, T* __restrict__ h_out,
-    int32_t* __restrict__ draws_out, int draws_stride, unsigned long long* __restrict__ sample_counter,
-    int* __restrict__ chunk_counter) {
+__global__ void __launch_bounds__(kK3Threads) k3_encode_sampled(K3Args a) {
     using Coef = typename CoefT<T>::type;
     extern __shared__ __align__(16) unsigned char smem[];
     const int h = blockIdx.y;
     const int tid = threadIdx.x, lane = tid & 31;
     const int oct = lane >> 3, l8 = lane & 7;
     const unsigned omask = 0xFFu << (oct * 8);
+    const int d_in = a.d_in, n = a.n, heads = a.heads;
 
-    // ---- shared memory carve-up
     uint64_t* s_thr = reinterpret_cast<uint64_t*>(smem);
     Coef* s_coef = reinterpret_cast<Coef*>(s_thr + d_in);
     uint16_t* s_guide = reinterpret_cast<uint16_t*>(s_coef + d_in);
-    int* s_order = reinterpret_cast<int*>(s_guide + kGuide);
-    int* s_key = s_order + kChunk;
-    int* s_misc = s_key + kChunk;  // [0] chunk id, [1] group counter
-    T* s_w = reinterpret_cast<T*>(smem + ((((size_t)d_in * (8 + sizeof(Coef)) + kGuide * 2 + (2 * kChunk + 4) * 4) + 127) & ~(size_t)127));
+    T* s_w = reinterpret_cast<T*>(smem + ((((size_t)d_in * (8 + sizeof(Coef)) + kGuide * 2) + 127) & ~(size_t)127));
 
     const size_t HD = (size_t)heads * kDh;
+    const T* wv = reinterpret_cast<const T*>(a.wv);
     for (int i = tid; i < d_in; i += kK3Threads) {
-        s_thr[i] = thr_all[(size_t)h * d_in + i];
-        if constexpr (sizeof(Coef) == 8) s_coef[i] = (Coef)probs_all[(size_t)h * d_in + i];
-        else s_coef[i] = (Coef)invp_all[(size_t)h * d_in + i];
+        s_thr[i] = a.thr[(size_t)h * d_in + i];
+        if constexpr (sizeof(Coef) == 8) s_coef[i] = (Coef)a.probs[(size_t)h * d_in + i];
+        else s_coef[i] = (Coef)a.invp[(size_t)h * d_in + i];
     }
-    for (int g = tid; g < kGuide; g += kK3Threads) s_guide[g] = guide_all[(size_t)h * kGuide + g];
+    for (int g = tid; g < kGuide; g += kK3Threads) s_guide[g] = a.guide[(size_t)h * kGuide + g];
     if constexpr (kWSmem) {
-        constexpr int kVec = 16 / sizeof(T);            // elements per 16-byte vector
+        constexpr int kVec = 16 / sizeof(T);
         const int vecs_per_row = kDh / kVec;
         for (int e = tid; e < d_in * vecs_per_row; e += kK3Threads) {
             const int i = e / vecs_per_row, v = e % vecs_per_row;
@@ -80,143 +103,177 @@ __global__ void __launch_bounds__(kK3Threads) k3_encode(
                 reinterpret_cast<const uint4*>(wv + (size_t)i * HD + (size_t)h * kDh)[v];
         }
     }
+    __syncthreads();
     const T* wsrc = kWSmem ? s_w : (wv + (size_t)h * kDh);
     const size_t wstride = kWSmem ? (size_t)kDh : HD;
-
-    const int chunks_per_seq = (n + kChunk - 1) / kChunk;
-    const int nchunks = B * chunks_per_seq;
+    const int nsamp = a.counts[2 * h];
+    const int32_t* list = a.samp_list + (size_t)h * a.tokens;
+    const T* x = reinterpret_cast<const T*>(a.x);
+    T* hout = reinterpret_cast<T*>(a.h_out);
     unsigned long long my_samples = 0;
 
     for (;;) {
-        __syncthreads();  // previous chunk fully consumed (and tables staged on the first pass)
-        if (tid == 0) {
-            s_misc[0] = atomicAdd(chunk_counter + h, 1);
-            s_misc[1] = 0;
+        int t0 = 0;
+        if (lane == 0) t0 = atomicAdd(a.task_cursor + h, 4);
+        t0 = __shfl_sync(0xffffffffu, t0, 0);
+        if (t0 >= nsamp) break;
+        const int my = t0 + oct;
+        if (my >= nsamp) continue;                       // octet-uniform
+        const int tok = list[my];
+        const int b = tok / n, j = tok - b * n;
+        const size_t tokh = ((size_t)b * heads + h) * n + j;
+        const int r = a.budgets[tokh];
+        const T* xrow = x + (size_t)tok * d_in;
+        {   // pull the token's X row into L1 ahead of the random gathers
+            const int lines = (int)((d_in * sizeof(T) + 127) / 128);
+            for (int ln = l8; ln < lines; ln += 8)
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(reinterpret_cast<const char*>(xrow) + ln * 128));
         }
-        __syncthreads();
-        const int c = s_misc[0];
-        if (c >= nchunks) break;
-        const int b = c / chunks_per_seq, j0 = (c % chunks_per_seq) * kChunk;
-        const size_t tok_base = ((size_t)b * heads + h) * n;  // [B, H, n] index of token 0
+        const uint64_t stream = ((uint64_t)(a.b_offset + b) * heads + h) * (uint64_t)n + (uint64_t)j;
+        const float inv_r = 1.0f / (float)r;
+        const double rd = (double)r;
 
-        // rank-sort the chunk by cost: exact tokens first, then budget descending
-        if (tid < kChunk) {
-            const int j = j0 + tid;
-            int key = -1;
-            if (j < n) key = exact[tok_base + j] ? (1 << 30) : budgets[tok_base + j];
-            s_key[tid] = key;
-        }
-        __syncthreads();
-        if (tid < kChunk) {
-            const int key = s_key[tid];
-            int rank = 0;
-            for (int u = 0; u < kChunk; ++u) {
-                const int ku = s_key[u];
-                rank += (ku > key) || (ku == key && u < tid);
+        // round state: indices and raw X values of the two draws this lane owns
+        auto gen = [&](int base, int& i0, int& i1, T& x0, T& x1) {
+            uint64_t m0, m1;
+            philox_pair53(a.seed, stream, a.layer, (uint32_t)(base / 2 + l8), &m0, &m1);
+            const int k0 = base + 2 * l8;
+            i0 = k0 < r ? sample_index(s_thr, s_guide, m0) : 0;
+            i1 = k0 + 1 < r ? sample_index(s_thr, s_guide, m1) : 0;
+            x0 = xrow[i0];
+            x1 = xrow[i1];
+        };
+        auto coef = [&](int i, T xv) -> Acc {
+            if constexpr (sizeof(Coef) == 8) return (Acc)__ddiv_rn((double)to_f32(xv), __dmul_rn(rd, (double)s_coef[i]));
+            else return (Acc)(to_f32(xv) * (float)s_coef[i] * inv_r);
+        };
+
+        Acc acc[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc[u] = (Acc)0;
+        int ni0, ni1;
+        T nx0, nx1;
+        gen(0, ni0, ni1, nx0, nx1);
+        for (int base = 0; base < r; base += 16) {
+            const int i0 = ni0, i1 = ni1;
+            const T x0 = nx0, x1 = nx1;
+            if (base + 16 < r) gen(base + 16, ni0, ni1, nx0, nx1);   // next round's loads in flight
+            const Acc c0 = coef(i0, x0), c1 = coef(i1, x1);
+            if (a.draws_out) {
+                const int k0 = base + 2 * l8;
+                if (k0 < r && k0 < a.draws_stride) a.draws_out[tokh * a.draws_stride + k0] = i0;
+                if (k0 + 1 < r && k0 + 1 < a.draws_stride) a.draws_out[tokh * a.draws_stride + k0 + 1] = i1;
             }
-            s_order[rank] = tid;
-        }
-        __syncthreads();
-
-        for (;;) {
-            int grp = 0;
-            if (lane == 0) grp = atomicAdd(&s_misc[1], 1);
-            grp = __shfl_sync(0xffffffffu, grp, 0);
-            if (grp * 4 >= kChunk) break;
-            const int t = s_order[grp * 4 + oct];
-            const int j = j0 + t;
-            if (s_key[t] < 0) continue;  // padding past n (octet-uniform)
-            const size_t tok = tok_base + j;
-            const int r = budgets[tok];
-            const bool ex = exact[tok] != 0;
-            const T* xrow = x + ((size_t)b * n + j) * d_in;
-            Acc acc[8];
+            const int cnt = min(16, r - base);
+            for (int s = 0; s < cnt; ++s) {
+                const int src = s >> 1;
+                const int idx = __shfl_sync(omask, (s & 1) ? i1 : i0, src, 8);
+                const Acc cf = __shfl_sync(omask, (s & 1) ? c1 : c0, src, 8);
+                float wr[8];
+                load8(wsrc + (size_t)idx * wstride + 8 * l8, wr);
 #pragma unroll
-            for (int u = 0; u < 8; ++u) acc[u] = (Acc)0;
-
-            if (ex) {
-                for (int i0 = 0; i0 < d_in; i0 += 8) {
-                    const float xv = (i0 + l8 < d_in) ? to_f32(xrow[i0 + l8]) : 0.0f;
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) {
-                        const float xi = __shfl_sync(omask, xv, u, 8);
-                        if (i0 + u < d_in) {
-                            float wr[8];
-                            load8w(wsrc + (size_t)(i0 + u) * wstride + 8 * l8, wr);
-#pragma unroll
-                            for (int q = 0; q < 8; ++q) acc[q] += (Acc)xi * (Acc)wr[q];
-                        }
-                    }
-                }
-                if (draws_out && l8 == 0)
-                    for (int k = 0; k < draws_stride; ++k) draws_out[tok * draws_stride + k] = -1;
-            } else {
-                const uint64_t stream = ((uint64_t)(b_offset + b) * heads + h) * (uint64_t)n + (uint64_t)j;
-                const float inv_r = 1.0f / (float)r;
-                const double rd = (double)r;
-                for (int base = 0; base < r; base += 16) {
-                    uint64_t m0, m1;
-                    philox_pair53(seed, stream, layer, (uint32_t)(base / 2 + l8), &m0, &m1);
-                    const int k0 = base + 2 * l8, k1 = k0 + 1;
-                    int i0 = 0, i1 = 0;
-                    Acc c0 = 0, c1 = 0;
-                    if (k0 < r) {
-                        i0 = sample_index(s_thr, s_guide, m0);
-                        const float xv = to_f32(xrow[i0]);
-                        if constexpr (sizeof(Coef) == 8) c0 = (Acc)__ddiv_rn((double)xv, __dmul_rn(rd, (double)s_coef[i0]));
-                        else c0 = (Acc)(xv * (float)s_coef[i0] * inv_r);
-                    }
-                    if (k1 < r) {
-                        i1 = sample_index(s_thr, s_guide, m1);
-                        const float xv = to_f32(xrow[i1]);
-                        if constexpr (sizeof(Coef) == 8) c1 = (Acc)__ddiv_rn((double)xv, __dmul_rn(rd, (double)s_coef[i1]));
-                        else c1 = (Acc)(xv * (float)s_coef[i1] * inv_r);
-                    }
-                    if (draws_out) {
-                        if (k0 < r && k0 < draws_stride) draws_out[tok * draws_stride + k0] = i0;
-                        if (k1 < r && k1 < draws_stride) draws_out[tok * draws_stride + k1] = i1;
-                    }
-                    const int cnt = min(16, r - base);
-                    for (int s = 0; s < cnt; ++s) {
-                        const int src = s >> 1;
-                        const int idx = __shfl_sync(omask, (s & 1) ? i1 : i0, src, 8);
-                        const Acc cf = __shfl_sync(omask, (s & 1) ? c1 : c0, src, 8);
-                        float wr[8];
-                        load8w(wsrc + (size_t)idx * wstride + 8 * l8, wr);
-#pragma unroll
-                        for (int q = 0; q < 8; ++q) acc[q] += cf * (Acc)wr[q];
-                    }
-                    if (l8 == 0) my_samples += (unsigned long long)cnt;
-                }
-                if (draws_out && l8 == 0)
-                    for (int k = r; k < draws_stride; ++k) draws_out[tok * draws_stride + k] = -1;
+                for (int q = 0; q < 8; ++q) acc[q] += cf * (Acc)wr[q];
             }
-            float o[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) o[u] = (float)acc[u];
-            T* dst = h_out + ((size_t)b * n + j) * HD + (size_t)h * kDh + 8 * l8;
-            store8(dst, o);
+            if (l8 == 0) my_samples += (unsigned long long)cnt;
         }
+        if (a.draws_out && l8 == 0)
+            for (int k = r; k < a.draws_stride; ++k) a.draws_out[tokh * a.draws_stride + k] = -1;
+        float o[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) o[u] = (float)acc[u];
+        store8(hout + (size_t)tok * HD + (size_t)h * kDh + 8 * l8, o);
     }
-    if (sample_counter) {
+    if (a.sample_counter) {
         for (int off = 16; off; off >>= 1) my_samples += __shfl_xor_sync(0xffffffffu, my_samples, off);
-        if (lane == 0 && my_samples) atomicAdd(sample_counter, my_samples);
+        if (lane == 0 && my_samples) atomicAdd(a.sample_counter, my_samples);
     }
 }
 
-size_t k3_smem_bytes(int d_in, size_t elem, size_t coef, bool wsmem) {
-    size_t head = (((size_t)d_in * (8 + coef) + kGuide * 2 + (2 * kChunk + 4) * 4) + 127) & ~(size_t)127;
-    return head + (wsmem ? (size_t)d_in * kDh * elem : 0);
+// Exact tokens: tiles of 64 listed tokens x 64 outputs; 256 threads, each 4 x 4.
+template <class T, class Acc>
+__global__ void __launch_bounds__(256) k3b_encode_exact(K3Args a) {
+    constexpr int kTM = 64, kTK = 32;
+    __shared__ Acc xs[kTK][kTM + 4];     // transposed X chunk: xs[k][token]
+    __shared__ Acc ws[kTK][kDh + 4];
+    __shared__ int toks[kTM];
+    const int h = blockIdx.y;
+    const int ne = a.counts[2 * h + 1];
+    const int tiles = (ne + kTM - 1) / kTM;
+    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;   // outputs 4*tx.., tokens 4*ty..
+    const size_t HD = (size_t)a.heads * kDh;
+    const T* x = reinterpret_cast<const T*>(a.x);
+    const T* wv = reinterpret_cast<const T*>(a.wv);
+    T* hout = reinterpret_cast<T*>(a.h_out);
+    const int32_t* list = a.exact_list + (size_t)h * a.tokens;
+    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        __syncthreads();
+        if (tid < kTM) toks[tid] = (tile * kTM + tid < ne) ? list[tile * kTM + tid] : -1;
+        __syncthreads();
+        Acc acc[4][4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) acc[i][jj] = (Acc)0;
+        for (int k0 = 0; k0 < a.d_in; k0 += kTK) {
+            // X chunk: 64 tokens x 32 k (8 consecutive k per thread), W chunk: 32 k x 64 outputs
+            {
+                const int tm = tid >> 2, kq = (tid & 3) * 8;
+                const int tok = toks[tm];
+                float v[8];
+                if (tok >= 0 && k0 + kq + 8 <= a.d_in) {
+                    load8(x + (size_t)tok * a.d_in + k0 + kq, v);
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 8; ++e)
+                        v[e] = (tok >= 0 && k0 + kq + e < a.d_in) ? to_f32(x[(size_t)tok * a.d_in + k0 + kq + e]) : 0.f;
+                }
+#pragma unroll
+                for (int e = 0; e < 8; ++e) xs[kq + e][tm] = (Acc)v[e];
+                const int kr = tid >> 3, c8 = (tid & 7) * 8;
+                float w8[8];
+                if (k0 + kr < a.d_in) load8(wv + (size_t)(k0 + kr) * HD + (size_t)h * kDh + c8, w8);
+                else
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) w8[e] = 0.f;
+#pragma unroll
+                for (int e = 0; e < 8; ++e) ws[kr][c8 + e] = (Acc)w8[e];
+            }
+            __syncthreads();
+#pragma unroll 8
+            for (int kk = 0; kk < kTK; ++kk) {
+                Acc av[4], bv[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) av[i] = xs[kk][ty * 4 + i];
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) bv[jj] = ws[kk][tx * 4 + jj];
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int jj = 0; jj < 4; ++jj) acc[i][jj] += av[i] * bv[jj];
+            }
+            __syncthreads();
+        }
+        if (a.draws_out && tid < kTM && toks[tid] >= 0) {   // exact token-heads draw nothing
+            const int tok = toks[tid], b = tok / a.n, j = tok - b * a.n;
+            const size_t tokh = ((size_t)b * a.heads + h) * a.n + j;
+            for (int k = 0; k < a.draws_stride; ++k) a.draws_out[tokh * a.draws_stride + k] = -1;
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int tok = toks[ty * 4 + i];
+            if (tok < 0) continue;
+            T* dst = hout + (size_t)tok * HD + (size_t)h * kDh + tx * 4;
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) dst[jj] = from_f32<T>((float)acc[i][jj]);
+        }
+    }
 }
 
-#define MCA_K3_INST(T, A, S)                                                                                       \
-    template __global__ void k3_encode<T, A, S>(const T*, const T*, int, int, int, int, long, uint32_t, uint64_t,    \
-                                                const int32_t*, const uint8_t*, const uint64_t*, const uint16_t*,    \
-                                                const double*, const float*, T*, int32_t*, int, unsigned long long*, \
-                                                int*);
-MCA_K3_INST(float, double, true)
-MCA_K3_INST(float, double, false)
-MCA_K3_INST(__nv_bfloat16, float, true)
-MCA_K3_INST(__nv_bfloat16, float, false)
+template __global__ void k3_encode_sampled<float, double, true>(K3Args);
+template __global__ void k3_encode_sampled<float, double, false>(K3Args);
+template __global__ void k3_encode_sampled<__nv_bfloat16, float, true>(K3Args);
+template __global__ void k3_encode_sampled<__nv_bfloat16, float, false>(K3Args);
+template __global__ void k3b_encode_exact<float, double>(K3Args);
+template __global__ void k3b_encode_exact<__nv_bfloat16, float>(K3Args);
 
 }  // namespace mca_dev

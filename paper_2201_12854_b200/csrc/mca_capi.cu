@@ -129,8 +129,13 @@ struct mca_weights {
     int32_t* budgets = nullptr;               // [B, H, n]
     uint8_t* exact = nullptr;                 // [B, H, n]
     void* hbuf = nullptr;                     // [B, n, H*dh]
+    int32_t* samp_list = nullptr;             // [H, B*n] sampled tokens per head, budget-descending
+    int32_t* exact_list = nullptr;            // [H, B*n] exact tokens per head
     unsigned long long* counters = nullptr;   // [8]
-    int* chunk_counter = nullptr;             // [heads]
+    unsigned int* hist = nullptr;             // [H, d_in + 1] budget histogram
+    unsigned int* cursor = nullptr;           // [H, d_in + 1] scatter cursors
+    int* counts = nullptr;                    // [H, 2] sampled / exact token counts
+    int* task_cursor = nullptr;               // [H] K3 work cursor
     // timing
     bool timing = false;
     cudaEvent_t ev[5] = {};
@@ -148,6 +153,10 @@ void free_workspace(mca_weights* w) {
     cudaFree(w->budgets);
     cudaFree(w->exact);
     cudaFree(w->hbuf);
+    cudaFree(w->samp_list);
+    cudaFree(w->exact_list);
+    w->samp_list = nullptr;
+    w->exact_list = nullptr;
     w->lse = nullptr;
     w->row_m = nullptr;
     w->row_l = nullptr;
@@ -169,7 +178,9 @@ mca_status ensure_workspace(mca_weights* w, long tokens, mca_stream_t stream) {
         cudaMalloc(&w->colkey, th * sizeof(unsigned long long)) != cudaSuccess ||
         cudaMalloc(&w->budgets, th * sizeof(int32_t)) != cudaSuccess ||
         cudaMalloc(&w->exact, th * sizeof(uint8_t)) != cudaSuccess ||
-        cudaMalloc(&w->hbuf, th * w->dh * dtype_size(w->wdt)) != cudaSuccess) {
+        cudaMalloc(&w->hbuf, th * w->dh * dtype_size(w->wdt)) != cudaSuccess ||
+        cudaMalloc(&w->samp_list, th * sizeof(int32_t)) != cudaSuccess ||
+        cudaMalloc(&w->exact_list, th * sizeof(int32_t)) != cudaSuccess) {
         cudaGetLastError();
         free_workspace(w);
         return fail(MCA_ERR_ALLOC, "workspace allocation for %ld tokens failed", tokens);
@@ -192,22 +203,49 @@ template <class T, class Acc>
 mca_status launch_k3(mca_weights* w, const void* x, int B, int n, long b_offset, uint32_t layer, uint64_t seed,
                      void* hout, int32_t* draws, int draws_stride, mca_stream_t stream, int& launches) {
     using Coef = typename CoefT<T>::type;
+    K3Args a{};
+    a.x = x;
+    a.wv = w->w;
+    a.d_in = w->d_in;
+    a.heads = w->heads;
+    a.n = n;
+    a.tokens = (long)B * n;
+    a.b_offset = b_offset;
+    a.layer = layer;
+    a.seed = seed;
+    a.budgets = w->budgets;
+    a.thr = w->thr;
+    a.guide = w->guide;
+    a.probs = w->probs;
+    a.invp = w->invp;
+    a.h_out = hout;
+    a.draws_out = draws;
+    a.draws_stride = draws_stride;
+    a.sample_counter = w->counters + 3;
+    a.samp_list = w->samp_list;
+    a.exact_list = w->exact_list;
+    a.counts = w->counts;
+    a.task_cursor = w->task_cursor;
     size_t smem = k3_smem_bytes(w->d_in, sizeof(T), sizeof(Coef), true);
-    bool wsmem = smem <= 200 * 1024;
+    const bool wsmem = smem <= 200 * 1024;
     if (!wsmem) smem = k3_smem_bytes(w->d_in, sizeof(T), sizeof(Coef), false);
-    auto kern = wsmem ? k3_encode<T, Acc, true> : k3_encode<T, Acc, false>;
+    auto kern = wsmem ? k3_encode_sampled<T, Acc, true> : k3_encode_sampled<T, Acc, false>;
     MCA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int occ = 0;
     MCA_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kK3Threads, smem));
     if (occ < 1) occ = 1;
-    const int chunks = B * ((n + kChunk - 1) / kChunk);
     int G = (sm_count() * occ + w->heads - 1) / w->heads;
-    if (G > chunks) G = chunks;
+    const long cap = (a.tokens + 31) / 32;   // at most one CTA per 32 tokens of a head
+    if (G > cap) G = (int)cap;
     if (G < 1) G = 1;
-    kern<<<dim3(G, w->heads), kK3Threads, smem, stream>>>(
-        (const T*)x, (const T*)w->w, w->d_in, w->heads, n, B, b_offset, layer, seed, w->budgets, w->exact, w->thr,
-        w->guide, w->probs, w->invp, (T*)hout, draws, draws_stride, w->counters + 3, w->chunk_counter);
-    MCA_LAUNCH_CHECK("k3_encode");
+    kern<<<dim3(G, w->heads), kK3Threads, smem, stream>>>(a);
+    MCA_LAUNCH_CHECK("k3_encode_sampled");
+    int Ge = (2 * sm_count() + w->heads - 1) / w->heads;
+    const long ecap = (a.tokens + 63) / 64;
+    if (Ge > ecap) Ge = (int)ecap;
+    if (Ge < 1) Ge = 1;
+    k3b_encode_exact<T, Acc><<<dim3(Ge, w->heads), 256, 0, stream>>>(a);
+    MCA_LAUNCH_CHECK("k3b_encode_exact");
     return MCA_OK;
 }
 
@@ -251,7 +289,10 @@ mca_status mca_prepare_weights(const void* w_v, mca_dtype wdt, int d_in, int hea
         cudaMalloc(&w->cdf, hd * 8) != cudaSuccess || cudaMalloc(&w->thr, hd * 8) != cudaSuccess ||
         cudaMalloc(&w->invp, hd * 4) != cudaSuccess || cudaMalloc(&w->guide, (size_t)heads * kGuide * 2) != cudaSuccess ||
         cudaMalloc(&w->counters, 8 * sizeof(unsigned long long)) != cudaSuccess ||
-        cudaMalloc(&w->chunk_counter, heads * sizeof(int)) != cudaSuccess || cudaMalloc(&sq, hd * 8) != cudaSuccess ||
+        cudaMalloc(&w->hist, (size_t)heads * (d_in + 1) * 4) != cudaSuccess ||
+        cudaMalloc(&w->cursor, (size_t)heads * (d_in + 1) * 4) != cudaSuccess ||
+        cudaMalloc(&w->counts, heads * 2 * sizeof(int)) != cudaSuccess ||
+        cudaMalloc(&w->task_cursor, heads * sizeof(int)) != cudaSuccess || cudaMalloc(&sq, hd * 8) != cudaSuccess ||
         cudaMalloc(&status, heads * sizeof(int)) != cudaSuccess) {
         cudaGetLastError();
         return cleanup(fail(MCA_ERR_ALLOC, "weight table allocation failed"));
@@ -282,7 +323,10 @@ void mca_weights_free(mca_weights* w) {
     cudaFree(w->invp);
     cudaFree(w->guide);
     cudaFree(w->counters);
-    cudaFree(w->chunk_counter);
+    cudaFree(w->hist);
+    cudaFree(w->cursor);
+    cudaFree(w->counts);
+    cudaFree(w->task_cursor);
     for (auto& e : w->ev)
         if (e) cudaEventDestroy(e);
     delete w;
@@ -329,10 +373,12 @@ mca_status mca_stage_budgets(const double* cmax, long count, int n, int d, const
     if (count < 0 || n <= 0 || d <= 0) return fail(MCA_ERR_SHAPE, "bad count / n / d");
     if (count == 0) return MCA_OK;
     int launches = 0;
-    const int grid = (int)std::min<long>((count + 255) / 256, 65535);
+    if (count > 0x7FFFFFFF) return fail(MCA_ERR_SHAPE, "count too large");
+    const dim3 grid((unsigned)((count + 255) / 256), 1);
     K2Args a{};
     a.cmax_in = cmax;
     a.count = count;
+    a.row_len = (int)count;
     a.n = n;
     a.heads = 1;
     a.d = d;
@@ -374,7 +420,8 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
     if (w->timing) MCA_CUDA_TRY(cudaEventRecord(w->ev[0], stream));
     MCA_CUDA_TRY(cudaMemsetAsync(w->colkey, 0, th * sizeof(unsigned long long), stream));
     MCA_CUDA_TRY(cudaMemsetAsync(w->counters, 0, 8 * sizeof(unsigned long long), stream));
-    MCA_CUDA_TRY(cudaMemsetAsync(w->chunk_counter, 0, H * sizeof(int), stream));
+    MCA_CUDA_TRY(cudaMemsetAsync(w->hist, 0, (size_t)H * (w->d_in + 1) * 4, stream));
+    MCA_CUDA_TRY(cudaMemsetAsync(w->task_cursor, 0, H * sizeof(int), stream));
 
     // K1: row statistics + column maxima
     {
@@ -405,7 +452,7 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
     if (w->timing) MCA_CUDA_TRY(cudaEventRecord(w->ev[1], stream));
     // K2: Eq. 9 budgets
     {
-        const int grid = (int)std::min<long>((th + 255) / 256, 4 * 148 * 8);
+        const dim3 grid((n + 255) / 256, (unsigned)(B * H));
         K2Args a{};
         a.colkey = w->colkey;
         a.cmax_in = dbg ? dbg->cmax_override : nullptr;
@@ -415,6 +462,7 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
         a.k = k;
         a.scale = scale;
         a.count = th;
+        a.row_len = n;
         a.n = n;
         a.heads = H;
         a.d = w->d_in;
@@ -428,10 +476,16 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
         a.exact = w->exact;
         a.cmax_out = dbg ? dbg->cmax_out : nullptr;
         a.counters = w->counters;
+        a.hist = w->hist;
         if (a.cmax_in) k2_budgets<kGivenCmax, float><<<grid, 256, 0, stream>>>(a);
         else if (dt == MCA_F32) k2_budgets<kKeyValue, float><<<grid, 256, 0, stream>>>(a);
         else k2_budgets<kKeyArgmax, __nv_bfloat16><<<grid, 256, 0, stream>>>(a);
         MCA_LAUNCH_CHECK("k2_budgets");
+        k2_scan<<<H, 1024, 0, stream>>>(w->hist, w->d_in, w->cursor, w->counts);
+        MCA_LAUNCH_CHECK("k2_scan");
+        k2_scatter<<<grid, 256, 0, stream>>>(w->budgets, w->exact, n, H, w->d_in, tokens, w->cursor, w->samp_list,
+                                             w->exact_list);
+        MCA_LAUNCH_CHECK("k2_scatter");
     }
     if (w->timing) MCA_CUDA_TRY(cudaEventRecord(w->ev[2], stream));
     // K3: encoding
