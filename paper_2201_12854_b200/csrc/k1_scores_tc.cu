@@ -1,79 +1,89 @@
 // k1_scores_tc.cu — K1 on the 5th-generation tensor cores: the score pass of
-// attention_matrix + col_max (matrix.hpp:46-53) for one
-// (b, h, 128-query tile) per CTA, bf16 inputs.
+// attention_matrix + col_max (matrix.hpp:46-53), bf16.
 //
-//   S_kb = Q K_kb^T     tcgen05.mma M=128 N=128 K=64 into TMEM (fp32), issued by
-//                       one thread; Q and K tiles arrive by TMA (128B swizzle)
-//   sweep 1 (per row):  online m = max t, l = sum exp(t - m), t = scale*S, in
-//                       the log2 domain with ex2.approx (one TMEM lane per row)
-//   sweep 2 (per col):  v = t - m - log l; warp butterfly max (reduce-scatter),
-//                       cross-warp max in smem, then the winning row is found by
-//                       exact comparison and packed into the argmax key that K2
-//                       re-evaluates in fp64 (k1_scores_simt.cu explains the key)
-// For n <= 512 every S block stays resident in TMEM (4 x 128 columns), so
-// sweep 2 re-reads TMEM instead of recomputing; for n > 512 the K blocks stream
-// twice through a 4-stage TMA ring and S is recomputed in sweep 2.
-// Warp roles (192 threads): 0 TMA producer, 1 TMEM allocator + MMA issuer,
-// 2-5 softmax / column reduction.
+// Softmax needs a reduction along rows (max and sum per query) and Eq. 9 needs
+// one along columns (max per key). Each is made lane-local by putting the
+// reduced index on the TMEM lane axis, so neither needs shuffles or atomics:
+//
+//   K1a (kRowStats), CTA = (b, h, 128 queries):  S   = Q K_blk^T (lane = query)
+//       per lane: online m = max t, l = sum exp(t - m) over all keys,
+//       t = scale * S (log2 domain, ex2.approx)  -> row_m, row_l (fp64), lse
+//   K1b (kColMax),   CTA = (b, h, 128 keys):     S^T = K Q_blk^T (lane = key)
+//       per lane: max over all queries of v = t - lse_q and its first argmax
+//       q*, written as the argmax key K2 re-evaluates in fp64
+//       (k1_scores_simt.cu describes the key; one writer per key, no atomics)
+//
+// Same kernel body for both: the resident 128-row operand (Q or K) arrives by
+// TMA once, the streamed operand (K or Q blocks of 128) through a 3-stage TMA
+// ring; one thread issues tcgen05.mma M=128 N=128 K=16 x4 per block into a
+// double-buffered TMEM accumulator (2 x 128 columns, so two CTAs fit per SM).
+// Eight consumer warps: two per TMEM lane quadrant, each owning 64 of the 128
+// columns of a block; the two halves combine through shared memory at the end.
+// Warp 0: TMA producer, warp 1: TMEM allocator + MMA issuer.
 #include "mca_common.cuh"
 #include "tc_common.cuh"
 
 namespace mca_dev {
 
 namespace k1tc {
-constexpr int kBM = 128, kBK = 128, kBufs = 4;
-constexpr int kThreads = 192;
-constexpr uint32_t kTileBytes = 128 * kDh * 2;                 // 16 KB
-constexpr uint32_t kSmemQ = 0;
-constexpr uint32_t kSmemK = kTileBytes;                         // kBufs tiles
-constexpr uint32_t kSmemRed = kSmemK + kBufs * kTileBytes;      // [4][128] f32 warp maxima
-constexpr uint32_t kSmemColM = kSmemRed + 4 * 128 * 4;          // [128] f32
-constexpr uint32_t kSmemWin = kSmemColM + 128 * 4;              // [128] i32
-constexpr uint32_t kSmemBar = kSmemWin + 128 * 4;
+constexpr int kBM = 128, kBN = 128, kStages = 3;
+constexpr int kConsumers = 8;
+constexpr int kThreads = 64 + kConsumers * 32;
+constexpr uint32_t kTileBytes = 128 * kDh * 2;                   // 16 KB
+constexpr uint32_t kSmemA = 0;                                    // resident operand
+constexpr uint32_t kSmemB = kTileBytes;                           // kStages streamed tiles
+constexpr uint32_t kSmemLse = kSmemB + kStages * kTileBytes;      // [kMaxN] f32 (K1b)
+constexpr int kMaxN = 4096;
+constexpr uint32_t kSmemComb = kSmemLse + kMaxN * 4;              // partner exchange, 2 x [128] x 4 B
+constexpr uint32_t kSmemBar = kSmemComb + 4 * 128 * 4;
 constexpr uint32_t kSmemBytes = kSmemBar + 256 + 1024;
-constexpr uint32_t kIdescS = mca_tc::idesc_f16(1, 0, kBM, kBK);
+constexpr uint32_t kIdesc = mca_tc::idesc_f16(1, 0, kBM, kBN);
 }  // namespace k1tc
 
-__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
-}
+enum K1Mode { kRowStats = 0, kColMax = 1 };
 
-__global__ void __launch_bounds__(k1tc::kThreads, 1)
+template <int kMode>
+__global__ void __launch_bounds__(k1tc::kThreads, 2)
     k1_scores_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k, int n,
                  int heads, float scale, double* __restrict__ row_m, double* __restrict__ row_l,
-                 float* __restrict__ lse_out, unsigned long long* __restrict__ colkey) {
+                 float* __restrict__ lse, unsigned long long* __restrict__ colkey) {
     using namespace k1tc;
     using namespace mca_tc;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kSmemBar);
-    uint64_t* q_full = bars;
-    uint64_t* kv_full = bars + 1;            // [kBufs]
-    uint64_t* kv_empty = kv_full + kBufs;    // [kBufs]
-    uint64_t* s_full = kv_empty + kBufs;     // [kBufs]
-    uint64_t* s_empty = s_full + kBufs;      // [kBufs]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_empty + kBufs);
-    float* red = reinterpret_cast<float*>(smem + kSmemRed);
-    float* colM = reinterpret_cast<float*>(smem + kSmemColM);
-    int* win = reinterpret_cast<int*>(smem + kSmemWin);
+    uint64_t* a_full = bars;
+    uint64_t* b_full = bars + 1;              // [kStages]
+    uint64_t* b_empty = b_full + kStages;     // [kStages]
+    uint64_t* s_full = b_empty + kStages;     // [2]
+    uint64_t* s_empty = s_full + 2;           // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_empty + 2);
+    float* s_lse = reinterpret_cast<float*>(smem + kSmemLse);
+    float* comb = reinterpret_cast<float*>(smem + kSmemComb);
 
+    const CUtensorMap* tm_a = kMode == kRowStats ? &tm_q : &tm_k;   // resident rows
+    const CUtensorMap* tm_b = kMode == kRowStats ? &tm_k : &tm_q;   // streamed blocks
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int b = blockIdx.z, h = blockIdx.y, m0 = blockIdx.x * kBM;
-    const int nkb = (n + kBK - 1) / kBK;
-    const bool resident = nkb <= kBufs;
-    const int items = resident ? nkb : 2 * nkb;   // S blocks the tensor core produces
+    const int b = blockIdx.z, h = blockIdx.y, r0 = blockIdx.x * kBM;
+    const int nblk = (n + kBN - 1) / kBN;
+    const size_t bh = (size_t)b * heads + h;
 
     if (threadIdx.x == 0) {
-        mbar_init(q_full, 1);
-        for (int s = 0; s < kBufs; ++s) {
-            mbar_init(kv_full + s, 1);
-            mbar_init(kv_empty + s, 1);
-            mbar_init(s_full + s, 1);
-            mbar_init(s_empty + s, 128);
+        mbar_init(a_full, 1);
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(b_full + s, 1);
+            mbar_init(b_empty + s, 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(s_full + i, 1);
+            mbar_init(s_empty + i, kConsumers * 32);
         }
         fence_barrier_init();
     }
-    if (warp == 1) tmem_alloc<512>(tmem_slot);
+    if (kMode == kColMax) {   // query log-sum-exps of this (b, h), log2 domain
+        for (int i = threadIdx.x; i < n; i += k1tc::kThreads) s_lse[i] = lse[bh * n + i] * 1.4426950408889634f;
+    }
+    if (warp == 1) tmem_alloc<256>(tmem_slot);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -81,148 +91,143 @@ __global__ void __launch_bounds__(k1tc::kThreads, 1)
 
     if (warp == 0) {
         if (lane == 0) {  // ---------------- TMA producer
-            tma_prefetch(&tm_q);
-            tma_prefetch(&tm_k);
-            mbar_expect_tx(q_full, kTileBytes);
-            tma_load_3d(smem + kSmemQ, &tm_q, q_full, h * kDh, m0, b);
-            for (int i = 0; i < items; ++i) {
-                const int s = i % kBufs;
-                mbar_wait(kv_empty + s, ((i / kBufs) & 1) ^ 1);
-                mbar_expect_tx(kv_full + s, kTileBytes);
-                tma_load_3d(smem + kSmemK + s * kTileBytes, &tm_k, kv_full + s, h * kDh, (i % nkb) * kBK, b);
+            tma_prefetch(tm_a);
+            tma_prefetch(tm_b);
+            mbar_expect_tx(a_full, kTileBytes);
+            tma_load_3d(smem + kSmemA, tm_a, a_full, h * kDh, r0, b);
+            for (int i = 0; i < nblk; ++i) {
+                const int s = i % kStages;
+                mbar_wait(b_empty + s, ((i / kStages) & 1) ^ 1);
+                mbar_expect_tx(b_full + s, kTileBytes);
+                tma_load_3d(smem + kSmemB + s * kTileBytes, tm_b, b_full + s, h * kDh, i * kBN, b);
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {  // ---------------- MMA issuer
-            const uint32_t q_addr = smem_u32(smem + kSmemQ);
-            mbar_wait(q_full, 0);
-            for (int i = 0; i < items; ++i) {
-                const int s = i % kBufs;
-                const uint32_t ph = (i / kBufs) & 1;
-                mbar_wait(kv_full + s, ph);
-                mbar_wait(s_empty + s, ph ^ 1);
+            const uint32_t a_addr = smem_u32(smem + kSmemA);
+            mbar_wait(a_full, 0);
+            for (int i = 0; i < nblk; ++i) {
+                const int s = i % kStages, sb = i & 1;
+                mbar_wait(b_full + s, (i / kStages) & 1);
+                mbar_wait(s_empty + sb, ((i >> 1) & 1) ^ 1);
                 tc_fence_after();
-                const uint32_t k_addr = smem_u32(smem + kSmemK + s * kTileBytes);
+                const uint32_t b_addr = smem_u32(smem + kSmemB + s * kTileBytes);
 #pragma unroll
                 for (int kk = 0; kk < kDh / 16; ++kk)
-                    umma_f16(tmem + s * kBK, sw128_desc(q_addr + kk * 32, 16, 1024),
-                             sw128_desc(k_addr + kk * 32, 16, 1024), kIdescS, kk > 0 ? 1u : 0u);
-                umma_commit(s_full + s);
-                umma_commit(kv_empty + s);
+                    umma_f16(tmem + sb * kBN, sw128_desc(a_addr + kk * 32, 16, 1024),
+                             sw128_desc(b_addr + kk * 32, 16, 1024), kIdesc, kk > 0 ? 1u : 0u);
+                umma_commit(s_full + sb);
+                umma_commit(b_empty + s);
             }
         }
-    } else {  // ------------------------------- softmax / column reduction (warps 2..5)
-        const int quad = warp & 3;
-        const int wi = warp - 2;                   // 0..3, index into the smem reduction buffers
-        const int row = quad * 32 + lane;
-        const int grow = m0 + row;
-        const bool row_ok = grow < n;
-        const uint32_t lane_base = tmem + ((uint32_t)(quad * 32) << 16);
-        const float c2 = scale * 1.4426950408889634f;   // t2 = S * c2 (log2 domain)
-        // ---- sweep 1: row max / sum
-        float m2 = -INFINITY, l = 0.0f;
-        for (int kb = 0; kb < nkb; ++kb) {
-            const int s = kb % kBufs;
-            mbar_wait(s_full + s, (kb / kBufs) & 1);
+    } else {  // ------------------------------- consumers (warps 2..9)
+        const int cw = warp - 2;
+        const int quad = warp & 3;                 // TMEM lane quadrant this warp may access
+        const int half = cw >> 2;                  // which 64 columns of each block
+        const int row = quad * 32 + lane;          // TMEM lane = resident row (query or key)
+        const int grow = r0 + row;
+        const uint32_t lane_base = tmem + ((uint32_t)(quad * 32) << 16) + half * 64;
+        const float c2 = scale * 1.4426950408889634f;
+        float m2 = -INFINITY, l = 0.0f;            // kRowStats
+        float best = -INFINITY;                    // kColMax
+        int best_i = 0x7FFFFFFF;
+        for (int i = 0; i < nblk; ++i) {
+            const int sb = i & 1;
+            mbar_wait(s_full + sb, (i >> 1) & 1);
             tc_fence_after();
-            uint32_t sv[4][32];
-#pragma unroll
-            for (int q4 = 0; q4 < 4; ++q4) tmem_ld32(lane_base + s * kBK + q4 * 32, sv[q4]);
+            uint32_t sv[2][32];
+            tmem_ld32(lane_base + sb * kBN, sv[0]);
+            tmem_ld32(lane_base + sb * kBN + 32, sv[1]);
             tmem_ld_wait();
-            if (!resident) {
-                tc_fence_before();
-                mbar_arrive(s_empty + s);
-            }
-            const int valid = min(kBK, n - kb * kBK);
-            float bmax = -INFINITY;
+            tc_fence_before();
+            mbar_arrive(s_empty + sb);
+            const int c0 = i * kBN + half * 64;        // global column index of sv[0][0]
+            const int valid = min(64, n - c0);         // <= 0 for the right half of a short last block
+            if constexpr (kMode == kRowStats) {
+                float bmax = -INFINITY;
+                if (valid >= 64) {
 #pragma unroll
-            for (int q4 = 0; q4 < 4; ++q4)
+                    for (int e = 0; e < 64; ++e) bmax = fmaxf(bmax, __uint_as_float(sv[e >> 5][e & 31]));
+                } else {
 #pragma unroll
-                for (int e = 0; e < 32; ++e)
-                    if (q4 * 32 + e < valid) bmax = fmaxf(bmax, __uint_as_float(sv[q4][e]) * c2);
-            const float mn = fmaxf(m2, bmax);
-            float acc = 0.0f;
-#pragma unroll
-            for (int q4 = 0; q4 < 4; ++q4)
-#pragma unroll
-                for (int e = 0; e < 32; ++e)
-                    if (q4 * 32 + e < valid) acc += ex2_approx(__uint_as_float(sv[q4][e]) * c2 - mn);
-            l = (m2 == -INFINITY ? 0.0f : l * ex2_approx(m2 - mn)) + acc;
-            m2 = mn;
-        }
-        const float lse2 = m2 + __log2f(l);        // log2-domain log-sum-exp
-        if (row_ok) {
-            const size_t t = ((size_t)b * heads + h) * n + grow;
-            row_m[t] = (double)m2 * 0.6931471805599453;
-            row_l[t] = (double)l;
-            lse_out[t] = lse2 * 0.6931471805599453f;
-        }
-        // ---- sweep 2: per-column maxima of v = t2 - lse2 and their argmax rows
-        for (int kb = 0; kb < nkb; ++kb) {
-            const int item = resident ? kb : nkb + kb;
-            const int s = item % kBufs;
-            if (!resident) {
-                mbar_wait(s_full + s, (item / kBufs) & 1);
-                tc_fence_after();
-            }
-            const int kbase = kb * kBK;
-            for (int q4 = 0; q4 < 4; ++q4) {
-                uint32_t sv[32];
-                tmem_ld32(lane_base + s * kBK + q4 * 32, sv);
-                tmem_ld_wait();
-                float v[32];
-#pragma unroll
-                for (int e = 0; e < 32; ++e) v[e] = row_ok ? __fmaf_rn(__uint_as_float(sv[e]), c2, -lse2) : -INFINITY;
-                // butterfly reduce-scatter: lane L ends with the warp max of column L
-#pragma unroll
-                for (int wdt = 16; wdt >= 1; wdt >>= 1) {
-                    const bool upper = (lane & wdt) != 0;
-#pragma unroll
-                    for (int i = 0; i < wdt; ++i) {
-                        const float send = upper ? v[i] : v[i + wdt];
-                        const float keep = upper ? v[i + wdt] : v[i];
-                        v[i] = fmaxf(keep, __shfl_xor_sync(0xffffffffu, send, wdt));
-                    }
+                    for (int e = 0; e < 64; ++e)
+                        if (e < valid) bmax = fmaxf(bmax, __uint_as_float(sv[e >> 5][e & 31]));
                 }
-                red[wi * 128 + q4 * 32 + lane] = v[0];
-            }
-            named_bar_sync(1, 128);
-            {   // thread `row` now owns column kbase + row of this block
-                const float M = fmaxf(fmaxf(red[row], red[128 + row]), fmaxf(red[256 + row], red[384 + row]));
-                colM[row] = M;
-                win[row] = 0x7FFFFFFF;
-            }
-            named_bar_sync(1, 128);
-            // exact re-comparison finds the winning row(s); smallest row wins. The
-            // TMEM load is warp-collective (.sync.aligned): every lane executes it.
-            for (int q4 = 0; q4 < 4; ++q4) {
-                uint32_t sv[32];
-                tmem_ld32(lane_base + s * kBK + q4 * 32, sv);
-                tmem_ld_wait();
-                if (row_ok) {
+                if (valid > 0) {
+                    const float mn = fmaxf(m2, bmax * c2);
+                    float acc0 = 0.f, acc1 = 0.f;
+                    if (valid >= 64) {
 #pragma unroll
-                    for (int e = 0; e < 32; ++e) {
-                        const float vv = __fmaf_rn(__uint_as_float(sv[e]), c2, -lse2);
-                        if (vv == colM[q4 * 32 + e]) atomicMin(&win[q4 * 32 + e], grow);
+                        for (int e = 0; e < 64; e += 2) {
+                            acc0 += ex2_approx(__fmaf_rn(__uint_as_float(sv[e >> 5][e & 31]), c2, -mn));
+                            acc1 += ex2_approx(__fmaf_rn(__uint_as_float(sv[(e + 1) >> 5][(e + 1) & 31]), c2, -mn));
+                        }
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < 64; ++e)
+                            if (e < valid) acc0 += ex2_approx(__fmaf_rn(__uint_as_float(sv[e >> 5][e & 31]), c2, -mn));
+                    }
+                    l = (m2 == -INFINITY ? 0.0f : l * ex2_approx(m2 - mn)) + (acc0 + acc1);
+                    m2 = mn;
+                }
+            } else {
+                // v = t2 - lse2_q; strict > keeps the first (smallest) query on ties
+#pragma unroll
+                for (int g = 0; g < 64; g += 4) {
+                    if (g < valid) {
+                        const float4 ls = *reinterpret_cast<const float4*>(s_lse + c0 + g);
+                        const float lv[4] = {ls.x, ls.y, ls.z, ls.w};
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const float v = __fmaf_rn(__uint_as_float(sv[(g + e) >> 5][(g + e) & 31]), c2, -lv[e]);
+                            if (g + e < valid && v > best) {
+                                best = v;
+                                best_i = c0 + g + e;
+                            }
+                        }
                     }
                 }
             }
-            if (!resident) {
-                tc_fence_before();
-                mbar_arrive(s_empty + s);
+        }
+        // combine the two column halves of each row through shared memory
+        if constexpr (kMode == kRowStats) {
+            if (half == 1) {
+                comb[row] = m2;
+                comb[128 + row] = l;
             }
-            named_bar_sync(1, 128);
-            if (kbase + row < n) {
-                const unsigned long long key = ((unsigned long long)float_to_ordered(colM[row]) << 32) |
-                                               (unsigned long long)(0xFFFFFFFFu - (uint32_t)win[row]);
-                atomicMax(colkey + ((size_t)b * heads + h) * n + kbase + row, key);
+        } else {
+            if (half == 1) {
+                comb[row] = best;
+                reinterpret_cast<int*>(comb)[128 + row] = best_i;
             }
-            named_bar_sync(1, 128);   // red / colM / win are reused by the next block
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(kConsumers * 32) : "memory");
+        if (half == 0 && grow < n) {
+            if constexpr (kMode == kRowStats) {
+                const float m2b = comb[row], lb = comb[128 + row];
+                const float mn = fmaxf(m2, m2b);
+                const float lt = (m2 == -INFINITY ? 0.f : l * ex2_approx(m2 - mn)) +
+                                 (m2b == -INFINITY ? 0.f : lb * ex2_approx(m2b - mn));
+                const size_t t = bh * n + grow;
+                row_m[t] = (double)mn * 0.6931471805599453;
+                row_l[t] = (double)lt;
+                lse[t] = (mn + __log2f(lt)) * 0.6931471805599453f;
+            } else {
+                const float vb = comb[row];
+                const int ib = reinterpret_cast<int*>(comb)[128 + row];
+                // ties go to the smaller query index (deterministic, order-independent)
+                if (vb > best || (vb == best && ib < best_i)) {
+                    best = vb;
+                    best_i = ib;
+                }
+                colkey[bh * n + grow] = ((unsigned long long)float_to_ordered(best) << 32) |
+                                        (unsigned long long)(0xFFFFFFFFu - (uint32_t)best_i);
+            }
         }
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 1) tmem_dealloc<512>(tmem);
+    if (warp == 1) tmem_dealloc<256>(tmem);
 }
 
 }  // namespace mca_dev

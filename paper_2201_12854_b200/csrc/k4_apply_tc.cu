@@ -3,15 +3,14 @@
 //
 // A is never materialised. Per 128-key block:
 //   S  = Q K_blk^T                  tcgen05.mma M=128 N=128 K=64 -> TMEM (fp32)
-//   P  = exp(scale*S - lse)         4 softmax warps, 1 TMEM lane (= query row)
-//                                   each; lse from K1, so no online rescaling;
-//                                   P written bf16 into a 128B-swizzled K-major
-//                                   smem tile
+//   P  = exp(scale*S - lse)         8 softmax warps, 2 per TMEM lane quadrant
+//                                   (lane = query row), 64 keys each; lse from
+//                                   K1, so no online rescaling; P written bf16
+//                                   into a 128B-swizzled K-major smem tile
 //   O += P H~_blk                   tcgen05.mma M=128 N=64 K=128 (H~ MN-major)
-// Warp roles (192 threads): warp 0 TMA producer (Q once, then a 3-stage ring of
-// K/H~ blocks), warp 1 TMEM allocator + single-thread MMA issuer, warps 2-5
-// softmax + epilogue. S is double-buffered in TMEM and P in smem, so the
-// tensor core computes S(kb+1) while the softmax warps exponentiate S(kb), and
+// Warp roles (320 threads): warp 0 TMA producer (Q once, then a 3-stage ring of
+// K/H~ blocks), warp 1 TMEM allocator + single-thread MMA issuer, warps 2-9
+// softmax + epilogue. S is double-buffered in TMEM and P in smem, so the tensor core computes S(kb+1) while the softmax warps exponentiate S(kb), and
 // P(kb) . H~(kb) overlaps the exponentials of block kb+1. TMEM: S0 [0,128),
 // S1 [128,256), O [256,320).
 #include "mca_common.cuh"
@@ -21,7 +20,8 @@ namespace mca_dev {
 
 namespace k4tc {
 constexpr int kBM = 128, kBK = 128, kStages = 3;
-constexpr int kThreads = 192;
+constexpr int kConsumers = 8;                        // 2 warps per TMEM lane quadrant
+constexpr int kThreads = 64 + kConsumers * 32;
 constexpr uint32_t kTileBytes = kBK * kDh * 2;       // 16 KB: one 128 x 64 bf16 tile
 constexpr uint32_t kPBytes = kBM * kBK * 2;          // 32 KB: P tile (two 64-key swizzle atoms)
 constexpr uint32_t kSmemQ = 0;
@@ -65,8 +65,8 @@ __global__ void __launch_bounds__(k4tc::kThreads, 1)
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(s_full + i, 1);
-            mbar_init(s_empty + i, 128);
-            mbar_init(p_full + i, 128);
+            mbar_init(s_empty + i, kConsumers * 32);
+            mbar_init(p_full + i, kConsumers * 32);
             mbar_init(p_empty + i, 1);
         }
         mbar_init(o_full, 1);
@@ -130,8 +130,9 @@ __global__ void __launch_bounds__(k4tc::kThreads, 1)
             issue_pv(nkb - 1);
             umma_commit(o_full);
         }
-    } else {  // ------------------------------- softmax + epilogue (warps 2..5)
+    } else {  // ------------------------------- softmax + epilogue (warps 2..9)
         const int quad = warp & 3;                 // TMEM lane quadrant this warp may access
+        const int half = (warp - 2) >> 2;          // keys [64*half, 64*half+64) of each block
         const int row = quad * 32 + lane;          // query row within the tile
         const uint32_t lane_base = tmem + ((uint32_t)(quad * 32) << 16);
         const float c = scale * 1.4426950408889634f;
@@ -142,55 +143,48 @@ __global__ void __launch_bounds__(k4tc::kThreads, 1)
             const uint32_t ph = (kb >> 1) & 1;
             mbar_wait(s_full + sb, ph);
             tc_fence_after();
-            uint32_t sv[4][32];
-#pragma unroll
-            for (int q4 = 0; q4 < 4; ++q4) tmem_ld32(lane_base + sb * kBK + q4 * 32, sv[q4]);
+            uint32_t sv[2][32];
+            tmem_ld32(lane_base + sb * kBK + half * 64, sv[0]);
+            tmem_ld32(lane_base + sb * kBK + half * 64 + 32, sv[1]);
             tmem_ld_wait();
             tc_fence_before();
             mbar_arrive(s_empty + sb);
             mbar_wait(p_empty + sb, ph ^ 1);
-            uint8_t* pt = smem + kSmemP + sb * kPBytes;
-            const int kbase = kb * kBK;
+            // this warp's 64 keys form exactly one 128B-swizzle atom column of P
+            uint8_t* pt = smem + kSmemP + sb * kPBytes + half * (kBM * 128);
+            const int kbase = kb * kBK + half * 64;
+            const int valid = n - kbase;          // keys >= n contribute nothing
 #pragma unroll
-            for (int q4 = 0; q4 < 4; ++q4) {
+            for (int ch = 0; ch < 8; ++ch) {       // 16-byte chunks of 8 keys
+                uint32_t pk[4];
 #pragma unroll
-                for (int ch = 0; ch < 4; ++ch) {       // 16-byte chunks of 8 keys
-                    uint32_t pk[4];
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const int col = q4 * 32 + ch * 8 + 2 * e;
-                        float p0 = ex2_approx(__uint_as_float(sv[q4][ch * 8 + 2 * e]) * c - lse2);
-                        float p1 = ex2_approx(__uint_as_float(sv[q4][ch * 8 + 2 * e + 1]) * c - lse2);
-                        if (kbase + col >= n) p0 = 0.0f;
-                        if (kbase + col + 1 >= n) p1 = 0.0f;
-                        pk[e] = pack_bf16x2(p0, p1);
-                    }
-                    const int key0 = q4 * 32 + ch * 8;                   // first key of the chunk
-                    const uint32_t off = (key0 >> 6) * (kBM * 128) + sw128_offset(row, (key0 & 63) * 2);
-                    *reinterpret_cast<uint4*>(pt + off) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                for (int e = 0; e < 4; ++e) {
+                    const int col = ch * 8 + 2 * e;
+                    float p0 = ex2_approx(__fmaf_rn(__uint_as_float(sv[col >> 5][col & 31]), c, -lse2));
+                    float p1 = ex2_approx(__fmaf_rn(__uint_as_float(sv[(col + 1) >> 5][(col + 1) & 31]), c, -lse2));
+                    if (col >= valid) p0 = 0.0f;
+                    if (col + 1 >= valid) p1 = 0.0f;
+                    pk[e] = pack_bf16x2(p0, p1);
                 }
+                *reinterpret_cast<uint4*>(pt + sw128_offset(row, ch * 16)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
             }
             fence_proxy_async_smem();
             mbar_arrive(p_full + sb);
         }
-        // epilogue: O (fp32, TMEM cols 256..319) -> bf16 -> y
+        // epilogue: O (fp32, TMEM cols 256..319) -> bf16 -> y; each half writes 32 columns
         mbar_wait(o_full, 0);
         tc_fence_after();
-        uint32_t ov[2][32];
-        tmem_ld32(lane_base + 256, ov[0]);
-        tmem_ld32(lane_base + 288, ov[1]);
+        uint32_t ov[32];
+        tmem_ld32(lane_base + 256 + half * 32, ov);
         tmem_ld_wait();
         if (grow < n) {
-            __nv_bfloat16* dst = y + ((size_t)b * n + grow) * (size_t)heads * kDh + (size_t)h * kDh;
+            __nv_bfloat16* dst = y + ((size_t)b * n + grow) * (size_t)heads * kDh + (size_t)h * kDh + half * 32;
 #pragma unroll
-            for (int g = 0; g < 8; ++g) {
+            for (int g = 0; g < 4; ++g) {
                 uint32_t pk[4];
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const int cidx = g * 8 + 2 * e;
-                    pk[e] = pack_bf16x2(__uint_as_float(ov[cidx >> 5][cidx & 31]),
-                                        __uint_as_float(ov[(cidx + 1) >> 5][(cidx + 1) & 31]));
-                }
+                for (int e = 0; e < 4; ++e)
+                    pk[e] = pack_bf16x2(__uint_as_float(ov[g * 8 + 2 * e]), __uint_as_float(ov[g * 8 + 2 * e + 1]));
                 reinterpret_cast<uint4*>(dst)[g] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
             }
         }

@@ -418,7 +418,8 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
     int launches = 0;
 
     if (w->timing) MCA_CUDA_TRY(cudaEventRecord(w->ev[0], stream));
-    MCA_CUDA_TRY(cudaMemsetAsync(w->colkey, 0, th * sizeof(unsigned long long), stream));
+    if (dt == MCA_F32 || force_simt() || n > k1tc::kMaxN)   // atomicMax column keys (the TC pass writes each once)
+        MCA_CUDA_TRY(cudaMemsetAsync(w->colkey, 0, th * sizeof(unsigned long long), stream));
     MCA_CUDA_TRY(cudaMemsetAsync(w->counters, 0, 8 * sizeof(unsigned long long), stream));
     MCA_CUDA_TRY(cudaMemsetAsync(w->hist, 0, (size_t)H * (w->d_in + 1) * 4, stream));
     MCA_CUDA_TRY(cudaMemsetAsync(w->task_cursor, 0, H * sizeof(int), stream));
@@ -429,7 +430,7 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
         if (dt == MCA_F32)
             k1_scores_simt<float, double><<<grid, kThreads, 0, stream>>>((const float*)q, (const float*)k, n, H, scale,
                                                                          w->row_m, w->row_l, w->lse, w->colkey);
-        else if (force_simt())
+        else if (force_simt() || n > k1tc::kMaxN)
             k1_scores_simt<__nv_bfloat16, float><<<grid, kThreads, 0, stream>>>(
                 (const __nv_bfloat16*)q, (const __nv_bfloat16*)k, n, H, scale, w->row_m, w->row_l, w->lse,
                 w->colkey);
@@ -440,11 +441,17 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
                 return fail(MCA_ERR_CUDA, "cuTensorMapEncodeTiled failed for q/k");
             static bool attr = false;
             if (!attr) {
-                MCA_CUDA_TRY(cudaFuncSetAttribute(k1_scores_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                MCA_CUDA_TRY(cudaFuncSetAttribute(k1_scores_tc<kRowStats>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  (int)k1tc::kSmemBytes));
+                MCA_CUDA_TRY(cudaFuncSetAttribute(k1_scores_tc<kColMax>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                   (int)k1tc::kSmemBytes));
                 attr = true;
             }
-            k1_scores_tc<<<dim3((n + 127) / 128, H, B), k1tc::kThreads, k1tc::kSmemBytes, stream>>>(
+            const dim3 g1((n + 127) / 128, H, B);
+            k1_scores_tc<kRowStats><<<g1, k1tc::kThreads, k1tc::kSmemBytes, stream>>>(
+                tq, tk, n, H, (float)scale, w->row_m, w->row_l, w->lse, w->colkey);
+            MCA_LAUNCH_CHECK("k1a_row_stats");
+            k1_scores_tc<kColMax><<<g1, k1tc::kThreads, k1tc::kSmemBytes, stream>>>(
                 tq, tk, n, H, (float)scale, w->row_m, w->row_l, w->lse, w->colkey);
         }
         MCA_LAUNCH_CHECK("k1_scores");
