@@ -192,7 +192,7 @@ __global__ void __launch_bounds__(1024) k2_scan(const unsigned int* __restrict__
     }
 }
 
-// Scatter token ids (b * n + j) into the per-head lists. Order inside a bin is
+// Scatter token ids ((b << 16) | j) into the per-head lists. Order inside a bin is
 // whatever the atomics give: it only changes which warp encodes a token, never
 // the token's result.
 __global__ void __launch_bounds__(256) k2_scatter(const int32_t* __restrict__ budgets,
@@ -204,7 +204,7 @@ __global__ void __launch_bounds__(256) k2_scatter(const int32_t* __restrict__ bu
     if (j >= n) return;
     const long t = bh * n + j;
     const int b = (int)(bh / heads), h = (int)(bh - (long)b * heads);
-    const int tok = b * n + j;
+    const int tok = (b << 16) | j;   // list entry: (b << 16) | j (n, B <= 65535, checked by the host)
     if (exact[t]) {
         const unsigned int pos = atomicAdd(&cursor[(size_t)h * (d + 1) + d], 1u);
         exact_list[(size_t)h * tokens + pos] = tok;

@@ -66,17 +66,50 @@ struct K3Args {
     int* task_cursor;          // [H]
 };
 
-size_t k3_smem_bytes(int d_in, size_t elem, size_t coef, bool wsmem) {
-    const size_t head = (((size_t)d_in * (8 + coef) + kGuide * 2) + 127) & ~(size_t)127;
-    return head + (wsmem ? (size_t)d_in * kDh * elem : 0);
+constexpr int kK3Warps = 16;                          // 512 threads: one CTA per SM holds W_h once
+constexpr int kK3BlockThreads = kK3Warps * 32;
+
+template <class Acc>
+struct alignas(sizeof(Acc) == 8 ? 16 : 8) SamplePair {  // one draw, broadcast to its octet through smem
+    uint32_t row;   // sampled W_h row
+    Acc coef;       // x[j, row] / (r p(row))
+};
+
+// 4 consecutive W_h elements starting at column `col` of row `row`, as floats.
+__device__ __forceinline__ void load4w(const float* base, size_t stride, uint32_t row, int col, float v[4]) {
+    const float4 q = *reinterpret_cast<const float4*>(base + (size_t)row * stride + col);
+    v[0] = q.x;
+    v[1] = q.y;
+    v[2] = q.z;
+    v[3] = q.w;
+}
+__device__ __forceinline__ void load4w(const __nv_bfloat16* base, size_t stride, uint32_t row, int col, float v[4]) {
+    const uint2 u = *reinterpret_cast<const uint2*>(base + (size_t)row * stride + col);
+    v[0] = __uint_as_float(u.x << 16);
+    v[1] = __uint_as_float(u.x & 0xFFFF0000u);
+    v[2] = __uint_as_float(u.y << 16);
+    v[3] = __uint_as_float(u.y & 0xFFFF0000u);
 }
 
-template <class T, class Acc, bool kWSmem>
-__global__ void __launch_bounds__(kK3Threads) k3_encode_sampled(K3Args a) {
+// Shared-memory footprint: sampler tables + the per-warp sample-pair buffers +
+// (optionally) W_h in the staging type WS.
+size_t k3_smem_bytes(int d_in, size_t coef, size_t ws_elem, bool wsmem) {
+    const size_t tables = (((size_t)d_in * (8 + coef) + kGuide * 2) + 127) & ~(size_t)127;
+    const size_t pairs = (size_t)kK3Warps * 4 * 16 * (coef == 8 ? 16 : 8);
+    return tables + pairs + (wsmem ? (size_t)d_in * kDh * ws_elem : 0);
+}
+
+// T: activation / output dtype; WS: W_h staging dtype in smem (fp32 when it
+// fits, so the hot loop does no unpacking); Acc: accumulation type.
+// Lane l of an octet owns output columns [4l, 4l+4) and [32+4l, 32+4l+4):
+// the octet's two 16-byte reads of a sampled row hit 32 distinct banks.
+template <class T, class WS, class Acc, bool kWSmem>
+__global__ void __launch_bounds__(kK3BlockThreads, 1) k3_encode_sampled(K3Args a) {
     using Coef = typename CoefT<T>::type;
+    using Pair = SamplePair<Acc>;
     extern __shared__ __align__(16) unsigned char smem[];
     const int h = blockIdx.y;
-    const int tid = threadIdx.x, lane = tid & 31;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int oct = lane >> 3, l8 = lane & 7;
     const unsigned omask = 0xFFu << (oct * 8);
     const int d_in = a.d_in, n = a.n, heads = a.heads;
@@ -84,28 +117,36 @@ __global__ void __launch_bounds__(kK3Threads) k3_encode_sampled(K3Args a) {
     uint64_t* s_thr = reinterpret_cast<uint64_t*>(smem);
     Coef* s_coef = reinterpret_cast<Coef*>(s_thr + d_in);
     uint16_t* s_guide = reinterpret_cast<uint16_t*>(s_coef + d_in);
-    T* s_w = reinterpret_cast<T*>(smem + ((((size_t)d_in * (8 + sizeof(Coef)) + kGuide * 2) + 127) & ~(size_t)127));
+    Pair* s_pairs =
+        reinterpret_cast<Pair*>(smem + ((((size_t)d_in * (8 + sizeof(Coef)) + kGuide * 2) + 127) & ~(size_t)127));
+    WS* s_w = reinterpret_cast<WS*>(s_pairs + kK3Warps * 4 * 16);
+    Pair* my_pairs = s_pairs + (warp * 4 + oct) * 16;
 
     const size_t HD = (size_t)heads * kDh;
     const T* wv = reinterpret_cast<const T*>(a.wv);
-    for (int i = tid; i < d_in; i += kK3Threads) {
+    for (int i = tid; i < d_in; i += kK3BlockThreads) {
         s_thr[i] = a.thr[(size_t)h * d_in + i];
         if constexpr (sizeof(Coef) == 8) s_coef[i] = (Coef)a.probs[(size_t)h * d_in + i];
         else s_coef[i] = (Coef)a.invp[(size_t)h * d_in + i];
     }
-    for (int g = tid; g < kGuide; g += kK3Threads) s_guide[g] = a.guide[(size_t)h * kGuide + g];
-    if constexpr (kWSmem) {
-        constexpr int kVec = 16 / sizeof(T);
-        const int vecs_per_row = kDh / kVec;
-        for (int e = tid; e < d_in * vecs_per_row; e += kK3Threads) {
-            const int i = e / vecs_per_row, v = e % vecs_per_row;
-            reinterpret_cast<uint4*>(s_w + (size_t)i * kDh)[v] =
-                reinterpret_cast<const uint4*>(wv + (size_t)i * HD + (size_t)h * kDh)[v];
+    for (int g = tid; g < kGuide; g += kK3BlockThreads) s_guide[g] = a.guide[(size_t)h * kGuide + g];
+    if constexpr (kWSmem) {   // W_h -> smem, converted to WS, 8 elements per thread-iteration
+        for (int e = tid; e < d_in * (kDh / 8); e += kK3BlockThreads) {
+            const int i = e / (kDh / 8), c8 = (e % (kDh / 8)) * 8;
+            float v[8];
+            load8(wv + (size_t)i * HD + (size_t)h * kDh + c8, v);
+            if constexpr (sizeof(WS) == 4) {
+                reinterpret_cast<float4*>(s_w + (size_t)i * kDh + c8)[0] = make_float4(v[0], v[1], v[2], v[3]);
+                reinterpret_cast<float4*>(s_w + (size_t)i * kDh + c8)[1] = make_float4(v[4], v[5], v[6], v[7]);
+            } else {
+                store8(reinterpret_cast<__nv_bfloat16*>(s_w) + (size_t)i * kDh + c8, v);
+            }
         }
     }
     __syncthreads();
-    const T* wsrc = kWSmem ? s_w : (wv + (size_t)h * kDh);
+    const WS* wsrc = kWSmem ? s_w : reinterpret_cast<const WS*>(wv + (size_t)h * kDh);
     const size_t wstride = kWSmem ? (size_t)kDh : HD;
+    const int col0 = 4 * l8, col1 = 32 + 4 * l8;
     const int nsamp = a.counts[2 * h];
     const int32_t* list = a.samp_list + (size_t)h * a.tokens;
     const T* x = reinterpret_cast<const T*>(a.x);
@@ -119,11 +160,12 @@ __global__ void __launch_bounds__(kK3Threads) k3_encode_sampled(K3Args a) {
         if (t0 >= nsamp) break;
         const int my = t0 + oct;
         if (my >= nsamp) continue;                       // octet-uniform
-        const int tok = list[my];
-        const int b = tok / n, j = tok - b * n;
+        const int bj = list[my];                         // (b << 16) | j
+        const int b = bj >> 16, j = bj & 0xFFFF;
+        const size_t tok = (size_t)b * n + j;
         const size_t tokh = ((size_t)b * heads + h) * n + j;
         const int r = a.budgets[tokh];
-        const T* xrow = x + (size_t)tok * d_in;
+        const T* xrow = x + tok * d_in;
         {   // pull the token's X row into L1 ahead of the random gathers
             const int lines = (int)((d_in * sizeof(T) + 127) / 128);
             for (int ln = l8; ln < lines; ln += 8)
@@ -133,24 +175,35 @@ __global__ void __launch_bounds__(kK3Threads) k3_encode_sampled(K3Args a) {
         const float inv_r = 1.0f / (float)r;
         const double rd = (double)r;
 
-        // round state: indices and raw X values of the two draws this lane owns
         auto gen = [&](int base, int& i0, int& i1, T& x0, T& x1) {
             uint64_t m0, m1;
             philox_pair53(a.seed, stream, a.layer, (uint32_t)(base / 2 + l8), &m0, &m1);
             const int k0 = base + 2 * l8;
-            i0 = k0 < r ? sample_index(s_thr, s_guide, m0) : 0;
-            i1 = k0 + 1 < r ? sample_index(s_thr, s_guide, m1) : 0;
+            // draws past r resolve to some valid row and are never accumulated
+            sample_index2(s_thr, s_guide, m0, m1, i0, i1);
             x0 = xrow[i0];
             x1 = xrow[i1];
         };
         auto coef = [&](int i, T xv) -> Acc {
-            if constexpr (sizeof(Coef) == 8) return (Acc)__ddiv_rn((double)to_f32(xv), __dmul_rn(rd, (double)s_coef[i]));
-            else return (Acc)(to_f32(xv) * (float)s_coef[i] * inv_r);
+            if constexpr (sizeof(Coef) == 8)
+                return (Acc)__ddiv_rn((double)to_f32(xv), __dmul_rn(rd, (double)s_coef[i]));
+            else
+                return (Acc)(to_f32(xv) * (float)s_coef[i] * inv_r);
         };
-
         Acc acc[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) acc[u] = (Acc)0;
+        auto accumulate = [&](const Pair& p) {
+            float w0[4], w1[4];
+            load4w(wsrc, wstride, p.row, col0, w0);
+            load4w(wsrc, wstride, p.row, col1, w1);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                acc[q] += p.coef * (Acc)w0[q];
+                acc[4 + q] += p.coef * (Acc)w1[q];
+            }
+        };
+
         int ni0, ni1;
         T nx0, nx1;
         gen(0, ni0, ni1, nx0, nx1);
@@ -158,30 +211,45 @@ __global__ void __launch_bounds__(kK3Threads) k3_encode_sampled(K3Args a) {
             const int i0 = ni0, i1 = ni1;
             const T x0 = nx0, x1 = nx1;
             if (base + 16 < r) gen(base + 16, ni0, ni1, nx0, nx1);   // next round's loads in flight
-            const Acc c0 = coef(i0, x0), c1 = coef(i1, x1);
+            Pair p0, p1;
+            p0.row = (uint32_t)i0;
+            p0.coef = coef(i0, x0);
+            p1.row = (uint32_t)i1;
+            p1.coef = coef(i1, x1);
             if (a.draws_out) {
                 const int k0 = base + 2 * l8;
                 if (k0 < r && k0 < a.draws_stride) a.draws_out[tokh * a.draws_stride + k0] = i0;
                 if (k0 + 1 < r && k0 + 1 < a.draws_stride) a.draws_out[tokh * a.draws_stride + k0 + 1] = i1;
             }
+            __syncwarp(omask);                     // previous round's pairs fully consumed
+            my_pairs[2 * l8] = p0;
+            my_pairs[2 * l8 + 1] = p1;
+            __syncwarp(omask);
             const int cnt = min(16, r - base);
-            for (int s = 0; s < cnt; ++s) {
-                const int src = s >> 1;
-                const int idx = __shfl_sync(omask, (s & 1) ? i1 : i0, src, 8);
-                const Acc cf = __shfl_sync(omask, (s & 1) ? c1 : c0, src, 8);
-                float wr[8];
-                load8(wsrc + (size_t)idx * wstride + 8 * l8, wr);
+            if (cnt == 16) {
 #pragma unroll
-                for (int q = 0; q < 8; ++q) acc[q] += cf * (Acc)wr[q];
+                for (int s2 = 0; s2 < 16; ++s2) accumulate(my_pairs[s2]);
+            } else {
+                for (int s2 = 0; s2 < cnt; ++s2) accumulate(my_pairs[s2]);
             }
             if (l8 == 0) my_samples += (unsigned long long)cnt;
         }
+        __syncwarp(omask);
         if (a.draws_out && l8 == 0)
             for (int k = r; k < a.draws_stride; ++k) a.draws_out[tokh * a.draws_stride + k] = -1;
-        float o[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) o[u] = (float)acc[u];
-        store8(hout + (size_t)tok * HD + (size_t)h * kDh + 8 * l8, o);
+        T* dst = hout + tok * HD + (size_t)h * kDh;
+        if constexpr (sizeof(T) == 2) {
+            uint2 u0, u1;
+            u0.x = mca_pack_bf16x2((float)acc[0], (float)acc[1]);
+            u0.y = mca_pack_bf16x2((float)acc[2], (float)acc[3]);
+            u1.x = mca_pack_bf16x2((float)acc[4], (float)acc[5]);
+            u1.y = mca_pack_bf16x2((float)acc[6], (float)acc[7]);
+            *reinterpret_cast<uint2*>(dst + col0) = u0;
+            *reinterpret_cast<uint2*>(dst + col1) = u1;
+        } else {
+            *reinterpret_cast<float4*>(dst + col0) = make_float4((float)acc[0], (float)acc[1], (float)acc[2], (float)acc[3]);
+            *reinterpret_cast<float4*>(dst + col1) = make_float4((float)acc[4], (float)acc[5], (float)acc[6], (float)acc[7]);
+        }
     }
     if (a.sample_counter) {
         for (int off = 16; off; off >>= 1) my_samples += __shfl_xor_sync(0xffffffffu, my_samples, off);
@@ -207,7 +275,10 @@ __global__ void __launch_bounds__(256) k3b_encode_exact(K3Args a) {
     const int32_t* list = a.exact_list + (size_t)h * a.tokens;
     for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
         __syncthreads();
-        if (tid < kTM) toks[tid] = (tile * kTM + tid < ne) ? list[tile * kTM + tid] : -1;
+        if (tid < kTM) {
+            const int bj = (tile * kTM + tid < ne) ? list[tile * kTM + tid] : -1;   // (b << 16) | j
+            toks[tid] = bj < 0 ? -1 : (bj >> 16) * a.n + (bj & 0xFFFF);
+        }
         __syncthreads();
         Acc acc[4][4];
 #pragma unroll
@@ -269,10 +340,11 @@ __global__ void __launch_bounds__(256) k3b_encode_exact(K3Args a) {
     }
 }
 
-template __global__ void k3_encode_sampled<float, double, true>(K3Args);
-template __global__ void k3_encode_sampled<float, double, false>(K3Args);
-template __global__ void k3_encode_sampled<__nv_bfloat16, float, true>(K3Args);
-template __global__ void k3_encode_sampled<__nv_bfloat16, float, false>(K3Args);
+template __global__ void k3_encode_sampled<float, float, double, true>(K3Args);
+template __global__ void k3_encode_sampled<float, float, double, false>(K3Args);
+template __global__ void k3_encode_sampled<__nv_bfloat16, float, float, true>(K3Args);
+template __global__ void k3_encode_sampled<__nv_bfloat16, __nv_bfloat16, float, true>(K3Args);
+template __global__ void k3_encode_sampled<__nv_bfloat16, __nv_bfloat16, float, false>(K3Args);
 template __global__ void k3b_encode_exact<float, double>(K3Args);
 template __global__ void k3b_encode_exact<__nv_bfloat16, float>(K3Args);
 

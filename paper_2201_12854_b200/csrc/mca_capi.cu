@@ -25,6 +25,7 @@
 #include "k1_scores_tc.cu"
 #include "k2_budgets.cu"
 #include "k3_encode.cu"
+#include "k3b_exact_tc.cu"
 #include "k4_apply_simt.cu"
 #include "k4_apply_tc.cu"
 
@@ -226,26 +227,49 @@ mca_status launch_k3(mca_weights* w, const void* x, int B, int n, long b_offset,
     a.exact_list = w->exact_list;
     a.counts = w->counts;
     a.task_cursor = w->task_cursor;
-    size_t smem = k3_smem_bytes(w->d_in, sizeof(T), sizeof(Coef), true);
-    const bool wsmem = smem <= 200 * 1024;
-    if (!wsmem) smem = k3_smem_bytes(w->d_in, sizeof(T), sizeof(Coef), false);
-    auto kern = wsmem ? k3_encode_sampled<T, Acc, true> : k3_encode_sampled<T, Acc, false>;
+    // W_h staged in smem as fp32 when it fits (no unpacking in the hot loop),
+    // else as bf16, else read from global memory (L1/L2).
+    void (*kern)(K3Args) = nullptr;
+    size_t smem = k3_smem_bytes(w->d_in, sizeof(Coef), 4, true);
+    constexpr size_t kMaxSmem = 220 * 1024;
+    if (smem <= kMaxSmem) {
+        kern = k3_encode_sampled<T, float, Acc, true>;
+    } else if (sizeof(T) == 2 && k3_smem_bytes(w->d_in, sizeof(Coef), 2, true) <= kMaxSmem) {
+        smem = k3_smem_bytes(w->d_in, sizeof(Coef), 2, true);
+        kern = k3_encode_sampled<__nv_bfloat16, __nv_bfloat16, float, true>;
+    } else {
+        smem = k3_smem_bytes(w->d_in, sizeof(Coef), sizeof(T), false);
+        if constexpr (sizeof(T) == 2) kern = k3_encode_sampled<__nv_bfloat16, __nv_bfloat16, float, false>;
+        else kern = k3_encode_sampled<float, float, double, false>;
+    }
     MCA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int occ = 0;
-    MCA_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kK3Threads, smem));
+    MCA_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kK3BlockThreads, smem));
     if (occ < 1) occ = 1;
     int G = (sm_count() * occ + w->heads - 1) / w->heads;
-    const long cap = (a.tokens + 31) / 32;   // at most one CTA per 32 tokens of a head
+    const long cap = (a.tokens + 63) / 64;   // at most one CTA per 64 tokens of a head
     if (G > cap) G = (int)cap;
     if (G < 1) G = 1;
-    kern<<<dim3(G, w->heads), kK3Threads, smem, stream>>>(a);
+    kern<<<dim3(G, w->heads), kK3BlockThreads, smem, stream>>>(a);
     MCA_LAUNCH_CHECK("k3_encode_sampled");
-    int Ge = (2 * sm_count() + w->heads - 1) / w->heads;
-    const long ecap = (a.tokens + 63) / 64;
-    if (Ge > ecap) Ge = (int)ecap;
-    if (Ge < 1) Ge = 1;
-    k3b_encode_exact<T, Acc><<<dim3(Ge, w->heads), 256, 0, stream>>>(a);
-    MCA_LAUNCH_CHECK("k3b_encode_exact");
+    if (sizeof(T) == 2 && !force_simt()) {   // bf16: exact token-heads on the tensor cores
+        static bool attr = false;
+        if (!attr) {
+            MCA_CUDA_TRY(cudaFuncSetAttribute(k3b_exact_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)k3btc::kSmemBytes));
+            attr = true;
+        }
+        k3b_exact_tc<<<dim3((unsigned)((a.tokens + 127) / 128), w->heads), k3btc::kThreads, k3btc::kSmemBytes,
+                       stream>>>(a);
+        MCA_LAUNCH_CHECK("k3b_exact_tc");
+    } else {                                  // fp32 parity path: fp64 CUDA-core GEMM
+        int Ge = (2 * sm_count() + w->heads - 1) / w->heads;
+        const long ecap = (a.tokens + 63) / 64;
+        if (Ge > ecap) Ge = (int)ecap;
+        if (Ge < 1) Ge = 1;
+        k3b_encode_exact<T, Acc><<<dim3(Ge, w->heads), 256, 0, stream>>>(a);
+        MCA_LAUNCH_CHECK("k3b_encode_exact");
+    }
     return MCA_OK;
 }
 
@@ -401,6 +425,8 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
     if (B < 0 || n <= 0) return fail(MCA_ERR_SHAPE, "B = %d, n = %d: need B >= 0, n >= 1", B, n);
     if (dt != w->wdt) return fail(MCA_ERR_CONFIG, "activation dtype %d != weight dtype %d", (int)dt, (int)w->wdt);
     if (b_offset < 0) return fail(MCA_ERR_SHAPE, "b_offset < 0");
+    if (n > 65535 || B > 65535)
+        return fail(MCA_ERR_UNSUPPORTED, "B = %d, n = %d: work lists pack (b, j) into 16 bits each", B, n);
     const bool approx = cfg->mode == MCA_MODE_APPROX;
     if (dbg && dbg->budgets_override && !dbg->exact_override)
         return fail(MCA_ERR_NULL, "budgets_override needs exact_override");

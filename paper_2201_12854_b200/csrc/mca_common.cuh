@@ -12,7 +12,7 @@
 namespace mca_dev {
 
 constexpr int kDh = 64;            // head dimension the kernels implement (BERT base/large)
-constexpr int kGuideBits = 10;     // guide table: 1024 buckets over the 53-bit uniform
+constexpr int kGuideBits = 12;     // guide table: 4096 buckets over the 53-bit uniform (~5 per row at d = 768)
 constexpr int kGuide = 1 << kGuideBits;
 
 // ----------------------------------------------------------------- Philox
@@ -58,6 +58,17 @@ __device__ __forceinline__ int sample_index(const uint64_t* __restrict__ thr, co
     while (thr[i] <= m) ++i;
     return i;
 }
+// Two draws resolved by one scan loop (one divergent loop instead of two).
+__device__ __forceinline__ void sample_index2(const uint64_t* __restrict__ thr, const uint16_t* __restrict__ guide,
+                                              uint64_t m0, uint64_t m1, int& i0, int& i1) {
+    i0 = guide[(uint32_t)(m0 >> (53 - kGuideBits))];
+    i1 = guide[(uint32_t)(m1 >> (53 - kGuideBits))];
+    bool a0 = thr[i0] <= m0, a1 = thr[i1] <= m1;
+    while (a0 || a1) {
+        if (a0) a0 = thr[++i0] <= m0;
+        if (a1) a1 = thr[++i1] <= m1;
+    }
+}
 
 // ------------------------------------------------ order-preserving float keys
 __device__ __forceinline__ uint32_t float_to_ordered(float f) {
@@ -82,6 +93,11 @@ template <>
 __device__ __forceinline__ float from_f32<float>(float v) { return v; }
 template <>
 __device__ __forceinline__ __nv_bfloat16 from_f32<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
+
+__device__ __forceinline__ uint32_t mca_pack_bf16x2(float lo, float hi) {
+    const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<const uint32_t*>(&v);
+}
 
 // Load 8 consecutive elements as floats (16 B for bf16, 32 B for f32).
 __device__ __forceinline__ void load8(const __nv_bfloat16* p, float v[8]) {
