@@ -66,7 +66,7 @@ struct K3Args {
     int* task_cursor;          // [H]
 };
 
-constexpr int kK3Warps = 16;                          // 512 threads: one CTA per SM holds W_h once
+constexpr int kK3Warps = 32;                          // 1024 threads: one CTA per SM holds W_h once
 constexpr int kK3BlockThreads = kK3Warps * 32;
 
 template <class Acc>
@@ -75,7 +75,8 @@ struct alignas(sizeof(Acc) == 8 ? 16 : 8) SamplePair {  // one draw, broadcast t
     Acc coef;       // x[j, row] / (r p(row))
 };
 
-// 4 consecutive W_h elements starting at column `col` of row `row`, as floats.
+// 4 consecutive W_h elements starting at column `col` of row `row`, as floats
+// (kept for the wide-row layouts; the hot loop reads 8 per lane via load8).
 __device__ __forceinline__ void load4w(const float* base, size_t stride, uint32_t row, int col, float v[4]) {
     const float4 q = *reinterpret_cast<const float4*>(base + (size_t)row * stride + col);
     v[0] = q.x;
@@ -101,8 +102,8 @@ size_t k3_smem_bytes(int d_in, size_t coef, size_t ws_elem, bool wsmem) {
 
 // T: activation / output dtype; WS: W_h staging dtype in smem (fp32 when it
 // fits, so the hot loop does no unpacking); Acc: accumulation type.
-// Lane l of an octet owns output columns [4l, 4l+4) and [32+4l, 32+4l+4):
-// the octet's two 16-byte reads of a sampled row hit 32 distinct banks.
+// Lane l of an octet owns output columns [8l, 8l+8): the octet reads a sampled
+// bf16 row as eight 16-byte pieces, one shared-memory wavefront per sample.
 template <class T, class WS, class Acc, bool kWSmem>
 __global__ void __launch_bounds__(kK3BlockThreads, 1) k3_encode_sampled(K3Args a) {
     using Coef = typename CoefT<T>::type;
@@ -146,39 +147,26 @@ __global__ void __launch_bounds__(kK3BlockThreads, 1) k3_encode_sampled(K3Args a
     __syncthreads();
     const WS* wsrc = kWSmem ? s_w : reinterpret_cast<const WS*>(wv + (size_t)h * kDh);
     const size_t wstride = kWSmem ? (size_t)kDh : HD;
-    const int col0 = 4 * l8, col1 = 32 + 4 * l8;
+    const int col0 = 8 * l8;   // lane owns columns [8l, 8l+8): one conflict-free 16-byte bf16 read per sample
     const int nsamp = a.counts[2 * h];
     const int32_t* list = a.samp_list + (size_t)h * a.tokens;
     const T* x = reinterpret_cast<const T*>(a.x);
     T* hout = reinterpret_cast<T*>(a.h_out);
     unsigned long long my_samples = 0;
 
-    for (;;) {
-        int t0 = 0;
-        if (lane == 0) t0 = atomicAdd(a.task_cursor + h, 4);
-        t0 = __shfl_sync(0xffffffffu, t0, 0);
-        if (t0 >= nsamp) break;
-        const int my = t0 + oct;
-        if (my >= nsamp) continue;                       // octet-uniform
-        const int bj = list[my];                         // (b << 16) | j
+    // Accumulators: fp32 path keeps 8 fp64 sums; the bf16 path packs 8 fp32 sums
+    // as 4 float2 so each W element pair costs one FFMA2 (sm_100 packed FMA).
+    auto process_token = [&](int bj, int r) {
         const int b = bj >> 16, j = bj & 0xFFFF;
         const size_t tok = (size_t)b * n + j;
         const size_t tokh = ((size_t)b * heads + h) * n + j;
-        const int r = a.budgets[tokh];
         const T* xrow = x + tok * d_in;
-        {   // pull the token's X row into L1 ahead of the random gathers
-            const int lines = (int)((d_in * sizeof(T) + 127) / 128);
-            for (int ln = l8; ln < lines; ln += 8)
-                asm volatile("prefetch.global.L1 [%0];" ::"l"(reinterpret_cast<const char*>(xrow) + ln * 128));
-        }
         const uint64_t stream = ((uint64_t)(a.b_offset + b) * heads + h) * (uint64_t)n + (uint64_t)j;
         const float inv_r = 1.0f / (float)r;
         const double rd = (double)r;
-
         auto gen = [&](int base, int& i0, int& i1, T& x0, T& x1) {
             uint64_t m0, m1;
             philox_pair53(a.seed, stream, a.layer, (uint32_t)(base / 2 + l8), &m0, &m1);
-            const int k0 = base + 2 * l8;
             // draws past r resolve to some valid row and are never accumulated
             sample_index2(s_thr, s_guide, m0, m1, i0, i1);
             x0 = xrow[i0];
@@ -191,19 +179,23 @@ __global__ void __launch_bounds__(kK3BlockThreads, 1) k3_encode_sampled(K3Args a
                 return (Acc)(to_f32(xv) * (float)s_coef[i] * inv_r);
         };
         Acc acc[8];
+        float2 acc2[4];
 #pragma unroll
         for (int u = 0; u < 8; ++u) acc[u] = (Acc)0;
-        auto accumulate = [&](const Pair& p) {
-            float w0[4], w1[4];
-            load4w(wsrc, wstride, p.row, col0, w0);
-            load4w(wsrc, wstride, p.row, col1, w1);
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                acc[q] += p.coef * (Acc)w0[q];
-                acc[4 + q] += p.coef * (Acc)w1[q];
+        for (int u = 0; u < 4; ++u) acc2[u] = make_float2(0.f, 0.f);
+        auto accumulate = [&](const Pair& p) {
+            float w[8];
+            load8(wsrc + (size_t)p.row * wstride + col0, w);
+            if constexpr (sizeof(Acc) == 4) {
+                const float2 cc = make_float2((float)p.coef, (float)p.coef);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) acc2[q] = __ffma2_rn(make_float2(w[2 * q], w[2 * q + 1]), cc, acc2[q]);
+            } else {
+#pragma unroll
+                for (int q = 0; q < 8; ++q) acc[q] += p.coef * (Acc)w[q];
             }
         };
-
         int ni0, ni1;
         T nx0, nx1;
         gen(0, ni0, ni1, nx0, nx1);
@@ -227,7 +219,7 @@ __global__ void __launch_bounds__(kK3BlockThreads, 1) k3_encode_sampled(K3Args a
             __syncwarp(omask);
             const int cnt = min(16, r - base);
             if (cnt == 16) {
-#pragma unroll
+#pragma unroll 4
                 for (int s2 = 0; s2 < 16; ++s2) accumulate(my_pairs[s2]);
             } else {
                 for (int s2 = 0; s2 < cnt; ++s2) accumulate(my_pairs[s2]);
@@ -237,19 +229,42 @@ __global__ void __launch_bounds__(kK3BlockThreads, 1) k3_encode_sampled(K3Args a
         __syncwarp(omask);
         if (a.draws_out && l8 == 0)
             for (int k = r; k < a.draws_stride; ++k) a.draws_out[tokh * a.draws_stride + k] = -1;
-        T* dst = hout + tok * HD + (size_t)h * kDh;
-        if constexpr (sizeof(T) == 2) {
-            uint2 u0, u1;
-            u0.x = mca_pack_bf16x2((float)acc[0], (float)acc[1]);
-            u0.y = mca_pack_bf16x2((float)acc[2], (float)acc[3]);
-            u1.x = mca_pack_bf16x2((float)acc[4], (float)acc[5]);
-            u1.y = mca_pack_bf16x2((float)acc[6], (float)acc[7]);
-            *reinterpret_cast<uint2*>(dst + col0) = u0;
-            *reinterpret_cast<uint2*>(dst + col1) = u1;
-        } else {
-            *reinterpret_cast<float4*>(dst + col0) = make_float4((float)acc[0], (float)acc[1], (float)acc[2], (float)acc[3]);
-            *reinterpret_cast<float4*>(dst + col1) = make_float4((float)acc[4], (float)acc[5], (float)acc[6], (float)acc[7]);
+        if constexpr (sizeof(Acc) == 4) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                acc[2 * u] = acc2[u].x;
+                acc[2 * u + 1] = acc2[u].y;
+            }
         }
+        float o[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) o[u] = (float)acc[u];
+        store8(hout + tok * HD + (size_t)h * kDh + col0, o);
+    };
+    auto prefetch_row = [&](int bj) {   // pull a token's X row into L1 ahead of the random gathers
+        const T* xrow = x + ((size_t)(bj >> 16) * n + (bj & 0xFFFF)) * d_in;
+        const int lines = (int)((d_in * sizeof(T) + 127) / 128);
+        for (int ln = l8; ln < lines; ln += 8)
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(reinterpret_cast<const char*>(xrow) + ln * 128));
+    };
+
+    // Warp tasks of 8 consecutive list entries: octet o encodes entries o and 4 + o.
+    // Both entries' list / budget loads and row prefetches are issued before the
+    // first is encoded, so the second token's start-up latency is hidden.
+    for (;;) {
+        int t0 = 0;
+        if (lane == 0) t0 = atomicAdd(a.task_cursor + h, 8);
+        t0 = __shfl_sync(0xffffffffu, t0, 0);
+        if (t0 >= nsamp) break;
+        const int ea = t0 + oct, eb = t0 + 4 + oct;
+        const int bja = ea < nsamp ? list[ea] : -1;
+        const int bjb = eb < nsamp ? list[eb] : -1;
+        const int ra = bja >= 0 ? a.budgets[((size_t)(bja >> 16) * heads + h) * n + (bja & 0xFFFF)] : 0;
+        const int rb = bjb >= 0 ? a.budgets[((size_t)(bjb >> 16) * heads + h) * n + (bjb & 0xFFFF)] : 0;
+        if (bja >= 0) prefetch_row(bja);
+        if (bjb >= 0) prefetch_row(bjb);
+        if (bja >= 0) process_token(bja, ra);      // octet-uniform conditions
+        if (bjb >= 0) process_token(bjb, rb);
     }
     if (a.sample_counter) {
         for (int off = 16; off; off >>= 1) my_samples += __shfl_xor_sync(0xffffffffu, my_samples, off);

@@ -229,14 +229,14 @@ mca_status launch_k3(mca_weights* w, const void* x, int B, int n, long b_offset,
     a.task_cursor = w->task_cursor;
     // W_h staged in smem as fp32 when it fits (no unpacking in the hot loop),
     // else as bf16, else read from global memory (L1/L2).
+    // bf16: W_h staged as bf16 (one 128-byte smem wavefront per sample; smem
+    // bandwidth, not issue, bounds this loop). fp32 parity path: fp32 W_h.
     void (*kern)(K3Args) = nullptr;
-    size_t smem = k3_smem_bytes(w->d_in, sizeof(Coef), 4, true);
+    size_t smem = k3_smem_bytes(w->d_in, sizeof(Coef), sizeof(T), true);
     constexpr size_t kMaxSmem = 220 * 1024;
     if (smem <= kMaxSmem) {
-        kern = k3_encode_sampled<T, float, Acc, true>;
-    } else if (sizeof(T) == 2 && k3_smem_bytes(w->d_in, sizeof(Coef), 2, true) <= kMaxSmem) {
-        smem = k3_smem_bytes(w->d_in, sizeof(Coef), 2, true);
-        kern = k3_encode_sampled<__nv_bfloat16, __nv_bfloat16, float, true>;
+        if constexpr (sizeof(T) == 2) kern = k3_encode_sampled<__nv_bfloat16, __nv_bfloat16, float, true>;
+        else kern = k3_encode_sampled<float, float, double, true>;
     } else {
         smem = k3_smem_bytes(w->d_in, sizeof(Coef), sizeof(T), false);
         if constexpr (sizeof(T) == 2) kern = k3_encode_sampled<__nv_bfloat16, __nv_bfloat16, float, false>;
