@@ -26,6 +26,7 @@
 #include "k2_budgets.cu"
 #include "k3_encode.cu"
 #include "k3b_exact_tc.cu"
+#include "k3d_encode_dense.cu"
 #include "k4_apply_simt.cu"
 #include "k4_apply_tc.cu"
 
@@ -98,6 +99,18 @@ bool make_tmap_bf16(CUtensorMap* m, const void* base, uint64_t inner, uint64_t r
     return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// MCA_K3_DENSE=1 selects the densified tensor-core encoder (k3d) for bf16;
+// the default is the gather-scale-accumulate encoder (measured faster at
+// BERT shapes).
+bool gather_only() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("MCA_K3_DENSE");
+        v = (e && e[0] == '1') ? 0 : 1;
+    }
+    return v == 1;
 }
 
 bool force_simt() {
@@ -229,8 +242,23 @@ mca_status launch_k3(mca_weights* w, const void* x, int B, int n, long b_offset,
     a.task_cursor = w->task_cursor;
     // W_h staged in smem as fp32 when it fits (no unpacking in the hot loop),
     // else as bf16, else read from global memory (L1/L2).
-    // bf16: W_h staged as bf16 (one 128-byte smem wavefront per sample; smem
-    // bandwidth, not issue, bounds this loop). fp32 parity path: fp32 W_h.
+    if (sizeof(T) == 2 && !force_simt() && !gather_only() && k3d::smem_bytes(w->d_in) <= 227 * 1024) {
+        // bf16: densified sampled encoding on the tensor cores (persistent, W_h resident)
+        CUtensorMap tw;
+        if (!make_tmap_bf16(&tw, w->w, (uint64_t)w->heads * kDh, w->d_in, 1, 64))
+            return fail(MCA_ERR_CUDA, "cuTensorMapEncodeTiled failed for w_v");
+        const uint32_t smem = k3d::smem_bytes(w->d_in);
+        MCA_CUDA_TRY(cudaFuncSetAttribute(k3d_encode_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int G = sm_count() / w->heads;
+        const long cap = (a.tokens + k3d::kBM - 1) / k3d::kBM;
+        if (G > cap) G = (int)cap;
+        if (G < 1) G = 1;
+        k3d_encode_dense<<<dim3(G, w->heads), k3d::kThreads, smem, stream>>>(a, tw);
+        MCA_LAUNCH_CHECK("k3d_encode_dense");
+    } else {
+    // Gather-scale-accumulate: W_h staged as bf16 (one 128-byte smem wavefront
+    // per sample; smem bandwidth, not issue, bounds this loop) / fp32 for the
+    // fp32 parity path.
     void (*kern)(K3Args) = nullptr;
     size_t smem = k3_smem_bytes(w->d_in, sizeof(Coef), sizeof(T), true);
     constexpr size_t kMaxSmem = 220 * 1024;
@@ -252,6 +280,7 @@ mca_status launch_k3(mca_weights* w, const void* x, int B, int n, long b_offset,
     if (G < 1) G = 1;
     kern<<<dim3(G, w->heads), kK3BlockThreads, smem, stream>>>(a);
     MCA_LAUNCH_CHECK("k3_encode_sampled");
+    }
     if (sizeof(T) == 2 && !force_simt()) {   // bf16: exact token-heads on the tensor cores
         static bool attr = false;
         if (!attr) {
