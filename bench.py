@@ -45,7 +45,7 @@ CONFIGS = {
     # name: (B per GPU, n, d_in, heads, description)
     "c1": (1, 128, 768, 12, "BERT-base MCA attention layer, B=1, n=128 (configs[0])"),
     "c2": (64, 512, 768, 12, "BERT-base MCA attention layer, B=64, n=512, 1 B200 per 64 sequences (configs[1])"),
-    "c3": (128, 512, 1024, 16, "BERT-large MCA attention layer, B=128, n=512 (configs[2], one layer)"),
+    "c3": (128, 512, 1024, 16, "BERT-large 24-layer MCA attention stack, B=128, n=512 (configs[2])"),
     "c4": (16, 4096, 768, 12, "long-sequence BERT-base MCA layer, B=16, n=4096 (configs[3])"),
 }
 
@@ -177,28 +177,44 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
 
-    w = synthetic.make_weights(d_in, H).to(dtype)
+    L = args.layers
+    # per-layer W_V (seeded by layer); Q/K are the caller's projections (out of the
+    # path): one synthetic set shared by the layers; layer l uses
+    # Philox counter word `layer = l`, and X_{l+1} = Y_l chains the stack.
+    wl = [synthetic.make_weights(d_in, H, seed=1234 + l).to(dtype) for l in range(L)]
+    w = wl[0]
     inp = synthetic.make_inputs(B, n, d_in, H, seed=1234 + rank)  # rank's own shard of the global batch
-    weights = mca.AttentionWeights(w.to(dev), heads=H)
+    layer_weights = [mca.AttentionWeights(t.to(dev), heads=H) for t in wl]
+    weights = layer_weights[0]
     q, k, x = (t.to(dtype).to(dev) for t in (inp.q, inp.k, inp.x))
     y = torch.empty_like(q)
+    ybuf = [torch.empty_like(q), torch.empty_like(q)]
     cfg = mca.McaConfig(alpha=args.alpha)
     b_offset = rank * B
-    weights.reserve(B * n)
+    for lw in layer_weights:
+        lw.reserve(B * n)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
     stream = torch.cuda.current_stream()
 
     def step():
-        mca.mca_forward(weights, q, k, x, cfg, seed=42, b_offset=b_offset, y=y)
+        if L == 1:
+            mca.mca_forward(weights, q, k, x, cfg, seed=42, b_offset=b_offset, y=y)
+            return
+        xin = x
+        for l in range(L):
+            out_buf = ybuf[l & 1]
+            mca.mca_forward(layer_weights[l], q, k, xin, cfg, seed=42, b_offset=b_offset, layer=l, y=out_buf)
+            xin = out_buf
 
     out = mca.mca_forward(weights, q, k, x, cfg, seed=42, b_offset=b_offset, y=y, flops=True, return_plan=True)
     flops_report = out.flops
-    launches_per_step = weights.last_launch_count()
+    launches_per_step = weights.last_launch_count() * L
 
     sampler = ClockSampler(local_rank) if rank == 0 else None
     if sampler:
         sampler.start()
-    weights.set_timing(True)
+    for lw in layer_weights:
+        lw.set_timing(True)
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -213,18 +229,20 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         starts[i].record(stream)
         step()
         ends[i].record(stream)
-        st = weights.last_stage_ms()                    # events on the forward's own stream
-        for s in range(len(st)):
-            stage_tot[s] += st[s]
+        for lw in layer_weights:
+            st = lw.last_stage_ms()                     # events on the forward's own stream
+            for s in range(len(st)):
+                stage_tot[s] += st[s]
     torch.cuda.synchronize()
     total_ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
     if dist:
         t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
-    weights.set_timing(False)
+    for lw in layer_weights:
+        lw.set_timing(False)
     ms_per_step = total_ms / args.steps
-    value = world * B * n / (ms_per_step / 1e3)
+    value = world * B * n * L / (ms_per_step / 1e3)   # token-layers per second (= tokens/s for one layer)
 
     # e2e: host buffers through the C ABI (pinned H2D + forward + D2H), same stream
     hq, hk, hx = (t.to(dtype).pin_memory() for t in (inp.q, inp.k, inp.x))
@@ -235,8 +253,12 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         dq.copy_(hq, non_blocking=True)
         dk.copy_(hk, non_blocking=True)
         dx.copy_(hx, non_blocking=True)
-        mca.mca_forward(weights, dq, dk, dx, cfg, seed=42, b_offset=b_offset, y=y)
-        hy.copy_(y, non_blocking=True)
+        xin = dx
+        for l in range(L):
+            out_buf = ybuf[l & 1] if L > 1 else y
+            mca.mca_forward(layer_weights[l], dq, dk, xin, cfg, seed=42, b_offset=b_offset, layer=l, y=out_buf)
+            xin = out_buf
+        hy.copy_(xin, non_blocking=True)
 
     for _ in range(max(1, args.warmup)):
         e2e_step()
@@ -271,7 +293,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         return
 
     peaks = _peaks()
-    work = algorithmic_work(B, n, d_in, H, elem)
+    work = {k: (v[0], v[1] * L) for k, v in algorithmic_work(B, n, d_in, H, elem).items()}   # per step (L layers)
     names = ["score", "budgets", "encode", "apply"]
     stage_ms = {names[i]: stage_tot[i] / args.steps for i in range(4)}
     dom = max(names, key=lambda s: stage_ms[s])
@@ -294,22 +316,22 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             traffic = None
     roof["traffic"] = traffic
     enc_gbs = work["encode"][1] / (stage_ms["encode"] / 1e3) / 1e9
-    gather_gbs = flops_report.samples * 64 * elem / (stage_ms["encode"] / 1e3) / 1e9
+    gather_gbs = L * flops_report.samples * 64 * elem / (stage_ms["encode"] / 1e3) / 1e9   # layer 0's sample count x L
 
     cpu = None
     if not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
         rate, sample, _ = cpu_reference_rate(args.config, args.alpha, args.cpu_seconds, threads)
-        cpu = {"value": rate, "unit": "tokens/s", "cores": threads, "kind": "port", "sample": sample}
+        cpu = {"value": rate, "unit": "tokens/s (one layer)", "cores": threads, "kind": "port", "sample": sample}
 
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
-        "config": {"workload": desc, "global_batch": world * B, "B_per_gpu": B, "seq_len": n, "d_in": d_in,
+        "config": {"workload": desc, "layers": L, "global_batch": world * B, "B_per_gpu": B, "seq_len": n, "d_in": d_in,
                    "heads": H, "d_h": 64, "alpha": args.alpha, "seed": 42, "parallelism": f"dp{world} (batch shards)",
                    "l2": "flushed (256 MB write) before every timed step"},
-        "e2e": {"value": world * B * n / (e2e_ms / 1e3), "unit": "tokens/s",
+        "e2e": {"value": world * B * n * L / (e2e_ms / 1e3), "unit": "tokens/s",
                 "h2d_bytes_per_step": int(3 * q.numel() * elem), "d2h_bytes_per_step": int(y.numel() * elem)},
         "roofline": roof,
         "stages_ms": stage_ms,
@@ -336,10 +358,17 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--alpha", type=float, default=0.4)
     ap.add_argument("--dtype", default="bf16", choices=["bf16", "f32"])
+    ap.add_argument("--layers", type=int, default=0, help="layers per step (default: 24 for c3, else 1)")
+    ap.add_argument("--batch", type=int, default=0, help="override B per GPU")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.layers <= 0:
+        args.layers = 24 if args.config == "c3" else 1
+    if args.batch > 0:
+        B, n, d_in, H, desc = CONFIGS[args.config]
+        CONFIGS[args.config] = (args.batch, n, d_in, H, desc + f" [B overridden to {args.batch}]")
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))

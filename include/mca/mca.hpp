@@ -1,0 +1,221 @@
+// mca/mca.hpp — C++ host interface of the B200 MCA forward, header-only,
+// layered on the C ABI (mca/mca_cuda.h). It mirrors the reference's
+// operator interface for the path (SPEC.md:255-424 over matrix.hpp's Matrix)
+// so C++ callers of the reference can switch:
+//
+//   reference (SPEC op)                          here
+//   AttentionWeights{w, cached_dist}  :260-265   mca::b200::AttentionWeights (W_V on device + K0 tables)
+//   McaConfig{alpha, mode, min_samples, heads}   mca::b200::McaConfig
+//   multihead_forward(x, heads, cfg, seed)       mca::b200::multihead_forward(q, k, x, w, cfg, seed)
+//   mca_forward / regular_forward                same, cfg.mode approximation / regular
+//   sample_budgets(attn, cfg, d)                 mca::b200::sample_budgets(cmax, n, d, cfg) (device)
+//   FlopsReport                       :376-381   mca::b200::FlopsReport
+//
+// Errors follow matrix.hpp:33,52 and the SPEC error classes: shape errors
+// throw std::invalid_argument, domain errors std::domain_error, degenerate /
+// configuration / CUDA errors std::runtime_error. Every call reaches the GPU;
+// there is no host fallback.
+//
+// Two levels: device-pointer calls (zero copies; any cudaStream_t) and
+// Matrix-level calls for one sequence (fp64 host Matrix in, converted to the
+// fp32 parity-precision path, result copied back).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "mca/matrix.hpp"
+#include "mca/mca_cuda.h"
+
+namespace mca {
+namespace b200 {
+
+enum class Mode { regular = MCA_MODE_REGULAR, approximation = MCA_MODE_APPROX };
+
+struct McaConfig {
+    double alpha = 0.4;
+    Mode mode = Mode::approximation;
+    int min_samples = 1;
+    double scale = 0.0;  // <= 0: 1/sqrt(d_h)
+    mca_config c() const { return mca_config{alpha, scale, min_samples, static_cast<int32_t>(mode)}; }
+};
+
+struct FlopsReport {
+    uint64_t exact_encoding = 0, approx_encoding = 0, aggregation = 0, samples = 0, exact_tokens = 0;
+    double reduction_factor = 1.0, total_reduction = 1.0;
+};
+
+inline void check(mca_status s) {
+    if (s == MCA_OK) return;
+    const std::string msg = std::string("mca: ") + mca_last_error();
+    switch (s) {
+        case MCA_ERR_SHAPE: throw std::invalid_argument(msg);
+        case MCA_ERR_DOMAIN: throw std::domain_error(msg);
+        default: throw std::runtime_error(msg);
+    }
+}
+
+inline void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw std::runtime_error(std::string("mca: ") + what + ": " + cudaGetErrorString(e));
+}
+
+// W_V [d_in, heads*64] on the device plus its cached sampling tables.
+class AttentionWeights {
+   public:
+    // From a device buffer in `dtype` (row-major [d_in, heads*64]).
+    AttentionWeights(const void* w_v_device, mca_dtype dtype, int d_in, int heads, cudaStream_t stream = nullptr)
+        : dtype_(dtype), d_in_(d_in), heads_(heads) {
+        check(mca_prepare_weights(w_v_device, dtype, d_in, heads, 64, stream, &h_));
+    }
+    // From a host fp64 Matrix (d_in x heads*64): uploaded as fp32 (parity precision).
+    AttentionWeights(const Matrix& w_v, int heads, cudaStream_t stream = nullptr)
+        : dtype_(MCA_F32), d_in_(static_cast<int>(w_v.rows)), heads_(heads) {
+        if (heads <= 0 || w_v.cols != static_cast<std::size_t>(heads) * 64)
+            throw std::invalid_argument("mca: w_v must be d_in x heads*64");
+        std::vector<float> f(w_v.data.begin(), w_v.data.end());
+        void* d = nullptr;
+        cuda_check(cudaMalloc(&d, f.size() * sizeof(float)), "cudaMalloc");
+        cudaError_t e = cudaMemcpy(d, f.data(), f.size() * sizeof(float), cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) {
+            cudaFree(d);
+            cuda_check(e, "cudaMemcpy");
+        }
+        const mca_status s = mca_prepare_weights(d, MCA_F32, d_in_, heads, 64, stream, &h_);
+        cudaFree(d);  // the handle keeps its own copy
+        check(s);
+    }
+    AttentionWeights(const AttentionWeights&) = delete;
+    AttentionWeights& operator=(const AttentionWeights&) = delete;
+    AttentionWeights(AttentionWeights&& o) noexcept : h_(o.h_), dtype_(o.dtype_), d_in_(o.d_in_), heads_(o.heads_) {
+        o.h_ = nullptr;
+    }
+    ~AttentionWeights() { mca_weights_free(h_); }
+
+    mca_weights* handle() const { return h_; }
+    mca_dtype dtype() const { return dtype_; }
+    int d_in() const { return d_in_; }
+    int heads() const { return heads_; }
+
+    // Per-head p(i) and cdf, [heads * d_in] each (SamplingDistribution).
+    void distributions(std::vector<double>& probs, std::vector<double>& cdf) const {
+        probs.resize(static_cast<std::size_t>(heads_) * d_in_);
+        cdf.resize(probs.size());
+        check(mca_weights_export(h_, probs.data(), cdf.data()));
+    }
+
+   private:
+    mca_weights* h_ = nullptr;
+    mca_dtype dtype_;
+    int d_in_, heads_;
+};
+
+// ---------------------------------------------------------------- device level
+// q, k, y: [B, n, heads*64]; x: [B, n, d_in] device buffers in w.dtype().
+inline FlopsReport forward_device(const AttentionWeights& w, const void* q, const void* k, const void* x, int B, int n,
+                                  const McaConfig& cfg, uint64_t seed, void* y, int32_t* budgets = nullptr,
+                                  uint8_t* exact = nullptr, bool want_flops = false, long b_offset = 0,
+                                  uint32_t layer = 0, cudaStream_t stream = nullptr) {
+    const mca_config c = cfg.c();
+    mca_flops f{};
+    check(mca_forward(w.handle(), q, k, x, w.dtype(), B, n, b_offset, layer, &c, seed, y, budgets, exact,
+                      want_flops ? &f : nullptr, stream));
+    FlopsReport r;
+    if (want_flops) {
+        r.exact_encoding = f.exact_encoding;
+        r.approx_encoding = f.approx_encoding;
+        r.aggregation = f.aggregation;
+        r.samples = f.samples;
+        r.exact_tokens = f.exact_tokens;
+        r.reduction_factor = f.reduction_factor;
+        r.total_reduction = f.total_reduction;
+    }
+    return r;
+}
+
+// ---------------------------------------------------------------- Matrix level
+struct AttentionOutput {   // SPEC.md:280-283 (attn is never materialised on the device)
+    Matrix y;                        // n x heads*64
+    std::vector<int32_t> budgets;    // [heads, n]
+    std::vector<uint8_t> exact_mask; // [heads, n]
+    FlopsReport flops;
+};
+
+namespace detail {
+struct DeviceBuf {
+    void* p = nullptr;
+    explicit DeviceBuf(std::size_t bytes) { cuda_check(cudaMalloc(&p, bytes ? bytes : 1), "cudaMalloc"); }
+    ~DeviceBuf() { cudaFree(p); }
+    DeviceBuf(const DeviceBuf&) = delete;
+    DeviceBuf& operator=(const DeviceBuf&) = delete;
+};
+inline void upload_f32(const Matrix& m, DeviceBuf& d) {
+    std::vector<float> f(m.data.begin(), m.data.end());
+    cuda_check(cudaMemcpy(d.p, f.data(), f.size() * sizeof(float), cudaMemcpyHostToDevice), "cudaMemcpy H2D");
+}
+}  // namespace detail
+
+// multihead_forward for one sequence with the projections
+// given: q, k: n x heads*64, x: n x d_in. Weights must be fp32 (Matrix ctor).
+inline AttentionOutput multihead_forward(const Matrix& q, const Matrix& k, const Matrix& x, const AttentionWeights& w,
+                                         const McaConfig& cfg, uint64_t seed) {
+    const std::size_t H = static_cast<std::size_t>(w.heads()), n = q.rows;
+    if (w.dtype() != MCA_F32) throw std::invalid_argument("mca: Matrix-level forward needs fp32 weights");
+    if (q.cols != H * 64 || k.rows != n || k.cols != H * 64)
+        throw std::invalid_argument("mca: q, k must be n x heads*64");
+    if (x.rows != n || x.cols != static_cast<std::size_t>(w.d_in()))
+        throw std::invalid_argument("mca: x must be n x d_in");
+    detail::DeviceBuf dq(q.data.size() * 4), dk(k.data.size() * 4), dx(x.data.size() * 4), dy(q.data.size() * 4),
+        db(H * n * 4), de(H * n);
+    detail::upload_f32(q, dq);
+    detail::upload_f32(k, dk);
+    detail::upload_f32(x, dx);
+    AttentionOutput out;
+    out.flops = forward_device(w, dq.p, dk.p, dx.p, 1, static_cast<int>(n), cfg, seed, dy.p,
+                               static_cast<int32_t*>(db.p), static_cast<uint8_t*>(de.p), true);
+    std::vector<float> y(q.data.size());
+    cuda_check(cudaMemcpy(y.data(), dy.p, y.size() * 4, cudaMemcpyDeviceToHost), "cudaMemcpy D2H");
+    out.y.rows = n;
+    out.y.cols = H * 64;
+    out.y.data.assign(y.begin(), y.end());
+    out.budgets.resize(H * n);
+    out.exact_mask.resize(H * n);
+    cuda_check(cudaMemcpy(out.budgets.data(), db.p, H * n * 4, cudaMemcpyDeviceToHost), "cudaMemcpy D2H");
+    cuda_check(cudaMemcpy(out.exact_mask.data(), de.p, H * n, cudaMemcpyDeviceToHost), "cudaMemcpy D2H");
+    return out;
+}
+
+// mca_forward: the single-sequence forward in approximation mode.
+inline AttentionOutput mca_forward(const Matrix& q, const Matrix& k, const Matrix& x, const AttentionWeights& w,
+                                   const McaConfig& cfg, uint64_t seed) {
+    if (cfg.mode != Mode::approximation) throw std::runtime_error("mca: mca_forward requires approximation mode");
+    return multihead_forward(q, k, x, w, cfg, seed);
+}
+
+// regular_forward: the exact layer.
+inline AttentionOutput regular_forward(const Matrix& q, const Matrix& k, const Matrix& x, const AttentionWeights& w) {
+    McaConfig cfg;
+    cfg.mode = Mode::regular;
+    return multihead_forward(q, k, x, w, cfg, 0);
+}
+
+// sample_budgets on column maxima (host vector in, host out).
+inline void sample_budgets(const std::vector<double>& cmax, int n, int d, const McaConfig& cfg,
+                           std::vector<int32_t>& budgets, std::vector<uint8_t>& exact) {
+    const std::size_t m = cmax.size();
+    detail::DeviceBuf dc(m * 8), db(m * 4), de(m);
+    cuda_check(cudaMemcpy(dc.p, cmax.data(), m * 8, cudaMemcpyHostToDevice), "cudaMemcpy H2D");
+    const mca_config c = cfg.c();
+    check(mca_stage_budgets(static_cast<const double*>(dc.p), static_cast<long>(m), n, d, &c,
+                            static_cast<int32_t*>(db.p), static_cast<uint8_t*>(de.p), nullptr));
+    budgets.resize(m);
+    exact.resize(m);
+    cuda_check(cudaMemcpy(budgets.data(), db.p, m * 4, cudaMemcpyDeviceToHost), "cudaMemcpy D2H");
+    cuda_check(cudaMemcpy(exact.data(), de.p, m, cudaMemcpyDeviceToHost), "cudaMemcpy D2H");
+}
+
+}  // namespace b200
+}  // namespace mca

@@ -274,7 +274,7 @@ mca_status launch_k3(mca_weights* w, const void* x, int B, int n, long b_offset,
     int occ = 0;
     MCA_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kK3BlockThreads, smem));
     if (occ < 1) occ = 1;
-    int G = (sm_count() * occ + w->heads - 1) / w->heads;
+    int G = sm_count() * occ / w->heads;     // all CTAs resident: no second wave
     const long cap = (a.tokens + 63) / 64;   // at most one CTA per 64 tokens of a head
     if (G > cap) G = (int)cap;
     if (G < 1) G = 1;

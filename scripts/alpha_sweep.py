@@ -1,0 +1,78 @@
+"""Error-bound sweep (BASELINE.json configs[4]): for each alpha, MCA throughput,
+FLOP cut, and the measured error against the exact layer next to Theorem 1's
+bound alpha * beta * ||W_h||_F.
+
+  python scripts/alpha_sweep.py [--batch 64] [--n 512] [--seeds 8] [--out profiles/alpha_sweep.jsonl]
+
+Error statistics per alpha: mean over seeds, rows and heads of
+||Y~_h[i] - Y_h[i]|| / (alpha beta ||W_h||_F) (Theorem 1 says the mean is <= 1),
+and the relative Frobenius error of the whole output.
+"""
+import argparse
+import json
+import os
+import sys
+
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import paper_2201_12854_b200 as mca  # noqa: E402
+from paper_2201_12854_b200 import synthetic  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--batch", type=int, default=64)
+    ap.add_argument("--n", type=int, default=512)
+    ap.add_argument("--d", type=int, default=768)
+    ap.add_argument("--heads", type=int, default=12)
+    ap.add_argument("--seeds", type=int, default=8)
+    ap.add_argument("--alphas", default="0.05,0.1,0.2,0.4,0.6,1.0")
+    ap.add_argument("--out", default="")
+    args = ap.parse_args()
+    B, n, d, H = args.batch, args.n, args.d, args.heads
+    w = synthetic.make_weights(d, H).bfloat16()
+    inp = synthetic.make_inputs(B, n, d, H)
+    q, k, x = (t.bfloat16().cuda() for t in (inp.q, inp.k, inp.x))
+    weights = mca.AttentionWeights(w.cuda(), heads=H)
+    y_exact = mca.regular_forward(weights, q, k, x).float()
+    beta = x.float().norm(dim=2).mean(dim=1)                             # [B]: mean row norm per sequence
+    wnorm = w.float().view(d, H, 64).norm(dim=(0, 2)).cuda()             # [H]
+    lines = []
+    for alpha in [float(a) for a in args.alphas.split(",")]:
+        cfg = mca.McaConfig(alpha=alpha)
+        out = mca.mca_forward(weights, q, k, x, cfg, seed=1, flops=True)
+        for _ in range(3):
+            mca.mca_forward(weights, q, k, x, cfg, seed=1, y=out.y)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for s in range(10):
+            mca.mca_forward(weights, q, k, x, cfg, seed=100 + s, y=out.y)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / 10
+        ratios, rels = [], []
+        for s in range(args.seeds):
+            y = mca.mca_forward(weights, q, k, x, cfg, seed=1000 + s).y.float()
+            err = (y - y_exact).view(B, n, H, 64).norm(dim=3)                # [B, n, H]
+            bound = alpha * beta.view(B, 1, 1) * wnorm.view(1, 1, H)
+            ratios.append((err / bound).mean().item())
+            rels.append(((y - y_exact).norm() / y_exact.norm()).item())
+        rec = {"alpha": alpha, "B": B, "n": n, "d": d, "heads": H, "ms_per_layer": ms,
+               "tokens_per_s": B * n / (ms / 1e3), "reduction_factor": out.flops.reduction_factor,
+               "total_reduction": out.flops.total_reduction, "samples": out.flops.samples,
+               "exact_token_heads": out.flops.exact_tokens,
+               "mean_err_over_theorem1_bound": sum(ratios) / len(ratios),
+               "rel_frobenius_err": sum(rels) / len(rels), "seeds": args.seeds}
+        print(json.dumps(rec), flush=True)
+        lines.append(rec)
+    if args.out:
+        with open(args.out, "w") as f:
+            for r in lines:
+                f.write(json.dumps(r) + "\n")
+
+
+if __name__ == "__main__":
+    main()

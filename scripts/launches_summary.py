@@ -13,12 +13,14 @@ for r in rows[hdr + 1:]:
     if len(r) > vi:
         v = float(r[vi].replace(",", ""))
         unit = r[ui]
-        us = {"nsecond": v / 1e3, "usecond": v, "msecond": v * 1e3, "second": v * 1e6}.get(unit, v)
+        us = {"nsecond": v / 1e3, "ns": v / 1e3, "usecond": v, "us": v, "msecond": v * 1e3, "ms": v * 1e3,
+              "second": v * 1e6, "s": v * 1e6}.get(unit, v)
         name = r[ki].split("(")[0].replace("void ", "")[:48]
         d.setdefault(name, []).append(us)
-tot = sum(sum(v) / len(v) for k, v in d.items() if k.startswith("mca_dev"))
+per_forward = lambda k: k.startswith("mca_dev") and "k0_" not in k   # K0 is one-time weight preparation
+tot = sum(sum(v) / len(v) for k, v in d.items() if per_forward(k))
 print(f"{'kernel':50s} {'launches':>8s} {'mean_us':>9s} {'share':>6s}")
 for k, v in d.items():
     m = sum(v) / len(v)
-    share = m / tot if k.startswith("mca_dev") else 0
+    share = m / tot if per_forward(k) else 0
     print(f"{k:50s} {len(v):8d} {m:9.1f} {share:6.1%}")

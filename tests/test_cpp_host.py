@@ -1,0 +1,75 @@
+"""The C++ host mirror (include/mca/mca.hpp) as a reference C++ caller would
+use it: Matrix in, SPEC-named calls, matrix.hpp's exception types out.
+CPU: it compiles and links against libmca_b200.so. GPU: its results match the
+fp64 oracle (budgets bitwise, y within the fp32 tolerance)."""
+import os
+import struct
+import subprocess
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SRC = os.path.join(ROOT, "tests", "cpp", "host_api_demo.cpp")
+LIBDIR = os.path.join(ROOT, "paper_2201_12854_b200", "lib")
+
+
+def _build(out_dir):
+    from paper_2201_12854_b200 import _lib
+    if not os.path.exists(_lib.LIB_PATH):
+        _lib.build()
+    exe = os.path.join(out_dir, "host_api_demo")
+    subprocess.run(["/usr/bin/g++", "-std=c++17", "-O2", f"-I{ROOT}/include", "-I/usr/local/cuda/include", SRC,
+                    f"-L{LIBDIR}", "-lmca_b200", "-L/usr/local/cuda/lib64", "-lcudart", f"-Wl,-rpath,{LIBDIR}",
+                    "-Wl,-rpath,/usr/local/cuda/lib64", "-o", exe], check=True)
+    return exe
+
+
+def test_cpp_host_api_compiles(tmp_path):
+    assert os.path.exists(_build(str(tmp_path)))
+
+
+def _write_matrix(f, m):
+    m = np.ascontiguousarray(m, dtype=np.float64)
+    f.write(struct.pack("<qq", *m.shape))
+    f.write(m.tobytes())
+
+
+@pytest.mark.gpu
+def test_cpp_host_api_matches_oracle(tmp_path, orc):
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2201_12854_b200 import synthetic
+    exe = _build(str(tmp_path))
+    H, n, d = 12, 96, 768
+    w = synthetic.make_weights(d, H).double().numpy()
+    inp = synthetic.make_inputs(1, n, d, H)
+    q, k, x = (t[0].double().numpy() for t in (inp.q, inp.k, inp.x))
+    # the C++ path computes in fp32: give the oracle the same rounded inputs
+    q, k, x, w = (a.astype(np.float32).astype(np.float64) for a in (q, k, x, w))
+    inf, outf = tmp_path / "in.bin", tmp_path / "out.bin"
+    with open(inf, "wb") as f:
+        f.write(struct.pack("<qqd", H, 42, 0.4))
+        for m in (q, k, x, w):
+            _write_matrix(f, m)
+    subprocess.run([exe, str(inf), str(outf)], check=True)
+    raw = open(outf, "rb").read()
+    ny = n * H * 64
+    y = np.frombuffer(raw[: ny * 8], dtype=np.float64).reshape(n, H * 64)
+    ye = np.frombuffer(raw[ny * 8: 2 * ny * 8], dtype=np.float64).reshape(n, H * 64)
+    off = 2 * ny * 8
+    b = np.frombuffer(raw[off: off + H * n * 4], dtype=np.int32).reshape(H, n)
+    off += H * n * 4
+    e = np.frombuffer(raw[off: off + H * n], dtype=np.uint8).reshape(H, n)
+    off += H * n
+    rf, samples, errs = struct.unpack("<ddd", raw[off: off + 24])
+    ref = orc.batched_forward(q[None], k[None], x[None], w, heads=H, alpha=0.4, seed=42)
+    assert np.array_equal(b, ref.budgets[0]) and np.array_equal(e.astype(bool), ref.exact[0])
+    rel = np.linalg.norm(y - ref.y[0], axis=1) / np.linalg.norm(ref.y[0], axis=1)
+    assert rel.max() <= 1e-5
+    refe = orc.batched_forward(q[None], k[None], x[None], w, heads=H, mode="regular")
+    rel = np.linalg.norm(ye - refe.y[0], axis=1) / np.linalg.norm(refe.y[0], axis=1)
+    assert rel.max() <= 1e-5
+    assert rf == pytest.approx(ref.flops.reduction_factor)
+    assert int(errs) == 3          # std::domain_error for alpha = 0, std::invalid_argument for a bad shape
