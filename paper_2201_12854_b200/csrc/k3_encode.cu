@@ -70,10 +70,12 @@ constexpr int kK3Warps = 32;                          // 1024 threads: one CTA p
 constexpr int kK3BlockThreads = kK3Warps * 32;
 
 template <class Acc>
-struct alignas(sizeof(Acc) == 8 ? 16 : 8) SamplePair {  // one draw, broadcast to its octet through smem
+struct alignas(16) SamplePair {  // fp32 parity path: one draw, broadcast to its octet through smem
     uint32_t row;   // sampled W_h row
-    Acc coef;       // x[j, row] / (r p(row))
+    Acc coef;       // x[j, row] / (r p(row)), fp64
 };
+// bf16 path: row (low 16 bits) | bf16 coefficient (high 16 bits), 4 bytes per draw
+using PackedPair = uint32_t;
 
 // 4 consecutive W_h elements starting at column `col` of row `row`, as floats
 // (kept for the wide-row layouts; the hot loop reads 8 per lane via load8).
@@ -96,7 +98,7 @@ __device__ __forceinline__ void load4w(const __nv_bfloat16* base, size_t stride,
 // (optionally) W_h in the staging type WS.
 size_t k3_smem_bytes(int d_in, size_t coef, size_t ws_elem, bool wsmem) {
     const size_t tables = (((size_t)d_in * (8 + coef) + kGuide * 2) + 127) & ~(size_t)127;
-    const size_t pairs = (size_t)kK3Warps * 4 * 16 * (coef == 8 ? 16 : 8);
+    const size_t pairs = (size_t)kK3Warps * 4 * 16 * (coef == 8 ? 16 : 4);
     return tables + pairs + (wsmem ? (size_t)d_in * kDh * ws_elem : 0);
 }
 
@@ -270,6 +272,161 @@ __global__ void __launch_bounds__(kK3BlockThreads, 1) k3_encode_sampled(K3Args a
         for (int off = 16; off; off >>= 1) my_samples += __shfl_xor_sync(0xffffffffu, my_samples, off);
         if (lane == 0 && my_samples) atomicAdd(a.sample_counter, my_samples);
     }
+}
+
+// acc0 += lo(w2) * c, acc1 += hi(w2) * c with w2 two packed bf16 and c a bf16:
+// sm_100's mixed-precision FMA (SASS FHFMA.BF16, fp32 accumulator, bf16
+// operands selected by half-register), so the hot loop never unpacks W.
+__device__ __forceinline__ void fma2_bf16_f32(float& acc0, float& acc1, uint32_t w2, unsigned short c) {
+    asm("{\n\t.reg .b16 lo, hi;\n\t"
+        "mov.b32 {lo, hi}, %2;\n\t"
+        "fma.rn.f32.bf16 %0, lo, %3, %0;\n\t"
+        "fma.rn.f32.bf16 %1, hi, %3, %1;\n\t}"
+        : "+f"(acc0), "+f"(acc1)
+        : "r"(w2), "h"(c));
+}
+
+// bf16 gather-scale-accumulate encoder (the bf16 hot path). Same draws and
+// schedule as k3_encode_sampled; differences: a draw is broadcast to its octet
+// as one 32-bit word (row | bf16 coefficient << 16), and each lane accumulates
+// its 8 columns with 8 FHFMA straight from the packed bf16 W_h row (no unpack).
+// The coefficient x / (r p) is rounded to bf16 once (relative 2^-9): within
+// the bf16 path's H~ tolerance.
+__global__ void __launch_bounds__(kK3BlockThreads, 1) k3_encode_sampled_bf16(K3Args a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int h = blockIdx.y;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int oct = lane >> 3, l8 = lane & 7;
+    const unsigned omask = 0xFFu << (oct * 8);
+    const int d_in = a.d_in, n = a.n, heads = a.heads;
+
+    uint64_t* s_thr = reinterpret_cast<uint64_t*>(smem);
+    float* s_invp = reinterpret_cast<float*>(s_thr + d_in);
+    uint16_t* s_guide = reinterpret_cast<uint16_t*>(s_invp + d_in);
+    PackedPair* s_pairs = reinterpret_cast<PackedPair*>(smem + ((((size_t)d_in * 12 + kGuide * 2) + 127) & ~(size_t)127));
+    __nv_bfloat16* s_w = reinterpret_cast<__nv_bfloat16*>(s_pairs + kK3Warps * 4 * 16);
+    PackedPair* my_pairs = s_pairs + (warp * 4 + oct) * 16;
+
+    const size_t HD = (size_t)heads * kDh;
+    const __nv_bfloat16* wv = reinterpret_cast<const __nv_bfloat16*>(a.wv);
+    for (int i = tid; i < d_in; i += kK3BlockThreads) {
+        s_thr[i] = a.thr[(size_t)h * d_in + i];
+        s_invp[i] = a.invp[(size_t)h * d_in + i];
+    }
+    for (int g = tid; g < kGuide; g += kK3BlockThreads) s_guide[g] = a.guide[(size_t)h * kGuide + g];
+    for (int e = tid; e < d_in * (kDh / 8); e += kK3BlockThreads) {   // W_h -> smem, 16-byte pieces
+        const int i = e / (kDh / 8), c8 = (e % (kDh / 8)) * 8;
+        *reinterpret_cast<uint4*>(s_w + (size_t)i * kDh + c8) =
+            *reinterpret_cast<const uint4*>(wv + (size_t)i * HD + (size_t)h * kDh + c8);
+    }
+    __syncthreads();
+    const int col0 = 8 * l8;
+    const int nsamp = a.counts[2 * h];
+    const int32_t* list = a.samp_list + (size_t)h * a.tokens;
+    const __nv_bfloat16* x = reinterpret_cast<const __nv_bfloat16*>(a.x);
+    __nv_bfloat16* hout = reinterpret_cast<__nv_bfloat16*>(a.h_out);
+    const uint32_t wbase = static_cast<uint32_t>(__cvta_generic_to_shared(s_w)) + col0 * 2;
+    unsigned long long my_samples = 0;
+
+    auto process_token = [&](int bj, int r) {
+        const int b = bj >> 16, j = bj & 0xFFFF;
+        const size_t tok = (size_t)b * n + j;
+        const size_t tokh = ((size_t)b * heads + h) * n + j;
+        const __nv_bfloat16* xrow = x + tok * d_in;
+        const uint64_t stream = ((uint64_t)(a.b_offset + b) * heads + h) * (uint64_t)n + (uint64_t)j;
+        const float inv_r = 1.0f / (float)r;
+        auto gen = [&](int base, int& i0, int& i1, unsigned short& x0, unsigned short& x1) {
+            uint64_t m0, m1;
+            philox_pair53(a.seed, stream, a.layer, (uint32_t)(base / 2 + l8), &m0, &m1);
+            sample_index2(s_thr, s_guide, m0, m1, i0, i1);   // draws past r are never accumulated
+            x0 = reinterpret_cast<const unsigned short*>(xrow)[i0];
+            x1 = reinterpret_cast<const unsigned short*>(xrow)[i1];
+        };
+        auto pack = [&](int i, unsigned short xb) -> PackedPair {
+            const float c = __uint_as_float((uint32_t)xb << 16) * s_invp[i] * inv_r;
+            const __nv_bfloat16 cb = __float2bfloat16_rn(c);
+            return (uint32_t)i | ((uint32_t)(*reinterpret_cast<const unsigned short*>(&cb)) << 16);
+        };
+        float acc[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc[u] = 0.f;
+        auto accumulate = [&](PackedPair p) {
+            uint4 w;
+            asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w)
+                         : "r"(wbase + (p & 0xFFFFu) * (kDh * 2)));
+            const unsigned short c = (unsigned short)(p >> 16);
+            fma2_bf16_f32(acc[0], acc[1], w.x, c);
+            fma2_bf16_f32(acc[2], acc[3], w.y, c);
+            fma2_bf16_f32(acc[4], acc[5], w.z, c);
+            fma2_bf16_f32(acc[6], acc[7], w.w, c);
+        };
+        int ni0, ni1;
+        unsigned short nx0, nx1;
+        gen(0, ni0, ni1, nx0, nx1);
+        for (int base = 0; base < r; base += 16) {
+            const int i0 = ni0, i1 = ni1;
+            const unsigned short x0 = nx0, x1 = nx1;
+            if (base + 16 < r) gen(base + 16, ni0, ni1, nx0, nx1);   // next round's loads in flight
+            const PackedPair p0 = pack(i0, x0), p1 = pack(i1, x1);
+            if (a.draws_out) {
+                const int k0 = base + 2 * l8;
+                if (k0 < r && k0 < a.draws_stride) a.draws_out[tokh * a.draws_stride + k0] = i0;
+                if (k0 + 1 < r && k0 + 1 < a.draws_stride) a.draws_out[tokh * a.draws_stride + k0 + 1] = i1;
+            }
+            __syncwarp(omask);                     // previous round's pairs fully consumed
+            reinterpret_cast<uint2*>(my_pairs)[l8] = make_uint2(p0, p1);
+            __syncwarp(omask);
+            const int cnt = min(16, r - base);
+            if (cnt == 16) {
+#pragma unroll
+                for (int q4 = 0; q4 < 4; ++q4) {
+                    const uint4 pp = reinterpret_cast<const uint4*>(my_pairs)[q4];
+                    accumulate(pp.x);
+                    accumulate(pp.y);
+                    accumulate(pp.z);
+                    accumulate(pp.w);
+                }
+            } else {
+                for (int s2 = 0; s2 < cnt; ++s2) accumulate(my_pairs[s2]);
+            }
+            if (l8 == 0) my_samples += (unsigned long long)cnt;
+        }
+        __syncwarp(omask);
+        if (a.draws_out && l8 == 0)
+            for (int k = r; k < a.draws_stride; ++k) a.draws_out[tokh * a.draws_stride + k] = -1;
+        store8(hout + tok * HD + (size_t)h * kDh + col0, acc);
+    };
+    auto prefetch_row = [&](int bj) {
+        const __nv_bfloat16* xrow = x + ((size_t)(bj >> 16) * n + (bj & 0xFFFF)) * d_in;
+        const int lines = (d_in * 2 + 127) / 128;
+        for (int ln = l8; ln < lines; ln += 8)
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(reinterpret_cast<const char*>(xrow) + ln * 128));
+    };
+    for (;;) {
+        int t0 = 0;
+        if (lane == 0) t0 = atomicAdd(a.task_cursor + h, 8);
+        t0 = __shfl_sync(0xffffffffu, t0, 0);
+        if (t0 >= nsamp) break;
+        const int ea = t0 + oct, eb = t0 + 4 + oct;
+        const int bja = ea < nsamp ? list[ea] : -1;
+        const int bjb = eb < nsamp ? list[eb] : -1;
+        const int ra = bja >= 0 ? a.budgets[((size_t)(bja >> 16) * heads + h) * n + (bja & 0xFFFF)] : 0;
+        const int rb = bjb >= 0 ? a.budgets[((size_t)(bjb >> 16) * heads + h) * n + (bjb & 0xFFFF)] : 0;
+        if (bja >= 0) prefetch_row(bja);
+        if (bjb >= 0) prefetch_row(bjb);
+        if (bja >= 0) process_token(bja, ra);
+        if (bjb >= 0) process_token(bjb, rb);
+    }
+    if (a.sample_counter) {
+        for (int off = 16; off; off >>= 1) my_samples += __shfl_xor_sync(0xffffffffu, my_samples, off);
+        if (lane == 0 && my_samples) atomicAdd(a.sample_counter, my_samples);
+    }
+}
+
+size_t k3_bf16_smem_bytes(int d_in) {
+    return ((((size_t)d_in * 12 + kGuide * 2) + 127) & ~(size_t)127) + (size_t)kK3Warps * 4 * 16 * 4 +
+           (size_t)d_in * kDh * 2;
 }
 
 // Exact tokens: tiles of 64 listed tokens x 64 outputs; 256 threads, each 4 x 4.

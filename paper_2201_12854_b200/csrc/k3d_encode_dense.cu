@@ -6,19 +6,23 @@
 // A persistent CTA owns one head: W_h (d_in x 64 bf16, MN-major 128B-swizzled
 // chunks of 64 rows) arrives once by TMA and stays in shared memory. Per tile
 // of 64 tokens of the head's budget-sorted list:
-//   1. zero C (64 x d_in bf16, 128B-swizzled K-major: the UMMA A operand)
+//   1. zero the tile (64 x d_in, 128B-swizzled K-major: the UMMA A operand)
 //   2. every lane draws its own samples (Philox4x32-10 + guide-table inverse
-//      CDF: the same draws as the gather kernel) and adds x / (r p) into C
-//      with a shared-memory atomic; duplicate draws of a row add identical
-//      values, so the result does not depend on the atomics' order
-//   3. one thread issues tcgen05.mma M=64 N=64 K=16 over C and W_h, fp32 in TMEM
-//   4. warps 0-3 read the 64 rows back (M=64 layout: row m in TMEM lane
+//      CDF: the same draws as the gather kernel) and counts them: one 32-bit
+//      shared atomic on the 16-bit count of (token, row). No X is read here,
+//      so the draw loop has no global-memory latency in it.
+//   3. scale in place: C[m, i] = bf16(count * x[m, i] * (1/p_i) * (1/r_m)),
+//      reading X only for 16-byte chunks that hold a nonzero count (coalesced
+//      row pieces instead of one scattered gather per draw)
+//   4. one thread issues tcgen05.mma M=64 N=64 K=16 over C and W_h, fp32 in TMEM
+//   5. warps 0-3 read the 64 rows back (M=64 layout: row m in TMEM lane
 //      (m % 16) + 32 (m / 16)) and write H~ in bf16
-// Per sample this costs one Philox half-call, the search and one 2-byte shared
-// atomic, instead of a 128-byte W_h row read and 64 FMAs; the contraction with
-// W_h runs on the tensor core (2 * 64 * 64 * d_in flops per tile). C holds bf16
-// coefficients (relative rounding 2^-9), within the bf16 path's tolerance
-// (DESIGN.md §4). The fp32 parity path keeps the gather kernel.
+// Per draw this costs one Philox half-call, the search and one shared atomic,
+// instead of a 128-byte W_h row read and 64 FMAs; the contraction with W_h
+// runs on the tensor core (2 * 64 * 64 * d_in flops per tile). Counts are
+// exact integers, so the result is independent of the atomics' order; each
+// coefficient is rounded to bf16 once (relative 2^-9), within the bf16 path's
+// tolerance. The fp32 parity path keeps the gather kernel.
 #include "mca_common.cuh"
 #include "tc_common.cuh"
 
@@ -104,22 +108,27 @@ __global__ void __launch_bounds__(k3d::kThreads, 1)
     unsigned long long my_samples = 0;
     uint32_t acc_phase = 0;
 
+    __shared__ int s_bj[kBM];
+    __shared__ int s_r[kBM];
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        // 1. zero C (the previous tile's MMAs completed before its epilogue released us)
+        // 1. zero the tile; fetch the tile's list entries and budgets once
         for (uint32_t off = tid * 16; off < natoms * kAtomBytes; off += k3d::kThreads * 16)
             *reinterpret_cast<uint4*>(cbuf + off) = make_uint4(0, 0, 0, 0);
+        if (tid < kBM) {
+            const int e = tile * kBM + tid;
+            const int bj = e < nsamp ? list[e] : -1;
+            s_bj[tid] = bj;
+            s_r[tid] = bj >= 0 ? a.budgets[((size_t)(bj >> 16) * heads + h) * n + (bj & 0xFFFF)] : 0;
+        }
         __syncthreads();
-        // 2. draws -> C
+        // 2. draws -> counts (16-bit, at the element's position in the swizzled tile)
         for (int m = warp; m < kBM; m += kWarps) {
-            const int e = tile * kBM + m;
-            if (e >= nsamp) break;                   // warp-uniform
-            const int bj = list[e];
+            const int bj = s_bj[m];
+            if (bj < 0) break;                       // warp-uniform (entries are contiguous)
             const int b = bj >> 16, j = bj & 0xFFFF;
+            const int r = s_r[m];
             const size_t tokh = ((size_t)b * heads + h) * n + j;
-            const int r = a.budgets[tokh];
-            const __nv_bfloat16* xrow = x + ((size_t)b * n + j) * d_in;
             const uint64_t stream = ((uint64_t)(a.b_offset + b) * heads + h) * (uint64_t)n + (uint64_t)j;
-            const float inv_r = 1.0f / (float)r;
             const uint32_t row_off = cbase + (uint32_t)(m >> 3) * 1024u + (uint32_t)(m & 7) * 128u;
             const uint32_t sw = (uint32_t)(m & 7);
             for (int base = 0; base < r; base += 64) {
@@ -133,21 +142,69 @@ __global__ void __launch_bounds__(k3d::kThreads, 1)
                     if (a1) a1 = s_thr[++i1] <= m1;
                 }
                 if (k0 < r) {
-                    const float c0 = __bfloat162float(xrow[i0]) * s_invp[i0] * inv_r;
-                    atomic_add_bf16_smem(row_off + (uint32_t)(i0 >> 6) * kAtomBytes +
-                                             ((((uint32_t)(i0 & 63) >> 3) ^ sw) << 4) + (uint32_t)(i0 & 7) * 2, c0);
+                    const uint32_t ad = row_off + (uint32_t)(i0 >> 6) * kAtomBytes +
+                                        ((((uint32_t)(i0 & 63) >> 3) ^ sw) << 4) + (uint32_t)(i0 & 7) * 2;
+                    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(ad & ~3u), "r"(1u << ((ad & 2u) * 8)) : "memory");
                     if (a.draws_out && k0 < a.draws_stride) a.draws_out[tokh * a.draws_stride + k0] = i0;
                 }
                 if (k0 + 1 < r) {
-                    const float c1 = __bfloat162float(xrow[i1]) * s_invp[i1] * inv_r;
-                    atomic_add_bf16_smem(row_off + (uint32_t)(i1 >> 6) * kAtomBytes +
-                                             ((((uint32_t)(i1 & 63) >> 3) ^ sw) << 4) + (uint32_t)(i1 & 7) * 2, c1);
+                    const uint32_t ad = row_off + (uint32_t)(i1 >> 6) * kAtomBytes +
+                                        ((((uint32_t)(i1 & 63) >> 3) ^ sw) << 4) + (uint32_t)(i1 & 7) * 2;
+                    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(ad & ~3u), "r"(1u << ((ad & 2u) * 8)) : "memory");
                     if (a.draws_out && k0 + 1 < a.draws_stride) a.draws_out[tokh * a.draws_stride + k0 + 1] = i1;
                 }
             }
             if (lane == 0) my_samples += (unsigned long long)r;
             if (a.draws_out)
                 for (int k = r + lane; k < a.draws_stride; k += 32) a.draws_out[tokh * a.draws_stride + k] = -1;
+        }
+        __syncthreads();
+        // 3. counts -> coefficients in place; X read only where a chunk has a count
+        {
+            constexpr int kChunksPerRow = 8;                    // 16-byte chunks per 128-byte row of an atom
+            const int nwork = kBM * natoms * kChunksPerRow;     // (row, atom, chunk)
+            for (int base = 0; base < nwork; base += k3d::kThreads * 4) {
+                uint4 cnt[4], xv[4];
+                uint32_t adr[4];
+                int col[4], row[4];
+                bool live[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {                   // pass A: read counts, issue X loads
+                    const int wi = base + u * k3d::kThreads + tid;
+                    live[u] = false;
+                    if (wi >= nwork) continue;
+                    const int atom = wi / (kBM * kChunksPerRow);
+                    const int rem = wi - atom * (kBM * kChunksPerRow);
+                    const int m = rem / kChunksPerRow, q = rem - m * kChunksPerRow;
+                    row[u] = m;
+                    col[u] = atom * 64 + q * 8;
+                    adr[u] = (uint32_t)atom * kAtomBytes + (uint32_t)(m >> 3) * 1024u + (uint32_t)(m & 7) * 128u +
+                             (((uint32_t)q ^ (uint32_t)(m & 7)) << 4);
+                    cnt[u] = *reinterpret_cast<const uint4*>(cbuf + adr[u]);
+                    live[u] = (cnt[u].x | cnt[u].y | cnt[u].z | cnt[u].w) != 0u;
+                    if (live[u]) {
+                        const int bj = s_bj[m];
+                        const __nv_bfloat16* xr = x + ((size_t)(bj >> 16) * n + (bj & 0xFFFF)) * d_in;
+                        xv[u] = *reinterpret_cast<const uint4*>(xr + col[u]);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {                   // pass B: scale and store bf16
+                    if (!live[u]) continue;
+                    const float inv_r = 1.0f / (float)s_r[row[u]];
+                    const uint32_t cw[4] = {cnt[u].x, cnt[u].y, cnt[u].z, cnt[u].w};
+                    const uint32_t xw[4] = {xv[u].x, xv[u].y, xv[u].z, xv[u].w};
+                    uint32_t outw[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const int i = col[u] + 2 * e;
+                        const float c0 = (float)(cw[e] & 0xFFFFu), c1 = (float)(cw[e] >> 16);
+                        const float x0 = __uint_as_float(xw[e] << 16), x1 = __uint_as_float(xw[e] & 0xFFFF0000u);
+                        outw[e] = pack_bf16x2(c0 * x0 * s_invp[i] * inv_r, c1 * x1 * s_invp[i + 1] * inv_r);
+                    }
+                    *reinterpret_cast<uint4*>(cbuf + adr[u]) = make_uint4(outw[0], outw[1], outw[2], outw[3]);
+                }
+            }
         }
         fence_proxy_async_smem();                     // C (generic-proxy writes) -> tensor core (async proxy)
         __syncthreads();
@@ -175,9 +232,8 @@ __global__ void __launch_bounds__(k3d::kThreads, 1)
             tmem_ld32(lane_base + 32, v[1]);
             tmem_ld_wait();
             const int m = warp * 16 + lane;
-            const int e = tile * kBM + m;
-            if (lane < 16 && e < nsamp) {
-                const int bj = list[e];
+            const int bj = lane < 16 ? s_bj[m] : -1;
+            if (bj >= 0) {
                 const size_t tok = (size_t)(bj >> 16) * n + (bj & 0xFFFF);
                 __nv_bfloat16* dst =
                     reinterpret_cast<__nv_bfloat16*>(a.h_out) + tok * (size_t)heads * kDh + (size_t)h * kDh;

@@ -262,7 +262,10 @@ mca_status launch_k3(mca_weights* w, const void* x, int B, int n, long b_offset,
     void (*kern)(K3Args) = nullptr;
     size_t smem = k3_smem_bytes(w->d_in, sizeof(Coef), sizeof(T), true);
     constexpr size_t kMaxSmem = 220 * 1024;
-    if (smem <= kMaxSmem) {
+    if (sizeof(T) == 2 && k3_bf16_smem_bytes(w->d_in) <= kMaxSmem) {
+        smem = k3_bf16_smem_bytes(w->d_in);
+        kern = k3_encode_sampled_bf16;
+    } else if (smem <= kMaxSmem) {
         if constexpr (sizeof(T) == 2) kern = k3_encode_sampled<__nv_bfloat16, __nv_bfloat16, float, true>;
         else kern = k3_encode_sampled<float, float, double, true>;
     } else {
