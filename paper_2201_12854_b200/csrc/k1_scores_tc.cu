@@ -10,8 +10,10 @@
 //       t = scale * S (log2 domain, ex2.approx)  -> row_m, row_l (fp64), lse
 //   K1b (kColMax),   CTA = (b, h, 128 keys):     S^T = K Q_blk^T (lane = key)
 //       per lane: max over all queries of v = t - lse_q and its first argmax
-//       q*, written as the argmax key K2 re-evaluates in fp64
-//       (k1_scores_simt.cu describes the key; one writer per key, no atomics)
+//       q*, written as the argmax key plus the winner's raw score S (fp32),
+//       which K2 re-evaluates in fp64 as exp(scale S - m_q*) / l_q* (the
+//       oracle's softmax form; k1_scores_simt.cu describes the key; one writer
+//       per key, no atomics)
 //
 // Same kernel body for both: the resident 128-row operand (Q or K) arrives by
 // TMA once, the streamed operand (K or Q blocks of 128) through a 3-stage TMA
@@ -34,7 +36,7 @@ constexpr uint32_t kSmemA = 0;                                    // resident op
 constexpr uint32_t kSmemB = kTileBytes;                           // kStages streamed tiles
 constexpr uint32_t kSmemLse = kSmemB + kStages * kTileBytes;      // [kMaxN] f32 (K1b)
 constexpr int kMaxN = 4096;
-constexpr uint32_t kSmemComb = kSmemLse + kMaxN * 4;              // partner exchange, 2 x [128] x 4 B
+constexpr uint32_t kSmemComb = kSmemLse + kMaxN * 4;              // partner exchange, 3 x [128] x 4 B
 constexpr uint32_t kSmemBar = kSmemComb + 4 * 128 * 4;
 constexpr uint32_t kSmemBytes = kSmemBar + 256 + 1024;
 constexpr uint32_t kIdesc = mca_tc::idesc_f16(1, 0, kBM, kBN);
@@ -46,7 +48,8 @@ template <int kMode>
 __global__ void __launch_bounds__(k1tc::kThreads, 2)
     k1_scores_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k, int n,
                  int heads, float scale, double* __restrict__ row_m, double* __restrict__ row_l,
-                 float* __restrict__ lse, unsigned long long* __restrict__ colkey) {
+                 float* __restrict__ lse, unsigned long long* __restrict__ colkey,
+                 float* __restrict__ colscore) {
     using namespace k1tc;
     using namespace mca_tc;
     extern __shared__ uint8_t smem_raw[];
@@ -131,6 +134,7 @@ __global__ void __launch_bounds__(k1tc::kThreads, 2)
         float m2 = -INFINITY, l = 0.0f;            // kRowStats
         float best = -INFINITY;                    // kColMax
         int best_i = 0x7FFFFFFF;
+        float best_s = 0.f;                        // raw score S of the winner (K2 re-evaluates exp(scale S - m) / l)
         for (int i = 0; i < nblk; ++i) {
             const int sb = i & 1;
             mbar_wait(s_full + sb, (i >> 1) & 1);
@@ -183,6 +187,7 @@ __global__ void __launch_bounds__(k1tc::kThreads, 2)
                             if (g + e < valid && v > best) {
                                 best = v;
                                 best_i = c0 + g + e;
+                                best_s = __uint_as_float(sv[(g + e) >> 5][(g + e) & 31]);
                             }
                         }
                     }
@@ -199,6 +204,7 @@ __global__ void __launch_bounds__(k1tc::kThreads, 2)
             if (half == 1) {
                 comb[row] = best;
                 reinterpret_cast<int*>(comb)[128 + row] = best_i;
+                comb[256 + row] = best_s;
             }
         }
         asm volatile("bar.sync 1, %0;" ::"n"(kConsumers * 32) : "memory");
@@ -219,7 +225,9 @@ __global__ void __launch_bounds__(k1tc::kThreads, 2)
                 if (vb > best || (vb == best && ib < best_i)) {
                     best = vb;
                     best_i = ib;
+                    best_s = comb[256 + row];
                 }
+                colscore[bh * n + grow] = best_s;
                 colkey[bh * n + grow] = ((unsigned long long)float_to_ordered(best) << 32) |
                                         (unsigned long long)(0xFFFFFFFFu - (uint32_t)best_i);
             }

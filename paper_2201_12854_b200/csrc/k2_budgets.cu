@@ -10,10 +10,11 @@
 //
 // cmax comes from K1's column key (k1_scores_*.cu):
 //   kKeyValue:  the key is the fp64 column maximum itself.
-//   kKeyArgmax: the key holds the winning row i*; the score t = scale q_i*.k_j is
-//               recomputed here in fp64 from the (bf16) inputs — products of
-//               bf16 values are exact in fp64 — and cmax = exp(t - m_i*) / l_i*,
-//               the oracle's softmax formula, with K1's row statistics.
+//   kKeyArgmax: the key holds the winning row i*; cmax = exp(scale S - m_i*) / l_i*,
+//               the oracle's softmax formula, in fp64 with K1's row statistics.
+//               S is the winner's tensor-core score from K1b (exact bf16
+//               products, fp32 sum), or, for the CUDA-core score pass,
+//               q_i*.k_j recomputed here in fp64.
 //
 // Bucketing ("tokens bucketed by sample count"): a block covers
 // 256 tokens of ONE (b, h) row, so it histograms budgets per head in shared
@@ -49,8 +50,9 @@ struct K2Args {
     const double* cmax_in;             // kGivenCmax
     const double* row_m;               // [B, H, n] (kKeyArgmax)
     const double* row_l;
-    const void* q;                     // [B, n, H*64] (kKeyArgmax)
+    const void* q;                     // [B, n, H*64] (kKeyArgmax without colscore)
     const void* k;
+    const float* colscore;             // [B, H, n] raw winning score (kKeyArgmax; nullable)
     double scale;
     long count;                        // B*H*n
     int row_len;                       // tokens per block row (= n in the forward)
@@ -110,11 +112,16 @@ __global__ void __launch_bounds__(256) k2_budgets(K2Args a) {
             } else {
                 const unsigned long long key = a.colkey[t];
                 const int i = (int)(0xFFFFFFFFu - (uint32_t)(key & 0xFFFFFFFFull));
-                const int b = (int)(bh / a.heads), h = (int)(bh - (long)b * a.heads);
-                const size_t HD = (size_t)a.heads * kDh;
-                const T* qi = reinterpret_cast<const T*>(a.q) + ((size_t)b * a.n + i) * HD + (size_t)h * kDh;
-                const T* kj = reinterpret_cast<const T*>(a.k) + ((size_t)b * a.n + j) * HD + (size_t)h * kDh;
-                const double s = dot64_f64(qi, kj);
+                double s;
+                if (a.colscore) {
+                    s = (double)a.colscore[t];   // tensor-core score: exact bf16 products, fp32 sum
+                } else {
+                    const int b = (int)(bh / a.heads), h = (int)(bh - (long)b * a.heads);
+                    const size_t HD = (size_t)a.heads * kDh;
+                    const T* qi = reinterpret_cast<const T*>(a.q) + ((size_t)b * a.n + i) * HD + (size_t)h * kDh;
+                    const T* kj = reinterpret_cast<const T*>(a.k) + ((size_t)b * a.n + j) * HD + (size_t)h * kDh;
+                    s = dot64_f64(qi, kj);
+                }
                 const size_t ri = (size_t)bh * a.n + i;
                 cm = __ddiv_rn(exp(__dsub_rn(__dmul_rn(a.scale, s), a.row_m[ri])), a.row_l[ri]);
             }

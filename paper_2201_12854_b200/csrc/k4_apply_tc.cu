@@ -1,40 +1,43 @@
 // k4_apply_tc.cu — K4 on the 5th-generation tensor cores: y = A . H~ for one
 // (b, h, 128-query tile) per CTA (matrix.hpp:33-34 `matmul`).
 //
-// A is never materialised. Per 128-key block:
-//   S  = Q K_blk^T                  tcgen05.mma M=128 N=128 K=64 -> TMEM (fp32)
+// A is never materialised. Per 64-key block:
+//   S  = Q K_blk^T                  tcgen05.mma M=128 N=64 K=64 -> TMEM (fp32)
 //   P  = exp(scale*S - lse)         8 softmax warps, 2 per TMEM lane quadrant
-//                                   (lane = query row), 64 keys each; lse from
+//                                   (lane = query row), 32 keys each; lse from
 //                                   K1, so no online rescaling; P written bf16
 //                                   into a 128B-swizzled K-major smem tile
-//   O += P H~_blk                   tcgen05.mma M=128 N=64 K=128 (H~ MN-major)
+//   O += P H~_blk                   tcgen05.mma M=128 N=64 K=64 (H~ MN-major)
 // Warp roles (320 threads): warp 0 TMA producer (Q once, then a 3-stage ring of
 // K/H~ blocks), warp 1 TMEM allocator + single-thread MMA issuer, warps 2-9
 // softmax + epilogue. S is double-buffered in TMEM and P in smem, so the tensor core computes S(kb+1) while the softmax warps exponentiate S(kb), and
-// P(kb) . H~(kb) overlaps the exponentials of block kb+1. TMEM: S0 [0,128),
-// S1 [128,256), O [256,320).
+// P(kb) . H~(kb) overlaps the exponentials of block kb+1. 64-key blocks keep
+// shared memory at ~98 KB and TMEM at 256 columns (S0 [0,64), S1 [64,128),
+// O [128,192)), so two CTAs run per SM and hide each other's prologue.
 #include "mca_common.cuh"
 #include "tc_common.cuh"
 
 namespace mca_dev {
 
 namespace k4tc {
-constexpr int kBM = 128, kBK = 128, kStages = 3;
+constexpr int kBM = 128, kBK = 64, kStages = 3;
 constexpr int kConsumers = 8;                        // 2 warps per TMEM lane quadrant
 constexpr int kThreads = 64 + kConsumers * 32;
-constexpr uint32_t kTileBytes = kBK * kDh * 2;       // 16 KB: one 128 x 64 bf16 tile
-constexpr uint32_t kPBytes = kBM * kBK * 2;          // 32 KB: P tile (two 64-key swizzle atoms)
+constexpr uint32_t kQBytes = kBM * kDh * 2;         // 16 KB: Q tile (128 x 64 bf16)
+constexpr uint32_t kTileBytes = kBK * kDh * 2;       // 8 KB: one 64-key K or H~ block
+constexpr uint32_t kPBytes = kBM * kBK * 2;          // 16 KB: P tile (one 64-key swizzle atom)
 constexpr uint32_t kSmemQ = 0;
-constexpr uint32_t kSmemK = kSmemQ + kTileBytes;                     // kStages tiles
+constexpr uint32_t kSmemK = kSmemQ + kQBytes;                        // kStages tiles
 constexpr uint32_t kSmemH = kSmemK + kStages * kTileBytes;           // kStages tiles
 constexpr uint32_t kSmemP = kSmemH + kStages * kTileBytes;           // 2 P tiles
 constexpr uint32_t kSmemBar = kSmemP + 2 * kPBytes;
 constexpr uint32_t kSmemBytes = kSmemBar + 256 + 1024;               // + alignment slack
 constexpr uint32_t kIdescS = mca_tc::idesc_f16(1, 0, kBM, kBK);      // bf16, B K-major
+constexpr uint32_t kOCol = 2 * kBK;                                 // TMEM: S0 [0,64), S1 [64,128), O [128,192)
 constexpr uint32_t kIdescO = mca_tc::idesc_f16(1, 1, kBM, kDh);      // bf16, B MN-major
 }  // namespace k4tc
 
-__global__ void __launch_bounds__(k4tc::kThreads, 1)
+__global__ void __launch_bounds__(k4tc::kThreads, 2)
     k4_apply_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                 const __grid_constant__ CUtensorMap tm_h, const float* __restrict__ lse, int n, int heads,
                 float scale, __nv_bfloat16* __restrict__ y) {
@@ -72,7 +75,7 @@ __global__ void __launch_bounds__(k4tc::kThreads, 1)
         mbar_init(o_full, 1);
         fence_barrier_init();
     }
-    if (warp == 1) tmem_alloc<512>(tmem_slot);
+    if (warp == 1) tmem_alloc<256>(tmem_slot);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -83,7 +86,7 @@ __global__ void __launch_bounds__(k4tc::kThreads, 1)
             tma_prefetch(&tm_q);
             tma_prefetch(&tm_k);
             tma_prefetch(&tm_h);
-            mbar_expect_tx(q_full, kTileBytes);
+            mbar_expect_tx(q_full, kQBytes);
             tma_load_3d(smem + kSmemQ, &tm_q, q_full, h * kDh, m0, b);
             for (int kb = 0; kb < nkb; ++kb) {
                 const int s = kb % kStages;
@@ -104,9 +107,9 @@ __global__ void __launch_bounds__(k4tc::kThreads, 1)
                 const uint32_t h_addr = smem_u32(smem + kSmemH + s * kTileBytes);
 #pragma unroll
                 for (int kk = 0; kk < kBK / 16; ++kk) {
-                    const uint64_t ad = sw128_desc(p_addr + (kk >> 2) * (kBM * 128) + (kk & 3) * 32, 16, 1024);
+                    const uint64_t ad = sw128_desc(p_addr + kk * 32, 16, 1024);
                     const uint64_t bd = sw128_desc(h_addr + kk * 2048, kBK * 128, 1024);
-                    umma_f16(tmem + 256, ad, bd, kIdescO, (j > 0 || kk > 0) ? 1u : 0u);
+                    umma_f16(tmem + kOCol, ad, bd, kIdescO, (j > 0 || kk > 0) ? 1u : 0u);
                 }
                 umma_commit(p_empty + pb);
                 umma_commit(kv_empty + s);
@@ -132,7 +135,7 @@ __global__ void __launch_bounds__(k4tc::kThreads, 1)
         }
     } else {  // ------------------------------- softmax + epilogue (warps 2..9)
         const int quad = warp & 3;                 // TMEM lane quadrant this warp may access
-        const int half = (warp - 2) >> 2;          // keys [64*half, 64*half+64) of each block
+        const int half = (warp - 2) >> 2;          // keys [32*half, 32*half+32) of each block
         const int row = quad * 32 + lane;          // query row within the tile
         const uint32_t lane_base = tmem + ((uint32_t)(quad * 32) << 16);
         const float c = scale * 1.4426950408889634f;
@@ -143,30 +146,29 @@ __global__ void __launch_bounds__(k4tc::kThreads, 1)
             const uint32_t ph = (kb >> 1) & 1;
             mbar_wait(s_full + sb, ph);
             tc_fence_after();
-            uint32_t sv[2][32];
-            tmem_ld32(lane_base + sb * kBK + half * 64, sv[0]);
-            tmem_ld32(lane_base + sb * kBK + half * 64 + 32, sv[1]);
+            uint32_t sv[32];
+            tmem_ld32(lane_base + sb * kBK + half * 32, sv);
             tmem_ld_wait();
             tc_fence_before();
             mbar_arrive(s_empty + sb);
             mbar_wait(p_empty + sb, ph ^ 1);
-            // this warp's 64 keys form exactly one 128B-swizzle atom column of P
-            uint8_t* pt = smem + kSmemP + sb * kPBytes + half * (kBM * 128);
-            const int kbase = kb * kBK + half * 64;
+            // this warp's 32 keys are chunks [4*half, 4*half+4) of the P tile's 128-byte rows
+            uint8_t* pt = smem + kSmemP + sb * kPBytes;
+            const int kbase = kb * kBK + half * 32;
             const int valid = n - kbase;          // keys >= n contribute nothing
 #pragma unroll
-            for (int ch = 0; ch < 8; ++ch) {       // 16-byte chunks of 8 keys
+            for (int ch = 0; ch < 4; ++ch) {       // 16-byte chunks of 8 keys
                 uint32_t pk[4];
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
                     const int col = ch * 8 + 2 * e;
-                    float p0 = ex2_approx(__fmaf_rn(__uint_as_float(sv[col >> 5][col & 31]), c, -lse2));
-                    float p1 = ex2_approx(__fmaf_rn(__uint_as_float(sv[(col + 1) >> 5][(col + 1) & 31]), c, -lse2));
+                    float p0 = ex2_approx(__fmaf_rn(__uint_as_float(sv[col]), c, -lse2));
+                    float p1 = ex2_approx(__fmaf_rn(__uint_as_float(sv[col + 1]), c, -lse2));
                     if (col >= valid) p0 = 0.0f;
                     if (col + 1 >= valid) p1 = 0.0f;
                     pk[e] = pack_bf16x2(p0, p1);
                 }
-                *reinterpret_cast<uint4*>(pt + sw128_offset(row, ch * 16)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                *reinterpret_cast<uint4*>(pt + sw128_offset(row, (half * 4 + ch) * 16)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
             }
             fence_proxy_async_smem();
             mbar_arrive(p_full + sb);
@@ -175,7 +177,7 @@ __global__ void __launch_bounds__(k4tc::kThreads, 1)
         mbar_wait(o_full, 0);
         tc_fence_after();
         uint32_t ov[32];
-        tmem_ld32(lane_base + 256 + half * 32, ov);
+        tmem_ld32(lane_base + kOCol + half * 32, ov);
         tmem_ld_wait();
         if (grow < n) {
             __nv_bfloat16* dst = y + ((size_t)b * n + grow) * (size_t)heads * kDh + (size_t)h * kDh + half * 32;
@@ -191,7 +193,7 @@ __global__ void __launch_bounds__(k4tc::kThreads, 1)
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 1) tmem_dealloc<512>(tmem);
+    if (warp == 1) tmem_dealloc<256>(tmem);
 }
 
 }  // namespace mca_dev

@@ -140,6 +140,7 @@ struct mca_weights {
     double* row_m = nullptr;                  // [B, H, n] row max of the scaled scores
     double* row_l = nullptr;                  // [B, H, n] row sum of exp(t - m)
     unsigned long long* colkey = nullptr;     // [B, H, n]
+    float* colscore = nullptr;                // [B, H, n] winning raw score (tensor-core score pass)
     int32_t* budgets = nullptr;               // [B, H, n]
     uint8_t* exact = nullptr;                 // [B, H, n]
     void* hbuf = nullptr;                     // [B, n, H*dh]
@@ -164,6 +165,7 @@ void free_workspace(mca_weights* w) {
     cudaFree(w->row_m);
     cudaFree(w->row_l);
     cudaFree(w->colkey);
+    cudaFree(w->colscore);
     cudaFree(w->budgets);
     cudaFree(w->exact);
     cudaFree(w->hbuf);
@@ -175,6 +177,7 @@ void free_workspace(mca_weights* w) {
     w->row_m = nullptr;
     w->row_l = nullptr;
     w->colkey = nullptr;
+    w->colscore = nullptr;
     w->budgets = nullptr;
     w->exact = nullptr;
     w->hbuf = nullptr;
@@ -190,6 +193,7 @@ mca_status ensure_workspace(mca_weights* w, long tokens, mca_stream_t stream) {
         cudaMalloc(&w->row_m, th * sizeof(double)) != cudaSuccess ||
         cudaMalloc(&w->row_l, th * sizeof(double)) != cudaSuccess ||
         cudaMalloc(&w->colkey, th * sizeof(unsigned long long)) != cudaSuccess ||
+        cudaMalloc(&w->colscore, th * sizeof(float)) != cudaSuccess ||
         cudaMalloc(&w->budgets, th * sizeof(int32_t)) != cudaSuccess ||
         cudaMalloc(&w->exact, th * sizeof(uint8_t)) != cudaSuccess ||
         cudaMalloc(&w->hbuf, th * w->dh * dtype_size(w->wdt)) != cudaSuccess ||
@@ -507,10 +511,10 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
             }
             const dim3 g1((n + 127) / 128, H, B);
             k1_scores_tc<kRowStats><<<g1, k1tc::kThreads, k1tc::kSmemBytes, stream>>>(
-                tq, tk, n, H, (float)scale, w->row_m, w->row_l, w->lse, w->colkey);
+                tq, tk, n, H, (float)scale, w->row_m, w->row_l, w->lse, w->colkey, w->colscore);
             MCA_LAUNCH_CHECK("k1a_row_stats");
             k1_scores_tc<kColMax><<<g1, k1tc::kThreads, k1tc::kSmemBytes, stream>>>(
-                tq, tk, n, H, (float)scale, w->row_m, w->row_l, w->lse, w->colkey);
+                tq, tk, n, H, (float)scale, w->row_m, w->row_l, w->lse, w->colkey, w->colscore);
         }
         MCA_LAUNCH_CHECK("k1_scores");
     }
@@ -525,6 +529,7 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
         a.row_l = w->row_l;
         a.q = q;
         a.k = k;
+        a.colscore = (dt == MCA_BF16 && !force_simt() && n <= k1tc::kMaxN) ? w->colscore : nullptr;
         a.scale = scale;
         a.count = th;
         a.row_len = n;
@@ -578,8 +583,8 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
         else {
             CUtensorMap tq, tk, th;
             if (!make_tmap_bf16(&tq, q, (uint64_t)H * kDh, n, B, 128) ||
-                !make_tmap_bf16(&tk, k, (uint64_t)H * kDh, n, B, 128) ||
-                !make_tmap_bf16(&th, w->hbuf, (uint64_t)H * kDh, n, B, 128))
+                !make_tmap_bf16(&tk, k, (uint64_t)H * kDh, n, B, k4tc::kBK) ||
+                !make_tmap_bf16(&th, w->hbuf, (uint64_t)H * kDh, n, B, k4tc::kBK))
                 return fail(MCA_ERR_CUDA, "cuTensorMapEncodeTiled failed for q/k/h");
             static bool attr = false;
             if (!attr) {
