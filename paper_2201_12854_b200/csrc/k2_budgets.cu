@@ -139,8 +139,12 @@ __global__ void __launch_bounds__(256) k2_budgets(K2Args a) {
         }
         // sort bin: budgets above d - 1 only occur through budgets_override (tests)
         const int bin = ex ? a.d : min(r, a.d - 1);
-        if (use_hist) atomicAdd(&s_hist[bin], 1u);
-        else if (a.hist) atomicAdd(&a.hist[(size_t)(bh % a.heads) * (a.d + 1) + bin], 1u);
+        // warp-aggregated: lanes with the same bin add once (small budgets are common)
+        const unsigned peers = __match_any_sync(__activemask(), bin);
+        if ((threadIdx.x & 31) == __ffs(peers) - 1) {
+            if (use_hist) atomicAdd(&s_hist[bin], (unsigned)__popc(peers));
+            else if (a.hist) atomicAdd(&a.hist[(size_t)(bh % a.heads) * (a.d + 1) + bin], (unsigned)__popc(peers));
+        }
     }
     if (a.counters) {
         for (int off = 16; off; off >>= 1) {  // warp reduce, one atomic per warp
@@ -212,13 +216,17 @@ __global__ void __launch_bounds__(256) k2_scatter(const int32_t* __restrict__ bu
     const long t = bh * n + j;
     const int b = (int)(bh / heads), h = (int)(bh - (long)b * heads);
     const int tok = (b << 16) | j;   // list entry: (b << 16) | j (n, B <= 65535, checked by the host)
-    if (exact[t]) {
-        const unsigned int pos = atomicAdd(&cursor[(size_t)h * (d + 1) + d], 1u);
-        exact_list[(size_t)h * tokens + pos] = tok;
-    } else {
-        const unsigned int pos = atomicAdd(&cursor[(size_t)h * (d + 1) + min(budgets[t], d - 1)], 1u);
-        samp_list[(size_t)h * tokens + pos] = tok;
-    }
+    const bool ex = exact[t] != 0;
+    const int bin = ex ? d : min(budgets[t], d - 1);
+    // warp-aggregated cursor bump: one atomic per distinct bin in the warp
+    const unsigned peers = __match_any_sync(__activemask(), bin);
+    const int leader = __ffs(peers) - 1;
+    const int lane = threadIdx.x & 31;
+    unsigned int base = 0;
+    if (lane == leader) base = atomicAdd(&cursor[(size_t)h * (d + 1) + bin], (unsigned)__popc(peers));
+    base = __shfl_sync(peers, base, leader);
+    const unsigned int pos = base + (unsigned)__popc(peers & ((1u << lane) - 1u));
+    (ex ? exact_list : samp_list)[(size_t)h * tokens + pos] = tok;
 }
 
 template __global__ void k2_budgets<kKeyValue, float>(K2Args);
