@@ -134,7 +134,6 @@ __global__ void __launch_bounds__(k1tc::kThreads, 2)
         float m2 = -INFINITY, l = 0.0f;            // kRowStats
         float best = -INFINITY;                    // kColMax
         int best_i = 0x7FFFFFFF;
-        float best_s = 0.f;                        // raw score S of the winner (K2 re-evaluates exp(scale S - m) / l)
         for (int i = 0; i < nblk; ++i) {
             const int sb = i & 1;
             mbar_wait(s_full + sb, (i >> 1) & 1);
@@ -187,7 +186,6 @@ __global__ void __launch_bounds__(k1tc::kThreads, 2)
                             if (g + e < valid && v > best) {
                                 best = v;
                                 best_i = c0 + g + e;
-                                best_s = __uint_as_float(sv[(g + e) >> 5][(g + e) & 31]);
                             }
                         }
                     }
@@ -204,7 +202,6 @@ __global__ void __launch_bounds__(k1tc::kThreads, 2)
             if (half == 1) {
                 comb[row] = best;
                 reinterpret_cast<int*>(comb)[128 + row] = best_i;
-                comb[256 + row] = best_s;
             }
         }
         asm volatile("bar.sync 1, %0;" ::"n"(kConsumers * 32) : "memory");
@@ -225,9 +222,9 @@ __global__ void __launch_bounds__(k1tc::kThreads, 2)
                 if (vb > best || (vb == best && ib < best_i)) {
                     best = vb;
                     best_i = ib;
-                    best_s = comb[256 + row];
                 }
-                colscore[bh * n + grow] = best_s;
+                // the winner's raw score, rebuilt from v = fma(S, c2, -lse2_q*) (exact when S = 0)
+                colscore[bh * n + grow] = (best + s_lse[best_i]) / c2;
                 colkey[bh * n + grow] = ((unsigned long long)float_to_ordered(best) << 32) |
                                         (unsigned long long)(0xFFFFFFFFu - (uint32_t)best_i);
             }
