@@ -88,7 +88,7 @@ typedef struct mca_flops {
 typedef struct mca_debug {
     double* cmax_out;                /* column maxima of A (fp64: exactly what Eq. 9 consumed) */
     float* lse_out;                  /* per-row log-sum-exp of the scaled scores             */
-    void* h_out;                     /* H~ [B, n, heads*d_h], compute dtype                  */
+    void* h_out;                     /* H~ [B, n, heads*d_h]: fp32 (fp32 path) / fp16 (bf16)  */
     int32_t* draws_out;              /* [B, heads, n, draws_stride]: first draws, -1 padded  */
     int32_t draws_stride;
     int32_t reserved;

@@ -213,7 +213,8 @@ def mca_forward(weights: AttentionWeights, q: torch.Tensor, k: torch.Tensor, x: 
     the device; with flops=True the FlopsReport is read back (synchronises).
 
     debug (parity testing) may hold CUDA tensors under the mca_debug field
-    names: cmax_out (f64), lse_out (f32), h_out, draws_out (+ draws_stride),
+    names: cmax_out (f64), lse_out (f32), h_out (H~: fp32 for fp32 inputs, fp16
+    for bf16 inputs), draws_out (+ draws_stride),
     cmax_override (f64), budgets_override (i32) + exact_override (u8).
     """
     cfg = cfg or McaConfig()

@@ -153,7 +153,8 @@ __global__ void __launch_bounds__(kK3BlockThreads, 1) k3_encode_sampled(K3Args a
     const int nsamp = a.counts[2 * h];
     const int32_t* list = a.samp_list + (size_t)h * a.tokens;
     const T* x = reinterpret_cast<const T*>(a.x);
-    T* hout = reinterpret_cast<T*>(a.h_out);
+    using HT = typename HType<T>::type;
+    HT* hout = reinterpret_cast<HT*>(a.h_out);
     unsigned long long my_samples = 0;
 
     // Accumulators: fp32 path keeps 8 fp64 sums; the bf16 path packs 8 fp32 sums
@@ -324,7 +325,7 @@ __global__ void __launch_bounds__(kK3BlockThreads, 1) k3_encode_sampled_bf16(K3A
     const int nsamp = a.counts[2 * h];
     const int32_t* list = a.samp_list + (size_t)h * a.tokens;
     const __nv_bfloat16* x = reinterpret_cast<const __nv_bfloat16*>(a.x);
-    __nv_bfloat16* hout = reinterpret_cast<__nv_bfloat16*>(a.h_out);
+    __half* hout = reinterpret_cast<__half*>(a.h_out);
     const uint32_t wbase = static_cast<uint32_t>(__cvta_generic_to_shared(s_w)) + col0 * 2;
     unsigned long long my_samples = 0;
 
@@ -443,7 +444,8 @@ __global__ void __launch_bounds__(256) k3b_encode_exact(K3Args a) {
     const size_t HD = (size_t)a.heads * kDh;
     const T* x = reinterpret_cast<const T*>(a.x);
     const T* wv = reinterpret_cast<const T*>(a.wv);
-    T* hout = reinterpret_cast<T*>(a.h_out);
+    using HT = typename HType<T>::type;
+    HT* hout = reinterpret_cast<HT*>(a.h_out);
     const int32_t* list = a.exact_list + (size_t)h * a.tokens;
     for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
         __syncthreads();
@@ -505,9 +507,9 @@ __global__ void __launch_bounds__(256) k3b_encode_exact(K3Args a) {
         for (int i = 0; i < 4; ++i) {
             const int tok = toks[ty * 4 + i];
             if (tok < 0) continue;
-            T* dst = hout + (size_t)tok * HD + (size_t)h * kDh + tx * 4;
+            HT* dst = hout + (size_t)tok * HD + (size_t)h * kDh + tx * 4;
 #pragma unroll
-            for (int jj = 0; jj < 4; ++jj) dst[jj] = from_f32<T>((float)acc[i][jj]);
+            for (int jj = 0; jj < 4; ++jj) dst[jj] = (HT)((float)acc[i][jj]);
         }
     }
 }

@@ -11,7 +11,7 @@
 //   B = W_h                              [d_in x 64], MN-major chunks of 64 rows
 //   D = tcgen05.mma M=128 N=64 K=16 (x4 per chunk), fp32 in TMEM (64 columns)
 // Warps 0-3: producers (cp.async of A and B, 4-stage ring) and then the
-// epilogue (TMEM -> bf16 -> H~ rows); warp 4: TMEM allocator + MMA issuer.
+// epilogue (TMEM -> fp16 -> H~ rows); warp 4: TMEM allocator + MMA issuer.
 #include "mca_common.cuh"
 #include "tc_common.cuh"
 
@@ -123,14 +123,14 @@ __global__ void __launch_bounds__(k3btc::kThreads, 2) k3b_exact_tc(K3Args a) {
         tmem_ld32(lane_base + 32, v[1]);
         tmem_ld_wait();
         if (bj >= 0) {
-            __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(a.h_out) + tok * HD + (size_t)h * kDh;
+            __half* dst = reinterpret_cast<__half*>(a.h_out) + tok * HD + (size_t)h * kDh;   // H~ is fp16
 #pragma unroll
             for (int g = 0; g < 8; ++g) {
                 uint32_t pk[4];
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
                     const int c = g * 8 + 2 * e;
-                    pk[e] = pack_bf16x2(__uint_as_float(v[c >> 5][c & 31]), __uint_as_float(v[(c + 1) >> 5][(c + 1) & 31]));
+                    pk[e] = pack_f16x2(__uint_as_float(v[c >> 5][c & 31]), __uint_as_float(v[(c + 1) >> 5][(c + 1) & 31]));
                 }
                 reinterpret_cast<uint4*>(dst)[g] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
             }

@@ -235,16 +235,15 @@ __global__ void __launch_bounds__(k3d::kThreads, 1)
             const int bj = lane < 16 ? s_bj[m] : -1;
             if (bj >= 0) {
                 const size_t tok = (size_t)(bj >> 16) * n + (bj & 0xFFFF);
-                __nv_bfloat16* dst =
-                    reinterpret_cast<__nv_bfloat16*>(a.h_out) + tok * (size_t)heads * kDh + (size_t)h * kDh;
+                __half* dst = reinterpret_cast<__half*>(a.h_out) + tok * (size_t)heads * kDh + (size_t)h * kDh;
 #pragma unroll
                 for (int g = 0; g < 8; ++g) {
                     uint32_t pk[4];
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
                         const int c = g * 8 + 2 * q;
-                        pk[q] = pack_bf16x2(__uint_as_float(v[c >> 5][c & 31]),
-                                            __uint_as_float(v[(c + 1) >> 5][(c + 1) & 31]));
+                        pk[q] = pack_f16x2(__uint_as_float(v[c >> 5][c & 31]),
+                                           __uint_as_float(v[(c + 1) >> 5][(c + 1) & 31]));
                     }
                     reinterpret_cast<uint4*>(dst)[g] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
                 }

@@ -16,7 +16,8 @@ constexpr int kT4 = 256;
 
 template <class T>
 __global__ void __launch_bounds__(kT4) k4_apply_simt(const T* __restrict__ q, const T* __restrict__ k,
-                                                     const T* __restrict__ hmat, const float* __restrict__ lse,
+                                                     const typename HType<T>::type* __restrict__ hmat,
+                                                     const float* __restrict__ lse,
                                                      int n, int heads, float scale, T* __restrict__ y) {
     __shared__ float qs[kQT4][kDh + 1];
     __shared__ float ks[kKT4][kDh + 1];
@@ -30,7 +31,7 @@ __global__ void __launch_bounds__(kT4) k4_apply_simt(const T* __restrict__ q, co
     const size_t HD = (size_t)heads * kDh;
     const T* qb = q + (size_t)b * n * HD + (size_t)h * kDh;
     const T* kb = k + (size_t)b * n * HD + (size_t)h * kDh;
-    const T* hb = hmat + (size_t)b * n * HD + (size_t)h * kDh;
+    const typename HType<T>::type* hb = hmat + (size_t)b * n * HD + (size_t)h * kDh;
 
     for (int e = tid; e < kQT4 * kDh; e += kT4) {
         const int rr = e / kDh, c = e % kDh;
@@ -73,8 +74,7 @@ __global__ void __launch_bounds__(kT4) k4_apply_simt(const T* __restrict__ q, co
 
 template __global__ void k4_apply_simt<float>(const float*, const float*, const float*, const float*, int, int, float,
                                               float*);
-template __global__ void k4_apply_simt<__nv_bfloat16>(const __nv_bfloat16*, const __nv_bfloat16*,
-                                                      const __nv_bfloat16*, const float*, int, int, float,
-                                                      __nv_bfloat16*);
+template __global__ void k4_apply_simt<__nv_bfloat16>(const __nv_bfloat16*, const __nv_bfloat16*, const __half*,
+                                                      const float*, int, int, float, __nv_bfloat16*);
 
 }  // namespace mca_dev

@@ -3,11 +3,12 @@
 //
 // A is never materialised. Per 64-key block:
 //   S  = Q K_blk^T                  tcgen05.mma M=128 N=64 K=64 -> TMEM (fp32)
-//   P  = exp(scale*S - lse)         8 softmax warps, 2 per TMEM lane quadrant
+//   P  = 2^(log2e (scale*S - lse))  8 softmax warps, 2 per TMEM lane quadrant
 //                                   (lane = query row), 32 keys each; lse from
-//                                   K1, so no online rescaling; P written bf16
-//                                   into a 128B-swizzled K-major smem tile
-//   O += P H~_blk                   tcgen05.mma M=128 N=64 K=64 (H~ MN-major)
+//                                   K1, so no online rescaling; two exponentials
+//                                   per MUFU op (ex2.approx.f16x2), P written
+//                                   fp16 into a 128B-swizzled K-major smem tile
+//   O += P H~_blk                   tcgen05.mma kind::f16, fp16 x fp16, M=128 N=64 K=64 (H~ MN-major)
 // Warp roles (320 threads): warp 0 TMA producer (Q once, then a 3-stage ring of
 // K/H~ blocks), warp 1 TMEM allocator + single-thread MMA issuer, warps 2-9
 // softmax + epilogue. S is double-buffered in TMEM and P in smem, so the tensor core computes S(kb+1) while the softmax warps exponentiate S(kb), and
@@ -34,7 +35,7 @@ constexpr uint32_t kSmemBar = kSmemP + 2 * kPBytes;
 constexpr uint32_t kSmemBytes = kSmemBar + 256 + 1024;               // + alignment slack
 constexpr uint32_t kIdescS = mca_tc::idesc_f16(1, 0, kBM, kBK);      // bf16, B K-major
 constexpr uint32_t kOCol = 2 * kBK;                                 // TMEM: S0 [0,64), S1 [64,128), O [128,192)
-constexpr uint32_t kIdescO = mca_tc::idesc_f16(1, 1, kBM, kDh);      // bf16, B MN-major
+constexpr uint32_t kIdescO = mca_tc::idesc_f16(0, 1, kBM, kDh);      // fp16 P x fp16 H~, B MN-major
 }  // namespace k4tc
 
 __global__ void __launch_bounds__(k4tc::kThreads, 2)
@@ -162,11 +163,13 @@ __global__ void __launch_bounds__(k4tc::kThreads, 2)
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
                     const int col = ch * 8 + 2 * e;
-                    float p0 = ex2_approx(__fmaf_rn(__uint_as_float(sv[col]), c, -lse2));
-                    float p1 = ex2_approx(__fmaf_rn(__uint_as_float(sv[col + 1]), c, -lse2));
-                    if (col >= valid) p0 = 0.0f;
-                    if (col + 1 >= valid) p1 = 0.0f;
-                    pk[e] = pack_bf16x2(p0, p1);
+                    // exponent in fp32, 2^x of the pair in one fp16x2 MUFU op; keys past n
+                    // get -inf (2^-inf = 0)
+                    float x0 = __fmaf_rn(__uint_as_float(sv[col]), c, -lse2);
+                    float x1 = __fmaf_rn(__uint_as_float(sv[col + 1]), c, -lse2);
+                    if (col >= valid) x0 = -INFINITY;
+                    if (col + 1 >= valid) x1 = -INFINITY;
+                    pk[e] = ex2_f16x2(pack_f16x2(x0, x1));
                 }
                 *reinterpret_cast<uint4*>(pt + sw128_offset(row, (half * 4 + ch) * 16)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
             }

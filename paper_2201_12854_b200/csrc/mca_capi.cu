@@ -89,14 +89,14 @@ PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
 // 3-D bf16 view [batch][rows][inner] with a {64, box_rows, 1} box and 128-byte
 // swizzle: the UMMA operand layout of tc_common.cuh. Rows past `rows` read as 0.
 bool make_tmap_bf16(CUtensorMap* m, const void* base, uint64_t inner, uint64_t rows, uint64_t batch,
-                    uint32_t box_rows) {
+                    uint32_t box_rows, CUtensorMapDataType type = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16) {
     auto enc = tmap_encoder();
     if (!enc) return false;
     cuuint64_t dims[3] = {inner, rows, batch};
     cuuint64_t strides[2] = {inner * 2, rows * inner * 2};
     cuuint32_t box[3] = {64, box_rows, 1};
     cuuint32_t estr[3] = {1, 1, 1};
-    return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+    return enc(m, type, 3, const_cast<void*>(base), dims, strides, box, estr,
                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
@@ -578,13 +578,13 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
                                                             w->lse, n, H, (float)scale, (float*)y);
         else if (force_simt())
             k4_apply_simt<__nv_bfloat16><<<grid, kT4, 0, stream>>>(
-                (const __nv_bfloat16*)q, (const __nv_bfloat16*)k, (const __nv_bfloat16*)w->hbuf, w->lse, n, H,
+                (const __nv_bfloat16*)q, (const __nv_bfloat16*)k, (const __half*)w->hbuf, w->lse, n, H,
                 (float)scale, (__nv_bfloat16*)y);
         else {
             CUtensorMap tq, tk, th;
             if (!make_tmap_bf16(&tq, q, (uint64_t)H * kDh, n, B, 128) ||
                 !make_tmap_bf16(&tk, k, (uint64_t)H * kDh, n, B, k4tc::kBK) ||
-                !make_tmap_bf16(&th, w->hbuf, (uint64_t)H * kDh, n, B, k4tc::kBK))
+                !make_tmap_bf16(&th, w->hbuf, (uint64_t)H * kDh, n, B, k4tc::kBK, CU_TENSOR_MAP_DATA_TYPE_FLOAT16))
                 return fail(MCA_ERR_CUDA, "cuTensorMapEncodeTiled failed for q/k/h");
             static bool attr = false;
             if (!attr) {

@@ -6,6 +6,7 @@
 #pragma once
 
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -126,6 +127,38 @@ __device__ __forceinline__ void store8(__nv_bfloat16* p, const float v[8]) {
     u.x = w[0]; u.y = w[1]; u.z = w[2]; u.w = w[3];
     *reinterpret_cast<uint4*>(p) = u;
 }
+__device__ __forceinline__ void store8(__half* p, const float v[8]) {
+    uint4 u;
+    uint32_t w[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const __half2 h = __floats2half2_rn(v[2 * i], v[2 * i + 1]);
+        w[i] = *reinterpret_cast<const uint32_t*>(&h);
+    }
+    u.x = w[0]; u.y = w[1]; u.z = w[2]; u.w = w[3];
+    *reinterpret_cast<uint4*>(p) = u;
+}
+__device__ __forceinline__ void load8(const __half* p, float v[8]) {
+    const uint4 u = *reinterpret_cast<const uint4*>(p);
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[i]));
+        v[2 * i] = f.x;
+        v[2 * i + 1] = f.y;
+    }
+}
+template <>
+__device__ __forceinline__ float to_f32<__half>(__half v) { return __half2float(v); }
+
+// H~ (the encodings) is fp32 on the fp32 path and fp16 on the bf16 path: fp16
+// has 3 more mantissa bits than bf16 and feeds K4's fp16 x fp16 tensor-core
+// P.H~ product, whose P comes straight out of ex2.approx.f16x2.
+template <class T>
+struct HType { using type = float; };
+template <>
+struct HType<__nv_bfloat16> { using type = __half; };
+
 __device__ __forceinline__ void store8(float* p, const float v[8]) {
     reinterpret_cast<float4*>(p)[0] = make_float4(v[0], v[1], v[2], v[3]);
     reinterpret_cast<float4*>(p)[1] = make_float4(v[4], v[5], v[6], v[7]);

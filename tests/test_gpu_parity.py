@@ -230,7 +230,8 @@ def test_c1_flops_counters(c1_f32):
 def test_bf16_parity(mca, syn, orc, B, n):
     H, d_in = 12, 768
     weights, w, q, k, x = _setup(mca, syn, B, n, d_in, H, torch.bfloat16, seed=7)
-    dbg = dict(cmax_out=torch.zeros((B, H, n), dtype=torch.float64, device="cuda"), h_out=torch.zeros_like(q),
+    dbg = dict(cmax_out=torch.zeros((B, H, n), dtype=torch.float64, device="cuda"),
+               h_out=torch.zeros_like(q, dtype=torch.float16),           # H~ is fp16 on the bf16 path
                draws_out=torch.zeros((B, H, n, 64), dtype=torch.int32, device="cuda"), draws_stride=64)
     out = mca.mca_forward(weights, q, k, x, mca.McaConfig(alpha=0.4), seed=42, return_plan=True, flops=True,
                           debug=dbg)
