@@ -9,10 +9,11 @@
 //                                   per MUFU op (ex2.approx.f16x2), P written
 //                                   fp16 into a 128B-swizzled K-major smem tile
 //   O += P H~_blk                   tcgen05.mma kind::f16, fp16 x fp16, M=128 N=64 K=64 (H~ MN-major)
-// Warp roles (320 threads): warp 0 TMA producer (Q once, then a 3-stage ring of
-// K/H~ blocks), warp 1 TMEM allocator + single-thread MMA issuer, warps 2-9
-// softmax + epilogue. S is double-buffered in TMEM and P in smem, so the tensor core computes S(kb+1) while the softmax warps exponentiate S(kb), and
-// P(kb) . H~(kb) overlaps the exponentials of block kb+1. 64-key blocks keep
+// Warp roles (320 threads): warp 0 TMA producers (lane 0: Q once, then a K ring
+// released as soon as S is computed; lane 16: an H~ ring released after P.H~), warp 1 TMEM allocator + single-thread MMA issuer, warps 2-9
+// softmax + epilogue. S is double-buffered in TMEM and P in smem; the issuer
+// keeps S two blocks ahead (S(kb+2) is issued right after P(kb).H~(kb)), so the
+// softmax warps always find the next S ready. 64-key blocks keep
 // shared memory at ~98 KB and TMEM at 256 columns (S0 [0,64), S1 [64,128),
 // O [128,192)), so two CTAs run per SM and hide each other's prologue.
 #include "mca_common.cuh"
@@ -21,7 +22,7 @@
 namespace mca_dev {
 
 namespace k4tc {
-constexpr int kBM = 128, kBK = 64, kStages = 3;
+constexpr int kBM = 128, kBK = 64, kStages = 3;   // separate K and H~ rings of kStages each (2 CTAs/SM fit)
 constexpr int kConsumers = 8;                        // 2 warps per TMEM lane quadrant
 constexpr int kThreads = 64 + kConsumers * 32;
 constexpr uint32_t kQBytes = kBM * kDh * 2;         // 16 KB: Q tile (128 x 64 bf16)
@@ -48,9 +49,11 @@ __global__ void __launch_bounds__(k4tc::kThreads, 2)
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kSmemBar);
     uint64_t* q_full = bars + 0;
-    uint64_t* kv_full = bars + 1;              // [kStages]
-    uint64_t* kv_empty = bars + 1 + kStages;   // [kStages]
-    uint64_t* s_full = bars + 1 + 2 * kStages; // [2]
+    uint64_t* k_full = bars + 1;               // [kStages]  K ring: freed when S(kb) completes
+    uint64_t* k_empty = k_full + kStages;      // [kStages]
+    uint64_t* h_full = k_empty + kStages;      // [kStages]  H~ ring: freed when P(kb).H~(kb) completes
+    uint64_t* h_empty = h_full + kStages;      // [kStages]
+    uint64_t* s_full = h_empty + kStages;      // [2]
     uint64_t* s_empty = s_full + 2;            // [2]
     uint64_t* p_full = s_full + 4;             // [2]
     uint64_t* p_empty = s_full + 6;            // [2]
@@ -64,8 +67,10 @@ __global__ void __launch_bounds__(k4tc::kThreads, 2)
     if (threadIdx.x == 0) {
         mbar_init(q_full, 1);
         for (int s = 0; s < kStages; ++s) {
-            mbar_init(kv_full + s, 1);
-            mbar_init(kv_empty + s, 1);
+            mbar_init(k_full + s, 1);
+            mbar_init(k_empty + s, 1);
+            mbar_init(h_full + s, 1);
+            mbar_init(h_empty + s, 1);
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(s_full + i, 1);
@@ -83,18 +88,24 @@ __global__ void __launch_bounds__(k4tc::kThreads, 2)
     const uint32_t tmem = *tmem_slot;
 
     if (warp == 0) {
-        if (lane == 0) {  // ---------------- TMA producer
+        if (lane == 0) {  // ---------------- TMA producer: Q, then the K ring
             tma_prefetch(&tm_q);
             tma_prefetch(&tm_k);
-            tma_prefetch(&tm_h);
             mbar_expect_tx(q_full, kQBytes);
             tma_load_3d(smem + kSmemQ, &tm_q, q_full, h * kDh, m0, b);
             for (int kb = 0; kb < nkb; ++kb) {
                 const int s = kb % kStages;
-                mbar_wait(kv_empty + s, ((kb / kStages) & 1) ^ 1);
-                mbar_expect_tx(kv_full + s, 2 * kTileBytes);
-                tma_load_3d(smem + kSmemK + s * kTileBytes, &tm_k, kv_full + s, h * kDh, kb * kBK, b);
-                tma_load_3d(smem + kSmemH + s * kTileBytes, &tm_h, kv_full + s, h * kDh, kb * kBK, b);
+                mbar_wait(k_empty + s, ((kb / kStages) & 1) ^ 1);
+                mbar_expect_tx(k_full + s, kTileBytes);
+                tma_load_3d(smem + kSmemK + s * kTileBytes, &tm_k, k_full + s, h * kDh, kb * kBK, b);
+            }
+        } else if (lane == 16) {  // ---------------- TMA producer: the H~ ring
+            tma_prefetch(&tm_h);
+            for (int kb = 0; kb < nkb; ++kb) {
+                const int s = kb % kStages;
+                mbar_wait(h_empty + s, ((kb / kStages) & 1) ^ 1);
+                mbar_expect_tx(h_full + s, kTileBytes);
+                tma_load_3d(smem + kSmemH + s * kTileBytes, &tm_h, h_full + s, h * kDh, kb * kBK, b);
             }
         }
     } else if (warp == 1) {
@@ -102,6 +113,7 @@ __global__ void __launch_bounds__(k4tc::kThreads, 2)
             const uint32_t q_addr = smem_u32(smem + kSmemQ);
             auto issue_pv = [&](int j) {
                 const int pb = j & 1, s = j % kStages;
+                mbar_wait(h_full + s, (j / kStages) & 1);
                 mbar_wait(p_full + pb, (j >> 1) & 1);
                 tc_fence_after();
                 const uint32_t p_addr = smem_u32(smem + kSmemP + pb * kPBytes);
@@ -113,12 +125,13 @@ __global__ void __launch_bounds__(k4tc::kThreads, 2)
                     umma_f16(tmem + kOCol, ad, bd, kIdescO, (j > 0 || kk > 0) ? 1u : 0u);
                 }
                 umma_commit(p_empty + pb);
-                umma_commit(kv_empty + s);
+                umma_commit(h_empty + s);
             };
-            mbar_wait(q_full, 0);
-            for (int kb = 0; kb < nkb; ++kb) {
+            // S runs two blocks ahead of P.H~ (as deep as the double-buffered S allows):
+            // while the softmax warps exponentiate S(kb+1), S(kb+2) is already computing.
+            auto issue_s = [&](int kb) {
                 const int s = kb % kStages, sb = kb & 1;
-                mbar_wait(kv_full + s, (kb / kStages) & 1);
+                mbar_wait(k_full + s, (kb / kStages) & 1);
                 mbar_wait(s_empty + sb, ((kb >> 1) & 1) ^ 1);
                 tc_fence_after();
                 const uint32_t k_addr = smem_u32(smem + kSmemK + s * kTileBytes);
@@ -129,9 +142,15 @@ __global__ void __launch_bounds__(k4tc::kThreads, 2)
                     umma_f16(tmem + sb * kBK, ad, bd, kIdescS, kk > 0 ? 1u : 0u);
                 }
                 umma_commit(s_full + sb);
-                if (kb > 0) issue_pv(kb - 1);
+                umma_commit(k_empty + s);
+            };
+            mbar_wait(q_full, 0);
+            issue_s(0);
+            if (nkb > 1) issue_s(1);
+            for (int kb = 0; kb < nkb; ++kb) {
+                issue_pv(kb);
+                if (kb + 2 < nkb) issue_s(kb + 2);
             }
-            issue_pv(nkb - 1);
             umma_commit(o_full);
         }
     } else {  // ------------------------------- softmax + epilogue (warps 2..9)

@@ -592,7 +592,7 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
                                                   (int)k4tc::kSmemBytes));
                 attr = true;
             }
-            k4_apply_tc<<<dim3((n + 127) / 128, H, B), k4tc::kThreads, k4tc::kSmemBytes, stream>>>(
+            k4_apply_tc<<<dim3((n + k4tc::kBM - 1) / k4tc::kBM, H, B), k4tc::kThreads, k4tc::kSmemBytes, stream>>>(
                 tq, tk, th, w->lse, n, H, (float)scale, (__nv_bfloat16*)y);
         }
         MCA_LAUNCH_CHECK("k4_apply");

@@ -41,19 +41,20 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
     uint32_t ok;
     asm volatile(
         "{\n\t.reg .pred P1;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
         "selp.b32 %0, 1, 0, P1;\n\t}"
         : "=r"(ok)
-        : "r"(smem_u32(bar)), "r"(parity), "r"(1000000)
+        : "r"(smem_u32(bar)), "r"(parity)
         : "memory");
     return ok != 0;
 }
 // Blocks until the phase with the given parity completed. A pipeline bug must
-// not hang the GPU: after ~20 s of failed waits the kernel traps (error, not hang).
+// not hang the GPU: after ~2^28 failed waits (each a hardware-timed try_wait,
+// far beyond any legitimate wait) the kernel traps (an error, not a hang).
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     if (mbar_try_wait(bar, parity)) return;
     for (uint32_t it = 0; !mbar_try_wait(bar, parity); ++it)
-        if (it > 20000) __trap();
+        if (it > (1u << 28)) __trap();
 }
 
 // ---------------------------------------------------------------------- TMA
