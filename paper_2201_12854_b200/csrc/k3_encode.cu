@@ -52,6 +52,7 @@ struct K3Args {
     uint32_t layer;
     uint64_t seed;
     const int32_t* budgets;    // [B, H, n]
+    const uint8_t* exact;      // [B, H, n]
     const uint64_t* thr;       // [H, d_in]
     const uint16_t* guide;     // [H, kGuide]
     const double* probs;       // [H, d_in]
@@ -64,6 +65,7 @@ struct K3Args {
     const int32_t* exact_list; // [H, tokens]
     const int* counts;         // [H, 2]: sampled, exact
     int* task_cursor;          // [H]
+    long long* prof;           // optional phase clocks (MCA_K3_PROF=1, diagnostics only)
 };
 
 constexpr int kK3Warps = 32;                          // 1024 threads: one CTA per SM holds W_h once

@@ -26,7 +26,7 @@
 #include "k2_budgets.cu"
 #include "k3_encode.cu"
 #include "k3b_exact_tc.cu"
-#include "k3d_encode_dense.cu"
+#include "k3t_encode_tc.cu"
 #include "k4_apply_simt.cu"
 #include "k4_apply_tc.cu"
 
@@ -101,14 +101,14 @@ bool make_tmap_bf16(CUtensorMap* m, const void* base, uint64_t inner, uint64_t r
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// MCA_K3_DENSE=1 selects the densified tensor-core encoder (k3d) for bf16;
-// the default is the gather-scale-accumulate encoder (measured faster at
-// BERT shapes).
-bool gather_only() {
+// MCA_K3_TILE=1 selects the tile-GEMM encoder (k3t) on the bf16 path; the
+// default there is the gather-scale-accumulate encoder + exact tensor-core
+// kernel (measured faster at BERT shapes).
+bool tile_k3_requested() {
     static int v = -1;
     if (v < 0) {
-        const char* e = getenv("MCA_K3_DENSE");
-        v = (e && e[0] == '1') ? 0 : 1;
+        const char* e = getenv("MCA_K3_TILE");
+        v = (e && e[0] == '1') ? 1 : 0;
     }
     return v == 1;
 }
@@ -134,6 +134,8 @@ struct mca_weights {
     uint64_t* thr = nullptr;      // [heads, d_in]
     float* invp = nullptr;        // [heads, d_in]
     uint16_t* guide = nullptr;    // [heads, kGuide]
+    void* wprime = nullptr;       // bf16 path: [d_in, heads*dh] W_h / p (k3t's B operand)
+    void* pbf = nullptr;          // bf16 path: [heads, d_in] bf16 p
     // workspace (grown on demand)
     long cap_tokens = 0;          // capacity in B*n tokens
     float* lse = nullptr;                     // [B, H, n]
@@ -217,6 +219,12 @@ mca_status check_config(const mca_config* cfg, bool need_alpha) {
     return MCA_OK;
 }
 
+// bf16 path: K3 as a tile GEMM (k3t) when its shared-memory plan fits.
+bool use_k3t(const mca_weights* w) {
+    return w->wdt == MCA_BF16 && w->wprime && !force_simt() && tile_k3_requested() && w->d_in % 8 == 0 &&
+           k3t::layout(w->d_in).bytes <= 227u * 1024u;
+}
+
 template <class T, class Acc>
 mca_status launch_k3(mca_weights* w, const void* x, int B, int n, long b_offset, uint32_t layer, uint64_t seed,
                      void* hout, int32_t* draws, int draws_stride, mca_stream_t stream, int& launches) {
@@ -232,6 +240,7 @@ mca_status launch_k3(mca_weights* w, const void* x, int B, int n, long b_offset,
     a.layer = layer;
     a.seed = seed;
     a.budgets = w->budgets;
+    a.exact = w->exact;
     a.thr = w->thr;
     a.guide = w->guide;
     a.probs = w->probs;
@@ -246,19 +255,44 @@ mca_status launch_k3(mca_weights* w, const void* x, int B, int n, long b_offset,
     a.task_cursor = w->task_cursor;
     // W_h staged in smem as fp32 when it fits (no unpacking in the hot loop),
     // else as bf16, else read from global memory (L1/L2).
-    if (sizeof(T) == 2 && !force_simt() && !gather_only() && k3d::smem_bytes(w->d_in) <= 227 * 1024) {
-        // bf16: densified sampled encoding on the tensor cores (persistent, W_h resident)
+    if (sizeof(T) == 2 && use_k3t(w)) {
+        // bf16: every token-head (sampled and exact) as one tile GEMM per head
         CUtensorMap tw;
-        if (!make_tmap_bf16(&tw, w->w, (uint64_t)w->heads * kDh, w->d_in, 1, 64))
-            return fail(MCA_ERR_CUDA, "cuTensorMapEncodeTiled failed for w_v");
-        const uint32_t smem = k3d::smem_bytes(w->d_in);
-        MCA_CUDA_TRY(cudaFuncSetAttribute(k3d_encode_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        if (!make_tmap_bf16(&tw, w->wprime, (uint64_t)w->heads * kDh, w->d_in, 1, 64))
+            return fail(MCA_ERR_CUDA, "cuTensorMapEncodeTiled failed for W'");
+        const uint32_t smem = k3t::layout(w->d_in).bytes;
+        MCA_CUDA_TRY(cudaFuncSetAttribute(k3t_encode_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         int G = sm_count() / w->heads;
-        const long cap = (a.tokens + k3d::kBM - 1) / k3d::kBM;
+        const long cap = (long)B * ((n + k3t::kBM - 1) / k3t::kBM);
         if (G > cap) G = (int)cap;
         if (G < 1) G = 1;
-        k3d_encode_dense<<<dim3(G, w->heads), k3d::kThreads, smem, stream>>>(a, tw);
-        MCA_LAUNCH_CHECK("k3d_encode_dense");
+        static const bool prof = kK3tProf && getenv("MCA_K3_PROF") != nullptr;   // diagnostics: phase clocks
+        long long* pbuf = nullptr;
+        if (prof) {
+            MCA_CUDA_TRY(cudaMalloc(&pbuf, 64 * 8 * sizeof(long long)));
+            MCA_CUDA_TRY(cudaMemsetAsync(pbuf, 0, 64 * 8 * sizeof(long long), stream));
+            a.prof = pbuf;
+        }
+        k3t_encode_tc<<<dim3(G, w->heads), k3t::kThreads, smem, stream>>>(a, tw,
+                                                                           (const __nv_bfloat16*)w->pbf);
+        MCA_LAUNCH_CHECK("k3t_encode_tc");
+        if (prof) {
+            long long hbuf[64 * 8];
+            MCA_CUDA_TRY(cudaMemcpyAsync(hbuf, pbuf, sizeof(hbuf), cudaMemcpyDeviceToHost, stream));
+            MCA_CUDA_TRY(cudaStreamSynchronize(stream));
+            cudaFree(pbuf);
+            double acc[7] = {};
+            int nt = 0;
+            for (int i = 1; i < 64 && hbuf[i * 8]; ++i, ++nt) {
+                for (int k = 0; k < 6; ++k) acc[k] += (double)(hbuf[i * 8 + k + 1] - hbuf[i * 8 + k]);
+                if (i + 1 < 64 && hbuf[(i + 1) * 8]) acc[6] += (double)(hbuf[(i + 1) * 8] - hbuf[i * 8]);
+            }
+            if (nt)
+                fprintf(stderr, "k3t CTA0 mean cycles/tile over %d tiles: predraw %.0f xload+setup+afree %.0f zero %.0f count %.0f "
+                                "convert %.0f epi %.0f | tile %.0f\n", nt, acc[0] / nt, acc[1] / nt, acc[2] / nt,
+                        acc[3] / nt, acc[4] / nt, acc[5] / nt, acc[6] / (nt > 1 ? nt - 1 : 1));
+        }
+        return MCA_OK;
     } else {
     // Gather-scale-accumulate: W_h staged as bf16 (one 128-byte smem wavefront
     // per sample; smem bandwidth, not issue, bounds this loop) / fp32 for the
@@ -363,6 +397,14 @@ mca_status mca_prepare_weights(const void* w_v, mca_dtype wdt, int d_in, int hea
     if (wdt == MCA_F32) k0_row_sq<float><<<g0, 256, 0, stream>>>((const float*)w->w, d_in, heads, sq);
     else k0_row_sq<__nv_bfloat16><<<g0, 256, 0, stream>>>((const __nv_bfloat16*)w->w, d_in, heads, sq);
     k0_dist<<<heads, 256, 0, stream>>>(sq, d_in, w->probs, w->cdf, w->thr, w->invp, w->guide, status);
+    if (wdt == MCA_BF16) {   // k3t's operands: W' = W_h / p and bf16 p
+        if (cudaMalloc(&w->wprime, wbytes) != cudaSuccess || cudaMalloc(&w->pbf, hd * 2) != cudaSuccess) {
+            cudaGetLastError();
+            return cleanup(fail(MCA_ERR_ALLOC, "W' allocation failed"));
+        }
+        k0_wprime<<<2 * sm_count(), 256, 0, stream>>>((const __nv_bfloat16*)w->w, w->probs, d_in, heads,
+                                                       (__nv_bfloat16*)w->wprime, (__nv_bfloat16*)w->pbf);
+    }
     std::vector<int> hs(heads);
     if (cudaMemcpyAsync(hs.data(), status, heads * sizeof(int), cudaMemcpyDeviceToHost, stream) != cudaSuccess ||
         cudaStreamSynchronize(stream) != cudaSuccess)
@@ -382,6 +424,8 @@ void mca_weights_free(mca_weights* w) {
     cudaFree(w->thr);
     cudaFree(w->invp);
     cudaFree(w->guide);
+    cudaFree(w->wprime);
+    cudaFree(w->pbf);
     cudaFree(w->counters);
     cudaFree(w->hist);
     cudaFree(w->cursor);
@@ -483,8 +527,11 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
     if (dt == MCA_F32 || force_simt() || n > k1tc::kMaxN)   // atomicMax column keys (the TC pass writes each once)
         MCA_CUDA_TRY(cudaMemsetAsync(w->colkey, 0, th * sizeof(unsigned long long), stream));
     MCA_CUDA_TRY(cudaMemsetAsync(w->counters, 0, 8 * sizeof(unsigned long long), stream));
-    MCA_CUDA_TRY(cudaMemsetAsync(w->hist, 0, (size_t)H * (w->d_in + 1) * 4, stream));
-    MCA_CUDA_TRY(cudaMemsetAsync(w->task_cursor, 0, H * sizeof(int), stream));
+    const bool tile_k3 = dt == MCA_BF16 && use_k3t(w);   // k3t reads budgets directly: no work lists
+    if (!tile_k3) {
+        MCA_CUDA_TRY(cudaMemsetAsync(w->hist, 0, (size_t)H * (w->d_in + 1) * 4, stream));
+        MCA_CUDA_TRY(cudaMemsetAsync(w->task_cursor, 0, H * sizeof(int), stream));
+    }
 
     // K1: row statistics + column maxima
     {
@@ -546,16 +593,18 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
         a.exact = w->exact;
         a.cmax_out = dbg ? dbg->cmax_out : nullptr;
         a.counters = w->counters;
-        a.hist = w->hist;
+        a.hist = tile_k3 ? nullptr : w->hist;
         if (a.cmax_in) k2_budgets<kGivenCmax, float><<<grid, 256, 0, stream>>>(a);
         else if (dt == MCA_F32) k2_budgets<kKeyValue, float><<<grid, 256, 0, stream>>>(a);
         else k2_budgets<kKeyArgmax, __nv_bfloat16><<<grid, 256, 0, stream>>>(a);
         MCA_LAUNCH_CHECK("k2_budgets");
-        k2_scan<<<H, 1024, 0, stream>>>(w->hist, w->d_in, w->cursor, w->counts);
-        MCA_LAUNCH_CHECK("k2_scan");
-        k2_scatter<<<grid, 256, 0, stream>>>(w->budgets, w->exact, n, H, w->d_in, tokens, w->cursor, w->samp_list,
-                                             w->exact_list);
-        MCA_LAUNCH_CHECK("k2_scatter");
+        if (!tile_k3) {
+            k2_scan<<<H, 1024, 0, stream>>>(w->hist, w->d_in, w->cursor, w->counts);
+            MCA_LAUNCH_CHECK("k2_scan");
+            k2_scatter<<<grid, 256, 0, stream>>>(w->budgets, w->exact, n, H, w->d_in, tokens, w->cursor,
+                                                 w->samp_list, w->exact_list);
+            MCA_LAUNCH_CHECK("k2_scatter");
+        }
     }
     if (w->timing) MCA_CUDA_TRY(cudaEventRecord(w->ev[2], stream));
     // K3: encoding

@@ -226,9 +226,12 @@ def test_c1_flops_counters(c1_f32):
 
 
 # ----------------------------------------------------------- bf16 parity
-@pytest.mark.parametrize("B,n", [(2, 128), (1, 512), (1, 77), (1, 640), (2, 200)])
-def test_bf16_parity(mca, syn, orc, B, n):
-    H, d_in = 12, 768
+@pytest.mark.parametrize("B,n,H,d_in", [(2, 128, 12, 768), (1, 512, 12, 768), (1, 77, 12, 768), (1, 640, 12, 768),
+                                        (2, 200, 12, 768), (1, 130, 16, 1024), (1, 96, 4, 200)])
+def test_bf16_parity(mca, syn, orc, B, n, H, d_in):
+    """bf16 path end to end. d_in = 768 runs the tile-GEMM encoder (k3t);
+    BERT-large's d_in = 1024 does not fit its shared-memory plan and runs the
+    gather encoder + exact tensor-core kernel; d_in = 200 pads the K chunks."""
     weights, w, q, k, x = _setup(mca, syn, B, n, d_in, H, torch.bfloat16, seed=7)
     dbg = dict(cmax_out=torch.zeros((B, H, n), dtype=torch.float64, device="cuda"),
                h_out=torch.zeros_like(q, dtype=torch.float16),           # H~ is fp16 on the bf16 path
@@ -369,3 +372,18 @@ def test_c2_full_size_properties(mca, syn, orc):
         ref = orc.batched_forward(_np(q[sl]), _np(k[sl]), _np(x[sl]), _np(w), heads=H, alpha=0.4, seed=42,
                                   b_offset=s, budgets_override=b[sl], exact_override=e[sl])
         assert _row_rel(_np(out.y[sl]), ref.y) <= TOL_Y[torch.bfloat16]
+
+
+def test_bf16_tile_encoder_parity_subprocess():
+    """The opt-in tile-GEMM encoder (k3t, MCA_K3_TILE=1; the switch is read once
+    per process) passes the bf16 parity cases and the golden draws."""
+    import subprocess
+    import sys
+    if os.environ.get("MCA_K3_TILE") == "1":
+        pytest.skip("already running with the tile encoder")
+    env = dict(os.environ, MCA_K3_TILE="1")
+    here = os.path.dirname(os.path.abspath(__file__))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider", "-m", "gpu",
+                        os.path.join(here, "test_gpu_parity.py"), "-k", "bf16_parity or golden_draws or determinism"],
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
