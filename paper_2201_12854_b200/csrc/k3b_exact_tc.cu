@@ -4,8 +4,9 @@
 // a full d_in x 64 dot product, so as CUDA-core work they rival the whole
 // sampled encoding; here they are one small GEMM per head over K2's exact list.
 //
-// CTA = (tile of 128 listed tokens, head h); grid.x covers the worst case and
-// CTAs past the head's exact count exit at once (the count is device-side).
+// Grid (G, heads), persistent: CTA x of head h walks the head's tiles of 128
+// listed tokens x, x + G, ... (the exact count is device-side, so the host
+// sizes G for one wave and idle CTAs exit at once).
 //   A = X rows of the 128 listed tokens  [128 x d_in], K-major, gathered with
 //       16-byte cp.async into 128B-swizzled K chunks of 64
 //   B = W_h                              [d_in x 64], MN-major chunks of 64 rows
@@ -41,9 +42,9 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 __global__ void __launch_bounds__(k3btc::kThreads, 2) k3b_exact_tc(K3Args a) {
     using namespace k3btc;
     using namespace mca_tc;
-    const int h = blockIdx.y, tile = blockIdx.x;
+    const int h = blockIdx.y;
     const int ne = a.counts[2 * h + 1];
-    if (tile * kBM >= ne) return;                      // uniform early exit, before any barrier / TMEM use
+    if ((int)blockIdx.x * kBM >= ne) return;           // uniform early exit, before any barrier / TMEM use
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kSmemBar);
@@ -70,90 +71,103 @@ __global__ void __launch_bounds__(k3btc::kThreads, 2) k3b_exact_tc(K3Args a) {
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
-    if (warp < 4) {
-        // ---------------- producers: thread t owns A row t (one token) and 4 16-byte pieces of B
-        const int t = threadIdx.x;
-        const int idx = tile * kBM + t;
-        const int bj = idx < ne ? a.exact_list[(size_t)h * a.tokens + idx] : -1;   // (b << 16) | j
-        const size_t tok = bj < 0 ? 0 : (size_t)(bj >> 16) * n + (bj & 0xFFFF);
-        const __nv_bfloat16* xrow = reinterpret_cast<const __nv_bfloat16*>(a.x) + tok * d_in;
-        const __nv_bfloat16* wh = reinterpret_cast<const __nv_bfloat16*>(a.wv) + (size_t)h * kDh;
-        auto issue = [&](int c) {
-            const int s = c % kStages;
-            const uint32_t sa = smem_u32(smem + s * kStageBytes);
-            const uint32_t sb = sa + kABytes;
-            const int k0 = c * kBK;
+    int it = 0;
+    for (int tile = blockIdx.x; tile * kBM < ne; tile += gridDim.x, ++it) {
+        const int g0 = it * nchunks;
+        if (warp < 4) {
+            // ---------------- producers: thread t owns A row t (one token) and 4 16-byte pieces of B
+            const int t = threadIdx.x;
+            const int idx = tile * kBM + t;
+            const int bj = idx < ne ? a.exact_list[(size_t)h * a.tokens + idx] : -1;   // (b << 16) | j
+            const size_t tok = bj < 0 ? 0 : (size_t)(bj >> 16) * n + (bj & 0xFFFF);
+            const __nv_bfloat16* xrow = reinterpret_cast<const __nv_bfloat16*>(a.x) + tok * d_in;
+            const __nv_bfloat16* wh = reinterpret_cast<const __nv_bfloat16*>(a.wv) + (size_t)h * kDh;
+            auto issue = [&](int c, int s) {
+                const uint32_t sa = smem_u32(smem + s * kStageBytes);
+                const uint32_t sb = sa + kABytes;
+                const int k0 = c * kBK;
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {          // A: 8 x 16 B of row t
-                const uint32_t dst = sa + sw128_offset(t, q * 16);
-                if (bj >= 0 && k0 + q * 8 + 8 <= d_in) cp_async16(dst, xrow + k0 + q * 8);
-                else cp_async_zero16(dst, a.wv);
-            }
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {          // B: 64 rows x 8 pieces; thread t takes 4
-                const int piece = t * 4 + q, r = piece >> 3, p8 = piece & 7;
-                const uint32_t dst = sb + sw128_offset(r, p8 * 16);
-                if (k0 + r < d_in) cp_async16(dst, wh + (size_t)(k0 + r) * HD + p8 * 8);
-                else cp_async_zero16(dst, a.wv);
-            }
-            cp_async_commit();
-        };
-        // prologue: kStages - 1 chunks in flight
-        for (int c = 0; c < kStages - 1; ++c)
-            if (c < nchunks) issue(c);
-            else cp_async_commit();
-        for (int c = 0; c < nchunks; ++c) {
-            const int cn = c + kStages - 1;
-            if (cn < nchunks) {
-                mbar_wait(empty + cn % kStages, ((cn / kStages) & 1) ^ 1);
-                issue(cn);
-            } else {
-                cp_async_commit();
-            }
-            cp_async_wait<kStages - 1>();          // chunk c has landed (this thread's copies)
-            fence_proxy_async_smem();               // make them visible to the tensor core (async proxy)
-            mbar_arrive(full + c % kStages);
-        }
-        // ---------------- epilogue: TMEM row t -> bf16 -> H~
-        mbar_wait(acc_full, 0);
-        tc_fence_after();
-        uint32_t v[2][32];
-        const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
-        tmem_ld32(lane_base, v[0]);
-        tmem_ld32(lane_base + 32, v[1]);
-        tmem_ld_wait();
-        if (bj >= 0) {
-            __half* dst = reinterpret_cast<__half*>(a.h_out) + tok * HD + (size_t)h * kDh;   // H~ is fp16
-#pragma unroll
-            for (int g = 0; g < 8; ++g) {
-                uint32_t pk[4];
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const int c = g * 8 + 2 * e;
-                    pk[e] = pack_f16x2(__uint_as_float(v[c >> 5][c & 31]), __uint_as_float(v[(c + 1) >> 5][(c + 1) & 31]));
+                for (int q = 0; q < 8; ++q) {          // A: 8 x 16 B of row t
+                    const uint32_t dst = sa + sw128_offset(t, q * 16);
+                    if (bj >= 0 && k0 + q * 8 + 8 <= d_in) cp_async16(dst, xrow + k0 + q * 8);
+                    else cp_async_zero16(dst, a.wv);
                 }
-                reinterpret_cast<uint4*>(dst)[g] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-            }
-            if (a.draws_out) {                     // exact token-heads draw nothing
-                const size_t tokh = ((size_t)(bj >> 16) * a.heads + h) * n + (bj & 0xFFFF);
-                for (int k = 0; k < a.draws_stride; ++k) a.draws_out[tokh * a.draws_stride + k] = -1;
-            }
-        }
-    } else if (lane == 0) {
-        // ---------------- MMA issuer
-        for (int c = 0; c < nchunks; ++c) {
-            const int s = c % kStages;
-            mbar_wait(full + s, (c / kStages) & 1);
-            tc_fence_after();
-            const uint32_t sa = smem_u32(smem + s * kStageBytes);
-            const uint32_t sb = sa + kABytes;
 #pragma unroll
-            for (int kk = 0; kk < kBK / 16; ++kk)
-                umma_f16(tmem, sw128_desc(sa + kk * 32, 16, 1024), sw128_desc(sb + kk * 2048, 8192, 1024), kIdesc,
-                         (c > 0 || kk > 0) ? 1u : 0u);
-            umma_commit(empty + s);
+                for (int q = 0; q < 4; ++q) {          // B: 64 rows x 8 pieces; thread t takes 4
+                    const int piece = t * 4 + q, r = piece >> 3, p8 = piece & 7;
+                    const uint32_t dst = sb + sw128_offset(r, p8 * 16);
+                    if (k0 + r < d_in) cp_async16(dst, wh + (size_t)(k0 + r) * HD + p8 * 8);
+                    else cp_async_zero16(dst, a.wv);
+                }
+                cp_async_commit();
+            };
+            // prologue: kStages - 1 chunks in flight
+            // ring slots / parities continue across tiles: chunk c of this tile is global chunk g0 + c
+            for (int c = 0; c < kStages - 1; ++c)
+                if (c < nchunks) {
+                    const int g = g0 + c;
+                    mbar_wait(empty + g % kStages, ((g / kStages) & 1) ^ 1);
+                    issue(c, g % kStages);
+                } else {
+                    cp_async_commit();
+                }
+            for (int c = 0; c < nchunks; ++c) {
+                const int cn = c + kStages - 1;
+                if (cn < nchunks) {
+                    const int g = g0 + cn;
+                    mbar_wait(empty + g % kStages, ((g / kStages) & 1) ^ 1);
+                    issue(cn, g % kStages);
+                } else {
+                    cp_async_commit();
+                }
+                cp_async_wait<kStages - 1>();          // chunk c has landed (this thread's copies)
+                fence_proxy_async_smem();               // make them visible to the tensor core (async proxy)
+                mbar_arrive(full + (g0 + c) % kStages);
+            }
+            // ---------------- epilogue: TMEM row t -> bf16 -> H~
+            mbar_wait(acc_full, it & 1);
+            tc_fence_after();
+            uint32_t v[2][32];
+            const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
+            tmem_ld32(lane_base, v[0]);
+            tmem_ld32(lane_base + 32, v[1]);
+            tmem_ld_wait();
+            if (bj >= 0) {
+                __half* dst = reinterpret_cast<__half*>(a.h_out) + tok * HD + (size_t)h * kDh;   // H~ is fp16
+#pragma unroll
+                for (int g = 0; g < 8; ++g) {
+                    uint32_t pk[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const int c = g * 8 + 2 * e;
+                        pk[e] = pack_f16x2(__uint_as_float(v[c >> 5][c & 31]), __uint_as_float(v[(c + 1) >> 5][(c + 1) & 31]));
+                    }
+                    reinterpret_cast<uint4*>(dst)[g] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                }
+                if (a.draws_out) {                     // exact token-heads draw nothing
+                    const size_t tokh = ((size_t)(bj >> 16) * a.heads + h) * n + (bj & 0xFFFF);
+                    for (int k = 0; k < a.draws_stride; ++k) a.draws_out[tokh * a.draws_stride + k] = -1;
+                }
+            }
+        } else if (lane == 0) {
+            // ---------------- MMA issuer
+            for (int c = 0; c < nchunks; ++c) {
+                const int g = g0 + c, s = g % kStages;
+                mbar_wait(full + s, (g / kStages) & 1);
+                tc_fence_after();
+                const uint32_t sa = smem_u32(smem + s * kStageBytes);
+                const uint32_t sb = sa + kABytes;
+#pragma unroll
+                for (int kk = 0; kk < kBK / 16; ++kk)
+                    umma_f16(tmem, sw128_desc(sa + kk * 32, 16, 1024), sw128_desc(sb + kk * 2048, 8192, 1024), kIdesc,
+                             (c > 0 || kk > 0) ? 1u : 0u);
+                umma_commit(empty + s);
+            }
+            umma_commit(acc_full);
         }
-        umma_commit(acc_full);
+        tc_fence_before();
+        __syncthreads();   // the accumulator is read out before the next tile's MMAs overwrite it
+        tc_fence_after();
     }
     tc_fence_before();
     __syncthreads();

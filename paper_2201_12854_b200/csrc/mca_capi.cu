@@ -329,8 +329,12 @@ mca_status launch_k3(mca_weights* w, const void* x, int B, int n, long b_offset,
                                               (int)k3btc::kSmemBytes));
             attr = true;
         }
-        k3b_exact_tc<<<dim3((unsigned)((a.tokens + 127) / 128), w->heads), k3btc::kThreads, k3btc::kSmemBytes,
-                       stream>>>(a);
+        // persistent: one wave (2 CTAs per SM), CTAs loop over their head's exact tiles
+        int Ge = (2 * sm_count() + w->heads - 1) / w->heads;
+        const long ecap = (a.tokens + k3btc::kBM - 1) / k3btc::kBM;
+        if (Ge > ecap) Ge = (int)ecap;
+        if (Ge < 1) Ge = 1;
+        k3b_exact_tc<<<dim3((unsigned)Ge, w->heads), k3btc::kThreads, k3btc::kSmemBytes, stream>>>(a);
         MCA_LAUNCH_CHECK("k3b_exact_tc");
     } else {                                  // fp32 parity path: fp64 CUDA-core GEMM
         int Ge = (2 * sm_count() + w->heads - 1) / w->heads;
