@@ -175,17 +175,33 @@ __global__ void __launch_bounds__(k1tc::kThreads, 2)
                 }
             } else {
                 // v = t2 - lse2_q; strict > keeps the first (smallest) query on ties
+                if (valid >= 64) {   // full chunk: no per-element bounds checks
 #pragma unroll
-                for (int g = 0; g < 64; g += 4) {
-                    if (g < valid) {
+                    for (int g = 0; g < 64; g += 4) {
                         const float4 ls = *reinterpret_cast<const float4*>(s_lse + c0 + g);
                         const float lv[4] = {ls.x, ls.y, ls.z, ls.w};
 #pragma unroll
                         for (int e = 0; e < 4; ++e) {
                             const float v = __fmaf_rn(__uint_as_float(sv[(g + e) >> 5][(g + e) & 31]), c2, -lv[e]);
-                            if (g + e < valid && v > best) {
+                            if (v > best) {
                                 best = v;
                                 best_i = c0 + g + e;
+                            }
+                        }
+                    }
+                } else {
+#pragma unroll
+                    for (int g = 0; g < 64; g += 4) {
+                        if (g < valid) {
+                            const float4 ls = *reinterpret_cast<const float4*>(s_lse + c0 + g);
+                            const float lv[4] = {ls.x, ls.y, ls.z, ls.w};
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) {
+                                const float v = __fmaf_rn(__uint_as_float(sv[(g + e) >> 5][(g + e) & 31]), c2, -lv[e]);
+                                if (g + e < valid && v > best) {
+                                    best = v;
+                                    best_i = c0 + g + e;
+                                }
                             }
                         }
                     }
