@@ -11,6 +11,7 @@
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -634,19 +635,30 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
                 (const __nv_bfloat16*)q, (const __nv_bfloat16*)k, (const __half*)w->hbuf, w->lse, n, H,
                 (float)scale, (__nv_bfloat16*)y);
         else {
-            CUtensorMap tq, tk, th;
-            if (!make_tmap_bf16(&tq, q, (uint64_t)H * kDh, n, B, 128) ||
-                !make_tmap_bf16(&tk, k, (uint64_t)H * kDh, n, B, k4tc::kBK) ||
+            CUtensorMap tk, th;
+            if (!make_tmap_bf16(&tk, k, (uint64_t)H * kDh, n, B, k4tc::kBK) ||
                 !make_tmap_bf16(&th, w->hbuf, (uint64_t)H * kDh, n, B, k4tc::kBK, CU_TENSOR_MAP_DATA_TYPE_FLOAT16))
-                return fail(MCA_ERR_CUDA, "cuTensorMapEncodeTiled failed for q/k/h");
+                return fail(MCA_ERR_CUDA, "cuTensorMapEncodeTiled failed for k/h");
             static bool attr = false;
             if (!attr) {
                 MCA_CUDA_TRY(cudaFuncSetAttribute(k4_apply_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                   (int)k4tc::kSmemBytes));
                 attr = true;
             }
-            k4_apply_tc<<<dim3((n + k4tc::kBM - 1) / k4tc::kBM, H, B), k4tc::kThreads, k4tc::kSmemBytes, stream>>>(
-                tq, tk, th, w->lse, n, H, (float)scale, (__nv_bfloat16*)y);
+            const long tiles = (long)B * H * ((n + k4tc::kBM - 1) / k4tc::kBM);
+            const int grid = (int)std::min<long>(tiles, 2L * sm_count());   // persistent: two CTAs per SM
+            k4_apply_tc<<<grid, k4tc::kThreads, k4tc::kSmemBytes, stream>>>(
+                (const __nv_bfloat16*)q, tk, th, w->lse, n, H, B, (float)scale, (__nv_bfloat16*)y);
+            if (MCA_K4_PROF) {   // diagnostics build: the first CTA's softmax timeline
+                long long t[64];
+                MCA_CUDA_TRY(cudaStreamSynchronize(stream));
+                MCA_CUDA_TRY(cudaMemcpyFromSymbol(t, g_k4_prof, sizeof(t)));
+                fprintf(stderr, "k4 CTA0 (2nd tile): start->softmax %lld |", t[0] - t[60]);
+                for (int kb = 0; kb < (n + k4tc::kBK - 1) / k4tc::kBK && kb < 16; ++kb)
+                    fprintf(stderr, " kb%d S@%lld P@%lld done@%lld", kb, t[1 + 3 * kb] - t[60], t[2 + 3 * kb] - t[60],
+                            t[3 + 3 * kb] - t[60]);
+                fprintf(stderr, " | O@%lld end@%lld\n", t[50] - t[60], t[51] - t[60]);
+            }
         }
         MCA_LAUNCH_CHECK("k4_apply");
     }
