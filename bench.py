@@ -16,7 +16,9 @@ validation.
 
 The JSON line also carries:
   e2e           the same metric through the C ABI with HOST buffers: pinned
-                H2D of q/k/x, forward, D2H of y inside the timed region
+                H2D of q/k/x, forward, D2H of y inside the timed region, every
+                step (HostPipeline: batch chunks whose copies and forward
+                overlap on three streams)
   roofline      the dominant kernel's achieved algorithmic GB/s or TFLOP/s vs
                 MEASURED_PEAKS.json (DESIGN.md §7 defines the per-unit work)
   cpu_baseline  the fp64 CPU oracle (the reference algorithm, test
@@ -165,6 +167,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     import torch
 
     import paper_2201_12854_b200 as mca
+    from paper_2201_12854_b200.pipeline import HostPipeline
     from paper_2201_12854_b200 import synthetic
 
     torch.cuda.set_device(local_rank)
@@ -244,21 +247,16 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     ms_per_step = total_ms / args.steps
     value = world * B * n * L / (ms_per_step / 1e3)   # token-layers per second (= tokens/s for one layer)
 
-    # e2e: host buffers through the C ABI (pinned H2D + forward + D2H), same stream
+    # e2e: host buffers through the package's pipelined host API (HostPipeline:
+    # every step copies its q, k, x from pinned host memory and reads y back,
+    # in chunks whose H2D / forward / D2H overlap on three streams)
     hq, hk, hx = (t.to(dtype).pin_memory() for t in (inp.q, inp.k, inp.x))
     hy = torch.empty(y.shape, dtype=dtype).pin_memory()
-    dq, dk, dx = torch.empty_like(q), torch.empty_like(k), torch.empty_like(x)
+    chunk = B // 8 if B >= 8 and B % 8 == 0 else B
+    pipe = HostPipeline(layer_weights, n, chunk, dtype, dev)
 
     def e2e_step():
-        dq.copy_(hq, non_blocking=True)
-        dk.copy_(hk, non_blocking=True)
-        dx.copy_(hx, non_blocking=True)
-        xin = dx
-        for l in range(L):
-            out_buf = ybuf[l & 1] if L > 1 else y
-            mca.mca_forward(layer_weights[l], dq, dk, xin, cfg, seed=42, b_offset=b_offset, layer=l, y=out_buf)
-            xin = out_buf
-        hy.copy_(xin, non_blocking=True)
+        pipe.forward(hq, hk, hx, hy, cfg, seed=42, b_offset=b_offset)
 
     for _ in range(max(1, args.warmup)):
         e2e_step()

@@ -26,4 +26,6 @@ from .api import (  # noqa: F401
     sample_budgets,
 )
 
+from .pipeline import HostPipeline  # noqa: F401,E402
+
 __version__ = "0.1.0"

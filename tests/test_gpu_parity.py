@@ -387,3 +387,26 @@ def test_bf16_tile_encoder_parity_subprocess():
                         os.path.join(here, "test_gpu_parity.py"), "-k", "bf16_parity or golden_draws or determinism"],
                        env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+def test_host_pipeline_matches_forward(mca, syn):
+    """HostPipeline (chunked, overlapped H2D / forward / D2H from pinned host
+    buffers) returns bitwise the output of one mca_forward on the whole batch,
+    for a single layer and a 2-layer stack."""
+    H, n, d_in, B = 12, 128, 768, 8
+    w = syn.make_weights(d_in, H).to(torch.bfloat16)
+    inp = syn.make_inputs(B, n, d_in, H)
+    q, k, x = (t.to(torch.bfloat16) for t in (inp.q, inp.k, inp.x))
+    layers = [mca.AttentionWeights(w.cuda(), heads=H), mca.AttentionWeights(w.cuda(), heads=H)]
+    cfg = mca.McaConfig(alpha=0.4)
+    for L in (1, 2):
+        ref_x = x.cuda()
+        for l in range(L):
+            ref_x = mca.mca_forward(layers[l], q.cuda(), k.cuda(), ref_x, cfg, seed=5, b_offset=3, layer=l).y
+        hq, hk, hx = (t.pin_memory() for t in (q, k, x))
+        hy = torch.empty((B, n, H * 64), dtype=torch.bfloat16).pin_memory()
+        pipe = mca.HostPipeline(layers[:L], n, chunk=2, dtype=torch.bfloat16)
+        pipe.forward(hq, hk, hx, hy, cfg, seed=5, b_offset=3)
+        pipe.forward(hq, hk, hx, hy, cfg, seed=5, b_offset=3)   # slots reused across calls
+        torch.cuda.synchronize()
+        assert torch.equal(hy, ref_x.cpu()), L
