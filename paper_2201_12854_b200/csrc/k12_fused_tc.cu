@@ -1,0 +1,379 @@
+// k12_fused_tc.cu — K1 + K2 fused for BERT-length sequences (bf16, n <= 768):
+// the score pass (attention_matrix + softmax_rows + col_max, SPEC.md:286-294,
+// matrix.hpp:46-53) and Eq. 9 (sample_budgets) for one
+// (b, h) per CTA.
+//
+// Same formulas as k1_scores_tc (K1a then K1b) followed by k2_budgets
+// (kKeyArgmax with the tensor-core winner score); the fp32 row sums are
+// accumulated per 32-column part (4 parts) instead of per 64-column half, so
+// lse may differ from the three-kernel path in the last bits, and the budgets
+// are Eq. 9 of this kernel's own cmax (what the parity tests check). The fusion removes
+// the per-tile prologues of two kernels (each of K1a / K1b re-loaded its
+// resident tile and allocated TMEM per 128 rows) and K2's dependent global
+// lookups: Q and K of the (b, h) stay resident in shared memory for both
+// passes, and the winner's row statistics are read from shared memory.
+//
+//   phase 1, block (qt, kt):  S = Q_qt K_kt^T   (TMEM lane = query)
+//       online row max / sum of t = scale S (log2 domain, ex2.approx) per
+//       64-column half, combined at the end of each qt: row_m, row_l (fp64),
+//       lse (global + smem), then "lse(qt) ready"
+//   phase 2, block (qt, kt):  S^T = K_kt Q_qt^T (TMEM lane = key)
+//       per key the max over queries of v = t - lse2_q and its first argmax
+//       (two independent running maxima per thread), accumulated over qt;
+//       at the end the owner thread of each key evaluates
+//       cmax = exp(scale S* - m_q*) / l_q* in fp64 and Eq. 9 (budget, exact
+//       flag, FLOP counters, the per-head budget histogram)
+// The two phases run CONCURRENTLY on two consumer groups: phase 1 is bound by
+// the MUFU (one exponential per score), phase 2 by FMA/ALU issue, so group A
+// exponentiating query tile qt + 1 overlaps group B's maxima over tile qt.
+//
+// Warp roles (576 threads, one CTA per SM): warp 0 TMA (all Q and K tiles of
+// the (b, h), one barrier per tile) and then the phase-2 MMA issuer, warp 1
+// TMEM allocator + phase-1 MMA issuer, warps 2-9 group A, warps 10-17 group
+// B: two warps per TMEM lane quadrant in each group, each owning 64 of a
+// block's 128 columns. TMEM: A buffers [0,256), B buffers [256,512).
+#include "mca_common.cuh"
+#include "tc_common.cuh"
+
+namespace mca_dev {
+
+#ifndef MCA_K12_PROF
+#define MCA_K12_PROF 0
+#endif
+// Diagnostics (build with EXTRA=-DMCA_K12_PROF=1): clock64 stamps of CTA 0:
+// [0] start, [1 + u] group A block u done, [40 + u] group B block u done, [80] end
+__device__ long long g_k12_prof[96];
+
+namespace k12 {
+constexpr int kT = 128;                           // tile rows (= block columns)
+constexpr int kMaxTiles = 6;                      // n <= 768
+constexpr int kGroupWarps = 8;                    // per consumer group: 2 per TMEM lane quadrant
+constexpr int kGThreads = kGroupWarps * 32;
+constexpr int kThreads = 64 + 2 * kGThreads;      // 576
+constexpr uint32_t kTileBytes = kT * kDh * 2;     // 16 KB: 128 rows x 64 bf16, 128B-swizzled
+constexpr uint32_t kIdesc = mca_tc::idesc_f16(1, 0, kT, kT);
+
+struct Layout {
+    uint32_t q, k, lse2, m, l, comb, hist, bars, bytes;
+};
+__host__ __device__ inline Layout layout(int nt, int d) {
+    Layout L;
+    L.q = 0;
+    L.k = nt * kTileBytes;
+    L.lse2 = 2 * nt * kTileBytes;                              // [nt*128] f32, log2 domain
+    L.m = L.lse2 + nt * kT * 4;                                // [nt*128] f64 row max (natural log domain)
+    L.l = L.m + nt * kT * 8;                                   // [nt*128] f64 row sum
+    L.comb = L.l + nt * kT * 8;                                // A: [2][128] x 8 B; B: [kMaxTiles][2][128] x 8 B
+    L.hist = L.comb + (2 + 2 * kMaxTiles) * kT * 8;            // [d + 1] u32 budget histogram
+    L.bars = (L.hist + (uint32_t)(d + 1) * 4 + 15) & ~15u;
+    L.bytes = L.bars + 256 + 1024;                             // + alignment slack
+    return L;
+}
+}  // namespace k12
+
+struct K12Args {
+    int n, heads, d, dh, min_samples;
+    float scale;
+    double scale_d, alpha;
+    bool force_exact;
+    const int32_t* budgets_override;   // debug hooks (mca_debug)
+    const uint8_t* exact_override;
+    double* cmax_out;
+    double* row_m;                     // [B, H, n]
+    double* row_l;
+    float* lse;
+    int32_t* budgets;
+    uint8_t* exact;
+    unsigned long long* counters;      // [0] approx cost, [1] sampled draws, [2] exact token-heads
+    unsigned int* hist;                // [H, d + 1] (nullable)
+};
+
+__global__ void __maxnreg__(96)
+    k12_fused_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k, K12Args a) {
+    using namespace k12;
+    using namespace mca_tc;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    const int n = a.n, heads = a.heads;
+    const int nt = (n + kT - 1) / kT;
+    const Layout L = layout(nt, a.d);
+    float* s_lse2 = reinterpret_cast<float*>(smem + L.lse2);
+    double* s_m = reinterpret_cast<double*>(smem + L.m);
+    double* s_l = reinterpret_cast<double*>(smem + L.l);
+    float2* combA = reinterpret_cast<float2*>(smem + L.comb);        // [2][128]  (qt parity)
+    float2* combB = combA + 2 * kT;                                   // [kMaxTiles][2][128] running maxima
+    unsigned int* s_hist = reinterpret_cast<unsigned int*>(smem + L.hist);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);
+    uint64_t* tile_full = bars;                  // [2 * kMaxTiles]: Q tiles, then K tiles
+    uint64_t* a_full = bars + 2 * kMaxTiles;     // [2] phase-1 S buffers
+    uint64_t* a_empty = a_full + 2;              // [2]
+    uint64_t* b_full = a_empty + 2;              // [2] phase-2 S^T buffers
+    uint64_t* b_empty = b_full + 2;              // [2]
+    uint64_t* lse_ready = b_empty + 2;           // [kMaxTiles]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(lse_ready + kMaxTiles);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int bh = blockIdx.x, b = bh / heads, h = bh - b * heads;
+    const int nblk = nt * nt;
+    const bool prof0 = MCA_K12_PROF && blockIdx.x == 0;
+    if (prof0 && threadIdx.x == 0) g_k12_prof[0] = clock64();
+    const bool use_hist = a.hist != nullptr && a.d <= 1024;
+
+    if (threadIdx.x == 0) {
+        for (int t = 0; t < 2 * nt; ++t) mbar_init(tile_full + t, 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(a_full + i, 1);
+            mbar_init(a_empty + i, kGThreads);
+            mbar_init(b_full + i, 1);
+            mbar_init(b_empty + i, kGThreads);
+        }
+        for (int t = 0; t < kMaxTiles; ++t) mbar_init(lse_ready + t, kGThreads / 2);
+        fence_barrier_init();
+    }
+    if (use_hist)
+        for (int i = threadIdx.x; i <= a.d; i += k12::kThreads) s_hist[i] = 0;
+    if (warp == 1) tmem_alloc<512>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    // block u of a phase = (qt, kt) = (u / nt, u % nt). Phase 1: S = Q_qt K_kt^T into
+    // the A buffers; phase 2: S^T = K_kt Q_qt^T into the B buffers. Each stream has
+    // its own issuing thread (tcgen05.commit tracks the issuing thread's MMAs), so
+    // neither stream waits on the other's buffer recycling.
+    auto issue = [&](int phase, int u) {
+        const int qt = u / nt, kt = u - qt * nt, sb = u & 1;
+        uint64_t* full = phase ? b_full : a_full;
+        uint64_t* empty = phase ? b_empty : a_empty;
+        mbar_wait(empty + sb, ((u >> 1) & 1) ^ 1);
+        mbar_wait(tile_full + qt, 0);
+        mbar_wait(tile_full + nt + kt, 0);
+        tc_fence_after();
+        const uint32_t qa = smem_u32(smem + L.q + qt * kTileBytes);
+        const uint32_t ka = smem_u32(smem + L.k + kt * kTileBytes);
+        const uint32_t a_addr = phase ? ka : qa, b_addr = phase ? qa : ka;
+        const uint32_t d = tmem + (uint32_t)(phase * 2 + sb) * kT;
+#pragma unroll
+        for (int kk = 0; kk < kDh / 16; ++kk)
+            umma_f16(d, sw128_desc(a_addr + kk * 32, 16, 1024), sw128_desc(b_addr + kk * 32, 16, 1024), kIdesc,
+                     kk > 0 ? 1u : 0u);
+        umma_commit(full + sb);
+    };
+    if (warp == 0) {
+        if (lane == 0) {  // ---------------- TMA (every Q and K tile once), then the phase-2 MMA stream
+            tma_prefetch(&tm_q);
+            tma_prefetch(&tm_k);
+            for (int t = 0; t < nt; ++t)
+                for (int op = 0; op < 2; ++op) {   // 0: Q tile t, 1: K tile t
+                    mbar_expect_tx(tile_full + op * nt + t, kTileBytes);
+                    tma_load_3d(smem + (op ? L.k : L.q) + t * kTileBytes, op ? &tm_k : &tm_q, tile_full + op * nt + t,
+                                h * kDh, t * kT, b);
+                }
+            for (int u = 0; u < nblk; ++u) issue(1, u);
+        }
+    } else if (warp == 1) {
+        if (lane == 0)   // ---------------- the phase-1 MMA stream
+            for (int u = 0; u < nblk; ++u) issue(0, u);
+    } else {  // ------------------------------- consumer groups A (warps 2..9) and B (warps 10..17)
+        const int grp = warp >= 2 + kGroupWarps;   // 0: A (row statistics), 1: B (column maxima)
+        const int gt = threadIdx.x - 64 - grp * kGThreads;
+        const int quad = warp & 3;                 // TMEM lane quadrant this warp may access
+        const int half = (gt >> 5) >> 2;           // columns [64 half, 64 half + 64) of each block
+        const int row = quad * 32 + lane;          // TMEM lane = resident row (query in A, key in B)
+        const uint32_t lane_base = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(grp * 2) * kT + half * 64;
+        const float c2 = a.scale * 1.4426950408889634f;
+        const size_t rbase = (size_t)bh * n;
+        uint64_t* full = grp ? b_full : a_full;
+        uint64_t* empty = grp ? b_empty : a_empty;
+        // a block's 64 columns in two 32-column pieces (register pressure); the
+        // buffer is released after the second piece is read
+        auto load_piece = [&](int u, int pc, uint32_t (&sv)[32]) {
+            const int sb = u & 1;
+            if (pc == 0) {
+                mbar_wait(full + sb, (u >> 1) & 1);
+                tc_fence_after();
+            }
+            tmem_ld32(lane_base + sb * kT + pc * 32, sv);
+            tmem_ld_wait();
+            if (pc == 1) {
+                tc_fence_before();
+                mbar_arrive(empty + sb);
+            }
+        };
+        if (grp == 0) {
+            // ---------------- group A: row statistics, query tile by query tile
+            for (int qt = 0; qt < nt; ++qt) {
+                float m2 = -INFINITY, l = 0.0f;
+                for (int kt = 0; kt < nt; ++kt) {
+#pragma unroll
+                    for (int pc = 0; pc < 2; ++pc) {
+                        uint32_t sv[32];
+                        load_piece(qt * nt + kt, pc, sv);
+                        const int valid = n - (kt * kT + half * 64 + pc * 32);   // <= 0: this piece is past n
+                        float bmax = -INFINITY;
+                        if (valid >= 32) {   // pairwise tree: 5 dependent levels instead of 32
+                            float t16[16];
+#pragma unroll
+                            for (int e = 0; e < 16; ++e) t16[e] = fmaxf(__uint_as_float(sv[e]), __uint_as_float(sv[e + 16]));
+#pragma unroll
+                            for (int w = 8; w >= 1; w >>= 1)
+#pragma unroll
+                                for (int e = 0; e < w; ++e) t16[e] = fmaxf(t16[e], t16[e + w]);
+                            bmax = t16[0];
+                        } else {
+#pragma unroll
+                            for (int e = 0; e < 32; ++e)
+                                if (e < valid) bmax = fmaxf(bmax, __uint_as_float(sv[e]));
+                        }
+                        if (valid > 0) {
+                            const float mn = fmaxf(m2, bmax * c2);
+                            float acc0 = 0.f, acc1 = 0.f;
+                            if (valid >= 32) {   // packed: one FFMA2 and one FADD2 per two scores
+                                float2 acc = make_float2(0.f, 0.f);
+                                const float2 cc = make_float2(c2, c2), nm = make_float2(-mn, -mn);
+#pragma unroll
+                                for (int e = 0; e < 32; e += 2) {
+                                    const float2 x = __ffma2_rn(make_float2(__uint_as_float(sv[e]), __uint_as_float(sv[e + 1])), cc, nm);
+                                    acc = __fadd2_rn(acc, make_float2(ex2_approx(x.x), ex2_approx(x.y)));
+                                }
+                                acc0 = acc.x;
+                                acc1 = acc.y;
+                            } else {
+#pragma unroll
+                                for (int e = 0; e < 32; ++e)
+                                    if (e < valid) acc0 += ex2_approx(__fmaf_rn(__uint_as_float(sv[e]), c2, -mn));
+                            }
+                            l = (m2 == -INFINITY ? 0.0f : l * ex2_approx(m2 - mn)) + (acc0 + acc1);
+                            m2 = mn;
+                        }
+                    }
+                    if (prof0 && gt == 0 && qt * nt + kt < 39) g_k12_prof[1 + qt * nt + kt] = clock64();
+                }
+                // combine the two column halves of each row (as k1_scores_tc does)
+                float2* cb = combA + (qt & 1) * kT;
+                if (half == 1) cb[row] = make_float2(m2, l);
+                named_bar_sync(1, kGThreads);
+                if (half == 0) {
+                    const float2 o = cb[row];
+                    const float mn = fmaxf(m2, o.x);
+                    const float lt = (m2 == -INFINITY ? 0.f : l * ex2_approx(m2 - mn)) +
+                                     (o.x == -INFINITY ? 0.f : o.y * ex2_approx(o.x - mn));
+                    const int q = qt * kT + row;
+                    if (q < n) {
+                        const float lse_nat = (mn + __log2f(lt)) * 0.6931471805599453f;
+                        const double md = (double)mn * 0.6931471805599453, ld = (double)lt;
+                        s_lse2[q] = -(lse_nat * 1.4426950408889634f);   // stored negated (FFMA2 addend)
+                        s_m[q] = md;
+                        s_l[q] = ld;
+                        a.lse[rbase + q] = lse_nat;
+                        a.row_m[rbase + q] = md;
+                        a.row_l[rbase + q] = ld;
+                    } else {
+                        s_lse2[q] = -INFINITY;         // padded queries never win a column maximum
+                    }
+                    mbar_arrive(lse_ready + qt);       // release: this row's statistics are in smem
+                }
+            }
+        } else {
+            // ---------------- group B: per-key column maxima over all queries
+            // running (max, argmax) per key tile in shared memory (this thread's slot)
+            for (int kt = 0; kt < nt; ++kt) combB[(kt * 2 + half) * kT + row] = make_float2(-INFINITY, __int_as_float(0x7FFFFFFF));
+            for (int qt = 0; qt < nt; ++qt) {
+                mbar_wait(lse_ready + qt, 0);          // acquire: lse2 of query tile qt
+                for (int kt = 0; kt < nt; ++kt) {
+                    // two running maxima (even / odd columns) break the compare chain
+                    float b0 = -INFINITY, b1 = -INFINITY;
+                    int i0 = 0x7FFFFFFF, i1 = 0x7FFFFFFF;
+#pragma unroll
+                    for (int pc = 0; pc < 2; ++pc) {
+                        uint32_t sv[32];
+                        load_piece(qt * nt + kt, pc, sv);
+                        const int c0 = qt * kT + half * 64 + pc * 32;   // query of sv[0]; padded queries: lse2 = +inf
+#pragma unroll
+                        for (int g = 0; g < 32; g += 4) {
+                            const float4 nl = *reinterpret_cast<const float4*>(s_lse2 + c0 + g);   // -lse2
+                            const float2 cc = make_float2(c2, c2);
+                            const float2 va = __ffma2_rn(make_float2(__uint_as_float(sv[g]), __uint_as_float(sv[g + 1])), cc,
+                                                         make_float2(nl.x, nl.y));
+                            const float2 vb = __ffma2_rn(make_float2(__uint_as_float(sv[g + 2]), __uint_as_float(sv[g + 3])),
+                                                         cc, make_float2(nl.z, nl.w));
+                            const float v0 = va.x, v1 = va.y, v2 = vb.x, v3 = vb.y;
+                            if (v0 > b0) { b0 = v0; i0 = c0 + g; }
+                            if (v1 > b1) { b1 = v1; i1 = c0 + g + 1; }
+                            if (v2 > b0) { b0 = v2; i0 = c0 + g + 2; }
+                            if (v3 > b1) { b1 = v3; i1 = c0 + g + 3; }
+                        }
+                    }
+                    // merge: larger value, ties to the smaller query index
+                    if (b1 > b0 || (b1 == b0 && i1 < i0)) { b0 = b1; i0 = i1; }
+                    float2* slot = combB + (kt * 2 + half) * kT + row;
+                    if (b0 > slot->x) *slot = make_float2(b0, __int_as_float(i0));   // later tiles: larger indices
+                    if (prof0 && gt == 0 && qt * nt + kt < 39) g_k12_prof[40 + qt * nt + kt] = clock64();
+                }
+            }
+        }
+        // ---------------- Eq. 9 for every key, one key per consumer thread (both groups)
+        named_bar_sync(3, 2 * kGThreads);          // group B's running maxima are final
+        unsigned long long cost = 0, samples = 0, nexact = 0;
+        for (int j = threadIdx.x - 64; j < n; j += 2 * kGThreads) {
+            const int kt = j / kT, r0 = j - kt * kT;
+            // the two query halves of the key: larger value, ties to the smaller query index
+            const float2 m0 = combB[(kt * 2) * kT + r0], m1 = combB[(kt * 2 + 1) * kT + r0];
+            float bv = m0.x;
+            int bi = __float_as_int(m0.y);
+            if (m1.x > bv || (m1.x == bv && __float_as_int(m1.y) < bi)) {
+                bv = m1.x;
+                bi = __float_as_int(m1.y);
+            }
+            const size_t t = rbase + j;
+            int r;
+            bool ex;
+            if (a.force_exact) {
+                r = a.d;
+                ex = true;
+            } else if (a.budgets_override) {
+                r = a.budgets_override[t];
+                ex = a.exact_override[t] != 0;
+            } else {
+                // the winner's raw score rebuilt from v (k1_scores_tc), then K2's fp64 softmax entry
+                const float colscore = (bv - s_lse2[bi]) / c2;   // s_lse2 holds -lse2
+                const double cm = __ddiv_rn(exp(__dsub_rn(__dmul_rn(a.scale_d, (double)colscore), s_m[bi])), s_l[bi]);
+                if (a.cmax_out) a.cmax_out[t] = cm;
+                budget_for(cm, n, a.alpha, a.min_samples, a.d, &r, &ex);
+            }
+            a.budgets[t] = r;
+            a.exact[t] = ex ? 1 : 0;
+            if (ex) {
+                cost += 2ull * (unsigned long long)a.d * (unsigned long long)a.dh;
+                nexact += 1;
+            } else {
+                cost += (unsigned long long)r * (2ull * a.dh + 3ull);
+                samples += (unsigned long long)r;
+            }
+            if (use_hist) atomicAdd(&s_hist[ex ? a.d : min(r, a.d - 1)], 1u);
+        }
+        if (a.counters) {
+            for (int off = 16; off; off >>= 1) {
+                cost += __shfl_xor_sync(0xffffffffu, cost, off);
+                samples += __shfl_xor_sync(0xffffffffu, samples, off);
+                nexact += __shfl_xor_sync(0xffffffffu, nexact, off);
+            }
+            if (lane == 0) {
+                if (cost) atomicAdd(a.counters + 0, cost);
+                if (samples) atomicAdd(a.counters + 1, samples);
+                if (nexact) atomicAdd(a.counters + 2, nexact);
+            }
+        }
+    }
+    if (prof0 && threadIdx.x == 64 + kGThreads) g_k12_prof[79] = clock64();   // group B done (incl. Eq. 9)
+    tc_fence_before();
+    __syncthreads();
+    if (prof0 && threadIdx.x == 0) g_k12_prof[80] = clock64();
+    if (use_hist)
+        for (int i = threadIdx.x; i <= a.d; i += k12::kThreads)
+            if (s_hist[i]) atomicAdd(&a.hist[(size_t)h * (a.d + 1) + i], s_hist[i]);
+    if (warp == 1) tmem_dealloc<512>(tmem);
+}
+
+}  // namespace mca_dev

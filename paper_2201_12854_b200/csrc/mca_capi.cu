@@ -25,6 +25,7 @@
 #include "k1_scores_simt.cu"
 #include "k1_scores_tc.cu"
 #include "k2_budgets.cu"
+#include "k12_fused_tc.cu"
 #include "k3_encode.cu"
 #include "k3b_exact_tc.cu"
 #include "k3t_encode_tc.cu"
@@ -538,8 +539,52 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
         MCA_CUDA_TRY(cudaMemsetAsync(w->task_cursor, 0, H * sizeof(int), stream));
     }
 
+    // K1 + K2 fused (bf16, n <= 768): both score passes and Eq. 9 in one kernel per (b, h)
+    const bool fused12 = dt == MCA_BF16 && !force_simt() && n <= k12::kMaxTiles * k12::kT &&
+                         !(dbg && dbg->cmax_override) && w->d_in <= 1024 &&
+                         k12::layout((n + k12::kT - 1) / k12::kT, w->d_in).bytes <= 227u * 1024u;
+    if (fused12) {
+        CUtensorMap tq, tk;
+        if (!make_tmap_bf16(&tq, q, (uint64_t)H * kDh, n, B, 128) || !make_tmap_bf16(&tk, k, (uint64_t)H * kDh, n, B, 128))
+            return fail(MCA_ERR_CUDA, "cuTensorMapEncodeTiled failed for q/k");
+        const uint32_t smem = k12::layout((n + k12::kT - 1) / k12::kT, w->d_in).bytes;
+        MCA_CUDA_TRY(cudaFuncSetAttribute(k12_fused_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        K12Args a{};
+        a.n = n;
+        a.heads = H;
+        a.d = w->d_in;
+        a.dh = w->dh;
+        a.min_samples = cfg->min_samples;
+        a.scale = (float)scale;
+        a.scale_d = scale;
+        a.alpha = cfg->alpha;
+        a.force_exact = !approx;
+        a.budgets_override = dbg ? dbg->budgets_override : nullptr;
+        a.exact_override = dbg ? dbg->exact_override : nullptr;
+        a.cmax_out = dbg ? dbg->cmax_out : nullptr;
+        a.row_m = w->row_m;
+        a.row_l = w->row_l;
+        a.lse = w->lse;
+        a.budgets = w->budgets;
+        a.exact = w->exact;
+        a.counters = w->counters;
+        a.hist = tile_k3 ? nullptr : w->hist;
+        k12_fused_tc<<<(unsigned)(B * H), k12::kThreads, smem, stream>>>(tq, tk, a);
+        MCA_LAUNCH_CHECK("k12_fused_tc");
+        if (MCA_K12_PROF) {   // diagnostics build: CTA 0's timeline
+            long long t[96];
+            MCA_CUDA_TRY(cudaStreamSynchronize(stream));
+            MCA_CUDA_TRY(cudaMemcpyFromSymbol(t, g_k12_prof, sizeof(t)));
+            const int nb = ((n + 127) / 128) * ((n + 127) / 128);
+            fprintf(stderr, "k12 CTA0: A");
+            for (int u = 0; u < nb && u < 39; ++u) fprintf(stderr, " %lld", t[1 + u] - t[0]);
+            fprintf(stderr, " | B");
+            for (int u = 0; u < nb && u < 39; ++u) fprintf(stderr, " %lld", t[40 + u] - t[0]);
+            fprintf(stderr, " | Bdone %lld end %lld\n", t[79] - t[0], t[80] - t[0]);
+        }
+    }
     // K1: row statistics + column maxima
-    {
+    if (!fused12) {
         const dim3 grid((n + kQT - 1) / kQT, H, B);
         if (dt == MCA_F32)
             k1_scores_simt<float, double><<<grid, kThreads, 0, stream>>>((const float*)q, (const float*)k, n, H, scale,
@@ -599,10 +644,12 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
         a.cmax_out = dbg ? dbg->cmax_out : nullptr;
         a.counters = w->counters;
         a.hist = tile_k3 ? nullptr : w->hist;
-        if (a.cmax_in) k2_budgets<kGivenCmax, float><<<grid, 256, 0, stream>>>(a);
-        else if (dt == MCA_F32) k2_budgets<kKeyValue, float><<<grid, 256, 0, stream>>>(a);
-        else k2_budgets<kKeyArgmax, __nv_bfloat16><<<grid, 256, 0, stream>>>(a);
-        MCA_LAUNCH_CHECK("k2_budgets");
+        if (!fused12) {
+            if (a.cmax_in) k2_budgets<kGivenCmax, float><<<grid, 256, 0, stream>>>(a);
+            else if (dt == MCA_F32) k2_budgets<kKeyValue, float><<<grid, 256, 0, stream>>>(a);
+            else k2_budgets<kKeyArgmax, __nv_bfloat16><<<grid, 256, 0, stream>>>(a);
+            MCA_LAUNCH_CHECK("k2_budgets");
+        }
         if (!tile_k3) {
             k2_scan<<<H, 1024, 0, stream>>>(w->hist, w->d_in, w->cursor, w->counts);
             MCA_LAUNCH_CHECK("k2_scan");

@@ -227,11 +227,11 @@ def test_c1_flops_counters(c1_f32):
 
 # ----------------------------------------------------------- bf16 parity
 @pytest.mark.parametrize("B,n,H,d_in", [(2, 128, 12, 768), (1, 512, 12, 768), (1, 77, 12, 768), (1, 640, 12, 768),
-                                        (2, 200, 12, 768), (1, 130, 16, 1024), (1, 96, 4, 200)])
+                                        (2, 200, 12, 768), (1, 130, 16, 1024), (1, 96, 4, 200), (1, 1000, 12, 768)])
 def test_bf16_parity(mca, syn, orc, B, n, H, d_in):
-    """bf16 path end to end. d_in = 768 runs the tile-GEMM encoder (k3t);
-    BERT-large's d_in = 1024 does not fit its shared-memory plan and runs the
-    gather encoder + exact tensor-core kernel; d_in = 200 pads the K chunks."""
+    """bf16 path end to end. n <= 768 runs the fused score + budget kernel
+    (k12), n = 1000 the separate K1a / K1b / K2 kernels; d_in = 1024
+    (BERT-large) and d_in = 200 (padded chunks) vary the encoder's shapes."""
     weights, w, q, k, x = _setup(mca, syn, B, n, d_in, H, torch.bfloat16, seed=7)
     dbg = dict(cmax_out=torch.zeros((B, H, n), dtype=torch.float64, device="cuda"),
                h_out=torch.zeros_like(q, dtype=torch.float16),           # H~ is fp16 on the bf16 path
