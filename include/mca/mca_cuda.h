@@ -14,6 +14,10 @@
  *                         sample_budgets + approx_encode_row /
  *                         draw_indices + matmul(A, H~)
  *                         (matrix.hpp:33-34) + flops_for_plan
+ *   mca_set_projections   AttentionWeights.w_q / w_k: with them
+ *                         attached, mca_forward takes x alone and computes
+ *                         attention_matrix's projections q = x w_q, k = x w_k
+ *                          on the device
  *   mca_regular_forward   regular_forward
  *   mca_stage_budgets     sample_budgets on given column maxima
  *
@@ -95,6 +99,8 @@ typedef struct mca_debug {
     const double* cmax_override;     /* replace the score pass's cmax before Eq. 9           */
     const int32_t* budgets_override; /* replace Eq. 9's budgets (with exact_override)        */
     const uint8_t* exact_override;
+    void* q_out;                     /* the projected q [B, n, heads*d_h] (q == NULL forwards) */
+    void* k_out;                     /* the projected k                                      */
 } mca_debug;
 
 typedef struct mca_weights mca_weights;
@@ -107,6 +113,12 @@ mca_status mca_prepare_weights(const void* w_v, mca_dtype wdt, int d_in, int hea
                                mca_stream_t stream, mca_weights** out);
 void mca_weights_free(mca_weights* w);
 
+/* Attach W_q and W_k ([d_in, heads*d_h], the weights' dtype, device
+ * pointers; copied). A forward called with q == k == NULL then computes
+ * q = x W_q and k = x W_k on `stream` first (one strided-batched GEMM, fp32
+ * accumulation; the fp32 path without TF32). */
+mca_status mca_set_projections(mca_weights* w, const void* w_q, const void* w_k, mca_stream_t stream);
+
 /* Copy the per-head fp64 probabilities / cdf ([heads, d_in], host buffers). */
 mca_status mca_weights_export(const mca_weights* w, double* probs_host, double* cdf_host);
 
@@ -115,8 +127,10 @@ mca_status mca_weights_export(const mca_weights* w, double* probs_host, double* 
 mca_status mca_reserve(mca_weights* w, long max_tokens, mca_stream_t stream);
 
 /* MCA forward (approximation mode, or cfg->mode == MCA_MODE_REGULAR for the
- * exact layer). budgets_out / exact_out are optional device outputs;
- * flops_out is an optional HOST output (synchronises the stream). */
+ * exact layer). q and k may both be NULL when the weights carry W_q / W_k
+ * (mca_set_projections): the reference's mca_forward(x, weights, ...).
+ * budgets_out / exact_out are optional device outputs; flops_out is an
+ * optional HOST output (synchronises the stream). */
 mca_status mca_forward(mca_weights* w, const void* q, const void* k, const void* x, mca_dtype dt, int B, int n,
                        long b_offset, uint32_t layer, const mca_config* cfg, uint64_t seed, void* y,
                        int32_t* budgets_out, uint8_t* exact_out, mca_flops* flops_out, mca_stream_t stream);

@@ -37,12 +37,13 @@ class McaDebugC(ctypes.Structure):
     _fields_ = [("cmax_out", ctypes.c_void_p), ("lse_out", ctypes.c_void_p), ("h_out", ctypes.c_void_p),
                 ("draws_out", ctypes.c_void_p), ("draws_stride", ctypes.c_int32), ("reserved", ctypes.c_int32),
                 ("cmax_override", ctypes.c_void_p), ("budgets_override", ctypes.c_void_p),
-                ("exact_override", ctypes.c_void_p)]
+                ("exact_override", ctypes.c_void_p), ("q_out", ctypes.c_void_p), ("k_out", ctypes.c_void_p)]
 
 
 # Every symbol declared in include/mca/mca_cuda.h (tests/test_capi.py checks both directions).
 EXPORTS = (
-    "mca_prepare_weights", "mca_weights_free", "mca_weights_export", "mca_reserve", "mca_forward", "mca_forward_ex",
+    "mca_prepare_weights", "mca_weights_free", "mca_weights_export", "mca_set_projections", "mca_reserve",
+    "mca_forward", "mca_forward_ex",
     "mca_regular_forward", "mca_stage_budgets", "mca_set_timing", "mca_last_stage_ms", "mca_last_launch_count",
     "mca_last_error", "mca_version",
 )
@@ -76,6 +77,7 @@ def lib() -> ctypes.CDLL:
     L.mca_weights_free.argtypes = [vp]
     L.mca_weights_free.restype = None
     L.mca_weights_export.argtypes = [vp, vp, vp]
+    L.mca_set_projections.argtypes = [vp, vp, vp, vp]
     L.mca_reserve.argtypes = [vp, i64, vp]
     L.mca_forward.argtypes = [vp, vp, vp, vp, i32, i32, i32, i64, u32, ctypes.POINTER(McaConfigC), u64, vp, vp, vp,
                               ctypes.POINTER(McaFlopsC), vp]

@@ -121,11 +121,14 @@ class FlopsReport:
 
 
 class AttentionWeights:
-    """W_V prepared on the device: the per-head sampling
-    distributions p(i) = ||W_h[i]||^2 / ||W_h||_F^2 are built once (K0) and
-    cached with the weights."""
+    """SPEC.md:260-265 AttentionWeights{w_q, w_k, w, cached_dist} on the device:
+    W_V with its per-head sampling distributions p(i) = ||W_h[i]||^2 /
+    ||W_h||_F^2, built once (K0) and cached, and optionally
+    W_q / W_k ([d_in, heads*d_h]): with them, mca_forward takes x alone and
+    projects q = x W_q, k = x W_k on the device."""
 
-    def __init__(self, w_v: torch.Tensor, heads: int, d_h: int = 64, stream=None):
+    def __init__(self, w_v: torch.Tensor, heads: int, d_h: int = 64, stream=None, w_q: torch.Tensor | None = None,
+                 w_k: torch.Tensor | None = None):
         _need_cuda("w_v", w_v)
         if w_v.dim() != 2 or w_v.shape[1] != heads * d_h:
             raise ShapeError(f"w_v must be [d_in, heads*d_h] = [*, {heads * d_h}], got {tuple(w_v.shape)}")
@@ -137,6 +140,17 @@ class AttentionWeights:
             _check(L.lib().mca_prepare_weights(_ptr(w_v), _dt(w_v), self.d_in, heads, d_h, _stream(stream),
                                                ctypes.byref(h)))
         self._h = h
+        self.has_projections = False
+        if (w_q is None) != (w_k is None):
+            raise ConfigError("pass both w_q and w_k, or neither")
+        if w_q is not None:
+            for name, t in (("w_q", w_q), ("w_k", w_k)):
+                _need_cuda(name, t)
+                if t.shape != w_v.shape or t.dtype != w_v.dtype:
+                    raise ShapeError(f"{name} must match w_v: {tuple(w_v.shape)} {w_v.dtype}")
+            with torch.cuda.device(w_v.device):
+                _check(L.lib().mca_set_projections(self._h, _ptr(w_q), _ptr(w_k), _stream(stream)))
+            self.has_projections = True
 
     @property
     def handle(self) -> ctypes.c_void_p:
@@ -189,25 +203,36 @@ class AttentionOutput:
 
 
 def _check_inputs(weights: AttentionWeights, q, k, x):
+    """q and k may both be None when the weights carry W_q / W_k."""
+    if (q is None) != (k is None):
+        raise ShapeError("pass both q and k, or neither (then the weights must carry W_q / W_k)")
+    if q is None and not weights.has_projections:
+        raise ConfigError("q / k omitted but the weights carry no W_q / W_k")
     for name, t in (("q", q), ("k", k), ("x", x)):
+        if t is None:
+            continue
         _need_cuda(name, t)
         if t.dtype != weights.dtype:
             raise ConfigError(f"{name}.dtype {t.dtype} != weights dtype {weights.dtype}")
-    if q.dim() != 3 or q.shape != k.shape or q.shape[2] != weights.heads * weights.d_h:
-        raise ShapeError(f"q, k must be [B, n, {weights.heads * weights.d_h}], got {tuple(q.shape)}, {tuple(k.shape)}")
-    if x.dim() != 3 or x.shape[:2] != q.shape[:2] or x.shape[2] != weights.d_in:
+    if x.dim() != 3 or x.shape[2] != weights.d_in:
         raise ShapeError(f"x must be [B, n, {weights.d_in}], got {tuple(x.shape)}")
-    return int(q.shape[0]), int(q.shape[1])
+    if q is not None:
+        if q.dim() != 3 or q.shape != k.shape or q.shape[2] != weights.heads * weights.d_h:
+            raise ShapeError(f"q, k must be [B, n, {weights.heads * weights.d_h}], got {tuple(q.shape)}, {tuple(k.shape)}")
+        if x.shape[:2] != q.shape[:2]:
+            raise ShapeError(f"x must be [B, n, {weights.d_in}] with q's B, n, got {tuple(x.shape)}")
+    return int(x.shape[0]), int(x.shape[1])
 
 
-def mca_forward(weights: AttentionWeights, q: torch.Tensor, k: torch.Tensor, x: torch.Tensor,
+def mca_forward(weights: AttentionWeights, q: torch.Tensor | None, k: torch.Tensor | None, x: torch.Tensor,
                 cfg: McaConfig | None = None, seed: int = 0, *, b_offset: int = 0, layer: int = 0,
                 y: torch.Tensor | None = None, return_plan: bool = False, flops: bool = False,
                 debug: dict | None = None, stream=None) -> AttentionOutput:
     """Monte-Carlo Attention forward for a batch of sequences and all heads.
 
-    q, k: [B, n, heads*64]; x: [B, n, d_in]; returns y [B, n, heads*64] in the
-    input dtype. Head h of sequence b draws from Philox stream
+    q, k: [B, n, heads*64] (or both None: weights with W_q / W_k project them
+    from x on the device, SPEC.md:306-314's mca_forward(x, weights, ...));
+    x: [B, n, d_in]; returns y [B, n, heads*64] in the input dtype. Head h of sequence b draws from Philox stream
     ((b_offset + b) * heads + h) * n + j (SPEC.md:356 generalised). With
     return_plan the per-token budgets / exact mask [B, heads, n] come back on
     the device; with flops=True the FlopsReport is read back (synchronises).
@@ -215,30 +240,31 @@ def mca_forward(weights: AttentionWeights, q: torch.Tensor, k: torch.Tensor, x: 
     debug (parity testing) may hold CUDA tensors under the mca_debug field
     names: cmax_out (f64), lse_out (f32), h_out (H~: fp32 for fp32 inputs, fp16
     for bf16 inputs), draws_out (+ draws_stride),
-    cmax_override (f64), budgets_override (i32) + exact_override (u8).
+    cmax_override (f64), budgets_override (i32) + exact_override (u8), and for
+    q = k = None forwards q_out / k_out (the projected q, k).
     """
     cfg = cfg or McaConfig()
     B, n = _check_inputs(weights, q, k, x)
     if y is None:
-        y = torch.empty_like(q)
+        y = torch.empty((B, n, weights.heads * weights.d_h), dtype=x.dtype, device=x.device)
     budgets = exact = None
     if return_plan:
-        budgets = torch.empty((B, weights.heads, n), dtype=torch.int32, device=q.device)
-        exact = torch.empty((B, weights.heads, n), dtype=torch.uint8, device=q.device)
+        budgets = torch.empty((B, weights.heads, n), dtype=torch.int32, device=x.device)
+        exact = torch.empty((B, weights.heads, n), dtype=torch.uint8, device=x.device)
     fl = L.McaFlopsC() if flops else None
     c = cfg.to_c()
     dbg = None
     if debug:
         dbg = L.McaDebugC()
         for name in ("cmax_out", "lse_out", "h_out", "draws_out", "cmax_override", "budgets_override",
-                     "exact_override"):
+                     "exact_override", "q_out", "k_out"):
             t = debug.get(name)
             if t is not None:
                 _need_cuda(name, t)
                 setattr(dbg, name, t.data_ptr())
         dbg.draws_stride = int(debug.get("draws_stride", 0))
-    with torch.cuda.device(q.device):
-        args = (weights.handle, _ptr(q), _ptr(k), _ptr(x), _dt(q), B, n, int(b_offset), int(layer), ctypes.byref(c),
+    with torch.cuda.device(x.device):
+        args = (weights.handle, _ptr(q), _ptr(k), _ptr(x), _dt(x), B, n, int(b_offset), int(layer), ctypes.byref(c),
                 ctypes.c_uint64(seed & 0xFFFFFFFFFFFFFFFF), _ptr(y), _ptr(budgets), _ptr(exact),
                 ctypes.byref(fl) if fl is not None else None)
         if dbg is not None:
@@ -258,12 +284,13 @@ def multihead_forward(weights: AttentionWeights, q, k, x, cfg: McaConfig | None 
 
 def regular_forward(weights: AttentionWeights, q, k, x, scale: float = 0.0, y: torch.Tensor | None = None,
                     stream=None) -> torch.Tensor:
-    """Exact Y = softmax(a Q K^T) (X W_V)."""
+    """Exact Y = softmax(a Q K^T) (X W_V); q = k = None with
+    projection-carrying weights, as in mca_forward."""
     B, n = _check_inputs(weights, q, k, x)
     if y is None:
-        y = torch.empty_like(q)
-    with torch.cuda.device(q.device):
-        _check(L.lib().mca_regular_forward(weights.handle, _ptr(q), _ptr(k), _ptr(x), _dt(q), B, n, float(scale),
+        y = torch.empty((B, n, weights.heads * weights.d_h), dtype=x.dtype, device=x.device)
+    with torch.cuda.device(x.device):
+        _check(L.lib().mca_regular_forward(weights.handle, _ptr(q), _ptr(k), _ptr(x), _dt(x), B, n, float(scale),
                                            _ptr(y), _stream(stream)))
     return y
 

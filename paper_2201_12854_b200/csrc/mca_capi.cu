@@ -7,6 +7,7 @@
 //
 // Unity build: the kernel translation units are included here so one nvcc
 // invocation produces libmca_b200.so (no relocatable device code needed).
+#include <cublas_v2.h>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
@@ -137,6 +138,10 @@ struct mca_weights {
     float* invp = nullptr;        // [heads, d_in]
     uint16_t* guide = nullptr;    // [heads, kGuide]
     void* wprime = nullptr;       // bf16 path: [d_in, heads*dh] W_h / p (k3t's B operand)
+    void* wqk = nullptr;          // optional [2][d_in][heads*dh] W_q, W_k (mca_set_projections)
+    cublasHandle_t blas = nullptr;
+    void* qk = nullptr;           // [2][B*n][heads*dh] projected q, k (workspace, grown on demand)
+    long cap_qk = 0;
     void* pbf = nullptr;          // bf16 path: [heads, d_in] bf16 p
     // workspace (grown on demand)
     long cap_tokens = 0;          // capacity in B*n tokens
@@ -432,6 +437,9 @@ void mca_weights_free(mca_weights* w) {
     cudaFree(w->guide);
     cudaFree(w->wprime);
     cudaFree(w->pbf);
+    cudaFree(w->wqk);
+    cudaFree(w->qk);
+    if (w->blas) cublasDestroy(w->blas);
     cudaFree(w->counters);
     cudaFree(w->hist);
     cudaFree(w->cursor);
@@ -440,6 +448,21 @@ void mca_weights_free(mca_weights* w) {
     for (auto& e : w->ev)
         if (e) cudaEventDestroy(e);
     delete w;
+}
+
+mca_status mca_set_projections(mca_weights* w, const void* w_q, const void* w_k, mca_stream_t stream) {
+    if (!w || !w_q || !w_k) return fail(MCA_ERR_NULL, "weights / w_q / w_k is NULL");
+    const size_t bytes = (size_t)w->d_in * w->heads * w->dh * dtype_size(w->wdt);
+    if (!w->wqk && cudaMalloc(&w->wqk, 2 * bytes) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(MCA_ERR_ALLOC, "W_q / W_k allocation failed");
+    }
+    if (!w->blas) {
+        if (cublasCreate(&w->blas) != CUBLAS_STATUS_SUCCESS) return fail(MCA_ERR_CUDA, "cublasCreate failed");
+    }
+    MCA_CUDA_TRY(cudaMemcpyAsync(w->wqk, w_q, bytes, cudaMemcpyDeviceToDevice, stream));
+    MCA_CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(w->wqk) + bytes, w_k, bytes, cudaMemcpyDeviceToDevice, stream));
+    return MCA_OK;
 }
 
 mca_status mca_weights_export(const mca_weights* w, double* probs_host, double* cdf_host) {
@@ -521,15 +544,45 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
         w->last_launches = 0;
         return MCA_OK;
     }
-    if (!q || !k || !x || !y) return fail(MCA_ERR_NULL, "q / k / x / y is NULL");
+    if (!x || !y || (!q) != (!k)) return fail(MCA_ERR_NULL, "x / y is NULL, or only one of q / k is");
+    if (!q && !w->wqk) return fail(MCA_ERR_NULL, "q / k are NULL and the weights carry no W_q / W_k");
     const long tokens = (long)B * n;
     if (mca_status s = ensure_workspace(w, tokens, stream)) return s;
     const int H = w->heads;
+    int launches = 0;
+    if (w->timing) MCA_CUDA_TRY(cudaEventRecord(w->ev[0], stream));   // the score stage includes the projection
+    if (!q) {   // q = x W_q, k = x W_k: one strided-batched GEMM (row-major C = X W as col-major C^T = W^T X^T)
+        const size_t HD = (size_t)H * w->dh, esz = dtype_size(dt);
+        if (tokens > w->cap_qk) {
+            if (w->cap_qk) MCA_CUDA_TRY(cudaStreamSynchronize(stream));
+            cudaFree(w->qk);
+            w->qk = nullptr;
+            w->cap_qk = 0;
+            if (cudaMalloc(&w->qk, 2 * (size_t)tokens * HD * esz) != cudaSuccess) {
+                cudaGetLastError();
+                return fail(MCA_ERR_ALLOC, "q / k workspace allocation failed");
+            }
+            w->cap_qk = tokens;
+        }
+        const float one = 1.0f, zero = 0.0f;
+        const cudaDataType_t ty = dt == MCA_BF16 ? CUDA_R_16BF : CUDA_R_32F;
+        const cublasComputeType_t ct = dt == MCA_BF16 ? CUBLAS_COMPUTE_32F : CUBLAS_COMPUTE_32F_PEDANTIC;
+        if (cublasSetStream(w->blas, stream) != CUBLAS_STATUS_SUCCESS ||
+            cublasGemmStridedBatchedEx(w->blas, CUBLAS_OP_N, CUBLAS_OP_N, (int)HD, (int)tokens, w->d_in, &one, w->wqk,
+                                       ty, (int)HD, (long long)w->d_in * HD, x, ty, w->d_in, 0, &zero, w->qk, ty,
+                                       (int)HD, (long long)tokens * HD, 2, ct,
+                                       CUBLAS_GEMM_DEFAULT) != CUBLAS_STATUS_SUCCESS)
+            return fail(MCA_ERR_CUDA, "q / k projection GEMM failed");
+        q = w->qk;
+        k = static_cast<const char*>(w->qk) + (size_t)tokens * HD * esz;
+        if (dbg && dbg->q_out)
+            MCA_CUDA_TRY(cudaMemcpyAsync(dbg->q_out, q, (size_t)tokens * HD * esz, cudaMemcpyDeviceToDevice, stream));
+        if (dbg && dbg->k_out)
+            MCA_CUDA_TRY(cudaMemcpyAsync(dbg->k_out, k, (size_t)tokens * HD * esz, cudaMemcpyDeviceToDevice, stream));
+    }
     const long th = tokens * H;
     const double scale = cfg->scale > 0.0 ? cfg->scale : 1.0 / std::sqrt((double)w->dh);
-    int launches = 0;
 
-    if (w->timing) MCA_CUDA_TRY(cudaEventRecord(w->ev[0], stream));
     if (dt == MCA_F32 || force_simt() || n > k1tc::kMaxN)   // atomicMax column keys (the TC pass writes each once)
         MCA_CUDA_TRY(cudaMemsetAsync(w->colkey, 0, th * sizeof(unsigned long long), stream));
     MCA_CUDA_TRY(cudaMemsetAsync(w->counters, 0, 8 * sizeof(unsigned long long), stream));

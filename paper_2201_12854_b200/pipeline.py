@@ -3,7 +3,8 @@ serving process makes when activations live in host memory).
 
 The batch is split into chunks of `chunk` sequences; chunk c runs
 
-    h2d stream:     q, k, x (pinned host) -> device slot c % depth
+    h2d stream:     x (and q, k unless the weights project them) pinned host
+                    -> device slot c % depth
     compute stream: the MCA layer stack on that slot (libmca_b200 kernels)
     d2h stream:     y -> pinned host
 
@@ -34,6 +35,7 @@ class HostPipeline:
             raise ValueError("stacked layers feed y back as x: need d_in == heads * d_h")
         mk = lambda c: torch.empty((self.chunk, self.n, c), dtype=dtype, device=self.device)  # noqa: E731
         self.slots = [dict(q=mk(HD), k=mk(HD), x=mk(d_in), y=mk(HD), y2=mk(HD)) for _ in range(self.depth)]
+        self.project = all(w.has_projections for w in layers)
         self.s_h2d = torch.cuda.Stream(self.device)
         self.s_comp = torch.cuda.Stream(self.device)
         self.s_d2h = torch.cuda.Stream(self.device)
@@ -41,14 +43,17 @@ class HostPipeline:
         self.loaded, self.computed, self.freed = ev(), ev(), ev()
         self.used = [False] * self.depth
 
-    def forward(self, hq: torch.Tensor, hk: torch.Tensor, hx: torch.Tensor, hy: torch.Tensor,
+    def forward(self, hq: torch.Tensor | None, hk: torch.Tensor | None, hx: torch.Tensor, hy: torch.Tensor,
                 cfg: McaConfig | None = None, seed: int = 0, b_offset: int = 0) -> None:
-        """hq, hk: [B, n, H*64], hx: [B, n, d_in] pinned host tensors; writes hy
+        """hq, hk: [B, n, H*64] (None: the weights carry W_q / W_k and only x is
+        transferred), hx: [B, n, d_in] pinned host tensors; writes hy
         [B, n, H*64] (pinned host). Asynchronous: returns once the work is
         enqueued; the d2h stream's completion (`self.s_d2h`) marks hy ready."""
-        B = hq.shape[0]
-        if hq.shape[1] != self.n or B % self.chunk:
-            raise ValueError(f"batch [{B}, {hq.shape[1]}] does not split into chunks of {self.chunk} x {self.n}")
+        B = hx.shape[0]
+        if hq is None and not self.project:
+            raise ValueError("q / k omitted but the layers carry no W_q / W_k")
+        if hx.shape[1] != self.n or B % self.chunk:
+            raise ValueError(f"batch [{B}, {hx.shape[1]}] does not split into chunks of {self.chunk} x {self.n}")
         cur = torch.cuda.current_stream(self.device)
         for st in (self.s_h2d, self.s_comp, self.s_d2h):
             st.wait_stream(cur)
@@ -59,8 +64,9 @@ class HostPipeline:
             with torch.cuda.stream(self.s_h2d):
                 if self.used[i]:
                     self.s_h2d.wait_event(self.freed[i])          # the slot's previous read-back finished
-                sl["q"].copy_(hq[rows], non_blocking=True)
-                sl["k"].copy_(hk[rows], non_blocking=True)
+                if hq is not None:
+                    sl["q"].copy_(hq[rows], non_blocking=True)
+                    sl["k"].copy_(hk[rows], non_blocking=True)
                 sl["x"].copy_(hx[rows], non_blocking=True)
                 self.loaded[i].record(self.s_h2d)
             with torch.cuda.stream(self.s_comp):
@@ -68,7 +74,8 @@ class HostPipeline:
                 xin, bufs = sl["x"], (sl["y"], sl["y2"])
                 for l, w in enumerate(self.layers):
                     out = bufs[l & 1]
-                    mca_forward(w, sl["q"], sl["k"], xin, cfg, seed, b_offset=b_offset + c * self.chunk, layer=l,
+                    qq, kk = (sl["q"], sl["k"]) if hq is not None else (None, None)
+                    mca_forward(w, qq, kk, xin, cfg, seed, b_offset=b_offset + c * self.chunk, layer=l,
                                 y=out, stream=self.s_comp)
                     xin = out
                 self.computed[i].record(self.s_comp)

@@ -410,3 +410,39 @@ def test_host_pipeline_matches_forward(mca, syn):
         pipe.forward(hq, hk, hx, hy, cfg, seed=5, b_offset=3)   # slots reused across calls
         torch.cuda.synchronize()
         assert torch.equal(hy, ref_x.cpu()), L
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_projection_path(mca, syn, dtype):
+    """Weights carrying W_q / W_k (SPEC AttentionWeights{w_q, w_k, w}): the
+    x-only forward projects q = x W_q, k = x W_k on the device (checked
+    against a torch fp64 matmul), then runs exactly the q/k forward on them
+    (bitwise equal outputs); the x-only HostPipeline matches too."""
+    H, n, d_in, B = 12, 128, 768, 4
+    g = torch.Generator().manual_seed(11)
+    w_v = syn.make_weights(d_in, H).to(dtype).cuda()
+    w_q = (torch.randn((d_in, H * 64), generator=g) / d_in ** 0.5).to(dtype).cuda()
+    w_k = (torch.randn((d_in, H * 64), generator=g) / d_in ** 0.5).to(dtype).cuda()
+    x = syn.make_inputs(B, n, d_in, H).x.to(dtype).cuda()
+    weights = mca.AttentionWeights(w_v, heads=H, w_q=w_q, w_k=w_k)
+    q_out, k_out = torch.empty((B, n, H * 64), dtype=dtype, device="cuda"), torch.empty((B, n, H * 64), dtype=dtype,
+                                                                                       device="cuda")
+    cfg = mca.McaConfig(alpha=0.4)
+    y = mca.mca_forward(weights, None, None, x, cfg, seed=3, debug=dict(q_out=q_out, k_out=k_out)).y
+    torch.cuda.synchronize()
+    for got, wm in ((q_out, w_q), (k_out, w_k)):
+        ref = x.double() @ wm.double()
+        tol = 1e-5 if dtype == torch.float32 else 1e-2
+        assert _row_rel(_np(got), ref.cpu().numpy()) <= tol
+    plain = mca.AttentionWeights(w_v, heads=H)
+    y2 = mca.mca_forward(plain, q_out, k_out, x, cfg, seed=3).y
+    assert torch.equal(y, y2)
+    # regular mode through the projections equals regular_forward on the projected q, k
+    assert torch.equal(mca.regular_forward(weights, None, None, x), mca.regular_forward(plain, q_out, k_out, x))
+    if dtype == torch.bfloat16:
+        hx = x.cpu().pin_memory()
+        hy = torch.empty((B, n, H * 64), dtype=dtype).pin_memory()
+        pipe = mca.HostPipeline([weights], n, chunk=2, dtype=dtype)
+        pipe.forward(None, None, hx, hy, cfg, seed=3)
+        torch.cuda.synchronize()
+        assert torch.equal(hy, y.cpu())
