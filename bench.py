@@ -3,10 +3,14 @@
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                   [--config c2|c1|c3|c4] [--alpha A] [--dtype bf16|f32]
 
-One step = one MCA attention-layer forward (score pass + Eq. 9 budgets +
-sampled encoding + A.H~) over one batch of synthetic BERT-shaped inputs
-already resident in HBM. Default workload: BASELINE.json configs[1] — BERT-base
-(d=768, 12 heads of 64), B=64 sequences of n=512 per GPU, bf16, alpha=0.4.
+One step = one MCA attention-layer forward over one batch of synthetic
+BERT-shaped inputs already resident in HBM: the Q/K projections (q = x W_q,
+k = x W_k: the reference's mca_forward(x, weights) takes x),
+the score pass + Eq. 9 budgets, the sampled encoding and A.H~. Default
+workload: BASELINE.json configs[1] — BERT-base (d=768, 12 heads of 64), B=64
+sequences of n=512 per GPU, bf16, alpha=0.4. `--inputs qkx` gives q and k as
+inputs instead (the default for the 24-layer c3 stack, whose layers chain
+y -> x).
 
 Multi-GPU (torchrun, one process per GPU): every rank runs its own B=64
 sequences with b_offset = rank*B (weak scaling; no collective in the hot
@@ -16,9 +20,10 @@ validation.
 
 The JSON line also carries:
   e2e           the same metric through the C ABI with HOST buffers: pinned
-                H2D of q/k/x, forward, D2H of y inside the timed region, every
-                step (HostPipeline: batch chunks whose copies and forward
-                overlap on three streams)
+                H2D of the step's inputs (x; q, k too with --inputs qkx), the
+                forward, D2H of y inside the timed region, every step
+                (HostPipeline: 4 batch chunks whose copies and forward overlap
+                on three streams)
   roofline      the dominant kernel's achieved algorithmic GB/s or TFLOP/s vs
                 MEASURED_PEAKS.json (DESIGN.md §7 defines the per-unit work)
   cpu_baseline  the fp64 CPU oracle (the reference algorithm, test
@@ -42,6 +47,11 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "MCA attn-layer tokens/sec @BERT-base/large 1/2/4/8 B200; HBM GB/s frac; FLOP cut"
+
+INPUTS_DESC = {
+    "qkx": "q, k, x (the caller's Q/K projections given)",
+    "x": "x only; q = x W_q, k = x W_k on the device (the reference's mca_forward(x, weights))",
+}
 
 CONFIGS = {
     # name: (B per GPU, n, d_in, heads, description)
@@ -107,9 +117,12 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------- CPU legs
-def cpu_reference_rate(cfg_name: str, alpha: float, budget_s: float, threads: int):
+def cpu_reference_rate(cfg_name: str, alpha: float, budget_s: float, threads: int, inputs: str = "qkx"):
     """Tokens/s of the fp64 CPU oracle (oracle/, the reference algorithm) on a
-    bounded sample of the workload: whole sequences until ~budget_s seconds."""
+    bounded sample of the workload: whole sequences until ~budget_s seconds.
+    inputs == "x": the projections q = x W_q, k = x W_k are part of the timed
+    work (numpy fp64 matmul on all threads, a strong CPU GEMM)."""
+    import numpy as np
     from oracle import oracle as orc
     from paper_2201_12854_b200 import synthetic
     B, n, d_in, H, _ = CONFIGS[cfg_name]
@@ -118,14 +131,22 @@ def cpu_reference_rate(cfg_name: str, alpha: float, budget_s: float, threads: in
     done_tokens, t_total, b = 0, 0.0, 0
     per = max(1, threads)  # sequences per call: keep every thread busy on (b, h) pairs
     while t_total < budget_s and b < 4 * B:
-        inp = synthetic.make_inputs(per, n, d_in, H, seed=1234 + b)
-        q, k, x = (t.double().numpy() for t in (inp.q, inp.k, inp.x))
-        t0 = time.perf_counter()
+        if inputs == "x":
+            pin = synthetic.make_projected_inputs(per, n, d_in, H, seed=1234 + b)
+            x, wq, wk = (t.double().numpy() for t in (pin.x, pin.w_q, pin.w_k))
+            t0 = time.perf_counter()
+            q, k = np.matmul(x, wq), np.matmul(x, wk)
+        else:
+            inp = synthetic.make_inputs(per, n, d_in, H, seed=1234 + b)
+            q, k, x = (t.double().numpy() for t in (inp.q, inp.k, inp.x))
+            t0 = time.perf_counter()
         orc.batched_forward(q, k, x, w, heads=H, alpha=alpha, seed=42, b_offset=b, want_h=False)
         t_total += time.perf_counter() - t0
         done_tokens += per * n
         b += per
-    return done_tokens / t_total, f"{b} sequences of n={n} ({done_tokens} tokens), fp64, {threads} threads", t_total
+    proj = " incl. q = x W_q, k = x W_k (numpy)" if inputs == "x" else ""
+    return (done_tokens / t_total, f"{b} sequences of n={n} ({done_tokens} tokens){proj}, fp64, {threads} threads",
+            t_total)
 
 
 def run_reference(args, rank: int):
@@ -136,7 +157,7 @@ def run_reference(args, rank: int):
     per_step_budget = max(2.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
     rates = []
     for i in range(args.warmup + args.steps):
-        r, sample, _ = cpu_reference_rate(args.config, args.alpha, per_step_budget, threads)
+        r, sample, _ = cpu_reference_rate(args.config, args.alpha, per_step_budget, threads, args.inputs)
         if i >= args.warmup:
             rates.append(r)
     value = statistics.median(rates)
@@ -144,7 +165,7 @@ def run_reference(args, rank: int):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * B * n / value,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": desc, "B": B, "n": n, "d_in": d_in, "heads": H, "d_h": 64, "alpha": args.alpha,
-                       "seed": 42},
+                       "seed": 42, "inputs": INPUTS_DESC[args.inputs]},
             "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "port",
                              "sample": sample},
             "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -154,12 +175,13 @@ def run_reference(args, rank: int):
 
 
 # ---------------------------------------------------------------- GPU leg
-def algorithmic_work(B, n, d_in, H, elem):
+def algorithmic_work(B, n, d_in, H, elem, project: bool = False):
     dh = 64
     flops_qk = 2.0 * B * H * n * n * dh
+    flops_proj = 2.0 * 2.0 * B * n * d_in * H * dh if project else 0.0   # q = x W_q, k = x W_k
     k3_bytes = B * n * d_in * elem + B * n * H * dh * elem + 4.0 * B * H * n + H * d_in * (dh * elem + 12)
     k2_bytes = B * H * n * (8 + 4 + 1)
-    return {"score": ("tensor", flops_qk), "budgets": ("hbm", k2_bytes), "encode": ("hbm", k3_bytes),
+    return {"score": ("tensor", flops_qk + flops_proj), "budgets": ("hbm", k2_bytes), "encode": ("hbm", k3_bytes),
             "apply": ("tensor", flops_qk)}
 
 
@@ -186,12 +208,24 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     # Philox counter word `layer = l`, and X_{l+1} = Y_l chains the stack.
     wl = [synthetic.make_weights(d_in, H, seed=1234 + l).to(dtype) for l in range(L)]
     w = wl[0]
-    inp = synthetic.make_inputs(B, n, d_in, H, seed=1234 + rank)  # rank's own shard of the global batch
-    layer_weights = [mca.AttentionWeights(t.to(dev), heads=H) for t in wl]
+    project = args.inputs == "x"
+    if project:   # x in, W_q / W_k with the weights: the reference's mca_forward(x, weights, ...)
+        if L != 1:
+            raise SystemExit("--inputs x runs one layer (the synthetic projections model layer-0 statistics)")
+        pin = synthetic.make_projected_inputs(B, n, d_in, H, seed=1234 + rank)
+        layer_weights = [mca.AttentionWeights(wl[0].to(dev), heads=H, w_q=pin.w_q.to(dtype).to(dev),
+                                              w_k=pin.w_k.to(dtype).to(dev))]
+        q = k = None
+        x = pin.x.to(dtype).to(dev)
+        host_inputs = (pin.x,)
+    else:
+        inp = synthetic.make_inputs(B, n, d_in, H, seed=1234 + rank)  # rank's own shard of the global batch
+        layer_weights = [mca.AttentionWeights(t.to(dev), heads=H) for t in wl]
+        q, k, x = (t.to(dtype).to(dev) for t in (inp.q, inp.k, inp.x))
+        host_inputs = (inp.q, inp.k, inp.x)
     weights = layer_weights[0]
-    q, k, x = (t.to(dtype).to(dev) for t in (inp.q, inp.k, inp.x))
-    y = torch.empty_like(q)
-    ybuf = [torch.empty_like(q), torch.empty_like(q)]
+    y = torch.empty((B, n, H * 64), dtype=dtype, device=dev)
+    ybuf = [torch.empty_like(y), torch.empty_like(y)]
     cfg = mca.McaConfig(alpha=args.alpha)
     b_offset = rank * B
     for lw in layer_weights:
@@ -255,9 +289,14 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     # e2e: host buffers through the package's pipelined host API (HostPipeline:
     # every step copies its q, k, x from pinned host memory and reads y back,
     # in chunks whose H2D / forward / D2H overlap on three streams)
-    hq, hk, hx = (t.to(dtype).pin_memory() for t in (inp.q, inp.k, inp.x))
+    if project:
+        hq = hk = None
+        hx = pin.x.to(dtype).pin_memory()
+    else:
+        hq, hk, hx = (t.to(dtype).pin_memory() for t in (inp.q, inp.k, inp.x))
     hy = torch.empty(y.shape, dtype=dtype).pin_memory()
-    chunk = B // 8 if B >= 8 and B % 8 == 0 else B
+    nch = args.e2e_chunks if B % args.e2e_chunks == 0 else 1
+    chunk = B // nch
     pipe = HostPipeline(layer_weights, n, chunk, dtype, dev)
 
     def e2e_step():
@@ -296,7 +335,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         return
 
     peaks = _peaks()
-    work = {k: (v[0], v[1] * L) for k, v in algorithmic_work(B, n, d_in, H, elem).items()}   # per step (L layers)
+    work = {k: (v[0], v[1] * L) for k, v in algorithmic_work(B, n, d_in, H, elem, project).items()}   # per step
     names = ["score", "budgets", "encode", "apply"]
     stage_ms = {names[i]: stage_tot[i] / args.steps for i in range(4)}
     dom = max(names, key=lambda s: stage_ms[s])
@@ -324,7 +363,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     cpu = None
     if not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
-        rate, sample, _ = cpu_reference_rate(args.config, args.alpha, args.cpu_seconds, threads)
+        rate, sample, _ = cpu_reference_rate(args.config, args.alpha, args.cpu_seconds, threads, args.inputs)
         cpu = {"value": rate, "unit": "tokens/s (one layer)", "cores": threads, "kind": "port", "sample": sample}
 
     line = {
@@ -333,9 +372,10 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
         "config": {"workload": desc, "layers": L, "global_batch": world * B, "B_per_gpu": B, "seq_len": n, "d_in": d_in,
                    "heads": H, "d_h": 64, "alpha": args.alpha, "seed": 42, "parallelism": f"dp{world} (batch shards)",
-                   "l2": "flushed (256 MB write) before every timed step"},
+                   "l2": "flushed (256 MB write) before every timed step", "inputs": INPUTS_DESC[args.inputs]},
         "e2e": {"value": world * B * n * L / (e2e_ms / 1e3), "unit": "tokens/s",
-                "h2d_bytes_per_step": int(3 * q.numel() * elem), "d2h_bytes_per_step": int(y.numel() * elem)},
+                "h2d_bytes_per_step": int(sum(t.numel() for t in host_inputs) * elem),
+                "d2h_bytes_per_step": int(y.numel() * elem)},
         "roofline": roof,
         "stages_ms": stage_ms,
         "encode": {"algorithmic_GBps": enc_gbs, "hbm_frac": enc_gbs / peaks["hbm_gbs"], "gather_GBps": gather_gbs,
@@ -365,10 +405,16 @@ def main():
     ap.add_argument("--batch", type=int, default=0, help="override B per GPU")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-chunks", type=int, default=4, help="HostPipeline chunks per step (e2e leg)")
+    ap.add_argument("--inputs", default=None, choices=sorted(INPUTS_DESC),
+                    help="x: x alone, q/k projected on the device (default for one-layer configs: the "
+                         "reference's mca_forward(x, weights)); qkx: q, k, x given (default for the c3 stack)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.layers <= 0:
         args.layers = 24 if args.config == "c3" else 1
+    if args.inputs is None:
+        args.inputs = "x" if args.layers == 1 else "qkx"
     if args.batch > 0:
         B, n, d_in, H, desc = CONFIGS[args.config]
         CONFIGS[args.config] = (args.batch, n, d_in, H, desc + f" [B overridden to {args.batch}]")
