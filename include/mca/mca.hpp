@@ -4,7 +4,9 @@
 // so C++ callers of the reference can switch:
 //
 //   reference (SPEC op)                          here
-//   AttentionWeights{w, cached_dist}  :260-265   mca::b200::AttentionWeights (W_V on device + K0 tables)
+//   AttentionWeights{w_q, w_k, w, cached_dist}   mca::b200::AttentionWeights (W_V on device + K0 tables,
+//                                     :260-265   optionally W_q / W_k)
+//   mca_forward(x, weights, cfg, seed)  :306-314 mca::b200::mca_forward(x, weights, cfg, seed) (x alone)
 //   McaConfig{alpha, mode, min_samples, heads}   mca::b200::McaConfig
 //   multihead_forward(x, heads, cfg, seed)       mca::b200::multihead_forward(q, k, x, w, cfg, seed)
 //   mca_forward / regular_forward                same, cfg.mode approximation / regular
@@ -74,23 +76,37 @@ class AttentionWeights {
     // From a host fp64 Matrix (d_in x heads*64): uploaded as fp32 (parity precision).
     AttentionWeights(const Matrix& w_v, int heads, cudaStream_t stream = nullptr)
         : dtype_(MCA_F32), d_in_(static_cast<int>(w_v.rows)), heads_(heads) {
-        if (heads <= 0 || w_v.cols != static_cast<std::size_t>(heads) * 64)
-            throw std::invalid_argument("mca: w_v must be d_in x heads*64");
-        std::vector<float> f(w_v.data.begin(), w_v.data.end());
-        void* d = nullptr;
-        cuda_check(cudaMalloc(&d, f.size() * sizeof(float)), "cudaMalloc");
-        cudaError_t e = cudaMemcpy(d, f.data(), f.size() * sizeof(float), cudaMemcpyHostToDevice);
-        if (e != cudaSuccess) {
-            cudaFree(d);
-            cuda_check(e, "cudaMemcpy");
-        }
+        check_shape(w_v);
+        void* d = upload_f32(w_v);
         const mca_status s = mca_prepare_weights(d, MCA_F32, d_in_, heads, 64, stream, &h_);
         cudaFree(d);  // the handle keeps its own copy
         check(s);
     }
+    // SPEC's AttentionWeights{w_q, w_k, w}: host fp64 matrices (all d_in x heads*64),
+    // uploaded as fp32; forwards then take x alone.
+    AttentionWeights(const Matrix& w_q, const Matrix& w_k, const Matrix& w_v, int heads, cudaStream_t stream = nullptr)
+        : AttentionWeights(w_v, heads, stream) {
+        check_shape(w_q);
+        check_shape(w_k);
+        void* dq = upload_f32(w_q);
+        void* dk = upload_f32(w_k);
+        const mca_status s = mca_set_projections(h_, dq, dk, stream);
+        cudaStreamSynchronize(stream);
+        cudaFree(dq);
+        cudaFree(dk);
+        check(s);
+        projections_ = true;
+    }
+    // Attach device W_q / W_k (this handle's dtype, d_in x heads*64).
+    void set_projections(const void* w_q_device, const void* w_k_device, cudaStream_t stream = nullptr) {
+        check(mca_set_projections(h_, w_q_device, w_k_device, stream));
+        projections_ = true;
+    }
+    bool has_projections() const { return projections_; }
     AttentionWeights(const AttentionWeights&) = delete;
     AttentionWeights& operator=(const AttentionWeights&) = delete;
-    AttentionWeights(AttentionWeights&& o) noexcept : h_(o.h_), dtype_(o.dtype_), d_in_(o.d_in_), heads_(o.heads_) {
+    AttentionWeights(AttentionWeights&& o) noexcept
+        : h_(o.h_), dtype_(o.dtype_), d_in_(o.d_in_), heads_(o.heads_), projections_(o.projections_) {
         o.h_ = nullptr;
     }
     ~AttentionWeights() { mca_weights_free(h_); }
@@ -108,13 +124,30 @@ class AttentionWeights {
     }
 
    private:
+    void check_shape(const Matrix& m) const {
+        if (heads_ <= 0 || m.cols != static_cast<std::size_t>(heads_) * 64 || m.rows != static_cast<std::size_t>(d_in_))
+            throw std::invalid_argument("mca: weight matrices must be d_in x heads*64");
+    }
+    static void* upload_f32(const Matrix& m) {
+        std::vector<float> f(m.data.begin(), m.data.end());
+        void* d = nullptr;
+        cuda_check(cudaMalloc(&d, f.size() * sizeof(float)), "cudaMalloc");
+        cudaError_t e = cudaMemcpy(d, f.data(), f.size() * sizeof(float), cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) {
+            cudaFree(d);
+            cuda_check(e, "cudaMemcpy");
+        }
+        return d;
+    }
     mca_weights* h_ = nullptr;
     mca_dtype dtype_;
     int d_in_, heads_;
+    bool projections_ = false;
 };
 
 // ---------------------------------------------------------------- device level
 // q, k, y: [B, n, heads*64]; x: [B, n, d_in] device buffers in w.dtype().
+// q = k = nullptr with projection-carrying weights: q, k are computed from x.
 inline FlopsReport forward_device(const AttentionWeights& w, const void* q, const void* k, const void* x, int B, int n,
                                   const McaConfig& cfg, uint64_t seed, void* y, int32_t* budgets = nullptr,
                                   uint8_t* exact = nullptr, bool want_flops = false, long b_offset = 0,
@@ -177,6 +210,31 @@ inline AttentionOutput multihead_forward(const Matrix& q, const Matrix& k, const
     out.flops = forward_device(w, dq.p, dk.p, dx.p, 1, static_cast<int>(n), cfg, seed, dy.p,
                                static_cast<int32_t*>(db.p), static_cast<uint8_t*>(de.p), true);
     std::vector<float> y(q.data.size());
+    cuda_check(cudaMemcpy(y.data(), dy.p, y.size() * 4, cudaMemcpyDeviceToHost), "cudaMemcpy D2H");
+    out.y.rows = n;
+    out.y.cols = H * 64;
+    out.y.data.assign(y.begin(), y.end());
+    out.budgets.resize(H * n);
+    out.exact_mask.resize(H * n);
+    cuda_check(cudaMemcpy(out.budgets.data(), db.p, H * n * 4, cudaMemcpyDeviceToHost), "cudaMemcpy D2H");
+    cuda_check(cudaMemcpy(out.exact_mask.data(), de.p, H * n, cudaMemcpyDeviceToHost), "cudaMemcpy D2H");
+    return out;
+}
+
+// mca_forward(x, weights, cfg, seed) for one sequence with
+// projection-carrying weights: x is n x d_in; returns y (n x heads*64).
+inline AttentionOutput mca_forward(const Matrix& x, const AttentionWeights& w, const McaConfig& cfg, uint64_t seed) {
+    if (!w.has_projections()) throw std::invalid_argument("mca: mca_forward(x, w) needs weights with W_q / W_k");
+    if (cfg.mode != Mode::approximation) throw std::runtime_error("mca: mca_forward requires approximation mode");
+    if (w.dtype() != MCA_F32) throw std::invalid_argument("mca: Matrix-level forward needs fp32 weights");
+    const std::size_t H = static_cast<std::size_t>(w.heads()), n = x.rows;
+    if (x.cols != static_cast<std::size_t>(w.d_in())) throw std::invalid_argument("mca: x must be n x d_in");
+    detail::DeviceBuf dx(x.data.size() * 4), dy(n * H * 64 * 4), db(H * n * 4), de(H * n);
+    detail::upload_f32(x, dx);
+    AttentionOutput out;
+    out.flops = forward_device(w, nullptr, nullptr, dx.p, 1, static_cast<int>(n), cfg, seed, dy.p,
+                               static_cast<int32_t*>(db.p), static_cast<uint8_t*>(de.p), true);
+    std::vector<float> y(n * H * 64);
     cuda_check(cudaMemcpy(y.data(), dy.p, y.size() * 4, cudaMemcpyDeviceToHost), "cudaMemcpy D2H");
     out.y.rows = n;
     out.y.cols = H * 64;

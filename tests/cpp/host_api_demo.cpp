@@ -1,8 +1,10 @@
 // A C++ caller of the B200 MCA path through include/mca/mca.hpp (the host
 // mirror of the reference's SPEC interface over matrix.hpp's Matrix).
-// Reads q, k, x (n x ...), W_V (d x heads*64) as fp64 from argv[1], runs
-// mca_forward and regular_forward for one sequence, writes y_mca, y_exact,
-// budgets, exact_mask, flops to argv[2]. tests/test_cpp_host.py drives it.
+// Reads q, k, x (n x ...), W_V, W_q, W_k (d x heads*64) as fp64 from argv[1],
+// runs mca_forward and regular_forward for one sequence on (q, k, x), then the
+// reference's mca_forward(x, weights) with W_q / W_k on the weights, and
+// writes y_mca, y_exact, budgets, exact_mask, flops, y_x, budgets_x to
+// argv[2]. tests/test_cpp_host.py drives it.
 #include <cstdio>
 #include <cstdint>
 #include <fstream>
@@ -34,6 +36,7 @@ int main(int argc, char** argv) {
     in.read(reinterpret_cast<char*>(&seed), 8);
     in.read(reinterpret_cast<char*>(&alpha), 8);
     const mca::Matrix q = read_matrix(in), k = read_matrix(in), x = read_matrix(in), w = read_matrix(in);
+    const mca::Matrix wq = read_matrix(in), wk = read_matrix(in);
     try {
         mca::b200::AttentionWeights weights(w, static_cast<int>(heads));
         mca::b200::McaConfig cfg;
@@ -66,6 +69,11 @@ int main(int argc, char** argv) {
         const double fl[3] = {approx.flops.reduction_factor, static_cast<double>(approx.flops.samples),
                               (domain_error ? 1.0 : 0.0) + (shape_error ? 2.0 : 0.0)};
         out.write(reinterpret_cast<const char*>(fl), sizeof(fl));
+        // SPEC's AttentionWeights{w_q, w_k, w} and mca_forward(x, weights, cfg, seed)
+        mca::b200::AttentionWeights full(wq, wk, w, static_cast<int>(heads));
+        const auto viax = mca::b200::mca_forward(x, full, cfg, static_cast<uint64_t>(seed));
+        out.write(reinterpret_cast<const char*>(viax.y.data.data()), static_cast<std::streamsize>(viax.y.data.size() * 8));
+        out.write(reinterpret_cast<const char*>(viax.budgets.data()), static_cast<std::streamsize>(viax.budgets.size() * 4));
     } catch (const std::exception& e) {
         std::fprintf(stderr, "error: %s\n", e.what());
         return 1;

@@ -48,10 +48,12 @@ def test_cpp_host_api_matches_oracle(tmp_path, orc):
     q, k, x = (t[0].double().numpy() for t in (inp.q, inp.k, inp.x))
     # the C++ path computes in fp32: give the oracle the same rounded inputs
     q, k, x, w = (a.astype(np.float32).astype(np.float64) for a in (q, k, x, w))
+    # projections exact in fp32 (identity, 0.25 identity): the x-only path's q, k are x and x / 4
+    wq, wk = np.eye(d), 0.25 * np.eye(d)
     inf, outf = tmp_path / "in.bin", tmp_path / "out.bin"
     with open(inf, "wb") as f:
         f.write(struct.pack("<qqd", H, 42, 0.4))
-        for m in (q, k, x, w):
+        for m in (q, k, x, w, wq, wk):
             _write_matrix(f, m)
     subprocess.run([exe, str(inf), str(outf)], check=True)
     raw = open(outf, "rb").read()
@@ -73,3 +75,10 @@ def test_cpp_host_api_matches_oracle(tmp_path, orc):
     assert rel.max() <= 1e-5
     assert rf == pytest.approx(ref.flops.reduction_factor)
     assert int(errs) == 3          # std::domain_error for alpha = 0, std::invalid_argument for a bad shape
+    off += 24
+    yx = np.frombuffer(raw[off: off + ny * 8], dtype=np.float64).reshape(n, H * 64)
+    bx = np.frombuffer(raw[off + ny * 8: off + ny * 8 + H * n * 4], dtype=np.int32).reshape(H, n)
+    refx = orc.batched_forward(x[None], 0.25 * x[None], x[None], w, heads=H, alpha=0.4, seed=42)
+    assert np.array_equal(bx, refx.budgets[0])
+    rel = np.linalg.norm(yx - refx.y[0], axis=1) / np.linalg.norm(refx.y[0], axis=1)
+    assert rel.max() <= 1e-5
