@@ -17,7 +17,9 @@ for r in rows[hdr + 1:]:
               "second": v * 1e6, "s": v * 1e6}.get(unit, v)
         name = r[ki].split("(")[0].replace("void ", "")[:48]
         d.setdefault(name, []).append(us)
-per_forward = lambda k: k.split("::")[-1].startswith("k") and "k0_" not in k   # our kernels; K0 is one-time weight prep
+# everything inside the NVTX "mca_step" range is the forward (ours + the cuBLAS
+# projection GEMM); K0 is one-time weight preparation (outside the range)
+per_forward = lambda k: "k0_" not in k and "elementwise" not in k
 tot = sum(sum(v) / len(v) for k, v in d.items() if per_forward(k))
 print(f"{'kernel':50s} {'launches':>8s} {'mean_us':>9s} {'share':>6s}")
 for k, v in d.items():

@@ -26,7 +26,7 @@ METRICS = [
 ]
 UNIT = {"second": 1.0, "s": 1.0, "msecond": 1e-3, "ms": 1e-3, "usecond": 1e-6, "us": 1e-6, "nsecond": 1e-9, "ns": 1e-9, "byte": 1.0, "Kbyte": 1e3,
         "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "inst": 1.0, "Kinst": 1e3, "Minst": 1e6, "Ginst": 1e9}
-STAGE = {"k1_scores_tc": "score", "k2_budgets": "budgets", "k3_encode_sampled": "encode", "k3t_encode_tc": "encode",
+STAGE = {"k12_fused_tc": "score", "k1_scores_tc": "score", "k2_budgets": "budgets", "k2_scan": "budgets", "k2_scatter": "budgets", "k3_encode_sampled": "encode", "k3t_encode_tc": "encode",
          "k3b_exact_tc": "encode_exact", "k4_apply_tc": "apply"}
 
 
