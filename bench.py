@@ -255,32 +255,40 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     sampler = ClockSampler(local_rank) if rank == 0 else None
     if sampler:
         sampler.start()
-    for lw in layer_weights:
-        lw.set_timing(True)
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
+    # the timed steps carry no per-stage events (an event between two kernels
+    # would stop the next one from starting early: programmatic dependent launch)
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    stage_tot = [0.0, 0.0, 0.0, 0.0]
     for i in range(args.steps):
         flush.zero_()                                   # L2 flushed between timed steps (untimed)
         starts[i].record(stream)
         step()
         ends[i].record(stream)
-        for lw in layer_weights:
-            st = lw.last_stage_ms()                     # events on the forward's own stream
-            for s in range(len(st)):
-                stage_tot[s] += st[s]
     torch.cuda.synchronize()
     total_ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
     if dist:
         t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
+    # per-stage device times (roofline / stages_ms): separate steps with the
+    # forward's stage events on, same L2 flush
+    for lw in layer_weights:
+        lw.set_timing(True)
+    stage_tot = [0.0, 0.0, 0.0, 0.0]
+    for i in range(args.steps):
+        flush.zero_()
+        step()
+        for lw in layer_weights:
+            st = lw.last_stage_ms()                     # events on the forward's own stream
+            for s in range(len(st)):
+                stage_tot[s] += st[s]
+    torch.cuda.synchronize()
     for lw in layer_weights:
         lw.set_timing(False)
     ms_per_step = total_ms / args.steps

@@ -116,6 +116,7 @@ __global__ void __maxnreg__(96)
     const int bh = blockIdx.x, b = bh / heads, h = bh - b * heads;
     const int nblk = nt * nt;
     const bool prof0 = MCA_K12_PROF && blockIdx.x == 0;
+    griddep_trigger();   // the work-list kernels may launch (they wait for this grid to complete)
     if (prof0 && threadIdx.x == 0) g_k12_prof[0] = clock64();
     const bool use_hist = a.hist != nullptr && a.d <= 1024;
 

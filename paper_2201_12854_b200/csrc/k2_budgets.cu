@@ -173,6 +173,8 @@ __global__ void __launch_bounds__(1024) k2_scan(const unsigned int* __restrict__
                                                 unsigned int* __restrict__ cursor, int* __restrict__ counts) {
     __shared__ unsigned int s[1024];
     __shared__ unsigned int carry;
+    griddep_trigger();
+    griddep_wait();      // the histograms of the budget pass
     const int h = blockIdx.x;
     const unsigned int* hh = hist + (size_t)h * (d + 1);
     unsigned int* cc = cursor + (size_t)h * (d + 1);
@@ -212,6 +214,8 @@ __global__ void __launch_bounds__(256) k2_scatter(const int32_t* __restrict__ bu
                                                   int32_t* __restrict__ samp_list, int32_t* __restrict__ exact_list) {
     const long bh = blockIdx.y;
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    griddep_trigger();
+    griddep_wait();      // the scan's cursors
     if (j >= n) return;
     const long t = bh * n + j;
     const int b = (int)(bh / heads), h = (int)(bh - (long)b * heads);

@@ -309,6 +309,7 @@ __global__ void __launch_bounds__(kK3BlockThreads, 1) k3_encode_sampled_bf16(K3A
     PackedPair* s_pairs = reinterpret_cast<PackedPair*>(smem + ((((size_t)d_in * 12 + kGuide * 2) + 127) & ~(size_t)127));
     __nv_bfloat16* s_w = reinterpret_cast<__nv_bfloat16*>(s_pairs + kK3Warps * 4 * 16);
     PackedPair* my_pairs = s_pairs + (warp * 4 + oct) * 16;
+    griddep_trigger();
 
     const size_t HD = (size_t)heads * kDh;
     const __nv_bfloat16* wv = reinterpret_cast<const __nv_bfloat16*>(a.wv);
@@ -323,6 +324,7 @@ __global__ void __launch_bounds__(kK3BlockThreads, 1) k3_encode_sampled_bf16(K3A
             *reinterpret_cast<const uint4*>(wv + (size_t)i * HD + (size_t)h * kDh + c8);
     }
     __syncthreads();
+    griddep_wait();      // W_h and the tables above are weights; the work lists come from the scatter
     const int col0 = 8 * l8;
     const int nsamp = a.counts[2 * h];
     const int32_t* list = a.samp_list + (size_t)h * a.tokens;

@@ -43,6 +43,8 @@ __global__ void __launch_bounds__(k3btc::kThreads, 2) k3b_exact_tc(K3Args a) {
     using namespace k3btc;
     using namespace mca_tc;
     const int h = blockIdx.y;
+    griddep_trigger();
+    griddep_wait();      // the exact lists (and K3's H~ writes: both encoders write disjoint rows)
     const int ne = a.counts[2 * h + 1];
     if ((int)blockIdx.x * kBM >= ne) return;           // uniform early exit, before any barrier / TMEM use
     extern __shared__ uint8_t smem_raw[];

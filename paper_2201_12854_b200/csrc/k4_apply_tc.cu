@@ -52,6 +52,10 @@ constexpr uint32_t kIdescS = mca_tc::idesc_f16(1, 0, kBM, kBK);      // bf16 Q (
 constexpr uint32_t kIdescO = mca_tc::idesc_f16(0, 1, kBM, kDh);      // fp16 P (TMEM) x fp16 H~, B MN-major
 constexpr uint32_t kOCol = 2 * kBK;                                  // O [128,192)
 constexpr uint32_t kQCol = kOCol + kDh;                              // Q [192,224): 64 bf16 per lane
+#ifndef MCA_K4_POLY
+#define MCA_K4_POLY 4
+#endif
+constexpr int kPolyPairs = MCA_K4_POLY;   // per thread and block: pairs exponentiated on the FMA pipe (of 16)
 }  // namespace k4tc
 
 // TMEM column of P's K-step kk (16 keys) in S/P buffer sb: the warp owning keys
@@ -81,6 +85,9 @@ __global__ void __launch_bounds__(k4tc::kThreads, 2)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 5);
 
     if (MCA_K4_PROF && blockIdx.x == 0 && threadIdx.x == 64) g_k4_prof[60] = clock64();
+    griddep_trigger();
+    // Q and K are inputs: their loads and the first S MMAs may run while the
+    // encoders drain; lse (score pass) and H~ (encoders) are read after griddep_wait()
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nmt = (n + kBM - 1) / kBM;                   // query tiles per (b, h)
     const int nkb = (n + kBK - 1) / kBK;
@@ -125,6 +132,7 @@ __global__ void __launch_bounds__(k4tc::kThreads, 2)
             uint64_t* empty = lane == 0 ? k_empty : h_empty;
             const uint32_t base = lane == 0 ? kSmemK : kSmemH;
             tma_prefetch(tm);
+            if (lane == 16) griddep_wait();   // H~ is the encoders' output
             for (int i = 0, g = 0; i < my_tiles; ++i) {
                 int b, h, m0;
                 tile_coords(i, b, h, m0);
@@ -188,6 +196,7 @@ __global__ void __launch_bounds__(k4tc::kThreads, 2)
         // this thread's 32 Q values (64 bytes) of tile i and its row's lse (log2 domain)
         uint32_t qv[16];
         float lse2_next = 0.f;
+        bool waited = false;
         auto load_q = [&](int i) {
             int b, h, m0;
             tile_coords(i, b, h, m0);
@@ -201,6 +210,10 @@ __global__ void __launch_bounds__(k4tc::kThreads, 2)
                     qv[4 * u + 1] = t.y;
                     qv[4 * u + 2] = t.z;
                     qv[4 * u + 3] = t.w;
+                }
+                if (!waited) {   // lse is the score pass's output
+                    griddep_wait();
+                    waited = true;
                 }
                 lse2_next = lse[((size_t)b * heads + h) * n + grow] * 1.4426950408889634f;
             } else {
@@ -240,10 +253,18 @@ __global__ void __launch_bounds__(k4tc::kThreads, 2)
                 uint32_t pk[16];
                 const int valid = n - (kb * kBK + 32 * half);
                 if (valid >= 32) {
+                    // the MUFU is this loop's bound: kPolyPairs of the 16 pairs take the FMA-pipe exp2
 #pragma unroll
-                    for (int e = 0; e < 16; ++e)
-                        pk[e] = ex2_f16x2(pack_f16x2(__fmaf_rn(__uint_as_float(sv[2 * e]), c, -lse2),
-                                                     __fmaf_rn(__uint_as_float(sv[2 * e + 1]), c, -lse2)));
+                    for (int e = 0; e < 16; ++e) {
+                        const float2 xv = __ffma2_rn(make_float2(__uint_as_float(sv[2 * e]), __uint_as_float(sv[2 * e + 1])),
+                                                     make_float2(c, c), make_float2(-lse2, -lse2));
+                        if (e < kPolyPairs) {
+                            const float2 pv = ex2_poly2(xv);
+                            pk[e] = pack_f16x2(pv.x, pv.y);
+                        } else {
+                            pk[e] = ex2_f16x2(pack_f16x2(xv.x, xv.y));
+                        }
+                    }
                 } else {
 #pragma unroll
                     for (int e = 0; e < 16; ++e) {

@@ -18,6 +18,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "mca/mca_cuda.h"
@@ -155,6 +156,7 @@ struct mca_weights {
     void* hbuf = nullptr;                     // [B, n, H*dh]
     int32_t* samp_list = nullptr;             // [H, B*n] sampled tokens per head, budget-descending
     int32_t* exact_list = nullptr;            // [H, B*n] exact tokens per head
+    void* zeroed = nullptr;                   // counters | task_cursor | hist (zeroed once per forward)
     unsigned long long* counters = nullptr;   // [8]
     unsigned int* hist = nullptr;             // [H, d_in + 1] budget histogram
     unsigned int* cursor = nullptr;           // [H, d_in + 1] scatter cursors
@@ -227,6 +229,27 @@ mca_status check_config(const mca_config* cfg, bool need_alpha) {
 }
 
 // bf16 path: K3 as a tile GEMM (k3t) when its shared-memory plan fits.
+// Launch with programmatic stream serialization (PDL): the kernel may start
+// while its stream predecessor drains; it calls griddep_wait() before reading
+// the predecessor's output (mca_common.cuh).
+template <class... KArgs, class... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                       Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
+size_t zeroed_bytes(int heads, int d_in) { return 64 + (((size_t)heads * 4 + 63) & ~(size_t)63) + (size_t)heads * (d_in + 1) * 4; }
+
 bool use_k3t(const mca_weights* w) {
     return w->wdt == MCA_BF16 && w->wprime && !force_simt() && tile_k3_requested() && w->d_in % 8 == 0 &&
            k3t::layout(w->d_in).bytes <= 227u * 1024u;
@@ -326,7 +349,8 @@ mca_status launch_k3(mca_weights* w, const void* x, int B, int n, long b_offset,
     const long cap = (a.tokens + 63) / 64;   // at most one CTA per 64 tokens of a head
     if (G > cap) G = (int)cap;
     if (G < 1) G = 1;
-    kern<<<dim3(G, w->heads), kK3BlockThreads, smem, stream>>>(a);
+    if (kern == k3_encode_sampled_bf16) MCA_CUDA_TRY(launch_pdl(kern, dim3(G, w->heads), dim3(kK3BlockThreads), smem, stream, a));
+    else kern<<<dim3(G, w->heads), kK3BlockThreads, smem, stream>>>(a);
     MCA_LAUNCH_CHECK("k3_encode_sampled");
     }
     if (sizeof(T) == 2 && !force_simt()) {   // bf16: exact token-heads on the tensor cores
@@ -341,7 +365,8 @@ mca_status launch_k3(mca_weights* w, const void* x, int B, int n, long b_offset,
         const long ecap = (a.tokens + k3btc::kBM - 1) / k3btc::kBM;
         if (Ge > ecap) Ge = (int)ecap;
         if (Ge < 1) Ge = 1;
-        k3b_exact_tc<<<dim3((unsigned)Ge, w->heads), k3btc::kThreads, k3btc::kSmemBytes, stream>>>(a);
+        MCA_CUDA_TRY(launch_pdl(k3b_exact_tc, dim3((unsigned)Ge, w->heads), dim3(k3btc::kThreads), k3btc::kSmemBytes,
+                                stream, a));
         MCA_LAUNCH_CHECK("k3b_exact_tc");
     } else {                                  // fp32 parity path: fp64 CUDA-core GEMM
         int Ge = (2 * sm_count() + w->heads - 1) / w->heads;
@@ -393,15 +418,18 @@ mca_status mca_prepare_weights(const void* w_v, mca_dtype wdt, int d_in, int hea
     if (cudaMalloc(&w->w, wbytes) != cudaSuccess || cudaMalloc(&w->probs, hd * 8) != cudaSuccess ||
         cudaMalloc(&w->cdf, hd * 8) != cudaSuccess || cudaMalloc(&w->thr, hd * 8) != cudaSuccess ||
         cudaMalloc(&w->invp, hd * 4) != cudaSuccess || cudaMalloc(&w->guide, (size_t)heads * kGuide * 2) != cudaSuccess ||
-        cudaMalloc(&w->counters, 8 * sizeof(unsigned long long)) != cudaSuccess ||
-        cudaMalloc(&w->hist, (size_t)heads * (d_in + 1) * 4) != cudaSuccess ||
+        cudaMalloc(&w->zeroed, zeroed_bytes(heads, d_in)) != cudaSuccess ||
         cudaMalloc(&w->cursor, (size_t)heads * (d_in + 1) * 4) != cudaSuccess ||
         cudaMalloc(&w->counts, heads * 2 * sizeof(int)) != cudaSuccess ||
-        cudaMalloc(&w->task_cursor, heads * sizeof(int)) != cudaSuccess || cudaMalloc(&sq, hd * 8) != cudaSuccess ||
+        cudaMalloc(&sq, hd * 8) != cudaSuccess ||
         cudaMalloc(&status, heads * sizeof(int)) != cudaSuccess) {
         cudaGetLastError();
         return cleanup(fail(MCA_ERR_ALLOC, "weight table allocation failed"));
     }
+    // counters | task cursors | budget histograms: one region, one memset per forward
+    w->counters = static_cast<unsigned long long*>(w->zeroed);
+    w->task_cursor = reinterpret_cast<int*>(static_cast<char*>(w->zeroed) + 64);
+    w->hist = reinterpret_cast<unsigned int*>(static_cast<char*>(w->zeroed) + 64 + ((heads * 4 + 63) & ~63));
     if (cudaMemcpyAsync(w->w, w_v, wbytes, cudaMemcpyDeviceToDevice, stream) != cudaSuccess)
         return cleanup(fail(MCA_ERR_CUDA, "copying w_v failed: %s", cudaGetErrorString(cudaGetLastError())));
     const dim3 g0((d_in + 255) / 256, heads);
@@ -440,11 +468,9 @@ void mca_weights_free(mca_weights* w) {
     cudaFree(w->wqk);
     cudaFree(w->qk);
     if (w->blas) cublasDestroy(w->blas);
-    cudaFree(w->counters);
-    cudaFree(w->hist);
+    cudaFree(w->zeroed);
     cudaFree(w->cursor);
     cudaFree(w->counts);
-    cudaFree(w->task_cursor);
     for (auto& e : w->ev)
         if (e) cudaEventDestroy(e);
     delete w;
@@ -585,12 +611,9 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
 
     if (dt == MCA_F32 || force_simt() || n > k1tc::kMaxN)   // atomicMax column keys (the TC pass writes each once)
         MCA_CUDA_TRY(cudaMemsetAsync(w->colkey, 0, th * sizeof(unsigned long long), stream));
-    MCA_CUDA_TRY(cudaMemsetAsync(w->counters, 0, 8 * sizeof(unsigned long long), stream));
+    MCA_CUDA_TRY(cudaMemsetAsync(w->zeroed, 0, zeroed_bytes(H, w->d_in), stream));   // counters, cursors, histograms
     const bool tile_k3 = dt == MCA_BF16 && use_k3t(w);   // k3t reads budgets directly: no work lists
-    if (!tile_k3) {
-        MCA_CUDA_TRY(cudaMemsetAsync(w->hist, 0, (size_t)H * (w->d_in + 1) * 4, stream));
-        MCA_CUDA_TRY(cudaMemsetAsync(w->task_cursor, 0, H * sizeof(int), stream));
-    }
+
 
     // K1 + K2 fused (bf16, n <= 768): both score passes and Eq. 9 in one kernel per (b, h)
     const bool fused12 = dt == MCA_BF16 && !force_simt() && n <= k12::kMaxTiles * k12::kT &&
@@ -704,10 +727,12 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
             MCA_LAUNCH_CHECK("k2_budgets");
         }
         if (!tile_k3) {
-            k2_scan<<<H, 1024, 0, stream>>>(w->hist, w->d_in, w->cursor, w->counts);
+            MCA_CUDA_TRY(launch_pdl(k2_scan, dim3(H), dim3(1024), 0, stream, (const unsigned int*)w->hist, w->d_in,
+                                    w->cursor, w->counts));
             MCA_LAUNCH_CHECK("k2_scan");
-            k2_scatter<<<grid, 256, 0, stream>>>(w->budgets, w->exact, n, H, w->d_in, tokens, w->cursor,
-                                                 w->samp_list, w->exact_list);
+            MCA_CUDA_TRY(launch_pdl(k2_scatter, grid, dim3(256), 0, stream, (const int32_t*)w->budgets,
+                                    (const uint8_t*)w->exact, n, H, w->d_in, tokens, w->cursor, w->samp_list,
+                                    w->exact_list));
             MCA_LAUNCH_CHECK("k2_scatter");
         }
     }
@@ -747,8 +772,9 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
             }
             const long tiles = (long)B * H * ((n + k4tc::kBM - 1) / k4tc::kBM);
             const int grid = (int)std::min<long>(tiles, 2L * sm_count());   // persistent: two CTAs per SM
-            k4_apply_tc<<<grid, k4tc::kThreads, k4tc::kSmemBytes, stream>>>(
-                (const __nv_bfloat16*)q, tk, th, w->lse, n, H, B, (float)scale, (__nv_bfloat16*)y);
+            MCA_CUDA_TRY(launch_pdl(k4_apply_tc, dim3(grid), dim3(k4tc::kThreads), k4tc::kSmemBytes, stream,
+                                    (const __nv_bfloat16*)q, tk, th, (const float*)w->lse, n, H, B, (float)scale,
+                                    (__nv_bfloat16*)y));
             if (MCA_K4_PROF) {   // diagnostics build: the first CTA's softmax timeline
                 long long t[64];
                 MCA_CUDA_TRY(cudaStreamSynchronize(stream));

@@ -16,6 +16,16 @@ constexpr int kDh = 64;            // head dimension the kernels implement (BERT
 constexpr int kGuideBits = 12;     // guide table: 4096 buckets over the 53-bit uniform (~5 per row at d = 768)
 constexpr int kGuide = 1 << kGuideBits;
 
+// ----------------------------------------------- programmatic dependent launch
+// Kernels of the forward are launched with programmatic stream serialization
+// (mca_capi.cu launch_pdl): a kernel may start while its predecessor drains.
+// griddep_trigger() lets the next kernel launch; griddep_wait() blocks the
+// calling thread until the predecessor grid has completed and its writes are
+// visible, so it goes before the first read of a predecessor's output. Both
+// are no-ops for a kernel launched without the attribute.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // ----------------------------------------------------------------- Philox
 __device__ __forceinline__ void philox4x32_10(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0,
                                               uint32_t k1, uint32_t out[4]) {

@@ -192,6 +192,24 @@ __device__ __forceinline__ uint32_t ex2_f16x2(uint32_t x2) {
     asm("ex2.approx.f16x2 %0, %1;" : "=r"(r) : "r"(x2));
     return r;
 }
+// 2^x for two fp32 values on the FMA pipe (no MUFU): x is clamped to >= -30,
+// split as j + f with j = rint(x) (1.5 * 2^23 rounding trick) and |f| <= 0.5,
+// 2^f from a degree-3 near-minimax polynomial (max relative error 1.1e-4,
+// below fp16's half ulp), and j added to the exponent bits. For outputs
+// stored in fp16 (K4's P).
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+    x.x = fmaxf(x.x, -30.f);
+    x.y = fmaxf(x.y, -30.f);
+    const float2 magic = make_float2(12582912.f, 12582912.f);
+    const float2 t = __fadd2_rn(x, magic);
+    const float2 j = __fadd2_rn(t, make_float2(-12582912.f, -12582912.f));
+    const float2 f = __ffma2_rn(j, make_float2(-1.f, -1.f), x);
+    float2 p = __ffma2_rn(f, make_float2(0.054615006f, 0.054615006f), make_float2(0.24221799f, 0.24221799f));
+    p = __ffma2_rn(f, p, make_float2(0.69336408f, 0.69336408f));
+    p = __ffma2_rn(f, p, make_float2(1.f, 1.f));
+    return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+                       __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
+}
 __device__ __forceinline__ float ex2_approx(float x) {
     float r;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
