@@ -165,6 +165,7 @@ __global__ void __maxnreg__(96)
         if (lane == 0) {  // ---------------- TMA (every Q and K tile once), then the phase-2 MMA stream
             tma_prefetch(&tm_q);
             tma_prefetch(&tm_k);
+            griddep_wait();   // q, k may be the projection GEMM's output
             for (int t = 0; t < nt; ++t)
                 for (int op = 0; op < 2; ++op) {   // 0: Q tile t, 1: K tile t
                     mbar_expect_tx(tile_full + op * nt + t, kTileBytes);

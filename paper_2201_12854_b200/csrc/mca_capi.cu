@@ -645,7 +645,7 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
         a.exact = w->exact;
         a.counters = w->counters;
         a.hist = tile_k3 ? nullptr : w->hist;
-        k12_fused_tc<<<(unsigned)(B * H), k12::kThreads, smem, stream>>>(tq, tk, a);
+        MCA_CUDA_TRY(launch_pdl(k12_fused_tc, dim3((unsigned)(B * H)), dim3(k12::kThreads), smem, stream, tq, tk, a));
         MCA_LAUNCH_CHECK("k12_fused_tc");
         if (MCA_K12_PROF) {   // diagnostics build: CTA 0's timeline
             long long t[96];
