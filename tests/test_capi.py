@@ -101,3 +101,17 @@ def test_oracle_satisfies_reference_header(tmp_path):
                     f"-Wl,-rpath,{os.path.join(ROOT, 'oracle', '_ref')}"], check=True)
     out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()
     assert out[0] == "1" and abs(float(out[1]) - 29.454371) < 1e-5
+
+
+def test_torch_custom_op_registered_with_fake_kernel():
+    """The PyTorch binding registers torch.ops.mca_b200.attention with a fake
+    (meta) kernel: shape propagation works without a GPU (no library call)."""
+    torch = pytest.importorskip("torch")
+    from torch._subclasses.fake_tensor import FakeTensorMode
+    import paper_2201_12854_b200.torch_op  # noqa: F401
+    with FakeTensorMode():
+        q = torch.empty(2, 16, 768)
+        x = torch.empty(2, 16, 768)
+        w = torch.empty(768, 768)
+        y = torch.ops.mca_b200.attention(q, q, x, w, 12, 0.4, 0, "approximation", 0)
+    assert tuple(y.shape) == (2, 16, 768)

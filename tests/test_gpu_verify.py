@@ -1,0 +1,58 @@
+"""GPU verify suites (acceptance criteria 3-6 and 10) and the
+PyTorch binding."""
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def verify():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2201_12854_b200 import verify
+    return verify
+
+
+@pytest.mark.parametrize("suite,trials", [("lemma1", 2000), ("scaling", 1000), ("unbiased", 20000),
+                                          ("theorem1", 4000), ("monotone", 1000)])
+def test_verify_suite(verify, suite, trials):
+    rep = verify.SUITES[suite](trials=trials)
+    assert rep.passed, rep.csv()
+
+
+def test_verify_cli_deterministic(verify, capsys):
+    assert verify.main(["--suite", "lemma1", "--trials", "500", "--seed", "9"]) == 0
+    a = capsys.readouterr().out
+    assert verify.main(["--suite", "lemma1", "--trials", "500", "--seed", "9"]) == 0
+    assert capsys.readouterr().out == a                      # identical CSV for the same seed
+
+
+def test_torch_module_regular_matches_dense():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2201_12854_b200.torch_op import McaSelfAttention
+    torch.manual_seed(0)
+    m = McaSelfAttention(768, 12, mode="regular").cuda()
+    hs = torch.randn(2, 64, 768, device="cuda")
+    with torch.no_grad():
+        y = m(hs)
+        q, k, v = m.query(hs), m.key(hs), m.value(hs)
+        sh = lambda t: t.view(2, 64, 12, 64).transpose(1, 2)   # noqa: E731
+        att = torch.softmax(sh(q) @ sh(k).transpose(-1, -2) / 8.0, dim=-1)
+        ref = (att @ sh(v)).transpose(1, 2).reshape(2, 64, 768)
+    assert float((y - ref).norm() / ref.norm()) < 1e-5
+    m.mode = "approximation"
+    m.alpha = 1e-7                                            # every budget clamps to exact: the regular layer
+    with torch.no_grad():
+        ye = m(hs)
+    assert float((ye - ref).norm() / ref.norm()) < 1e-5
+    m.alpha = 0.4                                             # Monte-Carlo layer: Theorem 1's per-row bound
+    with torch.no_grad():
+        ya = m(hs)
+        err = (ya - ref).view(2, 64, 12, 64).norm(dim=3)      # [b, j, h]
+        beta = hs.double().norm(dim=2).mean(dim=1)            # per sequence
+        wn = m.value.weight.t().double().reshape(768, 12, 64).norm(dim=(0, 2))
+        bound = 0.4 * beta[:, None, None] * wn[None, None, :]
+    assert bool(torch.isfinite(ya).all()) and bool((err.mean(dim=1) <= bound[:, 0, :]).all())
