@@ -47,9 +47,11 @@ __device__ long long g_k12_prof[96];
 namespace k12 {
 constexpr int kT = 128;                           // tile rows (= block columns)
 constexpr int kMaxTiles = 6;                      // n <= 768
-constexpr int kGroupWarps = 8;                    // per consumer group: 2 per TMEM lane quadrant
-constexpr int kGThreads = kGroupWarps * 32;
-constexpr int kThreads = 64 + 2 * kGThreads;      // 576
+constexpr int kAWarps = 16;                       // group A: 4 per TMEM lane quadrant, 32 columns each
+constexpr int kBWarps = 8;                        // group B: 2 per TMEM lane quadrant, 64 columns each
+constexpr int kAThreads = kAWarps * 32, kBThreads = kBWarps * 32;
+constexpr int kCThreads = kAThreads + kBThreads;
+constexpr int kThreads = 64 + kCThreads;          // 832
 constexpr uint32_t kTileBytes = kT * kDh * 2;     // 16 KB: 128 rows x 64 bf16, 128B-swizzled
 constexpr uint32_t kIdesc = mca_tc::idesc_f16(1, 0, kT, kT);
 
@@ -63,8 +65,8 @@ __host__ __device__ inline Layout layout(int nt, int d) {
     L.lse2 = 2 * nt * kTileBytes;                              // [nt*128] f32, log2 domain
     L.m = L.lse2 + nt * kT * 4;                                // [nt*128] f64 row max (natural log domain)
     L.l = L.m + nt * kT * 8;                                   // [nt*128] f64 row sum
-    L.comb = L.l + nt * kT * 8;                                // A: [2][128] x 8 B; B: [kMaxTiles][2][128] x 8 B
-    L.hist = L.comb + (2 + 2 * kMaxTiles) * kT * 8;            // [d + 1] u32 budget histogram
+    L.comb = L.l + nt * kT * 8;                                // A: [2][4][128] x 8 B; B: [kMaxTiles][2][128] x 8 B
+    L.hist = L.comb + (2 * 4 + 2 * kMaxTiles) * kT * 8;        // [d + 1] u32 budget histogram
     L.bars = (L.hist + (uint32_t)(d + 1) * 4 + 15) & ~15u;
     L.bytes = L.bars + 256 + 1024;                             // + alignment slack
     return L;
@@ -88,7 +90,7 @@ struct K12Args {
     unsigned int* hist;                // [H, d + 1] (nullable)
 };
 
-__global__ void __maxnreg__(96)
+__global__ void __maxnreg__(72)
     k12_fused_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k, K12Args a) {
     using namespace k12;
     using namespace mca_tc;
@@ -100,8 +102,8 @@ __global__ void __maxnreg__(96)
     float* s_lse2 = reinterpret_cast<float*>(smem + L.lse2);
     double* s_m = reinterpret_cast<double*>(smem + L.m);
     double* s_l = reinterpret_cast<double*>(smem + L.l);
-    float2* combA = reinterpret_cast<float2*>(smem + L.comb);        // [2][128]  (qt parity)
-    float2* combB = combA + 2 * kT;                                   // [kMaxTiles][2][128] running maxima
+    float2* combA = reinterpret_cast<float2*>(smem + L.comb);        // [2][4][128]  (qt parity, column part)
+    float2* combB = combA + 2 * 4 * kT;                               // [kMaxTiles][2][128] running maxima
     unsigned int* s_hist = reinterpret_cast<unsigned int*>(smem + L.hist);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);
     uint64_t* tile_full = bars;                  // [2 * kMaxTiles]: Q tiles, then K tiles
@@ -124,11 +126,11 @@ __global__ void __maxnreg__(96)
         for (int t = 0; t < 2 * nt; ++t) mbar_init(tile_full + t, 1);
         for (int i = 0; i < 2; ++i) {
             mbar_init(a_full + i, 1);
-            mbar_init(a_empty + i, kGThreads);
+            mbar_init(a_empty + i, kAThreads);
             mbar_init(b_full + i, 1);
-            mbar_init(b_empty + i, kGThreads);
+            mbar_init(b_empty + i, kBThreads);
         }
-        for (int t = 0; t < kMaxTiles; ++t) mbar_init(lse_ready + t, kGThreads / 2);
+        for (int t = 0; t < kMaxTiles; ++t) mbar_init(lse_ready + t, kAThreads / 4);
         fence_barrier_init();
     }
     if (use_hist)
@@ -178,12 +180,13 @@ __global__ void __maxnreg__(96)
         if (lane == 0)   // ---------------- the phase-1 MMA stream
             for (int u = 0; u < nblk; ++u) issue(0, u);
     } else {  // ------------------------------- consumer groups A (warps 2..9) and B (warps 10..17)
-        const int grp = warp >= 2 + kGroupWarps;   // 0: A (row statistics), 1: B (column maxima)
-        const int gt = threadIdx.x - 64 - grp * kGThreads;
+        const int grp = warp >= 2 + kAWarps;       // 0: A (row statistics), 1: B (column maxima)
+        const int gt = threadIdx.x - 64 - grp * kAThreads;
         const int quad = warp & 3;                 // TMEM lane quadrant this warp may access
-        const int half = (gt >> 5) >> 2;           // columns [64 half, 64 half + 64) of each block
+        const int half = (gt >> 5) >> 2;           // A: columns [32 half, +32) (4 parts); B: [64 half, +64)
         const int row = quad * 32 + lane;          // TMEM lane = resident row (query in A, key in B)
-        const uint32_t lane_base = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(grp * 2) * kT + half * 64;
+        const uint32_t lane_base =
+            tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(grp * 2) * kT + (uint32_t)half * (grp ? 64u : 32u);
         const float c2 = a.scale * 1.4426950408889634f;
         const size_t rbase = (size_t)bh * n;
         uint64_t* full = grp ? b_full : a_full;
@@ -208,11 +211,16 @@ __global__ void __maxnreg__(96)
             for (int qt = 0; qt < nt; ++qt) {
                 float m2 = -INFINITY, l = 0.0f;
                 for (int kt = 0; kt < nt; ++kt) {
-#pragma unroll
-                    for (int pc = 0; pc < 2; ++pc) {
+                    {
                         uint32_t sv[32];
-                        load_piece(qt * nt + kt, pc, sv);
-                        const int valid = n - (kt * kT + half * 64 + pc * 32);   // <= 0: this piece is past n
+                        const int u = qt * nt + kt, sb = u & 1;
+                        mbar_wait(full + sb, (u >> 1) & 1);
+                        tc_fence_after();
+                        tmem_ld32(lane_base + sb * kT, sv);
+                        tmem_ld_wait();
+                        tc_fence_before();
+                        mbar_arrive(empty + sb);
+                        const int valid = n - (kt * kT + half * 32);   // <= 0: this part is past n
                         float bmax = -INFINITY;
                         if (valid >= 32) {   // pairwise tree: 5 dependent levels instead of 32
                             float t16[16];
@@ -252,15 +260,20 @@ __global__ void __maxnreg__(96)
                     }
                     if (prof0 && gt == 0 && qt * nt + kt < 39) g_k12_prof[1 + qt * nt + kt] = clock64();
                 }
-                // combine the two column halves of each row (as k1_scores_tc does)
-                float2* cb = combA + (qt & 1) * kT;
-                if (half == 1) cb[row] = make_float2(m2, l);
-                named_bar_sync(1, kGThreads);
+                // combine the four column parts of each row
+                float2* cb = combA + (qt & 1) * 4 * kT;
+                if (half != 0) cb[half * kT + row] = make_float2(m2, l);
+                named_bar_sync(1, kAThreads);
                 if (half == 0) {
-                    const float2 o = cb[row];
-                    const float mn = fmaxf(m2, o.x);
-                    const float lt = (m2 == -INFINITY ? 0.f : l * ex2_approx(m2 - mn)) +
-                                     (o.x == -INFINITY ? 0.f : o.y * ex2_approx(o.x - mn));
+                    float mn = m2;
+#pragma unroll
+                    for (int p = 1; p < 4; ++p) mn = fmaxf(mn, cb[p * kT + row].x);
+                    float lt = m2 == -INFINITY ? 0.f : l * ex2_approx(m2 - mn);
+#pragma unroll
+                    for (int p = 1; p < 4; ++p) {
+                        const float2 o = cb[p * kT + row];
+                        lt += o.x == -INFINITY ? 0.f : o.y * ex2_approx(o.x - mn);
+                    }
                     const int q = qt * kT + row;
                     if (q < n) {
                         const float lse_nat = (mn + __log2f(lt)) * 0.6931471805599453f;
@@ -316,9 +329,9 @@ __global__ void __maxnreg__(96)
             }
         }
         // ---------------- Eq. 9 for every key, one key per consumer thread (both groups)
-        named_bar_sync(3, 2 * kGThreads);          // group B's running maxima are final
+        named_bar_sync(3, kCThreads);              // group B's running maxima are final
         unsigned long long cost = 0, samples = 0, nexact = 0;
-        for (int j = threadIdx.x - 64; j < n; j += 2 * kGThreads) {
+        for (int j = threadIdx.x - 64; j < n; j += kCThreads) {
             const int kt = j / kT, r0 = j - kt * kT;
             // the two query halves of the key: larger value, ties to the smaller query index
             const float2 m0 = combB[(kt * 2) * kT + r0], m1 = combB[(kt * 2 + 1) * kT + r0];
@@ -368,7 +381,7 @@ __global__ void __maxnreg__(96)
             }
         }
     }
-    if (prof0 && threadIdx.x == 64 + kGThreads) g_k12_prof[79] = clock64();   // group B done (incl. Eq. 9)
+    if (prof0 && threadIdx.x == 64 + kAThreads) g_k12_prof[79] = clock64();   // group B done (incl. Eq. 9)
     tc_fence_before();
     __syncthreads();
     if (prof0 && threadIdx.x == 0) g_k12_prof[80] = clock64();
