@@ -76,7 +76,8 @@ struct alignas(16) SamplePair {  // fp32 parity path: one draw, broadcast to its
     uint32_t row;   // sampled W_h row
     Acc coef;       // x[j, row] / (r p(row)), fp64
 };
-// bf16 path: row (low 16 bits) | bf16 coefficient (high 16 bits), 4 bytes per draw
+// bf16 path: row * 8 (the row's offset in 16-byte units, low 16 bits) | bf16
+// coefficient (high 16 bits), 4 bytes per draw
 using PackedPair = uint32_t;
 
 // 4 consecutive W_h elements starting at column `col` of row `row`, as floats
@@ -350,16 +351,18 @@ __global__ void __launch_bounds__(kK3BlockThreads, 1) k3_encode_sampled_bf16(K3A
         auto pack = [&](int i, unsigned short xb) -> PackedPair {
             const float c = __uint_as_float((uint32_t)xb << 16) * s_invp[i] * inv_r;
             const __nv_bfloat16 cb = __float2bfloat16_rn(c);
-            return (uint32_t)i | ((uint32_t)(*reinterpret_cast<const unsigned short*>(&cb)) << 16);
+            return ((uint32_t)i << 3) | ((uint32_t)(*reinterpret_cast<const unsigned short*>(&cb)) << 16);
         };
         float acc[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) acc[u] = 0.f;
         auto accumulate = [&](PackedPair p) {
             uint4 w;
+            uint32_t addr;
+            asm("mad.lo.u32 %0, %1, 16, %2;" : "=r"(addr) : "r"(p & 0xFFFFu), "r"(wbase));   // LOP3 + one IMAD/LEA
             asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
                          : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w)
-                         : "r"(wbase + (p & 0xFFFFu) * (kDh * 2)));
+                         : "r"(addr));
             const unsigned short c = (unsigned short)(p >> 16);
             fma2_bf16_f32(acc[0], acc[1], w.x, c);
             fma2_bf16_f32(acc[2], acc[3], w.y, c);
