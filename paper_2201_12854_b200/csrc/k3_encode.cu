@@ -301,7 +301,6 @@ __global__ void __launch_bounds__(kK3BlockThreads, 1) k3_encode_sampled_bf16(K3A
     const int h = blockIdx.y;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int oct = lane >> 3, l8 = lane & 7;
-    const unsigned omask = 0xFFu << (oct * 8);
     const int d_in = a.d_in, n = a.n, heads = a.heads;
 
     uint64_t* s_thr = reinterpret_cast<uint64_t*>(smem);
@@ -334,13 +333,20 @@ __global__ void __launch_bounds__(kK3BlockThreads, 1) k3_encode_sampled_bf16(K3A
     const uint32_t wbase = static_cast<uint32_t>(__cvta_generic_to_shared(s_w)) + col0 * 2;
     unsigned long long my_samples = 0;
 
+    // Every lane of the warp calls process_token (r = 0: no token for this octet) and
+    // the warp runs the warp-wide maximum number of rounds, octets past their own
+    // budget idle: the four octets stay in lockstep, so the pair buffer needs only
+    // full-warp __syncwarp()s (the budget-sorted list keeps a task's budgets near-equal).
     auto process_token = [&](int bj, int r) {
+        const int rw = __reduce_max_sync(0xffffffffu, r);
+        const bool has = r > 0;
+        if (!has) bj = 0;
         const int b = bj >> 16, j = bj & 0xFFFF;
         const size_t tok = (size_t)b * n + j;
         const size_t tokh = ((size_t)b * heads + h) * n + j;
         const __nv_bfloat16* xrow = x + tok * d_in;
         const uint64_t stream = ((uint64_t)(a.b_offset + b) * heads + h) * (uint64_t)n + (uint64_t)j;
-        const float inv_r = 1.0f / (float)r;
+        const float inv_r = has ? 1.0f / (float)r : 0.0f;
         auto gen = [&](int base, int& i0, int& i1, unsigned short& x0, unsigned short& x1) {
             uint64_t m0, m1;
             philox_pair53(a.seed, stream, a.layer, (uint32_t)(base / 2 + l8), &m0, &m1);
@@ -369,23 +375,28 @@ __global__ void __launch_bounds__(kK3BlockThreads, 1) k3_encode_sampled_bf16(K3A
             fma2_bf16_f32(acc[4], acc[5], w.z, c);
             fma2_bf16_f32(acc[6], acc[7], w.w, c);
         };
-        int ni0, ni1;
-        unsigned short nx0, nx1;
-        gen(0, ni0, ni1, nx0, nx1);
-        for (int base = 0; base < r; base += 16) {
+        int ni0 = 0, ni1 = 0;
+        unsigned short nx0 = 0, nx1 = 0;
+        if (has) gen(0, ni0, ni1, nx0, nx1);
+        for (int base = 0; base < rw; base += 16) {
+            const bool act = base < r;
             const int i0 = ni0, i1 = ni1;
             const unsigned short x0 = nx0, x1 = nx1;
             if (base + 16 < r) gen(base + 16, ni0, ni1, nx0, nx1);   // next round's loads in flight
-            const PackedPair p0 = pack(i0, x0), p1 = pack(i1, x1);
-            if (a.draws_out) {
-                const int k0 = base + 2 * l8;
-                if (k0 < r && k0 < a.draws_stride) a.draws_out[tokh * a.draws_stride + k0] = i0;
-                if (k0 + 1 < r && k0 + 1 < a.draws_stride) a.draws_out[tokh * a.draws_stride + k0 + 1] = i1;
+            PackedPair p0 = 0, p1 = 0;
+            if (act) {
+                p0 = pack(i0, x0);
+                p1 = pack(i1, x1);
+                if (a.draws_out) {
+                    const int k0 = base + 2 * l8;
+                    if (k0 < r && k0 < a.draws_stride) a.draws_out[tokh * a.draws_stride + k0] = i0;
+                    if (k0 + 1 < r && k0 + 1 < a.draws_stride) a.draws_out[tokh * a.draws_stride + k0 + 1] = i1;
+                }
             }
-            __syncwarp(omask);                     // previous round's pairs fully consumed
-            reinterpret_cast<uint2*>(my_pairs)[l8] = make_uint2(p0, p1);
-            __syncwarp(omask);
-            const int cnt = min(16, r - base);
+            __syncwarp();                          // previous round's pairs fully consumed
+            if (act) reinterpret_cast<uint2*>(my_pairs)[l8] = make_uint2(p0, p1);
+            __syncwarp();
+            const int cnt = act ? min(16, r - base) : 0;
             if (cnt == 16) {
 #pragma unroll
                 for (int q4 = 0; q4 < 4; ++q4) {
@@ -400,7 +411,8 @@ __global__ void __launch_bounds__(kK3BlockThreads, 1) k3_encode_sampled_bf16(K3A
             }
             if (l8 == 0) my_samples += (unsigned long long)cnt;
         }
-        __syncwarp(omask);
+        __syncwarp();
+        if (!has) return;
         if (a.draws_out && l8 == 0)
             for (int k = r; k < a.draws_stride; ++k) a.draws_out[tokh * a.draws_stride + k] = -1;
         store8(hout + tok * HD + (size_t)h * kDh + col0, acc);
@@ -423,8 +435,8 @@ __global__ void __launch_bounds__(kK3BlockThreads, 1) k3_encode_sampled_bf16(K3A
         const int rb = bjb >= 0 ? a.budgets[((size_t)(bjb >> 16) * heads + h) * n + (bjb & 0xFFFF)] : 0;
         if (bja >= 0) prefetch_row(bja);
         if (bjb >= 0) prefetch_row(bjb);
-        if (bja >= 0) process_token(bja, ra);
-        if (bjb >= 0) process_token(bjb, rb);
+        process_token(bja, ra);                    // all lanes: lockstep rounds (r = 0: idle octet)
+        process_token(bjb, rb);
     }
     if (a.sample_counter) {
         for (int off = 16; off; off >>= 1) my_samples += __shfl_xor_sync(0xffffffffu, my_samples, off);
