@@ -446,3 +446,22 @@ def test_projection_path(mca, syn, dtype):
         pipe.forward(None, None, hx, hy, cfg, seed=3)
         torch.cuda.synchronize()
         assert torch.equal(hy, y.cpu())
+
+
+@pytest.mark.parametrize("n", [1, 2, 127, 128, 129, 255, 256, 383, 511, 767, 768])
+def test_fused_score_budget_kernel_lengths(mca, syn, orc, n):
+    """The fused score + budget kernel (k12, bf16, n <= 768) across tile
+    boundaries: Eq. 9 bitwise on the device's cmax, the plan's y within the
+    bf16 tolerance of the oracle, lse close to the oracle's."""
+    H, d_in, B = 4, 256, 1
+    weights, w, q, k, x = _setup(mca, syn, B, n, d_in, H, torch.bfloat16, seed=n)
+    dbg = dict(cmax_out=torch.zeros((B, H, n), dtype=torch.float64, device="cuda"),
+               lse_out=torch.zeros((B, H, n), device="cuda"))
+    out = mca.mca_forward(weights, q, k, x, mca.McaConfig(alpha=0.4), seed=7, return_plan=True, debug=dbg)
+    b = out.budgets.cpu().numpy()
+    e = out.exact_mask.cpu().numpy().astype(bool)
+    rb, re = orc.sample_budgets_from_cmax(dbg["cmax_out"].cpu().numpy(), n, 0.4, 1, d_in)
+    assert np.array_equal(b, rb) and np.array_equal(e, re)
+    ref = _oracle(orc, w, q, k, x, H, alpha=0.4, seed=7, budgets_override=b, exact_override=e)
+    assert _row_rel(_np(out.y), ref.y) <= TOL_Y[torch.bfloat16]
+    np.testing.assert_allclose(dbg["lse_out"].cpu().numpy(), ref.lse, rtol=2e-3, atol=2e-3)
