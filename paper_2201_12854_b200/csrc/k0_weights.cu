@@ -11,7 +11,8 @@
 // p and cdf are bitwise equal to the oracle's. Then, for the sampler:
 //   thr[i]   = ceil(cdf[i] * 2^53)   (u64; exact: power-of-two scaling)
 //   invp[i]  = (float)(1 / p[i])     (0 where p = 0; never drawn)
-//   guide[g] = first i with thr[i] > g * 2^43
+//   guide[g] = first i with thr[i] > g * 2^39, | 0x8000 when thr[i] >= (g + 1) * 2^39
+//              (the whole bucket draws row i: no compare needed)
 // One-time cost; it runs once per weight matrix ("embedded in the model or
 // cached").
 #include "mca_common.cuh"
@@ -87,7 +88,8 @@ __global__ void k0_dist(const double* __restrict__ sq, int d_in, double* __restr
             const int mid = (lo + hi) >> 1;
             if (t[mid] > key) hi = mid; else lo = mid + 1;
         }
-        guide[(size_t)h * kGuide + g] = (uint16_t)lo;
+        const uint64_t upper = (uint64_t)(g + 1) << (53 - kGuideBits);   // bucket = [key, upper)
+        guide[(size_t)h * kGuide + g] = (uint16_t)(lo | (t[lo] >= upper ? kGuideClean : 0u));
     }
 }
 

@@ -43,6 +43,8 @@ constexpr uint32_t kChunkBytes = kBM * 128;      // one 64-column chunk of the t
 constexpr uint32_t kIdesc = mca_tc::idesc_f16(1, 1, kBM, kDh);   // bf16 x bf16, B (W') MN-major
 constexpr int kPre = kBM + 33;                   // pair prefix + padding read by the lane search
 constexpr int kMaxAtoms = 12;                    // d_in <= 768: X row chunks a convert thread holds
+constexpr int kGuideBitsT = 12;                  // coarser guide table in smem: every 4th entry of K0's
+constexpr int kGuideT = 1 << kGuideBitsT;
 
 struct Plan {                     // one tile's draw plan (double-buffered)
     int rb[kBM];                  // budgets of sampled rows (0 otherwise)
@@ -70,7 +72,7 @@ __host__ __device__ inline Layout layout(int d_in) {
     L.tile = L.natoms * 8192u;                             // counts, then A in place: natoms x [64 x 64] (K-major A)
     L.thr = L.tile + L.natoms * kChunkBytes;
     L.guide = L.thr + (((uint32_t)d_in * 8u + 15u) & ~15u);
-    L.pbf = L.guide + kGuide * 2u;
+    L.pbf = L.guide + kGuideT * 2u;
     L.meta = L.pbf + L.dpad * 2u;
     L.bytes = L.meta + (uint32_t)((sizeof(Meta) + 15) & ~(size_t)15) + 1024u;   // + alignment slack
     if (L.natoms > (uint32_t)kMaxAtoms) L.bytes = 0xFFFFFFFFu;                   // not supported: gather path
@@ -232,7 +234,8 @@ __global__ void __launch_bounds__(k3t::kThreads, 1)
         tmem_alloc<128>(&M.tmem_slot);
     } else {
         for (int i = tid; i < d_in; i += kWorkerThreads) s_thr[i] = a.thr[(size_t)h * d_in + i];
-        for (int g = tid; g < kGuide; g += kWorkerThreads) s_guide[g] = a.guide[(size_t)h * kGuide + g];
+        for (int g = tid; g < kGuideT; g += kWorkerThreads)   // coarse entries, clean bits masked off
+            s_guide[g] = a.guide[(size_t)h * kGuide + ((size_t)g << (kGuideBits - kGuideBitsT))] & 0x7FFFu;
         for (int i = tid; i < (int)L.dpad; i += kWorkerThreads)
             s_pbf[i] = i < d_in ? pbf_g[(size_t)h * d_in + i] : __float2bfloat16(0.f);
         if (warp == 0 && my_tiles > 0) {
@@ -319,7 +322,7 @@ __global__ void __launch_bounds__(k3t::kThreads, 1)
             uint64_t m0, m1;
             philox_pair53(a.seed, stream, a.layer, (uint32_t)p, &m0, &m1);
             int i0, i1;
-            sample_index2(s_thr, s_guide, m0, m1, i0, i1);
+            sample_index2<kGuideBitsT>(s_thr, s_guide, m0, m1, i0, i1);
             const bool second = 2 * p + 1 < r;
             if (a.draws_out) {
                 int32_t* dr = a.draws_out + (((size_t)b * heads + h) * n + j0 + m) * a.draws_stride;

@@ -13,8 +13,12 @@
 namespace mca_dev {
 
 constexpr int kDh = 64;            // head dimension the kernels implement (BERT base/large)
-constexpr int kGuideBits = 12;     // guide table: 4096 buckets over the 53-bit uniform (~5 per row at d = 768)
+constexpr int kGuideBits = 14;     // guide table: 16384 buckets over the 53-bit uniform (~21 per row at d = 768)
 constexpr int kGuide = 1 << kGuideBits;
+// Guide entry: bits 0-14 the first row whose threshold exceeds the bucket's
+// lower end; bit 15 set when the whole bucket maps to that row ("clean":
+// thr[row] >= the bucket's upper end), so the draw needs no threshold compare.
+constexpr uint16_t kGuideClean = 0x8000u;
 
 // ----------------------------------------------- programmatic dependent launch
 // Kernels of the forward are launched with programmatic stream serialization
@@ -63,18 +67,27 @@ __device__ __forceinline__ void philox_pair53(uint64_t seed, uint64_t stream_id,
 // Inverse CDF: first i with thr[i] > m, thr[i] = ceil(cdf[i] * 2^53). The guide
 // entry for m's top kGuideBits bits is a lower bound on the answer, so the
 // forward scan returns exactly std::upper_bound(cdf, m * 2^-53).
+// kBits < kGuideBits: a coarser table (entry g = entry g << (kGuideBits - kBits)
+// of the full one, with the clean bits masked off: a fine bucket's flag says
+// nothing about the coarse bucket containing it).
+template <int kBits = kGuideBits>
 __device__ __forceinline__ int sample_index(const uint64_t* __restrict__ thr, const uint16_t* __restrict__ guide,
                                             uint64_t m) {
-    int i = guide[(uint32_t)(m >> (53 - kGuideBits))];
+    const uint32_t e = guide[(uint32_t)(m >> (53 - kBits))];
+    int i = (int)(e & 0x7FFFu);
+    if (e & kGuideClean) return i;
     while (thr[i] <= m) ++i;
     return i;
 }
 // Two draws resolved by one scan loop (one divergent loop instead of two).
+template <int kBits = kGuideBits>
 __device__ __forceinline__ void sample_index2(const uint64_t* __restrict__ thr, const uint16_t* __restrict__ guide,
                                               uint64_t m0, uint64_t m1, int& i0, int& i1) {
-    i0 = guide[(uint32_t)(m0 >> (53 - kGuideBits))];
-    i1 = guide[(uint32_t)(m1 >> (53 - kGuideBits))];
-    bool a0 = thr[i0] <= m0, a1 = thr[i1] <= m1;
+    const uint32_t e0 = guide[(uint32_t)(m0 >> (53 - kBits))], e1 = guide[(uint32_t)(m1 >> (53 - kBits))];
+    i0 = (int)(e0 & 0x7FFFu);
+    i1 = (int)(e1 & 0x7FFFu);
+    if (e0 & e1 & kGuideClean) return;   // both buckets clean: no threshold compare
+    bool a0 = !(e0 & kGuideClean) && thr[i0] <= m0, a1 = !(e1 & kGuideClean) && thr[i1] <= m1;
     while (a0 || a1) {
         if (a0) a0 = thr[++i0] <= m0;
         if (a1) a1 = thr[++i1] <= m1;
