@@ -27,11 +27,11 @@
 // the MUFU (one exponential per score), phase 2 by FMA/ALU issue, so group A
 // exponentiating query tile qt + 1 overlaps group B's maxima over tile qt.
 //
-// Warp roles (576 threads, one CTA per SM): warp 0 TMA (all Q and K tiles of
-// the (b, h), one barrier per tile) and then the phase-2 MMA issuer, warp 1
-// TMEM allocator + phase-1 MMA issuer, warps 2-9 group A, warps 10-17 group
-// B: two warps per TMEM lane quadrant in each group, each owning 64 of a
-// block's 128 columns. TMEM: A buffers [0,256), B buffers [256,512).
+// Warp roles (864 threads, one persistent CTA per SM): warp 0 the phase-2 MMA
+// issuer, warp 1 TMEM allocator + phase-1 MMA issuer, warps 2-17 group A (four
+// warps per TMEM lane quadrant, 32 columns of a block each), warps 18-25 group
+// B (two per quadrant, 64 columns each), warp 26 the TMA producer.
+// TMEM: A buffers [0,256), B buffers [256,512).
 #include "mca_common.cuh"
 #include "tc_common.cuh"
 
@@ -43,6 +43,13 @@ namespace mca_dev {
 // Diagnostics (build with EXTRA=-DMCA_K12_PROF=1): clock64 stamps of CTA 0:
 // [0] start, [1 + u] group A block u done, [40 + u] group B block u done, [80] end
 __device__ long long g_k12_prof[96];
+// per CTA: smid, globaltimer at start and at exit (ns), clocks at exit - start
+__device__ unsigned long long g_k12_cta[4096][4];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 
 namespace k12 {
 constexpr int kT = 128;                           // tile rows (= block columns)
@@ -51,30 +58,31 @@ constexpr int kAWarps = 16;                       // group A: 4 per TMEM lane qu
 constexpr int kBWarps = 8;                        // group B: 2 per TMEM lane quadrant, 64 columns each
 constexpr int kAThreads = kAWarps * 32, kBThreads = kBWarps * 32;
 constexpr int kCThreads = kAThreads + kBThreads;
-constexpr int kThreads = 64 + kCThreads;          // 832
+constexpr int kThreads = 64 + kCThreads + 32;     // 864: + the TMA producer warp
 constexpr uint32_t kTileBytes = kT * kDh * 2;     // 16 KB: 128 rows x 64 bf16, 128B-swizzled
 constexpr uint32_t kIdesc = mca_tc::idesc_f16(1, 0, kT, kT);
 
 struct Layout {
-    uint32_t q, k, lse2, m, l, comb, hist, bars, bytes;
+    uint32_t q, k, lse2, ml, comb, hist, bars, bytes;
 };
+// Row statistics are double-buffered by item parity: group A writes item i + 1's
+// while group B's Eq. 9 still reads item i's.
 __host__ __device__ inline Layout layout(int nt, int d) {
     Layout L;
     L.q = 0;
     L.k = nt * kTileBytes;
-    L.lse2 = 2 * nt * kTileBytes;                              // [nt*128] f32, log2 domain
-    L.m = L.lse2 + nt * kT * 4;                                // [nt*128] f64 row max (natural log domain)
-    L.l = L.m + nt * kT * 8;                                   // [nt*128] f64 row sum
-    L.comb = L.l + nt * kT * 8;                                // A: [2][4][128] x 8 B; B: [kMaxTiles][2][128] x 8 B
+    L.lse2 = 2 * nt * kTileBytes;                              // [2][nt*128] f32, -lse in the log2 domain
+    L.ml = L.lse2 + 2 * nt * kT * 4;                           // [2][nt*128] float2 (row max log2, row sum)
+    L.comb = L.ml + 2 * nt * kT * 8;                           // A: [2][4][128] x 8 B; B: [kMaxTiles][2][128] x 8 B
     L.hist = L.comb + (2 * 4 + 2 * kMaxTiles) * kT * 8;        // [d + 1] u32 budget histogram
     L.bars = (L.hist + (uint32_t)(d + 1) * 4 + 15) & ~15u;
-    L.bytes = L.bars + 256 + 1024;                             // + alignment slack
+    L.bytes = L.bars + 512 + 1024;                             // barriers; + alignment slack
     return L;
 }
 }  // namespace k12
 
 struct K12Args {
-    int n, heads, d, dh, min_samples;
+    int n, heads, items, d, dh, min_samples;   // items = B * H (b, h) pairs
     float scale;
     double scale_d, alpha;
     bool force_exact;
@@ -90,6 +98,15 @@ struct K12Args {
     unsigned int* hist;                // [H, d + 1] (nullable)
 };
 
+// Persistent: one CTA per SM walks the items (b, h) = blockIdx.x, + gridDim.x, ...
+// Every stream (TMA, the two MMA issuers, both consumer groups) runs ahead into
+// the next item as far as its buffers allow, so the next item's tile loads and
+// group A's first query tile overlap group B's last query tile and Eq. 9 of the
+// current one (no per-item prologue, no tail where one group idles).
+//   Q tile t of item i is overwritten for item i + 1 once phase 2 has consumed it
+//   (q_empty[t], committed by the phase-2 issuer after block (t, nt - 1)) and
+//   phase 1 has (lse_ready[t] of item i); K tile t once phase 2's block
+//   (nt - 1, t) is done (k_empty[t]) and lse_ready[nt - 1].
 __global__ void __maxnreg__(72)
     k12_fused_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k, K12Args a) {
     using namespace k12;
@@ -99,15 +116,15 @@ __global__ void __maxnreg__(72)
     const int n = a.n, heads = a.heads;
     const int nt = (n + kT - 1) / kT;
     const Layout L = layout(nt, a.d);
-    float* s_lse2 = reinterpret_cast<float*>(smem + L.lse2);
-    double* s_m = reinterpret_cast<double*>(smem + L.m);
-    double* s_l = reinterpret_cast<double*>(smem + L.l);
+    float* s_lse2b = reinterpret_cast<float*>(smem + L.lse2);
+    float2* s_mlb = reinterpret_cast<float2*>(smem + L.ml);
     float2* combA = reinterpret_cast<float2*>(smem + L.comb);        // [2][4][128]  (qt parity, column part)
     float2* combB = combA + 2 * 4 * kT;                               // [kMaxTiles][2][128] running maxima
     unsigned int* s_hist = reinterpret_cast<unsigned int*>(smem + L.hist);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);
     uint64_t* tile_full = bars;                  // [2 * kMaxTiles]: Q tiles, then K tiles
-    uint64_t* a_full = bars + 2 * kMaxTiles;     // [2] phase-1 S buffers
+    uint64_t* tile_empty = bars + 2 * kMaxTiles; // [2 * kMaxTiles]: phase 2 is done with the tile
+    uint64_t* a_full = bars + 4 * kMaxTiles;     // [2] phase-1 S buffers
     uint64_t* a_empty = a_full + 2;              // [2]
     uint64_t* b_full = a_empty + 2;              // [2] phase-2 S^T buffers
     uint64_t* b_empty = b_full + 2;              // [2]
@@ -115,15 +132,25 @@ __global__ void __maxnreg__(72)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(lse_ready + kMaxTiles);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int bh = blockIdx.x, b = bh / heads, h = bh - b * heads;
     const int nblk = nt * nt;
     const bool prof0 = MCA_K12_PROF && blockIdx.x == 0;
     griddep_trigger();   // the work-list kernels may launch (they wait for this grid to complete)
     if (prof0 && threadIdx.x == 0) g_k12_prof[0] = clock64();
+    long long c_start = 0;
+    if (MCA_K12_PROF && threadIdx.x == 0 && blockIdx.x < 4096) {
+        unsigned int sm;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+        g_k12_cta[blockIdx.x][0] = sm;
+        g_k12_cta[blockIdx.x][1] = gtimer();
+        c_start = clock64();
+    }
     const bool use_hist = a.hist != nullptr && a.d <= 1024;
 
     if (threadIdx.x == 0) {
-        for (int t = 0; t < 2 * nt; ++t) mbar_init(tile_full + t, 1);
+        for (int t = 0; t < 2 * nt; ++t) {
+            mbar_init(tile_full + t, 1);
+            mbar_init(tile_empty + t, 1);
+        }
         for (int i = 0; i < 2; ++i) {
             mbar_init(a_full + i, 1);
             mbar_init(a_empty + i, kAThreads);
@@ -141,17 +168,19 @@ __global__ void __maxnreg__(72)
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
-    // block u of a phase = (qt, kt) = (u / nt, u % nt). Phase 1: S = Q_qt K_kt^T into
-    // the A buffers; phase 2: S^T = K_kt Q_qt^T into the B buffers. Each stream has
-    // its own issuing thread (tcgen05.commit tracks the issuing thread's MMAs), so
-    // neither stream waits on the other's buffer recycling.
-    auto issue = [&](int phase, int u) {
-        const int qt = u / nt, kt = u - qt * nt, sb = u & 1;
+    // block u of an item = (qt, kt) = (u / nt, u % nt); U = li * nblk + u counts the
+    // CTA's blocks across items (buffer index and barrier parity). Phase 1: S =
+    // Q_qt K_kt^T into the A buffers; phase 2: S^T = K_kt Q_qt^T into the B
+    // buffers. Each stream has its own issuing thread (tcgen05.commit tracks the
+    // issuing thread's MMAs), so neither waits on the other's buffer recycling.
+    auto issue = [&](int phase, int li, int u) {
+        const int U = li * nblk + u;
+        const int qt = u / nt, kt = u - qt * nt, sb = U & 1;
         uint64_t* full = phase ? b_full : a_full;
         uint64_t* empty = phase ? b_empty : a_empty;
-        mbar_wait(empty + sb, ((u >> 1) & 1) ^ 1);
-        mbar_wait(tile_full + qt, 0);
-        mbar_wait(tile_full + nt + kt, 0);
+        mbar_wait(empty + sb, ((U >> 1) & 1) ^ 1);
+        mbar_wait(tile_full + qt, li & 1);
+        mbar_wait(tile_full + nt + kt, li & 1);
         tc_fence_after();
         const uint32_t qa = smem_u32(smem + L.q + qt * kTileBytes);
         const uint32_t ka = smem_u32(smem + L.k + kt * kTileBytes);
@@ -162,24 +191,35 @@ __global__ void __maxnreg__(72)
             umma_f16(d, sw128_desc(a_addr + kk * 32, 16, 1024), sw128_desc(b_addr + kk * 32, 16, 1024), kIdesc,
                      kk > 0 ? 1u : 0u);
         umma_commit(full + sb);
+        if (phase) {   // phase 2 is the tiles' last reader
+            if (kt == nt - 1) umma_commit(tile_empty + qt);
+            if (qt == nt - 1) umma_commit(tile_empty + nt + kt);
+        }
     };
-    if (warp == 0) {
-        if (lane == 0) {  // ---------------- TMA (every Q and K tile once), then the phase-2 MMA stream
+    if (warp == k12::kThreads / 32 - 1) {
+        if (lane == 0) {  // ---------------- TMA: every Q and K tile of each item once
             tma_prefetch(&tm_q);
             tma_prefetch(&tm_k);
             griddep_wait();   // q, k may be the projection GEMM's output
-            for (int t = 0; t < nt; ++t)
-                for (int op = 0; op < 2; ++op) {   // 0: Q tile t, 1: K tile t
-                    mbar_expect_tx(tile_full + op * nt + t, kTileBytes);
-                    tma_load_3d(smem + (op ? L.k : L.q) + t * kTileBytes, op ? &tm_k : &tm_q, tile_full + op * nt + t,
-                                h * kDh, t * kT, b);
-                }
-            for (int u = 0; u < nblk; ++u) issue(1, u);
+            for (int it = blockIdx.x, li = 0; it < a.items; it += gridDim.x, ++li) {
+                const int b = it / heads, h = it - b * heads;
+                for (int t = 0; t < nt; ++t)
+                    for (int op = 0; op < 2; ++op) {   // 0: Q tile t, 1: K tile t
+                        if (li > 0) {   // phase 2, then phase 1 of the previous item are done with the slot
+                            mbar_wait(tile_empty + op * nt + t, (li - 1) & 1);
+                            mbar_wait(lse_ready + (op ? nt - 1 : t), (li - 1) & 1);
+                        }
+                        mbar_expect_tx(tile_full + op * nt + t, kTileBytes);
+                        tma_load_3d(smem + (op ? L.k : L.q) + t * kTileBytes, op ? &tm_k : &tm_q,
+                                    tile_full + op * nt + t, h * kDh, t * kT, b);
+                    }
+            }
         }
-    } else if (warp == 1) {
-        if (lane == 0)   // ---------------- the phase-1 MMA stream
-            for (int u = 0; u < nblk; ++u) issue(0, u);
-    } else {  // ------------------------------- consumer groups A (warps 2..9) and B (warps 10..17)
+    } else if (warp < 2) {
+        if (lane == 0)   // ---------------- warp 0: the phase-2 MMA stream; warp 1: phase 1
+            for (int it = blockIdx.x, li = 0; it < a.items; it += gridDim.x, ++li)
+                for (int u = 0; u < nblk; ++u) issue(warp == 0, li, u);
+    } else {  // ------------------------------- consumer groups A (warps 2..17) and B (warps 18..25)
         const int grp = warp >= 2 + kAWarps;       // 0: A (row statistics), 1: B (column maxima)
         const int gt = threadIdx.x - 64 - grp * kAThreads;
         const int quad = warp & 3;                 // TMEM lane quadrant this warp may access
@@ -188,33 +228,20 @@ __global__ void __maxnreg__(72)
         const uint32_t lane_base =
             tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(grp * 2) * kT + (uint32_t)half * (grp ? 64u : 32u);
         const float c2 = a.scale * 1.4426950408889634f;
-        const size_t rbase = (size_t)bh * n;
         uint64_t* full = grp ? b_full : a_full;
         uint64_t* empty = grp ? b_empty : a_empty;
-        // a block's 64 columns in two 32-column pieces (register pressure); the
-        // buffer is released after the second piece is read
-        auto load_piece = [&](int u, int pc, uint32_t (&sv)[32]) {
-            const int sb = u & 1;
-            if (pc == 0) {
-                mbar_wait(full + sb, (u >> 1) & 1);
-                tc_fence_after();
-            }
-            tmem_ld32(lane_base + sb * kT + pc * 32, sv);
-            tmem_ld_wait();
-            if (pc == 1) {
-                tc_fence_before();
-                mbar_arrive(empty + sb);
-            }
-        };
         if (grp == 0) {
             // ---------------- group A: row statistics, query tile by query tile
-            for (int qt = 0; qt < nt; ++qt) {
-                float m2 = -INFINITY, l = 0.0f;
-                for (int kt = 0; kt < nt; ++kt) {
-                    {
+            for (int it = blockIdx.x, li = 0; it < a.items; it += gridDim.x, ++li) {
+                const size_t rbase = (size_t)it * n;
+                float* s_lse2 = s_lse2b + (li & 1) * nt * kT;
+                float2* s_ml = s_mlb + (li & 1) * nt * kT;
+                for (int qt = 0; qt < nt; ++qt) {
+                    float m2 = -INFINITY, l = 0.0f;
+                    for (int kt = 0; kt < nt; ++kt) {
                         uint32_t sv[32];
-                        const int u = qt * nt + kt, sb = u & 1;
-                        mbar_wait(full + sb, (u >> 1) & 1);
+                        const int U = li * nblk + qt * nt + kt, sb = U & 1;
+                        mbar_wait(full + sb, (U >> 1) & 1);
                         tc_fence_after();
                         tmem_ld32(lane_base + sb * kT, sv);
                         tmem_ld_wait();
@@ -257,137 +284,162 @@ __global__ void __maxnreg__(72)
                             l = (m2 == -INFINITY ? 0.0f : l * ex2_approx(m2 - mn)) + (acc0 + acc1);
                             m2 = mn;
                         }
+                        if (prof0 && gt == 0 && U < 39) g_k12_prof[1 + U] = clock64();
                     }
-                    if (prof0 && gt == 0 && qt * nt + kt < 39) g_k12_prof[1 + qt * nt + kt] = clock64();
-                }
-                // combine the four column parts of each row
-                float2* cb = combA + (qt & 1) * 4 * kT;
-                if (half != 0) cb[half * kT + row] = make_float2(m2, l);
-                named_bar_sync(1, kAThreads);
-                if (half == 0) {
-                    float mn = m2;
+                    // combine the four column parts of each row
+                    float2* cb = combA + ((li * nt + qt) & 1) * 4 * kT;
+                    if (half != 0) cb[half * kT + row] = make_float2(m2, l);
+                    named_bar_sync(1, kAThreads);
+                    if (half == 0) {
+                        float mn = m2;
 #pragma unroll
-                    for (int p = 1; p < 4; ++p) mn = fmaxf(mn, cb[p * kT + row].x);
-                    float lt = m2 == -INFINITY ? 0.f : l * ex2_approx(m2 - mn);
+                        for (int p = 1; p < 4; ++p) mn = fmaxf(mn, cb[p * kT + row].x);
+                        float lt = m2 == -INFINITY ? 0.f : l * ex2_approx(m2 - mn);
 #pragma unroll
-                    for (int p = 1; p < 4; ++p) {
-                        const float2 o = cb[p * kT + row];
-                        lt += o.x == -INFINITY ? 0.f : o.y * ex2_approx(o.x - mn);
+                        for (int p = 1; p < 4; ++p) {
+                            const float2 o = cb[p * kT + row];
+                            lt += o.x == -INFINITY ? 0.f : o.y * ex2_approx(o.x - mn);
+                        }
+                        const int q = qt * kT + row;
+                        if (q < n) {
+                            const float lse_nat = (mn + __log2f(lt)) * 0.6931471805599453f;
+                            s_lse2[q] = -(lse_nat * 1.4426950408889634f);   // stored negated (FFMA2 addend)
+                            s_ml[q] = make_float2(mn, lt);
+                            a.lse[rbase + q] = lse_nat;
+                            a.row_m[rbase + q] = (double)mn * 0.6931471805599453;
+                            a.row_l[rbase + q] = (double)lt;
+                        } else {
+                            s_lse2[q] = -INFINITY;         // padded queries never win a column maximum
+                        }
+                        mbar_arrive(lse_ready + qt);       // release: this row's statistics are in smem
                     }
-                    const int q = qt * kT + row;
-                    if (q < n) {
-                        const float lse_nat = (mn + __log2f(lt)) * 0.6931471805599453f;
-                        const double md = (double)mn * 0.6931471805599453, ld = (double)lt;
-                        s_lse2[q] = -(lse_nat * 1.4426950408889634f);   // stored negated (FFMA2 addend)
-                        s_m[q] = md;
-                        s_l[q] = ld;
-                        a.lse[rbase + q] = lse_nat;
-                        a.row_m[rbase + q] = md;
-                        a.row_l[rbase + q] = ld;
-                    } else {
-                        s_lse2[q] = -INFINITY;         // padded queries never win a column maximum
-                    }
-                    mbar_arrive(lse_ready + qt);       // release: this row's statistics are in smem
                 }
             }
         } else {
-            // ---------------- group B: per-key column maxima over all queries
-            // running (max, argmax) per key tile in shared memory (this thread's slot)
-            for (int kt = 0; kt < nt; ++kt) combB[(kt * 2 + half) * kT + row] = make_float2(-INFINITY, __int_as_float(0x7FFFFFFF));
-            for (int qt = 0; qt < nt; ++qt) {
-                mbar_wait(lse_ready + qt, 0);          // acquire: lse2 of query tile qt
-                for (int kt = 0; kt < nt; ++kt) {
-                    // two running maxima (even / odd columns) break the compare chain
-                    float b0 = -INFINITY, b1 = -INFINITY;
-                    int i0 = 0x7FFFFFFF, i1 = 0x7FFFFFFF;
+            // ---------------- group B: per-key column maxima over all queries, then Eq. 9
+            for (int it = blockIdx.x, li = 0; it < a.items; it += gridDim.x, ++li) {
+                const int h = it % heads;
+                const size_t rbase = (size_t)it * n;
+                const float* s_lse2 = s_lse2b + (li & 1) * nt * kT;
+                const float2* s_ml = s_mlb + (li & 1) * nt * kT;
+                for (int qt = 0; qt < nt; ++qt) {
+                    mbar_wait(lse_ready + qt, li & 1);     // acquire: lse2 of query tile qt
+                    for (int kt = 0; kt < nt; ++kt) {
+                        const int U = li * nblk + qt * nt + kt, sb = U & 1;
+                        // two running maxima (even / odd columns) break the compare chain
+                        float b0 = -INFINITY, b1 = -INFINITY;
+                        int i0 = 0x7FFFFFFF, i1 = 0x7FFFFFFF;
 #pragma unroll
-                    for (int pc = 0; pc < 2; ++pc) {
-                        uint32_t sv[32];
-                        load_piece(qt * nt + kt, pc, sv);
-                        const int c0 = qt * kT + half * 64 + pc * 32;   // query of sv[0]; padded queries: lse2 = +inf
+                        for (int pc = 0; pc < 2; ++pc) {   // 64 columns in two 32-column pieces (registers)
+                            uint32_t sv[32];
+                            if (pc == 0) {
+                                mbar_wait(full + sb, (U >> 1) & 1);
+                                tc_fence_after();
+                            }
+                            tmem_ld32(lane_base + sb * kT + pc * 32, sv);
+                            tmem_ld_wait();
+                            if (pc == 1) {
+                                tc_fence_before();
+                                mbar_arrive(empty + sb);
+                            }
+                            const int c0 = qt * kT + half * 64 + pc * 32;   // query of sv[0]; padded: lse2 = +inf
 #pragma unroll
-                        for (int g = 0; g < 32; g += 4) {
-                            const float4 nl = *reinterpret_cast<const float4*>(s_lse2 + c0 + g);   // -lse2
-                            const float2 cc = make_float2(c2, c2);
-                            const float2 va = __ffma2_rn(make_float2(__uint_as_float(sv[g]), __uint_as_float(sv[g + 1])), cc,
-                                                         make_float2(nl.x, nl.y));
-                            const float2 vb = __ffma2_rn(make_float2(__uint_as_float(sv[g + 2]), __uint_as_float(sv[g + 3])),
-                                                         cc, make_float2(nl.z, nl.w));
-                            const float v0 = va.x, v1 = va.y, v2 = vb.x, v3 = vb.y;
-                            if (v0 > b0) { b0 = v0; i0 = c0 + g; }
-                            if (v1 > b1) { b1 = v1; i1 = c0 + g + 1; }
-                            if (v2 > b0) { b0 = v2; i0 = c0 + g + 2; }
-                            if (v3 > b1) { b1 = v3; i1 = c0 + g + 3; }
+                            for (int g = 0; g < 32; g += 4) {
+                                const float4 nl = *reinterpret_cast<const float4*>(s_lse2 + c0 + g);   // -lse2
+                                const float2 cc = make_float2(c2, c2);
+                                const float2 va = __ffma2_rn(make_float2(__uint_as_float(sv[g]), __uint_as_float(sv[g + 1])),
+                                                             cc, make_float2(nl.x, nl.y));
+                                const float2 vb = __ffma2_rn(make_float2(__uint_as_float(sv[g + 2]), __uint_as_float(sv[g + 3])),
+                                                             cc, make_float2(nl.z, nl.w));
+                                const float v0 = va.x, v1 = va.y, v2 = vb.x, v3 = vb.y;
+                                if (v0 > b0) { b0 = v0; i0 = c0 + g; }
+                                if (v1 > b1) { b1 = v1; i1 = c0 + g + 1; }
+                                if (v2 > b0) { b0 = v2; i0 = c0 + g + 2; }
+                                if (v3 > b1) { b1 = v3; i1 = c0 + g + 3; }
+                            }
+                        }
+                        // merge: larger value, ties to the smaller query index
+                        if (b1 > b0 || (b1 == b0 && i1 < i0)) { b0 = b1; i0 = i1; }
+                        float2* slot = combB + (kt * 2 + half) * kT + row;
+                        if (qt == 0 || b0 > slot->x) *slot = make_float2(b0, __int_as_float(i0));   // later tiles: larger indices
+                        if (prof0 && gt == 0 && U < 39) g_k12_prof[40 + U] = clock64();
+                    }
+                }
+                // ---------------- Eq. 9, one key per group-B thread
+                named_bar_sync(2, kBThreads);          // the running maxima of this item are final
+                unsigned long long cost = 0, samples = 0, nexact = 0;
+                for (int j = gt; j < n; j += kBThreads) {
+                    const int kt = j / kT, r0 = j - kt * kT;
+                    // the two query halves of the key: larger value, ties to the smaller query index
+                    const float2 m0 = combB[(kt * 2) * kT + r0], m1 = combB[(kt * 2 + 1) * kT + r0];
+                    float bv = m0.x;
+                    int bi = __float_as_int(m0.y);
+                    if (m1.x > bv || (m1.x == bv && __float_as_int(m1.y) < bi)) {
+                        bv = m1.x;
+                        bi = __float_as_int(m1.y);
+                    }
+                    const size_t t = rbase + j;
+                    int r;
+                    bool ex;
+                    if (a.force_exact) {
+                        r = a.d;
+                        ex = true;
+                    } else if (a.budgets_override) {
+                        r = a.budgets_override[t];
+                        ex = a.exact_override[t] != 0;
+                    } else {
+                        // the winner's raw score rebuilt from v (k1_scores_tc), then K2's fp64 softmax entry
+                        const float colscore = (bv - s_lse2[bi]) / c2;   // s_lse2 holds -lse2
+                        const float2 ml = s_ml[bi];
+                        const double md = (double)ml.x * 0.6931471805599453;
+                        const double cm =
+                            __ddiv_rn(exp(__dsub_rn(__dmul_rn(a.scale_d, (double)colscore), md)), (double)ml.y);
+                        if (a.cmax_out) a.cmax_out[t] = cm;
+                        budget_for(cm, n, a.alpha, a.min_samples, a.d, &r, &ex);
+                    }
+                    a.budgets[t] = r;
+                    a.exact[t] = ex ? 1 : 0;
+                    if (ex) {
+                        cost += 2ull * (unsigned long long)a.d * (unsigned long long)a.dh;
+                        nexact += 1;
+                    } else {
+                        cost += (unsigned long long)r * (2ull * a.dh + 3ull);
+                        samples += (unsigned long long)r;
+                    }
+                    if (use_hist) atomicAdd(&s_hist[ex ? a.d : min(r, a.d - 1)], 1u);
+                }
+                if (a.counters) {
+                    for (int off = 16; off; off >>= 1) {
+                        cost += __shfl_xor_sync(0xffffffffu, cost, off);
+                        samples += __shfl_xor_sync(0xffffffffu, samples, off);
+                        nexact += __shfl_xor_sync(0xffffffffu, nexact, off);
+                    }
+                    if (lane == 0) {
+                        if (cost) atomicAdd(a.counters + 0, cost);
+                        if (samples) atomicAdd(a.counters + 1, samples);
+                        if (nexact) atomicAdd(a.counters + 2, nexact);
+                    }
+                }
+                named_bar_sync(2, kBThreads);          // Eq. 9 has read the maxima and the histogram is complete
+                if (use_hist)
+                    for (int i = gt; i <= a.d; i += kBThreads) {
+                        const unsigned int v = s_hist[i];
+                        if (v) {
+                            atomicAdd(&a.hist[(size_t)h * (a.d + 1) + i], v);
+                            s_hist[i] = 0;
                         }
                     }
-                    // merge: larger value, ties to the smaller query index
-                    if (b1 > b0 || (b1 == b0 && i1 < i0)) { b0 = b1; i0 = i1; }
-                    float2* slot = combB + (kt * 2 + half) * kT + row;
-                    if (b0 > slot->x) *slot = make_float2(b0, __int_as_float(i0));   // later tiles: larger indices
-                    if (prof0 && gt == 0 && qt * nt + kt < 39) g_k12_prof[40 + qt * nt + kt] = clock64();
-                }
             }
-        }
-        // ---------------- Eq. 9 for every key, one key per consumer thread (both groups)
-        named_bar_sync(3, kCThreads);              // group B's running maxima are final
-        unsigned long long cost = 0, samples = 0, nexact = 0;
-        for (int j = threadIdx.x - 64; j < n; j += kCThreads) {
-            const int kt = j / kT, r0 = j - kt * kT;
-            // the two query halves of the key: larger value, ties to the smaller query index
-            const float2 m0 = combB[(kt * 2) * kT + r0], m1 = combB[(kt * 2 + 1) * kT + r0];
-            float bv = m0.x;
-            int bi = __float_as_int(m0.y);
-            if (m1.x > bv || (m1.x == bv && __float_as_int(m1.y) < bi)) {
-                bv = m1.x;
-                bi = __float_as_int(m1.y);
-            }
-            const size_t t = rbase + j;
-            int r;
-            bool ex;
-            if (a.force_exact) {
-                r = a.d;
-                ex = true;
-            } else if (a.budgets_override) {
-                r = a.budgets_override[t];
-                ex = a.exact_override[t] != 0;
-            } else {
-                // the winner's raw score rebuilt from v (k1_scores_tc), then K2's fp64 softmax entry
-                const float colscore = (bv - s_lse2[bi]) / c2;   // s_lse2 holds -lse2
-                const double cm = __ddiv_rn(exp(__dsub_rn(__dmul_rn(a.scale_d, (double)colscore), s_m[bi])), s_l[bi]);
-                if (a.cmax_out) a.cmax_out[t] = cm;
-                budget_for(cm, n, a.alpha, a.min_samples, a.d, &r, &ex);
-            }
-            a.budgets[t] = r;
-            a.exact[t] = ex ? 1 : 0;
-            if (ex) {
-                cost += 2ull * (unsigned long long)a.d * (unsigned long long)a.dh;
-                nexact += 1;
-            } else {
-                cost += (unsigned long long)r * (2ull * a.dh + 3ull);
-                samples += (unsigned long long)r;
-            }
-            if (use_hist) atomicAdd(&s_hist[ex ? a.d : min(r, a.d - 1)], 1u);
-        }
-        if (a.counters) {
-            for (int off = 16; off; off >>= 1) {
-                cost += __shfl_xor_sync(0xffffffffu, cost, off);
-                samples += __shfl_xor_sync(0xffffffffu, samples, off);
-                nexact += __shfl_xor_sync(0xffffffffu, nexact, off);
-            }
-            if (lane == 0) {
-                if (cost) atomicAdd(a.counters + 0, cost);
-                if (samples) atomicAdd(a.counters + 1, samples);
-                if (nexact) atomicAdd(a.counters + 2, nexact);
-            }
+            if (prof0 && gt == 0) g_k12_prof[79] = clock64();   // group B done (incl. Eq. 9)
         }
     }
-    if (prof0 && threadIdx.x == 64 + kAThreads) g_k12_prof[79] = clock64();   // group B done (incl. Eq. 9)
     tc_fence_before();
     __syncthreads();
     if (prof0 && threadIdx.x == 0) g_k12_prof[80] = clock64();
-    if (use_hist)
-        for (int i = threadIdx.x; i <= a.d; i += k12::kThreads)
-            if (s_hist[i]) atomicAdd(&a.hist[(size_t)h * (a.d + 1) + i], s_hist[i]);
+    if (MCA_K12_PROF && threadIdx.x == 0 && blockIdx.x < 4096) {
+        g_k12_cta[blockIdx.x][2] = gtimer();
+        g_k12_cta[blockIdx.x][3] = clock64() - c_start;
+    }
     if (warp == 1) tmem_dealloc<512>(tmem);
 }
 

@@ -645,7 +645,9 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
         a.exact = w->exact;
         a.counters = w->counters;
         a.hist = tile_k3 ? nullptr : w->hist;
-        MCA_CUDA_TRY(launch_pdl(k12_fused_tc, dim3((unsigned)(B * H)), dim3(k12::kThreads), smem, stream, tq, tk, a));
+        a.items = B * H;
+        const int grid = std::min(B * H, sm_count());   // persistent: one CTA per SM
+        MCA_CUDA_TRY(launch_pdl(k12_fused_tc, dim3((unsigned)grid), dim3(k12::kThreads), smem, stream, tq, tk, a));
         MCA_LAUNCH_CHECK("k12_fused_tc");
         if (MCA_K12_PROF) {   // diagnostics build: CTA 0's timeline
             long long t[96];
@@ -657,6 +659,16 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
             fprintf(stderr, " | B");
             for (int u = 0; u < nb && u < 39; ++u) fprintf(stderr, " %lld", t[40 + u] - t[0]);
             fprintf(stderr, " | Bdone %lld end %lld\n", t[79] - t[0], t[80] - t[0]);
+            // every CTA: SM, start / end (ns from the first start), cycles
+            static unsigned long long c[4096][4];
+            const int nc = grid < 4096 ? grid : 4096;
+            MCA_CUDA_TRY(cudaMemcpyFromSymbol(c, g_k12_cta, sizeof(unsigned long long) * 4 * nc));
+            unsigned long long t0 = ~0ull;
+            for (int i = 0; i < nc; ++i) t0 = c[i][1] < t0 ? c[i][1] : t0;
+            fprintf(stderr, "k12 CTAS");
+            for (int i = 0; i < nc; ++i)
+                fprintf(stderr, " %llu:%llu:%llu:%llu", c[i][0], c[i][1] - t0, c[i][2] - t0, c[i][3]);
+            fprintf(stderr, "\n");
         }
     }
     // K1: row statistics + column maxima
