@@ -18,11 +18,12 @@
 //       64-column half, combined at the end of each qt: row_m, row_l (fp64),
 //       lse (global + smem), then "lse(qt) ready"
 //   phase 2, block (qt, kt):  S^T = K_kt Q_qt^T (TMEM lane = key)
-//       per key the max over queries of v = t - lse2_q and its first argmax
-//       (two independent running maxima per thread), accumulated over qt;
-//       at the end the owner thread of each key evaluates
-//       cmax = exp(scale S* - m_q*) / l_q* in fp64 and Eq. 9 (budget, exact
-//       flag, FLOP counters, the per-head budget histogram)
+//       per key the max over queries of v = log2(e) (t - lse_q) (one FFMA2
+//       and one three-input max per two scores, two running maxima per
+//       thread), accumulated over qt; at the end group B evaluates
+//       cmax = max_q exp(t_qj - lse_q) = 2^max v in fp64 and Eq. 9 (budget,
+//       exact flag, FLOP counters, the per-head budget histogram). No argmax:
+//       the maximum itself is the softmax entry.
 // The two phases run CONCURRENTLY on two consumer groups: phase 1 is bound by
 // the MUFU (one exponential per score), phase 2 by FMA/ALU issue, so group A
 // exponentiating query tile qt + 1 overlaps group B's maxima over tile qt.
@@ -63,7 +64,7 @@ constexpr uint32_t kTileBytes = kT * kDh * 2;     // 16 KB: 128 rows x 64 bf16, 
 constexpr uint32_t kIdesc = mca_tc::idesc_f16(1, 0, kT, kT);
 
 struct Layout {
-    uint32_t q, k, lse2, ml, comb, hist, bars, bytes;
+    uint32_t q, k, lse2, comb, hist, bars, bytes;
 };
 // Row statistics are double-buffered by item parity: group A writes item i + 1's
 // while group B's Eq. 9 still reads item i's.
@@ -72,9 +73,8 @@ __host__ __device__ inline Layout layout(int nt, int d) {
     L.q = 0;
     L.k = nt * kTileBytes;
     L.lse2 = 2 * nt * kTileBytes;                              // [2][nt*128] f32, -lse in the log2 domain
-    L.ml = L.lse2 + 2 * nt * kT * 4;                           // [2][nt*128] float2 (row max log2, row sum)
-    L.comb = L.ml + 2 * nt * kT * 8;                           // A: [2][4][128] x 8 B; B: [kMaxTiles][2][128] x 8 B
-    L.hist = L.comb + (2 * 4 + 2 * kMaxTiles) * kT * 8;        // [d + 1] u32 budget histogram
+    L.comb = L.lse2 + 2 * nt * kT * 4;                         // A: [2][4][128] x 8 B; B: [kMaxTiles][2][128] x 4 B
+    L.hist = L.comb + 2 * 4 * kT * 8 + 2 * kMaxTiles * kT * 4; // [d + 1] u32 budget histogram
     L.bars = (L.hist + (uint32_t)(d + 1) * 4 + 15) & ~15u;
     L.bytes = L.bars + 512 + 1024;                             // barriers; + alignment slack
     return L;
@@ -117,9 +117,8 @@ __global__ void __maxnreg__(72)
     const int nt = (n + kT - 1) / kT;
     const Layout L = layout(nt, a.d);
     float* s_lse2b = reinterpret_cast<float*>(smem + L.lse2);
-    float2* s_mlb = reinterpret_cast<float2*>(smem + L.ml);
     float2* combA = reinterpret_cast<float2*>(smem + L.comb);        // [2][4][128]  (qt parity, column part)
-    float2* combB = combA + 2 * 4 * kT;                               // [kMaxTiles][2][128] running maxima
+    float* combB = reinterpret_cast<float*>(combA + 2 * 4 * kT);      // [kMaxTiles][2][128] running maxima
     unsigned int* s_hist = reinterpret_cast<unsigned int*>(smem + L.hist);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);
     uint64_t* tile_full = bars;                  // [2 * kMaxTiles]: Q tiles, then K tiles
@@ -235,7 +234,6 @@ __global__ void __maxnreg__(72)
             for (int it = blockIdx.x, li = 0; it < a.items; it += gridDim.x, ++li) {
                 const size_t rbase = (size_t)it * n;
                 float* s_lse2 = s_lse2b + (li & 1) * nt * kT;
-                float2* s_ml = s_mlb + (li & 1) * nt * kT;
                 for (int qt = 0; qt < nt; ++qt) {
                     float m2 = -INFINITY, l = 0.0f;
                     for (int kt = 0; kt < nt; ++kt) {
@@ -304,7 +302,6 @@ __global__ void __maxnreg__(72)
                         if (q < n) {
                             const float lse_nat = (mn + __log2f(lt)) * 0.6931471805599453f;
                             s_lse2[q] = -(lse_nat * 1.4426950408889634f);   // stored negated (FFMA2 addend)
-                            s_ml[q] = make_float2(mn, lt);
                             a.lse[rbase + q] = lse_nat;
                             a.row_m[rbase + q] = (double)mn * 0.6931471805599453;
                             a.row_l[rbase + q] = (double)lt;
@@ -321,14 +318,12 @@ __global__ void __maxnreg__(72)
                 const int h = it % heads;
                 const size_t rbase = (size_t)it * n;
                 const float* s_lse2 = s_lse2b + (li & 1) * nt * kT;
-                const float2* s_ml = s_mlb + (li & 1) * nt * kT;
                 for (int qt = 0; qt < nt; ++qt) {
                     mbar_wait(lse_ready + qt, li & 1);     // acquire: lse2 of query tile qt
                     for (int kt = 0; kt < nt; ++kt) {
                         const int U = li * nblk + qt * nt + kt, sb = U & 1;
-                        // two running maxima (even / odd columns) break the compare chain
-                        float b0 = -INFINITY, b1 = -INFINITY;
-                        int i0 = 0x7FFFFFFF, i1 = 0x7FFFFFFF;
+                        // two running maxima (even / odd columns) break the dependency chain
+                        float m0 = -INFINITY, m1 = -INFINITY;
 #pragma unroll
                         for (int pc = 0; pc < 2; ++pc) {   // 64 columns in two 32-column pieces (registers)
                             uint32_t sv[32];
@@ -342,7 +337,7 @@ __global__ void __maxnreg__(72)
                                 tc_fence_before();
                                 mbar_arrive(empty + sb);
                             }
-                            const int c0 = qt * kT + half * 64 + pc * 32;   // query of sv[0]; padded: lse2 = +inf
+                            const int c0 = qt * kT + half * 64 + pc * 32;   // query of sv[0]; padded: -lse2 = -inf
 #pragma unroll
                             for (int g = 0; g < 32; g += 4) {
                                 const float4 nl = *reinterpret_cast<const float4*>(s_lse2 + c0 + g);   // -lse2
@@ -351,17 +346,12 @@ __global__ void __maxnreg__(72)
                                                              cc, make_float2(nl.x, nl.y));
                                 const float2 vb = __ffma2_rn(make_float2(__uint_as_float(sv[g + 2]), __uint_as_float(sv[g + 3])),
                                                              cc, make_float2(nl.z, nl.w));
-                                const float v0 = va.x, v1 = va.y, v2 = vb.x, v3 = vb.y;
-                                if (v0 > b0) { b0 = v0; i0 = c0 + g; }
-                                if (v1 > b1) { b1 = v1; i1 = c0 + g + 1; }
-                                if (v2 > b0) { b0 = v2; i0 = c0 + g + 2; }
-                                if (v3 > b1) { b1 = v3; i1 = c0 + g + 3; }
+                                m0 = fmaxf(m0, fmaxf(va.x, va.y));   // FMNMX3
+                                m1 = fmaxf(m1, fmaxf(vb.x, vb.y));
                             }
                         }
-                        // merge: larger value, ties to the smaller query index
-                        if (b1 > b0 || (b1 == b0 && i1 < i0)) { b0 = b1; i0 = i1; }
-                        float2* slot = combB + (kt * 2 + half) * kT + row;
-                        if (qt == 0 || b0 > slot->x) *slot = make_float2(b0, __int_as_float(i0));   // later tiles: larger indices
+                        float* slot = combB + (kt * 2 + half) * kT + row;
+                        *slot = qt == 0 ? fmaxf(m0, m1) : fmaxf(*slot, fmaxf(m0, m1));
                         if (prof0 && gt == 0 && U < 39) g_k12_prof[40 + U] = clock64();
                     }
                 }
@@ -370,14 +360,8 @@ __global__ void __maxnreg__(72)
                 unsigned long long cost = 0, samples = 0, nexact = 0;
                 for (int j = gt; j < n; j += kBThreads) {
                     const int kt = j / kT, r0 = j - kt * kT;
-                    // the two query halves of the key: larger value, ties to the smaller query index
-                    const float2 m0 = combB[(kt * 2) * kT + r0], m1 = combB[(kt * 2 + 1) * kT + r0];
-                    float bv = m0.x;
-                    int bi = __float_as_int(m0.y);
-                    if (m1.x > bv || (m1.x == bv && __float_as_int(m1.y) < bi)) {
-                        bv = m1.x;
-                        bi = __float_as_int(m1.y);
-                    }
+                    // v = t - lse in the log2 domain, maximised over both query halves
+                    const float vmax = fmaxf(combB[(kt * 2) * kT + r0], combB[(kt * 2 + 1) * kT + r0]);
                     const size_t t = rbase + j;
                     int r;
                     bool ex;
@@ -388,12 +372,8 @@ __global__ void __maxnreg__(72)
                         r = a.budgets_override[t];
                         ex = a.exact_override[t] != 0;
                     } else {
-                        // the winner's raw score rebuilt from v (k1_scores_tc), then K2's fp64 softmax entry
-                        const float colscore = (bv - s_lse2[bi]) / c2;   // s_lse2 holds -lse2
-                        const float2 ml = s_ml[bi];
-                        const double md = (double)ml.x * 0.6931471805599453;
-                        const double cm =
-                            __ddiv_rn(exp(__dsub_rn(__dmul_rn(a.scale_d, (double)colscore), md)), (double)ml.y);
+                        // cmax = max_q exp(t_qj - lse_q) = 2^vmax, evaluated in fp64
+                        const double cm = exp2((double)vmax);
                         if (a.cmax_out) a.cmax_out[t] = cm;
                         budget_for(cm, n, a.alpha, a.min_samples, a.d, &r, &ex);
                     }
