@@ -1,37 +1,42 @@
 // k12_fused_tc.cu — K1 + K2 fused for BERT-length sequences (bf16, n <= 768):
 // the score pass (attention_matrix + softmax_rows + col_max, SPEC.md:286-294,
-// matrix.hpp:46-53) and Eq. 9 (sample_budgets) for one
-// (b, h) per CTA.
+// matrix.hpp:46-53) and Eq. 9 (sample_budgets) for every
+// (b, h) "item", persistent CTAs (one per SM) walking the items.
 //
-// Same formulas as k1_scores_tc (K1a then K1b) followed by k2_budgets
-// (kKeyArgmax with the tensor-core winner score); the fp32 row sums are
-// accumulated per 32-column part (4 parts) instead of per 64-column half, so
-// lse may differ from the three-kernel path in the last bits, and the budgets
-// are Eq. 9 of this kernel's own cmax (what the parity tests check). The fusion removes
-// the per-tile prologues of two kernels (each of K1a / K1b re-loaded its
-// resident tile and allocated TMEM per 128 rows) and K2's dependent global
-// lookups: Q and K of the (b, h) stay resident in shared memory for both
-// passes, and the winner's row statistics are read from shared memory.
+// Same formulas as k1_scores_tc (K1a then K1b) followed by k2_budgets; the
+// fp32 row sums are accumulated in 4 partial sums per row instead of 2, so lse
+// may differ from the three-kernel path in the last bits, and the budgets are
+// Eq. 9 of this kernel's own cmax (what the parity tests check). Q and K of an
+// item stay resident in shared memory for both passes.
 //
 //   phase 1, block (qt, kt):  S = Q_qt K_kt^T   (TMEM lane = query)
-//       online row max / sum of t = scale S (log2 domain, ex2.approx) per
-//       64-column half, combined at the end of each qt: row_m, row_l (fp64),
-//       lse (global + smem), then "lse(qt) ready"
+//       online row max / sum of t = scale S (log2 domain, ex2.approx) by
+//       group A: 4 partial (max, sum) per row, handed to group B at the end
+//       of each query tile
 //   phase 2, block (qt, kt):  S^T = K_kt Q_qt^T (TMEM lane = key)
-//       per key the max over queries of v = log2(e) (t - lse_q) (one FFMA2
-//       and one three-input max per two scores, two running maxima per
-//       thread), accumulated over qt; at the end group B evaluates
+//       group B combines the partials of query tile qt into lse (global
+//       lse / row_m / row_l, and -lse2 in smem), then per key the max over
+//       queries of v = log2(e) (t - lse_q) (one FFMA2 and one three-input
+//       max per two scores, two running maxima per thread), accumulated over
+//       qt; at the end of the item group B evaluates
 //       cmax = max_q exp(t_qj - lse_q) = 2^max v in fp64 and Eq. 9 (budget,
 //       exact flag, FLOP counters, the per-head budget histogram). No argmax:
 //       the maximum itself is the softmax entry.
-// The two phases run CONCURRENTLY on two consumer groups: phase 1 is bound by
-// the MUFU (one exponential per score), phase 2 by FMA/ALU issue, so group A
-// exponentiating query tile qt + 1 overlaps group B's maxima over tile qt.
+// The two phases run CONCURRENTLY: group A (bound by the MUFU, one exponential
+// per score) streams blocks without ever waiting for group B; group B trails it
+// by a query tile.
+//
+// Group A is split into two sub-groups that take alternate blocks (even /
+// odd block counter, S buffer 0 / 1), 64 columns per warp. On each SM
+// sub-partition two warps exponentiate block u while the other two load and
+// reduce block u + 1, so the exponential unit stays busy across block
+// boundaries (with all four warps on one block they reached the row max /
+// load / wait phases together and the MUFU idled meanwhile).
 //
 // Warp roles (864 threads, one persistent CTA per SM): warp 0 the phase-2 MMA
 // issuer, warp 1 TMEM allocator + phase-1 MMA issuer, warps 2-17 group A (four
-// warps per TMEM lane quadrant, 32 columns of a block each), warps 18-25 group
-// B (two per quadrant, 64 columns each), warp 26 the TMA producer.
+// warps per TMEM lane quadrant), warps 18-25 group B (two per quadrant, 64
+// columns each), warp 26 the TMA producer.
 // TMEM: A buffers [0,256), B buffers [256,512).
 #include "mca_common.cuh"
 #include "tc_common.cuh"
@@ -43,7 +48,7 @@ namespace mca_dev {
 #endif
 // Diagnostics (build with EXTRA=-DMCA_K12_PROF=1): clock64 stamps of CTA 0:
 // [0] start, [1 + u] group A block u done, [40 + u] group B block u done, [80] end
-__device__ long long g_k12_prof[96];
+__device__ long long g_k12_prof[160];   // + [96 + U] A wait done, [112 + U] A load done, [128 + qt] A combine done
 // per CTA: smid, globaltimer at start and at exit (ns), clocks at exit - start
 __device__ unsigned long long g_k12_cta[4096][4];
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -55,7 +60,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 namespace k12 {
 constexpr int kT = 128;                           // tile rows (= block columns)
 constexpr int kMaxTiles = 6;                      // n <= 768
-constexpr int kAWarps = 16;                       // group A: 4 per TMEM lane quadrant, 32 columns each
+constexpr int kAWarps = 16;                       // group A: 4 per TMEM lane quadrant (2 sub-groups x 2 column halves)
 constexpr int kBWarps = 8;                        // group B: 2 per TMEM lane quadrant, 64 columns each
 constexpr int kAThreads = kAWarps * 32, kBThreads = kBWarps * 32;
 constexpr int kCThreads = kAThreads + kBThreads;
@@ -66,14 +71,12 @@ constexpr uint32_t kIdesc = mca_tc::idesc_f16(1, 0, kT, kT);
 struct Layout {
     uint32_t q, k, lse2, comb, hist, bars, bytes;
 };
-// Row statistics are double-buffered by item parity: group A writes item i + 1's
-// while group B's Eq. 9 still reads item i's.
 __host__ __device__ inline Layout layout(int nt, int d) {
     Layout L;
     L.q = 0;
     L.k = nt * kTileBytes;
-    L.lse2 = 2 * nt * kTileBytes;                              // [2][nt*128] f32, -lse in the log2 domain
-    L.comb = L.lse2 + 2 * nt * kT * 4;                         // A: [2][4][128] x 8 B; B: [kMaxTiles][2][128] x 4 B
+    L.lse2 = 2 * nt * kTileBytes;                              // [2][128] f32: -lse2 of a query tile (qt parity)
+    L.comb = L.lse2 + 2 * kT * 4;                              // A partials [2][4][128] x 8 B; B maxima [kMaxTiles][2][128] x 4 B
     L.hist = L.comb + 2 * 4 * kT * 8 + 2 * kMaxTiles * kT * 4; // [d + 1] u32 budget histogram
     L.bars = (L.hist + (uint32_t)(d + 1) * 4 + 15) & ~15u;
     L.bytes = L.bars + 512 + 1024;                             // barriers; + alignment slack
@@ -101,12 +104,10 @@ struct K12Args {
 // Persistent: one CTA per SM walks the items (b, h) = blockIdx.x, + gridDim.x, ...
 // Every stream (TMA, the two MMA issuers, both consumer groups) runs ahead into
 // the next item as far as its buffers allow, so the next item's tile loads and
-// group A's first query tile overlap group B's last query tile and Eq. 9 of the
-// current one (no per-item prologue, no tail where one group idles).
-//   Q tile t of item i is overwritten for item i + 1 once phase 2 has consumed it
-//   (q_empty[t], committed by the phase-2 issuer after block (t, nt - 1)) and
-//   phase 1 has (lse_ready[t] of item i); K tile t once phase 2's block
-//   (nt - 1, t) is done (k_empty[t]) and lse_ready[nt - 1].
+// group A's first query tile overlap group B's last query tile and Eq. 9.
+// Q tile t / K tile t of item i is overwritten for item i + 1 once the last
+// MMA of each phase reading it completed (tile_empty1 / tile_empty2, committed
+// by the phase's issuer after its last block using the tile).
 __global__ void __maxnreg__(72)
     k12_fused_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k, K12Args a) {
     using namespace k12;
@@ -116,19 +117,21 @@ __global__ void __maxnreg__(72)
     const int n = a.n, heads = a.heads;
     const int nt = (n + kT - 1) / kT;
     const Layout L = layout(nt, a.d);
-    float* s_lse2b = reinterpret_cast<float*>(smem + L.lse2);
-    float2* combA = reinterpret_cast<float2*>(smem + L.comb);        // [2][4][128]  (qt parity, column part)
+    float* s_lse2b = reinterpret_cast<float*>(smem + L.lse2);          // [2][128]
+    float2* combA = reinterpret_cast<float2*>(smem + L.comb);        // [2][4][128] (query-tile parity, part)
     float* combB = reinterpret_cast<float*>(combA + 2 * 4 * kT);      // [kMaxTiles][2][128] running maxima
     unsigned int* s_hist = reinterpret_cast<unsigned int*>(smem + L.hist);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);
     uint64_t* tile_full = bars;                  // [2 * kMaxTiles]: Q tiles, then K tiles
-    uint64_t* tile_empty = bars + 2 * kMaxTiles; // [2 * kMaxTiles]: phase 2 is done with the tile
-    uint64_t* a_full = bars + 4 * kMaxTiles;     // [2] phase-1 S buffers
+    uint64_t* tile_empty1 = bars + 2 * kMaxTiles;   // phase 1 is done with the tile
+    uint64_t* tile_empty2 = bars + 4 * kMaxTiles;   // phase 2 is done with the tile
+    uint64_t* a_full = bars + 6 * kMaxTiles;     // [2] phase-1 S buffers
     uint64_t* a_empty = a_full + 2;              // [2]
     uint64_t* b_full = a_empty + 2;              // [2] phase-2 S^T buffers
     uint64_t* b_empty = b_full + 2;              // [2]
-    uint64_t* lse_ready = b_empty + 2;           // [kMaxTiles]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(lse_ready + kMaxTiles);
+    uint64_t* comb_full = b_empty + 2;           // [2] A's partials of a query tile are in combA
+    uint64_t* comb_empty = comb_full + 2;        // [2] B has read them
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(comb_empty + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nblk = nt * nt;
@@ -148,15 +151,17 @@ __global__ void __maxnreg__(72)
     if (threadIdx.x == 0) {
         for (int t = 0; t < 2 * nt; ++t) {
             mbar_init(tile_full + t, 1);
-            mbar_init(tile_empty + t, 1);
+            mbar_init(tile_empty1 + t, 1);
+            mbar_init(tile_empty2 + t, 1);
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(a_full + i, 1);
-            mbar_init(a_empty + i, kAThreads);
+            mbar_init(a_empty + i, kAThreads / 2);   // one sub-group per buffer
             mbar_init(b_full + i, 1);
             mbar_init(b_empty + i, kBThreads);
+            mbar_init(comb_full + i, kAThreads);
+            mbar_init(comb_empty + i, 1);
         }
-        for (int t = 0; t < kMaxTiles; ++t) mbar_init(lse_ready + t, kAThreads / 4);
         fence_barrier_init();
     }
     if (use_hist)
@@ -190,10 +195,9 @@ __global__ void __maxnreg__(72)
             umma_f16(d, sw128_desc(a_addr + kk * 32, 16, 1024), sw128_desc(b_addr + kk * 32, 16, 1024), kIdesc,
                      kk > 0 ? 1u : 0u);
         umma_commit(full + sb);
-        if (phase) {   // phase 2 is the tiles' last reader
-            if (kt == nt - 1) umma_commit(tile_empty + qt);
-            if (qt == nt - 1) umma_commit(tile_empty + nt + kt);
-        }
+        uint64_t* tile_empty = phase ? tile_empty2 : tile_empty1;   // this phase's last read of a tile
+        if (kt == nt - 1) umma_commit(tile_empty + qt);
+        if (qt == nt - 1) umma_commit(tile_empty + nt + kt);
     };
     if (warp == k12::kThreads / 32 - 1) {
         if (lane == 0) {  // ---------------- TMA: every Q and K tile of each item once
@@ -204,9 +208,9 @@ __global__ void __maxnreg__(72)
                 const int b = it / heads, h = it - b * heads;
                 for (int t = 0; t < nt; ++t)
                     for (int op = 0; op < 2; ++op) {   // 0: Q tile t, 1: K tile t
-                        if (li > 0) {   // phase 2, then phase 1 of the previous item are done with the slot
-                            mbar_wait(tile_empty + op * nt + t, (li - 1) & 1);
-                            mbar_wait(lse_ready + (op ? nt - 1 : t), (li - 1) & 1);
+                        if (li > 0) {   // both phases of the previous item are done with the slot
+                            mbar_wait(tile_empty1 + op * nt + t, (li - 1) & 1);
+                            mbar_wait(tile_empty2 + op * nt + t, (li - 1) & 1);
                         }
                         mbar_expect_tx(tile_full + op * nt + t, kTileBytes);
                         tma_load_3d(smem + (op ? L.k : L.q) + t * kTileBytes, op ? &tm_k : &tm_q,
@@ -218,34 +222,36 @@ __global__ void __maxnreg__(72)
         if (lane == 0)   // ---------------- warp 0: the phase-2 MMA stream; warp 1: phase 1
             for (int it = blockIdx.x, li = 0; it < a.items; it += gridDim.x, ++li)
                 for (int u = 0; u < nblk; ++u) issue(warp == 0, li, u);
-    } else {  // ------------------------------- consumer groups A (warps 2..17) and B (warps 18..25)
-        const int grp = warp >= 2 + kAWarps;       // 0: A (row statistics), 1: B (column maxima)
-        const int gt = threadIdx.x - 64 - grp * kAThreads;
+    } else if (warp < 2 + kAWarps) {
+        // ---------------- group A: partial row statistics. Sub-group sub takes the
+        // blocks with U & 1 == sub (S buffer sub), 64 columns [64 ch, +64) per warp.
+        const int gt = threadIdx.x - 64;
         const int quad = warp & 3;                 // TMEM lane quadrant this warp may access
-        const int half = (gt >> 5) >> 2;           // A: columns [32 half, +32) (4 parts); B: [64 half, +64)
-        const int row = quad * 32 + lane;          // TMEM lane = resident row (query in A, key in B)
-        const uint32_t lane_base =
-            tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(grp * 2) * kT + (uint32_t)half * (grp ? 64u : 32u);
+        const int part = gt >> 7;                  // 0..3: (sub, ch) = (part >> 1, part & 1)
+        const int sub = part >> 1, ch = part & 1;
+        const int row = quad * 32 + lane;          // TMEM lane = query row of the tile
+        const uint32_t lane_base = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)sub * kT + (uint32_t)ch * 64u;
         const float c2 = a.scale * 1.4426950408889634f;
-        uint64_t* full = grp ? b_full : a_full;
-        uint64_t* empty = grp ? b_empty : a_empty;
-        if (grp == 0) {
-            // ---------------- group A: row statistics, query tile by query tile
-            for (int it = blockIdx.x, li = 0; it < a.items; it += gridDim.x, ++li) {
-                const size_t rbase = (size_t)it * n;
-                float* s_lse2 = s_lse2b + (li & 1) * nt * kT;
-                for (int qt = 0; qt < nt; ++qt) {
-                    float m2 = -INFINITY, l = 0.0f;
-                    for (int kt = 0; kt < nt; ++kt) {
+        for (int it = blockIdx.x, li = 0; it < a.items; it += gridDim.x, ++li) {
+            for (int qt = 0; qt < nt; ++qt) {
+                float m2 = -INFINITY, l = 0.0f;
+                for (int kt = 0; kt < nt; ++kt) {
+                    const int U = li * nblk + qt * nt + kt;
+                    if ((U & 1) != sub) continue;
+                    mbar_wait(a_full + sub, (U >> 1) & 1);
+                    if (prof0 && gt == 0 && U < 16) g_k12_prof[96 + U] = clock64();
+                    tc_fence_after();
+#pragma unroll 1
+                    for (int pc = 0; pc < 2; ++pc) {
                         uint32_t sv[32];
-                        const int U = li * nblk + qt * nt + kt, sb = U & 1;
-                        mbar_wait(full + sb, (U >> 1) & 1);
-                        tc_fence_after();
-                        tmem_ld32(lane_base + sb * kT, sv);
+                        tmem_ld32(lane_base + pc * 32, sv);
                         tmem_ld_wait();
-                        tc_fence_before();
-                        mbar_arrive(empty + sb);
-                        const int valid = n - (kt * kT + half * 32);   // <= 0: this part is past n
+                        if (pc == 1) {
+                            tc_fence_before();
+                            mbar_arrive(a_empty + sub);
+                        }
+                        if (prof0 && gt == 0 && U < 16 && pc == 0) g_k12_prof[112 + U] = clock64();
+                        const int valid = n - (kt * kT + ch * 64 + pc * 32);   // <= 0: this piece is past n
                         float bmax = -INFINITY;
                         if (valid >= 32) {   // pairwise tree: 5 dependent levels instead of 32
                             float t16[16];
@@ -282,136 +288,147 @@ __global__ void __maxnreg__(72)
                             l = (m2 == -INFINITY ? 0.0f : l * ex2_approx(m2 - mn)) + (acc0 + acc1);
                             m2 = mn;
                         }
-                        if (prof0 && gt == 0 && U < 39) g_k12_prof[1 + U] = clock64();
                     }
-                    // combine the four column parts of each row
-                    float2* cb = combA + ((li * nt + qt) & 1) * 4 * kT;
-                    if (half != 0) cb[half * kT + row] = make_float2(m2, l);
-                    named_bar_sync(1, kAThreads);
-                    if (half == 0) {
-                        float mn = m2;
-#pragma unroll
-                        for (int p = 1; p < 4; ++p) mn = fmaxf(mn, cb[p * kT + row].x);
-                        float lt = m2 == -INFINITY ? 0.f : l * ex2_approx(m2 - mn);
-#pragma unroll
-                        for (int p = 1; p < 4; ++p) {
-                            const float2 o = cb[p * kT + row];
-                            lt += o.x == -INFINITY ? 0.f : o.y * ex2_approx(o.x - mn);
-                        }
-                        const int q = qt * kT + row;
-                        if (q < n) {
-                            const float lse_nat = (mn + __log2f(lt)) * 0.6931471805599453f;
-                            s_lse2[q] = -(lse_nat * 1.4426950408889634f);   // stored negated (FFMA2 addend)
-                            a.lse[rbase + q] = lse_nat;
-                            a.row_m[rbase + q] = (double)mn * 0.6931471805599453;
-                            a.row_l[rbase + q] = (double)lt;
-                        } else {
-                            s_lse2[q] = -INFINITY;         // padded queries never win a column maximum
-                        }
-                        mbar_arrive(lse_ready + qt);       // release: this row's statistics are in smem
-                    }
+                    if (prof0 && gt == 0 && U < 39) g_k12_prof[1 + U] = clock64();
                 }
+                // hand this row's partial (max, sum) to group B
+                const int gq = li * nt + qt;
+                mbar_wait(comb_empty + (gq & 1), ((gq >> 1) & 1) ^ 1);
+                combA[((gq & 1) * 4 + part) * kT + row] = make_float2(m2, l);
+                mbar_arrive(comb_full + (gq & 1));
             }
-        } else {
-            // ---------------- group B: per-key column maxima over all queries, then Eq. 9
-            for (int it = blockIdx.x, li = 0; it < a.items; it += gridDim.x, ++li) {
-                const int h = it % heads;
-                const size_t rbase = (size_t)it * n;
-                const float* s_lse2 = s_lse2b + (li & 1) * nt * kT;
-                for (int qt = 0; qt < nt; ++qt) {
-                    mbar_wait(lse_ready + qt, li & 1);     // acquire: lse2 of query tile qt
-                    for (int kt = 0; kt < nt; ++kt) {
-                        const int U = li * nblk + qt * nt + kt, sb = U & 1;
-                        // two running maxima (even / odd columns) break the dependency chain
-                        float m0 = -INFINITY, m1 = -INFINITY;
-#pragma unroll
-                        for (int pc = 0; pc < 2; ++pc) {   // 64 columns in two 32-column pieces (registers)
-                            uint32_t sv[32];
-                            if (pc == 0) {
-                                mbar_wait(full + sb, (U >> 1) & 1);
-                                tc_fence_after();
-                            }
-                            tmem_ld32(lane_base + sb * kT + pc * 32, sv);
-                            tmem_ld_wait();
-                            if (pc == 1) {
-                                tc_fence_before();
-                                mbar_arrive(empty + sb);
-                            }
-                            const int c0 = qt * kT + half * 64 + pc * 32;   // query of sv[0]; padded: -lse2 = -inf
-#pragma unroll
-                            for (int g = 0; g < 32; g += 4) {
-                                const float4 nl = *reinterpret_cast<const float4*>(s_lse2 + c0 + g);   // -lse2
-                                const float2 cc = make_float2(c2, c2);
-                                const float2 va = __ffma2_rn(make_float2(__uint_as_float(sv[g]), __uint_as_float(sv[g + 1])),
-                                                             cc, make_float2(nl.x, nl.y));
-                                const float2 vb = __ffma2_rn(make_float2(__uint_as_float(sv[g + 2]), __uint_as_float(sv[g + 3])),
-                                                             cc, make_float2(nl.z, nl.w));
-                                m0 = fmaxf(m0, fmaxf(va.x, va.y));   // FMNMX3
-                                m1 = fmaxf(m1, fmaxf(vb.x, vb.y));
-                            }
-                        }
-                        float* slot = combB + (kt * 2 + half) * kT + row;
-                        *slot = qt == 0 ? fmaxf(m0, m1) : fmaxf(*slot, fmaxf(m0, m1));
-                        if (prof0 && gt == 0 && U < 39) g_k12_prof[40 + U] = clock64();
-                    }
-                }
-                // ---------------- Eq. 9, one key per group-B thread
-                named_bar_sync(2, kBThreads);          // the running maxima of this item are final
-                unsigned long long cost = 0, samples = 0, nexact = 0;
-                for (int j = gt; j < n; j += kBThreads) {
-                    const int kt = j / kT, r0 = j - kt * kT;
-                    // v = t - lse in the log2 domain, maximised over both query halves
-                    const float vmax = fmaxf(combB[(kt * 2) * kT + r0], combB[(kt * 2 + 1) * kT + r0]);
-                    const size_t t = rbase + j;
-                    int r;
-                    bool ex;
-                    if (a.force_exact) {
-                        r = a.d;
-                        ex = true;
-                    } else if (a.budgets_override) {
-                        r = a.budgets_override[t];
-                        ex = a.exact_override[t] != 0;
-                    } else {
-                        // cmax = max_q exp(t_qj - lse_q) = 2^vmax, evaluated in fp64
-                        const double cm = exp2((double)vmax);
-                        if (a.cmax_out) a.cmax_out[t] = cm;
-                        budget_for(cm, n, a.alpha, a.min_samples, a.d, &r, &ex);
-                    }
-                    a.budgets[t] = r;
-                    a.exact[t] = ex ? 1 : 0;
-                    if (ex) {
-                        cost += 2ull * (unsigned long long)a.d * (unsigned long long)a.dh;
-                        nexact += 1;
-                    } else {
-                        cost += (unsigned long long)r * (2ull * a.dh + 3ull);
-                        samples += (unsigned long long)r;
-                    }
-                    if (use_hist) atomicAdd(&s_hist[ex ? a.d : min(r, a.d - 1)], 1u);
-                }
-                if (a.counters) {
-                    for (int off = 16; off; off >>= 1) {
-                        cost += __shfl_xor_sync(0xffffffffu, cost, off);
-                        samples += __shfl_xor_sync(0xffffffffu, samples, off);
-                        nexact += __shfl_xor_sync(0xffffffffu, nexact, off);
-                    }
-                    if (lane == 0) {
-                        if (cost) atomicAdd(a.counters + 0, cost);
-                        if (samples) atomicAdd(a.counters + 1, samples);
-                        if (nexact) atomicAdd(a.counters + 2, nexact);
-                    }
-                }
-                named_bar_sync(2, kBThreads);          // Eq. 9 has read the maxima and the histogram is complete
-                if (use_hist)
-                    for (int i = gt; i <= a.d; i += kBThreads) {
-                        const unsigned int v = s_hist[i];
-                        if (v) {
-                            atomicAdd(&a.hist[(size_t)h * (a.d + 1) + i], v);
-                            s_hist[i] = 0;
-                        }
-                    }
-            }
-            if (prof0 && gt == 0) g_k12_prof[79] = clock64();   // group B done (incl. Eq. 9)
         }
+    } else {
+        // ---------------- group B: lse of each query tile, per-key column maxima, Eq. 9
+        const int gt = threadIdx.x - 64 - kAThreads;
+        const int quad = warp & 3;
+        const int half = gt >> 7;                  // columns (queries) [64 half, +64) of a block
+        const int row = quad * 32 + lane;          // TMEM lane = key row of the tile
+        const uint32_t lane_base = tmem + ((uint32_t)(quad * 32) << 16) + 2u * kT + (uint32_t)half * 64u;
+        const float c2 = a.scale * 1.4426950408889634f;
+        for (int it = blockIdx.x, li = 0; it < a.items; it += gridDim.x, ++li) {
+            const int h = it % heads;
+            const size_t rbase = (size_t)it * n;
+            for (int qt = 0; qt < nt; ++qt) {
+                const int gq = li * nt + qt;
+                float* s_lse2 = s_lse2b + (gq & 1) * kT;
+                mbar_wait(comb_full + (gq & 1), (gq >> 1) & 1);   // acquire: group A's partials of tile qt
+                if (gt < kT) {   // combine the four partials of query row gt
+                    const float2* cb = combA + (gq & 1) * 4 * kT + gt;
+                    float mn = cb[0].x;
+#pragma unroll
+                    for (int p = 1; p < 4; ++p) mn = fmaxf(mn, cb[p * kT].x);
+                    float lt = 0.f;
+#pragma unroll
+                    for (int p = 0; p < 4; ++p) {
+                        const float2 o = cb[p * kT];
+                        lt += o.x == -INFINITY ? 0.f : o.y * ex2_approx(o.x - mn);
+                    }
+                    const int q = qt * kT + gt;
+                    if (q < n) {
+                        const float lse_nat = (mn + __log2f(lt)) * 0.6931471805599453f;
+                        s_lse2[gt] = -(lse_nat * 1.4426950408889634f);   // stored negated (FFMA2 addend)
+                        a.lse[rbase + q] = lse_nat;
+                        a.row_m[rbase + q] = (double)mn * 0.6931471805599453;
+                        a.row_l[rbase + q] = (double)lt;
+                    } else {
+                        s_lse2[gt] = -INFINITY;         // padded queries never win a column maximum
+                    }
+                }
+                named_bar_sync(2, kBThreads);          // -lse2 of tile qt is in smem; the partials are read
+                if (gt == 0) mbar_arrive(comb_empty + (gq & 1));
+                if (prof0 && gt == 0 && qt < 16 && li == 0) g_k12_prof[128 + qt] = clock64();
+                for (int kt = 0; kt < nt; ++kt) {
+                    const int U = li * nblk + qt * nt + kt, sb = U & 1;
+                    // two running maxima break the dependency chain
+                    float m0 = -INFINITY, m1 = -INFINITY;
+#pragma unroll
+                    for (int pc = 0; pc < 2; ++pc) {   // 64 columns in two 32-column pieces (registers)
+                        uint32_t sv[32];
+                        if (pc == 0) {
+                            mbar_wait(b_full + sb, (U >> 1) & 1);
+                            tc_fence_after();
+                        }
+                        tmem_ld32(lane_base + sb * kT + pc * 32, sv);
+                        tmem_ld_wait();
+                        if (pc == 1) {
+                            tc_fence_before();
+                            mbar_arrive(b_empty + sb);
+                        }
+                        const int c0 = half * 64 + pc * 32;   // query (in the tile) of sv[0]
+#pragma unroll
+                        for (int g = 0; g < 32; g += 4) {
+                            const float4 nl = *reinterpret_cast<const float4*>(s_lse2 + c0 + g);   // -lse2
+                            const float2 cc = make_float2(c2, c2);
+                            const float2 va = __ffma2_rn(make_float2(__uint_as_float(sv[g]), __uint_as_float(sv[g + 1])),
+                                                         cc, make_float2(nl.x, nl.y));
+                            const float2 vb = __ffma2_rn(make_float2(__uint_as_float(sv[g + 2]), __uint_as_float(sv[g + 3])),
+                                                         cc, make_float2(nl.z, nl.w));
+                            m0 = fmaxf(m0, fmaxf(va.x, va.y));   // FMNMX3
+                            m1 = fmaxf(m1, fmaxf(vb.x, vb.y));
+                        }
+                    }
+                    float* slot = combB + (kt * 2 + half) * kT + row;
+                    *slot = qt == 0 ? fmaxf(m0, m1) : fmaxf(*slot, fmaxf(m0, m1));
+                    if (prof0 && gt == 0 && U < 39) g_k12_prof[40 + U] = clock64();
+                }
+            }
+            // ---------------- Eq. 9, one key per group-B thread
+            named_bar_sync(2, kBThreads);          // the running maxima of this item are final
+            unsigned long long cost = 0, samples = 0, nexact = 0;
+            for (int j = gt; j < n; j += kBThreads) {
+                const int kt = j / kT, r0 = j - kt * kT;
+                // v = t - lse in the log2 domain, maximised over both query halves
+                const float vmax = fmaxf(combB[(kt * 2) * kT + r0], combB[(kt * 2 + 1) * kT + r0]);
+                const size_t t = rbase + j;
+                int r;
+                bool ex;
+                if (a.force_exact) {
+                    r = a.d;
+                    ex = true;
+                } else if (a.budgets_override) {
+                    r = a.budgets_override[t];
+                    ex = a.exact_override[t] != 0;
+                } else {
+                    // cmax = max_q exp(t_qj - lse_q) = 2^vmax, evaluated in fp64
+                    const double cm = exp2((double)vmax);
+                    if (a.cmax_out) a.cmax_out[t] = cm;
+                    budget_for(cm, n, a.alpha, a.min_samples, a.d, &r, &ex);
+                }
+                a.budgets[t] = r;
+                a.exact[t] = ex ? 1 : 0;
+                if (ex) {
+                    cost += 2ull * (unsigned long long)a.d * (unsigned long long)a.dh;
+                    nexact += 1;
+                } else {
+                    cost += (unsigned long long)r * (2ull * a.dh + 3ull);
+                    samples += (unsigned long long)r;
+                }
+                if (use_hist) atomicAdd(&s_hist[ex ? a.d : min(r, a.d - 1)], 1u);
+            }
+            if (a.counters) {
+                for (int off = 16; off; off >>= 1) {
+                    cost += __shfl_xor_sync(0xffffffffu, cost, off);
+                    samples += __shfl_xor_sync(0xffffffffu, samples, off);
+                    nexact += __shfl_xor_sync(0xffffffffu, nexact, off);
+                }
+                if (lane == 0) {
+                    if (cost) atomicAdd(a.counters + 0, cost);
+                    if (samples) atomicAdd(a.counters + 1, samples);
+                    if (nexact) atomicAdd(a.counters + 2, nexact);
+                }
+            }
+            named_bar_sync(2, kBThreads);          // Eq. 9 has read the maxima and the histogram is complete
+            if (use_hist)
+                for (int i = gt; i <= a.d; i += kBThreads) {
+                    const unsigned int v = s_hist[i];
+                    if (v) {
+                        atomicAdd(&a.hist[(size_t)h * (a.d + 1) + i], v);
+                        s_hist[i] = 0;
+                    }
+                }
+        }
+        if (prof0 && gt == 0) g_k12_prof[79] = clock64();   // group B done (incl. Eq. 9)
     }
     tc_fence_before();
     __syncthreads();

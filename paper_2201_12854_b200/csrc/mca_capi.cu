@@ -650,7 +650,7 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
         MCA_CUDA_TRY(launch_pdl(k12_fused_tc, dim3((unsigned)grid), dim3(k12::kThreads), smem, stream, tq, tk, a));
         MCA_LAUNCH_CHECK("k12_fused_tc");
         if (MCA_K12_PROF) {   // diagnostics build: CTA 0's timeline
-            long long t[96];
+            long long t[160];
             MCA_CUDA_TRY(cudaStreamSynchronize(stream));
             MCA_CUDA_TRY(cudaMemcpyFromSymbol(t, g_k12_prof, sizeof(t)));
             const int nb = ((n + 127) / 128) * ((n + 127) / 128);
@@ -659,6 +659,12 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
             fprintf(stderr, " | B");
             for (int u = 0; u < nb && u < 39; ++u) fprintf(stderr, " %lld", t[40 + u] - t[0]);
             fprintf(stderr, " | Bdone %lld end %lld\n", t[79] - t[0], t[80] - t[0]);
+            fprintf(stderr, "k12 CTA0 A wait/load/end:");
+            for (int u = 0; u < nb && u < 16; ++u)
+                fprintf(stderr, " %lld/%lld/%lld", t[96 + u] - t[0], t[112 + u] - t[0], t[1 + u] - t[0]);
+            fprintf(stderr, " | combine");
+            for (int q = 0; q * q < nb && q < 16; ++q) fprintf(stderr, " %lld", t[128 + q] - t[0]);
+            fprintf(stderr, "\n");
             // every CTA: SM, start / end (ns from the first start), cycles
             static unsigned long long c[4096][4];
             const int nc = grid < 4096 ? grid : 4096;
