@@ -48,7 +48,7 @@ namespace mca_dev {
 #endif
 // Diagnostics (build with EXTRA=-DMCA_K12_PROF=1): clock64 stamps of CTA 0:
 // [0] start, [1 + u] group A block u done, [40 + u] group B block u done, [80] end
-__device__ long long g_k12_prof[160];   // + [96 + U] A wait done, [112 + U] A load done, [128 + qt] A combine done
+__device__ long long g_k12_prof[256];   // + [96 + U] A wait done, [128 + U] / [160 + U] A piece loads done, [192 + U] phase-1 MMA issued, [224 + qt] lse of tile qt
 // per CTA: smid, globaltimer at start and at exit (ns), clocks at exit - start
 __device__ unsigned long long g_k12_cta[4096][4];
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -195,6 +195,7 @@ __global__ void __maxnreg__(72)
             umma_f16(d, sw128_desc(a_addr + kk * 32, 16, 1024), sw128_desc(b_addr + kk * 32, 16, 1024), kIdesc,
                      kk > 0 ? 1u : 0u);
         umma_commit(full + sb);
+        if (prof0 && phase == 0 && U < 32) g_k12_prof[192 + U] = clock64();
         uint64_t* tile_empty = phase ? tile_empty2 : tile_empty1;   // this phase's last read of a tile
         if (kt == nt - 1) umma_commit(tile_empty + qt);
         if (qt == nt - 1) umma_commit(tile_empty + nt + kt);
@@ -239,7 +240,7 @@ __global__ void __maxnreg__(72)
                     const int U = li * nblk + qt * nt + kt;
                     if ((U & 1) != sub) continue;
                     mbar_wait(a_full + sub, (U >> 1) & 1);
-                    if (prof0 && gt == 0 && U < 16) g_k12_prof[96 + U] = clock64();
+                    if (prof0 && (gt & 255) == 0 && U < 32) g_k12_prof[96 + U] = clock64();
                     tc_fence_after();
 #pragma unroll 1
                     for (int pc = 0; pc < 2; ++pc) {
@@ -250,7 +251,7 @@ __global__ void __maxnreg__(72)
                             tc_fence_before();
                             mbar_arrive(a_empty + sub);
                         }
-                        if (prof0 && gt == 0 && U < 16 && pc == 0) g_k12_prof[112 + U] = clock64();
+                        if (prof0 && (gt & 255) == 0 && U < 32) g_k12_prof[128 + 32 * pc + U] = clock64();
                         const int valid = n - (kt * kT + ch * 64 + pc * 32);   // <= 0: this piece is past n
                         float bmax = -INFINITY;
                         if (valid >= 32) {   // pairwise tree: 5 dependent levels instead of 32
@@ -289,7 +290,7 @@ __global__ void __maxnreg__(72)
                             m2 = mn;
                         }
                     }
-                    if (prof0 && gt == 0 && U < 39) g_k12_prof[1 + U] = clock64();
+                    if (prof0 && (gt & 255) == 0 && U < 39) g_k12_prof[1 + U] = clock64();
                 }
                 // hand this row's partial (max, sum) to group B
                 const int gq = li * nt + qt;
@@ -337,7 +338,7 @@ __global__ void __maxnreg__(72)
                 }
                 named_bar_sync(2, kBThreads);          // -lse2 of tile qt is in smem; the partials are read
                 if (gt == 0) mbar_arrive(comb_empty + (gq & 1));
-                if (prof0 && gt == 0 && qt < 16 && li == 0) g_k12_prof[128 + qt] = clock64();
+                if (prof0 && gt == 0 && li * nt + qt < 32) g_k12_prof[224 + li * nt + qt] = clock64();
                 for (int kt = 0; kt < nt; ++kt) {
                     const int U = li * nblk + qt * nt + kt, sb = U & 1;
                     // two running maxima break the dependency chain

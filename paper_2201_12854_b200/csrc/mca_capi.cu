@@ -650,20 +650,22 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
         MCA_CUDA_TRY(launch_pdl(k12_fused_tc, dim3((unsigned)grid), dim3(k12::kThreads), smem, stream, tq, tk, a));
         MCA_LAUNCH_CHECK("k12_fused_tc");
         if (MCA_K12_PROF) {   // diagnostics build: CTA 0's timeline
-            long long t[160];
+            long long t[256];
             MCA_CUDA_TRY(cudaStreamSynchronize(stream));
             MCA_CUDA_TRY(cudaMemcpyFromSymbol(t, g_k12_prof, sizeof(t)));
-            const int nb = ((n + 127) / 128) * ((n + 127) / 128);
-            fprintf(stderr, "k12 CTA0: A");
-            for (int u = 0; u < nb && u < 39; ++u) fprintf(stderr, " %lld", t[1 + u] - t[0]);
-            fprintf(stderr, " | B");
-            for (int u = 0; u < nb && u < 39; ++u) fprintf(stderr, " %lld", t[40 + u] - t[0]);
-            fprintf(stderr, " | Bdone %lld end %lld\n", t[79] - t[0], t[80] - t[0]);
-            fprintf(stderr, "k12 CTA0 A wait/load/end:");
-            for (int u = 0; u < nb && u < 16; ++u)
-                fprintf(stderr, " %lld/%lld/%lld", t[96 + u] - t[0], t[112 + u] - t[0], t[1 + u] - t[0]);
-            fprintf(stderr, " | combine");
-            for (int q = 0; q * q < nb && q < 16; ++q) fprintf(stderr, " %lld", t[128 + q] - t[0]);
+            const int nb = ((n + 127) / 128) * ((n + 127) / 128), ntq = (n + 127) / 128;
+            auto rel = [&](long long v) { return v ? v - t[0] : -1; };
+            fprintf(stderr, "k12 CTA0: A end");
+            for (int u = 0; u < 2 * nb && u < 39; ++u) fprintf(stderr, " %lld", rel(t[1 + u]));
+            fprintf(stderr, " | B end");
+            for (int u = 0; u < 2 * nb && u < 39; ++u) fprintf(stderr, " %lld", rel(t[40 + u]));
+            fprintf(stderr, " | Bdone %lld end %lld\n", rel(t[79]), rel(t[80]));
+            fprintf(stderr, "k12 CTA0 A issue/wait/ld0/ld1/end:");
+            for (int u = 0; u < 2 * nb && u < 32; ++u)
+                fprintf(stderr, " %lld/%lld/%lld/%lld/%lld", rel(t[192 + u]), rel(t[96 + u]), rel(t[128 + u]),
+                        rel(t[160 + u]), rel(t[1 + u]));
+            fprintf(stderr, " | lse");
+            for (int q = 0; q < 2 * ntq && q < 32; ++q) fprintf(stderr, " %lld", rel(t[224 + q]));
             fprintf(stderr, "\n");
             // every CTA: SM, start / end (ns from the first start), cycles
             static unsigned long long c[4096][4];
