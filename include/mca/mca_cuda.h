@@ -20,6 +20,8 @@
  *                          on the device
  *   mca_regular_forward   regular_forward
  *   mca_stage_budgets     sample_budgets on given column maxima
+ *   mca_forward_attn      the layer on a given attention matrix: what cmd_bench /
+ *                         cmd_attn_import drive
  *
  * Conventions:
  *   - Plain C: pointers and sizes only, no exceptions cross this boundary.
@@ -140,6 +142,16 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
                           long b_offset, uint32_t layer, const mca_config* cfg, uint64_t seed, void* y,
                           int32_t* budgets_out, uint8_t* exact_out, mca_flops* flops_out, const mca_debug* dbg,
                           mca_stream_t stream);
+
+/* The layer on a GIVEN attention matrix (the cli's imported or synthetic
+ * attention, cmd_bench / cmd_attn_import): budgets from attn's
+ * column maxima (Eq. 9 on the exact fp64 entries), H~ by the forward's encoding
+ * kernels, y = attn . H~ (fp64 accumulation). attn: DEVICE fp64
+ * [B, heads, n, n], row i = query i. cfg->mode == MCA_MODE_REGULAR gives
+ * attn . (x W_V). Desk-scale analysis path (CUDA-core aggregation). */
+mca_status mca_forward_attn(mca_weights* w, const double* attn, const void* x, mca_dtype dt, int B, int n,
+                            long b_offset, uint32_t layer, const mca_config* cfg, uint64_t seed, void* y,
+                            int32_t* budgets_out, uint8_t* exact_out, mca_flops* flops_out, mca_stream_t stream);
 
 /* Exact layer Y = softmax(a Q K^T) (X W_V). */
 mca_status mca_regular_forward(mca_weights* w, const void* q, const void* k, const void* x, mca_dtype dt, int B,

@@ -20,6 +20,7 @@ from .api import (  # noqa: F401
     McaError,
     ShapeError,
     UnsupportedError,
+    forward_given_attention,
     mca_forward,
     multihead_forward,
     regular_forward,

@@ -43,7 +43,7 @@ class McaDebugC(ctypes.Structure):
 # Every symbol declared in include/mca/mca_cuda.h (tests/test_capi.py checks both directions).
 EXPORTS = (
     "mca_prepare_weights", "mca_weights_free", "mca_weights_export", "mca_set_projections", "mca_reserve",
-    "mca_forward", "mca_forward_ex",
+    "mca_forward", "mca_forward_ex", "mca_forward_attn",
     "mca_regular_forward", "mca_stage_budgets", "mca_set_timing", "mca_last_stage_ms", "mca_last_launch_count",
     "mca_last_error", "mca_version",
 )
@@ -82,6 +82,8 @@ def lib() -> ctypes.CDLL:
     L.mca_forward.argtypes = [vp, vp, vp, vp, i32, i32, i32, i64, u32, ctypes.POINTER(McaConfigC), u64, vp, vp, vp,
                               ctypes.POINTER(McaFlopsC), vp]
     L.mca_forward_ex.argtypes = L.mca_forward.argtypes[:-1] + [ctypes.POINTER(McaDebugC), vp]
+    L.mca_forward_attn.argtypes = [vp, vp, vp, i32, i32, i32, i64, u32, ctypes.POINTER(McaConfigC), u64, vp, vp, vp,
+                                   ctypes.POINTER(McaFlopsC), vp]
     L.mca_regular_forward.argtypes = [vp, vp, vp, vp, i32, i32, i32, d, vp, vp]
     L.mca_stage_budgets.argtypes = [vp, i64, i32, i32, ctypes.POINTER(McaConfigC), vp, vp, vp]
     L.mca_set_timing.argtypes = [vp, i32]
@@ -90,7 +92,7 @@ def lib() -> ctypes.CDLL:
     L.mca_last_launch_count.argtypes = [vp]
     L.mca_last_launch_count.restype = i32
     for name in ("mca_prepare_weights", "mca_weights_export", "mca_reserve", "mca_forward", "mca_forward_ex",
-                 "mca_regular_forward", "mca_stage_budgets", "mca_set_timing"):
+                 "mca_forward_attn", "mca_regular_forward", "mca_stage_budgets", "mca_set_timing"):
         getattr(L, name).restype = i32
     _lib = L
     return L

@@ -275,6 +275,43 @@ def mca_forward(weights: AttentionWeights, q: torch.Tensor | None, k: torch.Tens
                            flops=FlopsReport.from_c(fl) if fl is not None else None, debug=debug or {})
 
 
+def forward_given_attention(weights: AttentionWeights, attn: torch.Tensor, x: torch.Tensor,
+                            cfg: McaConfig | None = None, seed: int = 0, *, b_offset: int = 0, layer: int = 0,
+                            y: torch.Tensor | None = None, return_plan: bool = False, flops: bool = False,
+                            stream=None) -> AttentionOutput:
+    """The layer on a given attention matrix (what the reference's cli drives
+    with an imported or synthetic dump): budgets from attn's
+    column maxima, H~ from the forward's encoding kernels, y = attn . H~.
+    attn: float64 CUDA [B, heads, n, n] (row i = query i); x: [B, n, d_in].
+    cfg.mode "approximation", or "regular" (attn . (x W_V))."""
+    cfg = cfg or McaConfig()
+    _need_cuda("attn", attn)
+    _need_cuda("x", x)
+    if x.dtype != weights.dtype:
+        raise ConfigError(f"x.dtype {x.dtype} != weights dtype {weights.dtype}")
+    if x.dim() != 3 or x.shape[2] != weights.d_in:
+        raise ShapeError(f"x must be [B, n, {weights.d_in}], got {tuple(x.shape)}")
+    B, n = int(x.shape[0]), int(x.shape[1])
+    if attn.dtype != torch.float64 or tuple(attn.shape) != (B, weights.heads, n, n) or not attn.is_contiguous():
+        raise ShapeError(f"attn must be contiguous float64 [{B}, {weights.heads}, {n}, {n}], got "
+                         f"{attn.dtype} {tuple(attn.shape)}")
+    if y is None:
+        y = torch.empty((B, n, weights.heads * weights.d_h), dtype=x.dtype, device=x.device)
+    budgets = exact = None
+    if return_plan:
+        budgets = torch.empty((B, weights.heads, n), dtype=torch.int32, device=x.device)
+        exact = torch.empty((B, weights.heads, n), dtype=torch.uint8, device=x.device)
+    fl = L.McaFlopsC() if flops else None
+    c = cfg.to_c()
+    with torch.cuda.device(x.device):
+        _check(L.lib().mca_forward_attn(weights.handle, _ptr(attn), _ptr(x), _dt(x), B, n, int(b_offset), int(layer),
+                                        ctypes.byref(c), ctypes.c_uint64(seed & 0xFFFFFFFFFFFFFFFF), _ptr(y),
+                                        _ptr(budgets), _ptr(exact), ctypes.byref(fl) if fl is not None else None,
+                                        _stream(stream)))
+    return AttentionOutput(y=y, budgets=budgets, exact_mask=exact,
+                           flops=FlopsReport.from_c(fl) if fl is not None else None)
+
+
 def multihead_forward(weights: AttentionWeights, q, k, x, cfg: McaConfig | None = None, seed: int = 0, **kw):
     """every head runs the MCA forward on its slice with its
     own cached distribution and stream namespace; outputs are concatenated on

@@ -33,6 +33,7 @@
 #include "k3t_encode_tc.cu"
 #include "k4_apply_simt.cu"
 #include "k4_apply_tc.cu"
+#include "ka_given_attn.cu"
 
 using namespace mca_dev;
 
@@ -376,6 +377,23 @@ mca_status launch_k3(mca_weights* w, const void* x, int B, int n, long b_offset,
         k3b_encode_exact<T, Acc><<<dim3(Ge, w->heads), 256, 0, stream>>>(a);
         MCA_LAUNCH_CHECK("k3b_encode_exact");
     }
+    return MCA_OK;
+}
+
+// FlopsReport of the last plan from the device counters; synchronises.
+mca_status read_flops(mca_weights* w, int B, int n, bool approx, mca_flops* out, mca_stream_t stream) {
+    unsigned long long c[8];
+    MCA_CUDA_TRY(cudaMemcpyAsync(c, w->counters, sizeof(c), cudaMemcpyDeviceToHost, stream));
+    MCA_CUDA_TRY(cudaStreamSynchronize(stream));
+    const long th = (long)B * n * w->heads;
+    out->exact_encoding = (uint64_t)th * 2ull * w->d_in * w->dh;
+    out->approx_encoding = approx ? c[0] : out->exact_encoding;
+    out->aggregation = (uint64_t)B * w->heads * 2ull * n * n * w->dh;
+    out->samples = c[3];
+    out->exact_tokens = c[2];
+    out->reduction_factor = (double)out->exact_encoding / (double)out->approx_encoding;
+    out->total_reduction = (double)(out->exact_encoding + out->aggregation) /
+                           (double)(out->approx_encoding + out->aggregation);
     return MCA_OK;
 }
 
@@ -823,19 +841,79 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
         MCA_CUDA_TRY(cudaMemcpyAsync(dbg->h_out, w->hbuf, th * w->dh * dtype_size(dt), cudaMemcpyDeviceToDevice,
                                      stream));
     w->last_launches = launches;
-    if (flops_out) {
-        unsigned long long c[8];
-        MCA_CUDA_TRY(cudaMemcpyAsync(c, w->counters, sizeof(c), cudaMemcpyDeviceToHost, stream));
-        MCA_CUDA_TRY(cudaStreamSynchronize(stream));
-        flops_out->exact_encoding = (uint64_t)th * 2ull * w->d_in * w->dh;
-        flops_out->approx_encoding = approx ? c[0] : flops_out->exact_encoding;
-        flops_out->aggregation = (uint64_t)B * H * 2ull * n * n * w->dh;
-        flops_out->samples = c[3];
-        flops_out->exact_tokens = c[2];
-        flops_out->reduction_factor = (double)flops_out->exact_encoding / (double)flops_out->approx_encoding;
-        flops_out->total_reduction = (double)(flops_out->exact_encoding + flops_out->aggregation) /
-                                     (double)(flops_out->approx_encoding + flops_out->aggregation);
+    if (flops_out) return read_flops(w, B, n, approx, flops_out, stream);
+    return MCA_OK;
+}
+
+mca_status mca_forward_attn(mca_weights* w, const double* attn, const void* x, mca_dtype dt, int B, int n,
+                            long b_offset, uint32_t layer, const mca_config* cfg, uint64_t seed, void* y,
+                            int32_t* budgets_out, uint8_t* exact_out, mca_flops* flops_out, mca_stream_t stream) {
+    if (!w) return fail(MCA_ERR_NULL, "weights is NULL");
+    if (mca_status s = check_config(cfg, true)) return s;
+    if (B < 0 || n <= 0) return fail(MCA_ERR_SHAPE, "B = %d, n = %d: need B >= 0, n >= 1", B, n);
+    if (dt != w->wdt) return fail(MCA_ERR_CONFIG, "activation dtype %d != weight dtype %d", (int)dt, (int)w->wdt);
+    if (b_offset < 0) return fail(MCA_ERR_SHAPE, "b_offset < 0");
+    if (n > 65535 || B > 65535)
+        return fail(MCA_ERR_UNSUPPORTED, "B = %d, n = %d: work lists pack (b, j) into 16 bits each", B, n);
+    if (flops_out) std::memset(flops_out, 0, sizeof(*flops_out));
+    if (B == 0) {
+        w->last_launches = 0;
+        return MCA_OK;
     }
+    if (!attn || !x || !y) return fail(MCA_ERR_NULL, "attn / x / y is NULL");
+    const bool approx = cfg->mode == MCA_MODE_APPROX;
+    const long tokens = (long)B * n;
+    if (mca_status s = ensure_workspace(w, tokens, stream)) return s;
+    const int H = w->heads;
+    const long th = tokens * H;
+    int launches = 0;
+    MCA_CUDA_TRY(cudaMemsetAsync(w->zeroed, 0, zeroed_bytes(H, w->d_in), stream));   // counters, cursors, histograms
+    double* cmax = reinterpret_cast<double*>(w->colkey);                             // [B, H, n] scratch
+    const dim3 grid((n + 255) / 256, (unsigned)(B * H));
+    ka_colmax<<<grid, 256, 0, stream>>>(attn, n, cmax);
+    MCA_LAUNCH_CHECK("ka_colmax");
+    K2Args a{};
+    a.cmax_in = cmax;
+    a.count = th;
+    a.row_len = n;
+    a.n = n;
+    a.heads = H;
+    a.d = w->d_in;
+    a.dh = w->dh;
+    a.min_samples = cfg->min_samples;
+    a.alpha = cfg->alpha;
+    a.force_exact = !approx;
+    a.budgets = w->budgets;
+    a.exact = w->exact;
+    a.counters = w->counters;
+    a.hist = w->hist;
+    k2_budgets<kGivenCmax, float><<<grid, 256, 0, stream>>>(a);
+    MCA_LAUNCH_CHECK("k2_budgets");
+    MCA_CUDA_TRY(launch_pdl(k2_scan, dim3(H), dim3(1024), 0, stream, (const unsigned int*)w->hist, w->d_in, w->cursor,
+                            w->counts));
+    MCA_CUDA_TRY(launch_pdl(k2_scatter, grid, dim3(256), 0, stream, (const int32_t*)w->budgets,
+                            (const uint8_t*)w->exact, n, H, w->d_in, tokens, w->cursor, w->samp_list, w->exact_list));
+    MCA_LAUNCH_CHECK("k2_scatter");
+    launches += 4;
+    mca_status s = dt == MCA_F32 ? launch_k3<float, double>(w, x, B, n, b_offset, layer, seed, w->hbuf, nullptr, 0,
+                                                            stream, launches)
+                                 : launch_k3<__nv_bfloat16, float>(w, x, B, n, b_offset, layer, seed, w->hbuf, nullptr,
+                                                                   0, stream, launches);
+    if (s) return s;
+    const dim3 ga(n, H, B);
+    if (dt == MCA_F32)
+        ka_aggregate<float, float><<<ga, kDh, 0, stream>>>(attn, (const float*)w->hbuf, n, H, (float*)y);
+    else
+        ka_aggregate<__nv_bfloat16, __half><<<ga, kDh, 0, stream>>>(attn, (const __half*)w->hbuf, n, H,
+                                                                   (__nv_bfloat16*)y);
+    MCA_LAUNCH_CHECK("ka_aggregate");
+    launches += 1;
+    if (budgets_out)
+        MCA_CUDA_TRY(cudaMemcpyAsync(budgets_out, w->budgets, th * sizeof(int32_t), cudaMemcpyDeviceToDevice, stream));
+    if (exact_out)
+        MCA_CUDA_TRY(cudaMemcpyAsync(exact_out, w->exact, th * sizeof(uint8_t), cudaMemcpyDeviceToDevice, stream));
+    w->last_launches = launches;
+    if (flops_out) return read_flops(w, B, n, approx, flops_out, stream);
     return MCA_OK;
 }
 
