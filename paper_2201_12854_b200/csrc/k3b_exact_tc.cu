@@ -39,12 +39,22 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
+#ifndef MCA_K3B_PROF
+#define MCA_K3B_PROF 0
+#endif
+// Diagnostics (EXTRA=-DMCA_K3B_PROF=1): CTA (0, 0)'s clock64 at entry, after the
+// dependency wait, per chunk landed / MMA issued, epilogue start and end.
+__device__ long long g_k3b_prof[64];
+
 __global__ void __launch_bounds__(k3btc::kThreads, 2) k3b_exact_tc(K3Args a) {
     using namespace k3btc;
     using namespace mca_tc;
     const int h = blockIdx.y;
+    const bool prof = MCA_K3B_PROF && blockIdx.x == 0 && blockIdx.y == 0;
+    if (prof && threadIdx.x == 0) g_k3b_prof[0] = clock64();
     griddep_trigger();
     griddep_wait();      // the exact lists (and K3's H~ writes: both encoders write disjoint rows)
+    if (prof && threadIdx.x == 0) g_k3b_prof[1] = clock64();
     const int ne = a.counts[2 * h + 1];
     if ((int)blockIdx.x * kBM >= ne) return;           // uniform early exit, before any barrier / TMEM use
     extern __shared__ uint8_t smem_raw[];
@@ -82,16 +92,30 @@ __global__ void __launch_bounds__(k3btc::kThreads, 2) k3b_exact_tc(K3Args a) {
             const int idx = tile * kBM + t;
             const int bj = idx < ne ? a.exact_list[(size_t)h * a.tokens + idx] : -1;   // (b << 16) | j
             const size_t tok = bj < 0 ? 0 : (size_t)(bj >> 16) * n + (bj & 0xFFFF);
-            const __nv_bfloat16* xrow = reinterpret_cast<const __nv_bfloat16*>(a.x) + tok * d_in;
             const __nv_bfloat16* wh = reinterpret_cast<const __nv_bfloat16*>(a.wv) + (size_t)h * kDh;
+            // A's gather is warp-cooperative: per chunk, lanes 8k..8k+7 copy one row's
+            // 128 bytes (one coalesced line request) instead of each thread copying its
+            // own row in 16-byte pieces (eight requests per line: the gather was bound
+            // by L2 request throughput). Lane l covers rows 32 warp + 4 j + (l >> 3).
+            const __nv_bfloat16* grow[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int r = 32 * warp + 4 * j + (lane >> 3), gi = tile * kBM + r;
+                const int gbj = gi < ne ? a.exact_list[(size_t)h * a.tokens + gi] : -1;
+                grow[j] = gbj < 0 ? nullptr
+                                  : reinterpret_cast<const __nv_bfloat16*>(a.x) +
+                                        ((size_t)(gbj >> 16) * n + (gbj & 0xFFFF)) * d_in;
+            }
             auto issue = [&](int c, int s) {
                 const uint32_t sa = smem_u32(smem + s * kStageBytes);
                 const uint32_t sb = sa + kABytes;
                 const int k0 = c * kBK;
+                const int q = lane & 7;                // A: this lane's 16-byte piece of 8 rows
 #pragma unroll
-                for (int q = 0; q < 8; ++q) {          // A: 8 x 16 B of row t
-                    const uint32_t dst = sa + sw128_offset(t, q * 16);
-                    if (bj >= 0 && k0 + q * 8 + 8 <= d_in) cp_async16(dst, xrow + k0 + q * 8);
+                for (int j = 0; j < 8; ++j) {
+                    const int r = 32 * warp + 4 * j + (lane >> 3);
+                    const uint32_t dst = sa + sw128_offset(r, q * 16);
+                    if (grow[j] && k0 + q * 8 + 8 <= d_in) cp_async16(dst, grow[j] + k0 + q * 8);
                     else cp_async_zero16(dst, a.wv);
                 }
 #pragma unroll
@@ -125,9 +149,11 @@ __global__ void __launch_bounds__(k3btc::kThreads, 2) k3b_exact_tc(K3Args a) {
                 cp_async_wait<kStages - 1>();          // chunk c has landed (this thread's copies)
                 fence_proxy_async_smem();               // make them visible to the tensor core (async proxy)
                 mbar_arrive(full + (g0 + c) % kStages);
+                if (prof && threadIdx.x == 0 && it == 0 && c < 16) g_k3b_prof[2 + c] = clock64();
             }
             // ---------------- epilogue: TMEM row t -> bf16 -> H~
             mbar_wait(acc_full, it & 1);
+            if (prof && threadIdx.x == 0 && it == 0) g_k3b_prof[40] = clock64();
             tc_fence_after();
             uint32_t v[2][32];
             const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
@@ -156,6 +182,7 @@ __global__ void __launch_bounds__(k3btc::kThreads, 2) k3b_exact_tc(K3Args a) {
             for (int c = 0; c < nchunks; ++c) {
                 const int g = g0 + c, s = g % kStages;
                 mbar_wait(full + s, (g / kStages) & 1);
+                if (prof && it == 0 && c < 16) g_k3b_prof[20 + c] = clock64();
                 tc_fence_after();
                 const uint32_t sa = smem_u32(smem + s * kStageBytes);
                 const uint32_t sb = sa + kABytes;
@@ -173,6 +200,7 @@ __global__ void __launch_bounds__(k3btc::kThreads, 2) k3b_exact_tc(K3Args a) {
     }
     tc_fence_before();
     __syncthreads();
+    if (prof && threadIdx.x == 0) g_k3b_prof[41] = clock64();
     if (warp == 4) tmem_dealloc<64>(tmem);
 }
 

@@ -369,6 +369,16 @@ mca_status launch_k3(mca_weights* w, const void* x, int B, int n, long b_offset,
         MCA_CUDA_TRY(launch_pdl(k3b_exact_tc, dim3((unsigned)Ge, w->heads), dim3(k3btc::kThreads), k3btc::kSmemBytes,
                                 stream, a));
         MCA_LAUNCH_CHECK("k3b_exact_tc");
+        if (MCA_K3B_PROF) {   // diagnostics build: CTA (0, 0)'s timeline
+            long long t[64];
+            MCA_CUDA_TRY(cudaStreamSynchronize(stream));
+            MCA_CUDA_TRY(cudaMemcpyFromSymbol(t, g_k3b_prof, sizeof(t)));
+            fprintf(stderr, "k3b CTA0: waited %lld | landed", t[1] - t[0]);
+            for (int c = 0; c < 12; ++c) fprintf(stderr, " %lld", t[2 + c] - t[0]);
+            fprintf(stderr, " | mma");
+            for (int c = 0; c < 12; ++c) fprintf(stderr, " %lld", t[20 + c] - t[0]);
+            fprintf(stderr, " | acc %lld end %lld\n", t[40] - t[0], t[41] - t[0]);
+        }
     } else {                                  // fp32 parity path: fp64 CUDA-core GEMM
         int Ge = (2 * sm_count() + w->heads - 1) / w->heads;
         const long ecap = (a.tokens + 63) / 64;
