@@ -296,12 +296,34 @@ __device__ __forceinline__ void fma2_bf16_f32(float& acc0, float& acc1, uint32_t
 // its 8 columns with 8 FHFMA straight from the packed bf16 W_h row (no unpack).
 // The coefficient x / (r p) is rounded to bf16 once (relative 2^-9): within
 // the bf16 path's H~ tolerance.
+#ifndef MCA_K3S_PROF
+#define MCA_K3S_PROF 0
+#endif
+#ifndef MCA_K3_STEAL
+#define MCA_K3_STEAL 512
+#endif
+constexpr int kK3StealMin = MCA_K3_STEAL;   // list entries a head must have left to be worth joining
+// Diagnostics (EXTRA=-DMCA_K3S_PROF=1): per CTA the globaltimer at start, after
+// the prologue, at exit, and its head.
+__device__ unsigned long long g_k3s_cta[1024][4];
+
 __global__ void __launch_bounds__(kK3BlockThreads, 1) k3_encode_sampled_bf16(K3Args a) {
     extern __shared__ __align__(16) unsigned char smem[];
-    const int h = blockIdx.y;
+    const int cta = blockIdx.x;
+    auto gt_now = []() {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        return t;
+    };
+    if (MCA_K3S_PROF && threadIdx.x == 0 && cta < 1024) {
+        g_k3s_cta[cta][0] = gt_now();
+        g_k3s_cta[cta][3] = blockIdx.x % a.heads;
+    }
+    int h = blockIdx.x % a.heads;   // 1-D grid: the CTA's first head; it moves on once that list is drained
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int oct = lane >> 3, l8 = lane & 7;
     const int d_in = a.d_in, n = a.n, heads = a.heads;
+    __shared__ int s_next_head;
 
     uint64_t* s_thr = reinterpret_cast<uint64_t*>(smem);
     float* s_invp = reinterpret_cast<float*>(s_thr + d_in);
@@ -313,11 +335,22 @@ __global__ void __launch_bounds__(kK3BlockThreads, 1) k3_encode_sampled_bf16(K3A
 
     const size_t HD = (size_t)heads * kDh;
     const __nv_bfloat16* wv = reinterpret_cast<const __nv_bfloat16*>(a.wv);
-    for (int i = tid; i < d_in; i += kK3BlockThreads) {
-        s_thr[i] = a.thr[(size_t)h * d_in + i];
-        s_invp[i] = a.invp[(size_t)h * d_in + i];
+    unsigned long long my_samples = 0;
+    for (;;) {   // ---------------- per head: stage its tables and W_h, then drain its list
+    if (d_in % 4 == 0) {   // 16-byte copies of the sampler tables (the prologue is latency bound)
+        const uint4* gt = reinterpret_cast<const uint4*>(a.thr + (size_t)h * d_in);
+        for (int i = tid; i < d_in / 2; i += kK3BlockThreads) reinterpret_cast<uint4*>(s_thr)[i] = gt[i];
+        const uint4* gi = reinterpret_cast<const uint4*>(a.invp + (size_t)h * d_in);
+        for (int i = tid; i < d_in / 4; i += kK3BlockThreads) reinterpret_cast<uint4*>(s_invp)[i] = gi[i];
+        const uint4* gg = reinterpret_cast<const uint4*>(a.guide + (size_t)h * kGuide);
+        for (int i = tid; i < kGuide / 8; i += kK3BlockThreads) reinterpret_cast<uint4*>(s_guide)[i] = gg[i];
+    } else {
+        for (int i = tid; i < d_in; i += kK3BlockThreads) {
+            s_thr[i] = a.thr[(size_t)h * d_in + i];
+            s_invp[i] = a.invp[(size_t)h * d_in + i];
+        }
+        for (int g = tid; g < kGuide; g += kK3BlockThreads) s_guide[g] = a.guide[(size_t)h * kGuide + g];
     }
-    for (int g = tid; g < kGuide; g += kK3BlockThreads) s_guide[g] = a.guide[(size_t)h * kGuide + g];
     for (int e = tid; e < d_in * (kDh / 8); e += kK3BlockThreads) {   // W_h -> smem, 16-byte pieces
         const int i = e / (kDh / 8), c8 = (e % (kDh / 8)) * 8;
         *reinterpret_cast<uint4*>(s_w + (size_t)i * kDh + c8) =
@@ -325,13 +358,13 @@ __global__ void __launch_bounds__(kK3BlockThreads, 1) k3_encode_sampled_bf16(K3A
     }
     __syncthreads();
     griddep_wait();      // W_h and the tables above are weights; the work lists come from the scatter
+    if (MCA_K3S_PROF && threadIdx.x == 0 && cta < 1024) g_k3s_cta[cta][1] = gt_now();
     const int col0 = 8 * l8;
     const int nsamp = a.counts[2 * h];
     const int32_t* list = a.samp_list + (size_t)h * a.tokens;
     const __nv_bfloat16* x = reinterpret_cast<const __nv_bfloat16*>(a.x);
     __half* hout = reinterpret_cast<__half*>(a.h_out);
     const uint32_t wbase = static_cast<uint32_t>(__cvta_generic_to_shared(s_w)) + col0 * 2;
-    unsigned long long my_samples = 0;
 
     // Every lane of the warp calls process_token (r = 0: no token for this octet) and
     // the warp runs the warp-wide maximum number of rounds, octets past their own
@@ -438,9 +471,31 @@ __global__ void __launch_bounds__(kK3BlockThreads, 1) k3_encode_sampled_bf16(K3A
         process_token(bja, ra);                    // all lanes: lockstep rounds (r = 0: idle octet)
         process_token(bjb, rb);
     }
+    // Head drained: help the head with the most work left, if it is worth
+    // restaging tables and W_h (~4 us); heads differ by ~10% in total draws.
+    __syncthreads();                               // every warp is past this head's tasks
+    if (tid == 0) {
+        int best = -1, best_left = kK3StealMin;
+        for (int hh = 0; hh < heads; ++hh) {
+            const int left = a.counts[2 * hh] - *reinterpret_cast<volatile const int*>(a.task_cursor + hh);
+            if (left > best_left) {
+                best_left = left;
+                best = hh;
+            }
+        }
+        s_next_head = best;
+    }
+    __syncthreads();
+    if (s_next_head < 0) break;
+    h = s_next_head;
+    }
     if (a.sample_counter) {
         for (int off = 16; off; off >>= 1) my_samples += __shfl_xor_sync(0xffffffffu, my_samples, off);
         if (lane == 0 && my_samples) atomicAdd(a.sample_counter, my_samples);
+    }
+    if (MCA_K3S_PROF) {
+        __syncthreads();
+        if (threadIdx.x == 0 && cta < 1024) g_k3s_cta[cta][2] = gt_now();
     }
 }
 

@@ -350,9 +350,32 @@ mca_status launch_k3(mca_weights* w, const void* x, int B, int n, long b_offset,
     const long cap = (a.tokens + 63) / 64;   // at most one CTA per 64 tokens of a head
     if (G > cap) G = (int)cap;
     if (G < 1) G = 1;
-    if (kern == k3_encode_sampled_bf16) MCA_CUDA_TRY(launch_pdl(kern, dim3(G, w->heads), dim3(kK3BlockThreads), smem, stream, a));
+    // bf16: a 1-D grid filling every SM (CTA c starts on head c % heads and
+    // then joins whichever head has the most work left)
+    const int G1 = (int)std::min<long>((long)sm_count() * occ, (long)std::max(G, 1) * w->heads + (long)w->heads);
+    if (kern == k3_encode_sampled_bf16) MCA_CUDA_TRY(launch_pdl(kern, dim3(G1), dim3(kK3BlockThreads), smem, stream, a));
     else kern<<<dim3(G, w->heads), kK3BlockThreads, smem, stream>>>(a);
     MCA_LAUNCH_CHECK("k3_encode_sampled");
+    if (MCA_K3S_PROF && kern == k3_encode_sampled_bf16) {   // diagnostics build: per-head CTA spread
+        static unsigned long long c[1024][4];
+        const int nc = std::min(G1, 1024);
+        MCA_CUDA_TRY(cudaStreamSynchronize(stream));
+        MCA_CUDA_TRY(cudaMemcpyFromSymbol(c, g_k3s_cta, sizeof(unsigned long long) * 4 * nc));
+        unsigned long long t0 = ~0ull;
+        for (int i = 0; i < nc; ++i) t0 = std::min(t0, c[i][0]);
+        fprintf(stderr, "k3s heads (prologue end, first exit, last exit in us):");
+        for (int hh = 0; hh < w->heads; ++hh) {
+            unsigned long long pe = 0, e0 = ~0ull, e1 = 0;
+            for (int i = 0; i < nc; ++i)
+                if ((int)c[i][3] == hh) {
+                    pe = std::max(pe, c[i][1] - t0);
+                    e0 = std::min(e0, c[i][2] - t0);
+                    e1 = std::max(e1, c[i][2] - t0);
+                }
+            fprintf(stderr, " | h%d %.1f %.1f %.1f", hh, pe / 1e3, e0 / 1e3, e1 / 1e3);
+        }
+        fprintf(stderr, "\n");
+    }
     }
     if (sizeof(T) == 2 && !force_simt()) {   // bf16: exact token-heads on the tensor cores
         static bool attr = false;
