@@ -456,12 +456,16 @@ __global__ void __launch_bounds__(kK3BlockThreads, 1) k3_encode_sampled_bf16(K3A
         for (int ln = l8; ln < lines; ln += 8)
             asm volatile("prefetch.global.L1 [%0];" ::"l"(reinterpret_cast<const char*>(xrow) + ln * 128));
     };
+    // Tasks of 8 list entries (two tokens per octet); a short list (few tokens
+    // per warp that may serve this head) takes 4 per task instead, so the most
+    // expensive tokens (the list is budget-descending) run on separate warps.
+    const int tsz = nsamp < 2 * 8 * kK3Warps * ((int)gridDim.x / heads + 1) ? 4 : 8;
     for (;;) {
         int t0 = 0;
-        if (lane == 0) t0 = atomicAdd(a.task_cursor + h, 8);
+        if (lane == 0) t0 = atomicAdd(a.task_cursor + h, tsz);
         t0 = __shfl_sync(0xffffffffu, t0, 0);
         if (t0 >= nsamp) break;
-        const int ea = t0 + oct, eb = t0 + 4 + oct;
+        const int ea = t0 + oct, eb = tsz == 8 ? t0 + 4 + oct : nsamp;
         const int bja = ea < nsamp ? list[ea] : -1;
         const int bjb = eb < nsamp ? list[eb] : -1;
         const int ra = bja >= 0 ? a.budgets[((size_t)(bja >> 16) * heads + h) * n + (bja & 0xFFFF)] : 0;
@@ -469,7 +473,7 @@ __global__ void __launch_bounds__(kK3BlockThreads, 1) k3_encode_sampled_bf16(K3A
         if (bja >= 0) prefetch_row(bja);
         if (bjb >= 0) prefetch_row(bjb);
         process_token(bja, ra);                    // all lanes: lockstep rounds (r = 0: idle octet)
-        process_token(bjb, rb);
+        if (tsz == 8) process_token(bjb, rb);
     }
     // Head drained: help the head with the most work left, if it is worth
     // restaging tables and W_h (~4 us); heads differ by ~10% in total draws.
