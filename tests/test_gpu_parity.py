@@ -471,3 +471,31 @@ def test_fused_score_budget_kernel_lengths(mca, syn, orc, n):
     ref = _oracle(orc, w, q, k, x, H, alpha=0.4, seed=7, budgets_override=b, exact_override=e)
     assert _row_rel(_np(out.y), ref.y) <= TOL_Y[torch.bfloat16]
     np.testing.assert_allclose(dbg["lse_out"].cpu().numpy(), ref.lse, rtol=2e-3, atol=2e-3)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [77, 200, 640, 768])
+def test_fused_kernel_multi_item_per_cta(mca, syn, orc, n):
+    """More (b, h) items than SMs: the persistent fused kernel's CTAs run 2
+    items back to back, carrying block counters, S-buffer parities, the K-tile
+    refills and the double-buffered row statistics across items (odd block
+    counts included: n = 640 gives 25 blocks per item). Eq. 9 bitwise on the
+    device's cmax, cmax vs the fp64 oracle, y for two sequences."""
+    H, d_in = 12, 768
+    B = 13                                                   # 156 items > 148 SMs
+    weights, w, q, k, x = _setup(mca, syn, B, n, d_in, H, torch.bfloat16, seed=n + 1)
+    cm = torch.zeros((B, H, n), dtype=torch.float64, device="cuda")
+    out = mca.mca_forward(weights, q, k, x, mca.McaConfig(alpha=0.4), seed=5, return_plan=True,
+                          debug=dict(cmax_out=cm))
+    b = out.budgets.cpu().numpy()
+    e = out.exact_mask.cpu().numpy().astype(bool)
+    rb, re = orc.sample_budgets_from_cmax(cm.cpu().numpy(), n, 0.4, 1, d_in)
+    assert np.array_equal(b, rb) and np.array_equal(e, re)
+    for s in (0, B - 1):                                     # first and last items of the run
+        sl = slice(s, s + 1)
+        ref = orc.batched_forward(_np(q[sl]), _np(k[sl]), _np(x[sl]), _np(w), heads=H, alpha=0.4, seed=5,
+                                  b_offset=s, budgets_override=b[sl], exact_override=e[sl])
+        ref0 = orc.batched_forward(_np(q[sl]), _np(k[sl]), _np(x[sl]), _np(w), heads=H, alpha=0.4, seed=5,
+                                   b_offset=s)
+        assert np.abs(cm[sl].cpu().numpy() / ref0.cmax - 1.0).max() <= 1e-4
+        assert _row_rel(_np(out.y[sl]), ref.y) <= TOL_Y[torch.bfloat16]
