@@ -12,10 +12,15 @@
 //   thr[i]   = ceil(cdf[i] * 2^53)   (u64; exact: power-of-two scaling)
 //   invp[i]  = (float)(1 / p[i])     (0 where p = 0; never drawn)
 //   guide[g] = first i with thr[i] > g * 2^39, | 0x8000 when thr[i] >= (g + 1) * 2^39
+//   (one row covers the bucket), else | 0x4000 when thr[i + 1] >= (g + 1) * 2^39 (one boundary)
 //              (the whole bucket draws row i: no compare needed)
 // One-time cost; it runs once per weight matrix ("embedded in the model or
 // cached").
 #include "mca_common.cuh"
+
+#ifndef MCA_GUIDE_ONE
+#define MCA_GUIDE_ONE 1
+#endif
 
 namespace mca_dev {
 
@@ -89,7 +94,8 @@ __global__ void k0_dist(const double* __restrict__ sq, int d_in, double* __restr
             if (t[mid] > key) hi = mid; else lo = mid + 1;
         }
         const uint64_t upper = (uint64_t)(g + 1) << (53 - kGuideBits);   // bucket = [key, upper)
-        guide[(size_t)h * kGuide + g] = (uint16_t)(lo | (t[lo] >= upper ? kGuideClean : 0u));
+        const uint16_t flag = t[lo] >= upper ? kGuideClean : (MCA_GUIDE_ONE && t[lo + 1] >= upper ? kGuideOne : 0u);
+        guide[(size_t)h * kGuide + g] = (uint16_t)(lo | flag);
     }
 }
 

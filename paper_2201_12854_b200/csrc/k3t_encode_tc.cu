@@ -235,7 +235,7 @@ __global__ void __launch_bounds__(k3t::kThreads, 1)
     } else {
         for (int i = tid; i < d_in; i += kWorkerThreads) s_thr[i] = a.thr[(size_t)h * d_in + i];
         for (int g = tid; g < kGuideT; g += kWorkerThreads)   // coarse entries, clean bits masked off
-            s_guide[g] = a.guide[(size_t)h * kGuide + ((size_t)g << (kGuideBits - kGuideBitsT))] & 0x7FFFu;
+            s_guide[g] = a.guide[(size_t)h * kGuide + ((size_t)g << (kGuideBits - kGuideBitsT))] & kGuideRow;
         for (int i = tid; i < (int)L.dpad; i += kWorkerThreads)
             s_pbf[i] = i < d_in ? pbf_g[(size_t)h * d_in + i] : __float2bfloat16(0.f);
         if (warp == 0 && my_tiles > 0) {

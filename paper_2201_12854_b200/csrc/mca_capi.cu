@@ -444,7 +444,7 @@ mca_status mca_prepare_weights(const void* w_v, mca_dtype wdt, int d_in, int hea
     if (wdt != MCA_F32 && wdt != MCA_BF16) return fail(MCA_ERR_CONFIG, "unknown dtype %d", (int)wdt);
     if (d_in <= 0 || heads <= 0 || d_h <= 0) return fail(MCA_ERR_SHAPE, "d_in, heads, d_h must be positive");
     if (d_h != kDh) return fail(MCA_ERR_UNSUPPORTED, "d_h = %d: the sm_100a kernels implement d_h = 64", d_h);
-    if (d_in > 32767) return fail(MCA_ERR_UNSUPPORTED, "d_in = %d exceeds the guide table's 15-bit rows", d_in);
+    if (d_in > 16384) return fail(MCA_ERR_UNSUPPORTED, "d_in = %d exceeds the guide table's 14-bit rows", d_in);
     int dev_count = 0;
     if (cudaGetDeviceCount(&dev_count) != cudaSuccess || dev_count == 0) {
         cudaGetLastError();

@@ -18,7 +18,9 @@ constexpr int kGuide = 1 << kGuideBits;
 // Guide entry: bits 0-14 the first row whose threshold exceeds the bucket's
 // lower end; bit 15 set when the whole bucket maps to that row ("clean":
 // thr[row] >= the bucket's upper end), so the draw needs no threshold compare.
-constexpr uint16_t kGuideClean = 0x8000u;
+constexpr uint16_t kGuideClean = 0x8000u;   // the bucket lies inside one row: the entry is the answer
+constexpr uint16_t kGuideOne = 0x4000u;     // the bucket holds exactly one row boundary: entry or entry + 1
+constexpr uint16_t kGuideRow = 0x3FFFu;     // row bits (d_in <= 16384)
 
 // ----------------------------------------------- programmatic dependent launch
 // Kernels of the forward are launched with programmatic stream serialization
@@ -74,20 +76,26 @@ template <int kBits = kGuideBits>
 __device__ __forceinline__ int sample_index(const uint64_t* __restrict__ thr, const uint16_t* __restrict__ guide,
                                             uint64_t m) {
     const uint32_t e = guide[(uint32_t)(m >> (53 - kBits))];
-    int i = (int)(e & 0x7FFFu);
+    int i = (int)(e & kGuideRow);
     if (e & kGuideClean) return i;
     while (thr[i] <= m) ++i;
     return i;
 }
-// Two draws resolved by one scan loop (one divergent loop instead of two).
+// Two draws resolved together. Clean buckets need no compare; a bucket with
+// exactly one boundary needs one (branch-free); only buckets with several
+// boundaries (rows of tiny p) fall into the scan loop.
 template <int kBits = kGuideBits>
 __device__ __forceinline__ void sample_index2(const uint64_t* __restrict__ thr, const uint16_t* __restrict__ guide,
                                               uint64_t m0, uint64_t m1, int& i0, int& i1) {
     const uint32_t e0 = guide[(uint32_t)(m0 >> (53 - kBits))], e1 = guide[(uint32_t)(m1 >> (53 - kBits))];
-    i0 = (int)(e0 & 0x7FFFu);
-    i1 = (int)(e1 & 0x7FFFu);
+    i0 = (int)(e0 & kGuideRow);
+    i1 = (int)(e1 & kGuideRow);
     if (e0 & e1 & kGuideClean) return;   // both buckets clean: no threshold compare
-    bool a0 = !(e0 & kGuideClean) && thr[i0] <= m0, a1 = !(e1 & kGuideClean) && thr[i1] <= m1;
+    if (!(e0 & kGuideClean)) i0 += thr[i0] <= m0;
+    if (!(e1 & kGuideClean)) i1 += thr[i1] <= m1;
+    if ((e0 & (kGuideClean | kGuideOne)) && (e1 & (kGuideClean | kGuideOne))) return;   // resolved
+    bool a0 = !(e0 & (kGuideClean | kGuideOne)) && thr[i0] <= m0;   // several boundaries: keep scanning
+    bool a1 = !(e1 & (kGuideClean | kGuideOne)) && thr[i1] <= m1;
     while (a0 || a1) {
         if (a0) a0 = thr[++i0] <= m0;
         if (a1) a1 = thr[++i1] <= m1;
