@@ -307,6 +307,10 @@ constexpr int kK3StealMin = MCA_K3_STEAL;   // list entries a head must have lef
 // the prologue, at exit, and its head.
 __device__ unsigned long long g_k3s_cta[1024][4];
 
+// kDin > 0: d_in fixed at compile time (BERT-base 768, -large 1024), so every
+// shared-memory table address is an immediate and the 64-register hot loop
+// does not spend instructions rematerialising them; kDin = 0: any d_in.
+template <int kDin>
 __global__ void __launch_bounds__(kK3BlockThreads, 1) k3_encode_sampled_bf16(K3Args a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int cta = blockIdx.x;
@@ -322,7 +326,7 @@ __global__ void __launch_bounds__(kK3BlockThreads, 1) k3_encode_sampled_bf16(K3A
     int h = blockIdx.x % a.heads;   // 1-D grid: the CTA's first head; it moves on once that list is drained
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int oct = lane >> 3, l8 = lane & 7;
-    const int d_in = a.d_in, n = a.n, heads = a.heads;
+    const int d_in = kDin > 0 ? kDin : a.d_in, n = a.n, heads = a.heads;
     __shared__ int s_next_head;
 
     uint64_t* s_thr = reinterpret_cast<uint64_t*>(smem);

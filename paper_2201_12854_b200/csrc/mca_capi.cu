@@ -35,6 +35,10 @@
 #include "k4_apply_tc.cu"
 #include "ka_given_attn.cu"
 
+#ifndef MCA_K3_SPECIALIZE
+#define MCA_K3_SPECIALIZE 1   // d_in = 768 / 1024 encoders with compile-time table offsets
+#endif
+
 using namespace mca_dev;
 
 namespace {
@@ -333,7 +337,10 @@ mca_status launch_k3(mca_weights* w, const void* x, int B, int n, long b_offset,
     constexpr size_t kMaxSmem = 220 * 1024;
     if (sizeof(T) == 2 && k3_bf16_smem_bytes(w->d_in) <= kMaxSmem) {
         smem = k3_bf16_smem_bytes(w->d_in);
-        kern = k3_encode_sampled_bf16;
+        kern = !MCA_K3_SPECIALIZE ? k3_encode_sampled_bf16<0>
+               : w->d_in == 768 ? k3_encode_sampled_bf16<768>
+               : w->d_in == 1024 ? k3_encode_sampled_bf16<1024>
+                                 : k3_encode_sampled_bf16<0>;
     } else if (smem <= kMaxSmem) {
         if constexpr (sizeof(T) == 2) kern = k3_encode_sampled<__nv_bfloat16, __nv_bfloat16, float, true>;
         else kern = k3_encode_sampled<float, float, double, true>;
@@ -353,10 +360,12 @@ mca_status launch_k3(mca_weights* w, const void* x, int B, int n, long b_offset,
     // bf16: a 1-D grid filling every SM (CTA c starts on head c % heads and
     // then joins whichever head has the most work left)
     const int G1 = (int)std::min<long>((long)sm_count() * occ, (long)std::max(G, 1) * w->heads + (long)w->heads);
-    if (kern == k3_encode_sampled_bf16) MCA_CUDA_TRY(launch_pdl(kern, dim3(G1), dim3(kK3BlockThreads), smem, stream, a));
+    const bool bf16_kern = kern == k3_encode_sampled_bf16<768> || kern == k3_encode_sampled_bf16<1024> ||
+                           kern == k3_encode_sampled_bf16<0>;
+    if (bf16_kern) MCA_CUDA_TRY(launch_pdl(kern, dim3(G1), dim3(kK3BlockThreads), smem, stream, a));
     else kern<<<dim3(G, w->heads), kK3BlockThreads, smem, stream>>>(a);
     MCA_LAUNCH_CHECK("k3_encode_sampled");
-    if (MCA_K3S_PROF && kern == k3_encode_sampled_bf16) {   // diagnostics build: per-head CTA spread
+    if (MCA_K3S_PROF && bf16_kern) {   // diagnostics build: per-head CTA spread
         static unsigned long long c[1024][4];
         const int nc = std::min(G1, 1024);
         MCA_CUDA_TRY(cudaStreamSynchronize(stream));
