@@ -35,6 +35,9 @@
 #include "k4_apply_tc.cu"
 #include "ka_given_attn.cu"
 
+#ifndef MCA_K2_FUSED_SCAN
+#define MCA_K2_FUSED_SCAN 1   // work lists by one scan + scatter kernel
+#endif
 #ifndef MCA_K3_SPECIALIZE
 #define MCA_K3_SPECIALIZE 1   // d_in = 768 / 1024 encoders with compile-time table offsets
 #endif
@@ -161,7 +164,8 @@ struct mca_weights {
     void* hbuf = nullptr;                     // [B, n, H*dh]
     int32_t* samp_list = nullptr;             // [H, B*n] sampled tokens per head, budget-descending
     int32_t* exact_list = nullptr;            // [H, B*n] exact tokens per head
-    void* zeroed = nullptr;                   // counters | task_cursor | hist (zeroed once per forward)
+    void* zeroed = nullptr;                   // counters | task_cursor | hist | fill (zeroed once per forward)
+    unsigned int* fill = nullptr;             // [H, d + 1] per-bin list fill counters (k2_scan_scatter)
     unsigned long long* counters = nullptr;   // [8]
     unsigned int* hist = nullptr;             // [H, d_in + 1] budget histogram
     unsigned int* cursor = nullptr;           // [H, d_in + 1] scatter cursors
@@ -253,7 +257,8 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
     return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
-size_t zeroed_bytes(int heads, int d_in) { return 64 + (((size_t)heads * 4 + 63) & ~(size_t)63) + (size_t)heads * (d_in + 1) * 4; }
+// counters (64 B) | task cursors | budget histograms [H, d + 1] | list fill counters [H, d + 1]
+size_t zeroed_bytes(int heads, int d_in) { return 64 + (((size_t)heads * 4 + 63) & ~(size_t)63) + 2 * (size_t)heads * (d_in + 1) * 4; }
 
 bool use_k3t(const mca_weights* w) {
     return w->wdt == MCA_BF16 && w->wprime && !force_simt() && tile_k3_requested() && w->d_in % 8 == 0 &&
@@ -422,6 +427,27 @@ mca_status launch_k3(mca_weights* w, const void* x, int B, int n, long b_offset,
     return MCA_OK;
 }
 
+// Budget-sorted work lists from the histograms: one scan + scatter kernel
+// (k2_scan_scatter), or the two-kernel form (MCA_K2_FUSED_SCAN=0).
+mca_status launch_lists(mca_weights* w, dim3 grid, int n, long tokens, mca_stream_t stream, int& launches) {
+    const int H = w->heads;
+    if (MCA_K2_FUSED_SCAN) {
+        MCA_CUDA_TRY(launch_pdl(k2_scan_scatter, grid, dim3(256), 2 * (size_t)(w->d_in + 1) * 4, stream,
+                                (const int32_t*)w->budgets, (const uint8_t*)w->exact, (const unsigned int*)w->hist, n,
+                                H, w->d_in, tokens, w->fill, w->counts, w->samp_list, w->exact_list));
+        MCA_LAUNCH_CHECK("k2_scan_scatter");
+    } else {
+        MCA_CUDA_TRY(launch_pdl(k2_scan, dim3(H), dim3(1024), 0, stream, (const unsigned int*)w->hist, w->d_in,
+                                w->cursor, w->counts));
+        MCA_LAUNCH_CHECK("k2_scan");
+        MCA_CUDA_TRY(launch_pdl(k2_scatter, grid, dim3(256), 0, stream, (const int32_t*)w->budgets,
+                                (const uint8_t*)w->exact, n, H, w->d_in, tokens, w->cursor, w->samp_list,
+                                w->exact_list));
+        MCA_LAUNCH_CHECK("k2_scatter");
+    }
+    return MCA_OK;
+}
+
 // FlopsReport of the last plan from the device counters; synchronises.
 mca_status read_flops(mca_weights* w, int B, int n, bool approx, mca_flops* out, mca_stream_t stream) {
     unsigned long long c[8];
@@ -490,6 +516,7 @@ mca_status mca_prepare_weights(const void* w_v, mca_dtype wdt, int d_in, int hea
     w->counters = static_cast<unsigned long long*>(w->zeroed);
     w->task_cursor = reinterpret_cast<int*>(static_cast<char*>(w->zeroed) + 64);
     w->hist = reinterpret_cast<unsigned int*>(static_cast<char*>(w->zeroed) + 64 + ((heads * 4 + 63) & ~63));
+    w->fill = w->hist + (size_t)heads * (d_in + 1);
     if (cudaMemcpyAsync(w->w, w_v, wbytes, cudaMemcpyDeviceToDevice, stream) != cudaSuccess)
         return cleanup(fail(MCA_ERR_CUDA, "copying w_v failed: %s", cudaGetErrorString(cudaGetLastError())));
     const dim3 g0((d_in + 255) / 256, heads);
@@ -807,13 +834,7 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
             MCA_LAUNCH_CHECK("k2_budgets");
         }
         if (!tile_k3) {
-            MCA_CUDA_TRY(launch_pdl(k2_scan, dim3(H), dim3(1024), 0, stream, (const unsigned int*)w->hist, w->d_in,
-                                    w->cursor, w->counts));
-            MCA_LAUNCH_CHECK("k2_scan");
-            MCA_CUDA_TRY(launch_pdl(k2_scatter, grid, dim3(256), 0, stream, (const int32_t*)w->budgets,
-                                    (const uint8_t*)w->exact, n, H, w->d_in, tokens, w->cursor, w->samp_list,
-                                    w->exact_list));
-            MCA_LAUNCH_CHECK("k2_scatter");
+            if (mca_status s = launch_lists(w, grid, n, tokens, stream, launches)) return s;
         }
     }
     if (w->timing) MCA_CUDA_TRY(cudaEventRecord(w->ev[2], stream));
@@ -931,12 +952,7 @@ mca_status mca_forward_attn(mca_weights* w, const double* attn, const void* x, m
     a.hist = w->hist;
     k2_budgets<kGivenCmax, float><<<grid, 256, 0, stream>>>(a);
     MCA_LAUNCH_CHECK("k2_budgets");
-    MCA_CUDA_TRY(launch_pdl(k2_scan, dim3(H), dim3(1024), 0, stream, (const unsigned int*)w->hist, w->d_in, w->cursor,
-                            w->counts));
-    MCA_CUDA_TRY(launch_pdl(k2_scatter, grid, dim3(256), 0, stream, (const int32_t*)w->budgets,
-                            (const uint8_t*)w->exact, n, H, w->d_in, tokens, w->cursor, w->samp_list, w->exact_list));
-    MCA_LAUNCH_CHECK("k2_scatter");
-    launches += 4;
+    if (mca_status s = launch_lists(w, grid, n, tokens, stream, launches)) return s;
     mca_status s = dt == MCA_F32 ? launch_k3<float, double>(w, x, B, n, b_offset, layer, seed, w->hbuf, nullptr, 0,
                                                             stream, launches)
                                  : launch_k3<__nv_bfloat16, float>(w, x, B, n, b_offset, layer, seed, w->hbuf, nullptr,
@@ -949,7 +965,6 @@ mca_status mca_forward_attn(mca_weights* w, const double* attn, const void* x, m
         ka_aggregate<__nv_bfloat16, __half><<<ga, kDh, 0, stream>>>(attn, (const __half*)w->hbuf, n, H,
                                                                    (__nv_bfloat16*)y);
     MCA_LAUNCH_CHECK("ka_aggregate");
-    launches += 1;
     if (budgets_out)
         MCA_CUDA_TRY(cudaMemcpyAsync(budgets_out, w->budgets, th * sizeof(int32_t), cudaMemcpyDeviceToDevice, stream));
     if (exact_out)
