@@ -233,29 +233,31 @@ __global__ void __launch_bounds__(256) k2_scatter(const int32_t* __restrict__ bu
     (ex ? exact_list : samp_list)[(size_t)h * tokens + pos] = tok;
 }
 
-// Scan and scatter in one kernel: every CTA recomputes its head's bin bases
+// Scan and scatter in one kernel: every CTA (2048 tokens of one head) recomputes its head's bin bases
 // from the (complete) histogram in shared memory (a 1 K-bin exclusive scan is
 // cheaper than a separate kernel and its dependency hop), then places its
 // tokens at base[bin] + a bump of the zero-initialised fill counter.
 // Same lists as k2_scan + k2_scatter: bins in descending budget order.
-__global__ void __launch_bounds__(256) k2_scan_scatter(const int32_t* __restrict__ budgets,
-                                                       const uint8_t* __restrict__ exact,
-                                                       const unsigned int* __restrict__ hist, int n, int heads, int d,
-                                                       long tokens, unsigned int* __restrict__ fill,
-                                                       int* __restrict__ counts, int32_t* __restrict__ samp_list,
-                                                       int32_t* __restrict__ exact_list) {
+constexpr int kScatterThreads = 1024, kScatterPerThread = 2;   // 2048 tokens of one head per CTA
+__global__ void __launch_bounds__(kScatterThreads) k2_scan_scatter(const int32_t* __restrict__ budgets,
+                                                                   const uint8_t* __restrict__ exact,
+                                                                   const unsigned int* __restrict__ hist, int n,
+                                                                   int heads, int d, long tokens,
+                                                                   unsigned int* __restrict__ fill,
+                                                                   int* __restrict__ counts,
+                                                                   int32_t* __restrict__ samp_list,
+                                                                   int32_t* __restrict__ exact_list) {
     extern __shared__ unsigned int s_base[];   // [d + 1] bin bases, then [d + 1] this CTA's per-bin counts / offsets
     unsigned int* s_cnt = s_base + (d + 1);
-    __shared__ unsigned int s_warp[8];
-    const long bh = blockIdx.y;
-    const int b = (int)(bh / heads), h = (int)(bh - (long)b * heads);
+    __shared__ unsigned int s_warp[kScatterThreads / 32];
+    const int h = blockIdx.y;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     griddep_trigger();
+    for (int i = tid; i <= d; i += kScatterThreads) s_cnt[i] = 0;
     griddep_wait();      // the histograms of the budget pass
-    for (int i = tid; i <= d; i += 256) s_cnt[i] = 0;
     const unsigned int* hh = hist + (size_t)h * (d + 1);
     // thread tid owns descending positions [tid * per, +per): bins r = d - 1 - position
-    const int nb = d - 1, per = (nb + 255) / 256;
+    const int nb = d - 1, per = (nb + kScatterThreads - 1) / kScatterThreads;
     unsigned int loc = 0;
     for (int k = 0; k < per; ++k) {
         const int idx = tid * per + k;
@@ -281,32 +283,39 @@ __global__ void __launch_bounds__(256) k2_scan_scatter(const int32_t* __restrict
         }
     }
     if (tid == 0) s_base[d] = 0;
-    if (blockIdx.x == 0 && b == 0 && tid == 255) {
+    if (blockIdx.x == 0 && tid == kScatterThreads - 1) {
         counts[2 * h + 0] = (int)run;           // the last thread's running total: all sampled tokens
         counts[2 * h + 1] = (int)hh[d];
     }
-    __syncthreads();
-    // this CTA's tokens: rank within their bin in shared memory, then one global
-    // reservation per non-empty bin (hot bins see one atomic per CTA, not per warp)
-    const int j = blockIdx.x * blockDim.x + tid;
-    const long t = bh * n + j;
-    bool ex = false;
-    int bin = -1;
-    unsigned int rank = 0;
-    if (j < n) {
-        ex = exact[t] != 0;
-        bin = ex ? d : min(budgets[t], d - 1);
-        rank = atomicAdd(&s_cnt[bin], 1u);
+    // this CTA's tokens (positions g of the head's B*n, sequence-major): rank within
+    // their bin in shared memory, then one global reservation per non-empty bin
+    int bin[kScatterPerThread];
+    unsigned int rank[kScatterPerThread];
+#pragma unroll
+    for (int u = 0; u < kScatterPerThread; ++u) {
+        const long g = ((long)blockIdx.x * kScatterPerThread + u) * kScatterThreads + tid;
+        bin[u] = -1;
+        if (g < tokens) {
+            const long b = g / n, j = g - b * n;
+            const long t = (b * heads + h) * n + j;
+            bin[u] = exact[t] ? d : min(budgets[t], d - 1);
+            rank[u] = atomicAdd(&s_cnt[bin[u]], 1u);
+        }
     }
     __syncthreads();
-    for (int i = tid; i <= d; i += 256) {
+    for (int i = tid; i <= d; i += kScatterThreads) {
         const unsigned int c = s_cnt[i];
         if (c) s_cnt[i] = atomicAdd(&fill[(size_t)h * (d + 1) + i], c);
     }
     __syncthreads();
-    if (j >= n) return;
-    const unsigned int pos = s_base[bin] + s_cnt[bin] + rank;
-    (ex ? exact_list : samp_list)[(size_t)h * tokens + pos] = (b << 16) | j;   // (n, B <= 65535, host-checked)
+#pragma unroll
+    for (int u = 0; u < kScatterPerThread; ++u) {
+        if (bin[u] < 0) continue;
+        const long g = ((long)blockIdx.x * kScatterPerThread + u) * kScatterThreads + tid;
+        const int b = (int)(g / n), j = (int)(g - (long)b * n);
+        const unsigned int pos = s_base[bin[u]] + s_cnt[bin[u]] + rank[u];
+        (bin[u] == d ? exact_list : samp_list)[(size_t)h * tokens + pos] = (b << 16) | j;   // (n, B <= 65535)
+    }
 }
 
 template __global__ void k2_budgets<kKeyValue, float>(K2Args);
