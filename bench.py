@@ -368,8 +368,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     enc_gbs = work["encode"][1] / (stage_ms["encode"] / 1e3) / 1e9
     gather_gbs = L * flops_report.samples * 64 * elem / (stage_ms["encode"] / 1e3) / 1e9   # layer 0's sample count x L
 
-    cpu = None
-    if not args.no_cpu_baseline:
+    cpu = None   # the CPU baseline runs on rank 0 at N = 1 only (multi-GPU lines carry null)
+    if not args.no_cpu_baseline and world == 1:
         threads = os.cpu_count() or 1
         rate, sample, _ = cpu_reference_rate(args.config, args.alpha, args.cpu_seconds, threads, args.inputs)
         cpu = {"value": rate, "unit": "tokens/s (one layer)", "cores": threads, "kind": "port", "sample": sample}
