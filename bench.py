@@ -413,7 +413,7 @@ def main():
     ap.add_argument("--batch", type=int, default=0, help="override B per GPU")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-chunks", type=int, default=4, help="HostPipeline chunks per step (e2e leg)")
+    ap.add_argument("--e2e-chunks", type=int, default=8, help="HostPipeline chunks per step (e2e leg)")
     ap.add_argument("--inputs", default=None, choices=sorted(INPUTS_DESC),
                     help="x: x alone, q/k projected on the device (default for one-layer configs: the "
                          "reference's mca_forward(x, weights)); qkx: q, k, x given (default for the c3 stack)")
