@@ -305,7 +305,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     hy = torch.empty(y.shape, dtype=dtype).pin_memory()
     nch = args.e2e_chunks if B % args.e2e_chunks == 0 else 1
     chunk = B // nch
-    pipe = HostPipeline(layer_weights, n, chunk, dtype, dev)
+    pipe = HostPipeline(layer_weights, n, chunk, dtype, dev, depth=args.e2e_depth)
 
     def e2e_step():
         pipe.forward(hq, hk, hx, hy, cfg, seed=42, b_offset=b_offset)
@@ -414,6 +414,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-chunks", type=int, default=8, help="HostPipeline chunks per step (e2e leg)")
+    ap.add_argument("--e2e-depth", type=int, default=4, help="HostPipeline device slots in flight (e2e leg)")
     ap.add_argument("--inputs", default=None, choices=sorted(INPUTS_DESC),
                     help="x: x alone, q/k projected on the device (default for one-layer configs: the "
                          "reference's mca_forward(x, weights)); qkx: q, k, x given (default for the c3 stack)")
