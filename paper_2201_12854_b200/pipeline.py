@@ -23,7 +23,7 @@ from .api import AttentionWeights, McaConfig, mca_forward
 
 class HostPipeline:
     def __init__(self, layers: list[AttentionWeights], n: int, chunk: int, dtype: torch.dtype,
-                 device: torch.device | str = "cuda", depth: int = 3):
+                 device: torch.device | str = "cuda", depth: int = 4):
         if not layers:
             raise ValueError("need at least one layer")
         self.layers = layers
