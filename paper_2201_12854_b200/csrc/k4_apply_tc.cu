@@ -195,7 +195,7 @@ __global__ void __launch_bounds__(k4tc::kThreads, 2)
         const bool prof = MCA_K4_PROF && blockIdx.x == 0 && warp == 2 && lane == 0;
         // this thread's 32 Q values (64 bytes) of tile i and its row's lse (log2 domain)
         uint32_t qv[16];
-        float lse2_next = 0.f;
+        float lse_next = 0.f;   // raw: scaled at the next tile's start, so the load overlaps the last block
         bool waited = false;
         auto load_q = [&](int i) {
             int b, h, m0;
@@ -215,11 +215,11 @@ __global__ void __launch_bounds__(k4tc::kThreads, 2)
                     griddep_wait();
                     waited = true;
                 }
-                lse2_next = lse[((size_t)b * heads + h) * n + grow] * 1.4426950408889634f;
+                lse_next = lse[((size_t)b * heads + h) * n + grow];
             } else {
 #pragma unroll
                 for (int u = 0; u < 16; ++u) qv[u] = 0u;
-                lse2_next = 0.f;
+                lse_next = 0.f;
             }
         };
         auto publish_q = [&]() {   // Q registers -> TMEM columns kQCol + [16 half, 16 half + 16)
@@ -234,7 +234,7 @@ __global__ void __launch_bounds__(k4tc::kThreads, 2)
             int b, h, m0;
             tile_coords(i, b, h, m0);
             const int grow = m0 + row;
-            const float lse2 = lse2_next;
+            const float lse2 = lse_next * 1.4426950408889634f;
             const int g0 = i * nkb;
             if (prof && i == 1) g_k4_prof[0] = clock64();
             for (int kb = 0; kb < nkb; ++kb) {
