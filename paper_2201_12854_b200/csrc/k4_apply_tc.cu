@@ -32,6 +32,9 @@
 
 namespace mca_dev {
 
+#ifndef MCA_K4_QAHEAD
+#define MCA_K4_QAHEAD 2   // blocks before the last at which the next tile's Q loads are issued
+#endif
 #ifndef MCA_K4_PROF
 #define MCA_K4_PROF 0
 #endif
@@ -239,7 +242,8 @@ __global__ void __launch_bounds__(k4tc::kThreads, 2)
             if (prof && i == 1) g_k4_prof[0] = clock64();
             for (int kb = 0; kb < nkb; ++kb) {
                 const int g = g0 + kb, sb = g & 1;
-                if (kb == nkb - 1) load_q(i + 1);   // next tile's Q in flight during the last block
+                if (kb == (nkb > MCA_K4_QAHEAD ? nkb - 1 - MCA_K4_QAHEAD : 0))
+                    load_q(i + 1);   // next tile's Q (and lse) in flight during the tile's last blocks
                 mbar_wait(s_full + sb, (g >> 1) & 1);
                 if (prof && i == 1 && kb < 16) g_k4_prof[1 + 3 * kb] = clock64();
                 tc_fence_after();
