@@ -355,10 +355,31 @@ __global__ void __launch_bounds__(kK3BlockThreads, 1) k3_encode_sampled_bf16(K3A
         }
         for (int g = tid; g < kGuide; g += kK3BlockThreads) s_guide[g] = a.guide[(size_t)h * kGuide + g];
     }
-    for (int e = tid; e < d_in * (kDh / 8); e += kK3BlockThreads) {   // W_h -> smem, 16-byte pieces
-        const int i = e / (kDh / 8), c8 = (e % (kDh / 8)) * 8;
-        *reinterpret_cast<uint4*>(s_w + (size_t)i * kDh + c8) =
-            *reinterpret_cast<const uint4*>(wv + (size_t)i * HD + (size_t)h * kDh + c8);
+    {   // W_h -> smem, 16-byte pieces: all of a thread's loads first, then the stores
+        constexpr int kMaxPer = 8;   // pieces per thread at d_in <= 1024
+        const int total = d_in * (kDh / 8);
+        if (total <= kMaxPer * kK3BlockThreads) {
+            uint4 v[kMaxPer];
+#pragma unroll
+            for (int k = 0; k < kMaxPer; ++k) {
+                const int e = tid + k * kK3BlockThreads;
+                if (e < total) {
+                    const int i = e / (kDh / 8), c8 = (e % (kDh / 8)) * 8;
+                    v[k] = *reinterpret_cast<const uint4*>(wv + (size_t)i * HD + (size_t)h * kDh + c8);
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < kMaxPer; ++k) {
+                const int e = tid + k * kK3BlockThreads;
+                if (e < total) *reinterpret_cast<uint4*>(s_w + (size_t)e * 8) = v[k];
+            }
+        } else {
+            for (int e = tid; e < total; e += kK3BlockThreads) {
+                const int i = e / (kDh / 8), c8 = (e % (kDh / 8)) * 8;
+                *reinterpret_cast<uint4*>(s_w + (size_t)i * kDh + c8) =
+                    *reinterpret_cast<const uint4*>(wv + (size_t)i * HD + (size_t)h * kDh + c8);
+            }
+        }
     }
     __syncthreads();
     griddep_wait();      // W_h and the tables above are weights; the work lists come from the scatter
