@@ -101,7 +101,7 @@ __device__ __forceinline__ void load4w(const __nv_bfloat16* base, size_t stride,
 // (optionally) W_h in the staging type WS.
 size_t k3_smem_bytes(int d_in, size_t coef, size_t ws_elem, bool wsmem) {
     const size_t tables = (((size_t)d_in * (8 + coef) + kGuide * 2) + 127) & ~(size_t)127;
-    const size_t pairs = (size_t)kK3Warps * 4 * 16 * (coef == 8 ? 16 : 4);
+    const size_t pairs = (size_t)kK3Warps * 4 * 16 * 16;   // sizeof(SamplePair<Acc>) = 16 (alignas) for either Acc
     return tables + pairs + (wsmem ? (size_t)d_in * kDh * ws_elem : 0);
 }
 

@@ -432,9 +432,15 @@ mca_status launch_k3(mca_weights* w, const void* x, int B, int n, long b_offset,
 mca_status launch_lists(mca_weights* w, dim3 grid, int n, long tokens, mca_stream_t stream, int& launches) {
     const int H = w->heads;
     if (MCA_K2_FUSED_SCAN) {
+        const size_t smem = 2 * (size_t)(w->d_in + 1) * 4;   // bin bases + this CTA's bin counts
+        static size_t smem_set = 48 * 1024;
+        if (smem > smem_set) {
+            MCA_CUDA_TRY(cudaFuncSetAttribute(k2_scan_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            smem_set = smem;
+        }
         const dim3 gs((unsigned)((tokens + kScatterThreads * kScatterPerThread - 1) / (kScatterThreads * kScatterPerThread)),
                       (unsigned)H);
-        MCA_CUDA_TRY(launch_pdl(k2_scan_scatter, gs, dim3(kScatterThreads), 2 * (size_t)(w->d_in + 1) * 4, stream,
+        MCA_CUDA_TRY(launch_pdl(k2_scan_scatter, gs, dim3(kScatterThreads), smem, stream,
                                 (const int32_t*)w->budgets, (const uint8_t*)w->exact, (const unsigned int*)w->hist, n,
                                 H, w->d_in, tokens, w->fill, w->counts, w->samp_list, w->exact_list));
         MCA_LAUNCH_CHECK("k2_scan_scatter");

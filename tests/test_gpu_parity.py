@@ -321,6 +321,15 @@ def test_edge_shapes(mca, syn, orc):
         ref = _oracle(orc, w, q, k, x, H, alpha=0.5, seed=5)
         assert np.array_equal(out.budgets.cpu().numpy(), ref.budgets), (B, n)
         assert _row_rel(_np(out.y), ref.y) <= 1e-5, (B, n)
+    # a wide contraction: the work-list kernel's bin tables outgrow the default
+    # 48 KB of shared memory (2 (d_in + 1) words); budgets and y still match
+    for dtype, d_big in ((torch.float32, 8192), (torch.bfloat16, 6000)):
+        weights, w, q, k, x = _setup(mca, syn, 1, 48, d_big, 2, dtype, seed=d_big)
+        out = mca.mca_forward(weights, q, k, x, mca.McaConfig(alpha=0.5), seed=5, return_plan=True)
+        ref = _oracle(orc, w, q, k, x, 2, alpha=0.5, seed=5, budgets_override=out.budgets.cpu().numpy(),
+                      exact_override=out.exact_mask.cpu().numpy().astype(bool))
+        assert _row_rel(_np(out.y), ref.y) <= (1e-5 if dtype == torch.float32 else 2e-2), (dtype, d_big)
+        assert int(out.exact_mask.sum()) < out.exact_mask.numel()             # the sampled path ran
     # B = 0 is a no-op
     weights, w, q, k, x = _setup(mca, syn, 1, 8, d_in, H, torch.float32)
     e = q[:0]
