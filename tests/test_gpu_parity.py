@@ -404,6 +404,37 @@ def test_bf16_tile_encoder_parity_subprocess():
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
 
 
+def test_bf16_cuda_core_score_path_subprocess():
+    """The CUDA-core score pass (k1_scores_simt for bf16, MCA_FORCE_SIMT=1 or
+    n > 4096; the switch is read once per process) passes the bf16 parity cases."""
+    import subprocess
+    import sys
+    if os.environ.get("MCA_FORCE_SIMT") == "1":
+        pytest.skip("already running on the CUDA-core path")
+    env = dict(os.environ, MCA_FORCE_SIMT="1")
+    here = os.path.dirname(os.path.abspath(__file__))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider", "-m", "gpu",
+                        os.path.join(here, "test_gpu_parity.py"), "-k", "bf16_parity and not 1000"],
+                       env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+def test_bf16_longer_than_tensor_core_score_pass(mca, syn, orc):
+    """n = 4100 > 4096: the bf16 score pass falls back to the CUDA-core kernel
+    (DESIGN §8); Eq. 9 bitwise on its cmax, y within the bf16 tolerance."""
+    B, n, H, d_in = 1, 4100, 2, 256
+    weights, w, q, k, x = _setup(mca, syn, B, n, d_in, H, torch.bfloat16, seed=41)
+    cm = torch.zeros((B, H, n), dtype=torch.float64, device="cuda")
+    out = mca.mca_forward(weights, q, k, x, mca.McaConfig(alpha=0.4), seed=3, return_plan=True,
+                          debug=dict(cmax_out=cm))
+    b = out.budgets.cpu().numpy()
+    e = out.exact_mask.cpu().numpy().astype(bool)
+    rb, re = orc.sample_budgets_from_cmax(cm.cpu().numpy(), n, 0.4, 1, d_in)
+    assert np.array_equal(b, rb) and np.array_equal(e, re)
+    ref = _oracle(orc, w, q, k, x, H, alpha=0.4, seed=3, budgets_override=b, exact_override=e)
+    assert _row_rel(_np(out.y), ref.y) <= TOL_Y[torch.bfloat16]
+
+
 def test_host_pipeline_matches_forward(mca, syn):
     """HostPipeline (chunked, overlapped H2D / forward / D2H from pinned host
     buffers) returns bitwise the output of one mca_forward on the whole batch,
