@@ -56,3 +56,20 @@ def test_torch_module_regular_matches_dense():
         wn = m.value.weight.t().double().reshape(768, 12, 64).norm(dim=(0, 2))
         bound = 0.4 * beta[:, None, None] * wn[None, None, :]
     assert bool(torch.isfinite(ya).all()) and bool((err.mean(dim=1) <= bound[:, 0, :]).all())
+
+
+@pytest.mark.gpu
+def test_torch_op_approximation_mode_matches_forward():
+    """torch.ops.mca_b200.attention in approximation mode is mca_forward on the
+    same tensors (same seed / layer): bitwise equal outputs."""
+    import torch
+    import paper_2201_12854_b200 as mca
+    from paper_2201_12854_b200 import synthetic
+    import paper_2201_12854_b200.torch_op  # noqa: F401
+    H, n, d_in = 12, 128, 768
+    w = synthetic.make_weights(d_in, H, seed=3).to(torch.bfloat16).cuda()
+    inp = synthetic.make_inputs(2, n, d_in, H, seed=3)
+    q, k, x = (t.to(torch.bfloat16).cuda() for t in (inp.q, inp.k, inp.x))
+    y_op = torch.ops.mca_b200.attention(q, k, x, w, H, 0.4, 11, "approximation", 2)
+    y_fw = mca.mca_forward(mca.AttentionWeights(w, heads=H), q, k, x, mca.McaConfig(alpha=0.4), seed=11, layer=2).y
+    assert torch.equal(y_op, y_fw)

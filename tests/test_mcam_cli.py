@@ -153,6 +153,28 @@ def test_forward_given_attention_matches_oracle(orc, kind):
 
 
 @pytest.mark.gpu
+def test_forward_given_attention_bf16(orc):
+    """bf16 inputs (fp16 H~, bf16 y) on a given attention matrix: budgets
+    bitwise (the dump is fp64 either way), y within the bf16 tolerance."""
+    import torch
+    from paper_2201_12854_b200 import api
+    n, d, heads, seed = 64, 256, 4, 2
+    attn = cli.synthetic_attention("gaussian", n, seed=8, temperature=0.25)
+    x, w = cli.synthetic_inputs(n, d, heads, seed)
+    weights = api.AttentionWeights(torch.from_numpy(w).to(torch.bfloat16).cuda(), heads=heads)
+    xt = torch.from_numpy(x).to(torch.bfloat16).cuda()[None]
+    at = torch.from_numpy(attn).cuda()[None, None].expand(1, heads, n, n).contiguous()
+    xf = xt[0].double().cpu().numpy()
+    wf = torch.from_numpy(w).to(torch.bfloat16).double().numpy()
+    out = api.forward_given_attention(weights, at, xt, api.McaConfig(alpha=0.3), seed=seed, return_plan=True)
+    ref_y, ref_b = _oracle_given_attn(orc, attn, xf, wf, heads, 0.3, seed)
+    assert np.array_equal(out.budgets[0].cpu().numpy(), ref_b)
+    got = out.y[0].double().cpu().numpy()
+    rel = np.linalg.norm(got - ref_y, axis=1) / np.maximum(np.linalg.norm(ref_y, axis=1), 1e-30)
+    assert rel.max() <= 2e-2
+
+
+@pytest.mark.gpu
 def test_cli_bench_csv(capsys, tmp_path):
     # uniform attention, alpha = 1: every budget is 1, so the reduction is
     # 2 d_in d_h / (2 d_h + 3) exactly (SPEC.md:458 with d_h = 64 heads)
