@@ -303,9 +303,17 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     else:
         hq, hk, hx = (t.to(dtype).pin_memory() for t in (inp.q, inp.k, inp.x))
     hy = torch.empty(y.shape, dtype=dtype).pin_memory()
-    nch = args.e2e_chunks if B % args.e2e_chunks == 0 else 1
+    # chunking: a PCIe-bound step (device time under half the transfer time at ~50 GB/s)
+    # overlaps best in 8 chunks with 4 in flight; a compute-bound one (C3's 24
+    # layers, fp32, long sequences) in 4 chunks with 3 in flight (smaller chunks
+    # cost kernel efficiency there). --e2e-chunks / --e2e-depth override.
+    xfer_ms = (sum(t.numel() for t in host_inputs) + y.numel()) * elem / 50e9 * 1e3
+    pcie_bound = ms_per_step < 0.5 * xfer_ms
+    want = args.e2e_chunks or (8 if pcie_bound else 4)
+    depth = args.e2e_depth or (4 if pcie_bound else 3)
+    nch = want if B % want == 0 else 1
     chunk = B // nch
-    pipe = HostPipeline(layer_weights, n, chunk, dtype, dev, depth=args.e2e_depth)
+    pipe = HostPipeline(layer_weights, n, chunk, dtype, dev, depth=depth)
 
     def e2e_step():
         pipe.forward(hq, hk, hx, hy, cfg, seed=42, b_offset=b_offset)
@@ -380,7 +388,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
         "config": {"workload": desc, "layers": L, "global_batch": world * B, "B_per_gpu": B, "seq_len": n, "d_in": d_in,
                    "heads": H, "d_h": 64, "alpha": args.alpha, "seed": 42, "parallelism": f"dp{world} (batch shards)",
-                   "l2": "flushed (256 MB write) before every timed step", "inputs": INPUTS_DESC[args.inputs]},
+                   "l2": "flushed (256 MB write) before every timed step", "inputs": INPUTS_DESC[args.inputs],
+                   "e2e_pipeline": f"{nch} chunks, {depth} in flight"},
         "e2e": {"value": world * B * n * L / (e2e_ms / 1e3), "unit": "tokens/s",
                 "h2d_bytes_per_step": int(sum(t.numel() for t in host_inputs) * elem),
                 "d2h_bytes_per_step": int(y.numel() * elem)},
@@ -413,8 +422,8 @@ def main():
     ap.add_argument("--batch", type=int, default=0, help="override B per GPU")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-chunks", type=int, default=8, help="HostPipeline chunks per step (e2e leg)")
-    ap.add_argument("--e2e-depth", type=int, default=4, help="HostPipeline device slots in flight (e2e leg)")
+    ap.add_argument("--e2e-chunks", type=int, default=0, help="HostPipeline chunks per step (e2e leg; 0: auto)")
+    ap.add_argument("--e2e-depth", type=int, default=0, help="HostPipeline device slots in flight (e2e leg; 0: auto)")
     ap.add_argument("--inputs", default=None, choices=sorted(INPUTS_DESC),
                     help="x: x alone, q/k projected on the device (default for one-layer configs: the "
                          "reference's mca_forward(x, weights)); qkx: q, k, x given (default for the c3 stack)")
