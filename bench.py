@@ -164,8 +164,10 @@ def run_reference(args, rank: int):
     line = {"metric": METRIC, "impl": "reference", "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * B * n / value,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": desc, "B": B, "n": n, "d_in": d_in, "heads": H, "d_h": 64, "alpha": args.alpha,
-                       "seed": 42, "inputs": INPUTS_DESC[args.inputs]},
+            "config": {"workload": desc, "layers": args.layers, "global_batch": B * max(1, args.gpus), "B_per_gpu": B,
+                       "seq_len": n, "d_in": d_in, "heads": H, "d_h": 64, "alpha": args.alpha, "seed": 42,
+                       "parallelism": f"dp{max(1, args.gpus)} (batch shards)", "inputs": INPUTS_DESC[args.inputs],
+                       "reference_sample": "bounded CPU sample per step, timed on this host's cores"},
             "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "port",
                              "sample": sample},
             "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
