@@ -6,15 +6,20 @@
 // with s_k = first i such that thr_h[i] > m_k, m_k = draw k of Philox stream
 // ((b_offset + b) * heads + h) * n + j, layer `layer`.
 //
-// k3_encode_sampled (gather-scale-accumulate):
+// k3_encode_sampled (gather-scale-accumulate), the generic
+// encoder (the fp32 parity path, and bf16 when W_h does not fit the bf16
+// kernel's smem plan):
 //   - grid = (G, heads); a CTA owns one head: W_h (d_in x 64) is staged in
-//     shared memory once with 16-byte coalesced loads, together with the
-//     sampler tables (53-bit thresholds, 1024-entry guide table, 1/p).
-//   - Work comes from K2's per-head list, sorted by budget, largest first.
-//     Warps pull 4 consecutive tokens at a time from a per-head atomic cursor
+//     shared memory once with 16-byte coalesced loads (when it fits), together
+//     with the sampler tables (53-bit thresholds, the 16384-entry guide table,
+//     p or 1/p).
+//   - Work comes from the per-head list, sorted by budget, largest first.
+//     Warps pull 8 consecutive entries at a time from a per-head atomic cursor
 //     (LPT order: the expensive tokens start first, the cheap ones fill the
-//     tail), so the 4 tokens a warp encodes together have near-equal budgets
+//     tail), so the tokens a warp encodes together have near-equal budgets
 //     and the warp's octets stay converged.
+// k3_encode_sampled_bf16<kDin> (further below) is the bf16 hot path: packed
+// 4-byte draws, FHFMA accumulation, a 1-D grid whose CTAs move between heads.
 //   - An octet of 8 lanes encodes one token; lane l owns output columns
 //     [8l, 8l+8). Per round the octet draws 16 samples (8 Philox calls, 2
 //     53-bit draws each) and resolves them with the guide table; the next
