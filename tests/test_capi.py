@@ -61,6 +61,19 @@ def test_errors_are_status_codes_not_crashes(lib):
     assert lib.mca_version().startswith(b"mca_b200")
 
 
+def test_forward_attn_argument_errors(lib):
+    """mca_forward_attn (the cli's device path) reports bad arguments as
+    status codes before touching the device."""
+    from paper_2201_12854_b200 import _lib
+    cfg = _lib.McaConfigC(0.4, 0.0, 1, _lib.MCA_MODE_APPROX)
+    rc = lib.mca_forward_attn(None, None, None, 0, 1, 16, 0, 0, ctypes.byref(cfg), 1, None, None, None, None, None)
+    assert rc == _lib.MCA_ERR_NULL and b"weights" in lib.mca_last_error()
+    bad = _lib.McaConfigC(1.5, 0.0, 1, _lib.MCA_MODE_APPROX)        # alpha outside (0, 1] (SPEC.md:353)
+    rc = lib.mca_forward_attn(ctypes.c_void_p(8), None, None, 0, 1, 16, 0, 0, ctypes.byref(bad), 1, None, None, None,
+                              None, None)
+    assert rc == _lib.MCA_ERR_DOMAIN
+
+
 def test_no_cuda_device_is_reported_loudly(lib):
     """On a host without a GPU the forward must fail loudly (MCA_ERR_CUDA),
     never fall back to a CPU computation."""
