@@ -174,6 +174,16 @@ struct mca_weights {
     // timing
     bool timing = false;
     cudaEvent_t ev[5] = {};
+    void* blas_ws = nullptr;                  // explicit cuBLAS workspace (capture-safe projection GEMM)
+    // MCA_GRAPHS=1: CUDA graphs of repeated identical forwards (key = every argument).
+    // The first call of a key runs eagerly (it may size buffers), the second is
+    // captured, later ones replay the graph: one launch instead of ~10.
+    struct GraphEntry {
+        uint64_t key[16];
+        int seen = 0;
+        cudaGraphExec_t exec = nullptr;
+    };
+    std::vector<GraphEntry> graphs;
     bool ev_valid = false;
     int last_launches = 0;
 };
@@ -204,9 +214,17 @@ void free_workspace(mca_weights* w) {
     w->cap_tokens = 0;
 }
 
+// Captured forwards point into the workspace: drop them when it moves.
+void drop_graphs(mca_weights* w) {
+    for (auto& g : w->graphs)
+        if (g.exec) cudaGraphExecDestroy(g.exec);
+    w->graphs.clear();
+}
+
 mca_status ensure_workspace(mca_weights* w, long tokens, mca_stream_t stream) {
     if (tokens <= w->cap_tokens) return MCA_OK;
     if (w->cap_tokens) MCA_CUDA_TRY(cudaStreamSynchronize(stream));  // old buffers may still be in use
+    drop_graphs(w);
     free_workspace(w);
     const size_t th = (size_t)tokens * w->heads;
     if (cudaMalloc(&w->lse, th * sizeof(float)) != cudaSuccess ||
@@ -563,6 +581,9 @@ void mca_weights_free(mca_weights* w) {
     cudaFree(w->wqk);
     cudaFree(w->qk);
     if (w->blas) cublasDestroy(w->blas);
+    cudaFree(w->blas_ws);
+    for (auto& g : w->graphs)
+        if (g.exec) cudaGraphExecDestroy(g.exec);
     cudaFree(w->zeroed);
     cudaFree(w->cursor);
     cudaFree(w->counts);
@@ -580,6 +601,12 @@ mca_status mca_set_projections(mca_weights* w, const void* w_q, const void* w_k,
     }
     if (!w->blas) {
         if (cublasCreate(&w->blas) != CUBLAS_STATUS_SUCCESS) return fail(MCA_ERR_CUDA, "cublasCreate failed");
+        constexpr size_t kWs = 32u << 20;   // explicit workspace: no allocation inside a captured forward
+        if (cudaMalloc(&w->blas_ws, kWs) != cudaSuccess ||
+            cublasSetWorkspace(w->blas, w->blas_ws, kWs) != CUBLAS_STATUS_SUCCESS) {
+            cudaGetLastError();
+            return fail(MCA_ERR_ALLOC, "cuBLAS workspace allocation failed");
+        }
     }
     MCA_CUDA_TRY(cudaMemcpyAsync(w->wqk, w_q, bytes, cudaMemcpyDeviceToDevice, stream));
     MCA_CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(w->wqk) + bytes, w_k, bytes, cudaMemcpyDeviceToDevice, stream));
@@ -676,6 +703,7 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
         const size_t HD = (size_t)H * w->dh, esz = dtype_size(dt);
         if (tokens > w->cap_qk) {
             if (w->cap_qk) MCA_CUDA_TRY(cudaStreamSynchronize(stream));
+            drop_graphs(w);
             cudaFree(w->qk);
             w->qk = nullptr;
             w->cap_qk = 0;
@@ -985,8 +1013,49 @@ mca_status mca_forward_attn(mca_weights* w, const double* attn, const void* x, m
 mca_status mca_forward(mca_weights* w, const void* q, const void* k, const void* x, mca_dtype dt, int B, int n,
                        long b_offset, uint32_t layer, const mca_config* cfg, uint64_t seed, void* y,
                        int32_t* budgets_out, uint8_t* exact_out, mca_flops* flops_out, mca_stream_t stream) {
-    return mca_forward_ex(w, q, k, x, dt, B, n, b_offset, layer, cfg, seed, y, budgets_out, exact_out, flops_out,
-                          nullptr, stream);
+    static const bool use_graphs = !getenv("MCA_GRAPHS") || atoi(getenv("MCA_GRAPHS")) != 0;   // default on
+    // graphs need a capturable stream, no host read-back and no stage events
+    if (!use_graphs || !w || !cfg || !stream || flops_out || w->timing)
+        return mca_forward_ex(w, q, k, x, dt, B, n, b_offset, layer, cfg, seed, y, budgets_out, exact_out, flops_out,
+                              nullptr, stream);
+    uint64_t key[16] = {(uint64_t)q, (uint64_t)k, (uint64_t)x, (uint64_t)y, (uint64_t)dt, (uint64_t)B, (uint64_t)n,
+                        (uint64_t)b_offset, (uint64_t)layer, seed, (uint64_t)budgets_out, (uint64_t)exact_out,
+                        (uint64_t)stream, 0, 0, (uint64_t)cfg->min_samples | ((uint64_t)cfg->mode << 32)};
+    std::memcpy(&key[13], &cfg->alpha, 8);
+    std::memcpy(&key[14], &cfg->scale, 8);
+    mca_weights::GraphEntry* e = nullptr;
+    for (auto& g : w->graphs)
+        if (std::memcmp(g.key, key, sizeof(key)) == 0) e = &g;
+    if (e && e->exec) {
+        MCA_CUDA_TRY(cudaGraphLaunch(e->exec, stream));
+        return MCA_OK;
+    }
+    if (!e) {   // first sighting: eager (sizes the workspace), remembered
+        if (w->graphs.size() >= 64) {
+            if (w->graphs.front().exec) cudaGraphExecDestroy(w->graphs.front().exec);
+            w->graphs.erase(w->graphs.begin());
+        }
+        w->graphs.push_back({});
+        std::memcpy(w->graphs.back().key, key, sizeof(key));
+        return mca_forward_ex(w, q, k, x, dt, B, n, b_offset, layer, cfg, seed, y, budgets_out, exact_out, nullptr,
+                              nullptr, stream);
+    }
+    // second sighting: capture this forward and replay it from now on
+    MCA_CUDA_TRY(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+    const mca_status s = mca_forward_ex(w, q, k, x, dt, B, n, b_offset, layer, cfg, seed, y, budgets_out, exact_out,
+                                        nullptr, nullptr, stream);
+    cudaGraph_t graph = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(stream, &graph);
+    if (s != MCA_OK) {
+        if (graph) cudaGraphDestroy(graph);
+        return s;
+    }
+    if (ce != cudaSuccess) return fail(MCA_ERR_CUDA, "capturing the forward failed: %s", cudaGetErrorString(ce));
+    const cudaError_t ie = cudaGraphInstantiate(&e->exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ie != cudaSuccess) return fail(MCA_ERR_CUDA, "instantiating the forward graph failed: %s", cudaGetErrorString(ie));
+    MCA_CUDA_TRY(cudaGraphLaunch(e->exec, stream));
+    return MCA_OK;
 }
 
 mca_status mca_regular_forward(mca_weights* w, const void* q, const void* k, const void* x, mca_dtype dt, int B,

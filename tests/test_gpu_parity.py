@@ -539,3 +539,39 @@ def test_fused_kernel_multi_item_per_cta(mca, syn, orc, n):
                                    b_offset=s)
         assert np.abs(cm[sl].cpu().numpy() / ref0.cmax - 1.0).max() <= 1e-4
         assert _row_rel(_np(out.y[sl]), ref.y) <= TOL_Y[torch.bfloat16]
+
+
+def test_graph_replay_matches_eager(mca, syn):
+    """Repeated identical forwards are captured into a CUDA graph and replayed
+    (MCA_GRAPHS, default on): every replay equals the eager forward bitwise,
+    including after the inputs change in place (a replay reads the current
+    data), and a larger batch (workspace reallocation) drops the stale graphs."""
+    H, n, d_in = 12, 128, 768
+    weights, w, q, k, x = _setup(mca, syn, 3, n, d_in, H, torch.bfloat16, seed=77)
+    cfg = mca.McaConfig(alpha=0.4)
+    stream = torch.cuda.Stream()
+    y = torch.empty((3, n, H * 64), dtype=torch.bfloat16, device="cuda")
+
+    def eager(qq, kk, xx):   # the debug entry point never uses graphs
+        return mca.mca_forward(weights, qq, kk, xx, cfg, seed=9, debug=dict(draws_stride=0)).y.clone()
+
+    with torch.cuda.stream(stream):
+        outs = []
+        for _ in range(4):   # eager, captured, replayed, replayed
+            mca.mca_forward(weights, q, k, x, cfg, seed=9, y=y, stream=stream)
+            outs.append(y.clone())
+        stream.synchronize()
+        ref = eager(q, k, x)
+        for o in outs:
+            assert torch.equal(o, ref)
+        x.mul_(-0.5)
+        q.mul_(1.25)                                             # same pointers, new data
+        mca.mca_forward(weights, q, k, x, cfg, seed=9, y=y, stream=stream)
+        stream.synchronize()
+        assert torch.equal(y, eager(q, k, x))
+        big = _setup(mca, syn, 6, n, d_in, H, torch.bfloat16, seed=78)
+        mca.mca_forward(weights, big[2], big[3], big[4], cfg, seed=9, stream=stream)   # grows the workspace
+        mca.mca_forward(weights, q, k, x, cfg, seed=9, y=y, stream=stream)
+        mca.mca_forward(weights, q, k, x, cfg, seed=9, y=y, stream=stream)
+        stream.synchronize()
+        assert torch.equal(y, eager(q, k, x))
