@@ -18,12 +18,10 @@
 // configuration / CUDA errors std::runtime_error. Every call reaches the GPU;
 // there is no host fallback.
 //
-// Two levels: device-pointer calls (zero copies; any cudaStream_t) and
+// Two levels: device-pointer calls (zero copies; any mca_stream_t) and
 // Matrix-level calls for one sequence (fp64 host Matrix in, converted to the
 // fp32 parity-precision path, result copied back).
 #pragma once
-
-#include <cuda_runtime.h>
 
 #include <cstdint>
 #include <stdexcept>
@@ -61,44 +59,46 @@ inline void check(mca_status s) {
     }
 }
 
-inline void cuda_check(cudaError_t e, const char* what) {
-    if (e != cudaSuccess) throw std::runtime_error(std::string("mca: ") + what + ": " + cudaGetErrorString(e));
+// Device buffers and copies go through libmca_b200's own helpers (mca_cuda.h),
+// so a caller links -lmca_b200 alone (no direct libcudart dependency).
+inline void dev_check(mca_status s, const char* what) {
+    if (s != MCA_OK) throw std::runtime_error(std::string("mca: ") + what + ": " + mca_last_error());
 }
 
 // W_V [d_in, heads*64] on the device plus its cached sampling tables.
 class AttentionWeights {
    public:
     // From a device buffer in `dtype` (row-major [d_in, heads*64]).
-    AttentionWeights(const void* w_v_device, mca_dtype dtype, int d_in, int heads, cudaStream_t stream = nullptr)
+    AttentionWeights(const void* w_v_device, mca_dtype dtype, int d_in, int heads, mca_stream_t stream = nullptr)
         : dtype_(dtype), d_in_(d_in), heads_(heads) {
         check(mca_prepare_weights(w_v_device, dtype, d_in, heads, 64, stream, &h_));
     }
     // From a host fp64 Matrix (d_in x heads*64): uploaded as fp32 (parity precision).
-    AttentionWeights(const Matrix& w_v, int heads, cudaStream_t stream = nullptr)
+    AttentionWeights(const Matrix& w_v, int heads, mca_stream_t stream = nullptr)
         : dtype_(MCA_F32), d_in_(static_cast<int>(w_v.rows)), heads_(heads) {
         check_shape(w_v);
         void* d = upload_f32(w_v);
         const mca_status s = mca_prepare_weights(d, MCA_F32, d_in_, heads, 64, stream, &h_);
-        cudaFree(d);  // the handle keeps its own copy
+        mca_device_free(d);  // the handle keeps its own copy
         check(s);
     }
     // SPEC's AttentionWeights{w_q, w_k, w}: host fp64 matrices (all d_in x heads*64),
     // uploaded as fp32; forwards then take x alone.
-    AttentionWeights(const Matrix& w_q, const Matrix& w_k, const Matrix& w_v, int heads, cudaStream_t stream = nullptr)
+    AttentionWeights(const Matrix& w_q, const Matrix& w_k, const Matrix& w_v, int heads, mca_stream_t stream = nullptr)
         : AttentionWeights(w_v, heads, stream) {
         check_shape(w_q);
         check_shape(w_k);
         void* dq = upload_f32(w_q);
         void* dk = upload_f32(w_k);
         const mca_status s = mca_set_projections(h_, dq, dk, stream);
-        cudaStreamSynchronize(stream);
-        cudaFree(dq);
-        cudaFree(dk);
+        mca_stream_sync(stream);
+        mca_device_free(dq);
+        mca_device_free(dk);
         check(s);
         projections_ = true;
     }
     // Attach device W_q / W_k (this handle's dtype, d_in x heads*64).
-    void set_projections(const void* w_q_device, const void* w_k_device, cudaStream_t stream = nullptr) {
+    void set_projections(const void* w_q_device, const void* w_k_device, mca_stream_t stream = nullptr) {
         check(mca_set_projections(h_, w_q_device, w_k_device, stream));
         projections_ = true;
     }
@@ -131,11 +131,11 @@ class AttentionWeights {
     static void* upload_f32(const Matrix& m) {
         std::vector<float> f(m.data.begin(), m.data.end());
         void* d = nullptr;
-        cuda_check(cudaMalloc(&d, f.size() * sizeof(float)), "cudaMalloc");
-        cudaError_t e = cudaMemcpy(d, f.data(), f.size() * sizeof(float), cudaMemcpyHostToDevice);
-        if (e != cudaSuccess) {
-            cudaFree(d);
-            cuda_check(e, "cudaMemcpy");
+        dev_check(mca_device_alloc(f.size() * sizeof(float), &d), "device allocation");
+        const mca_status e = mca_copy(d, f.data(), f.size() * sizeof(float), MCA_COPY_H2D);
+        if (e != MCA_OK) {
+            mca_device_free(d);
+            dev_check(e, "H2D copy");
         }
         return d;
     }
@@ -151,7 +151,7 @@ class AttentionWeights {
 inline FlopsReport forward_device(const AttentionWeights& w, const void* q, const void* k, const void* x, int B, int n,
                                   const McaConfig& cfg, uint64_t seed, void* y, int32_t* budgets = nullptr,
                                   uint8_t* exact = nullptr, bool want_flops = false, long b_offset = 0,
-                                  uint32_t layer = 0, cudaStream_t stream = nullptr) {
+                                  uint32_t layer = 0, mca_stream_t stream = nullptr) {
     const mca_config c = cfg.c();
     mca_flops f{};
     check(mca_forward(w.handle(), q, k, x, w.dtype(), B, n, b_offset, layer, &c, seed, y, budgets, exact,
@@ -180,14 +180,14 @@ struct AttentionOutput {   // SPEC.md:280-283 (attn is never materialised on the
 namespace detail {
 struct DeviceBuf {
     void* p = nullptr;
-    explicit DeviceBuf(std::size_t bytes) { cuda_check(cudaMalloc(&p, bytes ? bytes : 1), "cudaMalloc"); }
-    ~DeviceBuf() { cudaFree(p); }
+    explicit DeviceBuf(std::size_t bytes) { dev_check(mca_device_alloc(bytes ? bytes : 1, &p), "device allocation"); }
+    ~DeviceBuf() { mca_device_free(p); }
     DeviceBuf(const DeviceBuf&) = delete;
     DeviceBuf& operator=(const DeviceBuf&) = delete;
 };
 inline void upload_f32(const Matrix& m, DeviceBuf& d) {
     std::vector<float> f(m.data.begin(), m.data.end());
-    cuda_check(cudaMemcpy(d.p, f.data(), f.size() * sizeof(float), cudaMemcpyHostToDevice), "cudaMemcpy H2D");
+    dev_check(mca_copy(d.p, f.data(), f.size() * sizeof(float), MCA_COPY_H2D), "H2D copy");
 }
 }  // namespace detail
 
@@ -210,14 +210,14 @@ inline AttentionOutput multihead_forward(const Matrix& q, const Matrix& k, const
     out.flops = forward_device(w, dq.p, dk.p, dx.p, 1, static_cast<int>(n), cfg, seed, dy.p,
                                static_cast<int32_t*>(db.p), static_cast<uint8_t*>(de.p), true);
     std::vector<float> y(q.data.size());
-    cuda_check(cudaMemcpy(y.data(), dy.p, y.size() * 4, cudaMemcpyDeviceToHost), "cudaMemcpy D2H");
+    dev_check(mca_copy(y.data(), dy.p, y.size() * 4, MCA_COPY_D2H), "D2H copy");
     out.y.rows = n;
     out.y.cols = H * 64;
     out.y.data.assign(y.begin(), y.end());
     out.budgets.resize(H * n);
     out.exact_mask.resize(H * n);
-    cuda_check(cudaMemcpy(out.budgets.data(), db.p, H * n * 4, cudaMemcpyDeviceToHost), "cudaMemcpy D2H");
-    cuda_check(cudaMemcpy(out.exact_mask.data(), de.p, H * n, cudaMemcpyDeviceToHost), "cudaMemcpy D2H");
+    dev_check(mca_copy(out.budgets.data(), db.p, H * n * 4, MCA_COPY_D2H), "D2H copy");
+    dev_check(mca_copy(out.exact_mask.data(), de.p, H * n, MCA_COPY_D2H), "D2H copy");
     return out;
 }
 
@@ -235,14 +235,14 @@ inline AttentionOutput mca_forward(const Matrix& x, const AttentionWeights& w, c
     out.flops = forward_device(w, nullptr, nullptr, dx.p, 1, static_cast<int>(n), cfg, seed, dy.p,
                                static_cast<int32_t*>(db.p), static_cast<uint8_t*>(de.p), true);
     std::vector<float> y(n * H * 64);
-    cuda_check(cudaMemcpy(y.data(), dy.p, y.size() * 4, cudaMemcpyDeviceToHost), "cudaMemcpy D2H");
+    dev_check(mca_copy(y.data(), dy.p, y.size() * 4, MCA_COPY_D2H), "D2H copy");
     out.y.rows = n;
     out.y.cols = H * 64;
     out.y.data.assign(y.begin(), y.end());
     out.budgets.resize(H * n);
     out.exact_mask.resize(H * n);
-    cuda_check(cudaMemcpy(out.budgets.data(), db.p, H * n * 4, cudaMemcpyDeviceToHost), "cudaMemcpy D2H");
-    cuda_check(cudaMemcpy(out.exact_mask.data(), de.p, H * n, cudaMemcpyDeviceToHost), "cudaMemcpy D2H");
+    dev_check(mca_copy(out.budgets.data(), db.p, H * n * 4, MCA_COPY_D2H), "D2H copy");
+    dev_check(mca_copy(out.exact_mask.data(), de.p, H * n, MCA_COPY_D2H), "D2H copy");
     return out;
 }
 
@@ -265,14 +265,14 @@ inline void sample_budgets(const std::vector<double>& cmax, int n, int d, const 
                            std::vector<int32_t>& budgets, std::vector<uint8_t>& exact) {
     const std::size_t m = cmax.size();
     detail::DeviceBuf dc(m * 8), db(m * 4), de(m);
-    cuda_check(cudaMemcpy(dc.p, cmax.data(), m * 8, cudaMemcpyHostToDevice), "cudaMemcpy H2D");
+    dev_check(mca_copy(dc.p, cmax.data(), m * 8, MCA_COPY_H2D), "H2D copy");
     const mca_config c = cfg.c();
     check(mca_stage_budgets(static_cast<const double*>(dc.p), static_cast<long>(m), n, d, &c,
                             static_cast<int32_t*>(db.p), static_cast<uint8_t*>(de.p), nullptr));
     budgets.resize(m);
     exact.resize(m);
-    cuda_check(cudaMemcpy(budgets.data(), db.p, m * 4, cudaMemcpyDeviceToHost), "cudaMemcpy D2H");
-    cuda_check(cudaMemcpy(exact.data(), de.p, m, cudaMemcpyDeviceToHost), "cudaMemcpy D2H");
+    dev_check(mca_copy(budgets.data(), db.p, m * 4, MCA_COPY_D2H), "D2H copy");
+    dev_check(mca_copy(exact.data(), de.p, m, MCA_COPY_D2H), "D2H copy");
 }
 
 }  // namespace b200

@@ -172,6 +172,15 @@ int mca_last_stage_ms(const mca_weights* w, float* ms, int max_stages);
 /* Number of kernels the last forward enqueued. */
 int mca_last_launch_count(const mca_weights* w);
 
+/* Device buffers and synchronous copies for host callers that do not link the
+ * CUDA runtime themselves (include/mca/mca.hpp uses these, so a C++ caller
+ * links -lmca_b200 alone). Allocation is on the current device. */
+typedef enum mca_copy_kind { MCA_COPY_H2D = 0, MCA_COPY_D2H = 1, MCA_COPY_D2D = 2 } mca_copy_kind;
+mca_status mca_device_alloc(size_t bytes, void** out);
+void mca_device_free(void* p);
+mca_status mca_copy(void* dst, const void* src, size_t bytes, mca_copy_kind kind);
+mca_status mca_stream_sync(mca_stream_t stream);
+
 const char* mca_last_error(void);
 const char* mca_version(void);
 

@@ -48,9 +48,9 @@ namespace mca_dev {
 #endif
 // Diagnostics (build with EXTRA=-DMCA_K12_PROF=1): clock64 stamps of CTA 0:
 // [0] start, [1 + u] group A block u done, [40 + u] group B block u done, [80] end
-__device__ long long g_k12_prof[256];   // + [96 + U] A wait done, [128 + U] / [160 + U] A piece loads done, [192 + U] phase-1 MMA issued, [224 + qt] lse of tile qt
+__device__ long long g_k12_prof[MCA_K12_PROF ? 256 : 1];   // + [96 + U] A wait done, [128 + U] / [160 + U] A piece loads done, [192 + U] phase-1 MMA issued, [224 + qt] lse of tile qt
 // per CTA: smid, globaltimer at start and at exit (ns), clocks at exit - start
-__device__ unsigned long long g_k12_cta[4096][4];
+__device__ unsigned long long g_k12_cta[MCA_K12_PROF ? 4096 : 1][4];
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));

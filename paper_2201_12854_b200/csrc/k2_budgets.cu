@@ -90,10 +90,10 @@ __global__ void __launch_bounds__(256) k2_budgets(K2Args a) {
     if (use_hist)
         for (int i = threadIdx.x; i <= a.d; i += blockDim.x) s_hist[i] = 0;
     __syncthreads();
-    const long bh = blockIdx.y;
+    const long bh = grid_bh();
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     unsigned long long cost = 0, samples = 0, nexact = 0;
-    if (j < a.row_len) {
+    if (j < a.row_len && bh * a.row_len < a.count) {
         const long t = bh * a.row_len + j;
         int r;
         bool ex;
@@ -212,11 +212,11 @@ __global__ void __launch_bounds__(256) k2_scatter(const int32_t* __restrict__ bu
                                                   const uint8_t* __restrict__ exact, int n, int heads, int d,
                                                   long tokens, unsigned int* __restrict__ cursor,
                                                   int32_t* __restrict__ samp_list, int32_t* __restrict__ exact_list) {
-    const long bh = blockIdx.y;
+    const long bh = grid_bh();
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     griddep_trigger();
     griddep_wait();      // the scan's cursors
-    if (j >= n) return;
+    if (j >= n || bh * n >= tokens * heads) return;
     const long t = bh * n + j;
     const int b = (int)(bh / heads), h = (int)(bh - (long)b * heads);
     const int tok = (b << 16) | j;   // list entry: (b << 16) | j (n, B <= 65535, checked by the host)

@@ -310,7 +310,7 @@ __device__ __forceinline__ void fma2_bf16_f32(float& acc0, float& acc1, uint32_t
 constexpr int kK3StealMin = MCA_K3_STEAL;   // list entries a head must have left to be worth joining
 // Diagnostics (EXTRA=-DMCA_K3S_PROF=1): per CTA the globaltimer at start, after
 // the prologue, at exit, and its head.
-__device__ unsigned long long g_k3s_cta[1024][4];
+__device__ unsigned long long g_k3s_cta[MCA_K3S_PROF ? 1024 : 1][4];
 
 // kDin > 0: d_in fixed at compile time (BERT-base 768, -large 1024), so every
 // shared-memory table address is an immediate and the 64-register hot loop

@@ -44,7 +44,7 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 #endif
 // Diagnostics (EXTRA=-DMCA_K3B_PROF=1): CTA (0, 0)'s clock64 at entry, after the
 // dependency wait, per chunk landed / MMA issued, epilogue start and end.
-__device__ long long g_k3b_prof[64];
+__device__ long long g_k3b_prof[MCA_K3B_PROF ? 64 : 1];
 
 __global__ void __launch_bounds__(k3btc::kThreads, 2) k3b_exact_tc(K3Args a) {
     using namespace k3btc;

@@ -40,7 +40,7 @@ namespace mca_dev {
 #endif
 // Diagnostics (build with EXTRA=-DMCA_K4_PROF=1): clock64 stamps of the first
 // CTA's softmax thread 0 into this device buffer.
-__device__ long long g_k4_prof[64];
+__device__ long long g_k4_prof[MCA_K4_PROF ? 64 : 1];
 
 namespace k4tc {
 constexpr int kBM = 128, kBK = 64, kStages = 4;      // separate K and H~ rings of kStages each

@@ -15,10 +15,10 @@
 namespace mca_dev {
 
 // grid ((n + 255) / 256, B * H), 256 threads: thread = column j (coalesced rows)
-__global__ void ka_colmax(const double* __restrict__ attn, int n, double* __restrict__ cmax) {
-    const long bh = blockIdx.y;
+__global__ void ka_colmax(const double* __restrict__ attn, int n, long bh_count, double* __restrict__ cmax) {
+    const long bh = grid_bh();
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= n) return;
+    if (j >= n || bh >= bh_count) return;
     const double* a = attn + (size_t)bh * n * n + j;
     double m = -INFINITY;
     for (int i = 0; i < n; ++i) m = fmax(m, a[(size_t)i * n]);

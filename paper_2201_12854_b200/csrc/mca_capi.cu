@@ -17,6 +17,8 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 #include <utility>
 #include <vector>
@@ -34,6 +36,7 @@
 #include "k4_apply_simt.cu"
 #include "k4_apply_tc.cu"
 #include "ka_given_attn.cu"
+#include "mca_diag.cuh"
 
 #ifndef MCA_K2_FUSED_SCAN
 #define MCA_K2_FUSED_SCAN 1   // work lists by one scan + scatter kernel
@@ -74,15 +77,54 @@ mca_status fail(mca_status s, const char* fmt, ...) {
 
 size_t dtype_size(mca_dtype t) { return t == MCA_BF16 ? 2 : 4; }
 
+constexpr size_t kMaxGraphs = 256;              // captured forwards kept per handle (LRU)
+constexpr size_t kBlasWorkspace = 32u << 20;   // explicit cuBLAS workspace (capture-safe projection GEMM)
+
+// Per-device facts and settings. Everything here is keyed by the current
+// device: one process may drive several GPUs (one handle per device), and
+// kernel attributes such as the >48 KB shared-memory opt-in are per device.
+int current_device() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return dev;
+}
+
 int sm_count() {
-    static int c = 0;
-    if (!c) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&c, cudaDevAttrMultiProcessorCount, dev);
-        if (c <= 0) c = 148;
-    }
+    static std::mutex mu;
+    static std::map<int, int> by_dev;
+    const int dev = current_device();
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = by_dev.find(dev);
+    if (it != by_dev.end()) return it->second;
+    int c = 0;
+    cudaDeviceGetAttribute(&c, cudaDevAttrMultiProcessorCount, dev);
+    if (c <= 0) c = 148;
+    by_dev[dev] = c;
     return c;
+}
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (device, kernel),
+// raised when a launch needs more than the last setting.
+cudaError_t ensure_smem(const void* fn, size_t bytes) {
+    static std::mutex mu;
+    static std::map<std::pair<int, const void*>, size_t> set;
+    const auto key = std::make_pair(current_device(), fn);
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = set.find(key);
+    if (it != set.end() && it->second >= bytes) return cudaSuccess;
+    const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess) set[key] = bytes;
+    return e;
+}
+template <class F>
+cudaError_t ensure_smem(F* fn, size_t bytes) {
+    return ensure_smem(reinterpret_cast<const void*>(fn), bytes);
+}
+
+// [B*H]-row grid: x covers a row's tokens, (y, z) the B*H rows (grid_bh()).
+dim3 bh_grid(unsigned x, long bh) {
+    const unsigned y = (unsigned)std::min<long>(bh, 65535);
+    return dim3(x, y, (unsigned)((bh + y - 1) / y));
 }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
@@ -180,10 +222,12 @@ struct mca_weights {
     // captured, later ones replay the graph: one launch instead of ~10.
     struct GraphEntry {
         uint64_t key[16];
-        int seen = 0;
+        uint64_t last_use = 0;        // LRU clock
+        bool graphable = true;        // false after a failed capture: always eager
         cudaGraphExec_t exec = nullptr;
     };
     std::vector<GraphEntry> graphs;
+    uint64_t graph_clock = 0;
     bool ev_valid = false;
     int last_launches = 0;
 };
@@ -319,37 +363,16 @@ mca_status launch_k3(mca_weights* w, const void* x, int B, int n, long b_offset,
         if (!make_tmap_bf16(&tw, w->wprime, (uint64_t)w->heads * kDh, w->d_in, 1, 64))
             return fail(MCA_ERR_CUDA, "cuTensorMapEncodeTiled failed for W'");
         const uint32_t smem = k3t::layout(w->d_in).bytes;
-        MCA_CUDA_TRY(cudaFuncSetAttribute(k3t_encode_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        MCA_CUDA_TRY(ensure_smem(k3t_encode_tc, smem));
         int G = sm_count() / w->heads;
         const long cap = (long)B * ((n + k3t::kBM - 1) / k3t::kBM);
         if (G > cap) G = (int)cap;
         if (G < 1) G = 1;
-        static const bool prof = kK3tProf && getenv("MCA_K3_PROF") != nullptr;   // diagnostics: phase clocks
-        long long* pbuf = nullptr;
-        if (prof) {
-            MCA_CUDA_TRY(cudaMalloc(&pbuf, 64 * 8 * sizeof(long long)));
-            MCA_CUDA_TRY(cudaMemsetAsync(pbuf, 0, 64 * 8 * sizeof(long long), stream));
-            a.prof = pbuf;
-        }
+        a.prof = mca_diag::k3t_prof_begin(stream);   // diagnostics builds only
         k3t_encode_tc<<<dim3(G, w->heads), k3t::kThreads, smem, stream>>>(a, tw,
                                                                            (const __nv_bfloat16*)w->pbf);
         MCA_LAUNCH_CHECK("k3t_encode_tc");
-        if (prof) {
-            long long hbuf[64 * 8];
-            MCA_CUDA_TRY(cudaMemcpyAsync(hbuf, pbuf, sizeof(hbuf), cudaMemcpyDeviceToHost, stream));
-            MCA_CUDA_TRY(cudaStreamSynchronize(stream));
-            cudaFree(pbuf);
-            double acc[7] = {};
-            int nt = 0;
-            for (int i = 1; i < 64 && hbuf[i * 8]; ++i, ++nt) {
-                for (int k = 0; k < 6; ++k) acc[k] += (double)(hbuf[i * 8 + k + 1] - hbuf[i * 8 + k]);
-                if (i + 1 < 64 && hbuf[(i + 1) * 8]) acc[6] += (double)(hbuf[(i + 1) * 8] - hbuf[i * 8]);
-            }
-            if (nt)
-                fprintf(stderr, "k3t CTA0 mean cycles/tile over %d tiles: predraw %.0f xload+setup+afree %.0f zero %.0f count %.0f "
-                                "convert %.0f epi %.0f | tile %.0f\n", nt, acc[0] / nt, acc[1] / nt, acc[2] / nt,
-                        acc[3] / nt, acc[4] / nt, acc[5] / nt, acc[6] / (nt > 1 ? nt - 1 : 1));
-        }
+        mca_diag::k3t_prof_end(stream, a.prof);
         return MCA_OK;
     } else {
     // Gather-scale-accumulate: W_h staged as bf16 (one 128-byte smem wavefront
@@ -372,7 +395,7 @@ mca_status launch_k3(mca_weights* w, const void* x, int B, int n, long b_offset,
         if constexpr (sizeof(T) == 2) kern = k3_encode_sampled<__nv_bfloat16, __nv_bfloat16, float, false>;
         else kern = k3_encode_sampled<float, float, double, false>;
     }
-    MCA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    MCA_CUDA_TRY(ensure_smem(kern, smem));
     int occ = 0;
     MCA_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kK3BlockThreads, smem));
     if (occ < 1) occ = 1;
@@ -388,34 +411,10 @@ mca_status launch_k3(mca_weights* w, const void* x, int B, int n, long b_offset,
     if (bf16_kern) MCA_CUDA_TRY(launch_pdl(kern, dim3(G1), dim3(kK3BlockThreads), smem, stream, a));
     else kern<<<dim3(G, w->heads), kK3BlockThreads, smem, stream>>>(a);
     MCA_LAUNCH_CHECK("k3_encode_sampled");
-    if (MCA_K3S_PROF && bf16_kern) {   // diagnostics build: per-head CTA spread
-        static unsigned long long c[1024][4];
-        const int nc = std::min(G1, 1024);
-        MCA_CUDA_TRY(cudaStreamSynchronize(stream));
-        MCA_CUDA_TRY(cudaMemcpyFromSymbol(c, g_k3s_cta, sizeof(unsigned long long) * 4 * nc));
-        unsigned long long t0 = ~0ull;
-        for (int i = 0; i < nc; ++i) t0 = std::min(t0, c[i][0]);
-        fprintf(stderr, "k3s heads (prologue end, first exit, last exit in us):");
-        for (int hh = 0; hh < w->heads; ++hh) {
-            unsigned long long pe = 0, e0 = ~0ull, e1 = 0;
-            for (int i = 0; i < nc; ++i)
-                if ((int)c[i][3] == hh) {
-                    pe = std::max(pe, c[i][1] - t0);
-                    e0 = std::min(e0, c[i][2] - t0);
-                    e1 = std::max(e1, c[i][2] - t0);
-                }
-            fprintf(stderr, " | h%d %.1f %.1f %.1f", hh, pe / 1e3, e0 / 1e3, e1 / 1e3);
-        }
-        fprintf(stderr, "\n");
-    }
+    if (bf16_kern) mca_diag::dump_k3s(stream, G1, w->heads);   // diagnostics builds only
     }
     if (sizeof(T) == 2 && !force_simt()) {   // bf16: exact token-heads on the tensor cores
-        static bool attr = false;
-        if (!attr) {
-            MCA_CUDA_TRY(cudaFuncSetAttribute(k3b_exact_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              (int)k3btc::kSmemBytes));
-            attr = true;
-        }
+        MCA_CUDA_TRY(ensure_smem(k3b_exact_tc, k3btc::kSmemBytes));
         // persistent: one wave (2 CTAs per SM), CTAs loop over their head's exact tiles
         int Ge = (2 * sm_count() + w->heads - 1) / w->heads;
         const long ecap = (a.tokens + k3btc::kBM - 1) / k3btc::kBM;
@@ -424,16 +423,7 @@ mca_status launch_k3(mca_weights* w, const void* x, int B, int n, long b_offset,
         MCA_CUDA_TRY(launch_pdl(k3b_exact_tc, dim3((unsigned)Ge, w->heads), dim3(k3btc::kThreads), k3btc::kSmemBytes,
                                 stream, a));
         MCA_LAUNCH_CHECK("k3b_exact_tc");
-        if (MCA_K3B_PROF) {   // diagnostics build: CTA (0, 0)'s timeline
-            long long t[64];
-            MCA_CUDA_TRY(cudaStreamSynchronize(stream));
-            MCA_CUDA_TRY(cudaMemcpyFromSymbol(t, g_k3b_prof, sizeof(t)));
-            fprintf(stderr, "k3b CTA0: waited %lld | landed", t[1] - t[0]);
-            for (int c = 0; c < 12; ++c) fprintf(stderr, " %lld", t[2 + c] - t[0]);
-            fprintf(stderr, " | mma");
-            for (int c = 0; c < 12; ++c) fprintf(stderr, " %lld", t[20 + c] - t[0]);
-            fprintf(stderr, " | acc %lld end %lld\n", t[40] - t[0], t[41] - t[0]);
-        }
+        mca_diag::dump_k3b(stream);   // diagnostics builds only
     } else {                                  // fp32 parity path: fp64 CUDA-core GEMM
         int Ge = (2 * sm_count() + w->heads - 1) / w->heads;
         const long ecap = (a.tokens + 63) / 64;
@@ -451,11 +441,7 @@ mca_status launch_lists(mca_weights* w, dim3 grid, int n, long tokens, mca_strea
     const int H = w->heads;
     if (MCA_K2_FUSED_SCAN) {
         const size_t smem = 2 * (size_t)(w->d_in + 1) * 4;   // bin bases + this CTA's bin counts
-        static size_t smem_set = 48 * 1024;
-        if (smem > smem_set) {
-            MCA_CUDA_TRY(cudaFuncSetAttribute(k2_scan_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            smem_set = smem;
-        }
+        if (smem > 48 * 1024) MCA_CUDA_TRY(ensure_smem(k2_scan_scatter, smem));
         const dim3 gs((unsigned)((tokens + kScatterThreads * kScatterPerThread - 1) / (kScatterThreads * kScatterPerThread)),
                       (unsigned)H);
         MCA_CUDA_TRY(launch_pdl(k2_scan_scatter, gs, dim3(kScatterThreads), smem, stream,
@@ -496,6 +482,33 @@ mca_status read_flops(mca_weights* w, int B, int n, bool approx, mca_flops* out,
 extern "C" {
 
 const char* mca_last_error(void) { return g_err.c_str(); }
+
+mca_status mca_device_alloc(size_t bytes, void** out) {
+    if (!out) return fail(MCA_ERR_NULL, "out is NULL");
+    *out = nullptr;
+    if (cudaMalloc(out, bytes) != cudaSuccess) {
+        const cudaError_t e = cudaGetLastError();
+        return fail(e == cudaErrorMemoryAllocation ? MCA_ERR_ALLOC : MCA_ERR_CUDA, "cudaMalloc(%zu) failed: %s", bytes,
+                    cudaGetErrorString(e));
+    }
+    return MCA_OK;
+}
+
+void mca_device_free(void* p) { cudaFree(p); }
+
+mca_status mca_copy(void* dst, const void* src, size_t bytes, mca_copy_kind kind) {
+    if ((!dst || !src) && bytes) return fail(MCA_ERR_NULL, "dst / src is NULL");
+    const cudaMemcpyKind k = kind == MCA_COPY_H2D   ? cudaMemcpyHostToDevice
+                             : kind == MCA_COPY_D2H ? cudaMemcpyDeviceToHost
+                                                    : cudaMemcpyDeviceToDevice;
+    MCA_CUDA_TRY(cudaMemcpy(dst, src, bytes, k));
+    return MCA_OK;
+}
+
+mca_status mca_stream_sync(mca_stream_t stream) {
+    MCA_CUDA_TRY(cudaStreamSynchronize(stream));
+    return MCA_OK;
+}
 const char* mca_version(void) { return "mca_b200 0.1 (sm_100a)"; }
 
 mca_status mca_prepare_weights(const void* w_v, mca_dtype wdt, int d_in, int heads, int d_h, mca_stream_t stream,
@@ -601,9 +614,8 @@ mca_status mca_set_projections(mca_weights* w, const void* w_q, const void* w_k,
     }
     if (!w->blas) {
         if (cublasCreate(&w->blas) != CUBLAS_STATUS_SUCCESS) return fail(MCA_ERR_CUDA, "cublasCreate failed");
-        constexpr size_t kWs = 32u << 20;   // explicit workspace: no allocation inside a captured forward
-        if (cudaMalloc(&w->blas_ws, kWs) != cudaSuccess ||
-            cublasSetWorkspace(w->blas, w->blas_ws, kWs) != CUBLAS_STATUS_SUCCESS) {
+        if (cudaMalloc(&w->blas_ws, kBlasWorkspace) != cudaSuccess ||
+            cublasSetWorkspace(w->blas, w->blas_ws, kBlasWorkspace) != CUBLAS_STATUS_SUCCESS) {
             cudaGetLastError();
             return fail(MCA_ERR_ALLOC, "cuBLAS workspace allocation failed");
         }
@@ -655,7 +667,7 @@ mca_status mca_stage_budgets(const double* cmax, long count, int n, int d, const
     if (count == 0) return MCA_OK;
     int launches = 0;
     if (count > 0x7FFFFFFF) return fail(MCA_ERR_SHAPE, "count too large");
-    const dim3 grid((unsigned)((count + 255) / 256), 1);
+    const dim3 grid((unsigned)((count + 255) / 256), 1);   // one row of `count` values
     K2Args a{};
     a.cmax_in = cmax;
     a.count = count;
@@ -716,7 +728,10 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
         const float one = 1.0f, zero = 0.0f;
         const cudaDataType_t ty = dt == MCA_BF16 ? CUDA_R_16BF : CUDA_R_32F;
         const cublasComputeType_t ct = dt == MCA_BF16 ? CUBLAS_COMPUTE_32F : CUBLAS_COMPUTE_32F_PEDANTIC;
+        // cublasSetStream resets the handle's workspace to cuBLAS's pool: re-attach
+        // the explicit one (no allocation inside a captured forward)
         if (cublasSetStream(w->blas, stream) != CUBLAS_STATUS_SUCCESS ||
+            cublasSetWorkspace(w->blas, w->blas_ws, kBlasWorkspace) != CUBLAS_STATUS_SUCCESS ||
             cublasGemmStridedBatchedEx(w->blas, CUBLAS_OP_N, CUBLAS_OP_N, (int)HD, (int)tokens, w->d_in, &one, w->wqk,
                                        ty, (int)HD, (long long)w->d_in * HD, x, ty, w->d_in, 0, &zero, w->qk, ty,
                                        (int)HD, (long long)tokens * HD, 2, ct,
@@ -747,7 +762,7 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
         if (!make_tmap_bf16(&tq, q, (uint64_t)H * kDh, n, B, 128) || !make_tmap_bf16(&tk, k, (uint64_t)H * kDh, n, B, 128))
             return fail(MCA_ERR_CUDA, "cuTensorMapEncodeTiled failed for q/k");
         const uint32_t smem = k12::layout((n + k12::kT - 1) / k12::kT, w->d_in).bytes;
-        MCA_CUDA_TRY(cudaFuncSetAttribute(k12_fused_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        MCA_CUDA_TRY(ensure_smem(k12_fused_tc, smem));
         K12Args a{};
         a.n = n;
         a.heads = H;
@@ -772,35 +787,7 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
         const int grid = std::min(B * H, sm_count());   // persistent: one CTA per SM
         MCA_CUDA_TRY(launch_pdl(k12_fused_tc, dim3((unsigned)grid), dim3(k12::kThreads), smem, stream, tq, tk, a));
         MCA_LAUNCH_CHECK("k12_fused_tc");
-        if (MCA_K12_PROF) {   // diagnostics build: CTA 0's timeline
-            long long t[256];
-            MCA_CUDA_TRY(cudaStreamSynchronize(stream));
-            MCA_CUDA_TRY(cudaMemcpyFromSymbol(t, g_k12_prof, sizeof(t)));
-            const int nb = ((n + 127) / 128) * ((n + 127) / 128), ntq = (n + 127) / 128;
-            auto rel = [&](long long v) { return v ? v - t[0] : -1; };
-            fprintf(stderr, "k12 CTA0: A end");
-            for (int u = 0; u < 2 * nb && u < 39; ++u) fprintf(stderr, " %lld", rel(t[1 + u]));
-            fprintf(stderr, " | B end");
-            for (int u = 0; u < 2 * nb && u < 39; ++u) fprintf(stderr, " %lld", rel(t[40 + u]));
-            fprintf(stderr, " | Bdone %lld end %lld\n", rel(t[79]), rel(t[80]));
-            fprintf(stderr, "k12 CTA0 A issue/wait/ld0/ld1/end:");
-            for (int u = 0; u < 2 * nb && u < 32; ++u)
-                fprintf(stderr, " %lld/%lld/%lld/%lld/%lld", rel(t[192 + u]), rel(t[96 + u]), rel(t[128 + u]),
-                        rel(t[160 + u]), rel(t[1 + u]));
-            fprintf(stderr, " | lse");
-            for (int q = 0; q < 2 * ntq && q < 32; ++q) fprintf(stderr, " %lld", rel(t[224 + q]));
-            fprintf(stderr, "\n");
-            // every CTA: SM, start / end (ns from the first start), cycles
-            static unsigned long long c[4096][4];
-            const int nc = grid < 4096 ? grid : 4096;
-            MCA_CUDA_TRY(cudaMemcpyFromSymbol(c, g_k12_cta, sizeof(unsigned long long) * 4 * nc));
-            unsigned long long t0 = ~0ull;
-            for (int i = 0; i < nc; ++i) t0 = c[i][1] < t0 ? c[i][1] : t0;
-            fprintf(stderr, "k12 CTAS");
-            for (int i = 0; i < nc; ++i)
-                fprintf(stderr, " %llu:%llu:%llu:%llu", c[i][0], c[i][1] - t0, c[i][2] - t0, c[i][3]);
-            fprintf(stderr, "\n");
-        }
+        mca_diag::dump_k12(stream, n, grid);   // diagnostics builds only
     }
     // K1: row statistics + column maxima
     if (!fused12) {
@@ -817,14 +804,8 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
             if (!make_tmap_bf16(&tq, q, (uint64_t)H * kDh, n, B, 128) ||
                 !make_tmap_bf16(&tk, k, (uint64_t)H * kDh, n, B, 128))
                 return fail(MCA_ERR_CUDA, "cuTensorMapEncodeTiled failed for q/k");
-            static bool attr = false;
-            if (!attr) {
-                MCA_CUDA_TRY(cudaFuncSetAttribute(k1_scores_tc<kRowStats>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                  (int)k1tc::kSmemBytes));
-                MCA_CUDA_TRY(cudaFuncSetAttribute(k1_scores_tc<kColMax>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                  (int)k1tc::kSmemBytes));
-                attr = true;
-            }
+            MCA_CUDA_TRY(ensure_smem(k1_scores_tc<kRowStats>, k1tc::kSmemBytes));
+            MCA_CUDA_TRY(ensure_smem(k1_scores_tc<kColMax>, k1tc::kSmemBytes));
             const dim3 g1((n + 127) / 128, H, B);
             k1_scores_tc<kRowStats><<<g1, k1tc::kThreads, k1tc::kSmemBytes, stream>>>(
                 tq, tk, n, H, (float)scale, w->row_m, w->row_l, w->lse, w->colkey, w->colscore);
@@ -837,7 +818,7 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
     if (w->timing) MCA_CUDA_TRY(cudaEventRecord(w->ev[1], stream));
     // K2: Eq. 9 budgets
     {
-        const dim3 grid((n + 255) / 256, (unsigned)(B * H));
+        const dim3 grid = bh_grid((n + 255) / 256, (long)B * H);
         K2Args a{};
         a.colkey = w->colkey;
         a.cmax_in = dbg ? dbg->cmax_override : nullptr;
@@ -901,27 +882,13 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
             if (!make_tmap_bf16(&tk, k, (uint64_t)H * kDh, n, B, k4tc::kBK) ||
                 !make_tmap_bf16(&th, w->hbuf, (uint64_t)H * kDh, n, B, k4tc::kBK, CU_TENSOR_MAP_DATA_TYPE_FLOAT16))
                 return fail(MCA_ERR_CUDA, "cuTensorMapEncodeTiled failed for k/h");
-            static bool attr = false;
-            if (!attr) {
-                MCA_CUDA_TRY(cudaFuncSetAttribute(k4_apply_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                  (int)k4tc::kSmemBytes));
-                attr = true;
-            }
+            MCA_CUDA_TRY(ensure_smem(k4_apply_tc, k4tc::kSmemBytes));
             const long tiles = (long)B * H * ((n + k4tc::kBM - 1) / k4tc::kBM);
             const int grid = (int)std::min<long>(tiles, 2L * sm_count());   // persistent: two CTAs per SM
             MCA_CUDA_TRY(launch_pdl(k4_apply_tc, dim3(grid), dim3(k4tc::kThreads), k4tc::kSmemBytes, stream,
                                     (const __nv_bfloat16*)q, tk, th, (const float*)w->lse, n, H, B, (float)scale,
                                     (__nv_bfloat16*)y));
-            if (MCA_K4_PROF) {   // diagnostics build: the first CTA's softmax timeline
-                long long t[64];
-                MCA_CUDA_TRY(cudaStreamSynchronize(stream));
-                MCA_CUDA_TRY(cudaMemcpyFromSymbol(t, g_k4_prof, sizeof(t)));
-                fprintf(stderr, "k4 CTA0 (2nd tile): start->softmax %lld |", t[0] - t[60]);
-                for (int kb = 0; kb < (n + k4tc::kBK - 1) / k4tc::kBK && kb < 16; ++kb)
-                    fprintf(stderr, " kb%d S@%lld P@%lld done@%lld", kb, t[1 + 3 * kb] - t[60], t[2 + 3 * kb] - t[60],
-                            t[3 + 3 * kb] - t[60]);
-                fprintf(stderr, " | O@%lld end@%lld\n", t[50] - t[60], t[51] - t[60]);
-            }
+            mca_diag::dump_k4(stream, n, k4tc::kBK);   // diagnostics builds only
         }
         MCA_LAUNCH_CHECK("k4_apply");
     }
@@ -968,8 +935,8 @@ mca_status mca_forward_attn(mca_weights* w, const double* attn, const void* x, m
     int launches = 0;
     MCA_CUDA_TRY(cudaMemsetAsync(w->zeroed, 0, zeroed_bytes(H, w->d_in), stream));   // counters, cursors, histograms
     double* cmax = reinterpret_cast<double*>(w->colkey);                             // [B, H, n] scratch
-    const dim3 grid((n + 255) / 256, (unsigned)(B * H));
-    ka_colmax<<<grid, 256, 0, stream>>>(attn, n, cmax);
+    const dim3 grid = bh_grid((n + 255) / 256, (long)B * H);
+    ka_colmax<<<grid, 256, 0, stream>>>(attn, n, (long)B * H, cmax);
     MCA_LAUNCH_CHECK("ka_colmax");
     K2Args a{};
     a.cmax_in = cmax;
@@ -1023,38 +990,73 @@ mca_status mca_forward(mca_weights* w, const void* q, const void* k, const void*
                         (uint64_t)stream, 0, 0, (uint64_t)cfg->min_samples | ((uint64_t)cfg->mode << 32)};
     std::memcpy(&key[13], &cfg->alpha, 8);
     std::memcpy(&key[14], &cfg->scale, 8);
+    auto eager = [&]() {
+        return mca_forward_ex(w, q, k, x, dt, B, n, b_offset, layer, cfg, seed, y, budgets_out, exact_out, nullptr,
+                              nullptr, stream);
+    };
+    // the caller may itself be capturing this stream (e.g. torch CUDA graphs):
+    // then our kernels simply join its capture
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(stream, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+        cudaGetLastError();
+        return eager();
+    }
     mca_weights::GraphEntry* e = nullptr;
     for (auto& g : w->graphs)
         if (std::memcmp(g.key, key, sizeof(key)) == 0) e = &g;
+    if (e) e->last_use = ++w->graph_clock;
     if (e && e->exec) {
         MCA_CUDA_TRY(cudaGraphLaunch(e->exec, stream));
         return MCA_OK;
     }
     if (!e) {   // first sighting: eager (sizes the workspace), remembered
-        if (w->graphs.size() >= 64) {
-            if (w->graphs.front().exec) cudaGraphExecDestroy(w->graphs.front().exec);
-            w->graphs.erase(w->graphs.begin());
+        if (w->graphs.size() >= kMaxGraphs) {   // evict the least recently used key
+            auto lru = std::min_element(w->graphs.begin(), w->graphs.end(),
+                                        [](const auto& a, const auto& b) { return a.last_use < b.last_use; });
+            if (lru->exec) cudaGraphExecDestroy(lru->exec);
+            *lru = w->graphs.back();
+            w->graphs.pop_back();
         }
         w->graphs.push_back({});
         std::memcpy(w->graphs.back().key, key, sizeof(key));
-        return mca_forward_ex(w, q, k, x, dt, B, n, b_offset, layer, cfg, seed, y, budgets_out, exact_out, nullptr,
-                              nullptr, stream);
+        w->graphs.back().last_use = ++w->graph_clock;
+        return eager();
     }
-    // second sighting: capture this forward and replay it from now on
-    MCA_CUDA_TRY(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+    if (!e->graphable) return eager();
+    // second sighting: capture this forward and replay it from now on. A
+    // capture or instantiation failure marks the key eager-only and still
+    // runs the forward.
+    if (cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+        cudaGetLastError();
+        e->graphable = false;
+        return eager();
+    }
     const mca_status s = mca_forward_ex(w, q, k, x, dt, B, n, b_offset, layer, cfg, seed, y, budgets_out, exact_out,
                                         nullptr, nullptr, stream);
     cudaGraph_t graph = nullptr;
     const cudaError_t ce = cudaStreamEndCapture(stream, &graph);
-    if (s != MCA_OK) {
-        if (graph) cudaGraphDestroy(graph);
-        return s;
+    cudaGraphExec_t exec = nullptr;
+    const bool ok = s == MCA_OK && ce == cudaSuccess && graph && cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess;
+    if (graph) cudaGraphDestroy(graph);
+    cudaGetLastError();
+    // the forward may have grown the workspace (drop_graphs cleared the cache): re-find the entry
+    e = nullptr;
+    for (auto& g : w->graphs)
+        if (std::memcmp(g.key, key, sizeof(key)) == 0) e = &g;
+    if (!e) {
+        w->graphs.push_back({});
+        e = &w->graphs.back();
+        std::memcpy(e->key, key, sizeof(key));
     }
-    if (ce != cudaSuccess) return fail(MCA_ERR_CUDA, "capturing the forward failed: %s", cudaGetErrorString(ce));
-    const cudaError_t ie = cudaGraphInstantiate(&e->exec, graph, 0);
-    cudaGraphDestroy(graph);
-    if (ie != cudaSuccess) return fail(MCA_ERR_CUDA, "instantiating the forward graph failed: %s", cudaGetErrorString(ie));
-    MCA_CUDA_TRY(cudaGraphLaunch(e->exec, stream));
+    if (!ok) {
+        if (exec) cudaGraphExecDestroy(exec);
+        if (s != MCA_OK && ce == cudaSuccess) return s;    // an argument / launch error: report it
+        e->graphable = false;
+        return eager();
+    }
+    e->exec = exec;
+    e->last_use = ++w->graph_clock;
+    MCA_CUDA_TRY(cudaGraphLaunch(exec, stream));
     return MCA_OK;
 }
 

@@ -32,6 +32,10 @@ constexpr uint16_t kGuideRow = 0x3FFFu;     // row bits (d_in <= 16384)
 __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void griddep_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// (b, h) row index of the [B*H]-row grids: gridDim.y caps at 65535, so the
+// host splits B*H over (y, z) (bh_grid in mca_capi.cu); rows past B*H exit.
+__device__ __forceinline__ long grid_bh() { return (long)blockIdx.z * gridDim.y + blockIdx.y; }
+
 // ----------------------------------------------------------------- Philox
 __device__ __forceinline__ void philox4x32_10(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0,
                                               uint32_t k1, uint32_t out[4]) {

@@ -12,8 +12,13 @@ paper's "regular vs approximation mode" switch inside a BERT self-attention).
       exact because every softmax row sums to 1 (A (X W + b) = A X W + b).
       `.mode` switches between "approximation" and "regular".
 
-Forward only (the reference has no backward: SPEC.md:13). Weights prepared on
-first use and cached per (tensor version, dtype, device).
+Forward only (the reference has no backward: SPEC.md:13). Prepared weights
+(K0's sampling tables) are cached per W_V tensor: the cache entry holds a
+strong reference to the tensor, so its storage cannot be freed and its
+address reused by another W_V while the entry lives, and the key carries the
+tensor's version counter, so an in-place update rebuilds the tables.
+McaSelfAttention keeps its own transposed W_V, rebuilt when value.weight
+changes (new storage or in-place update).
 """
 from __future__ import annotations
 
@@ -26,12 +31,13 @@ _CACHE: dict = {}
 
 def _weights(w_v: torch.Tensor, heads: int) -> AttentionWeights:
     key = (w_v.data_ptr(), w_v._version, tuple(w_v.shape), w_v.dtype, w_v.device, heads)
-    wt = _CACHE.get(key)
-    if wt is None:
-        if len(_CACHE) > 64:
-            _CACHE.clear()
-        wt = AttentionWeights(w_v.contiguous(), heads=heads)
-        _CACHE[key] = wt
+    hit = _CACHE.get(key)
+    if hit is not None and hit[0] is w_v:
+        return hit[1]
+    if len(_CACHE) >= 64:
+        _CACHE.clear()
+    wt = AttentionWeights(w_v.contiguous(), heads=heads)
+    _CACHE[key] = (w_v, wt)          # the strong reference pins w_v's address while cached
     return wt
 
 
@@ -66,11 +72,21 @@ class McaSelfAttention(torch.nn.Module):
         self.key = torch.nn.Linear(hidden, hidden)
         self.value = torch.nn.Linear(hidden, hidden)
         self.seed, self.layer = 0, 0
+        self._wv = None           # [in, out] copy of value.weight in the activation dtype
+        self._wv_src = None       # (data_ptr, version, dtype, device) it was made from
+
+    def _w_v(self, dtype: torch.dtype) -> torch.Tensor:
+        p = self.value.weight
+        src = (p.data_ptr(), p._version, dtype, p.device)
+        if self._wv is None or self._wv_src != src:
+            self._wv = p.detach().t().contiguous().to(dtype)   # Linear stores [out, in]
+            self._wv_src = src
+        return self._wv
 
     def forward(self, hidden_states: torch.Tensor) -> torch.Tensor:
         q = self.query(hidden_states)
         k = self.key(hidden_states)
-        w_v = self.value.weight.t().contiguous().to(hidden_states.dtype)   # Linear stores [out, in]
+        w_v = self._w_v(hidden_states.dtype)
         y = torch.ops.mca_b200.attention(q, k, hidden_states, w_v, self.heads, float(self.alpha), int(self.seed),
                                          self.mode, int(self.layer))
         return y + self.value.bias.to(y.dtype)

@@ -16,10 +16,7 @@ static mca::Matrix read_matrix(std::ifstream& f) {
     int64_t r = 0, c = 0;
     f.read(reinterpret_cast<char*>(&r), 8);
     f.read(reinterpret_cast<char*>(&c), 8);
-    mca::Matrix m;
-    m.rows = static_cast<std::size_t>(r);
-    m.cols = static_cast<std::size_t>(c);
-    m.data.resize(m.rows * m.cols);
+    mca::Matrix m(static_cast<std::size_t>(r), static_cast<std::size_t>(c));   // matrix.hpp:20, from libmca_b200
     f.read(reinterpret_cast<char*>(m.data.data()), static_cast<std::streamsize>(m.data.size() * 8));
     return m;
 }
@@ -54,9 +51,7 @@ int main(int argc, char** argv) {
         }
         bool shape_error = false;
         try {
-            mca::Matrix wrong = x;
-            wrong.cols -= 1;
-            wrong.data.resize(wrong.rows * wrong.cols);
+            mca::Matrix wrong(x.rows, x.cols - 1);
             (void)mca::b200::mca_forward(q, k, wrong, weights, cfg, 1);
         } catch (const std::invalid_argument&) {
             shape_error = true;

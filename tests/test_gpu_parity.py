@@ -575,3 +575,32 @@ def test_graph_replay_matches_eager(mca, syn):
         mca.mca_forward(weights, q, k, x, cfg, seed=9, y=y, stream=stream)
         stream.synchronize()
         assert torch.equal(y, eager(q, k, x))
+
+
+def test_graph_replay_x_only_and_external_capture(mca, syn):
+    """The x-only forward (q, k projected on the device) replays bitwise too,
+    and a forward issued while the caller is itself capturing the stream
+    (torch.cuda.graph) joins that capture instead of starting its own: the
+    caller's graph replays to the eager result."""
+    H, n, d_in, B = 12, 128, 768, 2
+    pin = syn.make_projected_inputs(B, n, d_in, H, seed=5)
+    bf = torch.bfloat16
+    weights = mca.AttentionWeights(syn.make_weights(d_in, H).to(bf).cuda(), heads=H,
+                                   w_q=pin.w_q.to(bf).cuda(), w_k=pin.w_k.to(bf).cuda())
+    x = pin.x.to(bf).cuda()
+    cfg = mca.McaConfig(alpha=0.4)
+    stream = torch.cuda.Stream()
+    y = torch.empty((B, n, H * 64), dtype=bf, device="cuda")
+    ref = mca.mca_forward(weights, None, None, x, cfg, seed=4, debug=dict(draws_stride=0)).y.clone()
+    with torch.cuda.stream(stream):
+        for _ in range(4):                                       # eager, captured, replayed, replayed
+            mca.mca_forward(weights, None, None, x, cfg, seed=4, y=y, stream=stream)
+            stream.synchronize()
+            assert torch.equal(y, ref)
+    g = torch.cuda.CUDAGraph()
+    y2 = torch.empty_like(y)
+    with torch.cuda.graph(g):
+        mca.mca_forward(weights, None, None, x, cfg, seed=4, y=y2)
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(y2, ref)

@@ -73,3 +73,40 @@ def test_torch_op_approximation_mode_matches_forward():
     y_op = torch.ops.mca_b200.attention(q, k, x, w, H, 0.4, 11, "approximation", 2)
     y_fw = mca.mca_forward(mca.AttentionWeights(w, heads=H), q, k, x, mca.McaConfig(alpha=0.4), seed=11, layer=2).y
     assert torch.equal(y_op, y_fw)
+
+
+@pytest.mark.gpu
+def test_torch_module_stack_uses_each_layers_weights():
+    """Two McaSelfAttention layers with different value weights, and one layer
+    after an in-place weight update: each call uses its own current W_V (the
+    prepared-weight cache never serves another tensor's tables)."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2201_12854_b200.torch_op import McaSelfAttention
+    torch.manual_seed(1)
+    hs = torch.randn(1, 32, 768, device="cuda")
+
+    def dense(m):
+        q, k, v = m.query(hs), m.key(hs), m.value(hs)
+        sh = lambda t: t.view(1, 32, 12, 64).transpose(1, 2)   # noqa: E731
+        att = torch.softmax(sh(q) @ sh(k).transpose(-1, -2) / 8.0, dim=-1)
+        return (att @ sh(v)).transpose(1, 2).reshape(1, 32, 768)
+
+    layers = [McaSelfAttention(768, 12, mode="regular").cuda() for _ in range(2)]
+    with torch.no_grad():
+        for _ in range(2):                                     # repeated calls alternate between the layers
+            for m in layers:
+                ref = dense(m)
+                assert float((m(hs) - ref).norm() / ref.norm()) < 1e-5
+        layers[0].value.weight.mul_(-2.0)                      # in place: same storage, new version
+        ref = dense(layers[0])
+        assert float((layers[0](hs) - ref).norm() / ref.norm()) < 1e-5
+        w_a = torch.randn(768, 768, device="cuda") / 30        # functional op on temporaries of equal size
+        w_b = torch.randn(768, 768, device="cuda") / 30
+        q = torch.randn(1, 32, 768, device="cuda")
+        for w_v in (w_a, w_b):
+            y = torch.ops.mca_b200.attention(q, q, hs, w_v.clone(), 12, 1.0, 0, "regular", 0)
+            att = torch.softmax(q.view(1, 32, 12, 64).transpose(1, 2) @ q.view(1, 32, 12, 64).transpose(1, 2)
+                                .transpose(-1, -2) / 8.0, dim=-1)
+            ref = (att @ (hs @ w_v).view(1, 32, 12, 64).transpose(1, 2)).transpose(1, 2).reshape(1, 32, 768)
+            assert float((y - ref).norm() / ref.norm()) < 1e-5
