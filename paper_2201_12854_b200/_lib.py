@@ -45,7 +45,7 @@ EXPORTS = (
     "mca_prepare_weights", "mca_weights_free", "mca_weights_export", "mca_set_projections", "mca_reserve",
     "mca_forward", "mca_forward_ex", "mca_forward_attn",
     "mca_regular_forward", "mca_stage_budgets", "mca_set_timing", "mca_last_stage_ms", "mca_last_launch_count",
-    "mca_last_error", "mca_version",
+    "mca_device_alloc", "mca_device_free", "mca_copy", "mca_stream_sync", "mca_last_error", "mca_version",
 )
 
 
@@ -91,8 +91,14 @@ def lib() -> ctypes.CDLL:
     L.mca_last_stage_ms.restype = i32
     L.mca_last_launch_count.argtypes = [vp]
     L.mca_last_launch_count.restype = i32
+    L.mca_device_alloc.argtypes = [ctypes.c_size_t, ctypes.POINTER(vp)]
+    L.mca_device_free.argtypes = [vp]
+    L.mca_device_free.restype = None
+    L.mca_copy.argtypes = [vp, vp, ctypes.c_size_t, i32]
+    L.mca_stream_sync.argtypes = [vp]
     for name in ("mca_prepare_weights", "mca_weights_export", "mca_reserve", "mca_forward", "mca_forward_ex",
-                 "mca_forward_attn", "mca_regular_forward", "mca_stage_budgets", "mca_set_timing"):
+                 "mca_forward_attn", "mca_regular_forward", "mca_stage_budgets", "mca_set_timing", "mca_device_alloc",
+                 "mca_copy", "mca_stream_sync"):
         getattr(L, name).restype = i32
     _lib = L
     return L
