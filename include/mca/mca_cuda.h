@@ -87,6 +87,8 @@ typedef struct mca_flops {
     uint64_t exact_tokens;
     double reduction_factor;
     double total_reduction;
+    uint64_t certified;      /* token-heads whose Eq. 9 value sat within 1e-5 of an integer
+                                boundary and was re-derived in binary64 (k2c_certify) */
 } mca_flops;
 
 /* Optional stage outputs / overrides for parity testing (all device, [B,heads,n]

@@ -30,7 +30,8 @@ class McaConfigC(ctypes.Structure):
 class McaFlopsC(ctypes.Structure):
     _fields_ = [("exact_encoding", ctypes.c_uint64), ("approx_encoding", ctypes.c_uint64),
                 ("aggregation", ctypes.c_uint64), ("samples", ctypes.c_uint64), ("exact_tokens", ctypes.c_uint64),
-                ("reduction_factor", ctypes.c_double), ("total_reduction", ctypes.c_double)]
+                ("reduction_factor", ctypes.c_double), ("total_reduction", ctypes.c_double),
+                ("certified", ctypes.c_uint64)]
 
 
 class McaDebugC(ctypes.Structure):

@@ -113,11 +113,12 @@ class FlopsReport:
     exact_tokens: int
     reduction_factor: float
     total_reduction: float
+    certified: int = 0          # token-heads whose budget was re-derived in binary64 (k2c_certify)
 
     @classmethod
     def from_c(cls, f: L.McaFlopsC) -> "FlopsReport":
         return cls(f.exact_encoding, f.approx_encoding, f.aggregation, f.samples, f.exact_tokens,
-                   f.reduction_factor, f.total_reduction)
+                   f.reduction_factor, f.total_reduction, f.certified)
 
 
 class AttentionWeights:

@@ -38,6 +38,7 @@
 // warps per TMEM lane quadrant), warps 18-25 group B (two per quadrant, 64
 // columns each), warp 26 the TMA producer.
 // TMEM: A buffers [0,256), B buffers [256,512).
+#include "k2c_certify.cu"
 #include "mca_common.cuh"
 #include "tc_common.cuh"
 
@@ -99,6 +100,7 @@ struct K12Args {
     uint8_t* exact;
     unsigned long long* counters;      // [0] approx cost, [1] sampled draws, [2] exact token-heads
     unsigned int* hist;                // [H, d + 1] (nullable)
+    CertSink cert;                     // Eq. 9 values at an integer boundary: deferred to k2c_certify
 };
 
 // Persistent: one CTA per SM walks the items (b, h) = blockIdx.x, + gridDim.x, ...
@@ -382,6 +384,7 @@ __global__ void __maxnreg__(72)
                 // v = t - lse in the log2 domain, maximised over both query halves
                 const float vmax = fmaxf(combB[(kt * 2) * kT + r0], combB[(kt * 2 + 1) * kT + r0]);
                 const size_t t = rbase + j;
+                if (a.cert.row_done) a.cert.row_done[t] = 0;   // k2c's row-statistics cache
                 int r;
                 bool ex;
                 if (a.force_exact) {
@@ -395,6 +398,10 @@ __global__ void __maxnreg__(72)
                     const double cm = exp2((double)vmax);
                     if (a.cmax_out) a.cmax_out[t] = cm;
                     budget_for(cm, n, a.alpha, a.min_samples, a.d, &r, &ex);
+                    if (a.cert.list && eq9_ambiguous(cm, n, a.alpha, a.min_samples, a.d)) {
+                        cert_push(a.cert, (long long)t);   // k2c re-derives it in fp64 and accounts it
+                        continue;
+                    }
                 }
                 a.budgets[t] = r;
                 a.exact[t] = ex ? 1 : 0;

@@ -21,6 +21,7 @@
 // memory; k2_scan turns the histograms into descending-budget offsets and
 // k2_scatter writes each head's sampled-token list sorted by budget (largest
 // first: LPT order for K3) and its exact-token list (for K3b).
+#include "k2c_certify.cu"
 #include "mca_common.cuh"
 
 namespace mca_dev {
@@ -66,6 +67,7 @@ struct K2Args {
     double* cmax_out;
     unsigned long long* counters;      // [0] approx cost, [1] sampled draws, [2] exact token-heads
     unsigned int* hist;                // [H, d + 1]: bins 1..d-1 sampled budgets, bin d = exact (nullable)
+    CertSink cert;                     // Eq. 9 values at an integer boundary: deferred to k2c_certify
 };
 
 template <class T>
@@ -95,8 +97,10 @@ __global__ void __launch_bounds__(256) k2_budgets(K2Args a) {
     unsigned long long cost = 0, samples = 0, nexact = 0;
     if (j < a.row_len && bh * a.row_len < a.count) {
         const long t = bh * a.row_len + j;
+        if (a.cert.row_done) a.cert.row_done[t] = 0;   // k2c's row-statistics cache
         int r;
         bool ex;
+        bool deferred = false;
         if (a.force_exact) {
             r = a.d;
             ex = true;
@@ -127,23 +131,30 @@ __global__ void __launch_bounds__(256) k2_budgets(K2Args a) {
             }
             if (a.cmax_out) a.cmax_out[t] = cm;
             budget_for(cm, a.n, a.alpha, a.min_samples, a.d, &r, &ex);
+            if (a.cert.list && eq9_ambiguous(cm, a.n, a.alpha, a.min_samples, a.d)) {
+                cert_push(a.cert, (long long)t);   // k2c re-derives it in fp64 and accounts it
+                deferred = true;
+            }
         }
-        a.budgets[t] = r;
-        a.exact[t] = ex ? 1 : 0;
-        if (ex) {
-            cost = 2ull * (unsigned long long)a.d * (unsigned long long)a.dh;
-            nexact = 1;
-        } else {
-            cost = (unsigned long long)r * (2ull * a.dh + 3ull);
-            samples = (unsigned long long)r;
-        }
-        // sort bin: budgets above d - 1 only occur through budgets_override (tests)
-        const int bin = ex ? a.d : min(r, a.d - 1);
-        // warp-aggregated: lanes with the same bin add once (small budgets are common)
-        const unsigned peers = __match_any_sync(__activemask(), bin);
-        if ((threadIdx.x & 31) == __ffs(peers) - 1) {
-            if (use_hist) atomicAdd(&s_hist[bin], (unsigned)__popc(peers));
-            else if (a.hist) atomicAdd(&a.hist[(size_t)(bh % a.heads) * (a.d + 1) + bin], (unsigned)__popc(peers));
+        if (!deferred) {
+            a.budgets[t] = r;
+            a.exact[t] = ex ? 1 : 0;
+            if (ex) {
+                cost = 2ull * (unsigned long long)a.d * (unsigned long long)a.dh;
+                nexact = 1;
+            } else {
+                cost = (unsigned long long)r * (2ull * a.dh + 3ull);
+                samples = (unsigned long long)r;
+            }
+            // sort bin: budgets above d - 1 only occur through budgets_override (tests)
+            const int bin = ex ? a.d : min(r, a.d - 1);
+            // warp-aggregated: lanes with the same bin add once (small budgets are common)
+            const unsigned peers = __match_any_sync(__activemask(), bin);
+            if ((threadIdx.x & 31) == __ffs(peers) - 1) {
+                if (use_hist) atomicAdd(&s_hist[bin], (unsigned)__popc(peers));
+                else if (a.hist)
+                    atomicAdd(&a.hist[(size_t)(bh % a.heads) * (a.d + 1) + bin], (unsigned)__popc(peers));
+            }
         }
     }
     if (a.counters) {

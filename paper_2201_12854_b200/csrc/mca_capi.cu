@@ -77,6 +77,7 @@ mca_status fail(mca_status s, const char* fmt, ...) {
 
 size_t dtype_size(mca_dtype t) { return t == MCA_BF16 ? 2 : 4; }
 
+constexpr int kCertCounter = 6;                // counters[6]: number of k2c-flagged token-heads
 constexpr size_t kMaxGraphs = 256;              // captured forwards kept per handle (LRU)
 constexpr size_t kBlasWorkspace = 32u << 20;   // explicit cuBLAS workspace (capture-safe projection GEMM)
 
@@ -206,6 +207,8 @@ struct mca_weights {
     void* hbuf = nullptr;                     // [B, n, H*dh]
     int32_t* samp_list = nullptr;             // [H, B*n] sampled tokens per head, budget-descending
     int32_t* exact_list = nullptr;            // [H, B*n] exact tokens per head
+    long long* cert_list = nullptr;           // [B, H, n] Eq. 9 values at an integer boundary (k2c_certify)
+    uint8_t* row_done = nullptr;              // [B, H, n] k2c's exact row-statistics cache flags
     void* zeroed = nullptr;                   // counters | task_cursor | hist | fill (zeroed once per forward)
     unsigned int* fill = nullptr;             // [H, d + 1] per-bin list fill counters (k2_scan_scatter)
     unsigned long long* counters = nullptr;   // [8]
@@ -245,6 +248,10 @@ void free_workspace(mca_weights* w) {
     cudaFree(w->hbuf);
     cudaFree(w->samp_list);
     cudaFree(w->exact_list);
+    cudaFree(w->cert_list);
+    cudaFree(w->row_done);
+    w->cert_list = nullptr;
+    w->row_done = nullptr;
     w->samp_list = nullptr;
     w->exact_list = nullptr;
     w->lse = nullptr;
@@ -280,7 +287,9 @@ mca_status ensure_workspace(mca_weights* w, long tokens, mca_stream_t stream) {
         cudaMalloc(&w->exact, th * sizeof(uint8_t)) != cudaSuccess ||
         cudaMalloc(&w->hbuf, th * w->dh * dtype_size(w->wdt)) != cudaSuccess ||
         cudaMalloc(&w->samp_list, th * sizeof(int32_t)) != cudaSuccess ||
-        cudaMalloc(&w->exact_list, th * sizeof(int32_t)) != cudaSuccess) {
+        cudaMalloc(&w->exact_list, th * sizeof(int32_t)) != cudaSuccess ||
+        cudaMalloc(&w->cert_list, th * sizeof(long long)) != cudaSuccess ||
+        cudaMalloc(&w->row_done, th * sizeof(uint8_t)) != cudaSuccess) {
         cudaGetLastError();
         free_workspace(w);
         return fail(MCA_ERR_ALLOC, "workspace allocation for %ld tokens failed", tokens);
@@ -471,6 +480,7 @@ mca_status read_flops(mca_weights* w, int B, int n, bool approx, mca_flops* out,
     out->aggregation = (uint64_t)B * w->heads * 2ull * n * n * w->dh;
     out->samples = c[3];
     out->exact_tokens = c[2];
+    out->certified = c[kCertCounter];
     out->reduction_factor = (double)out->exact_encoding / (double)out->approx_encoding;
     out->total_reduction = (double)(out->exact_encoding + out->aggregation) /
                            (double)(out->approx_encoding + out->aggregation);
@@ -751,6 +761,15 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
         MCA_CUDA_TRY(cudaMemsetAsync(w->colkey, 0, th * sizeof(unsigned long long), stream));
     MCA_CUDA_TRY(cudaMemsetAsync(w->zeroed, 0, zeroed_bytes(H, w->d_in), stream));   // counters, cursors, histograms
     const bool tile_k3 = dt == MCA_BF16 && use_k3t(w);   // k3t reads budgets directly: no work lists
+    // bf16 score passes: Eq. 9 values within kCertTau of an integer boundary are
+    // re-derived in binary64 by k2c_certify (the fp32 path's scores are fp64 already)
+    const bool certify = dt == MCA_BF16 && approx && !(dbg && (dbg->budgets_override || dbg->cmax_override));
+    CertSink cert{};
+    if (certify) {
+        cert.list = w->cert_list;
+        cert.count = w->counters + kCertCounter;
+        cert.row_done = w->row_done;
+    }
 
 
     // K1 + K2 fused (bf16, n <= 768): both score passes and Eq. 9 in one kernel per (b, h)
@@ -783,6 +802,7 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
         a.exact = w->exact;
         a.counters = w->counters;
         a.hist = tile_k3 ? nullptr : w->hist;
+        a.cert = cert;
         a.items = B * H;
         const int grid = std::min(B * H, sm_count());   // persistent: one CTA per SM
         MCA_CUDA_TRY(launch_pdl(k12_fused_tc, dim3((unsigned)grid), dim3(k12::kThreads), smem, stream, tq, tk, a));
@@ -844,11 +864,36 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
         a.cmax_out = dbg ? dbg->cmax_out : nullptr;
         a.counters = w->counters;
         a.hist = tile_k3 ? nullptr : w->hist;
+        a.cert = cert;
         if (!fused12) {
             if (a.cmax_in) k2_budgets<kGivenCmax, float><<<grid, 256, 0, stream>>>(a);
             else if (dt == MCA_F32) k2_budgets<kKeyValue, float><<<grid, 256, 0, stream>>>(a);
             else k2_budgets<kKeyArgmax, __nv_bfloat16><<<grid, 256, 0, stream>>>(a);
             MCA_LAUNCH_CHECK("k2_budgets");
+        }
+        if (certify) {   // the flagged token-heads' budgets, FLOP counts and histogram entries
+            K2cArgs c{};
+            c.q = q;
+            c.k = k;
+            c.lse = w->lse;
+            c.scale = scale;
+            c.n = n;
+            c.heads = H;
+            c.d = w->d_in;
+            c.dh = w->dh;
+            c.min_samples = cfg->min_samples;
+            c.alpha = cfg->alpha;
+            c.cert = cert;
+            c.row_m = w->row_m;
+            c.row_l = w->row_l;
+            c.budgets = w->budgets;
+            c.exact = w->exact;
+            c.cmax_out = dbg ? dbg->cmax_out : nullptr;
+            c.counters = w->counters;
+            c.hist = tile_k3 ? nullptr : w->hist;
+            MCA_CUDA_TRY(launch_pdl(k2c_certify<__nv_bfloat16>, dim3((unsigned)sm_count()), dim3(kCertWarps * 32), 0,
+                                    stream, c));
+            MCA_LAUNCH_CHECK("k2c_certify");
         }
         if (!tile_k3) {
             if (mca_status s = launch_lists(w, grid, n, tokens, stream, launches)) return s;

@@ -26,7 +26,7 @@ METRICS = [
 ]
 UNIT = {"second": 1.0, "s": 1.0, "msecond": 1e-3, "ms": 1e-3, "usecond": 1e-6, "us": 1e-6, "nsecond": 1e-9, "ns": 1e-9, "byte": 1.0, "Kbyte": 1e3,
         "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "inst": 1.0, "Kinst": 1e3, "Minst": 1e6, "Ginst": 1e9}
-STAGE = {"k12_fused_tc": "score", "k1_scores_tc": "score", "k2_budgets": "budgets", "k2_scan": "budgets", "k2_scatter": "budgets", "k3_encode_sampled": "encode", "k3t_encode_tc": "encode",
+STAGE = {"k2c_certify": "budgets", "kp_project_tc": "projection", "k12_fused_tc": "score", "k1_scores_tc": "score", "k2_budgets": "budgets", "k2_scan": "budgets", "k2_scatter": "budgets", "k3_encode_sampled": "encode", "k3t_encode_tc": "encode",
          "k3b_exact_tc": "encode_exact", "k4_apply_tc": "apply"}
 
 
@@ -39,6 +39,7 @@ def main(rep, md_out, traffic_out):
     col = {m: hdr.index(m) for m, _, _ in METRICS if m in hdr}
     lines = ["| kernel | " + " | ".join(t for _, t, _ in METRICS) + " |", "|---" * (len(METRICS) + 1) + "|"]
     traffic = {}
+    per_kernel = {}
     for r in rows[2:]:   # row 1 holds units
         if len(r) <= name_i:
             continue
@@ -58,7 +59,12 @@ def main(rep, md_out, traffic_out):
         stage = next((v for k, v in STAGE.items() if base.startswith(k)), None)
         if stage and "dram__bytes_read.sum" in col:
             b = si("dram__bytes_read.sum") + si("dram__bytes_write.sum")
-            traffic[stage] = traffic.get(stage, 0.0) + b
+            tot, cnt = per_kernel.get((stage, base), (0.0, 0))
+            per_kernel[(stage, base)] = (tot + b, cnt + 1)
+    # per launch: a kernel captured several times (one per profiled step) is
+    # averaged over its launches, then a stage sums its distinct kernels
+    for (stage, _), (tot, cnt) in per_kernel.items():
+        traffic[stage] = traffic.get(stage, 0.0) + tot / cnt
     with open(md_out, "w") as f:
         f.write("# ncu --set full summary (C2 bf16, one launch of each kernel of one step; cold-cache, serialised)\n\n")
         f.write(f"Source: `{rep.split('/')[-1]}` from scripts/profile_round.sh.\n\n")

@@ -1,0 +1,179 @@
+"""GPU parity at the shapes of BASELINE.json configs[2] (C3, BERT-large
+24-layer stack) and configs[3] (C4, n = 4096), against the fp64 oracle.
+
+C4: one whole n = 4096 sequence (all 12 heads): the tiled score pass (K1a / K1b
++ K2, n > 768), Eq. 9 bitwise on the device's column maxima, every draw of a
+sample of token-heads bitwise, y on the full sequence against the oracle run
+with the device's plan, and the end-to-end budgets against the oracle's own
+plan: zero mismatches (the token-heads at integer boundaries of raw are
+re-derived in binary64 by k2c_certify).
+
+C3: d_in = 1024, 16 heads, n = 512, a chained stack X_{l+1} = Y_l where every
+layer re-projects q = X_l W_q^l, k = X_l W_k^l on the device
+with its own W_V^l, W_q^l, W_k^l and Philox layer word l. Each
+layer is checked against the oracle chained the same way: the oracle layer l
+takes the device's X_l (the previous layer's rounded output) and the device's
+projections of it (which are themselves checked against fp64 X_l W^l).
+"""
+import numpy as np
+import pytest
+
+from parity_util import budget_mismatch_report, row_rel
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+ALPHA = 0.4
+TOL_Y_BF16 = 2e-2
+TOL_H_BF16 = 1e-2
+TOL_PROJ_BF16 = 8e-3        # bf16 output rounding of q = x W (2^-8 relative per element, worst row)
+CMAX_REL_BF16 = 1e-5
+
+
+@pytest.fixture(scope="module")
+def mca():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2201_12854_b200 as m
+    return m
+
+
+@pytest.fixture(scope="module")
+def syn():
+    from paper_2201_12854_b200 import synthetic
+    return synthetic
+
+
+def _np(t):
+    return t.detach().float().cpu().double().numpy()
+
+
+def _check_layer(orc, w, q, k, x, H, n, d_in, out, dbg, seed, b_offset, layer, label):
+    """Stage-isolated Eq. 9, y with the device's plan, H~, draws, and the
+    end-to-end mismatch report for one layer's forward."""
+    b = out.budgets.cpu().numpy()
+    e = out.exact_mask.cpu().numpy().astype(bool)
+    cm = dbg["cmax_out"].cpu().numpy()
+    rb, re = orc.sample_budgets_from_cmax(cm, n, ALPHA, 1, d_in)
+    assert np.array_equal(b, rb) and np.array_equal(e, re), label
+    qn, kn, xn, wn = _np(q), _np(k), _np(x), _np(w)
+    ref = orc.batched_forward(qn, kn, xn, wn, heads=H, alpha=ALPHA, seed=seed, b_offset=b_offset, layer=layer,
+                              budgets_override=b, exact_override=e)
+    assert row_rel(_np(out.y), ref.y) <= TOL_Y_BF16, label
+    assert row_rel(dbg["h_out"].double().cpu().numpy(), ref.h) <= TOL_H_BF16, label
+    full = orc.batched_forward(qn, kn, xn, wn, heads=H, alpha=ALPHA, seed=seed, want_h=False)
+    cm_rel = float(np.abs(cm / full.cmax - 1.0).max())
+    rep = budget_mismatch_report(b, e, full.budgets, full.exact, full.cmax, n, ALPHA)
+    print(f"{label}: cmax max rel {cm_rel:.2e}; budget mismatches vs the fp64 oracle {rep}; "
+          f"sampled {int((~e).sum())} exact {int(e.sum())}")
+    assert cm_rel <= CMAX_REL_BF16, (label, cm_rel)
+    assert rep["count"] == 0, (label, rep)
+    # draws of a sample of sampled token-heads, bitwise (first 64 of each)
+    draws = dbg["draws_out"].cpu().numpy()
+    rng = np.random.default_rng(layer + 17)
+    Bq = b.shape[0]
+    checked = 0
+    dists = {}
+    for _ in range(300):
+        bb, h, j = int(rng.integers(Bq)), int(rng.integers(H)), int(rng.integers(n))
+        if e[bb, h, j]:
+            assert np.all(draws[bb, h, j] == -1)
+            continue
+        if h not in dists:
+            dists[h] = orc.weight_probs(wn[:, h * 64:(h + 1) * 64])
+        r = min(int(b[bb, h, j]), 64)
+        idx = orc.draw_indices(dists[h], r, seed, ((b_offset + bb) * H + h) * n + j, layer)
+        assert np.array_equal(draws[bb, h, j, :r], idx), (label, bb, h, j)
+        checked += 1
+    assert checked > 100
+    return b, e
+
+
+def test_c4_long_sequence_parity(mca, syn, orc):
+    """BASELINE.json configs[3] shape: n = 4096, d = 768, 12 heads, bf16, one
+    whole sequence (the oracle's cost bounds the batch, not the kernels)."""
+    B, n, d_in, H = 1, 4096, 768, 12
+    bf = torch.bfloat16
+    w = syn.make_weights(d_in, H, seed=404).to(bf)
+    inp = syn.make_inputs(B, n, d_in, H, seed=404)
+    q, k, x = (t.to(bf).cuda() for t in (inp.q, inp.k, inp.x))
+    weights = mca.AttentionWeights(w.cuda(), heads=H)
+    dbg = dict(cmax_out=torch.zeros((B, H, n), dtype=torch.float64, device="cuda"),
+               h_out=torch.zeros((B, n, H * 64), dtype=torch.float16, device="cuda"),
+               draws_out=torch.zeros((B, H, n, 64), dtype=torch.int32, device="cuda"), draws_stride=64)
+    b_offset = 5                                      # a shard of a larger batch: stream ids use b + 5
+    out = mca.mca_forward(weights, q, k, x, mca.McaConfig(alpha=ALPHA), seed=42, b_offset=b_offset,
+                          return_plan=True, flops=True, debug=dbg)
+    torch.cuda.synchronize()
+    b, e = _check_layer(orc, w, q, k, x, H, n, d_in, out, dbg, 42, b_offset, 0, "C4 n=4096")
+    assert out.flops.samples == int(b[~e].sum())
+    # the sample-count imbalance C4 is meant to stress is present
+    r = b[~e]
+    assert np.percentile(r, 99) > 4 * np.percentile(r, 50)
+
+
+def test_c3_chained_stack_parity(mca, syn, orc):
+    """BASELINE.json configs[2] shape: BERT-large (d_in = 1024, 16 heads of
+    64), n = 512, B = 2 sequences, 3 chained layers; every layer projects its
+    own q, k from the previous layer's output on the device."""
+    B, n, d_in, H, L = 2, 512, 1024, 16, 3
+    bf = torch.bfloat16
+    pin0 = syn.make_projected_inputs(B, n, d_in, H, seed=300)
+    layers = []
+    for l in range(L):
+        pin = syn.make_projected_inputs(1, 1, d_in, H, seed=300 + l)
+        w_v = syn.make_weights(d_in, H, seed=1234 + l).to(bf)
+        layers.append((w_v, pin.w_q.to(bf), pin.w_k.to(bf)))
+    x = pin0.x.to(bf).cuda()
+    cfg = mca.McaConfig(alpha=ALPHA)
+    b_offset = 2                                      # rank 1 of a 2-way shard of B = 4
+    for l, (w_v, w_q, w_k) in enumerate(layers):
+        weights = mca.AttentionWeights(w_v.cuda(), heads=H, w_q=w_q.cuda(), w_k=w_k.cuda())
+        dbg = dict(cmax_out=torch.zeros((B, H, n), dtype=torch.float64, device="cuda"),
+                   h_out=torch.zeros((B, n, H * 64), dtype=torch.float16, device="cuda"),
+                   draws_out=torch.zeros((B, H, n, 64), dtype=torch.int32, device="cuda"), draws_stride=64,
+                   q_out=torch.empty((B, n, H * 64), dtype=bf, device="cuda"),
+                   k_out=torch.empty((B, n, H * 64), dtype=bf, device="cuda"))
+        out = mca.mca_forward(weights, None, None, x, cfg, seed=42, b_offset=b_offset, layer=l, return_plan=True,
+                              debug=dbg)
+        torch.cuda.synchronize()
+        xd = x.double().cpu()
+        for got, wm in ((dbg["q_out"], w_q), (dbg["k_out"], w_k)):
+            assert row_rel(_np(got), (xd @ wm.double()).numpy()) <= TOL_PROJ_BF16, l
+        _check_layer(orc, w_v, dbg["q_out"], dbg["k_out"], x, H, n, d_in, out, dbg, 42, b_offset, l,
+                     f"C3 layer {l}")
+        assert torch.isfinite(out.y.float()).all()
+        x = out.y                                     # X_{l+1} = Y_l
+
+
+@pytest.mark.parametrize("n", [256, 2048])
+def test_certified_budgets_on_tied_attention(mca, syn, orc, n):
+    """Degenerate input for the boundary certification: q = 0 makes every
+    attention row uniform, so every column maximum is 1/n, raw = 1 sits
+    exactly on an integer for alpha = 1 (every token-head is flagged) and every
+    query ties for every column's maximum. The budgets must still be the
+    SPEC's r = 1 everywhere, and half-tied columns (two equal
+    query rows) must match the oracle."""
+    H, d_in = 12, 768
+    bf = torch.bfloat16
+    w = syn.make_weights(d_in, H, seed=n).to(bf)
+    inp = syn.make_inputs(1, n, d_in, H, seed=n)
+    q, k, x = (t.to(bf).cuda() for t in (inp.q, inp.k, inp.x))
+    weights = mca.AttentionWeights(w.cuda(), heads=H)
+    qz = torch.zeros_like(q)
+    out = mca.mca_forward(weights, qz, k, x, mca.McaConfig(alpha=1.0), seed=1, return_plan=True, flops=True)
+    torch.cuda.synchronize()
+    assert bool((out.budgets == 1).all()) and not bool(out.exact_mask.bool().any())
+    assert out.flops.samples == H * n
+    # duplicated query rows: every column's maximum is attained twice
+    q2 = q.clone()
+    q2[:, 1::2] = q2[:, 0::2]
+    cm = torch.zeros((1, H, n), dtype=torch.float64, device="cuda")
+    out2 = mca.mca_forward(weights, q2, k, x, mca.McaConfig(alpha=ALPHA), seed=1, return_plan=True,
+                           debug=dict(cmax_out=cm))
+    torch.cuda.synchronize()
+    full = orc.batched_forward(_np(q2), _np(k), _np(x), _np(w), heads=H, alpha=ALPHA, seed=1, want_h=False)
+    rep = budget_mismatch_report(out2.budgets.cpu().numpy(), out2.exact_mask.cpu().numpy(), full.budgets, full.exact,
+                                 full.cmax, n, ALPHA)
+    assert rep["count"] == 0, rep

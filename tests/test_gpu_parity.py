@@ -17,6 +17,7 @@ import os
 
 import numpy as np
 import pytest
+from parity_util import budget_mismatch_report
 
 torch = pytest.importorskip("torch")
 
@@ -25,6 +26,12 @@ pytestmark = pytest.mark.gpu
 GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
 TOL_H = {torch.float32: 1e-5, torch.bfloat16: 1e-2}
 TOL_Y = {torch.float32: 1e-5, torch.bfloat16: 2e-2}
+# bf16 end to end vs the fp64 oracle on the same (bf16) q, k: the tensor-core
+# scores (fp32 accumulation) move a column maximum by <= ~2e-6 relative; the
+# token-heads whose raw = (n cmax / alpha)^2 lies within 1e-5 of an integer are
+# re-derived in binary64 (k2c_certify), so the budgets must equal the oracle's
+# end to end: zero mismatches
+CMAX_REL_BF16 = 1e-5
 
 
 @pytest.fixture(scope="module")
@@ -247,8 +254,12 @@ def test_bf16_parity(mca, syn, orc, B, n, H, d_in):
     # tensor-core scores move cmax by ~1e-6 relative, so budgets may differ
     # only where raw sits at an integer boundary
     ref0 = _oracle(orc, w, q, k, x, H, alpha=0.4, seed=42)
-    assert np.abs(dbg["cmax_out"].cpu().numpy() / ref0.cmax - 1.0).max() <= 1e-4
-    assert np.mean(b != ref0.budgets) <= 0.01
+    cm_rel = float(np.abs(dbg["cmax_out"].cpu().numpy() / ref0.cmax - 1.0).max())
+    assert cm_rel <= CMAX_REL_BF16, cm_rel
+    rep = budget_mismatch_report(b, e, ref0.budgets, ref0.exact, ref0.cmax, n, 0.4)
+    print(f"bf16 B={B} n={n} H={H} d_in={d_in}: cmax max rel {cm_rel:.2e}; budget mismatches vs the fp64 "
+          f"oracle {rep}")
+    assert rep["count"] == 0, rep
     # (4)/(5) with the GPU's plan
     ref = _oracle(orc, w, q, k, x, H, alpha=0.4, seed=42, budgets_override=b, exact_override=e)
     assert _row_rel(_np(dbg["h_out"]), ref.h) <= TOL_H[torch.bfloat16]
@@ -265,11 +276,6 @@ def test_bf16_parity(mca, syn, orc, B, n, H, d_in):
         ref_idx = orc.draw_indices(orc.weight_probs(wn[:, h * 64:(h + 1) * 64]), min(r, 64), 42,
                                    (bb * H + h) * n + j, 0)
         assert np.array_equal(draws[bb, h, j, :min(r, 64)], ref_idx)
-    # end-to-end budget agreement with the fp64 oracle is reported, not required (bf16 scores)
-    full = _oracle(orc, w, q, k, x, H, alpha=0.4, seed=42)
-    mism = int((full.budgets != b).sum())
-    print(f"bf16 B={B} n={n}: {mism} / {b.size} budgets differ from the fp64 oracle end to end")
-    assert mism <= max(5, b.size // 100)
 
 
 # -------------------------------------------------------------- properties
@@ -369,7 +375,7 @@ def test_theorem1_bound_on_gpu(mca, syn):
 
 def test_c2_full_size_properties(mca, syn, orc):
     """BASELINE.json configs[1] at full size (B=64, n=512, bf16): Eq. 9 parity
-    on all 393,216 token-heads, the FLOP counter, and oracle parity on two
+    on all 393,216 token-heads, the FLOP counter, and oracle parity on eight
     whole sequences (size-independent checks plus a sampled full check)."""
     H, n, d_in, B = 12, 512, 768, 64
     weights, w, q, k, x = _setup(mca, syn, B, n, d_in, H, torch.bfloat16)
@@ -382,11 +388,22 @@ def test_c2_full_size_properties(mca, syn, orc):
     assert np.array_equal(b, rb) and np.array_equal(e, re)
     assert out.flops.samples == int(b[~e].sum())
     assert torch.isfinite(out.y.float()).all()
-    for s in (0, 37):
+    # 8 whole sequences (first, last and six in between): y with the device's
+    # plan, and the end-to-end budgets against the fp64 oracle's own plan
+    seqs = [0, 9, 18, 27, 37, 45, 54, 63]
+    idx = np.array(seqs)
+    qs, ks, xs = (_np(t[idx]) for t in (q, k, x))
+    for i, s in enumerate(seqs):
         sl = slice(s, s + 1)
-        ref = orc.batched_forward(_np(q[sl]), _np(k[sl]), _np(x[sl]), _np(w), heads=H, alpha=0.4, seed=42,
+        ref = orc.batched_forward(qs[i:i + 1], ks[i:i + 1], xs[i:i + 1], _np(w), heads=H, alpha=0.4, seed=42,
                                   b_offset=s, budgets_override=b[sl], exact_override=e[sl])
-        assert _row_rel(_np(out.y[sl]), ref.y) <= TOL_Y[torch.bfloat16]
+        assert _row_rel(_np(out.y[sl]), ref.y) <= TOL_Y[torch.bfloat16], s
+    full = orc.batched_forward(qs, ks, xs, _np(w), heads=H, alpha=0.4, seed=42, want_h=False)
+    cm_rel = float(np.abs(cm[idx].cpu().numpy() / full.cmax - 1.0).max())
+    rep = budget_mismatch_report(b[idx], e[idx], full.budgets, full.exact, full.cmax, n, 0.4)
+    print(f"C2 8 sequences: cmax max rel {cm_rel:.2e}; budget mismatches vs the fp64 oracle {rep}")
+    assert cm_rel <= CMAX_REL_BF16
+    assert rep["count"] == 0, rep
 
 
 def test_bf16_tile_encoder_parity_subprocess():
@@ -537,7 +554,7 @@ def test_fused_kernel_multi_item_per_cta(mca, syn, orc, n):
                                   b_offset=s, budgets_override=b[sl], exact_override=e[sl])
         ref0 = orc.batched_forward(_np(q[sl]), _np(k[sl]), _np(x[sl]), _np(w), heads=H, alpha=0.4, seed=5,
                                    b_offset=s)
-        assert np.abs(cm[sl].cpu().numpy() / ref0.cmax - 1.0).max() <= 1e-4
+        assert np.abs(cm[sl].cpu().numpy() / ref0.cmax - 1.0).max() <= CMAX_REL_BF16
         assert _row_rel(_np(out.y[sl]), ref.y) <= TOL_Y[torch.bfloat16]
 
 
