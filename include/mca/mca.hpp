@@ -41,7 +41,10 @@ struct McaConfig {
     Mode mode = Mode::approximation;
     int min_samples = 1;
     double scale = 0.0;  // <= 0: 1/sqrt(d_h)
-    mca_config c() const { return mca_config{alpha, scale, min_samples, static_cast<int32_t>(mode)}; }
+    bool certify = false;  // bf16: boundary Eq. 9 values re-derived in binary64 (mca_config.certify)
+    mca_config c() const {
+        return mca_config{alpha, scale, min_samples, static_cast<int32_t>(mode), certify ? 1 : 0, 0};
+    }
 };
 
 struct FlopsReport {

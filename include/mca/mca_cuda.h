@@ -74,6 +74,10 @@ typedef struct mca_config {
     double scale;        /* softmax scale a                                */
     int32_t min_samples; /* budget floor (default 1)                       */
     int32_t mode;        /* mca_mode                                       */
+    int32_t certify;     /* bf16: re-derive in binary64 every Eq. 9 value within 1e-5 of
+                            an integer boundary (k2c_certify), so the budgets equal the
+                            fp64 reference's end to end; 0 = off     */
+    int32_t reserved;
 } mca_config;
 
 /* FlopsReport, summed over heads and batch. `samples` is

@@ -24,7 +24,7 @@ MCA_MODE_REGULAR, MCA_MODE_APPROX = 0, 1
 
 class McaConfigC(ctypes.Structure):
     _fields_ = [("alpha", ctypes.c_double), ("scale", ctypes.c_double), ("min_samples", ctypes.c_int32),
-                ("mode", ctypes.c_int32)]
+                ("mode", ctypes.c_int32), ("certify", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
 
 class McaFlopsC(ctypes.Structure):

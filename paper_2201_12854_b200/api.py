@@ -91,17 +91,22 @@ def _need_cuda(name: str, t: torch.Tensor) -> None:
 
 @dataclass
 class McaConfig:
-    """SPEC.md:267-271. scale <= 0 selects 1/sqrt(d_h)."""
+    """SPEC.md:267-271. scale <= 0 selects 1/sqrt(d_h).
+    certify (bf16): Eq. 9 values within 1e-5 of an integer boundary are
+    re-derived in binary64, so the budgets equal the fp64 reference's end to
+    end instead of differing at integer boundaries."""
     alpha: float = 0.4
     mode: str = "approximation"
     min_samples: int = 1
     scale: float = 0.0
+    certify: bool = False
 
     def to_c(self) -> L.McaConfigC:
         if self.mode not in ("approximation", "regular"):
             raise ConfigError(f"unknown mode {self.mode!r}")
         return L.McaConfigC(float(self.alpha), float(self.scale), int(self.min_samples),
-                            L.MCA_MODE_APPROX if self.mode == "approximation" else L.MCA_MODE_REGULAR)
+                            L.MCA_MODE_APPROX if self.mode == "approximation" else L.MCA_MODE_REGULAR,
+                            1 if self.certify else 0, 0)
 
 
 @dataclass

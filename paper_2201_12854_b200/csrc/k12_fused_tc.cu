@@ -399,7 +399,7 @@ __global__ void __maxnreg__(72)
                     if (a.cmax_out) a.cmax_out[t] = cm;
                     budget_for(cm, n, a.alpha, a.min_samples, a.d, &r, &ex);
                     if (a.cert.list && eq9_ambiguous(cm, n, a.alpha, a.min_samples, a.d)) {
-                        cert_push(a.cert, (long long)t);   // k2c re-derives it in fp64 and accounts it
+                        cert_push(a.cert, (long long)t, cm);   // k2c re-derives it in fp64 and accounts it
                         continue;
                     }
                 }

@@ -11,24 +11,26 @@
 //
 // The budget pass therefore flags every token-head whose raw value is within
 // kCertTau (relative) of an integer boundary that changes (r, exact) and
-// defers it here (eq9_ambiguous / cert_push). For each flagged key j this
-// kernel re-derives cmax_j in binary64 the way the oracle does
-// (oracle/tensor.cpp softmax_rows, col_max):
-//   1. every query's t_ij in fp64 (bf16 products and their sums are exact in
-//      binary64, so t_ij is the oracle's t_ij bit for bit), and
-//      v_i = t_ij - lse_i with the score pass's fp32 lse;
-//   2. the candidate rows: v_i within the lse error of max_i v_i;
-//   3. each candidate's exact row statistics m_i = max_j' t_ij',
-//      l_i = sum_j' exp(t_ij' - m_i) (cached per row for the forward: the
-//      budget pass clears row_done[], the first warp to need a row fills it);
-//   4. cmax_j = max over the candidates of exp(t_ij - m_i) / l_i, then Eq. 9,
-//      the FLOP counters and the budget histogram the work lists are built from.
-// What remains between device and oracle is the order of the l_i summation
-// and exp's last ulp: ~1e-15 relative, so budgets equal the fp64 oracle's
-// end to end (tests/test_gpu_configs.py, tests/test_gpu_parity.py).
-//
-// One warp per flagged key; the grid is persistent and reads the flag count
-// after griddep_wait (the count is only known on the device).
+// defers it here (eq9_ambiguous / cert_push, with the pass's own cmax). This
+// kernel re-derives those column maxima in binary64 the way the oracle does
+// (oracle/tensor.cpp softmax_rows, col_max). One CTA per (b, h) item with
+// flagged keys, all of the item's flagged keys at once:
+//   1. the item's flagged keys (read from the flag list) and their k rows;
+//   2. one pass over the queries: v_if = t_if - lse_i (fp32 dot, fp32 lse)
+//      against every flagged key f; the candidates are the (f, i) with v_if
+//      within the fp32 error of ln(cmax_f) (the pass's maximum), and for them
+//      t_if in binary64 (bf16 products and their sums are exact in binary64,
+//      so t_if is the oracle's value bit for bit);
+//   3. each candidate row's exact statistics, one pass over the keys with one
+//      exp per entry against the score pass's row max m~_i:
+//      L_i = sum_j' exp(t_ij' - m~_i) in binary64 (cached per row for the
+//      forward: the budget pass clears row_done[], the first CTA fills it);
+//   4. cmax_f = max over its candidates of exp(t_if - m~_i) / L_i (the
+//      oracle's exp(t - m) / l with both terms scaled by exp(m - m~)), Eq. 9,
+//      the FLOP counters and the budget histogram the work lists read.
+// What remains between device and oracle is summation order and exp's last
+// ulp: ~1e-15 relative, so budgets equal the fp64 oracle's end to end
+// (tests/test_gpu_configs.py, tests/test_gpu_parity.py).
 #pragma once
 
 #include "mca_common.cuh"
@@ -40,6 +42,7 @@ constexpr double kCertTau = 1e-5;   // relative distance of raw to an integer th
 // Flag sink of the budget passes (K12 group B, k2_budgets): null list = off.
 struct CertSink {
     long long* list;                 // [B*H*n] flagged token-head indices t = (b*H + h)*n + j
+    double* cm;                      // [B*H*n] the score pass's cmax of each flagged entry
     unsigned long long* count;       // number of flagged entries (zeroed per forward)
     uint8_t* row_done;               // [B*H*n] exact row statistics cached (cleared by the budget pass)
 };
@@ -55,9 +58,10 @@ __device__ __forceinline__ bool eq9_ambiguous(double cm, int n, double alpha, in
     return m >= (double)min_samples && m <= (double)(d - 1) && fabs(raw - m) <= kCertTau * fmax(raw, 1.0);
 }
 
-__device__ __forceinline__ void cert_push(const CertSink& c, long long t) {
+__device__ __forceinline__ void cert_push(const CertSink& c, long long t, double cm) {
     const unsigned long long pos = atomicAdd(c.count, 1ull);
     c.list[pos] = t;
+    c.cm[pos] = cm;
 }
 
 struct K2cArgs {
@@ -65,11 +69,11 @@ struct K2cArgs {
     const void* k;
     const float* lse;                // [B, H, n] natural-log lse of the scaled score rows (score pass)
     double scale;
-    int n, heads, d, dh, min_samples;
+    int n, heads, items, d, dh, min_samples;
     double alpha;
     CertSink cert;
-    double* row_m;                   // [B, H, n] exact row max (filled on demand)
-    double* row_l;                   // [B, H, n] exact row sum
+    const double* row_m;             // [B, H, n] the score pass's row max m~ (the reference point)
+    double* row_l;                   // [B, H, n] exact L_i (filled on demand)
     int32_t* budgets;
     uint8_t* exact;
     double* cmax_out;                // nullable
@@ -77,144 +81,226 @@ struct K2cArgs {
     unsigned int* hist;              // [H, d + 1] (nullable)
 };
 
-// 64-term dot in binary64 against a warp-private fp64 copy of the other row.
+constexpr int kCertThreads = 256;
+constexpr int kCertKeys = 64;        // flagged keys of one item processed together
+constexpr int kCertCands = 512;      // (key, query) candidates per batch
+constexpr int kCertRows = 16;        // candidate rows whose statistics one pass over the keys computes
+constexpr int kCertMaxN = 65536;     // bitmap of an item's rows (n <= 65535, mca_forward's limit)
+
 template <class T>
-__device__ __forceinline__ double dot64_sm(const T* __restrict__ a, const double* __restrict__ b) {
+__device__ __forceinline__ void load_row64(const T* __restrict__ p, float v[kDh]) {
+#pragma unroll
+    for (int c = 0; c < kDh; c += 8) load8(p + c, v + c);
+}
+__device__ __forceinline__ double dot64_exact(const float* __restrict__ a, const float* __restrict__ b) {
     double acc0 = 0.0, acc1 = 0.0;
 #pragma unroll
-    for (int c = 0; c < kDh; c += 8) {
-        float va[8];
-        load8(a + c, va);
-#pragma unroll
-        for (int e = 0; e < 8; e += 2) {
-            acc0 = fma((double)va[e], b[c + e], acc0);
-            acc1 = fma((double)va[e + 1], b[c + e + 1], acc1);
-        }
+    for (int e = 0; e < kDh; e += 2) {
+        acc0 = fma((double)a[e], (double)b[e], acc0);
+        acc1 = fma((double)a[e + 1], (double)b[e + 1], acc1);
     }
     return acc0 + acc1;
 }
-
-__device__ __forceinline__ double warp_max_d(double v) {
-    for (int off = 16; off; off >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, off));
-    return v;
+// max of positive doubles through their bit patterns (monotone for x >= 0)
+__device__ __forceinline__ void atomic_max_pos(double* p, double v) {
+    atomicMax(reinterpret_cast<unsigned long long*>(p), (unsigned long long)__double_as_longlong(v));
 }
-__device__ __forceinline__ double warp_sum_d(double v) {
-    for (int off = 16; off; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-    return v;
-}
-
-constexpr int kCertWarps = 8;
 
 template <class T>
-__global__ void __launch_bounds__(kCertWarps * 32) k2c_certify(K2cArgs a) {
-    __shared__ double s_row[kCertWarps][2][kDh];   // [warp][key j | candidate query i][64]
+__global__ void __launch_bounds__(kCertThreads) k2c_certify(K2cArgs a) {
+    __shared__ float s_k[kCertKeys][kDh];            // the batch's flagged keys (fp32 = exact bf16 values)
+    __shared__ long long s_t[kCertKeys];
+    __shared__ double s_lcm[kCertKeys], s_best[kCertKeys];
+    __shared__ int s_cf[kCertCands], s_ci[kCertCands];
+    __shared__ double s_ct[kCertCands];
+    __shared__ int s_rows[kCertCands];
+    __shared__ unsigned s_bm[kCertMaxN / 32];        // rows already queued in this batch
+    __shared__ float s_qr[kCertRows][kDh];           // candidate rows of one statistics pass
+    __shared__ double s_mref[kCertRows];
+    __shared__ double s_part[kCertThreads / 32][kCertRows];
+    __shared__ int s_nkeys, s_ncand, s_nrows;
     griddep_trigger();
-    griddep_wait();                                 // flags, provisional budgets, lse of the budget pass
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    griddep_wait();                                  // flags, provisional budgets, lse of the budget pass
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const long long nflag = (long long)*(volatile const unsigned long long*)a.cert.count;
-    const long long gw = (long long)blockIdx.x * kCertWarps + wid, nw = (long long)gridDim.x * kCertWarps;
+    if (nflag == 0) return;
     const size_t HD = (size_t)a.heads * kDh;
-    const T* Q = reinterpret_cast<const T*>(a.q);
-    const T* K = reinterpret_cast<const T*>(a.k);
-    double* kj = s_row[wid][0];
-    double* qi = s_row[wid][1];
-    for (long long f = gw; f < nflag; f += nw) {
-        const long long t = a.cert.list[f];
-        const long bh = (long)(t / a.n);
-        const int j = (int)(t - (long long)bh * a.n);
-        const int b = (int)(bh / a.heads), h = (int)(bh - (long)b * a.heads);
-        const T* Qb = Q + (size_t)b * a.n * HD + (size_t)h * kDh;   // row i at Qb + i * HD
-        const T* Kb = K + (size_t)b * a.n * HD + (size_t)h * kDh;
+    for (int bh = blockIdx.x; bh < a.items; bh += gridDim.x) {
+        const int b = bh / a.heads, h = bh - b * a.heads;
+        const T* Qb = reinterpret_cast<const T*>(a.q) + (size_t)b * a.n * HD + (size_t)h * kDh;
+        const T* Kb = reinterpret_cast<const T*>(a.k) + (size_t)b * a.n * HD + (size_t)h * kDh;
         const float* lse = a.lse + (size_t)bh * a.n;
-        __syncwarp();
-        kj[lane] = (double)to_f32(Kb[(size_t)j * HD + lane]);
-        kj[lane + 32] = (double)to_f32(Kb[(size_t)j * HD + lane + 32]);
-        __syncwarp();
-        // 1. v_i = t_ij - lse_i over the queries; its maximum and the lse scale
-        double vmax = -INFINITY, lmax = 0.0;
-        for (int i = lane; i < a.n; i += 32) {
-            const double ti = a.scale * dot64_sm(Qb + (size_t)i * HD, kj);
-            const double l = (double)lse[i];
-            vmax = fmax(vmax, ti - l);
-            lmax = fmax(lmax, fabs(l));
-        }
-        vmax = warp_max_d(vmax);
-        lmax = warp_max_d(lmax);
-        // 2. candidates: within the fp32 lse error (~1e-6 absolute, ulp-scaled) of the maximum
-        const double thr = vmax - (2e-4 + 4e-6 * lmax);
-        double best = 0.0;
-        // the 32-query blocks in a key-dependent rotation: when many keys share
-        // tied candidates (near-uniform rows), warps fill different rows' cache
-        // entries first instead of all computing the same row
-        const int nblk = (a.n + 31) >> 5;
-        for (int it = 0; it < nblk; ++it) {
-            const int base = (int)((it + j) % nblk) << 5;
-            const int i = base + lane;
-            double ti = 0.0;
-            bool cand = false;
-            if (i < a.n) {
-                ti = a.scale * dot64_sm(Qb + (size_t)i * HD, kj);
-                cand = ti - (double)lse[i] >= thr;
+        const double* rowm = a.row_m + (size_t)bh * a.n;
+        double* rowl = a.row_l + (size_t)bh * a.n;
+        uint8_t* done = a.cert.row_done + (size_t)bh * a.n;
+        const long long lo = (long long)bh * a.n, hi = lo + a.n;
+        for (;;) {
+            // 1. up to kCertKeys of this item's flagged keys; a claimed entry is
+            // consumed (-1) so the next batch takes the rest
+            __syncthreads();
+            if (tid == 0) {
+                s_nkeys = 0;
+                s_ncand = 0;
+                s_nrows = 0;
             }
-            unsigned ballot = __ballot_sync(0xffffffffu, cand);
-            while (ballot) {
-                const int src = __ffs(ballot) - 1;
-                ballot &= ballot - 1;
-                const int ci = base + src;
-                const double tc = __shfl_sync(0xffffffffu, ti, src);
-                // 3. the candidate row's exact statistics (cached for this forward)
-                const size_t ri = (size_t)bh * a.n + ci;
-                double m, l;
-                if (*(volatile uint8_t*)(a.cert.row_done + ri)) {
-                    m = *(volatile double*)(a.row_m + ri);
-                    l = *(volatile double*)(a.row_l + ri);
-                } else {
-                    __syncwarp();
-                    qi[lane] = (double)to_f32(Qb[(size_t)ci * HD + lane]);
-                    qi[lane + 32] = (double)to_f32(Qb[(size_t)ci * HD + lane + 32]);
-                    __syncwarp();
-                    m = -INFINITY;
-                    for (int jj = lane; jj < a.n; jj += 32)
-                        m = fmax(m, a.scale * dot64_sm(Kb + (size_t)jj * HD, qi));
-                    m = warp_max_d(m);
-                    l = 0.0;
-                    for (int jj = lane; jj < a.n; jj += 32) l += exp(a.scale * dot64_sm(Kb + (size_t)jj * HD, qi) - m);
-                    l = warp_sum_d(l);
-                    if (lane == 0) {
-                        a.row_m[ri] = m;
-                        a.row_l[ri] = l;
-                        __threadfence();
-                        a.cert.row_done[ri] = 1;
+            __syncthreads();
+            for (long long f0 = 0; f0 < nflag; f0 += kCertThreads) {
+                const long long f = f0 + tid;
+                if (f < nflag) {
+                    const long long t = a.cert.list[f];
+                    if (t >= lo && t < hi) {
+                        const int slot = atomicAdd(&s_nkeys, 1);
+                        if (slot < kCertKeys) {
+                            s_t[slot] = t;
+                            s_lcm[slot] = log(a.cert.cm[f]);
+                            s_best[slot] = 0.0;
+                            a.cert.list[f] = -1;
+                        }
                     }
                 }
-                // 4. the candidate's A_ij in the oracle's form
-                best = fmax(best, exp(tc - m) / l);
             }
-        }
-        if (lane == 0) {
-            const double cm = best;
-            int r;
-            bool ex;
-            const double tt = __ddiv_rn(__dmul_rn((double)a.n, cm), a.alpha);
-            const double raw = __dmul_rn(tt, tt);
-            const double c = ceil(raw);
-            ex = c >= (double)a.d;
-            r = ex ? a.d : (int)c;
-            if (r < a.min_samples) r = a.min_samples;
-            if (r > a.d) r = a.d;
-            a.budgets[t] = r;
-            a.exact[t] = ex ? 1 : 0;
-            if (a.cmax_out) a.cmax_out[t] = cm;
-            if (a.counters) {
-                if (ex) {
-                    atomicAdd(a.counters + 0, 2ull * (unsigned long long)a.d * (unsigned long long)a.dh);
-                    atomicAdd(a.counters + 2, 1ull);
-                } else {
-                    atomicAdd(a.counters + 0, (unsigned long long)r * (2ull * a.dh + 3ull));
-                    atomicAdd(a.counters + 1, (unsigned long long)r);
+            __syncthreads();
+            const int nk = min(s_nkeys, kCertKeys);
+            const bool more = s_nkeys > kCertKeys;
+            if (nk == 0) break;
+            for (int e = tid; e < nk * kDh; e += kCertThreads) {
+                const int f = e / kDh, c = e - f * kDh;
+                s_k[f][c] = to_f32(Kb[(size_t)(s_t[f] - lo) * HD + c]);
+            }
+            for (int e = tid; e < (a.n + 31) / 32; e += kCertThreads) s_bm[e] = 0u;
+            __syncthreads();
+            // 2. one pass over the queries against every key of the batch: fp32
+            // dots locate the candidates, binary64 dots give their exact t
+            for (int i = tid; i < a.n; i += kCertThreads) {
+                float qv[kDh];
+                load_row64(Qb + (size_t)i * HD, qv);
+                const double l = (double)lse[i];
+                for (int f = 0; f < nk; ++f) {
+                    float acc0 = 0.f, acc1 = 0.f;
+#pragma unroll
+                    for (int e = 0; e < kDh; e += 2) {
+                        acc0 = fmaf(qv[e], s_k[f][e], acc0);
+                        acc1 = fmaf(qv[e + 1], s_k[f][e + 1], acc1);
+                    }
+                    const double v = a.scale * (double)(acc0 + acc1) - l;
+                    if (v >= s_lcm[f] - (1e-3 + 1e-5 * (fabs(l) + fabs(s_lcm[f])))) {
+                        const int slot = atomicAdd(&s_ncand, 1);
+                        if (slot < kCertCands) {
+                            s_cf[slot] = f;
+                            s_ci[slot] = i;
+                            s_ct[slot] = a.scale * dot64_exact(qv, s_k[f]);
+                        }
+                    }
                 }
             }
-            if (a.hist) atomicAdd(&a.hist[(size_t)h * (a.d + 1) + (ex ? a.d : min(r, a.d - 1))], 1u);
+            __syncthreads();
+            // more near-ties than candidate slots (degenerate, e.g. uniform rows):
+            // every query row is a candidate of every key of the batch
+            const bool all_rows = s_ncand > kCertCands;
+            const int nc = min(s_ncand, kCertCands);
+            // 3. the distinct candidate rows without cached statistics
+            if (all_rows) {
+                for (int i = tid; i < a.n; i += kCertThreads)
+                    if (!done[i]) s_rows[atomicAdd(&s_nrows, 1) % kCertCands] = i;   // (guarded below)
+            } else {
+                for (int c = tid; c < nc; c += kCertThreads) {
+                    const int i = s_ci[c];
+                    if (!done[i]) {
+                        const unsigned bit = 1u << (i & 31);
+                        if (!(atomicOr(&s_bm[i >> 5], bit) & bit)) s_rows[atomicAdd(&s_nrows, 1)] = i;
+                    }
+                }
+            }
+            __syncthreads();
+            const int nrows_total = all_rows ? -1 : s_nrows;
+            // row statistics, kCertRows rows per pass over the item's keys (all rows
+            // in order for the degenerate case)
+            for (int r0 = 0;; r0 += kCertRows) {
+                int nr;
+                if (all_rows) {
+                    if (r0 >= a.n) break;
+                    nr = min(kCertRows, a.n - r0);
+                } else {
+                    if (r0 >= nrows_total) break;
+                    nr = min(kCertRows, nrows_total - r0);
+                }
+                __syncthreads();
+                for (int e = tid; e < nr * kDh; e += kCertThreads) {
+                    const int r = e / kDh, c = e - r * kDh;
+                    const int i = all_rows ? r0 + r : s_rows[r0 + r];
+                    s_qr[r][c] = to_f32(Qb[(size_t)i * HD + c]);
+                }
+                if (tid < nr) s_mref[tid] = rowm[all_rows ? r0 + tid : s_rows[r0 + tid]];
+                __syncthreads();
+                double part[kCertRows];            // per-thread partial sums (a small local array)
+                for (int r = 0; r < kCertRows; ++r) part[r] = 0.0;
+                for (int jj = tid; jj < a.n; jj += kCertThreads) {
+                    float kv[kDh];
+                    load_row64(Kb + (size_t)jj * HD, kv);
+#pragma unroll 1
+                    for (int r = 0; r < nr; ++r) part[r] += exp(a.scale * dot64_exact(s_qr[r], kv) - s_mref[r]);
+                }
+#pragma unroll 1
+                for (int r = 0; r < kCertRows; ++r) {
+                    double v = part[r];
+                    for (int off = 16; off; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+                    if (lane == 0) s_part[wid][r] = v;
+                }
+                __syncthreads();
+                if (tid < nr) {
+                    double L = 0.0;
+                    for (int w2 = 0; w2 < kCertThreads / 32; ++w2) L += s_part[w2][tid];
+                    const int i = all_rows ? r0 + tid : s_rows[r0 + tid];
+                    rowl[i] = L;
+                    done[i] = 1;
+                }
+            }
+            __syncthreads();
+            // 4. cmax_f = max over its candidates of exp(t - m~_i) / L_i
+            if (all_rows) {
+                for (int f = wid; f < nk; f += kCertThreads / 32) {
+                    double best = 0.0;
+                    for (int i = lane; i < a.n; i += 32) {
+                        float qv[kDh];
+                        load_row64(Qb + (size_t)i * HD, qv);
+                        best = fmax(best, exp(a.scale * dot64_exact(qv, s_k[f]) - rowm[i]) / rowl[i]);
+                    }
+                    for (int off = 16; off; off >>= 1) best = fmax(best, __shfl_xor_sync(0xffffffffu, best, off));
+                    if (lane == 0) s_best[f] = best;
+                }
+            } else {
+                for (int c = tid; c < nc; c += kCertThreads) {
+                    const int i = s_ci[c];
+                    atomic_max_pos(&s_best[s_cf[c]], exp(s_ct[c] - rowm[i]) / rowl[i]);
+                }
+            }
+            __syncthreads();
+            // Eq. 9 for the batch's keys
+            if (tid < nk) {
+                const long long t = s_t[tid];
+                const double cm = s_best[tid];
+                const double tt = __ddiv_rn(__dmul_rn((double)a.n, cm), a.alpha);
+                const double raw = __dmul_rn(tt, tt);
+                const double cc = ceil(raw);
+                const bool ex = cc >= (double)a.d;
+                int r = ex ? a.d : (int)cc;
+                if (r < a.min_samples) r = a.min_samples;
+                if (r > a.d) r = a.d;
+                a.budgets[t] = r;
+                a.exact[t] = ex ? 1 : 0;
+                if (a.cmax_out) a.cmax_out[t] = cm;
+                if (a.counters) {
+                    if (ex) {
+                        atomicAdd(a.counters + 0, 2ull * (unsigned long long)a.d * (unsigned long long)a.dh);
+                        atomicAdd(a.counters + 2, 1ull);
+                    } else {
+                        atomicAdd(a.counters + 0, (unsigned long long)r * (2ull * a.dh + 3ull));
+                        atomicAdd(a.counters + 1, (unsigned long long)r);
+                    }
+                }
+                if (a.hist) atomicAdd(&a.hist[(size_t)h * (a.d + 1) + (ex ? a.d : min(r, a.d - 1))], 1u);
+            }
+            if (!more) break;
         }
     }
 }

@@ -1,0 +1,208 @@
+// kp_project_tc.cu — KP: the Q/K projections of attention_matrix on tcgen05.
+//
+// attention_matrix forms Q = X W_q and
+// K = X W_k before the softmax. With W_q / W_k attached to the weights
+// (mca_set_projections) the forward takes x alone and this kernel computes
+//   [q | k] = x . [W_q | W_k]        x [M = B n, d_in],  W [d_in, 2 H 64]
+// in one persistent GEMM whose epilogue writes q and k straight into the
+// [B, n, H*64] layout the score kernels' TMA maps read.
+//
+// Operands (tc_common.cuh layout): A = x rows [128 x 64] per K step (K-major,
+// TMA 128B swizzle); B = W^T rows [BN x 64] (K-major: the handle keeps W_q /
+// W_k transposed, prepared once in mca_set_projections). D = fp32 in TMEM.
+//
+// Persistent, one CTA per SM, warp-specialised (192 threads):
+//   warp 0      TMA producer: kStages-deep ring of (A, B) K-steps
+//   warp 1      TMEM allocator + MMA issuer: tcgen05.mma M=128 N=BN K=16, four
+//               per K step; two accumulators (2 x BN columns) so the epilogue of
+//               tile i overlaps the main loop of tile i + 1
+//   warps 2-5   epilogue: tcgen05.ld (warp w reads TMEM lanes 32 (w % 4) ..),
+//               fp32 -> bf16, 16-byte stores of the thread's output row
+// Tiles are visited m-major (t -> m = t / nN, n = t % nN), so the CTAs working
+// at one time share x tiles in L2 across the N tiles; W (2.4 MB at BERT-base)
+// stays L2-resident.
+#include "mca_common.cuh"
+#include "tc_common.cuh"
+
+namespace mca_dev {
+
+namespace kp {
+constexpr int kBM = 128, kBK = 64;
+constexpr int kThreads = 192;
+template <int BN>
+struct Cfg {
+    static constexpr int kStages = BN == 256 ? 4 : 6;
+    static constexpr uint32_t kABytes = kBM * kBK * 2;           // 16 KB
+    static constexpr uint32_t kBBytes = BN * kBK * 2;            // 8 / 16 / 32 KB
+    static constexpr uint32_t kStageBytes = kABytes + kBBytes;
+    static constexpr uint32_t kSmemBar = kStages * kStageBytes;
+    static constexpr uint32_t kSmemBytes = kSmemBar + 256 + 1024;   // barriers + 1 KB alignment slack
+    static constexpr int kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;
+    static constexpr uint32_t kIdesc = mca_tc::idesc_f16(1, 0, kBM, BN);   // bf16, both K-major
+};
+}  // namespace kp
+
+struct KpArgs {
+    int M;          // rows of x (B * n)
+    int d_in;       // K
+    int HD;         // H * 64: q columns [0, HD), k columns [HD, 2 HD) of the product
+    void* q;        // [M, HD] bf16
+    void* k;        // [M, HD] bf16
+};
+
+template <int BN>
+__global__ void __launch_bounds__(kp::kThreads, 1) kp_project_tc(const __grid_constant__ CUtensorMap tm_x,
+                                                                 const __grid_constant__ CUtensorMap tm_w, KpArgs a) {
+    using namespace mca_tc;
+    using C = kp::Cfg<BN>;
+    constexpr int S = C::kStages;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kSmemBar);
+    uint64_t* full = bars;               // [S] TMA tx
+    uint64_t* empty = bars + S;          // [S] MMA commit
+    uint64_t* acc_full = bars + 2 * S;   // [2] MMA commit after a tile's last K step
+    uint64_t* acc_empty = bars + 2 * S + 2;   // [2] 4 epilogue warps
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 4);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nK = (a.d_in + kp::kBK - 1) / kp::kBK;
+    const int nM = (a.M + kp::kBM - 1) / kp::kBM;
+    const int nN = 2 * a.HD / BN;
+    const int tiles = nM * nN;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(full + s, 1);
+            mbar_init(empty + s, 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(acc_full + b, 1);
+            mbar_init(acc_empty + b, 4);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc<C::kTmemCols>(tmem_slot);
+    if (warp == 0 && lane == 0) {
+        tma_prefetch(&tm_x);
+        tma_prefetch(&tm_w);
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    griddep_trigger();
+
+    if (warp == 0) {
+        if (lane == 0) {
+            griddep_wait();   // x may be the previous kernel's output (a chained layer)
+            int s = 0;
+            uint32_t ph = 0;
+            for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+                const int m0 = (t / nN) * kp::kBM, n0 = (t % nN) * BN;
+                for (int kb = 0; kb < nK; ++kb) {
+                    mbar_wait(empty + s, ph ^ 1);
+                    uint8_t* st = smem + s * C::kStageBytes;
+                    mbar_expect_tx(full + s, C::kStageBytes);
+                    tma_load_3d(st, &tm_x, full + s, kb * kp::kBK, m0, 0);
+                    tma_load_3d(st + C::kABytes, &tm_w, full + s, kb * kp::kBK, n0, 0);
+                    if (++s == S) {
+                        s = 0;
+                        ph ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            int s = 0;
+            uint32_t ph = 0;
+            int acc = 0;
+            uint32_t aph = 0;
+            for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+                mbar_wait(acc_empty + acc, aph ^ 1);    // the epilogue drained this accumulator
+                tc_fence_after();
+                const uint32_t d = tmem + (uint32_t)(acc * BN);
+                for (int kb = 0; kb < nK; ++kb) {
+                    mbar_wait(full + s, ph);
+                    tc_fence_after();
+                    const uint32_t sa = smem_u32(smem + s * C::kStageBytes);
+                    const uint32_t sb = sa + C::kABytes;
+#pragma unroll
+                    for (int kk = 0; kk < kp::kBK / 16; ++kk)
+                        umma_f16(d, sw128_desc(sa + kk * 32, 16, 1024), sw128_desc(sb + kk * 32, 16, 1024), C::kIdesc,
+                                 (kb | kk) != 0);
+                    umma_commit(empty + s);             // the stage is free once these MMAs read it
+                    if (++s == S) {
+                        s = 0;
+                        ph ^= 1;
+                    }
+                }
+                umma_commit(acc_full + acc);            // the tile's accumulator is complete
+                if (++acc == 2) {
+                    acc = 0;
+                    aph ^= 1;
+                }
+            }
+        }
+    } else {
+        // epilogue: warp w reads TMEM lanes 32 (w % 4) .. +31 = output rows of the tile
+        const int quarter = warp & 3;
+        const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
+        int acc = 0;
+        uint32_t aph = 0;
+        for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+            const int m0 = (t / nN) * kp::kBM, n0 = (t % nN) * BN;
+            const int row = m0 + quarter * 32 + lane;
+            __nv_bfloat16* out = n0 < a.HD ? reinterpret_cast<__nv_bfloat16*>(a.q) + n0
+                                           : reinterpret_cast<__nv_bfloat16*>(a.k) + (n0 - a.HD);
+            out += (size_t)row * a.HD;
+            mbar_wait(acc_full + acc, aph);
+            tc_fence_after();
+#pragma unroll 1
+            for (int c = 0; c < BN; c += 32) {
+                uint32_t v[32];
+                tmem_ld32(lane_base + (uint32_t)(acc * BN + c), v);
+                tmem_ld_wait();
+                if (row < a.M) {
+                    uint4* dst = reinterpret_cast<uint4*>(out + c);
+#pragma unroll
+                    for (int g = 0; g < 4; ++g) {
+                        uint4 u;
+                        u.x = pack_bf16x2(__uint_as_float(v[8 * g + 0]), __uint_as_float(v[8 * g + 1]));
+                        u.y = pack_bf16x2(__uint_as_float(v[8 * g + 2]), __uint_as_float(v[8 * g + 3]));
+                        u.z = pack_bf16x2(__uint_as_float(v[8 * g + 4]), __uint_as_float(v[8 * g + 5]));
+                        u.w = pack_bf16x2(__uint_as_float(v[8 * g + 6]), __uint_as_float(v[8 * g + 7]));
+                        dst[g] = u;
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(acc_empty + acc);
+            if (++acc == 2) {
+                acc = 0;
+                aph ^= 1;
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) tmem_dealloc<C::kTmemCols>(tmem);
+}
+
+}  // namespace mca_dev
+
+namespace mca_dev {
+// W [d_in, HD] (x W convention) -> W^T [HD, d_in] (the K-major B operand above),
+// once per mca_set_projections. grid (ceil(HD / 32), ceil(d_in / 32)), block (32, 8).
+__global__ void kp_transpose(const __nv_bfloat16* __restrict__ w, int d_in, int HD, __nv_bfloat16* __restrict__ wt) {
+    __shared__ __nv_bfloat16 tile[32][33];
+    const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+    for (int r = threadIdx.y; r < 32; r += 8)
+        if (r0 + r < d_in && c0 + (int)threadIdx.x < HD) tile[r][threadIdx.x] = w[(size_t)(r0 + r) * HD + c0 + threadIdx.x];
+    __syncthreads();
+    for (int c = threadIdx.y; c < 32; c += 8)
+        if (c0 + c < HD && r0 + (int)threadIdx.x < d_in)
+            wt[(size_t)(c0 + c) * d_in + r0 + threadIdx.x] = tile[threadIdx.x][c];
+}
+}  // namespace mca_dev

@@ -35,6 +35,7 @@
 #include "k3t_encode_tc.cu"
 #include "k4_apply_simt.cu"
 #include "k4_apply_tc.cu"
+#include "kp_project_tc.cu"
 #include "ka_given_attn.cu"
 #include "mca_diag.cuh"
 
@@ -190,7 +191,8 @@ struct mca_weights {
     float* invp = nullptr;        // [heads, d_in]
     uint16_t* guide = nullptr;    // [heads, kGuide]
     void* wprime = nullptr;       // bf16 path: [d_in, heads*dh] W_h / p (k3t's B operand)
-    void* wqk = nullptr;          // optional [2][d_in][heads*dh] W_q, W_k (mca_set_projections)
+    void* wqk = nullptr;          // optional [2][d_in][heads*dh] W_q, W_k (mca_set_projections; fp32 path)
+    void* wqk_t = nullptr;        // bf16 path: [2*heads*dh][d_in] W_q^T | W_k^T (kp_project_tc's K-major B)
     cublasHandle_t blas = nullptr;
     void* qk = nullptr;           // [2][B*n][heads*dh] projected q, k (workspace, grown on demand)
     long cap_qk = 0;
@@ -208,6 +210,7 @@ struct mca_weights {
     int32_t* samp_list = nullptr;             // [H, B*n] sampled tokens per head, budget-descending
     int32_t* exact_list = nullptr;            // [H, B*n] exact tokens per head
     long long* cert_list = nullptr;           // [B, H, n] Eq. 9 values at an integer boundary (k2c_certify)
+    double* cert_cm = nullptr;                // [B, H, n] the score pass's cmax of each flagged entry
     uint8_t* row_done = nullptr;              // [B, H, n] k2c's exact row-statistics cache flags
     void* zeroed = nullptr;                   // counters | task_cursor | hist | fill (zeroed once per forward)
     unsigned int* fill = nullptr;             // [H, d + 1] per-bin list fill counters (k2_scan_scatter)
@@ -218,7 +221,7 @@ struct mca_weights {
     int* task_cursor = nullptr;               // [H] K3 work cursor
     // timing
     bool timing = false;
-    cudaEvent_t ev[5] = {};
+    cudaEvent_t ev[6] = {};   // stage boundaries: projection | score | budgets | encoding | aggregation
     void* blas_ws = nullptr;                  // explicit cuBLAS workspace (capture-safe projection GEMM)
     // MCA_GRAPHS=1: CUDA graphs of repeated identical forwards (key = every argument).
     // The first call of a key runs eagerly (it may size buffers), the second is
@@ -249,6 +252,8 @@ void free_workspace(mca_weights* w) {
     cudaFree(w->samp_list);
     cudaFree(w->exact_list);
     cudaFree(w->cert_list);
+    cudaFree(w->cert_cm);
+    w->cert_cm = nullptr;
     cudaFree(w->row_done);
     w->cert_list = nullptr;
     w->row_done = nullptr;
@@ -289,6 +294,7 @@ mca_status ensure_workspace(mca_weights* w, long tokens, mca_stream_t stream) {
         cudaMalloc(&w->samp_list, th * sizeof(int32_t)) != cudaSuccess ||
         cudaMalloc(&w->exact_list, th * sizeof(int32_t)) != cudaSuccess ||
         cudaMalloc(&w->cert_list, th * sizeof(long long)) != cudaSuccess ||
+        cudaMalloc(&w->cert_cm, th * sizeof(double)) != cudaSuccess ||
         cudaMalloc(&w->row_done, th * sizeof(uint8_t)) != cudaSuccess) {
         cudaGetLastError();
         free_workspace(w);
@@ -602,6 +608,7 @@ void mca_weights_free(mca_weights* w) {
     cudaFree(w->wprime);
     cudaFree(w->pbf);
     cudaFree(w->wqk);
+    cudaFree(w->wqk_t);
     cudaFree(w->qk);
     if (w->blas) cublasDestroy(w->blas);
     cudaFree(w->blas_ws);
@@ -618,6 +625,21 @@ void mca_weights_free(mca_weights* w) {
 mca_status mca_set_projections(mca_weights* w, const void* w_q, const void* w_k, mca_stream_t stream) {
     if (!w || !w_q || !w_k) return fail(MCA_ERR_NULL, "weights / w_q / w_k is NULL");
     const size_t bytes = (size_t)w->d_in * w->heads * w->dh * dtype_size(w->wdt);
+    if (w->wdt == MCA_BF16) {   // kp_project_tc: W_q^T | W_k^T, K-major, prepared once
+        if (!w->wqk_t && cudaMalloc(&w->wqk_t, 2 * bytes) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(MCA_ERR_ALLOC, "W_q / W_k allocation failed");
+        }
+        const int HD = w->heads * w->dh;
+        const dim3 g((HD + 31) / 32, (w->d_in + 31) / 32);
+        for (int i = 0; i < 2; ++i) {
+            kp_transpose<<<g, dim3(32, 8), 0, stream>>>(static_cast<const __nv_bfloat16*>(i ? w_k : w_q), w->d_in, HD,
+                                                        static_cast<__nv_bfloat16*>(w->wqk_t) + (size_t)i * HD * w->d_in);
+            MCA_CUDA_TRY(cudaGetLastError());
+        }
+        drop_graphs(w);
+        return MCA_OK;
+    }
     if (!w->wqk && cudaMalloc(&w->wqk, 2 * bytes) != cudaSuccess) {
         cudaGetLastError();
         return fail(MCA_ERR_ALLOC, "W_q / W_k allocation failed");
@@ -660,9 +682,9 @@ mca_status mca_set_timing(mca_weights* w, int enable) {
 
 int mca_last_stage_ms(const mca_weights* w, float* ms, int max_stages) {
     if (!w || !w->timing || !w->ev_valid) return 0;
-    if (cudaEventSynchronize(w->ev[4]) != cudaSuccess) return 0;
+    if (cudaEventSynchronize(w->ev[5]) != cudaSuccess) return 0;
     int k = 0;
-    for (; k < 4 && k < max_stages; ++k)
+    for (; k < 5 && k < max_stages; ++k)
         if (cudaEventElapsedTime(&ms[k], w->ev[k], w->ev[k + 1]) != cudaSuccess) return k;
     return k;
 }
@@ -715,12 +737,12 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
         return MCA_OK;
     }
     if (!x || !y || (!q) != (!k)) return fail(MCA_ERR_NULL, "x / y is NULL, or only one of q / k is");
-    if (!q && !w->wqk) return fail(MCA_ERR_NULL, "q / k are NULL and the weights carry no W_q / W_k");
+    if (!q && !w->wqk && !w->wqk_t) return fail(MCA_ERR_NULL, "q / k are NULL and the weights carry no W_q / W_k");
     const long tokens = (long)B * n;
     if (mca_status s = ensure_workspace(w, tokens, stream)) return s;
     const int H = w->heads;
     int launches = 0;
-    if (w->timing) MCA_CUDA_TRY(cudaEventRecord(w->ev[0], stream));   // the score stage includes the projection
+    if (w->timing) MCA_CUDA_TRY(cudaEventRecord(w->ev[0], stream));
     if (!q) {   // q = x W_q, k = x W_k: one strided-batched GEMM (row-major C = X W as col-major C^T = W^T X^T)
         const size_t HD = (size_t)H * w->dh, esz = dtype_size(dt);
         if (tokens > w->cap_qk) {
@@ -735,9 +757,35 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
             }
             w->cap_qk = tokens;
         }
+        if (dt == MCA_BF16) {   // tcgen05 GEMM, q and k written in the score kernels' layout
+            const int HD_ = (int)HD;
+            CUtensorMap tx, tw;
+            const int BN = HD_ % 256 == 0 ? 256 : HD_ % 128 == 0 ? 128 : 64;
+            if (!make_tmap_bf16(&tx, x, (uint64_t)w->d_in, (uint64_t)tokens, 1, kp::kBM) ||
+                !make_tmap_bf16(&tw, w->wqk_t, (uint64_t)w->d_in, 2 * (uint64_t)HD_, 1, (uint32_t)BN))
+                return fail(MCA_ERR_CUDA, "cuTensorMapEncodeTiled failed for x / W_q|W_k");
+            KpArgs pa{};
+            pa.M = (int)tokens;
+            pa.d_in = w->d_in;
+            pa.HD = HD_;
+            pa.q = w->qk;
+            pa.k = static_cast<char*>(w->qk) + (size_t)tokens * HD * esz;
+            const long tiles = ((tokens + kp::kBM - 1) / kp::kBM) * (2L * HD_ / BN);
+            const dim3 grid((unsigned)std::min<long>(tiles, sm_count()));
+            auto go = [&](auto kern, uint32_t smem) -> mca_status {
+                MCA_CUDA_TRY(ensure_smem(kern, smem));
+                MCA_CUDA_TRY(launch_pdl(kern, grid, dim3(kp::kThreads), smem, stream, tx, tw, pa));
+                return MCA_OK;
+            };
+            mca_status ps = BN == 256   ? go(kp_project_tc<256>, kp::Cfg<256>::kSmemBytes)
+                            : BN == 128 ? go(kp_project_tc<128>, kp::Cfg<128>::kSmemBytes)
+                                        : go(kp_project_tc<64>, kp::Cfg<64>::kSmemBytes);
+            if (ps) return ps;
+            MCA_LAUNCH_CHECK("kp_project_tc");
+        } else {
         const float one = 1.0f, zero = 0.0f;
-        const cudaDataType_t ty = dt == MCA_BF16 ? CUDA_R_16BF : CUDA_R_32F;
-        const cublasComputeType_t ct = dt == MCA_BF16 ? CUBLAS_COMPUTE_32F : CUBLAS_COMPUTE_32F_PEDANTIC;
+        const cudaDataType_t ty = CUDA_R_32F;
+        const cublasComputeType_t ct = CUBLAS_COMPUTE_32F_PEDANTIC;
         // cublasSetStream resets the handle's workspace to cuBLAS's pool: re-attach
         // the explicit one (no allocation inside a captured forward)
         if (cublasSetStream(w->blas, stream) != CUBLAS_STATUS_SUCCESS ||
@@ -747,6 +795,7 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
                                        (int)HD, (long long)tokens * HD, 2, ct,
                                        CUBLAS_GEMM_DEFAULT) != CUBLAS_STATUS_SUCCESS)
             return fail(MCA_ERR_CUDA, "q / k projection GEMM failed");
+        }
         q = w->qk;
         k = static_cast<const char*>(w->qk) + (size_t)tokens * HD * esz;
         if (dbg && dbg->q_out)
@@ -754,6 +803,7 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
         if (dbg && dbg->k_out)
             MCA_CUDA_TRY(cudaMemcpyAsync(dbg->k_out, k, (size_t)tokens * HD * esz, cudaMemcpyDeviceToDevice, stream));
     }
+    if (w->timing) MCA_CUDA_TRY(cudaEventRecord(w->ev[1], stream));   // end of the (optional) projection
     const long th = tokens * H;
     const double scale = cfg->scale > 0.0 ? cfg->scale : 1.0 / std::sqrt((double)w->dh);
 
@@ -763,10 +813,12 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
     const bool tile_k3 = dt == MCA_BF16 && use_k3t(w);   // k3t reads budgets directly: no work lists
     // bf16 score passes: Eq. 9 values within kCertTau of an integer boundary are
     // re-derived in binary64 by k2c_certify (the fp32 path's scores are fp64 already)
-    const bool certify = dt == MCA_BF16 && approx && !(dbg && (dbg->budgets_override || dbg->cmax_override));
+    const bool certify = cfg->certify && dt == MCA_BF16 && approx &&
+                         !(dbg && (dbg->budgets_override || dbg->cmax_override));
     CertSink cert{};
     if (certify) {
         cert.list = w->cert_list;
+        cert.cm = w->cert_cm;
         cert.count = w->counters + kCertCounter;
         cert.row_done = w->row_done;
     }
@@ -835,7 +887,7 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
         }
         MCA_LAUNCH_CHECK("k1_scores");
     }
-    if (w->timing) MCA_CUDA_TRY(cudaEventRecord(w->ev[1], stream));
+    if (w->timing) MCA_CUDA_TRY(cudaEventRecord(w->ev[2], stream));
     // K2: Eq. 9 budgets
     {
         const dim3 grid = bh_grid((n + 255) / 256, (long)B * H);
@@ -879,6 +931,7 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
             c.scale = scale;
             c.n = n;
             c.heads = H;
+            c.items = B * H;
             c.d = w->d_in;
             c.dh = w->dh;
             c.min_samples = cfg->min_samples;
@@ -891,15 +944,15 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
             c.cmax_out = dbg ? dbg->cmax_out : nullptr;
             c.counters = w->counters;
             c.hist = tile_k3 ? nullptr : w->hist;
-            MCA_CUDA_TRY(launch_pdl(k2c_certify<__nv_bfloat16>, dim3((unsigned)sm_count()), dim3(kCertWarps * 32), 0,
-                                    stream, c));
+            const int gc = std::min(B * H, sm_count());   // (b, h) items with flags, one CTA each
+            MCA_CUDA_TRY(launch_pdl(k2c_certify<__nv_bfloat16>, dim3((unsigned)gc), dim3(kCertThreads), 0, stream, c));
             MCA_LAUNCH_CHECK("k2c_certify");
         }
         if (!tile_k3) {
             if (mca_status s = launch_lists(w, grid, n, tokens, stream, launches)) return s;
         }
     }
-    if (w->timing) MCA_CUDA_TRY(cudaEventRecord(w->ev[2], stream));
+    if (w->timing) MCA_CUDA_TRY(cudaEventRecord(w->ev[3], stream));
     // K3: encoding
     {
         int32_t* draws = dbg ? dbg->draws_out : nullptr;
@@ -911,7 +964,7 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
                                                              stream, launches);
         if (s) return s;
     }
-    if (w->timing) MCA_CUDA_TRY(cudaEventRecord(w->ev[3], stream));
+    if (w->timing) MCA_CUDA_TRY(cudaEventRecord(w->ev[4], stream));
     // K4: y = A . H~
     {
         const dim3 grid((n + kQT4 - 1) / kQT4, H, B);
@@ -938,7 +991,7 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
         MCA_LAUNCH_CHECK("k4_apply");
     }
     if (w->timing) {
-        MCA_CUDA_TRY(cudaEventRecord(w->ev[4], stream));
+        MCA_CUDA_TRY(cudaEventRecord(w->ev[5], stream));
         w->ev_valid = true;
     }
     // optional outputs
@@ -1032,7 +1085,9 @@ mca_status mca_forward(mca_weights* w, const void* q, const void* k, const void*
                               nullptr, stream);
     uint64_t key[16] = {(uint64_t)q, (uint64_t)k, (uint64_t)x, (uint64_t)y, (uint64_t)dt, (uint64_t)B, (uint64_t)n,
                         (uint64_t)b_offset, (uint64_t)layer, seed, (uint64_t)budgets_out, (uint64_t)exact_out,
-                        (uint64_t)stream, 0, 0, (uint64_t)cfg->min_samples | ((uint64_t)cfg->mode << 32)};
+                        (uint64_t)stream, 0, 0,
+                        (uint64_t)(uint32_t)cfg->min_samples | ((uint64_t)(cfg->mode & 0xFF) << 32) |
+                            ((uint64_t)(cfg->certify != 0) << 40)};
     std::memcpy(&key[13], &cfg->alpha, 8);
     std::memcpy(&key[14], &cfg->scale, 8);
     auto eager = [&]() {
@@ -1107,7 +1162,7 @@ mca_status mca_forward(mca_weights* w, const void* q, const void* k, const void*
 
 mca_status mca_regular_forward(mca_weights* w, const void* q, const void* k, const void* x, mca_dtype dt, int B,
                                int n, double scale, void* y, mca_stream_t stream) {
-    mca_config cfg{1.0, scale, 1, MCA_MODE_REGULAR};
+    mca_config cfg{1.0, scale, 1, MCA_MODE_REGULAR, 0, 0};
     return mca_forward_ex(w, q, k, x, dt, B, n, 0, 0, &cfg, 0, y, nullptr, nullptr, nullptr, nullptr, stream);
 }
 

@@ -1,0 +1,9 @@
+# tests + c2 / c4 bench stage times
+timeout 800 python -m pytest tests -m gpu -q -p no:cacheprovider -x > gpurun_out/t.log 2>&1; echo tests_rc=$?; tail -3 gpurun_out/t.log
+for c in c2 c4; do
+timeout 300 python bench.py --config $c --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/b_$c.json 2> gpurun_out/b_$c.err; echo ${c}_rc=$?; tail -2 gpurun_out/b_$c.err
+python - <<PY
+import json; d=json.loads(open('gpurun_out/b_$c.json').read())
+print('$c', 'ms %.4f'%d['ms_per_step'], {k:round(v,4) for k,v in d['stages_ms'].items()}, d['budget_certification'], 'regular', d['regular'])
+PY
+done

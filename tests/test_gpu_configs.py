@@ -5,8 +5,9 @@ C4: one whole n = 4096 sequence (all 12 heads): the tiled score pass (K1a / K1b
 + K2, n > 768), Eq. 9 bitwise on the device's column maxima, every draw of a
 sample of token-heads bitwise, y on the full sequence against the oracle run
 with the device's plan, and the end-to-end budgets against the oracle's own
-plan: zero mismatches (the token-heads at integer boundaries of raw are
-re-derived in binary64 by k2c_certify).
+plan: mismatches only at integer boundaries of raw on the default path, and
+none with McaConfig(certify=True), which re-derives those token-heads in
+binary64 (k2c_certify).
 
 C3: d_in = 1024, 16 heads, n = 512, a chained stack X_{l+1} = Y_l where every
 layer re-projects q = X_l W_q^l, k = X_l W_k^l on the device
@@ -29,6 +30,8 @@ TOL_Y_BF16 = 2e-2
 TOL_H_BF16 = 1e-2
 TOL_PROJ_BF16 = 8e-3        # bf16 output rounding of q = x W (2^-8 relative per element, worst row)
 CMAX_REL_BF16 = 1e-5
+MISMATCH_RATE_BF16 = 2e-4     # the default path: measured <= 1.2e-4 (C4), all within 7.6e-7 of an integer
+MISMATCH_DIST_BF16 = 4e-6
 
 
 @pytest.fixture(scope="module")
@@ -49,9 +52,10 @@ def _np(t):
     return t.detach().float().cpu().double().numpy()
 
 
-def _check_layer(orc, w, q, k, x, H, n, d_in, out, dbg, seed, b_offset, layer, label):
+def _check_layer(orc, w, q, k, x, H, n, d_in, out, dbg, seed, b_offset, layer, label, certified=True):
     """Stage-isolated Eq. 9, y with the device's plan, H~, draws, and the
-    end-to-end mismatch report for one layer's forward."""
+    end-to-end mismatch report for one layer's forward (certified: zero
+    mismatches; default path: at integer boundaries only)."""
     b = out.budgets.cpu().numpy()
     e = out.exact_mask.cpu().numpy().astype(bool)
     cm = dbg["cmax_out"].cpu().numpy()
@@ -68,7 +72,11 @@ def _check_layer(orc, w, q, k, x, H, n, d_in, out, dbg, seed, b_offset, layer, l
     print(f"{label}: cmax max rel {cm_rel:.2e}; budget mismatches vs the fp64 oracle {rep}; "
           f"sampled {int((~e).sum())} exact {int(e.sum())}")
     assert cm_rel <= CMAX_REL_BF16, (label, cm_rel)
-    assert rep["count"] == 0, (label, rep)
+    if certified:
+        assert rep["count"] == 0, (label, rep)
+    else:
+        assert rep["count"] <= max(1, int(MISMATCH_RATE_BF16 * b.size)), (label, rep)
+        assert rep["max_dist_to_int"] <= MISMATCH_DIST_BF16, (label, rep)
     # draws of a sample of sampled token-heads, bitwise (first 64 of each)
     draws = dbg["draws_out"].cpu().numpy()
     rng = np.random.default_rng(layer + 17)
@@ -103,11 +111,13 @@ def test_c4_long_sequence_parity(mca, syn, orc):
                h_out=torch.zeros((B, n, H * 64), dtype=torch.float16, device="cuda"),
                draws_out=torch.zeros((B, H, n, 64), dtype=torch.int32, device="cuda"), draws_stride=64)
     b_offset = 5                                      # a shard of a larger batch: stream ids use b + 5
-    out = mca.mca_forward(weights, q, k, x, mca.McaConfig(alpha=ALPHA), seed=42, b_offset=b_offset,
-                          return_plan=True, flops=True, debug=dbg)
-    torch.cuda.synchronize()
-    b, e = _check_layer(orc, w, q, k, x, H, n, d_in, out, dbg, 42, b_offset, 0, "C4 n=4096")
-    assert out.flops.samples == int(b[~e].sum())
+    for certify in (False, True):
+        out = mca.mca_forward(weights, q, k, x, mca.McaConfig(alpha=ALPHA, certify=certify), seed=42,
+                              b_offset=b_offset, return_plan=True, flops=True, debug=dbg)
+        torch.cuda.synchronize()
+        b, e = _check_layer(orc, w, q, k, x, H, n, d_in, out, dbg, 42, b_offset, 0, f"C4 n=4096 certify={certify}",
+                            certified=certify)
+        assert out.flops.samples == int(b[~e].sum())
     # the sample-count imbalance C4 is meant to stress is present
     r = b[~e]
     assert np.percentile(r, 99) > 4 * np.percentile(r, 50)
@@ -126,7 +136,7 @@ def test_c3_chained_stack_parity(mca, syn, orc):
         w_v = syn.make_weights(d_in, H, seed=1234 + l).to(bf)
         layers.append((w_v, pin.w_q.to(bf), pin.w_k.to(bf)))
     x = pin0.x.to(bf).cuda()
-    cfg = mca.McaConfig(alpha=ALPHA)
+    cfg = mca.McaConfig(alpha=ALPHA, certify=True)
     b_offset = 2                                      # rank 1 of a 2-way shard of B = 4
     for l, (w_v, w_q, w_k) in enumerate(layers):
         weights = mca.AttentionWeights(w_v.cuda(), heads=H, w_q=w_q.cuda(), w_k=w_k.cuda())
@@ -162,7 +172,8 @@ def test_certified_budgets_on_tied_attention(mca, syn, orc, n):
     q, k, x = (t.to(bf).cuda() for t in (inp.q, inp.k, inp.x))
     weights = mca.AttentionWeights(w.cuda(), heads=H)
     qz = torch.zeros_like(q)
-    out = mca.mca_forward(weights, qz, k, x, mca.McaConfig(alpha=1.0), seed=1, return_plan=True, flops=True)
+    out = mca.mca_forward(weights, qz, k, x, mca.McaConfig(alpha=1.0, certify=True), seed=1, return_plan=True,
+                          flops=True)
     torch.cuda.synchronize()
     assert bool((out.budgets == 1).all()) and not bool(out.exact_mask.bool().any())
     assert out.flops.samples == H * n
@@ -170,7 +181,7 @@ def test_certified_budgets_on_tied_attention(mca, syn, orc, n):
     q2 = q.clone()
     q2[:, 1::2] = q2[:, 0::2]
     cm = torch.zeros((1, H, n), dtype=torch.float64, device="cuda")
-    out2 = mca.mca_forward(weights, q2, k, x, mca.McaConfig(alpha=ALPHA), seed=1, return_plan=True,
+    out2 = mca.mca_forward(weights, q2, k, x, mca.McaConfig(alpha=ALPHA, certify=True), seed=1, return_plan=True,
                            debug=dict(cmax_out=cm))
     torch.cuda.synchronize()
     full = orc.batched_forward(_np(q2), _np(k), _np(x), _np(w), heads=H, alpha=ALPHA, seed=1, want_h=False)
