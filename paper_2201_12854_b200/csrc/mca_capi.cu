@@ -764,17 +764,21 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
             if (!make_tmap_bf16(&tx, x, (uint64_t)w->d_in, (uint64_t)tokens, 1, kp::kBM) ||
                 !make_tmap_bf16(&tw, w->wqk_t, (uint64_t)w->d_in, 2 * (uint64_t)HD_, 1, (uint32_t)BN))
                 return fail(MCA_ERR_CUDA, "cuTensorMapEncodeTiled failed for x / W_q|W_k");
+            CUtensorMap tq_out, tk_out;
+            void* q_dst = w->qk;
+            void* k_dst = static_cast<char*>(w->qk) + (size_t)tokens * HD * esz;
+            if (!make_tmap_bf16(&tq_out, q_dst, (uint64_t)HD_, (uint64_t)tokens, 1, kp::kBM) ||
+                !make_tmap_bf16(&tk_out, k_dst, (uint64_t)HD_, (uint64_t)tokens, 1, kp::kBM))
+                return fail(MCA_ERR_CUDA, "cuTensorMapEncodeTiled failed for q / k");
             KpArgs pa{};
             pa.M = (int)tokens;
             pa.d_in = w->d_in;
             pa.HD = HD_;
-            pa.q = w->qk;
-            pa.k = static_cast<char*>(w->qk) + (size_t)tokens * HD * esz;
             const long tiles = ((tokens + kp::kBM - 1) / kp::kBM) * (2L * HD_ / BN);
             const dim3 grid((unsigned)std::min<long>(tiles, sm_count()));
             auto go = [&](auto kern, uint32_t smem) -> mca_status {
                 MCA_CUDA_TRY(ensure_smem(kern, smem));
-                MCA_CUDA_TRY(launch_pdl(kern, grid, dim3(kp::kThreads), smem, stream, tx, tw, pa));
+                MCA_CUDA_TRY(launch_pdl(kern, grid, dim3(kp::kThreads), smem, stream, tx, tw, tq_out, tk_out, pa));
                 return MCA_OK;
             };
             mca_status ps = BN == 256   ? go(kp_project_tc<256>, kp::Cfg<256>::kSmemBytes)
