@@ -162,6 +162,18 @@ __global__ void __launch_bounds__(k3btc::kThreads, 2) k3b_exact_tc(K3Args a) {
             tmem_ld_wait();
             if (bj >= 0) {
                 __half* dst = reinterpret_cast<__half*>(a.h_out) + tok * HD + (size_t)h * kDh;   // H~ is fp16
+                bool big = false;                      // fp16 range guard (mca_common.cuh)
+#pragma unroll
+                for (int c = 0; c < 64; ++c) big |= f16_overflows(__uint_as_float(v[c >> 5][c & 31]));
+                if (big) {
+                    const long long tokh = ((long long)(bj >> 16) * a.heads + h) * n + (bj & 0xFFFF);
+                    const int slot = ovf_push(a.ovf, tokh);
+#pragma unroll
+                    for (int c = 0; c < 64; ++c) {
+                        if (slot >= 0) a.ovf.rows[(size_t)slot * kDh + c] = __uint_as_float(v[c >> 5][c & 31]);
+                        v[c >> 5][c & 31] = 0u;
+                    }
+                }
 #pragma unroll
                 for (int g = 0; g < 8; ++g) {
                     uint32_t pk[4];

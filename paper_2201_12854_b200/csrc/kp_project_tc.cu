@@ -1,11 +1,15 @@
-// kp_project_tc.cu — KP: the Q/K projections of attention_matrix on tcgen05.
+// kp_project_tc.cu — KP: the layer's dense projections on tcgen05.
 //
 // attention_matrix forms Q = X W_q and
 // K = X W_k before the softmax. With W_q / W_k attached to the weights
 // (mca_set_projections) the forward takes x alone and this kernel computes
 //   [q | k] = x . [W_q | W_k]        x [M = B n, d_in],  W [d_in, 2 H 64]
 // in one persistent GEMM whose epilogue writes q and k straight into the
-// [B, n, H*64] layout the score kernels' TMA maps read.
+// [B, n, H*64] layout the score kernels' TMA maps read. regular_forward
+// adds a third segment, the exact encoding H = X W_V (fp16,
+// K4's operand), so the exact layer is one dense GEMM + the row statistics +
+// K4. Output segment s (columns [s HD, (s + 1) HD) of the product) goes to
+// tensor map s, in fp16 when bit s of f16_mask is set, else bf16.
 //
 // Operands (tc_common.cuh layout): A = x rows [128 x 64] per K step (K-major,
 // TMA 128B swizzle); B = W^T rows [BN x 64] (K-major: the handle keeps W_q /
@@ -51,14 +55,17 @@ struct Cfg {
 struct KpArgs {
     int M;          // rows of x (B * n)
     int d_in;       // K
-    int HD;         // H * 64: q columns [0, HD), k columns [HD, 2 HD) of the product
+    int HD;         // H * 64: segment s = product columns [s HD, (s + 1) HD)
+    int nseg;       // 1..3 output segments
+    int f16_mask;   // bit s: segment s stored as fp16 (else bf16)
 };
 
 template <int BN>
 __global__ void __launch_bounds__(kp::kThreads, 1) kp_project_tc(const __grid_constant__ CUtensorMap tm_x,
                                                                  const __grid_constant__ CUtensorMap tm_w,
-                                                                 const __grid_constant__ CUtensorMap tm_q,
-                                                                 const __grid_constant__ CUtensorMap tm_k, KpArgs a) {
+                                                                 const __grid_constant__ CUtensorMap tm_o0,
+                                                                 const __grid_constant__ CUtensorMap tm_o1,
+                                                                 const __grid_constant__ CUtensorMap tm_o2, KpArgs a) {
     using namespace mca_tc;
     using C = kp::Cfg<BN>;
     constexpr int S = C::kStages;
@@ -73,7 +80,7 @@ __global__ void __launch_bounds__(kp::kThreads, 1) kp_project_tc(const __grid_co
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nK = (a.d_in + kp::kBK - 1) / kp::kBK;
     const int nM = (a.M + kp::kBM - 1) / kp::kBM;
-    const int nN = 2 * a.HD / BN;
+    const int nN = a.nseg * a.HD / BN;
     const int tiles = nM * nN;
 
     if (threadIdx.x == 0) {
@@ -161,8 +168,10 @@ __global__ void __launch_bounds__(kp::kThreads, 1) kp_project_tc(const __grid_co
         uint32_t aph = 0;
         for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
             const int m0 = (t / nN) * kp::kBM, n0 = (t % nN) * BN;
-            const CUtensorMap* om = n0 < a.HD ? &tm_q : &tm_k;
-            const int oc = n0 < a.HD ? n0 : n0 - a.HD;
+            const int seg = n0 / a.HD;
+            const CUtensorMap* om = seg == 0 ? &tm_o0 : seg == 1 ? &tm_o1 : &tm_o2;
+            const int oc = n0 - seg * a.HD;
+            const bool f16 = (a.f16_mask >> seg) & 1;
             mbar_wait(acc_full + acc, aph);
             tc_fence_after();
 #pragma unroll 1
@@ -178,10 +187,17 @@ __global__ void __launch_bounds__(kp::kThreads, 1) kp_project_tc(const __grid_co
                 for (int g = 0; g < 8; ++g) {            // 16-byte chunk g = columns 8g .. 8g + 7
                     const uint32_t* src = &v[g >> 2][(g & 3) * 8];
                     uint4 u;
-                    u.x = pack_bf16x2(__uint_as_float(src[0]), __uint_as_float(src[1]));
-                    u.y = pack_bf16x2(__uint_as_float(src[2]), __uint_as_float(src[3]));
-                    u.z = pack_bf16x2(__uint_as_float(src[4]), __uint_as_float(src[5]));
-                    u.w = pack_bf16x2(__uint_as_float(src[6]), __uint_as_float(src[7]));
+                    if (f16) {
+                        u.x = pack_f16x2(__uint_as_float(src[0]), __uint_as_float(src[1]));
+                        u.y = pack_f16x2(__uint_as_float(src[2]), __uint_as_float(src[3]));
+                        u.z = pack_f16x2(__uint_as_float(src[4]), __uint_as_float(src[5]));
+                        u.w = pack_f16x2(__uint_as_float(src[6]), __uint_as_float(src[7]));
+                    } else {
+                        u.x = pack_bf16x2(__uint_as_float(src[0]), __uint_as_float(src[1]));
+                        u.y = pack_bf16x2(__uint_as_float(src[2]), __uint_as_float(src[3]));
+                        u.z = pack_bf16x2(__uint_as_float(src[4]), __uint_as_float(src[5]));
+                        u.w = pack_bf16x2(__uint_as_float(src[6]), __uint_as_float(src[7]));
+                    }
                     *reinterpret_cast<uint4*>(st + sw128_offset(r, (uint32_t)g * 16)) = u;
                 }
                 fence_proxy_async_smem();                // generic-proxy writes -> visible to the TMA store

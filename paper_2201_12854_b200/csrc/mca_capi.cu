@@ -37,6 +37,7 @@
 #include "k4_apply_tc.cu"
 #include "kp_project_tc.cu"
 #include "ka_given_attn.cu"
+#include "k4o_overflow.cu"
 #include "mca_diag.cuh"
 
 #ifndef MCA_K2_FUSED_SCAN
@@ -79,6 +80,8 @@ mca_status fail(mca_status s, const char* fmt, ...) {
 size_t dtype_size(mca_dtype t) { return t == MCA_BF16 ? 2 : 4; }
 
 constexpr int kCertCounter = 6;                // counters[6]: number of k2c-flagged token-heads
+constexpr int kOvfCounter = 7;                 // counters[7]: fp16-overflowing encodings queued for k4o_overflow
+constexpr long kOvfCap = 65536;                // queue capacity (token-heads per forward)
 constexpr size_t kMaxGraphs = 256;              // captured forwards kept per handle (LRU)
 constexpr size_t kBlasWorkspace = 32u << 20;   // explicit cuBLAS workspace (capture-safe projection GEMM)
 
@@ -192,7 +195,8 @@ struct mca_weights {
     uint16_t* guide = nullptr;    // [heads, kGuide]
     void* wprime = nullptr;       // bf16 path: [d_in, heads*dh] W_h / p (k3t's B operand)
     void* wqk = nullptr;          // optional [2][d_in][heads*dh] W_q, W_k (mca_set_projections; fp32 path)
-    void* wqk_t = nullptr;        // bf16 path: [2*heads*dh][d_in] W_q^T | W_k^T (kp_project_tc's K-major B)
+    void* wqkv_t = nullptr;       // bf16 path: [3*heads*dh][d_in] W_q^T | W_k^T | W_V^T (kp_project_tc's K-major B)
+    bool has_qk_t = false;        // the W_q^T | W_k^T rows are set (mca_set_projections)
     cublasHandle_t blas = nullptr;
     void* qk = nullptr;           // [2][B*n][heads*dh] projected q, k (workspace, grown on demand)
     long cap_qk = 0;
@@ -211,6 +215,9 @@ struct mca_weights {
     int32_t* exact_list = nullptr;            // [H, B*n] exact tokens per head
     long long* cert_list = nullptr;           // [B, H, n] Eq. 9 values at an integer boundary (k2c_certify)
     double* cert_cm = nullptr;                // [B, H, n] the score pass's cmax of each flagged entry
+    long long* ovf_list = nullptr;            // [kOvfCap] fp16-overflowing token-heads (bf16 path)
+    float* ovf_rows = nullptr;                // [kOvfCap][64] their fp32 encodings
+    long ovf_cap = 0;
     uint8_t* row_done = nullptr;              // [B, H, n] k2c's exact row-statistics cache flags
     void* zeroed = nullptr;                   // counters | task_cursor | hist | fill (zeroed once per forward)
     unsigned int* fill = nullptr;             // [H, d + 1] per-bin list fill counters (k2_scan_scatter)
@@ -254,6 +261,11 @@ void free_workspace(mca_weights* w) {
     cudaFree(w->cert_list);
     cudaFree(w->cert_cm);
     w->cert_cm = nullptr;
+    cudaFree(w->ovf_list);
+    cudaFree(w->ovf_rows);
+    w->ovf_list = nullptr;
+    w->ovf_rows = nullptr;
+    w->ovf_cap = 0;
     cudaFree(w->row_done);
     w->cert_list = nullptr;
     w->row_done = nullptr;
@@ -295,12 +307,15 @@ mca_status ensure_workspace(mca_weights* w, long tokens, mca_stream_t stream) {
         cudaMalloc(&w->exact_list, th * sizeof(int32_t)) != cudaSuccess ||
         cudaMalloc(&w->cert_list, th * sizeof(long long)) != cudaSuccess ||
         cudaMalloc(&w->cert_cm, th * sizeof(double)) != cudaSuccess ||
+        cudaMalloc(&w->ovf_list, std::min<long>((long)th, kOvfCap) * sizeof(long long)) != cudaSuccess ||
+        cudaMalloc(&w->ovf_rows, std::min<long>((long)th, kOvfCap) * 64 * sizeof(float)) != cudaSuccess ||
         cudaMalloc(&w->row_done, th * sizeof(uint8_t)) != cudaSuccess) {
         cudaGetLastError();
         free_workspace(w);
         return fail(MCA_ERR_ALLOC, "workspace allocation for %ld tokens failed", tokens);
     }
     w->cap_tokens = tokens;
+    w->ovf_cap = std::min<long>((long)th, kOvfCap);
     return MCA_OK;
 }
 
@@ -370,6 +385,10 @@ mca_status launch_k3(mca_weights* w, const void* x, int B, int n, long b_offset,
     a.exact_list = w->exact_list;
     a.counts = w->counts;
     a.task_cursor = w->task_cursor;
+    a.ovf.count = w->counters + kOvfCounter;
+    a.ovf.list = w->ovf_list;
+    a.ovf.rows = w->ovf_rows;
+    a.ovf.cap = (int)w->ovf_cap;
     // W_h staged in smem as fp32 when it fits (no unpacking in the hot loop),
     // else as bf16, else read from global memory (L1/L2).
     if (sizeof(T) == 2 && use_k3t(w)) {
@@ -475,6 +494,72 @@ mca_status launch_lists(mca_weights* w, dim3 grid, int n, long tokens, mca_strea
     return MCA_OK;
 }
 
+// The dense projection GEMM (kp_project_tc) over segments [seg0, seg0 + nseg) of
+// W^T = [W_q^T | W_k^T | W_V^T]: segment s of x W goes to outs[s] (bf16, or fp16
+// when bit s of f16_mask is set).
+mca_status launch_projection(mca_weights* w, const void* x, long tokens, int seg0, int nseg, void* const outs[3],
+                             int f16_mask, mca_stream_t stream, int& launches) {
+    const int HD = w->heads * w->dh;
+    const int BN = HD % 256 == 0 ? 256 : HD % 128 == 0 ? 128 : 64;
+    CUtensorMap tx, tw, to[3];
+    const __nv_bfloat16* wt = static_cast<const __nv_bfloat16*>(w->wqkv_t) + (size_t)seg0 * HD * w->d_in;
+    if (!make_tmap_bf16(&tx, x, (uint64_t)w->d_in, (uint64_t)tokens, 1, kp::kBM) ||
+        !make_tmap_bf16(&tw, wt, (uint64_t)w->d_in, (uint64_t)nseg * HD, 1, (uint32_t)BN))
+        return fail(MCA_ERR_CUDA, "cuTensorMapEncodeTiled failed for x / W^T");
+    int mask = 0;
+    for (int i = 0; i < 3; ++i) {
+        const int sg = std::min(seg0 + i, seg0 + nseg - 1);   // unused maps repeat the last segment
+        const bool f16 = (f16_mask >> sg) & 1;
+        if (i < nseg && f16) mask |= 1 << i;
+        if (!make_tmap_bf16(&to[i], outs[sg], (uint64_t)HD, (uint64_t)tokens, 1, kp::kBM,
+                            f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16))
+            return fail(MCA_ERR_CUDA, "cuTensorMapEncodeTiled failed for the projection outputs");
+    }
+    KpArgs pa{};
+    pa.M = (int)tokens;
+    pa.d_in = w->d_in;
+    pa.HD = HD;
+    pa.nseg = nseg;
+    pa.f16_mask = mask;
+    const long tiles = ((tokens + kp::kBM - 1) / kp::kBM) * ((long)nseg * HD / BN);
+    const dim3 grid((unsigned)std::min<long>(tiles, sm_count()));
+    auto go = [&](auto kern, uint32_t smem) -> mca_status {
+        MCA_CUDA_TRY(ensure_smem(kern, smem));
+        MCA_CUDA_TRY(launch_pdl(kern, grid, dim3(kp::kThreads), smem, stream, tx, tw, to[0], to[1], to[2], pa));
+        return MCA_OK;
+    };
+    mca_status ps = BN == 256   ? go(kp_project_tc<256>, kp::Cfg<256>::kSmemBytes)
+                    : BN == 128 ? go(kp_project_tc<128>, kp::Cfg<128>::kSmemBytes)
+                                : go(kp_project_tc<64>, kp::Cfg<64>::kSmemBytes);
+    if (ps) return ps;
+    MCA_LAUNCH_CHECK("kp_project_tc");
+    return MCA_OK;
+}
+
+// fp16 range guard's fix-up (k4o_overflow): after the aggregation, add P[:, j] H~_j
+// for the token-heads the encoders queued (normally none: one counter read).
+mca_status launch_overflow_fixup(mca_weights* w, bool given, const void* q, const void* k, const double* attn,
+                                 double scale, int B, int n, void* y, mca_stream_t stream, int& launches) {
+    K4oArgs o{};
+    o.ovf.count = w->counters + kOvfCounter;
+    o.ovf.list = w->ovf_list;
+    o.ovf.rows = w->ovf_rows;
+    o.ovf.cap = (int)w->ovf_cap;
+    o.q = q;
+    o.k = k;
+    o.lse = w->lse;
+    o.attn = attn;
+    o.scale = scale;
+    o.n = n;
+    o.heads = w->heads;
+    o.y = static_cast<__nv_bfloat16*>(y);
+    const dim3 grid((unsigned)std::min<long>((long)B * w->heads, sm_count()));
+    if (given) MCA_CUDA_TRY(launch_pdl(k4o_overflow<true>, grid, dim3(256), 0, stream, o));
+    else MCA_CUDA_TRY(launch_pdl(k4o_overflow<false>, grid, dim3(256), 0, stream, o));
+    MCA_LAUNCH_CHECK("k4o_overflow");
+    return MCA_OK;
+}
+
 // FlopsReport of the last plan from the device counters; synchronises.
 mca_status read_flops(mca_weights* w, int B, int n, bool approx, mca_flops* out, mca_stream_t stream) {
     unsigned long long c[8];
@@ -484,8 +569,8 @@ mca_status read_flops(mca_weights* w, int B, int n, bool approx, mca_flops* out,
     out->exact_encoding = (uint64_t)th * 2ull * w->d_in * w->dh;
     out->approx_encoding = approx ? c[0] : out->exact_encoding;
     out->aggregation = (uint64_t)B * w->heads * 2ull * n * n * w->dh;
-    out->samples = c[3];
-    out->exact_tokens = c[2];
+    out->samples = approx ? c[3] : 0;
+    out->exact_tokens = approx ? c[2] : (uint64_t)th;
     out->certified = c[kCertCounter];
     out->reduction_factor = (double)out->exact_encoding / (double)out->approx_encoding;
     out->total_reduction = (double)(out->exact_encoding + out->aggregation) /
@@ -585,6 +670,14 @@ mca_status mca_prepare_weights(const void* w_v, mca_dtype wdt, int d_in, int hea
         }
         k0_wprime<<<2 * sm_count(), 256, 0, stream>>>((const __nv_bfloat16*)w->w, w->probs, d_in, heads,
                                                        (__nv_bfloat16*)w->wprime, (__nv_bfloat16*)w->pbf);
+        // W_V^T as the third segment of the projection GEMM's B (the exact layer's H = X W_V)
+        if (cudaMalloc(&w->wqkv_t, 3 * wbytes) != cudaSuccess) {
+            cudaGetLastError();
+            return cleanup(fail(MCA_ERR_ALLOC, "W^T allocation failed"));
+        }
+        const int HD = heads * d_h;
+        kp_transpose<<<dim3((HD + 31) / 32, (d_in + 31) / 32), dim3(32, 8), 0, stream>>>(
+            (const __nv_bfloat16*)w->w, d_in, HD, static_cast<__nv_bfloat16*>(w->wqkv_t) + 2 * (size_t)HD * d_in);
     }
     std::vector<int> hs(heads);
     if (cudaMemcpyAsync(hs.data(), status, heads * sizeof(int), cudaMemcpyDeviceToHost, stream) != cudaSuccess ||
@@ -608,7 +701,7 @@ void mca_weights_free(mca_weights* w) {
     cudaFree(w->wprime);
     cudaFree(w->pbf);
     cudaFree(w->wqk);
-    cudaFree(w->wqk_t);
+    cudaFree(w->wqkv_t);
     cudaFree(w->qk);
     if (w->blas) cublasDestroy(w->blas);
     cudaFree(w->blas_ws);
@@ -625,18 +718,15 @@ void mca_weights_free(mca_weights* w) {
 mca_status mca_set_projections(mca_weights* w, const void* w_q, const void* w_k, mca_stream_t stream) {
     if (!w || !w_q || !w_k) return fail(MCA_ERR_NULL, "weights / w_q / w_k is NULL");
     const size_t bytes = (size_t)w->d_in * w->heads * w->dh * dtype_size(w->wdt);
-    if (w->wdt == MCA_BF16) {   // kp_project_tc: W_q^T | W_k^T, K-major, prepared once
-        if (!w->wqk_t && cudaMalloc(&w->wqk_t, 2 * bytes) != cudaSuccess) {
-            cudaGetLastError();
-            return fail(MCA_ERR_ALLOC, "W_q / W_k allocation failed");
-        }
+    if (w->wdt == MCA_BF16) {   // kp_project_tc: W_q^T | W_k^T rows of the handle's K-major W^T
         const int HD = w->heads * w->dh;
         const dim3 g((HD + 31) / 32, (w->d_in + 31) / 32);
         for (int i = 0; i < 2; ++i) {
             kp_transpose<<<g, dim3(32, 8), 0, stream>>>(static_cast<const __nv_bfloat16*>(i ? w_k : w_q), w->d_in, HD,
-                                                        static_cast<__nv_bfloat16*>(w->wqk_t) + (size_t)i * HD * w->d_in);
+                                                        static_cast<__nv_bfloat16*>(w->wqkv_t) + (size_t)i * HD * w->d_in);
             MCA_CUDA_TRY(cudaGetLastError());
         }
+        w->has_qk_t = true;
         drop_graphs(w);
         return MCA_OK;
     }
@@ -737,12 +827,13 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
         return MCA_OK;
     }
     if (!x || !y || (!q) != (!k)) return fail(MCA_ERR_NULL, "x / y is NULL, or only one of q / k is");
-    if (!q && !w->wqk && !w->wqk_t) return fail(MCA_ERR_NULL, "q / k are NULL and the weights carry no W_q / W_k");
+    if (!q && !w->wqk && !w->has_qk_t) return fail(MCA_ERR_NULL, "q / k are NULL and the weights carry no W_q / W_k");
     const long tokens = (long)B * n;
     if (mca_status s = ensure_workspace(w, tokens, stream)) return s;
     const int H = w->heads;
     int launches = 0;
     if (w->timing) MCA_CUDA_TRY(cudaEventRecord(w->ev[0], stream));
+    bool h_done = false;   // regular mode, bf16: H = x W_V came out of the projection GEMM
     if (!q) {   // q = x W_q, k = x W_k: one strided-batched GEMM (row-major C = X W as col-major C^T = W^T X^T)
         const size_t HD = (size_t)H * w->dh, esz = dtype_size(dt);
         if (tokens > w->cap_qk) {
@@ -758,34 +849,12 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
             w->cap_qk = tokens;
         }
         if (dt == MCA_BF16) {   // tcgen05 GEMM, q and k written in the score kernels' layout
-            const int HD_ = (int)HD;
-            CUtensorMap tx, tw;
-            const int BN = HD_ % 256 == 0 ? 256 : HD_ % 128 == 0 ? 128 : 64;
-            if (!make_tmap_bf16(&tx, x, (uint64_t)w->d_in, (uint64_t)tokens, 1, kp::kBM) ||
-                !make_tmap_bf16(&tw, w->wqk_t, (uint64_t)w->d_in, 2 * (uint64_t)HD_, 1, (uint32_t)BN))
-                return fail(MCA_ERR_CUDA, "cuTensorMapEncodeTiled failed for x / W_q|W_k");
-            CUtensorMap tq_out, tk_out;
-            void* q_dst = w->qk;
-            void* k_dst = static_cast<char*>(w->qk) + (size_t)tokens * HD * esz;
-            if (!make_tmap_bf16(&tq_out, q_dst, (uint64_t)HD_, (uint64_t)tokens, 1, kp::kBM) ||
-                !make_tmap_bf16(&tk_out, k_dst, (uint64_t)HD_, (uint64_t)tokens, 1, kp::kBM))
-                return fail(MCA_ERR_CUDA, "cuTensorMapEncodeTiled failed for q / k");
-            KpArgs pa{};
-            pa.M = (int)tokens;
-            pa.d_in = w->d_in;
-            pa.HD = HD_;
-            const long tiles = ((tokens + kp::kBM - 1) / kp::kBM) * (2L * HD_ / BN);
-            const dim3 grid((unsigned)std::min<long>(tiles, sm_count()));
-            auto go = [&](auto kern, uint32_t smem) -> mca_status {
-                MCA_CUDA_TRY(ensure_smem(kern, smem));
-                MCA_CUDA_TRY(launch_pdl(kern, grid, dim3(kp::kThreads), smem, stream, tx, tw, tq_out, tk_out, pa));
-                return MCA_OK;
-            };
-            mca_status ps = BN == 256   ? go(kp_project_tc<256>, kp::Cfg<256>::kSmemBytes)
-                            : BN == 128 ? go(kp_project_tc<128>, kp::Cfg<128>::kSmemBytes)
-                                        : go(kp_project_tc<64>, kp::Cfg<64>::kSmemBytes);
-            if (ps) return ps;
-            MCA_LAUNCH_CHECK("kp_project_tc");
+            // (regular mode: H = x W_V as a third segment, straight into K4's fp16 operand)
+            void* outs[3] = {w->qk, static_cast<char*>(w->qk) + (size_t)tokens * HD * esz, w->hbuf};
+            const bool dense_h = !approx && !force_simt() && !budgets_out && !exact_out;
+            if (mca_status ps = launch_projection(w, x, tokens, 0, dense_h ? 3 : 2, outs, 0b100, stream, launches))
+                return ps;
+            h_done = dense_h;
         } else {
         const float one = 1.0f, zero = 0.0f;
         const cudaDataType_t ty = CUDA_R_32F;
@@ -806,6 +875,13 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
             MCA_CUDA_TRY(cudaMemcpyAsync(dbg->q_out, q, (size_t)tokens * HD * esz, cudaMemcpyDeviceToDevice, stream));
         if (dbg && dbg->k_out)
             MCA_CUDA_TRY(cudaMemcpyAsync(dbg->k_out, k, (size_t)tokens * HD * esz, cudaMemcpyDeviceToDevice, stream));
+    }
+    // regular mode, bf16: the exact encoding H = x W_V is one dense tcgen05 GEMM
+    // (K4's fp16 operand) instead of per-head gathered exact encodings
+    if (!h_done && dt == MCA_BF16 && !approx && !force_simt() && !budgets_out && !exact_out) {
+        void* outs[3] = {nullptr, nullptr, w->hbuf};
+        if (mca_status ps = launch_projection(w, x, tokens, 2, 1, outs, 0b100, stream, launches)) return ps;
+        h_done = true;
     }
     if (w->timing) MCA_CUDA_TRY(cudaEventRecord(w->ev[1], stream));   // end of the (optional) projection
     const long th = tokens * H;
@@ -829,7 +905,7 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
 
 
     // K1 + K2 fused (bf16, n <= 768): both score passes and Eq. 9 in one kernel per (b, h)
-    const bool fused12 = dt == MCA_BF16 && !force_simt() && n <= k12::kMaxTiles * k12::kT &&
+    const bool fused12 = dt == MCA_BF16 && !force_simt() && !h_done && n <= k12::kMaxTiles * k12::kT &&
                          !(dbg && dbg->cmax_override) && w->d_in <= 1024 &&
                          k12::layout((n + k12::kT - 1) / k12::kT, w->d_in).bytes <= 227u * 1024u;
     if (fused12) {
@@ -885,15 +961,17 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
             const dim3 g1((n + 127) / 128, H, B);
             k1_scores_tc<kRowStats><<<g1, k1tc::kThreads, k1tc::kSmemBytes, stream>>>(
                 tq, tk, n, H, (float)scale, w->row_m, w->row_l, w->lse, w->colkey, w->colscore);
-            MCA_LAUNCH_CHECK("k1a_row_stats");
-            k1_scores_tc<kColMax><<<g1, k1tc::kThreads, k1tc::kSmemBytes, stream>>>(
-                tq, tk, n, H, (float)scale, w->row_m, w->row_l, w->lse, w->colkey, w->colscore);
+            if (!h_done) {   // the exact layer needs the row statistics (lse) only
+                MCA_LAUNCH_CHECK("k1a_row_stats");
+                k1_scores_tc<kColMax><<<g1, k1tc::kThreads, k1tc::kSmemBytes, stream>>>(
+                    tq, tk, n, H, (float)scale, w->row_m, w->row_l, w->lse, w->colkey, w->colscore);
+            }
         }
         MCA_LAUNCH_CHECK("k1_scores");
     }
     if (w->timing) MCA_CUDA_TRY(cudaEventRecord(w->ev[2], stream));
-    // K2: Eq. 9 budgets
-    {
+    // K2: Eq. 9 budgets (none for the dense exact layer)
+    if (!h_done) {
         const dim3 grid = bh_grid((n + 255) / 256, (long)B * H);
         K2Args a{};
         a.colkey = w->colkey;
@@ -957,8 +1035,8 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
         }
     }
     if (w->timing) MCA_CUDA_TRY(cudaEventRecord(w->ev[3], stream));
-    // K3: encoding
-    {
+    // K3: encoding (the dense exact layer's H came out of the projection GEMM)
+    if (!h_done) {
         int32_t* draws = dbg ? dbg->draws_out : nullptr;
         const int stride = dbg ? dbg->draws_stride : 0;
         mca_status s = dt == MCA_F32
@@ -993,6 +1071,8 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
             mca_diag::dump_k4(stream, n, k4tc::kBK);   // diagnostics builds only
         }
         MCA_LAUNCH_CHECK("k4_apply");
+        if (dt == MCA_BF16 && !h_done)   // encodings outside fp16's range (normally none)
+            if (mca_status s = launch_overflow_fixup(w, false, q, k, nullptr, scale, B, n, y, stream, launches)) return s;
     }
     if (w->timing) {
         MCA_CUDA_TRY(cudaEventRecord(w->ev[5], stream));
@@ -1070,6 +1150,9 @@ mca_status mca_forward_attn(mca_weights* w, const double* attn, const void* x, m
         ka_aggregate<__nv_bfloat16, __half><<<ga, kDh, 0, stream>>>(attn, (const __half*)w->hbuf, n, H,
                                                                    (__nv_bfloat16*)y);
     MCA_LAUNCH_CHECK("ka_aggregate");
+    if (dt == MCA_BF16)   // encodings outside fp16's range (normally none)
+        if (mca_status s2 = launch_overflow_fixup(w, true, nullptr, nullptr, attn, 0.0, B, n, y, stream, launches))
+            return s2;
     if (budgets_out)
         MCA_CUDA_TRY(cudaMemcpyAsync(budgets_out, w->budgets, th * sizeof(int32_t), cudaMemcpyDeviceToDevice, stream));
     if (exact_out)

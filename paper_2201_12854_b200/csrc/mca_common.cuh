@@ -194,6 +194,28 @@ struct HType { using type = float; };
 template <>
 struct HType<__nv_bfloat16> { using type = __half; };
 
+// ------------------------------------------------- fp16 H~ range guard
+// H~ is stored as fp16 on the bf16 path (K4's fp16 x fp16 P.H~ product). A
+// sampled contribution x[j,s] w[s] / (r p(s)) is unbounded (tiny p(s), outlier
+// x), so a token-head whose encoding leaves fp16's range is stored as zeros in
+// H~ and its fp32 row is queued here; k4o_overflow adds P[:, j] H~_j back into y
+// after the aggregation.
+constexpr float kH16Max = 65504.f;
+struct OvfSink {
+    unsigned long long* count;       // queued token-heads (zeroed per forward)
+    long long* list;                 // [cap] token-head t = (b H + h) n + j
+    float* rows;                     // [cap][64] the fp32 encodings
+    int cap;
+};
+// Queue token-head t; returns its slot, or -1 past the capacity (k4o_overflow traps on that).
+__device__ __forceinline__ int ovf_push(const OvfSink& o, long long t) {
+    const unsigned long long pos = atomicAdd(o.count, 1ull);
+    if (pos >= (unsigned long long)o.cap) return -1;
+    o.list[pos] = t;
+    return (int)pos;
+}
+__device__ __forceinline__ bool f16_overflows(float v) { return !(fabsf(v) <= kH16Max); }   // also inf / NaN
+
 __device__ __forceinline__ void store8(float* p, const float v[8]) {
     reinterpret_cast<float4*>(p)[0] = make_float4(v[0], v[1], v[2], v[3]);
     reinterpret_cast<float4*>(p)[1] = make_float4(v[4], v[5], v[6], v[7]);

@@ -673,3 +673,75 @@ def test_projection_gemm_shapes(mca, syn, B, n, d_in, H):
         assert _row_rel(_np(got), ref) <= 8e-3
     plain = mca.AttentionWeights(w_v, heads=H)
     assert torch.equal(y, mca.mca_forward(plain, q_out, k_out, x, cfg, seed=3).y)
+
+
+@pytest.mark.parametrize("B,n,H,d_in", [(2, 128, 12, 768), (1, 1000, 12, 768), (1, 77, 16, 1024), (2, 96, 4, 200)])
+def test_bf16_regular_forward_dense(mca, syn, orc, B, n, H, d_in):
+    """The exact layer on the bf16 path: H = x W_V as one dense tcgen05 GEMM
+    (kp_project_tc's fp16 segment), the row statistics pass, K4 -- against the
+    oracle's regular_forward on the same rounded inputs; with projections
+    attached, q, k and H come out of one three-segment GEMM."""
+    weights, w, q, k, x = _setup(mca, syn, B, n, d_in, H, torch.bfloat16, seed=n)
+    y = mca.regular_forward(weights, q, k, x)
+    torch.cuda.synchronize()
+    ref = _oracle(orc, w, q, k, x, H, mode="regular")
+    assert _row_rel(_np(y), ref.y) <= TOL_Y[torch.bfloat16]
+    out = mca.mca_forward(weights, q, k, x, mca.McaConfig(mode="regular"), flops=True)
+    assert torch.equal(out.y, y)
+    assert out.flops.reduction_factor == 1.0 and out.flops.exact_tokens == B * H * n and out.flops.samples == 0
+
+
+def test_fp16_encoding_range_guard(mca, syn, orc):
+    """bf16 path, H~ stored in fp16: a W_V row of near-zero norm (p ~ 1e-12)
+    and outlier tokens whose encodings leave fp16's range (|H~| > 65504, in
+    the sampled and the exact branch) must not produce inf / NaN or drop the
+    outliers' contribution: the encoders queue those rows in fp32 and
+    k4o_overflow adds P[:, j] H~_j back after K4."""
+    H, n, d_in = 12, 128, 768
+    w = syn.make_weights(d_in, H, seed=21)
+    w[7, :64] *= 3e-5                                   # p(7) ~ 1e-12 in head 0
+    w = w.to(torch.bfloat16)
+    inp = syn.make_inputs(1, n, d_in, H, seed=21)
+    x = inp.x.clone()
+    x[0, 5] *= 2e5                                      # outlier tokens: |H~| ~ 1e5 in every head
+    x[0, 77] *= 5e4
+    q, k, xb = (t.to(torch.bfloat16).cuda() for t in (inp.q, inp.k, x))
+    weights = mca.AttentionWeights(w.cuda(), heads=H)
+    p, _ = weights.distributions()
+    assert 0 < p[0, 7] < 1e-10
+    out = mca.mca_forward(weights, q, k, xb, mca.McaConfig(alpha=0.4), seed=3, return_plan=True)
+    torch.cuda.synchronize()
+    assert torch.isfinite(out.y.float()).all()
+    b = out.budgets.cpu().numpy()
+    e = out.exact_mask.cpu().numpy().astype(bool)
+    assert e[0, :, 5].any() or (~e[0, :, 5]).any()
+    ref = _oracle(orc, w, q, k, xb, H, alpha=0.4, seed=3, budgets_override=b, exact_override=e)
+    assert np.abs(ref.h).max() > 65504                  # the case is really out of fp16's range
+    assert _row_rel(_np(out.y), ref.y) <= TOL_Y[torch.bfloat16]
+
+
+def test_fp16_range_guard_given_attention(mca, syn, orc):
+    """The same guard on the given-attention path (cmd_bench's layer): y =
+    attn . H~ with an outlier token, against attn . (oracle H~) on the
+    device's plan."""
+    H, n, d_in = 4, 64, 256
+    w = syn.make_weights(d_in, H, seed=5).to(torch.bfloat16)
+    x = syn.make_inputs(1, n, d_in, H, seed=5).x.clone()
+    x[0, 9] *= 3e5
+    xb = x.to(torch.bfloat16).cuda()
+    rng = np.random.default_rng(0)
+    logits = rng.standard_normal((n, n)) * 2.0
+    attn = np.exp(logits - logits.max(axis=1, keepdims=True))
+    attn /= attn.sum(axis=1, keepdims=True)
+    at = torch.from_numpy(attn).cuda()[None, None].expand(1, H, n, n).contiguous()
+    weights = mca.AttentionWeights(w.cuda(), heads=H)
+    out = mca.forward_given_attention(weights, at, xb, mca.McaConfig(alpha=0.3), seed=2, return_plan=True)
+    torch.cuda.synchronize()
+    assert torch.isfinite(out.y.float()).all()
+    b = out.budgets.cpu().numpy()
+    e = out.exact_mask.cpu().numpy().astype(bool)
+    qz = torch.zeros((1, n, H * 64), dtype=torch.bfloat16, device="cuda")
+    ref = _oracle(orc, w, qz, qz, xb, H, alpha=0.3, seed=2, budgets_override=b, exact_override=e)
+    assert np.abs(ref.h).max() > 65504
+    yref = np.einsum("ij,jhd->ihd", attn, ref.h[0].reshape(n, H, 64)).reshape(n, H * 64)
+    assert _row_rel(_np(out.y[0]), yref) <= TOL_Y[torch.bfloat16]
