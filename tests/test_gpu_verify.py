@@ -110,3 +110,14 @@ def test_torch_module_stack_uses_each_layers_weights():
                                 .transpose(-1, -2) / 8.0, dim=-1)
             ref = (att @ (hs @ w_v).view(1, 32, 12, 64).transpose(1, 2)).transpose(1, 2).reshape(1, 32, 768)
             assert float((y - ref).norm() / ref.norm()) < 1e-5
+
+
+@pytest.mark.parametrize("suite", ["lemma1", "scaling", "unbiased", "theorem1", "monotone"])
+def test_verify_suite_bert_scale(verify, suite):
+    """The same acceptance criteria at BERT-base scale (d_in = 768, 12 heads,
+    synthetic BERT-init W_V, sink-model attention), 10^4 seeds per case
+    (SURVEY §8(f) #2)."""
+    rep = verify.SUITES[suite](scale="bert")
+    print(rep.csv())
+    assert rep.trials == verify.BERT_TRIALS
+    assert rep.passed, rep.csv()
