@@ -70,7 +70,7 @@ constexpr uint32_t kTileBytes = kT * kDh * 2;     // 16 KB: 128 rows x 64 bf16, 
 constexpr uint32_t kIdesc = mca_tc::idesc_f16(1, 0, kT, kT);
 
 struct Layout {
-    uint32_t q, k, lse2, comb, hist, bars, bytes;
+    uint32_t q, k, lse2, comb, hist, lmax, bars, bytes;
 };
 __host__ __device__ inline Layout layout(int nt, int d) {
     Layout L;
@@ -79,7 +79,8 @@ __host__ __device__ inline Layout layout(int nt, int d) {
     L.lse2 = 2 * nt * kTileBytes;                              // [2][128] f32: -lse2 of a query tile (qt parity)
     L.comb = L.lse2 + 2 * kT * 4;                              // A partials [2][4][128] x 8 B; B maxima [kMaxTiles][2][128] x 4 B
     L.hist = L.comb + 2 * 4 * kT * 8 + 2 * kMaxTiles * kT * 4; // [d + 1] u32 budget histogram
-    L.bars = (L.hist + (uint32_t)(d + 1) * 4 + 15) & ~15u;
+    L.lmax = L.hist + (uint32_t)(d + 1) * 4;                   // [4] u32: per-warp max |lse| of an item
+    L.bars = (L.lmax + 16 + 15) & ~15u;
     L.bytes = L.bars + 512 + 1024;                             // barriers; + alignment slack
     return L;
 }
@@ -312,6 +313,7 @@ __global__ void __maxnreg__(72)
         for (int it = blockIdx.x, li = 0; it < a.items; it += gridDim.x, ++li) {
             const int h = it % heads;
             const size_t rbase = (size_t)it * n;
+            float lmax = 0.f;                          // max |lse| of the item's queries (certification scale)
             for (int qt = 0; qt < nt; ++qt) {
                 const int gq = li * nt + qt;
                 float* s_lse2 = s_lse2b + (gq & 1) * kT;
@@ -330,6 +332,7 @@ __global__ void __maxnreg__(72)
                     const int q = qt * kT + gt;
                     if (q < n) {
                         const float lse_nat = (mn + __log2f(lt)) * 0.6931471805599453f;
+                        lmax = fmaxf(lmax, fabsf(lse_nat));
                         s_lse2[gt] = -(lse_nat * 1.4426950408889634f);   // stored negated (FFMA2 addend)
                         a.lse[rbase + q] = lse_nat;
                         a.row_m[rbase + q] = (double)mn * 0.6931471805599453;
@@ -377,7 +380,13 @@ __global__ void __maxnreg__(72)
                 }
             }
             // ---------------- Eq. 9, one key per group-B thread
+            unsigned* s_lmax = reinterpret_cast<unsigned*>(smem + L.lmax);
+            if (gt < kT) {                         // the four warps that combined the lse rows
+                const unsigned wm = __reduce_max_sync(0xffffffffu, __float_as_uint(lmax));
+                if (lane == 0) s_lmax[gt >> 5] = wm;
+            }
             named_bar_sync(2, kBThreads);          // the running maxima of this item are final
+            const float item_lmax = __uint_as_float(max(max(s_lmax[0], s_lmax[1]), max(s_lmax[2], s_lmax[3])));
             unsigned long long cost = 0, samples = 0, nexact = 0;
             for (int j = gt; j < n; j += kBThreads) {
                 const int kt = j / kT, r0 = j - kt * kT;
@@ -398,7 +407,10 @@ __global__ void __maxnreg__(72)
                     const double cm = exp2((double)vmax);
                     if (a.cmax_out) a.cmax_out[t] = cm;
                     budget_for(cm, n, a.alpha, a.min_samples, a.d, &r, &ex);
-                    if (a.cert.list && eq9_ambiguous(cm, n, a.alpha, a.min_samples, a.d)) {
+                    if (a.cert.list && eq9_ambiguous(cm, n, a.alpha, a.min_samples, a.d,
+                                                     (double)a.cert.tau_rel *
+                                                         (1.0 + fabs((double)vmax) * 0.6931471805599453 +
+                                                          2.0 * (double)item_lmax))) {
                         cert_push(a.cert, (long long)t, cm);   // k2c re-derives it in fp64 and accounts it
                         continue;
                     }

@@ -28,30 +28,52 @@
 namespace mca_dev {
 
 namespace k1tc {
-constexpr int kBM = 128, kBN = 128, kStages = 3;
+constexpr int kBM = 128, kBN = 128;
 constexpr int kConsumers = 8;
 constexpr int kThreads = 64 + kConsumers * 32;
-constexpr uint32_t kTileBytes = 128 * kDh * 2;                   // 16 KB
-constexpr uint32_t kSmemA = 0;                                    // resident operand
-constexpr uint32_t kSmemB = kTileBytes;                           // kStages streamed tiles
-constexpr uint32_t kSmemLse = kSmemB + kStages * kTileBytes;      // [kMaxN] f32 (K1b)
 constexpr int kMaxN = 4096;
-constexpr uint32_t kSmemComb = kSmemLse + kMaxN * 4;              // partner exchange, 3 x [128] x 4 B
-constexpr uint32_t kSmemBar = kSmemComb + 4 * 128 * 4;
-constexpr uint32_t kSmemBytes = kSmemBar + 256 + 1024;
-constexpr uint32_t kIdesc = mca_tc::idesc_f16(1, 0, kBM, kBN);
+constexpr uint32_t kAtomBytes = 128 * 128;                        // 128 rows x 128 B: one 128B-swizzled K atom
+// Operand layout per 128-row tile: bf16, one atom of 64 elements; or, for the
+// fp32 path (3xTF32), the hi and lo tf32 parts of the fp32 values, each two
+// atoms of 32 fp32 (part p, atom a at p * kPartBytes + a * kAtomBytes).
+template <bool kTf32>
+struct Lay {
+    static constexpr int kParts = kTf32 ? 2 : 1;
+    static constexpr int kAtoms = kTf32 ? 2 : 1;
+    static constexpr uint32_t kPartBytes = kAtoms * kAtomBytes;
+    static constexpr uint32_t kTileBytes = kParts * kPartBytes;   // 16 KB / 64 KB
+    static constexpr int kStages = kTf32 ? 2 : 3;
+    static constexpr uint32_t kSmemA = 0;                          // resident operand
+    static constexpr uint32_t kSmemB = kTileBytes;                 // kStages streamed tiles
+    static constexpr uint32_t kSmemLse = kSmemB + kStages * kTileBytes;   // [kMaxN] f32 (K1b)
+    static constexpr uint32_t kSmemComb = kSmemLse + kMaxN * 4;    // partner exchange, 3 x [128] x 4 B
+    static constexpr uint32_t kSmemBar = kSmemComb + 4 * 128 * 4;
+    static constexpr uint32_t kSmemBytes = kSmemBar + 256 + 1024;
+    static constexpr uint32_t kIdesc = kTf32 ? mca_tc::idesc_tf32(kBM, kBN) : mca_tc::idesc_f16(1, 0, kBM, kBN);
+};
+constexpr uint32_t kSmemBytes = Lay<false>::kSmemBytes;
+constexpr uint32_t kSmemBytesTf32 = Lay<true>::kSmemBytes;
 }  // namespace k1tc
 
 enum K1Mode { kRowStats = 0, kColMax = 1 };
 
-template <int kMode>
-__global__ void __launch_bounds__(k1tc::kThreads, 2)
-    k1_scores_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k, int n,
+// kTf32: the fp32 path. tm_q / tm_k hold the tf32-exact hi parts of q, k and
+// tm_q2 / tm_k2 the lo parts (fp32 - hi); S = hi.hi + hi.lo + lo.hi (3xTF32,
+// ~2^-22 relative per product), fp32 accumulation in TMEM.
+template <int kMode, bool kTf32 = false>
+__global__ void __launch_bounds__(k1tc::kThreads, kTf32 ? 1 : 2)
+    k1_scores_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                 const __grid_constant__ CUtensorMap tm_q2, const __grid_constant__ CUtensorMap tm_k2, int n,
                  int heads, float scale, double* __restrict__ row_m, double* __restrict__ row_l,
                  float* __restrict__ lse, unsigned long long* __restrict__ colkey,
                  float* __restrict__ colscore) {
     using namespace k1tc;
     using namespace mca_tc;
+    using Ly = Lay<kTf32>;
+    constexpr int kStages = Ly::kStages;
+    constexpr uint32_t kTileBytes = Ly::kTileBytes, kSmemA = Ly::kSmemA, kSmemB = Ly::kSmemB;
+    constexpr uint32_t kSmemLse = Ly::kSmemLse, kSmemComb = Ly::kSmemComb, kSmemBar = Ly::kSmemBar;
+    constexpr uint32_t kIdesc = Ly::kIdesc;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kSmemBar);
@@ -66,10 +88,21 @@ __global__ void __launch_bounds__(k1tc::kThreads, 2)
 
     const CUtensorMap* tm_a = kMode == kRowStats ? &tm_q : &tm_k;   // resident rows
     const CUtensorMap* tm_b = kMode == kRowStats ? &tm_k : &tm_q;   // streamed blocks
+    const CUtensorMap* tm_a2 = kMode == kRowStats ? &tm_q2 : &tm_k2;
+    const CUtensorMap* tm_b2 = kMode == kRowStats ? &tm_k2 : &tm_q2;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int b = blockIdx.z, h = blockIdx.y, r0 = blockIdx.x * kBM;
     const int nblk = (n + kBN - 1) / kBN;
     const size_t bh = (size_t)b * heads + h;
+    // one 128-row operand tile: every part and atom of it, arriving on `bar`
+    auto load_tile = [&](uint8_t* dst, const CUtensorMap* m1, const CUtensorMap* m2, uint64_t* bar, int row0) {
+#pragma unroll
+        for (int p = 0; p < Ly::kParts; ++p)
+#pragma unroll
+            for (int at = 0; at < Ly::kAtoms; ++at)
+                tma_load_3d(dst + p * Ly::kPartBytes + at * kAtomBytes, p ? m2 : m1, bar,
+                            h * kDh + at * (kTf32 ? 32 : 64), row0, b);
+    };
 
     if (threadIdx.x == 0) {
         mbar_init(a_full, 1);
@@ -97,12 +130,12 @@ __global__ void __launch_bounds__(k1tc::kThreads, 2)
             tma_prefetch(tm_a);
             tma_prefetch(tm_b);
             mbar_expect_tx(a_full, kTileBytes);
-            tma_load_3d(smem + kSmemA, tm_a, a_full, h * kDh, r0, b);
+            load_tile(smem + kSmemA, tm_a, tm_a2, a_full, r0);
             for (int i = 0; i < nblk; ++i) {
                 const int s = i % kStages;
                 mbar_wait(b_empty + s, ((i / kStages) & 1) ^ 1);
                 mbar_expect_tx(b_full + s, kTileBytes);
-                tma_load_3d(smem + kSmemB + s * kTileBytes, tm_b, b_full + s, h * kDh, i * kBN, b);
+                load_tile(smem + kSmemB + s * kTileBytes, tm_b, tm_b2, b_full + s, i * kBN);
             }
         }
     } else if (warp == 1) {
@@ -115,10 +148,26 @@ __global__ void __launch_bounds__(k1tc::kThreads, 2)
                 mbar_wait(s_empty + sb, ((i >> 1) & 1) ^ 1);
                 tc_fence_after();
                 const uint32_t b_addr = smem_u32(smem + kSmemB + s * kTileBytes);
+                if constexpr (!kTf32) {
 #pragma unroll
-                for (int kk = 0; kk < kDh / 16; ++kk)
-                    umma_f16(tmem + sb * kBN, sw128_desc(a_addr + kk * 32, 16, 1024),
-                             sw128_desc(b_addr + kk * 32, 16, 1024), kIdesc, kk > 0 ? 1u : 0u);
+                    for (int kk = 0; kk < kDh / 16; ++kk)
+                        umma_f16(tmem + sb * kBN, sw128_desc(a_addr + kk * 32, 16, 1024),
+                                 sw128_desc(b_addr + kk * 32, 16, 1024), kIdesc, kk > 0 ? 1u : 0u);
+                } else {   // hi.lo + lo.hi + hi.hi, K = 8 fp32 (32 B) per instruction. The small
+                           // products go first: every instruction rounds the fp32 accumulator,
+                           // and only the last eight (hi.hi) do so at the magnitude of S
+#pragma unroll
+                    for (int pr = 0; pr < 3; ++pr) {
+                        const uint32_t ap = pr == 1 ? Ly::kPartBytes : 0u, bp = pr == 0 ? Ly::kPartBytes : 0u;
+#pragma unroll
+                        for (int at = 0; at < 2; ++at)
+#pragma unroll
+                            for (int kk = 0; kk < 4; ++kk)
+                                umma_tf32(tmem + sb * kBN, sw128_desc(a_addr + ap + at * kAtomBytes + kk * 32, 16, 1024),
+                                          sw128_desc(b_addr + bp + at * kAtomBytes + kk * 32, 16, 1024), kIdesc,
+                                          (pr | at | kk) != 0);
+                    }
+                }
                 umma_commit(s_full + sb);
                 umma_commit(b_empty + s);
             }
@@ -251,4 +300,27 @@ __global__ void __launch_bounds__(k1tc::kThreads, 2)
     if (warp == 1) tmem_dealloc<256>(tmem);
 }
 
+}  // namespace mca_dev
+
+namespace mca_dev {
+// fp32 -> (hi, lo) for the 3xTF32 passes: hi keeps the top 11 significand bits
+// (exactly representable in tf32, whatever rounding the tensor core applies),
+// lo = v - hi exactly. n4 = element count / 4.
+__global__ void k_split_tf32(const float4* __restrict__ src, float4* __restrict__ hi, float4* __restrict__ lo,
+                             size_t n4) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x) {
+        const float4 v = src[i];
+        float4 a, c;
+        a.x = __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+        a.y = __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+        a.z = __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+        a.w = __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+        c.x = v.x - a.x;
+        c.y = v.y - a.y;
+        c.z = v.z - a.z;
+        c.w = v.w - a.w;
+        hi[i] = a;
+        lo[i] = c;
+    }
+}
 }  // namespace mca_dev

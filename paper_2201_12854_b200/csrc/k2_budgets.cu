@@ -101,6 +101,7 @@ __global__ void __launch_bounds__(256) k2_budgets(K2Args a) {
         int r;
         bool ex;
         bool deferred = false;
+        double cert_mag = 1.0;
         if (a.force_exact) {
             r = a.d;
             ex = true;
@@ -128,10 +129,12 @@ __global__ void __launch_bounds__(256) k2_budgets(K2Args a) {
                 }
                 const size_t ri = (size_t)bh * a.n + i;
                 cm = __ddiv_rn(exp(__dsub_rn(__dmul_rn(a.scale, s), a.row_m[ri])), a.row_l[ri]);
+                // certification scale: the winner's |t| and |lse| (k2c_certify.cu error model)
+                cert_mag = 1.0 + fabs(a.scale * s) + 2.0 * fabs(a.row_m[ri] + log(a.row_l[ri]));
             }
             if (a.cmax_out) a.cmax_out[t] = cm;
             budget_for(cm, a.n, a.alpha, a.min_samples, a.d, &r, &ex);
-            if (a.cert.list && eq9_ambiguous(cm, a.n, a.alpha, a.min_samples, a.d)) {
+            if (a.cert.list && eq9_ambiguous(cm, a.n, a.alpha, a.min_samples, a.d, (double)a.cert.tau_rel * cert_mag)) {
                 cert_push(a.cert, (long long)t, cm);   // k2c re-derives it in fp64 and accounts it
                 deferred = true;
             }

@@ -10,7 +10,7 @@
 // error of an integer could get a budget one off the fp64 reference's.
 //
 // The budget pass therefore flags every token-head whose raw value is within
-// kCertTau (relative) of an integer boundary that changes (r, exact) and
+// the pass's error bound (relative) of an integer boundary that changes (r, exact) and
 // defers it here (eq9_ambiguous / cert_push, with the pass's own cmax). This
 // kernel re-derives those column maxima in binary64 the way the oracle does
 // (oracle/tensor.cpp softmax_rows, col_max). One CTA per (b, h) item with
@@ -37,7 +37,15 @@
 
 namespace mca_dev {
 
-constexpr double kCertTau = 1e-5;   // relative distance of raw to an integer that is re-derived in fp64
+// Error model of the fp32-accumulated score passes. cmax = exp(v), v = t - lse:
+// the absolute error of v grows with the magnitudes fp32 carries, |t| and
+// |lse| (tensor-core fp32 accumulation rounds every K step). Measured
+// (scripts/tf32_accuracy.py, tests/test_gpu_configs.py): relative cmax error
+// <= ~1e-7 x M for the bf16 passes and <= ~3.4e-7 x M for the 3xTF32 passes,
+// M = 1 + |ln cmax| + 2 max|lse|. raw ~ cmax^2 doubles it; the flag threshold
+// on raw is tau_rel x M with a >= 4x margin.
+constexpr float kCertTauBf16 = 1e-6f;
+constexpr float kCertTauTf32 = 3e-6f;
 
 // Flag sink of the budget passes (K12 group B, k2_budgets): null list = off.
 struct CertSink {
@@ -45,17 +53,18 @@ struct CertSink {
     double* cm;                      // [B*H*n] the score pass's cmax of each flagged entry
     unsigned long long* count;       // number of flagged entries (zeroed per forward)
     uint8_t* row_done;               // [B*H*n] exact row statistics cached (cleared by the budget pass)
+    float tau_rel;                   // flag threshold per unit of M (kCertTauBf16 / kCertTauTf32)
 };
 
-// (r, exact) of Eq. 9 could change under a relative perturbation of cmax of
-// up to ~kCertTau / 2: raw lies within kCertTau of an integer m whose two sides
-// give different outcomes (m >= min_samples: below it both clamp to
-// min_samples; m <= d - 1: at or above d both are exact).
-__device__ __forceinline__ bool eq9_ambiguous(double cm, int n, double alpha, int min_samples, int d) {
+// (r, exact) of Eq. 9 could change under the score pass's cmax error: raw lies
+// within tau of an integer m whose two sides give different outcomes
+// (m >= min_samples: below it both clamp to min_samples; m <= d - 1: at or
+// above d both are exact). tau = tau_rel x mag, mag = 1 + |ln cm| + 2 max|lse|.
+__device__ __forceinline__ bool eq9_ambiguous(double cm, int n, double alpha, int min_samples, int d, double tau) {
     const double t = __ddiv_rn(__dmul_rn((double)n, cm), alpha);
     const double raw = __dmul_rn(t, t);
     const double m = rint(raw);
-    return m >= (double)min_samples && m <= (double)(d - 1) && fabs(raw - m) <= kCertTau * fmax(raw, 1.0);
+    return m >= (double)min_samples && m <= (double)(d - 1) && fabs(raw - m) <= tau * fmax(raw, 1.0);
 }
 
 __device__ __forceinline__ void cert_push(const CertSink& c, long long t, double cm) {

@@ -160,6 +160,20 @@ bool make_tmap_bf16(CUtensorMap* m, const void* base, uint64_t inner, uint64_t r
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// 3-D fp32 view [batch][rows][inner] with a {32, box_rows, 1} box (128 bytes) and
+// 128-byte swizzle: the tf32 operand atoms of k1_scores_tc<*, true>.
+bool make_tmap_f32(CUtensorMap* m, const void* base, uint64_t inner, uint64_t rows, uint64_t batch, uint32_t box_rows) {
+    auto enc = tmap_encoder();
+    if (!enc) return false;
+    cuuint64_t dims[3] = {inner, rows, batch};
+    cuuint64_t strides[2] = {inner * 4, rows * inner * 4};
+    cuuint32_t box[3] = {32, box_rows, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // MCA_K3_TILE=1 selects the tile-GEMM encoder (k3t) on the bf16 path; the
 // default there is the gather-scale-accumulate encoder + exact tensor-core
 // kernel (measured faster at BERT shapes).
@@ -217,6 +231,7 @@ struct mca_weights {
     double* cert_cm = nullptr;                // [B, H, n] the score pass's cmax of each flagged entry
     long long* ovf_list = nullptr;            // [kOvfCap] fp16-overflowing token-heads (bf16 path)
     float* ovf_rows = nullptr;                // [kOvfCap][64] their fp32 encodings
+    void* qk_split = nullptr;                 // fp32 path: q_hi | q_lo | k_hi | k_lo [B, n, H*64] (3xTF32)
     long ovf_cap = 0;
     uint8_t* row_done = nullptr;              // [B, H, n] k2c's exact row-statistics cache flags
     void* zeroed = nullptr;                   // counters | task_cursor | hist | fill (zeroed once per forward)
@@ -263,6 +278,8 @@ void free_workspace(mca_weights* w) {
     w->cert_cm = nullptr;
     cudaFree(w->ovf_list);
     cudaFree(w->ovf_rows);
+    cudaFree(w->qk_split);
+    w->qk_split = nullptr;
     w->ovf_list = nullptr;
     w->ovf_rows = nullptr;
     w->ovf_cap = 0;
@@ -309,6 +326,7 @@ mca_status ensure_workspace(mca_weights* w, long tokens, mca_stream_t stream) {
         cudaMalloc(&w->cert_cm, th * sizeof(double)) != cudaSuccess ||
         cudaMalloc(&w->ovf_list, std::min<long>((long)th, kOvfCap) * sizeof(long long)) != cudaSuccess ||
         cudaMalloc(&w->ovf_rows, std::min<long>((long)th, kOvfCap) * 64 * sizeof(float)) != cudaSuccess ||
+        (w->wdt == MCA_F32 && cudaMalloc(&w->qk_split, 4 * th * w->dh * sizeof(float)) != cudaSuccess) ||
         cudaMalloc(&w->row_done, th * sizeof(uint8_t)) != cudaSuccess) {
         cudaGetLastError();
         free_workspace(w);
@@ -893,7 +911,11 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
     const bool tile_k3 = dt == MCA_BF16 && use_k3t(w);   // k3t reads budgets directly: no work lists
     // bf16 score passes: Eq. 9 values within kCertTau of an integer boundary are
     // re-derived in binary64 by k2c_certify (the fp32 path's scores are fp64 already)
-    const bool certify = cfg->certify && dt == MCA_BF16 && approx &&
+    // fp32: the score passes run 3xTF32 on the tensor cores (column maxima within
+    // ~1e-6 of binary64, like the bf16 passes); their Eq. 9 boundary values are
+    // always certified, so the fp32 path keeps budgets equal to the fp64 oracle's
+    const bool tf32_scores = dt == MCA_F32 && !force_simt() && n <= k1tc::kMaxN && !h_done;
+    const bool certify = (cfg->certify || tf32_scores) && (dt == MCA_BF16 || tf32_scores) && approx &&
                          !(dbg && (dbg->budgets_override || dbg->cmax_override));
     CertSink cert{};
     if (certify) {
@@ -901,6 +923,7 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
         cert.cm = w->cert_cm;
         cert.count = w->counters + kCertCounter;
         cert.row_done = w->row_done;
+        cert.tau_rel = tf32_scores ? kCertTauTf32 : kCertTauBf16;
     }
 
 
@@ -944,7 +967,30 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
     // K1: row statistics + column maxima
     if (!fused12) {
         const dim3 grid((n + kQT - 1) / kQT, H, B);
-        if (dt == MCA_F32)
+        if (dt == MCA_F32 && tf32_scores) {   // 3xTF32 tensor-core score passes on split q, k
+            const size_t cnt = (size_t)tokens * H * kDh;
+            float* parts = static_cast<float*>(w->qk_split);   // q_hi | q_lo | k_hi | k_lo
+            const unsigned gs = (unsigned)std::min<size_t>((cnt / 4 + 255) / 256, 8 * (size_t)sm_count());
+            k_split_tf32<<<gs, 256, 0, stream>>>((const float4*)q, (float4*)parts, (float4*)(parts + cnt), cnt / 4);
+            k_split_tf32<<<gs, 256, 0, stream>>>((const float4*)k, (float4*)(parts + 2 * cnt), (float4*)(parts + 3 * cnt),
+                                                  cnt / 4);
+            MCA_LAUNCH_CHECK("k_split_tf32");
+            ++launches;
+            CUtensorMap tqh, tql, tkh, tkl;
+            if (!make_tmap_f32(&tqh, parts, (uint64_t)H * kDh, n, B, 128) ||
+                !make_tmap_f32(&tql, parts + cnt, (uint64_t)H * kDh, n, B, 128) ||
+                !make_tmap_f32(&tkh, parts + 2 * cnt, (uint64_t)H * kDh, n, B, 128) ||
+                !make_tmap_f32(&tkl, parts + 3 * cnt, (uint64_t)H * kDh, n, B, 128))
+                return fail(MCA_ERR_CUDA, "cuTensorMapEncodeTiled failed for the q/k tf32 parts");
+            MCA_CUDA_TRY(ensure_smem(k1_scores_tc<kRowStats, true>, k1tc::kSmemBytesTf32));
+            MCA_CUDA_TRY(ensure_smem(k1_scores_tc<kColMax, true>, k1tc::kSmemBytesTf32));
+            const dim3 g1((n + 127) / 128, H, B);
+            k1_scores_tc<kRowStats, true><<<g1, k1tc::kThreads, k1tc::kSmemBytesTf32, stream>>>(
+                tqh, tkh, tql, tkl, n, H, (float)scale, w->row_m, w->row_l, w->lse, w->colkey, w->colscore);
+            MCA_LAUNCH_CHECK("k1a_row_stats_tf32");
+            k1_scores_tc<kColMax, true><<<g1, k1tc::kThreads, k1tc::kSmemBytesTf32, stream>>>(
+                tqh, tkh, tql, tkl, n, H, (float)scale, w->row_m, w->row_l, w->lse, w->colkey, w->colscore);
+        } else if (dt == MCA_F32)
             k1_scores_simt<float, double><<<grid, kThreads, 0, stream>>>((const float*)q, (const float*)k, n, H, scale,
                                                                          w->row_m, w->row_l, w->lse, w->colkey);
         else if (force_simt() || n > k1tc::kMaxN)
@@ -960,11 +1006,11 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
             MCA_CUDA_TRY(ensure_smem(k1_scores_tc<kColMax>, k1tc::kSmemBytes));
             const dim3 g1((n + 127) / 128, H, B);
             k1_scores_tc<kRowStats><<<g1, k1tc::kThreads, k1tc::kSmemBytes, stream>>>(
-                tq, tk, n, H, (float)scale, w->row_m, w->row_l, w->lse, w->colkey, w->colscore);
+                tq, tk, tq, tk, n, H, (float)scale, w->row_m, w->row_l, w->lse, w->colkey, w->colscore);
             if (!h_done) {   // the exact layer needs the row statistics (lse) only
                 MCA_LAUNCH_CHECK("k1a_row_stats");
                 k1_scores_tc<kColMax><<<g1, k1tc::kThreads, k1tc::kSmemBytes, stream>>>(
-                    tq, tk, n, H, (float)scale, w->row_m, w->row_l, w->lse, w->colkey, w->colscore);
+                    tq, tk, tq, tk, n, H, (float)scale, w->row_m, w->row_l, w->lse, w->colkey, w->colscore);
             }
         }
         MCA_LAUNCH_CHECK("k1_scores");
@@ -1001,6 +1047,7 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
         a.cert = cert;
         if (!fused12) {
             if (a.cmax_in) k2_budgets<kGivenCmax, float><<<grid, 256, 0, stream>>>(a);
+            else if (tf32_scores) k2_budgets<kKeyArgmax, float><<<grid, 256, 0, stream>>>(a);   // fp64 winner re-evaluation
             else if (dt == MCA_F32) k2_budgets<kKeyValue, float><<<grid, 256, 0, stream>>>(a);
             else k2_budgets<kKeyArgmax, __nv_bfloat16><<<grid, 256, 0, stream>>>(a);
             MCA_LAUNCH_CHECK("k2_budgets");
@@ -1027,7 +1074,8 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
             c.counters = w->counters;
             c.hist = tile_k3 ? nullptr : w->hist;
             const int gc = std::min(B * H, sm_count());   // (b, h) items with flags, one CTA each
-            MCA_CUDA_TRY(launch_pdl(k2c_certify<__nv_bfloat16>, dim3((unsigned)gc), dim3(kCertThreads), 0, stream, c));
+            if (dt == MCA_F32) MCA_CUDA_TRY(launch_pdl(k2c_certify<float>, dim3((unsigned)gc), dim3(kCertThreads), 0, stream, c));
+            else MCA_CUDA_TRY(launch_pdl(k2c_certify<__nv_bfloat16>, dim3((unsigned)gc), dim3(kCertThreads), 0, stream, c));
             MCA_LAUNCH_CHECK("k2c_certify");
         }
         if (!tile_k3) {

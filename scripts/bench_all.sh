@@ -1,11 +1,8 @@
-# Round measurements: every config + the alpha sweep + the reference arm.
-set -x
-timeout 300 python bench.py --steps 20 --warmup 5 > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.err
-timeout 300 python bench.py --config c1 --steps 20 --warmup 5 --cpu-seconds 3 > gpurun_out/bench_c1.json 2> gpurun_out/bench_c1.err
-timeout 600 python bench.py --config c3 --steps 5 --warmup 3 --cpu-seconds 5 > gpurun_out/bench_c3.json 2> gpurun_out/bench_c3.err
-timeout 300 python bench.py --config c4 --steps 10 --warmup 3 --cpu-seconds 5 > gpurun_out/bench_c4.json 2> gpurun_out/bench_c4.err
-timeout 300 python bench.py --dtype f32 --steps 10 --warmup 3 --cpu-seconds 3 > gpurun_out/bench_c2_f32.json 2> gpurun_out/bench_c2_f32.err
-timeout 300 python scripts/alpha_sweep.py --out gpurun_out/alpha_sweep.jsonl > gpurun_out/alpha_sweep.log 2>&1
-timeout 400 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
-for f in gpurun_out/bench_*.json; do echo "== $f"; cut -c1-400 $f; done
-tail -n 3 gpurun_out/*.err
+# Every config's bench line (one B200) into gpurun_out/bench_<cfg>.json
+for c in c2 c1 c4 c3; do
+  steps=20; [ $c = c3 ] && steps=5
+  timeout 600 python bench.py --config $c --steps $steps --warmup 5 --cpu-seconds 8 > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err; echo ${c}_rc=$?
+done
+timeout 300 python bench.py --steps 20 --warmup 5 --certify --no-cpu-baseline > gpurun_out/bench_c2_certify.json 2> gpurun_out/bench_c2_certify.err; echo c2cert_rc=$?
+timeout 600 python bench.py --dtype f32 --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench_c2_f32.json 2> gpurun_out/bench_c2_f32.err; echo c2f32_rc=$?
+timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo ref_rc=$?
