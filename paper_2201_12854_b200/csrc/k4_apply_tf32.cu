@@ -1,0 +1,242 @@
+// k4_apply_tf32.cu — K4 for the fp32 path on the tensor cores (3xTF32):
+// y = attn . H~ (matmul, matrix.hpp:33-34) with the attention
+// never materialised, as in k4_apply_tc (bf16):
+//   S = q_i . k_j (3xTF32: hi.lo + lo.hi + hi.hi on the split operands K1
+//       left in the workspace, fp32 accumulation in TMEM)
+//   P = 2^(scale log2e S - lse2_i)   (ex2.approx.f32, the row statistics of K1)
+//   O += P . H~ (3xTF32 again: P and H~ split into tf32 hi + lo parts)
+// CTA = (b, h, 128-query tile); 64-key blocks. Operands in 128B-swizzled
+// K-major atoms of 32 fp32 (tc_common.cuh layout):
+//   Q  [128 q x 64 d]  hi | lo, resident                       64 KB
+//   K  [64 keys x 64 d] hi | lo, per block                      32 KB
+//   V  [64 d x 64 keys] hi | lo (H~ transposed per head, k_split_transpose_h)  32 KB
+//   P  [128 q x 64 keys] hi | lo, written by the softmax warps  64 KB
+// TMEM: S (64 columns) and O (64 columns).
+// Warp 0: TMA producer; warp 1: TMEM allocator + MMA issuer; warps 2-5:
+// softmax (one query row per thread) and the epilogue.
+// Overlap: K of block kb + 1 loads (and its S MMAs issue) while the softmax
+// warps turn S(kb) into P(kb); V(kb + 1) loads while P(kb) . V(kb) runs.
+#pragma once
+
+#include "mca_common.cuh"
+#include "tc_common.cuh"
+
+namespace mca_dev {
+
+namespace k4tf {
+constexpr int kBM = 128, kBK = 64;
+constexpr int kThreads = 192;
+constexpr uint32_t kAtom128 = 128 * 128;     // 128 rows x 128 B
+constexpr uint32_t kAtom64 = 64 * 128;       // 64 rows x 128 B
+constexpr uint32_t kQBytes = 2 * 2 * kAtom128;    // 2 parts x 2 atoms = 64 KB
+constexpr uint32_t kKBytes = 2 * 2 * kAtom64;     // 32 KB
+constexpr uint32_t kVBytes = 2 * 2 * kAtom64;     // 32 KB
+constexpr uint32_t kPBytes = 2 * 2 * kAtom128;    // 64 KB
+constexpr uint32_t kSmemQ = 0, kSmemK = kQBytes, kSmemV = kSmemK + kKBytes, kSmemP = kSmemV + kVBytes;
+constexpr uint32_t kSmemBar = kSmemP + kPBytes;
+constexpr uint32_t kSmemBytes = kSmemBar + 256 + 1024;
+constexpr uint32_t kIdesc = mca_tc::idesc_tf32(kBM, 64);
+}  // namespace k4tf
+
+// 3xTF32 of one [128 x 64] x [64 x 64]^T product into d: for each of the two
+// 32-wide K atoms, K = 8 per instruction; small products first (see k1_scores_tc)
+__device__ __forceinline__ void umma_3xtf32_k64(uint32_t d, uint32_t a, uint32_t a_part, uint32_t a_atom, uint32_t b,
+                                                uint32_t b_part, uint32_t b_atom, bool accumulate) {
+    using namespace mca_tc;
+#pragma unroll
+    for (int pr = 0; pr < 3; ++pr) {
+        const uint32_t ap = pr == 1 ? a_part : 0u, bp = pr == 0 ? b_part : 0u;
+#pragma unroll
+        for (int at = 0; at < 2; ++at)
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+                umma_tf32(d, sw128_desc(a + ap + at * a_atom + kk * 32, 16, 1024),
+                          sw128_desc(b + bp + at * b_atom + kk * 32, 16, 1024), k4tf::kIdesc,
+                          (accumulate || (pr | at | kk) != 0) ? 1u : 0u);
+    }
+}
+
+// maps: tm_qh / tm_ql, tm_kh / tm_kl: [B][n][H*64] fp32 views, box {32, 128} (q) / {32, 64} (k);
+// tm_vh / tm_vl: [B*H][64][n] fp32 (H~ transposed), box {32, 64}.
+__global__ void __launch_bounds__(k4tf::kThreads, 1)
+    k4_apply_tf32(const __grid_constant__ CUtensorMap tm_qh, const __grid_constant__ CUtensorMap tm_ql,
+                  const __grid_constant__ CUtensorMap tm_kh, const __grid_constant__ CUtensorMap tm_kl,
+                  const __grid_constant__ CUtensorMap tm_vh, const __grid_constant__ CUtensorMap tm_vl,
+                  const float* __restrict__ lse, int n, int heads, float scale, float* __restrict__ y) {
+    using namespace k4tf;
+    using namespace mca_tc;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kSmemBar);
+    uint64_t* q_full = bars + 0;
+    uint64_t* k_full = bars + 1;
+    uint64_t* k_empty = bars + 2;
+    uint64_t* v_full = bars + 3;
+    uint64_t* v_empty = bars + 4;
+    uint64_t* s_full = bars + 5;
+    uint64_t* s_free = bars + 6;
+    uint64_t* p_full = bars + 7;
+    uint64_t* p_free = bars + 8;
+    uint64_t* o_full = bars + 9;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int b = blockIdx.z, h = blockIdx.y, i0 = blockIdx.x * kBM;
+    const int nblk = (n + kBK - 1) / kBK;
+    const size_t bh = (size_t)b * heads + h;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < 10; ++i) mbar_init(bars + i, (i == 6 || i == 7) ? 4 : 1);   // s_free, p_full: 4 warps
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc<128>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;          // S: columns [0, 64), O: [64, 128)
+    griddep_trigger();
+
+    if (warp == 0) {
+        if (lane == 0) {   // ---------------- TMA producer
+            griddep_wait();   // H~ (transposed) and the split q / k of this forward
+            mbar_expect_tx(q_full, kQBytes);
+            for (int p = 0; p < 2; ++p)
+                for (int at = 0; at < 2; ++at)
+                    tma_load_3d(smem + kSmemQ + p * 2 * kAtom128 + at * kAtom128, p ? &tm_ql : &tm_qh, q_full,
+                                h * kDh + at * 32, i0, b);
+            for (int kb = 0; kb < nblk; ++kb) {
+                mbar_wait(k_empty, (kb & 1) ^ 1);
+                mbar_expect_tx(k_full, kKBytes);
+                for (int p = 0; p < 2; ++p)
+                    for (int at = 0; at < 2; ++at)
+                        tma_load_3d(smem + kSmemK + p * 2 * kAtom64 + at * kAtom64, p ? &tm_kl : &tm_kh, k_full,
+                                    h * kDh + at * 32, kb * kBK, b);
+                mbar_wait(v_empty, (kb & 1) ^ 1);
+                mbar_expect_tx(v_full, kVBytes);
+                for (int p = 0; p < 2; ++p)
+                    for (int at = 0; at < 2; ++at)
+                        tma_load_3d(smem + kSmemV + p * 2 * kAtom64 + at * kAtom64, p ? &tm_vl : &tm_vh, v_full,
+                                    kb * kBK + at * 32, 0, (int)bh);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {   // ---------------- MMA issuer
+            const uint32_t sq = smem_u32(smem + kSmemQ), sk = smem_u32(smem + kSmemK);
+            const uint32_t sv = smem_u32(smem + kSmemV), sp = smem_u32(smem + kSmemP);
+            mbar_wait(q_full, 0);
+            mbar_wait(k_full, 0);
+            tc_fence_after();
+            umma_3xtf32_k64(tmem, sq, 2 * kAtom128, kAtom128, sk, 2 * kAtom64, kAtom64, false);   // S(0)
+            umma_commit(s_full);
+            umma_commit(k_empty);
+            for (int kb = 0; kb < nblk; ++kb) {
+                if (kb + 1 < nblk) {   // S(kb + 1) runs while the softmax warps turn S(kb) into P(kb)
+                    mbar_wait(k_full, (kb + 1) & 1);
+                    mbar_wait(s_free, kb & 1);          // S(kb) is in the softmax warps' registers
+                    tc_fence_after();
+                    umma_3xtf32_k64(tmem, sq, 2 * kAtom128, kAtom128, sk, 2 * kAtom64, kAtom64, false);
+                    umma_commit(s_full);
+                    umma_commit(k_empty);
+                }
+                mbar_wait(p_full, kb & 1);
+                mbar_wait(v_full, kb & 1);
+                tc_fence_after();
+                umma_3xtf32_k64(tmem + 64, sp, 2 * kAtom128, kAtom128, sv, 2 * kAtom64, kAtom64, kb > 0);
+                umma_commit(p_free);
+                umma_commit(v_empty);
+            }
+            umma_commit(o_full);
+        }
+    } else {   // ------------------------------- softmax + epilogue (warps 2-5)
+        const int quad = warp & 3;
+        const int r = quad * 32 + lane;                 // TMEM lane = query row of the tile
+        const uint32_t lane_base = tmem + ((uint32_t)(quad * 32) << 16);
+        const float c2 = scale * 1.4426950408889634f;
+        const float l2 = (i0 + r < n) ? lse[bh * n + i0 + r] * 1.4426950408889634f : 0.f;
+        for (int kb = 0; kb < nblk; ++kb) {
+            mbar_wait(s_full, kb & 1);
+            tc_fence_after();
+            uint32_t sv[2][32];
+            tmem_ld32(lane_base, sv[0]);
+            tmem_ld32(lane_base + 32, sv[1]);
+            tmem_ld_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(s_free);
+            const int valid = min(kBK, n - kb * kBK);
+            mbar_wait(p_free, (kb & 1) ^ 1);            // P(kb - 1) . V has read the P buffer
+#pragma unroll
+            for (int at = 0; at < 2; ++at) {
+#pragma unroll
+                for (int g = 0; g < 8; ++g) {           // 16-byte chunk g of atom at: keys 32 at + 4 g ..
+                    float hi[4], lo[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const int c = at * 32 + g * 4 + e;
+                        const float p = c < valid ? ex2_approx(__fmaf_rn(__uint_as_float(sv[c >> 5][c & 31]), c2, -l2))
+                                                  : 0.f;
+                        hi[e] = __uint_as_float(__float_as_uint(p) & 0xFFFFE000u);
+                        lo[e] = p - hi[e];
+                    }
+                    const uint32_t off = at * kAtom128 + sw128_offset((uint32_t)r, (uint32_t)g * 16);
+                    *reinterpret_cast<float4*>(smem + kSmemP + off) = make_float4(hi[0], hi[1], hi[2], hi[3]);
+                    *reinterpret_cast<float4*>(smem + kSmemP + 2 * kAtom128 + off) =
+                        make_float4(lo[0], lo[1], lo[2], lo[3]);
+                }
+            }
+            fence_proxy_async_smem();                   // generic-proxy writes -> the tensor core
+            __syncwarp();
+            if (lane == 0) mbar_arrive(p_full);
+        }
+        // epilogue: O (fp32, exact 3xTF32 accumulation) -> y
+        mbar_wait(o_full, 0);
+        tc_fence_after();
+        uint32_t ov[2][32];
+        tmem_ld32(lane_base + 64, ov[0]);
+        tmem_ld32(lane_base + 96, ov[1]);
+        tmem_ld_wait();
+        if (i0 + r < n) {
+            float4* dst = reinterpret_cast<float4*>(y + ((size_t)b * n + i0 + r) * heads * kDh + (size_t)h * kDh);
+#pragma unroll
+            for (int g = 0; g < 16; ++g)
+                dst[g] = make_float4(__uint_as_float(ov[(4 * g) >> 5][(4 * g) & 31]),
+                                     __uint_as_float(ov[(4 * g + 1) >> 5][(4 * g + 1) & 31]),
+                                     __uint_as_float(ov[(4 * g + 2) >> 5][(4 * g + 2) & 31]),
+                                     __uint_as_float(ov[(4 * g + 3) >> 5][(4 * g + 3) & 31]));
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) tmem_dealloc<128>(tmem);
+}
+
+// H~ [B, n, H*64] fp32 -> per head transposed, split: V^T hi / lo [B*H][64][ld]
+// (the K-major B operand of P . H~; ld = n rounded up to 4 for TMA's 16-byte
+// stride rule). grid (ceil(n / 32), H, B), block (32, 8).
+__global__ void k_split_transpose_h(const float* __restrict__ hm, int n, int ld, int heads, float* __restrict__ vh,
+                                    float* __restrict__ vl) {
+    __shared__ float tile[2][32][33];
+    const int j0 = blockIdx.x * 32, h = blockIdx.y, b = blockIdx.z;
+    const size_t HD = (size_t)heads * kDh;
+    const size_t bh = (size_t)b * heads + h;
+    for (int half = 0; half < 2; ++half) {                  // dims [32 half, +32)
+        for (int jj = threadIdx.y; jj < 32; jj += 8) {
+            const int j = j0 + jj;
+            tile[half][jj][threadIdx.x] = j < n ? hm[((size_t)b * n + j) * HD + (size_t)h * kDh + half * 32 + threadIdx.x] : 0.f;
+        }
+    }
+    __syncthreads();
+    for (int half = 0; half < 2; ++half) {
+        for (int dd = threadIdx.y; dd < 32; dd += 8) {
+            const int j = j0 + threadIdx.x;
+            if (j < n) {
+                const float v = tile[half][threadIdx.x][dd];
+                const float hi = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+                const size_t o = (bh * kDh + half * 32 + dd) * (size_t)ld + j;
+                vh[o] = hi;
+                vl[o] = v - hi;
+            }
+        }
+    }
+}
+
+}  // namespace mca_dev

@@ -35,6 +35,7 @@
 #include "k3t_encode_tc.cu"
 #include "k4_apply_simt.cu"
 #include "k4_apply_tc.cu"
+#include "k4_apply_tf32.cu"
 #include "kp_project_tc.cu"
 #include "ka_given_attn.cu"
 #include "k4o_overflow.cu"
@@ -232,6 +233,8 @@ struct mca_weights {
     long long* ovf_list = nullptr;            // [kOvfCap] fp16-overflowing token-heads (bf16 path)
     float* ovf_rows = nullptr;                // [kOvfCap][64] their fp32 encodings
     void* qk_split = nullptr;                 // fp32 path: q_hi | q_lo | k_hi | k_lo [B, n, H*64] (3xTF32)
+    float* vt_split = nullptr;                // fp32 path: H~ transposed hi | lo [B*H][64][n_pad] (K4 3xTF32)
+    size_t cap_vt = 0;                        // floats
     long ovf_cap = 0;
     uint8_t* row_done = nullptr;              // [B, H, n] k2c's exact row-statistics cache flags
     void* zeroed = nullptr;                   // counters | task_cursor | hist | fill (zeroed once per forward)
@@ -280,6 +283,9 @@ void free_workspace(mca_weights* w) {
     cudaFree(w->ovf_rows);
     cudaFree(w->qk_split);
     w->qk_split = nullptr;
+    cudaFree(w->vt_split);
+    w->vt_split = nullptr;
+    w->cap_vt = 0;
     w->ovf_list = nullptr;
     w->ovf_rows = nullptr;
     w->ovf_cap = 0;
@@ -1098,7 +1104,51 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
     // K4: y = A . H~
     {
         const dim3 grid((n + kQT4 - 1) / kQT4, H, B);
-        if (dt == MCA_F32)
+        if (dt == MCA_F32 && tf32_scores) {   // 3xTF32 on the tensor cores: split q / k from K1, H~^T split here
+            const int n_pad = (n + 3) & ~3;     // TMA: the transposed rows' stride is a multiple of 16 B
+            const size_t need = 2 * (size_t)B * H * kDh * n_pad;
+            if (need > w->cap_vt) {
+                if (w->cap_vt) MCA_CUDA_TRY(cudaStreamSynchronize(stream));
+                drop_graphs(w);
+                cudaFree(w->vt_split);
+                w->vt_split = nullptr;
+                w->cap_vt = 0;
+                if (cudaMalloc(&w->vt_split, need * sizeof(float)) != cudaSuccess) {
+                    cudaGetLastError();
+                    return fail(MCA_ERR_ALLOC, "H~ split workspace allocation failed");
+                }
+                w->cap_vt = need;
+            }
+            float* vh = w->vt_split;
+            float* vl = w->vt_split + need / 2;
+            k_split_transpose_h<<<dim3((n + 31) / 32, H, B), dim3(32, 8), 0, stream>>>((const float*)w->hbuf, n, n_pad,
+                                                                                        H, vh, vl);
+            MCA_LAUNCH_CHECK("k_split_transpose_h");
+            const size_t cnt = (size_t)tokens * H * kDh;
+            float* parts = static_cast<float*>(w->qk_split);
+            CUtensorMap tqh, tql, tkh, tkl, tvh, tvl;
+            auto vmap = [&](CUtensorMap* m, const float* base) {
+                auto enc = tmap_encoder();
+                if (!enc) return false;
+                cuuint64_t dims[3] = {(cuuint64_t)n, (cuuint64_t)kDh, (cuuint64_t)B * H};
+                cuuint64_t strides[2] = {(cuuint64_t)n_pad * 4, (cuuint64_t)kDh * n_pad * 4};
+                cuuint32_t box[3] = {32, 64, 1};
+                cuuint32_t estr[3] = {1, 1, 1};
+                return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+            };
+            if (!make_tmap_f32(&tqh, parts, (uint64_t)H * kDh, n, B, 128) ||
+                !make_tmap_f32(&tql, parts + cnt, (uint64_t)H * kDh, n, B, 128) ||
+                !make_tmap_f32(&tkh, parts + 2 * cnt, (uint64_t)H * kDh, n, B, 64) ||
+                !make_tmap_f32(&tkl, parts + 3 * cnt, (uint64_t)H * kDh, n, B, 64) || !vmap(&tvh, vh) ||
+                !vmap(&tvl, vl))
+                return fail(MCA_ERR_CUDA, "cuTensorMapEncodeTiled failed for the K4 tf32 operands");
+            MCA_CUDA_TRY(ensure_smem(k4_apply_tf32, k4tf::kSmemBytes));
+            const dim3 g4((n + k4tf::kBM - 1) / k4tf::kBM, H, B);
+            MCA_CUDA_TRY(launch_pdl(k4_apply_tf32, g4, dim3(k4tf::kThreads), k4tf::kSmemBytes, stream, tqh, tql, tkh,
+                                    tkl, tvh, tvl, (const float*)w->lse, n, H, (float)scale, (float*)y));
+        } else if (dt == MCA_F32)
             k4_apply_simt<float><<<grid, kT4, 0, stream>>>((const float*)q, (const float*)k, (const float*)w->hbuf,
                                                             w->lse, n, H, (float)scale, (float*)y);
         else if (force_simt())
