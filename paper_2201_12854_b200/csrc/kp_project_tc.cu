@@ -35,20 +35,30 @@
 namespace mca_dev {
 
 namespace kp {
-constexpr int kBM = 128, kBK = 64;
+constexpr int kBM = 128;
 constexpr int kThreads = 192;
-template <int BN>
+// kTf32 (the fp32 path, 3xTF32): x and W^T arrive as tf32-exact hi and lo
+// parts; a K step is one 128-byte atom of 32 fp32 per part, and the product
+// is hi.lo + lo.hi + hi.hi (small products first, k1_scores_tc.cu). bf16: a
+// K step is one atom of 64 bf16. Outputs are staged [128 x 128 B] per chunk
+// (64 bf16 / fp16 or 32 fp32 columns).
+template <int BN, bool kTf32 = false>
 struct Cfg {
-    static constexpr int kStages = BN == 256 ? 4 : 6;
-    static constexpr uint32_t kABytes = kBM * kBK * 2;           // 16 KB
-    static constexpr uint32_t kBBytes = BN * kBK * 2;            // 8 / 16 / 32 KB
+    static constexpr int kBK = kTf32 ? 32 : 64;                  // elements per K step (one 128-byte atom)
+    static constexpr int kParts = kTf32 ? 2 : 1;
+    static constexpr int kStages = kTf32 ? (BN == 256 ? 2 : 3) : (BN == 256 ? 4 : 6);
+    static constexpr uint32_t kAPart = kBM * 128;                // 16 KB
+    static constexpr uint32_t kBPart = BN * 128;                 // 8 / 16 / 32 KB
+    static constexpr uint32_t kABytes = kParts * kAPart;
+    static constexpr uint32_t kBBytes = kParts * kBPart;
     static constexpr uint32_t kStageBytes = kABytes + kBBytes;
-    static constexpr uint32_t kSmemOut = kStages * kStageBytes;          // 2 x [128 x 64] bf16 staging tiles
-    static constexpr uint32_t kOutBytes = kBM * 64 * 2;                  // 16 KB
+    static constexpr uint32_t kSmemOut = kStages * kStageBytes;  // 2 x [128 x 128 B] staging tiles
+    static constexpr uint32_t kOutBytes = kBM * 128;             // 16 KB
+    static constexpr int kOutCols = kTf32 ? 32 : 64;             // output columns per staging tile
     static constexpr uint32_t kSmemBar = kSmemOut + 2 * kOutBytes;
     static constexpr uint32_t kSmemBytes = kSmemBar + 256 + 1024;   // barriers + 1 KB alignment slack
     static constexpr int kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;
-    static constexpr uint32_t kIdesc = mca_tc::idesc_f16(1, 0, kBM, BN);   // bf16, both K-major
+    static constexpr uint32_t kIdesc = kTf32 ? mca_tc::idesc_tf32(kBM, BN) : mca_tc::idesc_f16(1, 0, kBM, BN);
 };
 }  // namespace kp
 
@@ -60,14 +70,17 @@ struct KpArgs {
     int f16_mask;   // bit s: segment s stored as fp16 (else bf16)
 };
 
-template <int BN>
+// kTf32: tm_x / tm_w carry the hi parts and tm_x2 / tm_w2 the lo parts.
+template <int BN, bool kTf32 = false>
 __global__ void __launch_bounds__(kp::kThreads, 1) kp_project_tc(const __grid_constant__ CUtensorMap tm_x,
                                                                  const __grid_constant__ CUtensorMap tm_w,
+                                                                 const __grid_constant__ CUtensorMap tm_x2,
+                                                                 const __grid_constant__ CUtensorMap tm_w2,
                                                                  const __grid_constant__ CUtensorMap tm_o0,
                                                                  const __grid_constant__ CUtensorMap tm_o1,
                                                                  const __grid_constant__ CUtensorMap tm_o2, KpArgs a) {
     using namespace mca_tc;
-    using C = kp::Cfg<BN>;
+    using C = kp::Cfg<BN, kTf32>;
     constexpr int S = C::kStages;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -78,7 +91,7 @@ __global__ void __launch_bounds__(kp::kThreads, 1) kp_project_tc(const __grid_co
     uint64_t* acc_empty = bars + 2 * S + 2;   // [2] 4 epilogue warps
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 4);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int nK = (a.d_in + kp::kBK - 1) / kp::kBK;
+    const int nK = (a.d_in + C::kBK - 1) / C::kBK;
     const int nM = (a.M + kp::kBM - 1) / kp::kBM;
     const int nN = a.nseg * a.HD / BN;
     const int tiles = nM * nN;
@@ -116,8 +129,12 @@ __global__ void __launch_bounds__(kp::kThreads, 1) kp_project_tc(const __grid_co
                     mbar_wait(empty + s, ph ^ 1);
                     uint8_t* st = smem + s * C::kStageBytes;
                     mbar_expect_tx(full + s, C::kStageBytes);
-                    tma_load_3d(st, &tm_x, full + s, kb * kp::kBK, m0, 0);
-                    tma_load_3d(st + C::kABytes, &tm_w, full + s, kb * kp::kBK, n0, 0);
+                    tma_load_3d(st, &tm_x, full + s, kb * C::kBK, m0, 0);
+                    tma_load_3d(st + C::kABytes, &tm_w, full + s, kb * C::kBK, n0, 0);
+                    if constexpr (kTf32) {
+                        tma_load_3d(st + C::kAPart, &tm_x2, full + s, kb * C::kBK, m0, 0);
+                        tma_load_3d(st + C::kABytes + C::kBPart, &tm_w2, full + s, kb * C::kBK, n0, 0);
+                    }
                     if (++s == S) {
                         s = 0;
                         ph ^= 1;
@@ -140,10 +157,21 @@ __global__ void __launch_bounds__(kp::kThreads, 1) kp_project_tc(const __grid_co
                     tc_fence_after();
                     const uint32_t sa = smem_u32(smem + s * C::kStageBytes);
                     const uint32_t sb = sa + C::kABytes;
+                    if constexpr (kTf32) {   // hi.lo + lo.hi + hi.hi, K = 8 fp32 per instruction
 #pragma unroll
-                    for (int kk = 0; kk < kp::kBK / 16; ++kk)
-                        umma_f16(d, sw128_desc(sa + kk * 32, 16, 1024), sw128_desc(sb + kk * 32, 16, 1024), C::kIdesc,
-                                 (kb | kk) != 0);
+                        for (int pr = 0; pr < 3; ++pr) {
+                            const uint32_t ap = pr == 1 ? C::kAPart : 0u, bp = pr == 0 ? C::kBPart : 0u;
+#pragma unroll
+                            for (int kk = 0; kk < 4; ++kk)
+                                umma_tf32(d, sw128_desc(sa + ap + kk * 32, 16, 1024), sw128_desc(sb + bp + kk * 32, 16, 1024),
+                                          C::kIdesc, (kb | pr | kk) != 0);
+                        }
+                    } else {
+#pragma unroll
+                        for (int kk = 0; kk < 4; ++kk)
+                            umma_f16(d, sw128_desc(sa + kk * 32, 16, 1024), sw128_desc(sb + kk * 32, 16, 1024),
+                                     C::kIdesc, (kb | kk) != 0);
+                    }
                     umma_commit(empty + s);             // the stage is free once these MMAs read it
                     if (++s == S) {
                         s = 0;
@@ -175,30 +203,40 @@ __global__ void __launch_bounds__(kp::kThreads, 1) kp_project_tc(const __grid_co
             mbar_wait(acc_full + acc, aph);
             tc_fence_after();
 #pragma unroll 1
-            for (int c = 0; c < BN; c += 64) {
+            for (int c = 0; c < BN; c += C::kOutCols) {
                 if (et == 0) bulk_wait_read<1>();        // the store that used this buffer has read it
                 named_bar_sync(1, 128);
-                uint32_t v[2][32];
-                tmem_ld32(lane_base + (uint32_t)(acc * BN + c), v[0]);
-                tmem_ld32(lane_base + (uint32_t)(acc * BN + c + 32), v[1]);
-                tmem_ld_wait();
                 uint8_t* st = stage_out + ob * C::kOutBytes;
+                if constexpr (kTf32) {                    // 32 fp32 columns: one 128-byte row per thread
+                    uint32_t v[32];
+                    tmem_ld32(lane_base + (uint32_t)(acc * BN + c), v);
+                    tmem_ld_wait();
 #pragma unroll
-                for (int g = 0; g < 8; ++g) {            // 16-byte chunk g = columns 8g .. 8g + 7
-                    const uint32_t* src = &v[g >> 2][(g & 3) * 8];
-                    uint4 u;
-                    if (f16) {
-                        u.x = pack_f16x2(__uint_as_float(src[0]), __uint_as_float(src[1]));
-                        u.y = pack_f16x2(__uint_as_float(src[2]), __uint_as_float(src[3]));
-                        u.z = pack_f16x2(__uint_as_float(src[4]), __uint_as_float(src[5]));
-                        u.w = pack_f16x2(__uint_as_float(src[6]), __uint_as_float(src[7]));
-                    } else {
-                        u.x = pack_bf16x2(__uint_as_float(src[0]), __uint_as_float(src[1]));
-                        u.y = pack_bf16x2(__uint_as_float(src[2]), __uint_as_float(src[3]));
-                        u.z = pack_bf16x2(__uint_as_float(src[4]), __uint_as_float(src[5]));
-                        u.w = pack_bf16x2(__uint_as_float(src[6]), __uint_as_float(src[7]));
+                    for (int g = 0; g < 8; ++g)
+                        *reinterpret_cast<uint4*>(st + sw128_offset(r, (uint32_t)g * 16)) =
+                            make_uint4(v[4 * g], v[4 * g + 1], v[4 * g + 2], v[4 * g + 3]);
+                } else {
+                    uint32_t v[2][32];
+                    tmem_ld32(lane_base + (uint32_t)(acc * BN + c), v[0]);
+                    tmem_ld32(lane_base + (uint32_t)(acc * BN + c + 32), v[1]);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int g = 0; g < 8; ++g) {        // 16-byte chunk g = columns 8g .. 8g + 7
+                        const uint32_t* src = &v[g >> 2][(g & 3) * 8];
+                        uint4 u;
+                        if (f16) {
+                            u.x = pack_f16x2(__uint_as_float(src[0]), __uint_as_float(src[1]));
+                            u.y = pack_f16x2(__uint_as_float(src[2]), __uint_as_float(src[3]));
+                            u.z = pack_f16x2(__uint_as_float(src[4]), __uint_as_float(src[5]));
+                            u.w = pack_f16x2(__uint_as_float(src[6]), __uint_as_float(src[7]));
+                        } else {
+                            u.x = pack_bf16x2(__uint_as_float(src[0]), __uint_as_float(src[1]));
+                            u.y = pack_bf16x2(__uint_as_float(src[2]), __uint_as_float(src[3]));
+                            u.z = pack_bf16x2(__uint_as_float(src[4]), __uint_as_float(src[5]));
+                            u.w = pack_bf16x2(__uint_as_float(src[6]), __uint_as_float(src[7]));
+                        }
+                        *reinterpret_cast<uint4*>(st + sw128_offset(r, (uint32_t)g * 16)) = u;
                     }
-                    *reinterpret_cast<uint4*>(st + sw128_offset(r, (uint32_t)g * 16)) = u;
                 }
                 fence_proxy_async_smem();                // generic-proxy writes -> visible to the TMA store
                 named_bar_sync(1, 128);
@@ -237,5 +275,26 @@ __global__ void kp_transpose(const __nv_bfloat16* __restrict__ w, int d_in, int 
     for (int c = threadIdx.y; c < 32; c += 8)
         if (c0 + c < HD && r0 + (int)threadIdx.x < d_in)
             wt[(size_t)(c0 + c) * d_in + r0 + threadIdx.x] = tile[threadIdx.x][c];
+}
+}  // namespace mca_dev
+
+namespace mca_dev {
+// fp32 W [d_in, HD] -> W^T hi / lo [HD, d_in] (tf32-exact hi, lo = w - hi): the
+// 3xTF32 projection's K-major B parts. grid (ceil(HD / 32), ceil(d_in / 32)), block (32, 8).
+__global__ void kp_transpose_split_f32(const float* __restrict__ w, int d_in, int HD, float* __restrict__ wt_hi,
+                                       float* __restrict__ wt_lo) {
+    __shared__ float tile[32][33];
+    const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+    for (int r = threadIdx.y; r < 32; r += 8)
+        if (r0 + r < d_in && c0 + (int)threadIdx.x < HD) tile[r][threadIdx.x] = w[(size_t)(r0 + r) * HD + c0 + threadIdx.x];
+    __syncthreads();
+    for (int c = threadIdx.y; c < 32; c += 8)
+        if (c0 + c < HD && r0 + (int)threadIdx.x < d_in) {
+            const float v = tile[threadIdx.x][c];
+            const float hi = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+            const size_t o = (size_t)(c0 + c) * d_in + r0 + threadIdx.x;
+            wt_hi[o] = hi;
+            wt_lo[o] = v - hi;
+        }
 }
 }  // namespace mca_dev

@@ -7,7 +7,6 @@
 //
 // Unity build: the kernel translation units are included here so one nvcc
 // invocation produces libmca_b200.so (no relocatable device code needed).
-#include <cublas_v2.h>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
@@ -84,7 +83,6 @@ constexpr int kCertCounter = 6;                // counters[6]: number of k2c-fla
 constexpr int kOvfCounter = 7;                 // counters[7]: fp16-overflowing encodings queued for k4o_overflow
 constexpr long kOvfCap = 65536;                // queue capacity (token-heads per forward)
 constexpr size_t kMaxGraphs = 256;              // captured forwards kept per handle (LRU)
-constexpr size_t kBlasWorkspace = 32u << 20;   // explicit cuBLAS workspace (capture-safe projection GEMM)
 
 // Per-device facts and settings. Everything here is keyed by the current
 // device: one process may drive several GPUs (one handle per device), and
@@ -209,10 +207,12 @@ struct mca_weights {
     float* invp = nullptr;        // [heads, d_in]
     uint16_t* guide = nullptr;    // [heads, kGuide]
     void* wprime = nullptr;       // bf16 path: [d_in, heads*dh] W_h / p (k3t's B operand)
-    void* wqk = nullptr;          // optional [2][d_in][heads*dh] W_q, W_k (mca_set_projections; fp32 path)
-    void* wqkv_t = nullptr;       // bf16 path: [3*heads*dh][d_in] W_q^T | W_k^T | W_V^T (kp_project_tc's K-major B)
+    void* wqkv_t = nullptr;       // [3*heads*dh][d_in] W_q^T | W_k^T | W_V^T (kp_project_tc's K-major B): bf16, or
+                                  // for fp32 the tf32-exact hi parts, with the lo parts in wqkv_t_lo
+    void* wqkv_t_lo = nullptr;
+    void* x_split = nullptr;      // fp32 path: x hi | lo [B*n, d_in] (3xTF32 projection A parts)
+    long cap_x = 0;
     bool has_qk_t = false;        // the W_q^T | W_k^T rows are set (mca_set_projections)
-    cublasHandle_t blas = nullptr;
     void* qk = nullptr;           // [2][B*n][heads*dh] projected q, k (workspace, grown on demand)
     long cap_qk = 0;
     void* pbf = nullptr;          // bf16 path: [heads, d_in] bf16 p
@@ -247,7 +247,6 @@ struct mca_weights {
     // timing
     bool timing = false;
     cudaEvent_t ev[6] = {};   // stage boundaries: projection | score | budgets | encoding | aggregation
-    void* blas_ws = nullptr;                  // explicit cuBLAS workspace (capture-safe projection GEMM)
     // MCA_GRAPHS=1: CUDA graphs of repeated identical forwards (key = every argument).
     // The first call of a key runs eagerly (it may size buffers), the second is
     // captured, later ones replay the graph: one launch instead of ~10.
@@ -381,9 +380,11 @@ bool use_k3t(const mca_weights* w) {
            k3t::layout(w->d_in).bytes <= 227u * 1024u;
 }
 
+// skip_exact: the exact token-heads' encodings are already in hout (the dense GEMM).
 template <class T, class Acc>
 mca_status launch_k3(mca_weights* w, const void* x, int B, int n, long b_offset, uint32_t layer, uint64_t seed,
-                     void* hout, int32_t* draws, int draws_stride, mca_stream_t stream, int& launches) {
+                     void* hout, int32_t* draws, int draws_stride, mca_stream_t stream, int& launches,
+                     bool skip_exact = false) {
     using Coef = typename CoefT<T>::type;
     K3Args a{};
     a.x = x;
@@ -471,7 +472,8 @@ mca_status launch_k3(mca_weights* w, const void* x, int B, int n, long b_offset,
     MCA_LAUNCH_CHECK("k3_encode_sampled");
     if (bf16_kern) mca_diag::dump_k3s(stream, G1, w->heads);   // diagnostics builds only
     }
-    if (sizeof(T) == 2 && !force_simt()) {   // bf16: exact token-heads on the tensor cores
+    if (skip_exact) {
+    } else if (sizeof(T) == 2 && !force_simt()) {   // bf16: exact token-heads on the tensor cores
         MCA_CUDA_TRY(ensure_smem(k3b_exact_tc, k3btc::kSmemBytes));
         // persistent: one wave (2 CTAs per SM), CTAs loop over their head's exact tiles
         int Ge = (2 * sm_count() + w->heads - 1) / w->heads;
@@ -519,25 +521,63 @@ mca_status launch_lists(mca_weights* w, dim3 grid, int n, long tokens, mca_strea
 }
 
 // The dense projection GEMM (kp_project_tc) over segments [seg0, seg0 + nseg) of
-// W^T = [W_q^T | W_k^T | W_V^T]: segment s of x W goes to outs[s] (bf16, or fp16
-// when bit s of f16_mask is set).
+// W^T = [W_q^T | W_k^T | W_V^T]: segment s of x W goes to outs[s]. bf16 handles:
+// bf16 outputs, or fp16 when bit s of f16_mask is set. fp32 handles: 3xTF32 on
+// the hi / lo parts of x (split here) and W^T (split at preparation), fp32 outputs.
 mca_status launch_projection(mca_weights* w, const void* x, long tokens, int seg0, int nseg, void* const outs[3],
                              int f16_mask, mca_stream_t stream, int& launches) {
     const int HD = w->heads * w->dh;
+    const bool tf32 = w->wdt == MCA_F32;
     const int BN = HD % 256 == 0 ? 256 : HD % 128 == 0 ? 128 : 64;
-    CUtensorMap tx, tw, to[3];
-    const __nv_bfloat16* wt = static_cast<const __nv_bfloat16*>(w->wqkv_t) + (size_t)seg0 * HD * w->d_in;
-    if (!make_tmap_bf16(&tx, x, (uint64_t)w->d_in, (uint64_t)tokens, 1, kp::kBM) ||
-        !make_tmap_bf16(&tw, wt, (uint64_t)w->d_in, (uint64_t)nseg * HD, 1, (uint32_t)BN))
-        return fail(MCA_ERR_CUDA, "cuTensorMapEncodeTiled failed for x / W^T");
+    CUtensorMap tx, tw, tx2, tw2, to[3];
+    const size_t wofs = (size_t)seg0 * HD * w->d_in;
+    if (tf32) {
+        if (tokens > w->cap_x) {   // x hi | lo workspace
+            if (w->cap_x) MCA_CUDA_TRY(cudaStreamSynchronize(stream));
+            drop_graphs(w);
+            cudaFree(w->x_split);
+            w->x_split = nullptr;
+            w->cap_x = 0;
+            if (cudaMalloc(&w->x_split, 2 * (size_t)tokens * w->d_in * sizeof(float)) != cudaSuccess) {
+                cudaGetLastError();
+                return fail(MCA_ERR_ALLOC, "x split workspace allocation failed");
+            }
+            w->cap_x = tokens;
+        }
+        const size_t cnt = (size_t)tokens * w->d_in;
+        float* xh = static_cast<float*>(w->x_split);
+        float* xl = xh + cnt;
+        if (cnt % 4 == 0) {
+            const unsigned gs = (unsigned)std::min<size_t>((cnt / 4 + 255) / 256, 8 * (size_t)sm_count());
+            k_split_tf32<<<gs, 256, 0, stream>>>((const float4*)x, (float4*)xh, (float4*)xl, cnt / 4);
+        } else {
+            return fail(MCA_ERR_UNSUPPORTED, "fp32 projection needs B*n*d_in divisible by 4");
+        }
+        MCA_LAUNCH_CHECK("k_split_tf32");
+        if (!make_tmap_f32(&tx, xh, (uint64_t)w->d_in, (uint64_t)tokens, 1, kp::kBM) ||
+            !make_tmap_f32(&tx2, xl, (uint64_t)w->d_in, (uint64_t)tokens, 1, kp::kBM) ||
+            !make_tmap_f32(&tw, static_cast<const float*>(w->wqkv_t) + wofs, (uint64_t)w->d_in, (uint64_t)nseg * HD,
+                           1, (uint32_t)BN) ||
+            !make_tmap_f32(&tw2, static_cast<const float*>(w->wqkv_t_lo) + wofs, (uint64_t)w->d_in,
+                           (uint64_t)nseg * HD, 1, (uint32_t)BN))
+            return fail(MCA_ERR_CUDA, "cuTensorMapEncodeTiled failed for x / W^T (tf32 parts)");
+    } else {
+        const __nv_bfloat16* wt = static_cast<const __nv_bfloat16*>(w->wqkv_t) + wofs;
+        if (!make_tmap_bf16(&tx, x, (uint64_t)w->d_in, (uint64_t)tokens, 1, kp::kBM) ||
+            !make_tmap_bf16(&tw, wt, (uint64_t)w->d_in, (uint64_t)nseg * HD, 1, (uint32_t)BN))
+            return fail(MCA_ERR_CUDA, "cuTensorMapEncodeTiled failed for x / W^T");
+        tx2 = tx;
+        tw2 = tw;
+    }
     int mask = 0;
     for (int i = 0; i < 3; ++i) {
         const int sg = std::min(seg0 + i, seg0 + nseg - 1);   // unused maps repeat the last segment
-        const bool f16 = (f16_mask >> sg) & 1;
+        const bool f16 = !tf32 && ((f16_mask >> sg) & 1);
         if (i < nseg && f16) mask |= 1 << i;
-        if (!make_tmap_bf16(&to[i], outs[sg], (uint64_t)HD, (uint64_t)tokens, 1, kp::kBM,
-                            f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16))
-            return fail(MCA_ERR_CUDA, "cuTensorMapEncodeTiled failed for the projection outputs");
+        const bool ok = tf32 ? make_tmap_f32(&to[i], outs[sg], (uint64_t)HD, (uint64_t)tokens, 1, kp::kBM)
+                             : make_tmap_bf16(&to[i], outs[sg], (uint64_t)HD, (uint64_t)tokens, 1, kp::kBM,
+                                              f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16);
+        if (!ok) return fail(MCA_ERR_CUDA, "cuTensorMapEncodeTiled failed for the projection outputs");
     }
     KpArgs pa{};
     pa.M = (int)tokens;
@@ -549,12 +589,18 @@ mca_status launch_projection(mca_weights* w, const void* x, long tokens, int seg
     const dim3 grid((unsigned)std::min<long>(tiles, sm_count()));
     auto go = [&](auto kern, uint32_t smem) -> mca_status {
         MCA_CUDA_TRY(ensure_smem(kern, smem));
-        MCA_CUDA_TRY(launch_pdl(kern, grid, dim3(kp::kThreads), smem, stream, tx, tw, to[0], to[1], to[2], pa));
+        MCA_CUDA_TRY(launch_pdl(kern, grid, dim3(kp::kThreads), smem, stream, tx, tw, tx2, tw2, to[0], to[1], to[2], pa));
         return MCA_OK;
     };
-    mca_status ps = BN == 256   ? go(kp_project_tc<256>, kp::Cfg<256>::kSmemBytes)
-                    : BN == 128 ? go(kp_project_tc<128>, kp::Cfg<128>::kSmemBytes)
-                                : go(kp_project_tc<64>, kp::Cfg<64>::kSmemBytes);
+    mca_status ps;
+    if (tf32)
+        ps = BN == 256   ? go(kp_project_tc<256, true>, kp::Cfg<256, true>::kSmemBytes)
+             : BN == 128 ? go(kp_project_tc<128, true>, kp::Cfg<128, true>::kSmemBytes)
+                         : go(kp_project_tc<64, true>, kp::Cfg<64, true>::kSmemBytes);
+    else
+        ps = BN == 256   ? go(kp_project_tc<256>, kp::Cfg<256>::kSmemBytes)
+             : BN == 128 ? go(kp_project_tc<128>, kp::Cfg<128>::kSmemBytes)
+                         : go(kp_project_tc<64>, kp::Cfg<64>::kSmemBytes);
     if (ps) return ps;
     MCA_LAUNCH_CHECK("kp_project_tc");
     return MCA_OK;
@@ -687,6 +733,16 @@ mca_status mca_prepare_weights(const void* w_v, mca_dtype wdt, int d_in, int hea
     if (wdt == MCA_F32) k0_row_sq<float><<<g0, 256, 0, stream>>>((const float*)w->w, d_in, heads, sq);
     else k0_row_sq<__nv_bfloat16><<<g0, 256, 0, stream>>>((const __nv_bfloat16*)w->w, d_in, heads, sq);
     k0_dist<<<heads, 256, 0, stream>>>(sq, d_in, w->probs, w->cdf, w->thr, w->invp, w->guide, status);
+    if (wdt == MCA_F32) {    // W_V^T hi / lo: the third segment of the 3xTF32 projection GEMM (dense H = X W_V)
+        if (cudaMalloc(&w->wqkv_t, 3 * wbytes) != cudaSuccess || cudaMalloc(&w->wqkv_t_lo, 3 * wbytes) != cudaSuccess) {
+            cudaGetLastError();
+            return cleanup(fail(MCA_ERR_ALLOC, "W^T allocation failed"));
+        }
+        const int HD = heads * d_h;
+        kp_transpose_split_f32<<<dim3((HD + 31) / 32, (d_in + 31) / 32), dim3(32, 8), 0, stream>>>(
+            (const float*)w->w, d_in, HD, static_cast<float*>(w->wqkv_t) + 2 * (size_t)HD * d_in,
+            static_cast<float*>(w->wqkv_t_lo) + 2 * (size_t)HD * d_in);
+    }
     if (wdt == MCA_BF16) {   // k3t's operands: W' = W_h / p and bf16 p
         if (cudaMalloc(&w->wprime, wbytes) != cudaSuccess || cudaMalloc(&w->pbf, hd * 2) != cudaSuccess) {
             cudaGetLastError();
@@ -724,11 +780,10 @@ void mca_weights_free(mca_weights* w) {
     cudaFree(w->guide);
     cudaFree(w->wprime);
     cudaFree(w->pbf);
-    cudaFree(w->wqk);
     cudaFree(w->wqkv_t);
+    cudaFree(w->wqkv_t_lo);
+    cudaFree(w->x_split);
     cudaFree(w->qk);
-    if (w->blas) cublasDestroy(w->blas);
-    cudaFree(w->blas_ws);
     for (auto& g : w->graphs)
         if (g.exec) cudaGraphExecDestroy(g.exec);
     cudaFree(w->zeroed);
@@ -741,7 +796,6 @@ void mca_weights_free(mca_weights* w) {
 
 mca_status mca_set_projections(mca_weights* w, const void* w_q, const void* w_k, mca_stream_t stream) {
     if (!w || !w_q || !w_k) return fail(MCA_ERR_NULL, "weights / w_q / w_k is NULL");
-    const size_t bytes = (size_t)w->d_in * w->heads * w->dh * dtype_size(w->wdt);
     if (w->wdt == MCA_BF16) {   // kp_project_tc: W_q^T | W_k^T rows of the handle's K-major W^T
         const int HD = w->heads * w->dh;
         const dim3 g((HD + 31) / 32, (w->d_in + 31) / 32);
@@ -754,21 +808,20 @@ mca_status mca_set_projections(mca_weights* w, const void* w_q, const void* w_k,
         drop_graphs(w);
         return MCA_OK;
     }
-    if (!w->wqk && cudaMalloc(&w->wqk, 2 * bytes) != cudaSuccess) {
-        cudaGetLastError();
-        return fail(MCA_ERR_ALLOC, "W_q / W_k allocation failed");
-    }
-    if (!w->blas) {
-        if (cublasCreate(&w->blas) != CUBLAS_STATUS_SUCCESS) return fail(MCA_ERR_CUDA, "cublasCreate failed");
-        if (cudaMalloc(&w->blas_ws, kBlasWorkspace) != cudaSuccess ||
-            cublasSetWorkspace(w->blas, w->blas_ws, kBlasWorkspace) != CUBLAS_STATUS_SUCCESS) {
-            cudaGetLastError();
-            return fail(MCA_ERR_ALLOC, "cuBLAS workspace allocation failed");
+    {   // fp32: W_q^T, W_k^T hi / lo parts (3xTF32)
+        const int HD = w->heads * w->dh;
+        const dim3 g((HD + 31) / 32, (w->d_in + 31) / 32);
+        for (int i = 0; i < 2; ++i) {
+            kp_transpose_split_f32<<<g, dim3(32, 8), 0, stream>>>(
+                static_cast<const float*>(i ? w_k : w_q), w->d_in, HD,
+                static_cast<float*>(w->wqkv_t) + (size_t)i * HD * w->d_in,
+                static_cast<float*>(w->wqkv_t_lo) + (size_t)i * HD * w->d_in);
+            MCA_CUDA_TRY(cudaGetLastError());
         }
+        w->has_qk_t = true;
+        drop_graphs(w);
+        return MCA_OK;
     }
-    MCA_CUDA_TRY(cudaMemcpyAsync(w->wqk, w_q, bytes, cudaMemcpyDeviceToDevice, stream));
-    MCA_CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(w->wqk) + bytes, w_k, bytes, cudaMemcpyDeviceToDevice, stream));
-    return MCA_OK;
 }
 
 mca_status mca_weights_export(const mca_weights* w, double* probs_host, double* cdf_host) {
@@ -851,14 +904,21 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
         return MCA_OK;
     }
     if (!x || !y || (!q) != (!k)) return fail(MCA_ERR_NULL, "x / y is NULL, or only one of q / k is");
-    if (!q && !w->wqk && !w->has_qk_t) return fail(MCA_ERR_NULL, "q / k are NULL and the weights carry no W_q / W_k");
+    if (!q && !w->has_qk_t) return fail(MCA_ERR_NULL, "q / k are NULL and the weights carry no W_q / W_k");
     const long tokens = (long)B * n;
     if (mca_status s = ensure_workspace(w, tokens, stream)) return s;
     const int H = w->heads;
     int launches = 0;
     if (w->timing) MCA_CUDA_TRY(cudaEventRecord(w->ev[0], stream));
-    bool h_done = false;   // regular mode, bf16: H = x W_V came out of the projection GEMM
-    if (!q) {   // q = x W_q, k = x W_k: one strided-batched GEMM (row-major C = X W as col-major C^T = W^T X^T)
+    // The exact encodings as one dense GEMM (H = x W_V, the projection kernel's third
+    // segment): the whole exact layer in regular mode (bf16: straight into K4's fp16
+    // operand); on the fp32 path also the exact branch of approximation mode, whose
+    // sampled token-heads K3 then overwrites (3xTF32, so no fp64 CUDA-core K3b).
+    const bool want_dense_h = !force_simt() &&
+                              ((dt == MCA_F32 && !(dbg && dbg->draws_out)) ||
+                               (dt == MCA_BF16 && !approx && !budgets_out && !exact_out));
+    bool h_dense = false;
+    if (!q) {   // q = x W_q, k = x W_k (+ H): one tcgen05 GEMM, outputs in the score kernels' layout
         const size_t HD = (size_t)H * w->dh, esz = dtype_size(dt);
         if (tokens > w->cap_qk) {
             if (w->cap_qk) MCA_CUDA_TRY(cudaStreamSynchronize(stream));
@@ -872,27 +932,10 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
             }
             w->cap_qk = tokens;
         }
-        if (dt == MCA_BF16) {   // tcgen05 GEMM, q and k written in the score kernels' layout
-            // (regular mode: H = x W_V as a third segment, straight into K4's fp16 operand)
-            void* outs[3] = {w->qk, static_cast<char*>(w->qk) + (size_t)tokens * HD * esz, w->hbuf};
-            const bool dense_h = !approx && !force_simt() && !budgets_out && !exact_out;
-            if (mca_status ps = launch_projection(w, x, tokens, 0, dense_h ? 3 : 2, outs, 0b100, stream, launches))
-                return ps;
-            h_done = dense_h;
-        } else {
-        const float one = 1.0f, zero = 0.0f;
-        const cudaDataType_t ty = CUDA_R_32F;
-        const cublasComputeType_t ct = CUBLAS_COMPUTE_32F_PEDANTIC;
-        // cublasSetStream resets the handle's workspace to cuBLAS's pool: re-attach
-        // the explicit one (no allocation inside a captured forward)
-        if (cublasSetStream(w->blas, stream) != CUBLAS_STATUS_SUCCESS ||
-            cublasSetWorkspace(w->blas, w->blas_ws, kBlasWorkspace) != CUBLAS_STATUS_SUCCESS ||
-            cublasGemmStridedBatchedEx(w->blas, CUBLAS_OP_N, CUBLAS_OP_N, (int)HD, (int)tokens, w->d_in, &one, w->wqk,
-                                       ty, (int)HD, (long long)w->d_in * HD, x, ty, w->d_in, 0, &zero, w->qk, ty,
-                                       (int)HD, (long long)tokens * HD, 2, ct,
-                                       CUBLAS_GEMM_DEFAULT) != CUBLAS_STATUS_SUCCESS)
-            return fail(MCA_ERR_CUDA, "q / k projection GEMM failed");
-        }
+        void* outs[3] = {w->qk, static_cast<char*>(w->qk) + (size_t)tokens * HD * esz, w->hbuf};
+        if (mca_status ps = launch_projection(w, x, tokens, 0, want_dense_h ? 3 : 2, outs, 0b100, stream, launches))
+            return ps;
+        h_dense = want_dense_h;
         q = w->qk;
         k = static_cast<const char*>(w->qk) + (size_t)tokens * HD * esz;
         if (dbg && dbg->q_out)
@@ -900,13 +943,12 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
         if (dbg && dbg->k_out)
             MCA_CUDA_TRY(cudaMemcpyAsync(dbg->k_out, k, (size_t)tokens * HD * esz, cudaMemcpyDeviceToDevice, stream));
     }
-    // regular mode, bf16: the exact encoding H = x W_V is one dense tcgen05 GEMM
-    // (K4's fp16 operand) instead of per-head gathered exact encodings
-    if (!h_done && dt == MCA_BF16 && !approx && !force_simt() && !budgets_out && !exact_out) {
+    if (want_dense_h && !h_dense) {   // given q, k: the H segment alone
         void* outs[3] = {nullptr, nullptr, w->hbuf};
         if (mca_status ps = launch_projection(w, x, tokens, 2, 1, outs, 0b100, stream, launches)) return ps;
-        h_done = true;
+        h_dense = true;
     }
+    const bool h_done = h_dense && !approx;   // regular mode: no budgets, no encoders
     if (w->timing) MCA_CUDA_TRY(cudaEventRecord(w->ev[1], stream));   // end of the (optional) projection
     const long th = tokens * H;
     const double scale = cfg->scale > 0.0 ? cfg->scale : 1.0 / std::sqrt((double)w->dh);
@@ -920,7 +962,7 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
     // fp32: the score passes run 3xTF32 on the tensor cores (column maxima within
     // ~1e-6 of binary64, like the bf16 passes); their Eq. 9 boundary values are
     // always certified, so the fp32 path keeps budgets equal to the fp64 oracle's
-    const bool tf32_scores = dt == MCA_F32 && !force_simt() && n <= k1tc::kMaxN && !h_done;
+    const bool tf32_scores = dt == MCA_F32 && !force_simt() && n <= k1tc::kMaxN;
     const bool certify = (cfg->certify || tf32_scores) && (dt == MCA_BF16 || tf32_scores) && approx &&
                          !(dbg && (dbg->budgets_override || dbg->cmax_override));
     CertSink cert{};
@@ -993,9 +1035,11 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
             const dim3 g1((n + 127) / 128, H, B);
             k1_scores_tc<kRowStats, true><<<g1, k1tc::kThreads, k1tc::kSmemBytesTf32, stream>>>(
                 tqh, tkh, tql, tkl, n, H, (float)scale, w->row_m, w->row_l, w->lse, w->colkey, w->colscore);
-            MCA_LAUNCH_CHECK("k1a_row_stats_tf32");
-            k1_scores_tc<kColMax, true><<<g1, k1tc::kThreads, k1tc::kSmemBytesTf32, stream>>>(
-                tqh, tkh, tql, tkl, n, H, (float)scale, w->row_m, w->row_l, w->lse, w->colkey, w->colscore);
+            if (!h_done) {   // the exact layer needs the row statistics (lse) only
+                MCA_LAUNCH_CHECK("k1a_row_stats_tf32");
+                k1_scores_tc<kColMax, true><<<g1, k1tc::kThreads, k1tc::kSmemBytesTf32, stream>>>(
+                    tqh, tkh, tql, tkl, n, H, (float)scale, w->row_m, w->row_l, w->lse, w->colkey, w->colscore);
+            }
         } else if (dt == MCA_F32)
             k1_scores_simt<float, double><<<grid, kThreads, 0, stream>>>((const float*)q, (const float*)k, n, H, scale,
                                                                          w->row_m, w->row_l, w->lse, w->colkey);
@@ -1095,7 +1139,7 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
         const int stride = dbg ? dbg->draws_stride : 0;
         mca_status s = dt == MCA_F32
                            ? launch_k3<float, double>(w, x, B, n, b_offset, layer, seed, w->hbuf, draws, stride,
-                                                      stream, launches)
+                                                      stream, launches, h_dense)
                            : launch_k3<__nv_bfloat16, float>(w, x, B, n, b_offset, layer, seed, w->hbuf, draws, stride,
                                                              stream, launches);
         if (s) return s;
