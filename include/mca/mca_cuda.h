@@ -122,9 +122,9 @@ mca_status mca_prepare_weights(const void* w_v, mca_dtype wdt, int d_in, int hea
 void mca_weights_free(mca_weights* w);
 
 /* Attach W_q and W_k ([d_in, heads*d_h], the weights' dtype, device
- * pointers; copied). A forward called with q == k == NULL then computes
- * q = x W_q and k = x W_k on `stream` first (one strided-batched GEMM, fp32
- * accumulation; the fp32 path without TF32). */
+ * pointers; copied, transposed). A forward called with q == k == NULL then
+ * computes q = x W_q and k = x W_k on `stream` first (the tcgen05 projection
+ * GEMM: bf16 with fp32 accumulation, 3xTF32 on the fp32 path). */
 mca_status mca_set_projections(mca_weights* w, const void* w_q, const void* w_k, mca_stream_t stream);
 
 /* Copy the per-head fp64 probabilities / cdf ([heads, d_in], host buffers). */
