@@ -469,10 +469,14 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     pipe = HostPipeline(layer_weights, n, chunk, dtype, dev, depth=depth)
 
     def e2e_step():
-        pipe.forward(hq, hk, hx, hy, cfg, seed=42, b_offset=b_offset)
+        # serving-style: back-to-back steps pipeline across steps (the next step's
+        # H2D and forward overlap this step's D2H); every step still moves its
+        # own x in and y out, and the timed region ends when the last y landed
+        pipe.forward(hq, hk, hx, hy, cfg, seed=42, b_offset=b_offset, sync=False)
 
     for _ in range(max(1, args.warmup)):
         e2e_step()
+    pipe.wait()
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
@@ -480,6 +484,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     e0.record(stream)
     for _ in range(args.steps):
         e2e_step()
+    pipe.wait()
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1) / args.steps

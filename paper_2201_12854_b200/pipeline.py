@@ -44,11 +44,15 @@ class HostPipeline:
         self.used = [False] * self.depth
 
     def forward(self, hq: torch.Tensor | None, hk: torch.Tensor | None, hx: torch.Tensor, hy: torch.Tensor,
-                cfg: McaConfig | None = None, seed: int = 0, b_offset: int = 0) -> None:
+                cfg: McaConfig | None = None, seed: int = 0, b_offset: int = 0, sync: bool = True) -> None:
         """hq, hk: [B, n, H*64] (None: the weights carry W_q / W_k and only x is
         transferred), hx: [B, n, d_in] pinned host tensors; writes hy
         [B, n, H*64] (pinned host). Asynchronous: returns once the work is
-        enqueued; the d2h stream's completion (`self.s_d2h`) marks hy ready."""
+        enqueued. sync=True: the caller's current stream waits for hy
+        (stream-ordered, like one mca_forward). sync=False: it does not, so
+        back-to-back calls pipeline across calls too (the next call's H2D and
+        forward overlap this call's D2H; slots are reused only after their
+        read-back); `wait()` joins the current stream to every read-back."""
         B = hx.shape[0]
         if hq is None and not self.project:
             raise ValueError("q / k omitted but the layers carry no W_q / W_k")
@@ -56,7 +60,7 @@ class HostPipeline:
             raise ValueError(f"batch [{B}, {hx.shape[1]}] does not split into chunks of {self.chunk} x {self.n}")
         cur = torch.cuda.current_stream(self.device)
         for st in (self.s_h2d, self.s_comp, self.s_d2h):
-            st.wait_stream(cur)
+            st.wait_stream(cur)   # device-side inputs / weights the caller enqueued before this call
         for c in range(B // self.chunk):
             i = c % self.depth
             sl = self.slots[i]
@@ -84,4 +88,9 @@ class HostPipeline:
                 hy[rows].copy_(xin, non_blocking=True)
                 self.freed[i].record(self.s_d2h)
             self.used[i] = True
-        cur.wait_stream(self.s_d2h)
+        if sync:
+            cur.wait_stream(self.s_d2h)
+
+    def wait(self) -> None:
+        """The caller's current stream waits for every read-back enqueued so far."""
+        torch.cuda.current_stream(self.device).wait_stream(self.s_d2h)

@@ -501,6 +501,12 @@ def test_host_pipeline_matches_forward(mca, syn):
         pipe.forward(hq, hk, hx, hy, cfg, seed=5, b_offset=3)   # slots reused across calls
         torch.cuda.synchronize()
         assert torch.equal(hy, ref_x.cpu()), L
+        hy.zero_()
+        for _ in range(3):                                      # pipelined across calls (the bench's e2e loop)
+            pipe.forward(hq, hk, hx, hy, cfg, seed=5, b_offset=3, sync=False)
+        pipe.wait()
+        torch.cuda.synchronize()
+        assert torch.equal(hy, ref_x.cpu()), L
 
 
 @pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
