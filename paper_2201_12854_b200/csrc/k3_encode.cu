@@ -105,22 +105,28 @@ __device__ __forceinline__ void load4w(const __nv_bfloat16* base, size_t stride,
 
 // Shared-memory footprint: sampler tables + the per-warp sample-pair buffers +
 // (optionally) W_h in the staging type WS.
-size_t k3_smem_bytes(int d_in, size_t coef, size_t ws_elem, bool wsmem) {
+size_t k3_smem_bytes(int d_in, size_t coef, size_t ws_elem, bool wsmem, int cols = kDh) {
     const size_t tables = (((size_t)d_in * (8 + coef) + kGuide * 2) + 127) & ~(size_t)127;
     const size_t pairs = (size_t)kK3Warps * 4 * 16 * 16;   // sizeof(SamplePair<Acc>) = 16 (alignas) for either Acc
-    return tables + pairs + (wsmem ? (size_t)d_in * kDh * ws_elem : 0);
+    return tables + pairs + (wsmem ? (size_t)d_in * cols * ws_elem : 0);
 }
 
 // T: activation / output dtype; WS: W_h staging dtype in smem (fp32 when it
 // fits, so the hot loop does no unpacking); Acc: accumulation type.
 // Lane l of an octet owns output columns [8l, 8l+8): the octet reads a sampled
 // bf16 row as eight 16-byte pieces, one shared-memory wavefront per sample.
-template <class T, class WS, class Acc, bool kWSmem>
+// kCols = 4 (fp32 path): the CTA covers half of the head's 64 output columns
+// (blockIdx.z = half; both halves draw the same samples), so its fp32 W_h half
+// (d_in x 32) fits in shared memory beside the tables: one 128-byte wavefront
+// per sample (4 fp32 per lane) instead of 256-byte row reads from L2.
+template <class T, class WS, class Acc, bool kWSmem, int kCols = 8>
 __global__ void __launch_bounds__(kK3BlockThreads, 1) k3_encode_sampled(K3Args a) {
+    constexpr int kW = kCols * 8;   // output columns this CTA encodes (64, or 32 for a half)
     using Coef = typename CoefT<T>::type;
     using Pair = SamplePair<Acc>;
     extern __shared__ __align__(16) unsigned char smem[];
     const int h = blockIdx.y;
+    const int half = kCols == 8 ? 0 : (int)blockIdx.z;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int oct = lane >> 3, l8 = lane & 7;
     const unsigned omask = 0xFFu << (oct * 8);
@@ -142,23 +148,26 @@ __global__ void __launch_bounds__(kK3BlockThreads, 1) k3_encode_sampled(K3Args a
         else s_coef[i] = (Coef)a.invp[(size_t)h * d_in + i];
     }
     for (int g = tid; g < kGuide; g += kK3BlockThreads) s_guide[g] = a.guide[(size_t)h * kGuide + g];
-    if constexpr (kWSmem) {   // W_h -> smem, converted to WS, 8 elements per thread-iteration
-        for (int e = tid; e < d_in * (kDh / 8); e += kK3BlockThreads) {
-            const int i = e / (kDh / 8), c8 = (e % (kDh / 8)) * 8;
+    if constexpr (kWSmem) {   // W_h (or its column half) -> smem, converted to WS, 8 elements per thread-iteration
+        for (int e = tid; e < d_in * (kW / 8); e += kK3BlockThreads) {
+            const int i = e / (kW / 8), c8 = (e % (kW / 8)) * 8;
             float v[8];
-            load8(wv + (size_t)i * HD + (size_t)h * kDh + c8, v);
+            load8(wv + (size_t)i * HD + (size_t)h * kDh + half * kW + c8, v);
             if constexpr (sizeof(WS) == 4) {
-                reinterpret_cast<float4*>(s_w + (size_t)i * kDh + c8)[0] = make_float4(v[0], v[1], v[2], v[3]);
-                reinterpret_cast<float4*>(s_w + (size_t)i * kDh + c8)[1] = make_float4(v[4], v[5], v[6], v[7]);
+                reinterpret_cast<float4*>(s_w + (size_t)i * kW + c8)[0] = make_float4(v[0], v[1], v[2], v[3]);
+                reinterpret_cast<float4*>(s_w + (size_t)i * kW + c8)[1] = make_float4(v[4], v[5], v[6], v[7]);
             } else {
-                store8(reinterpret_cast<__nv_bfloat16*>(s_w) + (size_t)i * kDh + c8, v);
+                store8(reinterpret_cast<__nv_bfloat16*>(s_w) + (size_t)i * kW + c8, v);
             }
         }
     }
     __syncthreads();
-    const WS* wsrc = kWSmem ? s_w : reinterpret_cast<const WS*>(wv + (size_t)h * kDh);
-    const size_t wstride = kWSmem ? (size_t)kDh : HD;
-    const int col0 = 8 * l8;   // lane owns columns [8l, 8l+8): one conflict-free 16-byte bf16 read per sample
+    const WS* wsrc = kWSmem ? s_w : reinterpret_cast<const WS*>(wv + (size_t)h * kDh + half * kW);
+    const size_t wstride = kWSmem ? (size_t)kW : HD;
+    // lane owns columns [kCols l, kCols l + kCols) of the CTA's kW: one conflict-free
+    // 16-byte read per sample (8 bf16 or 4 fp32)
+    const int wcol = kCols * l8;
+    const int col0 = half * kW + wcol;
     const int nsamp = a.counts[2 * h];
     const int32_t* list = a.samp_list + (size_t)h * a.tokens;
     const T* x = reinterpret_cast<const T*>(a.x);
@@ -198,8 +207,16 @@ __global__ void __launch_bounds__(kK3BlockThreads, 1) k3_encode_sampled(K3Args a
         for (int u = 0; u < 4; ++u) acc2[u] = make_float2(0.f, 0.f);
         auto accumulate = [&](const Pair& p) {
             float w[8];
-            load8(wsrc + (size_t)p.row * wstride + col0, w);
-            if constexpr (sizeof(Acc) == 4) {
+            if constexpr (kCols == 4) {
+                const float4 w4 = *reinterpret_cast<const float4*>(wsrc + (size_t)p.row * wstride + wcol);
+                w[0] = w4.x; w[1] = w4.y; w[2] = w4.z; w[3] = w4.w;
+            } else {
+                load8(wsrc + (size_t)p.row * wstride + wcol, w);
+            }
+            if constexpr (kCols == 4) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) acc[q] += p.coef * (Acc)w[q];
+            } else if constexpr (sizeof(Acc) == 4) {
                 const float2 cc = make_float2((float)p.coef, (float)p.coef);
 #pragma unroll
                 for (int q = 0; q < 4; ++q) acc2[q] = __ffma2_rn(make_float2(w[2 * q], w[2 * q + 1]), cc, acc2[q]);
@@ -220,7 +237,7 @@ __global__ void __launch_bounds__(kK3BlockThreads, 1) k3_encode_sampled(K3Args a
             p0.coef = coef(i0, x0);
             p1.row = (uint32_t)i1;
             p1.coef = coef(i1, x1);
-            if (a.draws_out) {
+            if (a.draws_out && half == 0) {
                 const int k0 = base + 2 * l8;
                 if (k0 < r && k0 < a.draws_stride) a.draws_out[tokh * a.draws_stride + k0] = i0;
                 if (k0 + 1 < r && k0 + 1 < a.draws_stride) a.draws_out[tokh * a.draws_stride + k0 + 1] = i1;
@@ -236,11 +253,16 @@ __global__ void __launch_bounds__(kK3BlockThreads, 1) k3_encode_sampled(K3Args a
             } else {
                 for (int s2 = 0; s2 < cnt; ++s2) accumulate(my_pairs[s2]);
             }
-            if (l8 == 0) my_samples += (unsigned long long)cnt;
+            if (l8 == 0 && half == 0) my_samples += (unsigned long long)cnt;
         }
         __syncwarp(omask);
-        if (a.draws_out && l8 == 0)
+        if (a.draws_out && l8 == 0 && half == 0)
             for (int k = r; k < a.draws_stride; ++k) a.draws_out[tokh * a.draws_stride + k] = -1;
+        if constexpr (kCols == 4) {   // fp32 path: 4 columns per lane
+            *reinterpret_cast<float4*>(reinterpret_cast<float*>(hout) + tok * HD + (size_t)h * kDh + col0) =
+                make_float4((float)acc[0], (float)acc[1], (float)acc[2], (float)acc[3]);
+            return;
+        }
         if constexpr (sizeof(Acc) == 4) {
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
@@ -281,7 +303,7 @@ __global__ void __launch_bounds__(kK3BlockThreads, 1) k3_encode_sampled(K3Args a
     // first is encoded, so the second token's start-up latency is hidden.
     for (;;) {
         int t0 = 0;
-        if (lane == 0) t0 = atomicAdd(a.task_cursor + h, 8);
+        if (lane == 0) t0 = atomicAdd(a.task_cursor + h + half * heads, 8);   // each half walks the list
         t0 = __shfl_sync(0xffffffffu, t0, 0);
         if (t0 >= nsamp) break;
         const int ea = t0 + oct, eb = t0 + 4 + oct;

@@ -243,7 +243,7 @@ struct mca_weights {
     unsigned int* hist = nullptr;             // [H, d_in + 1] budget histogram
     unsigned int* cursor = nullptr;           // [H, d_in + 1] scatter cursors
     int* counts = nullptr;                    // [H, 2] sampled / exact token counts
-    int* task_cursor = nullptr;               // [H] K3 work cursor
+    int* task_cursor = nullptr;               // [2][H] K3 work cursors
     // timing
     bool timing = false;
     cudaEvent_t ev[6] = {};   // stage boundaries: projection | score | budgets | encoding | aggregation
@@ -373,7 +373,9 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
 }
 
 // counters (64 B) | task cursors | budget histograms [H, d + 1] | list fill counters [H, d + 1]
-size_t zeroed_bytes(int heads, int d_in) { return 64 + (((size_t)heads * 4 + 63) & ~(size_t)63) + 2 * (size_t)heads * (d_in + 1) * 4; }
+// counters (64 B) | task cursors [2][H] (K3; the fp32 column halves walk the lists separately)
+// | budget histograms [H, d + 1] | list fill counters [H, d + 1]
+size_t zeroed_bytes(int heads, int d_in) { return 64 + (((size_t)heads * 8 + 63) & ~(size_t)63) + 2 * (size_t)heads * (d_in + 1) * 4; }
 
 bool use_k3t(const mca_weights* w) {
     return w->wdt == MCA_BF16 && w->wprime && !force_simt() && tile_k3_requested() && w->d_in % 8 == 0 &&
@@ -438,6 +440,7 @@ mca_status launch_k3(mca_weights* w, const void* x, int B, int n, long b_offset,
     // per sample; smem bandwidth, not issue, bounds this loop) / fp32 for the
     // fp32 parity path.
     void (*kern)(K3Args) = nullptr;
+    bool launched = false;
     size_t smem = k3_smem_bytes(w->d_in, sizeof(Coef), sizeof(T), true);
     constexpr size_t kMaxSmem = 220 * 1024;
     if (sizeof(T) == 2 && k3_bf16_smem_bytes(w->d_in) <= kMaxSmem) {
@@ -446,6 +449,26 @@ mca_status launch_k3(mca_weights* w, const void* x, int B, int n, long b_offset,
                : w->d_in == 768 ? k3_encode_sampled_bf16<768>
                : w->d_in == 1024 ? k3_encode_sampled_bf16<1024>
                                  : k3_encode_sampled_bf16<0>;
+    } else if (sizeof(T) == 4 && a.tokens * w->heads <= (1L << 16) &&
+               k3_smem_bytes(w->d_in, sizeof(Coef), 4, true, kDh / 2) <= kMaxSmem) {
+        // fp32, small batches (latency-bound: C1 0.19 -> 0.10 ms): two CTAs per
+        // head-task, each with its fp32 half of W_h resident. At C2 the doubled
+        // draws cost more than the L2 row reads save (0.91 vs 0.79 ms).
+        if constexpr (sizeof(T) == 4) {
+            smem = k3_smem_bytes(w->d_in, sizeof(Coef), 4, true, kDh / 2);
+            auto kh = k3_encode_sampled<float, float, double, true, 4>;
+            MCA_CUDA_TRY(ensure_smem(kh, smem));
+            int occ = 0;
+            MCA_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kh, kK3BlockThreads, smem));
+            if (occ < 1) occ = 1;
+            int G = sm_count() * occ / (2 * w->heads);
+            const long cap = (a.tokens + 63) / 64;
+            if (G > cap) G = (int)cap;
+            if (G < 1) G = 1;
+            kh<<<dim3(G, w->heads, 2), kK3BlockThreads, smem, stream>>>(a);
+            MCA_LAUNCH_CHECK("k3_encode_sampled_f32h");
+            launched = true;
+        }
     } else if (smem <= kMaxSmem) {
         if constexpr (sizeof(T) == 2) kern = k3_encode_sampled<__nv_bfloat16, __nv_bfloat16, float, true>;
         else kern = k3_encode_sampled<float, float, double, true>;
@@ -454,6 +477,7 @@ mca_status launch_k3(mca_weights* w, const void* x, int B, int n, long b_offset,
         if constexpr (sizeof(T) == 2) kern = k3_encode_sampled<__nv_bfloat16, __nv_bfloat16, float, false>;
         else kern = k3_encode_sampled<float, float, double, false>;
     }
+    if (!launched) {
     MCA_CUDA_TRY(ensure_smem(kern, smem));
     int occ = 0;
     MCA_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kK3BlockThreads, smem));
@@ -471,6 +495,7 @@ mca_status launch_k3(mca_weights* w, const void* x, int B, int n, long b_offset,
     else kern<<<dim3(G, w->heads), kK3BlockThreads, smem, stream>>>(a);
     MCA_LAUNCH_CHECK("k3_encode_sampled");
     if (bf16_kern) mca_diag::dump_k3s(stream, G1, w->heads);   // diagnostics builds only
+    }
     }
     if (skip_exact) {
     } else if (sizeof(T) == 2 && !force_simt()) {   // bf16: exact token-heads on the tensor cores
@@ -725,7 +750,7 @@ mca_status mca_prepare_weights(const void* w_v, mca_dtype wdt, int d_in, int hea
     // counters | task cursors | budget histograms: one region, one memset per forward
     w->counters = static_cast<unsigned long long*>(w->zeroed);
     w->task_cursor = reinterpret_cast<int*>(static_cast<char*>(w->zeroed) + 64);
-    w->hist = reinterpret_cast<unsigned int*>(static_cast<char*>(w->zeroed) + 64 + ((heads * 4 + 63) & ~63));
+    w->hist = reinterpret_cast<unsigned int*>(static_cast<char*>(w->zeroed) + 64 + ((heads * 8 + 63) & ~63));
     w->fill = w->hist + (size_t)heads * (d_in + 1);
     if (cudaMemcpyAsync(w->w, w_v, wbytes, cudaMemcpyDeviceToDevice, stream) != cudaSuccess)
         return cleanup(fail(MCA_ERR_CUDA, "copying w_v failed: %s", cudaGetErrorString(cudaGetLastError())));
