@@ -27,6 +27,7 @@
 // ring), warp 1 TMEM allocator + single-thread MMA issuer, warps 2-9 load Q
 // into TMEM, then softmax and the epilogue. TMEM (256 columns, two CTAs per
 // SM): S/P0 [0,64), S/P1 [64,128), O [128,192), Q [192,224).
+#include "k4o_overflow.cu"
 #include "mca_common.cuh"
 #include "tc_common.cuh"
 
@@ -70,7 +71,8 @@ __device__ __forceinline__ uint32_t k4_p_col(int sb, int kk) {
 __global__ void __launch_bounds__(k4tc::kThreads, 2)
     k4_apply_tc(const __nv_bfloat16* __restrict__ q, const __grid_constant__ CUtensorMap tm_k,
                 const __grid_constant__ CUtensorMap tm_h, const float* __restrict__ lse, int n, int heads,
-                int batch, float scale, __nv_bfloat16* __restrict__ y) {
+                int batch, float scale, __nv_bfloat16* __restrict__ y, const K4oArgs oa,
+                unsigned long long* __restrict__ done_ctas) {
     using namespace k4tc;
     using namespace mca_tc;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -314,6 +316,23 @@ __global__ void __launch_bounds__(k4tc::kThreads, 2)
     tc_fence_before();
     __syncthreads();
     if (warp == 1) tmem_dealloc<256>(tmem);
+    // fp16 range guard (k4o_overflow.cu): the last CTA to finish adds P[:, j] H~_j for
+    // the encodings the encoders queued (normally none: one atomic per CTA)
+    if (done_ctas) {
+        int* s_last = reinterpret_cast<int*>(smem);
+        if (threadIdx.x == 0) {
+            __threadfence();
+            s_last[0] = atomicAdd(done_ctas, 1ull) == (unsigned long long)gridDim.x - 1;
+        }
+        __syncthreads();
+        if (s_last[0]) {
+            __threadfence();
+            const unsigned long long cnt = *(volatile const unsigned long long*)oa.ovf.count;
+            if (cnt > (unsigned long long)oa.ovf.cap) __trap();
+            if (cnt) ovf_fixup<false>(oa, cnt, 0, 1, reinterpret_cast<float*>(smem + 1024),
+                                      reinterpret_cast<float*>(smem + 2048));
+        }
+    }
 }
 
 }  // namespace mca_dev

@@ -8,8 +8,10 @@
 // with P_ij = exp(a q_i.k_j - lse_i) recomputed from the score pass's row
 // statistics (the forward), or the given attention entry (mca_forward_attn).
 // The queue is empty unless the weights or inputs are extreme (a row of W_V
-// with a tiny p(s) drawn for an outlier x), so the kernel
-// normally reads one counter and exits.
+// with a tiny p(s) drawn for an outlier x). On the
+// forward the fix-up runs at the end of K4 itself, in the last CTA to finish
+// (k4_apply_tc: no extra launch); the given-attention path launches
+// k4o_overflow after ka_aggregate.
 #pragma once
 
 #include "mca_common.cuh"
@@ -27,17 +29,14 @@ struct K4oArgs {
     __nv_bfloat16* y;                // [B, n, H*64]
 };
 
+// The fix-up for queue entries e0, e0 + step, ... by the calling CTA (every
+// thread of it; s_h, s_k: 64 floats each of shared memory).
 template <bool kGiven>
-__global__ void __launch_bounds__(256) k4o_overflow(K4oArgs a) {
-    __shared__ float s_h[kDh], s_k[kDh];
-    griddep_trigger();
-    griddep_wait();                  // the aggregation's y and the encoders' queue
-    const unsigned long long cnt = *(volatile const unsigned long long*)a.ovf.count;
-    if (cnt == 0) return;
-    if (cnt > (unsigned long long)a.ovf.cap) __trap();   // more out-of-range encodings than the queue holds
+__device__ __forceinline__ void ovf_fixup(const K4oArgs& a, unsigned long long cnt, unsigned long long e0,
+                                          unsigned long long step, float* s_h, float* s_k) {
     const int tid = threadIdx.x;
     const size_t HD = (size_t)a.heads * kDh;
-    for (unsigned long long e = blockIdx.x; e < cnt; e += gridDim.x) {
+    for (unsigned long long e = e0; e < cnt; e += step) {
         const long long t = a.ovf.list[e];
         const long bh = (long)(t / a.n);
         const int j = (int)(t - (long long)bh * a.n);
@@ -73,6 +72,18 @@ __global__ void __launch_bounds__(256) k4o_overflow(K4oArgs a) {
             for (int c = 0; c < kDh; c += 2) atomicAdd(yr + c / 2, __floats2bfloat162_rn(p * s_h[c], p * s_h[c + 1]));
         }
     }
+}
+
+// Standalone launch (the given-attention path): one CTA per queue entry stride.
+template <bool kGiven>
+__global__ void __launch_bounds__(256) k4o_overflow(K4oArgs a) {
+    __shared__ float s_h[kDh], s_k[kDh];
+    griddep_trigger();
+    griddep_wait();                  // the aggregation's y and the encoders' queue
+    const unsigned long long cnt = *(volatile const unsigned long long*)a.ovf.count;
+    if (cnt == 0) return;
+    if (cnt > (unsigned long long)a.ovf.cap) __trap();   // more out-of-range encodings than the queue holds
+    ovf_fixup<kGiven>(a, cnt, blockIdx.x, gridDim.x, s_h, s_k);
 }
 
 }  // namespace mca_dev

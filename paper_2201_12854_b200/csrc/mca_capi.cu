@@ -37,7 +37,6 @@
 #include "k4_apply_tf32.cu"
 #include "kp_project_tc.cu"
 #include "ka_given_attn.cu"
-#include "k4o_overflow.cu"
 #include "mca_diag.cuh"
 
 #ifndef MCA_K2_FUSED_SCAN
@@ -81,6 +80,7 @@ size_t dtype_size(mca_dtype t) { return t == MCA_BF16 ? 2 : 4; }
 
 constexpr int kCertCounter = 6;                // counters[6]: number of k2c-flagged token-heads
 constexpr int kOvfCounter = 7;                 // counters[7]: fp16-overflowing encodings queued for k4o_overflow
+constexpr int kK4DoneCounter = 5;              // counters[5]: K4 CTAs finished (its last CTA runs the range-guard fix-up)
 constexpr long kOvfCap = 65536;                // queue capacity (token-heads per forward)
 constexpr size_t kMaxGraphs = 256;              // captured forwards kept per handle (LRU)
 
@@ -1232,13 +1232,25 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
             MCA_CUDA_TRY(ensure_smem(k4_apply_tc, k4tc::kSmemBytes));
             const long tiles = (long)B * H * ((n + k4tc::kBM - 1) / k4tc::kBM);
             const int grid = (int)std::min<long>(tiles, 2L * sm_count());   // persistent: two CTAs per SM
+            K4oArgs o{};
+            o.ovf.count = w->counters + kOvfCounter;
+            o.ovf.list = w->ovf_list;
+            o.ovf.rows = w->ovf_rows;
+            o.ovf.cap = (int)w->ovf_cap;
+            o.q = q;
+            o.k = k;
+            o.lse = w->lse;
+            o.scale = scale;
+            o.n = n;
+            o.heads = H;
+            o.y = (__nv_bfloat16*)y;
             MCA_CUDA_TRY(launch_pdl(k4_apply_tc, dim3(grid), dim3(k4tc::kThreads), k4tc::kSmemBytes, stream,
                                     (const __nv_bfloat16*)q, tk, th, (const float*)w->lse, n, H, B, (float)scale,
-                                    (__nv_bfloat16*)y));
+                                    (__nv_bfloat16*)y, o, w->counters + kK4DoneCounter));
             mca_diag::dump_k4(stream, n, k4tc::kBK);   // diagnostics builds only
         }
         MCA_LAUNCH_CHECK("k4_apply");
-        if (dt == MCA_BF16 && !h_done)   // encodings outside fp16's range (normally none)
+        if (dt == MCA_BF16 && !h_done && force_simt())   // the CUDA-core K4 has no built-in range-guard fix-up
             if (mca_status s = launch_overflow_fixup(w, false, q, k, nullptr, scale, B, n, y, stream, launches)) return s;
     }
     if (w->timing) {
