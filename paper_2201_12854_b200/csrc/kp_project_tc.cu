@@ -46,7 +46,7 @@ template <int BN, bool kTf32 = false>
 struct Cfg {
     static constexpr int kBK = kTf32 ? 32 : 64;                  // elements per K step (one 128-byte atom)
     static constexpr int kParts = kTf32 ? 2 : 1;
-    static constexpr int kStages = kTf32 ? (BN == 256 ? 2 : 3) : (BN == 256 ? 4 : 6);
+    static constexpr int kStages = kTf32 ? (BN >= 192 ? 2 : 3) : (BN >= 192 ? 4 : 6);
     static constexpr uint32_t kAPart = kBM * 128;                // 16 KB
     static constexpr uint32_t kBPart = BN * 128;                 // 8 / 16 / 32 KB
     static constexpr uint32_t kABytes = kParts * kAPart;
@@ -57,7 +57,7 @@ struct Cfg {
     static constexpr int kOutCols = kTf32 ? 32 : 64;             // output columns per staging tile
     static constexpr uint32_t kSmemBar = kSmemOut + 2 * kOutBytes;
     static constexpr uint32_t kSmemBytes = kSmemBar + 256 + 1024;   // barriers + 1 KB alignment slack
-    static constexpr int kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;
+    static constexpr int kTmemCols = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
     static constexpr uint32_t kIdesc = kTf32 ? mca_tc::idesc_tf32(kBM, BN) : mca_tc::idesc_f16(1, 0, kBM, BN);
 };
 }  // namespace kp
