@@ -34,6 +34,12 @@
 
 namespace mca_dev {
 
+#ifndef KP_STAGES_256
+#define KP_STAGES_256 4
+#endif
+#ifndef KP_OUTBUFS_256
+#define KP_OUTBUFS_256 2
+#endif
 namespace kp {
 constexpr int kBM = 128;
 constexpr int kThreads = 192;
@@ -46,7 +52,8 @@ template <int BN, bool kTf32 = false>
 struct Cfg {
     static constexpr int kBK = kTf32 ? 32 : 64;                  // elements per K step (one 128-byte atom)
     static constexpr int kParts = kTf32 ? 2 : 1;
-    static constexpr int kStages = kTf32 ? (BN >= 192 ? 2 : 3) : (BN >= 192 ? 4 : 6);
+    static constexpr int kStages = kTf32 ? (BN >= 192 ? 2 : 3) : (BN >= 192 ? KP_STAGES_256 : 6);
+    static constexpr int kOutBufs = (kTf32 || BN < 192) ? 2 : KP_OUTBUFS_256;   // staging tiles in flight
     static constexpr uint32_t kAPart = kBM * 128;                // 16 KB
     static constexpr uint32_t kBPart = BN * 128;                 // 8 / 16 / 32 KB
     static constexpr uint32_t kABytes = kParts * kAPart;
@@ -55,7 +62,7 @@ struct Cfg {
     static constexpr uint32_t kSmemOut = kStages * kStageBytes;  // 2 x [128 x 128 B] staging tiles
     static constexpr uint32_t kOutBytes = kBM * 128;             // 16 KB
     static constexpr int kOutCols = kTf32 ? 32 : 64;             // output columns per staging tile
-    static constexpr uint32_t kSmemBar = kSmemOut + 2 * kOutBytes;
+    static constexpr uint32_t kSmemBar = kSmemOut + kOutBufs * kOutBytes;
     static constexpr uint32_t kSmemBytes = kSmemBar + 256 + 1024;   // barriers + 1 KB alignment slack
     static constexpr int kTmemCols = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
     static constexpr uint32_t kIdesc = kTf32 ? mca_tc::idesc_tf32(kBM, BN) : mca_tc::idesc_f16(1, 0, kBM, BN);
@@ -204,7 +211,7 @@ __global__ void __launch_bounds__(kp::kThreads, 1) kp_project_tc(const __grid_co
             tc_fence_after();
 #pragma unroll 1
             for (int c = 0; c < BN; c += C::kOutCols) {
-                if (et == 0) bulk_wait_read<1>();        // the store that used this buffer has read it
+                if (et == 0) bulk_wait_read<C::kOutBufs - 1>();   // the store that used this buffer has read it
                 named_bar_sync(1, 128);
                 uint8_t* st = stage_out + ob * C::kOutBytes;
                 if constexpr (kTf32) {                    // 32 fp32 columns: one 128-byte row per thread
@@ -244,7 +251,7 @@ __global__ void __launch_bounds__(kp::kThreads, 1) kp_project_tc(const __grid_co
                     tma_store_3d(om, st, oc + c, m0, 0);  // rows past M are clipped by the tensor map
                     bulk_commit();
                 }
-                ob ^= 1;
+                if (++ob == C::kOutBufs) ob = 0;
             }
             tc_fence_before();
             __syncwarp();
