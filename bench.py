@@ -311,10 +311,14 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     from paper_2201_12854_b200.pipeline import HostPipeline
     from paper_2201_12854_b200 import synthetic
 
-    if torch.cuda.device_count() <= local_rank:
+    # MCA_BENCH_SHARED_GPU=1 (functional tests of the N > 1 plumbing on a 1-GPU
+    # box only: every rank on device 0 over gloo; never a reported number)
+    shared = os.environ.get("MCA_BENCH_SHARED_GPU") == "1"
+    if torch.cuda.device_count() <= local_rank and not shared:
         raise SystemExit(f"rank {rank}: local rank {local_rank} but only {torch.cuda.device_count()} CUDA device(s)")
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    dev_index = 0 if shared else local_rank
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
     _, n, d_in, H, desc = CONFIGS[args.config]
     B, b_offset, GB, scaling = _shard(args, rank, world)
     dtype = torch.bfloat16 if args.dtype == "bf16" else torch.float32
@@ -322,7 +326,10 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     L = args.layers
     project = args.inputs == "x"
@@ -384,7 +391,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     flops_report = out.flops
     launches_per_step = weights.last_launch_count() * L
 
-    sampler = ClockSampler(local_rank) if rank == 0 else None
+    sampler = ClockSampler(dev_index) if rank == 0 else None
     if sampler:
         sampler.start()
     for _ in range(args.warmup):
@@ -494,12 +501,43 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         e2e_ms = float(t.item())
     clocks = sampler.stop() if sampler else None
 
-    # validation gather (outside timing): per-rank checksums of y and the plan
+    # validation (outside timing; NCCL only here): per-rank checksums of y and
+    # the plan, and for one-layer configs the outputs themselves: rank 0 gathers
+    # every shard's y and re-runs the LAST rank's shard on its own GPU from that
+    # rank's seeded inputs and weights with the same b_offset -- the shard must
+    # come back bitwise (Philox streams use the global sequence index)
     chk = torch.tensor([float(y.double().sum()), float(out.budgets.double().sum())], device=dev, dtype=torch.float64)
+    validation = {}
     if dist:
         allc = [torch.empty_like(chk) for _ in range(world)]
         dist.all_gather(allc, chk)
         checksums = [c.tolist() for c in allc]
+        if L == 1:
+            from paper_2201_12854_b200 import sharding
+            yall = sharding.gather_shards(y, GB, rank, world) if scaling == "strong" else None
+            if scaling == "weak":
+                bufs = [torch.empty_like(y) for _ in range(world)]
+                dist.all_gather(bufs, y)
+                yall = torch.cat(bufs)
+            if rank == 0:
+                r_last = world - 1
+                s_last, c_last = _shard(args, r_last, world)[1], _shard(args, r_last, world)[0]
+                if project:
+                    pl = (synthetic.make_projected_inputs(B, n, d_in, H, seed=1234 + r_last) if scaling == "weak"
+                          else pin)
+                    xl = (pl.x if scaling == "weak" else pin.x[s_last:s_last + c_last]).to(dtype).to(dev)
+                    wr = mca.AttentionWeights(wl[0].to(dev), heads=H, w_q=pl.w_q.to(dtype).to(dev),
+                                              w_k=pl.w_k.to(dtype).to(dev))
+                    yr = mca.mca_forward(wr, None, None, xl.contiguous(), cfg, seed=42, b_offset=s_last).y
+                else:
+                    il = (synthetic.make_inputs(B, n, d_in, H, seed=1234 + r_last) if scaling == "weak"
+                          else synthetic.make_inputs(GB, n, d_in, H, seed=1234))
+                    sl_ = slice(0, c_last) if scaling == "weak" else slice(s_last, s_last + c_last)
+                    ql, kl, xl = (t[sl_].contiguous().to(dtype).to(dev) for t in (il.q, il.k, il.x))
+                    yr = mca.mca_forward(weights, ql, kl, xl, cfg, seed=42, b_offset=s_last).y
+                off = s_last if scaling == "strong" else r_last * B
+                validation = {"gathered_y_bytes": int(yall.numel() * yall.element_size()),
+                              "last_shard_recomputed_on_rank0_bitwise": bool(torch.equal(yr, yall[off:off + c_last]))}
     else:
         checksums = [chk.tolist()]
 
@@ -563,7 +601,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         "gpu_launches": launches_per_step * args.steps,
         "cpu_baseline": cpu,
         "clocks": clocks,
-        "validation": {"rank_checksums": checksums},
+        "validation": {"rank_checksums": checksums, **validation},
     }
     print(json.dumps(line), flush=True)
     if dist:
