@@ -37,6 +37,9 @@ namespace mca_dev {
 #ifndef KP_STAGES_256
 #define KP_STAGES_256 4
 #endif
+#ifndef KP_STORE_HINT
+#define KP_STORE_HINT 0
+#endif
 #ifndef KP_OUTBUFS_256
 #define KP_OUTBUFS_256 2
 #endif
@@ -248,7 +251,13 @@ __global__ void __launch_bounds__(kp::kThreads, 1) kp_project_tc(const __grid_co
                 fence_proxy_async_smem();                // generic-proxy writes -> visible to the TMA store
                 named_bar_sync(1, 128);
                 if (et == 0) {
+#if KP_STORE_HINT == 1
+                    tma_store_3d_hint(om, st, oc + c, m0, 0, l2_policy_evict_first());
+#elif KP_STORE_HINT == 2
+                    tma_store_3d_hint(om, st, oc + c, m0, 0, l2_policy_evict_last());
+#else
                     tma_store_3d(om, st, oc + c, m0, 0);  // rows past M are clipped by the tensor map
+#endif
                     bulk_commit();
                 }
                 if (++ob == C::kOutBufs) ob = 0;
