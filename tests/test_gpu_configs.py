@@ -188,3 +188,44 @@ def test_certified_budgets_on_tied_attention(mca, syn, orc, n):
     rep = budget_mismatch_report(out2.budgets.cpu().numpy(), out2.exact_mask.cpu().numpy(), full.budgets, full.exact,
                                  full.cmax, n, ALPHA)
     assert rep["count"] == 0, rep
+
+
+def test_fp32_c2_shape_tensor_core_path(mca, syn, orc):
+    """BASELINE.json configs[1] in fp32 ("bf16/fp32") on the tensor-core fp32
+    path (3xTF32 projections, score passes and aggregation; binary64 encoders;
+    certified budgets): four whole n = 512 sequences of a B = 16 batch, x in,
+    against the oracle on the device's projected q, k -- budgets equal end to
+    end, H~ and y within the fp32 tolerance (1e-5)."""
+    B, n, d_in, H = 16, 512, 768, 12
+    pin = syn.make_projected_inputs(B, n, d_in, H, seed=512)
+    w = syn.make_weights(d_in, H, seed=512)
+    weights = mca.AttentionWeights(w.cuda(), heads=H, w_q=pin.w_q.cuda(), w_k=pin.w_k.cuda())
+    x = pin.x.cuda()
+    dbg = dict(q_out=torch.empty((B, n, H * 64), device="cuda"), k_out=torch.empty((B, n, H * 64), device="cuda"),
+               h_out=torch.empty((B, n, H * 64), device="cuda"))
+    out = mca.mca_forward(weights, None, None, x, mca.McaConfig(alpha=ALPHA), seed=42, return_plan=True, flops=True,
+                          debug=dbg)
+    torch.cuda.synchronize()
+    b = out.budgets.cpu().numpy()
+    e = out.exact_mask.cpu().numpy().astype(bool)
+    seqs = np.array([0, 5, 10, 15])
+    qn, kn, xn = (dbg["q_out"][seqs].double().cpu().numpy(), dbg["k_out"][seqs].double().cpu().numpy(),
+                  x[seqs].double().cpu().numpy())
+    wn = w.double().numpy()
+    full = orc.batched_forward(qn, kn, xn, wn, heads=H, alpha=ALPHA, seed=42, want_h=False)
+    rep = budget_mismatch_report(b[seqs], e[seqs], full.budgets, full.exact, full.cmax, n, ALPHA)
+    print(f"C2 fp32 4 sequences: mismatches {rep}; re-derived {out.flops.certified}")
+    assert rep["count"] == 0, rep
+    for i, s in enumerate(seqs):
+        ref = orc.batched_forward(qn[i:i + 1], kn[i:i + 1], xn[i:i + 1], wn, heads=H, alpha=ALPHA, seed=42,
+                                  b_offset=int(s), budgets_override=b[s:s + 1], exact_override=e[s:s + 1])
+        hd = dbg["h_out"][s:s + 1].double().cpu().numpy().reshape(n, H, 64)
+        hr = ref.h.reshape(n, H, 64)
+        err = np.linalg.norm(hd - hr, axis=2) / np.maximum(np.linalg.norm(hr, axis=2), 1e-30)   # [n, H]
+        ex = e[s].T                                                                                # [n, H]
+        print(f"seq {s}: head-row H~ rel err exact max {err[ex].max() if ex.any() else 0:.2e}, "
+              f"sampled max {err[~ex].max():.2e}")
+        assert row_rel(dbg["h_out"][s:s + 1].double().cpu().numpy(), ref.h) <= 1e-5, s
+        assert row_rel(out.y[s:s + 1].double().cpu().numpy(), ref.y) <= 1e-5, s
+    xd = x[seqs].double().cpu()
+    assert row_rel(qn, (xd @ pin.w_q.double()).numpy()) <= 1e-5     # 3xTF32 projection, fp32 accumulation
