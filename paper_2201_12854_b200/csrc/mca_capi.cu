@@ -553,6 +553,9 @@ mca_status launch_projection(mca_weights* w, const void* x, long tokens, int seg
                              int f16_mask, mca_stream_t stream, int& launches) {
     const int HD = w->heads * w->dh;
     const bool tf32 = w->wdt == MCA_F32;
+    if ((size_t)w->d_in * dtype_size(w->wdt) % 16 != 0)   // TMA: a 16-byte multiple row stride
+        return fail(MCA_ERR_UNSUPPORTED, "the on-device projections need d_in * %zu bytes to be a multiple of 16 "
+                    "(d_in = %d); pass q and k instead", dtype_size(w->wdt), w->d_in);
     // N tile: the widest of 256 / 128 / 64 that divides H*64 (192 for BERT-base's
     // finer wave quantisation measured 72 us vs 66 for 256: per-tile overheads)
     const int BN = HD % 256 == 0 ? 256 : HD % 128 == 0 ? 128 : 64;
@@ -574,12 +577,8 @@ mca_status launch_projection(mca_weights* w, const void* x, long tokens, int seg
         const size_t cnt = (size_t)tokens * w->d_in;
         float* xh = static_cast<float*>(w->x_split);
         float* xl = xh + cnt;
-        if (cnt % 4 == 0) {
-            const unsigned gs = (unsigned)std::min<size_t>((cnt / 4 + 255) / 256, 8 * (size_t)sm_count());
-            k_split_tf32<<<gs, 256, 0, stream>>>((const float4*)x, (float4*)xh, (float4*)xl, cnt / 4);
-        } else {
-            return fail(MCA_ERR_UNSUPPORTED, "fp32 projection needs B*n*d_in divisible by 4");
-        }
+        const unsigned gs = (unsigned)std::min<size_t>((cnt / 4 + 255) / 256, 8 * (size_t)sm_count());
+        k_split_tf32<<<gs, 256, 0, stream>>>((const float4*)x, (float4*)xh, (float4*)xl, cnt / 4);   // d_in % 4 == 0
         MCA_LAUNCH_CHECK("k_split_tf32");
         if (!make_tmap_f32(&tx, xh, (uint64_t)w->d_in, (uint64_t)tokens, 1, kp::kBM) ||
             !make_tmap_f32(&tx2, xl, (uint64_t)w->d_in, (uint64_t)tokens, 1, kp::kBM) ||
@@ -717,6 +716,9 @@ mca_status mca_prepare_weights(const void* w_v, mca_dtype wdt, int d_in, int hea
     if (d_in <= 0 || heads <= 0 || d_h <= 0) return fail(MCA_ERR_SHAPE, "d_in, heads, d_h must be positive");
     if (d_h != kDh) return fail(MCA_ERR_UNSUPPORTED, "d_h = %d: the sm_100a kernels implement d_h = 64", d_h);
     if (d_in > 16384) return fail(MCA_ERR_UNSUPPORTED, "d_in = %d exceeds the guide table's 14-bit rows", d_in);
+    if ((size_t)d_in * dtype_size(wdt) % 16 != 0)   // x rows are read with 16-byte vector / TMA / cp.async loads
+        return fail(MCA_ERR_UNSUPPORTED, "d_in = %d: x rows must be a multiple of 16 bytes (d_in %% %d == 0)", d_in,
+                    (int)(16 / dtype_size(wdt)));
     int dev_count = 0;
     if (cudaGetDeviceCount(&dev_count) != cudaSuccess || dev_count == 0) {
         cudaGetLastError();

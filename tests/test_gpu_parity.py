@@ -754,3 +754,17 @@ def test_fp16_range_guard_given_attention(mca, syn, orc):
     assert np.abs(ref.h).max() > 65504
     yref = np.einsum("ij,jhd->ihd", attn, ref.h[0].reshape(n, H, 64)).reshape(n, H * 64)
     assert _row_rel(_np(out.y[0]), yref) <= TOL_Y[torch.bfloat16]
+
+
+def test_unaligned_rows_are_refused(mca, syn):
+    """x rows are read with 16-byte vector / TMA / cp.async loads: d_in = 100 bf16
+    (200-byte rows) is refused at preparation with a clear UNSUPPORTED error
+    instead of a misaligned-address fault; d_in = 104 works."""
+    H = 2
+    with pytest.raises(mca.UnsupportedError):
+        mca.AttentionWeights(syn.make_weights(100, H).to(torch.bfloat16).cuda(), heads=H)
+    w = syn.make_weights(104, H).to(torch.bfloat16).cuda()
+    wq = (torch.randn((104, H * 64)) * 0.1).to(torch.bfloat16).cuda()
+    weights = mca.AttentionWeights(w, heads=H, w_q=wq, w_k=wq)
+    x = torch.randn((1, 16, 104)).to(torch.bfloat16).cuda()
+    assert torch.isfinite(mca.mca_forward(weights, None, None, x).y.float()).all()
