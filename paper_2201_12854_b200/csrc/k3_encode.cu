@@ -273,22 +273,7 @@ __global__ void __launch_bounds__(kK3BlockThreads, 1) k3_encode_sampled(K3Args a
         float o[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) o[u] = (float)acc[u];
-        if constexpr (sizeof(HT) == 2) {   // fp16 H~: range guard (octet-uniform, mca_common.cuh)
-            bool big = false;
-#pragma unroll
-            for (int u = 0; u < 8; ++u) big |= f16_overflows(o[u]);
-            const unsigned bal = __ballot_sync(omask, big);
-            if ((bal >> (lane & 24)) & 0xFFu) {
-                int slot = -1;
-                if (l8 == 0) slot = ovf_push(a.ovf, (long long)tokh);
-                slot = __shfl_sync(omask, slot, lane & 24);
-                if (slot >= 0)
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) a.ovf.rows[(size_t)slot * kDh + col0 + u] = o[u];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) o[u] = 0.f;
-            }
-        }
+        if constexpr (sizeof(HT) == 2) f16_guard8(a.ovf, (long long)tokh, col0 / 8, o);   // fp16 range guard
         store8(hout + tok * HD + (size_t)h * kDh + col0, o);
     };
     auto prefetch_row = [&](int bj) {   // pull a token's X row into L1 ahead of the random gathers
@@ -514,25 +499,10 @@ __global__ void __launch_bounds__(kK3BlockThreads, 1) k3_encode_sampled_bf16(K3A
             if (l8 == 0) my_samples += (unsigned long long)cnt;
         }
         __syncwarp();
-        // fp16 range guard: an octet whose encoding leaves fp16's range queues its fp32 row
-        bool big = false;
-#pragma unroll
-        for (int u = 0; u < 8; ++u) big |= f16_overflows(acc[u]);
-        const unsigned bal = __ballot_sync(0xffffffffu, big && has);
-        const bool oct_big = (bal >> (lane & 24)) & 0xFFu;
-        int slot = -1;
-        if (oct_big && l8 == 0) slot = ovf_push(a.ovf, (long long)tokh);
-        slot = __shfl_sync(0xffffffffu, slot, lane & 24);
         if (!has) return;
         if (a.draws_out && l8 == 0)
             for (int k = r; k < a.draws_stride; ++k) a.draws_out[tokh * a.draws_stride + k] = -1;
-        if (oct_big) {
-            if (slot >= 0)
-#pragma unroll
-                for (int u = 0; u < 8; ++u) a.ovf.rows[(size_t)slot * kDh + col0 + u] = acc[u];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) acc[u] = 0.f;
-        }
+        f16_guard8(a.ovf, (long long)tokh, l8, acc);   // fp16 range guard (mca_common.cuh)
         store8(hout + tok * HD + (size_t)h * kDh + col0, acc);
     };
     auto prefetch_row = [&](int bj) {

@@ -162,26 +162,16 @@ __global__ void __launch_bounds__(k3btc::kThreads, 2) k3b_exact_tc(K3Args a) {
             tmem_ld_wait();
             if (bj >= 0) {
                 __half* dst = reinterpret_cast<__half*>(a.h_out) + tok * HD + (size_t)h * kDh;   // H~ is fp16
-                bool big = false;                      // fp16 range guard (mca_common.cuh)
-#pragma unroll
-                for (int c = 0; c < 64; ++c) big |= f16_overflows(__uint_as_float(v[c >> 5][c & 31]));
-                if (big) {
-                    const long long tokh = ((long long)(bj >> 16) * a.heads + h) * n + (bj & 0xFFFF);
-                    const int slot = ovf_push(a.ovf, tokh);
-#pragma unroll
-                    for (int c = 0; c < 64; ++c) {
-                        if (slot >= 0) a.ovf.rows[(size_t)slot * kDh + c] = __uint_as_float(v[c >> 5][c & 31]);
-                        v[c >> 5][c & 31] = 0u;
-                    }
-                }
+                const long long tokh = ((long long)(bj >> 16) * a.heads + h) * n + (bj & 0xFFFF);
 #pragma unroll
                 for (int g = 0; g < 8; ++g) {
+                    float f[8];
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) f[e] = __uint_as_float(v[(g * 8 + e) >> 5][(g * 8 + e) & 31]);
+                    f16_guard8(a.ovf, tokh, g, f);    // fp16 range guard (mca_common.cuh)
                     uint32_t pk[4];
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const int c = g * 8 + 2 * e;
-                        pk[e] = pack_f16x2(__uint_as_float(v[c >> 5][c & 31]), __uint_as_float(v[(c + 1) >> 5][(c + 1) & 31]));
-                    }
+                    for (int e = 0; e < 4; ++e) pk[e] = pack_f16x2(f[2 * e], f[2 * e + 1]);
                     reinterpret_cast<uint4*>(dst)[g] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
                 }
                 if (a.draws_out) {                     // exact token-heads draw nothing

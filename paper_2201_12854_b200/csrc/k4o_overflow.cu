@@ -37,13 +37,14 @@ __device__ __forceinline__ void ovf_fixup(const K4oArgs& a, unsigned long long c
     const int tid = threadIdx.x;
     const size_t HD = (size_t)a.heads * kDh;
     for (unsigned long long e = e0; e < cnt; e += step) {
-        const long long t = a.ovf.list[e];
+        const long long t = a.ovf.list[e] >> 3;
+        const int chunk = (int)(a.ovf.list[e] & 7);   // columns [8 chunk, 8 chunk + 8)
         const long bh = (long)(t / a.n);
         const int j = (int)(t - (long long)bh * a.n);
         const int b = (int)(bh / a.heads), h = (int)(bh - (long)b * a.heads);
         __syncthreads();
         if (tid < kDh) {
-            s_h[tid] = a.ovf.rows[e * kDh + tid];
+            s_h[tid] = (tid >> 3) == chunk ? a.ovf.rows[e * 8 + (tid & 7)] : 0.f;
             if (!kGiven)
                 s_k[tid] = __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(a.k)[((size_t)b * a.n + j) * HD +
                                                                                      (size_t)h * kDh + tid]);
@@ -67,9 +68,11 @@ __device__ __forceinline__ void ovf_fixup(const K4oArgs& a, unsigned long long c
                 }
                 p = expf((float)a.scale * (d0 + d1) - a.lse[(size_t)bh * a.n + i]);
             }
-            __nv_bfloat162* yr = reinterpret_cast<__nv_bfloat162*>(a.y + ((size_t)b * a.n + i) * HD + (size_t)h * kDh);
-#pragma unroll 8
-            for (int c = 0; c < kDh; c += 2) atomicAdd(yr + c / 2, __floats2bfloat162_rn(p * s_h[c], p * s_h[c + 1]));
+            __nv_bfloat162* yr = reinterpret_cast<__nv_bfloat162*>(a.y + ((size_t)b * a.n + i) * HD + (size_t)h * kDh +
+                                                                  8 * chunk);
+#pragma unroll
+            for (int c = 0; c < 8; c += 2)
+                atomicAdd(yr + c / 2, __floats2bfloat162_rn(p * s_h[8 * chunk + c], p * s_h[8 * chunk + c + 1]));
         }
     }
 }

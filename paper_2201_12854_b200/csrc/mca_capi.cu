@@ -81,7 +81,7 @@ size_t dtype_size(mca_dtype t) { return t == MCA_BF16 ? 2 : 4; }
 constexpr int kCertCounter = 6;                // counters[6]: number of k2c-flagged token-heads
 constexpr int kOvfCounter = 7;                 // counters[7]: fp16-overflowing encodings queued for k4o_overflow
 constexpr int kK4DoneCounter = 5;              // counters[5]: K4 CTAs finished (its last CTA runs the range-guard fix-up)
-constexpr long kOvfCap = 65536;                // queue capacity (token-heads per forward)
+constexpr long kOvfCap = 1 << 18;              // queue capacity (8-column chunks per forward)
 constexpr size_t kMaxGraphs = 256;              // captured forwards kept per handle (LRU)
 
 // Per-device facts and settings. Everything here is keyed by the current
@@ -230,8 +230,8 @@ struct mca_weights {
     int32_t* exact_list = nullptr;            // [H, B*n] exact tokens per head
     long long* cert_list = nullptr;           // [B, H, n] Eq. 9 values at an integer boundary (k2c_certify)
     double* cert_cm = nullptr;                // [B, H, n] the score pass's cmax of each flagged entry
-    long long* ovf_list = nullptr;            // [kOvfCap] fp16-overflowing token-heads (bf16 path)
-    float* ovf_rows = nullptr;                // [kOvfCap][64] their fp32 encodings
+    long long* ovf_list = nullptr;            // [kOvfCap] fp16-overflowing 8-column chunks (bf16 path)
+    float* ovf_rows = nullptr;                // [kOvfCap][8] their fp32 values
     void* qk_split = nullptr;                 // fp32 path: q_hi | q_lo | k_hi | k_lo [B, n, H*64] (3xTF32)
     float* vt_split = nullptr;                // fp32 path: H~ transposed hi | lo [B*H][64][n_pad] (K4 3xTF32)
     size_t cap_vt = 0;                        // floats
@@ -329,8 +329,8 @@ mca_status ensure_workspace(mca_weights* w, long tokens, mca_stream_t stream) {
         cudaMalloc(&w->exact_list, th * sizeof(int32_t)) != cudaSuccess ||
         cudaMalloc(&w->cert_list, th * sizeof(long long)) != cudaSuccess ||
         cudaMalloc(&w->cert_cm, th * sizeof(double)) != cudaSuccess ||
-        cudaMalloc(&w->ovf_list, std::min<long>((long)th, kOvfCap) * sizeof(long long)) != cudaSuccess ||
-        cudaMalloc(&w->ovf_rows, std::min<long>((long)th, kOvfCap) * 64 * sizeof(float)) != cudaSuccess ||
+        cudaMalloc(&w->ovf_list, std::min<long>(8L * (long)th, kOvfCap) * sizeof(long long)) != cudaSuccess ||
+        cudaMalloc(&w->ovf_rows, std::min<long>(8L * (long)th, kOvfCap) * 8 * sizeof(float)) != cudaSuccess ||
         (w->wdt == MCA_F32 && cudaMalloc(&w->qk_split, 4 * th * w->dh * sizeof(float)) != cudaSuccess) ||
         cudaMalloc(&w->row_done, th * sizeof(uint8_t)) != cudaSuccess) {
         cudaGetLastError();
@@ -338,7 +338,7 @@ mca_status ensure_workspace(mca_weights* w, long tokens, mca_stream_t stream) {
         return fail(MCA_ERR_ALLOC, "workspace allocation for %ld tokens failed", tokens);
     }
     w->cap_tokens = tokens;
-    w->ovf_cap = std::min<long>((long)th, kOvfCap);
+    w->ovf_cap = std::min<long>(8L * (long)th, kOvfCap);
     return MCA_OK;
 }
 

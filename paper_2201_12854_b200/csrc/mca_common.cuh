@@ -197,24 +197,41 @@ struct HType<__nv_bfloat16> { using type = __half; };
 // ------------------------------------------------- fp16 H~ range guard
 // H~ is stored as fp16 on the bf16 path (K4's fp16 x fp16 P.H~ product). A
 // sampled contribution x[j,s] w[s] / (r p(s)) is unbounded (tiny p(s), outlier
-// x), so a token-head whose encoding leaves fp16's range is stored as zeros in
-// H~ and its fp32 row is queued here; k4o_overflow adds P[:, j] H~_j back into y
-// after the aggregation.
+// x), so an 8-column chunk of an encoding that leaves fp16's range is stored as
+// zeros in H~ and its fp32 values are queued here; the fix-up adds P[:, j] times
+// the chunk into y after the aggregation. Chunk-granular, so
+// every lane decides alone (no warp collectives in the encoders' store path).
+#ifndef MCA_F16_GUARD
+#define MCA_F16_GUARD 1   // 0: diagnostics builds only (measures the guard's cost)
+#endif
 constexpr float kH16Max = 65504.f;
 struct OvfSink {
-    unsigned long long* count;       // queued token-heads (zeroed per forward)
-    long long* list;                 // [cap] token-head t = (b H + h) n + j
-    float* rows;                     // [cap][64] the fp32 encodings
+    unsigned long long* count;       // queued chunks (zeroed per forward)
+    long long* list;                 // [cap] (token-head t = (b H + h) n + j) * 8 + chunk (8 columns each)
+    float* rows;                     // [cap][8] the fp32 values of each chunk
     int cap;
 };
-// Queue token-head t; returns its slot, or -1 past the capacity (k4o_overflow traps on that).
-__device__ __forceinline__ int ovf_push(const OvfSink& o, long long t) {
-    const unsigned long long pos = atomicAdd(o.count, 1ull);
-    if (pos >= (unsigned long long)o.cap) return -1;
-    o.list[pos] = t;
-    return (int)pos;
-}
 __device__ __forceinline__ bool f16_overflows(float v) { return !(fabsf(v) <= kH16Max); }   // also inf / NaN
+// Queue chunk `chunk` (columns [8 chunk, 8 chunk + 8)) of token-head t if any
+// of its 8 values leaves fp16's range; zero them in v (the fp16 store). Past
+// the capacity the entry is dropped and the count still grows: the fix-up traps.
+__device__ __forceinline__ void f16_guard8(const OvfSink& o, long long t, int chunk, float v[8]) {
+#if MCA_F16_GUARD
+    bool big = false;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) big |= f16_overflows(v[u]);
+    if (big) {
+        const unsigned long long pos = atomicAdd(o.count, 1ull);
+        if (pos < (unsigned long long)o.cap) {
+            o.list[pos] = t * 8 + chunk;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) o.rows[pos * 8 + u] = v[u];
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = 0.f;
+    }
+#endif
+}
 
 __device__ __forceinline__ void store8(float* p, const float v[8]) {
     reinterpret_cast<float4*>(p)[0] = make_float4(v[0], v[1], v[2], v[3]);
