@@ -411,7 +411,7 @@ __global__ void __maxnreg__(72)
                                                      (double)a.cert.tau_rel *
                                                          (1.0 + fabs((double)vmax) * 0.6931471805599453 +
                                                           2.0 * (double)item_lmax))) {
-                        cert_push(a.cert, (long long)t, cm);   // k2c re-derives it in fp64 and accounts it
+                        cert_push(a.cert, (long long)t, cm, n);   // k2c re-derives it in fp64 and accounts it
                         continue;
                     }
                 }

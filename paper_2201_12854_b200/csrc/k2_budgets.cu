@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(256) k2_budgets(K2Args a) {
             if (a.cmax_out) a.cmax_out[t] = cm;
             budget_for(cm, a.n, a.alpha, a.min_samples, a.d, &r, &ex);
             if (a.cert.list && eq9_ambiguous(cm, a.n, a.alpha, a.min_samples, a.d, (double)a.cert.tau_rel * cert_mag)) {
-                cert_push(a.cert, (long long)t, cm);   // k2c re-derives it in fp64 and accounts it
+                cert_push(a.cert, (long long)t, cm, a.n);   // k2c re-derives it in fp64 and accounts it
                 deferred = true;
             }
         }

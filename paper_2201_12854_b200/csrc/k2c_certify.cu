@@ -48,12 +48,20 @@ constexpr float kCertTauBf16 = 1e-6f;
 constexpr float kCertTauTf32 = 3e-6f;
 
 // Flag sink of the budget passes (K12 group B, k2_budgets): null list = off.
+// A flagged key goes to its (b, h) item's slots (item_cnt counts them; zeroed
+// per forward), so the certification kernel visits only items with flags and
+// finds their keys without scanning; past kCertSlots per item, keys spill to
+// the global list (scanned by that item's CTA only).
+constexpr int kCertSlots = 32;
 struct CertSink {
-    long long* list;                 // [B*H*n] flagged token-head indices t = (b*H + h)*n + j
-    double* cm;                      // [B*H*n] the score pass's cmax of each flagged entry
-    unsigned long long* count;       // number of flagged entries (zeroed per forward)
+    long long* list;                 // [B*H*n] spilled token-head indices t = (b*H + h)*n + j
+    double* cm;                      // [B*H*n] the score pass's cmax of each spilled entry
+    unsigned long long* count;       // number of spilled entries (zeroed per forward)
     uint8_t* row_done;               // [B*H*n] exact row statistics cached (cleared by the budget pass)
     float tau_rel;                   // flag threshold per unit of M (kCertTauBf16 / kCertTauTf32)
+    unsigned* item_cnt;              // [B*H] flagged keys per item (zeroed per forward)
+    int* slot_j;                     // [B*H][kCertSlots] key index j
+    double* slot_cm;                 // [B*H][kCertSlots] the score pass's cmax
 };
 
 // (r, exact) of Eq. 9 could change under the score pass's cmax error: raw lies
@@ -67,10 +75,17 @@ __device__ __forceinline__ bool eq9_ambiguous(double cm, int n, double alpha, in
     return m >= (double)min_samples && m <= (double)(d - 1) && fabs(raw - m) <= tau * fmax(raw, 1.0);
 }
 
-__device__ __forceinline__ void cert_push(const CertSink& c, long long t, double cm) {
-    const unsigned long long pos = atomicAdd(c.count, 1ull);
-    c.list[pos] = t;
-    c.cm[pos] = cm;
+__device__ __forceinline__ void cert_push(const CertSink& c, long long t, double cm, int n) {
+    const long long bh = t / n;
+    const unsigned pos = atomicAdd(c.item_cnt + bh, 1u);
+    if (pos < (unsigned)kCertSlots) {
+        c.slot_j[bh * kCertSlots + pos] = (int)(t - bh * n);
+        c.slot_cm[bh * kCertSlots + pos] = cm;
+    } else {
+        const unsigned long long g = atomicAdd(c.count, 1ull);
+        c.list[g] = t;
+        c.cm[g] = cm;
+    }
 }
 
 struct K2cArgs {
@@ -88,37 +103,78 @@ struct K2cArgs {
     double* cmax_out;                // nullable
     unsigned long long* counters;    // [0] approx cost, [1] sampled draws, [2] exact token-heads
     unsigned int* hist;              // [H, d + 1] (nullable)
+    unsigned long long* cert_total;  // number of re-derived token-heads (FlopsReport.certified)
 };
 
-constexpr int kCertThreads = 256;
-constexpr int kCertKeys = 64;        // flagged keys of one item processed together
-constexpr int kCertCands = 512;      // (key, query) candidates per batch
-constexpr int kCertRows = 16;        // candidate rows whose statistics one pass over the keys computes
+constexpr int kCertThreads = 128;    // 4 warps; 8 lanes (an octet) per query / key row
+constexpr int kCertKeys = 32;        // flagged keys of one item processed together
+constexpr int kCertCands = 256;      // (key, query) candidates per batch
+constexpr int kCertRows = 8;         // candidate rows whose statistics one pass over the keys computes
 constexpr int kCertMaxN = 65536;     // bitmap of an item's rows (n <= 65535, mca_forward's limit)
+constexpr int kCertStage = 64;       // rows staged in shared memory per chunk (one L2 round trip each)
 
+// 8 elements [8 l8, 8 l8 + 8) of a 64-wide row, as floats
 template <class T>
-__device__ __forceinline__ void load_row64(const T* __restrict__ p, float v[kDh]) {
-#pragma unroll
-    for (int c = 0; c < kDh; c += 8) load8(p + c, v + c);
+__device__ __forceinline__ void load_oct8(const T* __restrict__ row, int l8, float v[8]) {
+    load8(row + 8 * l8, v);
 }
-__device__ __forceinline__ double dot64_exact(const float* __restrict__ a, const float* __restrict__ b) {
-    double acc0 = 0.0, acc1 = 0.0;
+// octet sums: lanes 8o .. 8o + 7 hold partials of one dot product (the octet's
+// lanes always run together, so only they take part: octets of one warp may
+// leave a loop at different trip counts). Butterfly order makes the sum
+// identical in all 8 lanes.
+__device__ __forceinline__ unsigned oct_mask() { return 0xFFu << ((threadIdx.x & 31) & 24); }
+__device__ __forceinline__ float oct_sum(float v) {
+    const unsigned m = oct_mask();
+    v += __shfl_xor_sync(m, v, 1);
+    v += __shfl_xor_sync(m, v, 2);
+    v += __shfl_xor_sync(m, v, 4);
+    return v;
+}
+__device__ __forceinline__ double oct_sum(double v) {
+    const unsigned m = oct_mask();
+    v += __shfl_xor_sync(m, v, 1);
+    v += __shfl_xor_sync(m, v, 2);
+    v += __shfl_xor_sync(m, v, 4);
+    return v;
+}
+__device__ __forceinline__ double dot8_exact(const float a[8], const float* __restrict__ b) {
+    double acc = 0.0;
 #pragma unroll
-    for (int e = 0; e < kDh; e += 2) {
-        acc0 = fma((double)a[e], (double)b[e], acc0);
-        acc1 = fma((double)a[e + 1], (double)b[e + 1], acc1);
-    }
-    return acc0 + acc1;
+    for (int e = 0; e < 8; ++e) acc = fma((double)a[e], (double)b[e], acc);
+    return acc;   // a partial: exact products, the octet's sum in binary64 (exact for bf16 inputs)
 }
 // max of positive doubles through their bit patterns (monotone for x >= 0)
 __device__ __forceinline__ void atomic_max_pos(double* p, double v) {
     atomicMax(reinterpret_cast<unsigned long long*>(p), (unsigned long long)__double_as_longlong(v));
 }
 
+// Rows [c0, c0 + cnt) of a [n][HD]-strided 64-wide operand -> s_stage (fp32):
+// every thread issues its 16-byte loads at once, so a chunk costs one round trip.
+template <class T>
+__device__ __forceinline__ void stage_rows(float (*st)[kDh + 1], const T* __restrict__ base, size_t stride, int c0,
+                                           int cnt) {
+    constexpr int kPerRow = kDh / 8;                                  // pieces of 8 elements
+    constexpr int kPer = kCertStage * kPerRow / kCertThreads;        // pieces per thread (all loads in flight)
+    float v[kPer][8];
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+        const int e = threadIdx.x + u * kCertThreads, r = e / kPerRow, c = (e - r * kPerRow) * 8;
+        if (r < cnt) load8(base + (size_t)(c0 + r) * stride + c, v[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+        const int e = threadIdx.x + u * kCertThreads, r = e / kPerRow, c = (e - r * kPerRow) * 8;
+        if (r < cnt)
+#pragma unroll
+            for (int q = 0; q < 8; ++q) st[r][c + q] = v[u][q];
+    }
+}
+
+// One CTA per (b, h) item; items without flags exit after reading their count.
 template <class T>
 __global__ void __launch_bounds__(kCertThreads) k2c_certify(K2cArgs a) {
-    __shared__ float s_k[kCertKeys][kDh];            // the batch's flagged keys (fp32 = exact bf16 values)
-    __shared__ long long s_t[kCertKeys];
+    __shared__ float s_k[kCertKeys][kDh];            // the batch's flagged keys (fp32 = exact bf16 / fp32 values)
+    __shared__ int s_j[kCertKeys];
     __shared__ double s_lcm[kCertKeys], s_best[kCertKeys];
     __shared__ int s_cf[kCertCands], s_ci[kCertCands];
     __shared__ double s_ct[kCertCands];
@@ -127,32 +183,52 @@ __global__ void __launch_bounds__(kCertThreads) k2c_certify(K2cArgs a) {
     __shared__ float s_qr[kCertRows][kDh];           // candidate rows of one statistics pass
     __shared__ double s_mref[kCertRows];
     __shared__ double s_part[kCertThreads / 32][kCertRows];
-    __shared__ int s_nkeys, s_ncand, s_nrows;
+    __shared__ int s_nkeys, s_ncand, s_nrows, s_slot_next;
+    __shared__ float s_stage[kCertStage][kDh + 1];   // a chunk of the item's q or k rows (padded: a row per thread)
     griddep_trigger();
     griddep_wait();                                  // flags, provisional budgets, lse of the budget pass
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int bh = blockIdx.x;
+    const unsigned cnt = *(volatile const unsigned*)(a.cert.item_cnt + bh);
+    if (cnt == 0) return;
+    if (threadIdx.x == 0 && a.cert_total) atomicAdd(a.cert_total, (unsigned long long)cnt);
+    const int tid = threadIdx.x, lane = tid & 31, l8 = lane & 7, oct = tid >> 3;   // oct: 0..15
+    constexpr int kOcts = kCertThreads / 8;
     const long long nflag = (long long)*(volatile const unsigned long long*)a.cert.count;
-    if (nflag == 0) return;
     const size_t HD = (size_t)a.heads * kDh;
-    for (int bh = blockIdx.x; bh < a.items; bh += gridDim.x) {
-        const int b = bh / a.heads, h = bh - b * a.heads;
-        const T* Qb = reinterpret_cast<const T*>(a.q) + (size_t)b * a.n * HD + (size_t)h * kDh;
-        const T* Kb = reinterpret_cast<const T*>(a.k) + (size_t)b * a.n * HD + (size_t)h * kDh;
-        const float* lse = a.lse + (size_t)bh * a.n;
-        const double* rowm = a.row_m + (size_t)bh * a.n;
-        double* rowl = a.row_l + (size_t)bh * a.n;
-        uint8_t* done = a.cert.row_done + (size_t)bh * a.n;
-        const long long lo = (long long)bh * a.n, hi = lo + a.n;
-        for (;;) {
-            // 1. up to kCertKeys of this item's flagged keys; a claimed entry is
-            // consumed (-1) so the next batch takes the rest
-            __syncthreads();
-            if (tid == 0) {
-                s_nkeys = 0;
-                s_ncand = 0;
-                s_nrows = 0;
+    const int b = bh / a.heads, h = bh - b * a.heads;
+    const T* Qb = reinterpret_cast<const T*>(a.q) + (size_t)b * a.n * HD + (size_t)h * kDh;
+    const T* Kb = reinterpret_cast<const T*>(a.k) + (size_t)b * a.n * HD + (size_t)h * kDh;
+    const float* lse = a.lse + (size_t)bh * a.n;
+    const double* rowm = a.row_m + (size_t)bh * a.n;
+    double* rowl = a.row_l + (size_t)bh * a.n;
+    uint8_t* done = a.cert.row_done + (size_t)bh * a.n;
+    const long long lo = (long long)bh * a.n, hi = lo + a.n;
+    const int nslots = min(cnt, (unsigned)kCertSlots);
+    if (tid == 0) s_slot_next = 0;
+    for (;;) {
+        // 1. up to kCertKeys flagged keys: the item's slots first, then its spilled
+        // entries in the global list (consumed: -1, so the next batch takes the rest)
+        __syncthreads();
+        const int s0 = s_slot_next;
+        __syncthreads();                             // every thread has read s0 before it advances
+        if (tid == 0) {
+            s_nkeys = 0;
+            s_ncand = 0;
+            s_nrows = 0;
+        }
+        __syncthreads();
+        if (s0 < nslots) {
+            const int take = min(nslots - s0, kCertKeys);
+            if (tid < take) {
+                s_j[tid] = a.cert.slot_j[(size_t)bh * kCertSlots + s0 + tid];
+                s_lcm[tid] = log(a.cert.slot_cm[(size_t)bh * kCertSlots + s0 + tid]);
+                s_best[tid] = 0.0;
             }
-            __syncthreads();
+            if (tid == 0) {
+                s_nkeys = take;
+                s_slot_next = s0 + take;
+            }
+        } else if (cnt > (unsigned)kCertSlots) {
             for (long long f0 = 0; f0 < nflag; f0 += kCertThreads) {
                 const long long f = f0 + tid;
                 if (f < nflag) {
@@ -160,7 +236,7 @@ __global__ void __launch_bounds__(kCertThreads) k2c_certify(K2cArgs a) {
                     if (t >= lo && t < hi) {
                         const int slot = atomicAdd(&s_nkeys, 1);
                         if (slot < kCertKeys) {
-                            s_t[slot] = t;
+                            s_j[slot] = (int)(t - lo);
                             s_lcm[slot] = log(a.cert.cm[f]);
                             s_best[slot] = 0.0;
                             a.cert.list[f] = -1;
@@ -168,149 +244,167 @@ __global__ void __launch_bounds__(kCertThreads) k2c_certify(K2cArgs a) {
                     }
                 }
             }
+        }
+        __syncthreads();
+        const int nk = min(s_nkeys, kCertKeys);
+        if (nk == 0) break;
+        for (int e = tid; e < nk * kDh; e += kCertThreads) {
+            const int f = e / kDh, c = e - f * kDh;
+            s_k[f][c] = to_f32(Kb[(size_t)s_j[f] * HD + c]);
+        }
+        for (int e = tid; e < (a.n + 31) / 32; e += kCertThreads) s_bm[e] = 0u;
+        __syncthreads();
+        // 2. one pass over the queries (an octet per query): fp32 partial dots locate
+        // the candidates, binary64 partial dots give their exact t
+        for (int c0 = 0; c0 < a.n; c0 += kCertStage) {
+            const int cn = min(kCertStage, a.n - c0);
             __syncthreads();
-            const int nk = min(s_nkeys, kCertKeys);
-            const bool more = s_nkeys > kCertKeys;
-            if (nk == 0) break;
-            for (int e = tid; e < nk * kDh; e += kCertThreads) {
-                const int f = e / kDh, c = e - f * kDh;
-                s_k[f][c] = to_f32(Kb[(size_t)(s_t[f] - lo) * HD + c]);
-            }
-            for (int e = tid; e < (a.n + 31) / 32; e += kCertThreads) s_bm[e] = 0u;
+            stage_rows(s_stage, Qb, HD, c0, cn);
             __syncthreads();
-            // 2. one pass over the queries against every key of the batch: fp32
-            // dots locate the candidates, binary64 dots give their exact t
-            for (int i = tid; i < a.n; i += kCertThreads) {
-                float qv[kDh];
-                load_row64(Qb + (size_t)i * HD, qv);
+            static_assert(kCertThreads == 2 * kCertStage, "two threads per staged row");
+            const int ii = tid % kCertStage, half = tid / kCertStage;
+            if (ii < cn) {   // a query row per thread pair, the keys split between the two
+                const int i = c0 + ii;
                 const double l = (double)lse[i];
-                for (int f = 0; f < nk; ++f) {
+                for (int f = half; f < nk; f += 2) {
                     float acc0 = 0.f, acc1 = 0.f;
 #pragma unroll
                     for (int e = 0; e < kDh; e += 2) {
-                        acc0 = fmaf(qv[e], s_k[f][e], acc0);
-                        acc1 = fmaf(qv[e + 1], s_k[f][e + 1], acc1);
+                        acc0 = fmaf(s_stage[ii][e], s_k[f][e], acc0);
+                        acc1 = fmaf(s_stage[ii][e + 1], s_k[f][e + 1], acc1);
                     }
                     const double v = a.scale * (double)(acc0 + acc1) - l;
                     if (v >= s_lcm[f] - (1e-3 + 1e-5 * (fabs(l) + fabs(s_lcm[f])))) {
+                        double t0 = 0.0, t1 = 0.0;
+#pragma unroll
+                        for (int e = 0; e < kDh; e += 2) {
+                            t0 = fma((double)s_stage[ii][e], (double)s_k[f][e], t0);
+                            t1 = fma((double)s_stage[ii][e + 1], (double)s_k[f][e + 1], t1);
+                        }
                         const int slot = atomicAdd(&s_ncand, 1);
                         if (slot < kCertCands) {
                             s_cf[slot] = f;
                             s_ci[slot] = i;
-                            s_ct[slot] = a.scale * dot64_exact(qv, s_k[f]);
+                            s_ct[slot] = a.scale * (t0 + t1);
                         }
                     }
                 }
             }
-            __syncthreads();
-            // more near-ties than candidate slots (degenerate, e.g. uniform rows):
-            // every query row is a candidate of every key of the batch
-            const bool all_rows = s_ncand > kCertCands;
-            const int nc = min(s_ncand, kCertCands);
-            // 3. the distinct candidate rows without cached statistics
-            if (all_rows) {
-                for (int i = tid; i < a.n; i += kCertThreads)
-                    if (!done[i]) s_rows[atomicAdd(&s_nrows, 1) % kCertCands] = i;   // (guarded below)
-            } else {
-                for (int c = tid; c < nc; c += kCertThreads) {
-                    const int i = s_ci[c];
-                    if (!done[i]) {
-                        const unsigned bit = 1u << (i & 31);
-                        if (!(atomicOr(&s_bm[i >> 5], bit) & bit)) s_rows[atomicAdd(&s_nrows, 1)] = i;
-                    }
-                }
-            }
-            __syncthreads();
-            const int nrows_total = all_rows ? -1 : s_nrows;
-            // row statistics, kCertRows rows per pass over the item's keys (all rows
-            // in order for the degenerate case)
-            for (int r0 = 0;; r0 += kCertRows) {
-                int nr;
-                if (all_rows) {
-                    if (r0 >= a.n) break;
-                    nr = min(kCertRows, a.n - r0);
-                } else {
-                    if (r0 >= nrows_total) break;
-                    nr = min(kCertRows, nrows_total - r0);
-                }
-                __syncthreads();
-                for (int e = tid; e < nr * kDh; e += kCertThreads) {
-                    const int r = e / kDh, c = e - r * kDh;
-                    const int i = all_rows ? r0 + r : s_rows[r0 + r];
-                    s_qr[r][c] = to_f32(Qb[(size_t)i * HD + c]);
-                }
-                if (tid < nr) s_mref[tid] = rowm[all_rows ? r0 + tid : s_rows[r0 + tid]];
-                __syncthreads();
-                double part[kCertRows];            // per-thread partial sums (a small local array)
-                for (int r = 0; r < kCertRows; ++r) part[r] = 0.0;
-                for (int jj = tid; jj < a.n; jj += kCertThreads) {
-                    float kv[kDh];
-                    load_row64(Kb + (size_t)jj * HD, kv);
-#pragma unroll 1
-                    for (int r = 0; r < nr; ++r) part[r] += exp(a.scale * dot64_exact(s_qr[r], kv) - s_mref[r]);
-                }
-#pragma unroll 1
-                for (int r = 0; r < kCertRows; ++r) {
-                    double v = part[r];
-                    for (int off = 16; off; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-                    if (lane == 0) s_part[wid][r] = v;
-                }
-                __syncthreads();
-                if (tid < nr) {
-                    double L = 0.0;
-                    for (int w2 = 0; w2 < kCertThreads / 32; ++w2) L += s_part[w2][tid];
-                    const int i = all_rows ? r0 + tid : s_rows[r0 + tid];
-                    rowl[i] = L;
-                    done[i] = 1;
-                }
-            }
-            __syncthreads();
-            // 4. cmax_f = max over its candidates of exp(t - m~_i) / L_i
-            if (all_rows) {
-                for (int f = wid; f < nk; f += kCertThreads / 32) {
-                    double best = 0.0;
-                    for (int i = lane; i < a.n; i += 32) {
-                        float qv[kDh];
-                        load_row64(Qb + (size_t)i * HD, qv);
-                        best = fmax(best, exp(a.scale * dot64_exact(qv, s_k[f]) - rowm[i]) / rowl[i]);
-                    }
-                    for (int off = 16; off; off >>= 1) best = fmax(best, __shfl_xor_sync(0xffffffffu, best, off));
-                    if (lane == 0) s_best[f] = best;
-                }
-            } else {
-                for (int c = tid; c < nc; c += kCertThreads) {
-                    const int i = s_ci[c];
-                    atomic_max_pos(&s_best[s_cf[c]], exp(s_ct[c] - rowm[i]) / rowl[i]);
-                }
-            }
-            __syncthreads();
-            // Eq. 9 for the batch's keys
-            if (tid < nk) {
-                const long long t = s_t[tid];
-                const double cm = s_best[tid];
-                const double tt = __ddiv_rn(__dmul_rn((double)a.n, cm), a.alpha);
-                const double raw = __dmul_rn(tt, tt);
-                const double cc = ceil(raw);
-                const bool ex = cc >= (double)a.d;
-                int r = ex ? a.d : (int)cc;
-                if (r < a.min_samples) r = a.min_samples;
-                if (r > a.d) r = a.d;
-                a.budgets[t] = r;
-                a.exact[t] = ex ? 1 : 0;
-                if (a.cmax_out) a.cmax_out[t] = cm;
-                if (a.counters) {
-                    if (ex) {
-                        atomicAdd(a.counters + 0, 2ull * (unsigned long long)a.d * (unsigned long long)a.dh);
-                        atomicAdd(a.counters + 2, 1ull);
-                    } else {
-                        atomicAdd(a.counters + 0, (unsigned long long)r * (2ull * a.dh + 3ull));
-                        atomicAdd(a.counters + 1, (unsigned long long)r);
-                    }
-                }
-                if (a.hist) atomicAdd(&a.hist[(size_t)h * (a.d + 1) + (ex ? a.d : min(r, a.d - 1))], 1u);
-            }
-            if (!more) break;
         }
+        __syncthreads();
+        // more near-ties than candidate slots (degenerate, e.g. uniform rows):
+        // every query row is a candidate of every key of the batch
+        const bool all_rows = s_ncand > kCertCands;
+        const int nc = min(s_ncand, kCertCands);
+        // 3. the distinct candidate rows without cached statistics
+        if (!all_rows) {
+            for (int c = tid; c < nc; c += kCertThreads) {
+                const int i = s_ci[c];
+                if (!done[i]) {
+                    const unsigned bit = 1u << (i & 31);
+                    if (!(atomicOr(&s_bm[i >> 5], bit) & bit)) s_rows[atomicAdd(&s_nrows, 1)] = i;
+                }
+            }
+        }
+        __syncthreads();
+        const int nrows_total = all_rows ? a.n : s_nrows;
+        // row statistics, kCertRows rows per pass over the item's keys (an octet per key)
+        for (int r0 = 0; r0 < nrows_total; r0 += kCertRows) {
+            const int nr = min(kCertRows, nrows_total - r0);
+            __syncthreads();
+            for (int e = tid; e < nr * kDh; e += kCertThreads) {
+                const int r = e / kDh, c = e - r * kDh;
+                const int i = all_rows ? r0 + r : s_rows[r0 + r];
+                s_qr[r][c] = to_f32(Qb[(size_t)i * HD + c]);
+            }
+            if (tid < nr) s_mref[tid] = rowm[all_rows ? r0 + tid : s_rows[r0 + tid]];
+            __syncthreads();
+            double part[kCertRows];
+#pragma unroll
+            for (int r = 0; r < kCertRows; ++r) part[r] = 0.0;
+            for (int c0 = 0; c0 < a.n; c0 += kCertStage) {
+                const int cn = min(kCertStage, a.n - c0);
+                __syncthreads();
+                stage_rows(s_stage, Kb, HD, c0, cn);
+                __syncthreads();
+                const int jj = tid % kCertStage, half = tid / kCertStage;
+                if (jj < cn) {   // a key row per thread pair, the candidate rows split between the two
+#pragma unroll
+                    for (int r = 0; r < kCertRows; ++r) {
+                        if ((r & 1) == half && r < nr) {
+                            double t0 = 0.0, t1 = 0.0;
+#pragma unroll
+                            for (int e = 0; e < kDh; e += 2) {
+                                t0 = fma((double)s_stage[jj][e], (double)s_qr[r][e], t0);
+                                t1 = fma((double)s_stage[jj][e + 1], (double)s_qr[r][e + 1], t1);
+                            }
+                            part[r] += exp(a.scale * (t0 + t1) - s_mref[r]);
+                        }
+                    }
+                }
+            }
+#pragma unroll
+            for (int r = 0; r < kCertRows; ++r) {
+                double v = part[r];
+                for (int off = 16; off; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+                if (lane == 0) s_part[tid >> 5][r] = v;
+            }
+            __syncthreads();
+            if (tid < nr) {
+                double L = 0.0;
+                for (int w2 = 0; w2 < kCertThreads / 32; ++w2) L += s_part[w2][tid];
+                const int i = all_rows ? r0 + tid : s_rows[r0 + tid];
+                rowl[i] = L;
+                done[i] = 1;
+            }
+        }
+        __syncthreads();
+        // 4. cmax_f = max over its candidates of exp(t - m~_i) / L_i
+        if (all_rows) {
+            for (int f = 0; f < nk; ++f) {
+                double best = 0.0;
+                for (int i = oct; i < a.n; i += kOcts) {
+                    float qv[8];
+                    load_oct8(Qb + (size_t)i * HD, l8, qv);
+                    const double t = a.scale * oct_sum(dot8_exact(qv, &s_k[f][8 * l8]));
+                    best = fmax(best, exp(t - rowm[i]) / rowl[i]);
+                }
+                if (l8 == 0) atomic_max_pos(&s_best[f], best);
+            }
+        } else {
+            for (int c = tid; c < nc; c += kCertThreads) {
+                const int i = s_ci[c];
+                atomic_max_pos(&s_best[s_cf[c]], exp(s_ct[c] - rowm[i]) / rowl[i]);
+            }
+        }
+        __syncthreads();
+        // Eq. 9 for the batch's keys
+        if (tid < nk) {
+            const long long t = lo + s_j[tid];
+            const double cm = s_best[tid];
+            const double tt = __ddiv_rn(__dmul_rn((double)a.n, cm), a.alpha);
+            const double raw = __dmul_rn(tt, tt);
+            const double cc = ceil(raw);
+            const bool ex = cc >= (double)a.d;
+            int r = ex ? a.d : (int)cc;
+            if (r < a.min_samples) r = a.min_samples;
+            if (r > a.d) r = a.d;
+            a.budgets[t] = r;
+            a.exact[t] = ex ? 1 : 0;
+            if (a.cmax_out) a.cmax_out[t] = cm;
+            if (a.counters) {
+                if (ex) {
+                    atomicAdd(a.counters + 0, 2ull * (unsigned long long)a.d * (unsigned long long)a.dh);
+                    atomicAdd(a.counters + 2, 1ull);
+                } else {
+                    atomicAdd(a.counters + 0, (unsigned long long)r * (2ull * a.dh + 3ull));
+                    atomicAdd(a.counters + 1, (unsigned long long)r);
+                }
+            }
+            if (a.hist) atomicAdd(&a.hist[(size_t)h * (a.d + 1) + (ex ? a.d : min(r, a.d - 1))], 1u);
+        }
+        __syncthreads();
+        if (s_slot_next >= nslots && cnt <= (unsigned)kCertSlots) break;   // slots done, nothing spilled
     }
 }
 

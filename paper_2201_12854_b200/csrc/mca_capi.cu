@@ -78,7 +78,8 @@ mca_status fail(mca_status s, const char* fmt, ...) {
 
 size_t dtype_size(mca_dtype t) { return t == MCA_BF16 ? 2 : 4; }
 
-constexpr int kCertCounter = 6;                // counters[6]: number of k2c-flagged token-heads
+constexpr int kCertCounter = 6;                // counters[6]: k2c-flagged token-heads spilled past their item's slots
+constexpr int kCertTotal = 4;                  // counters[4]: token-heads k2c re-derived (FlopsReport.certified)
 constexpr int kOvfCounter = 7;                 // counters[7]: fp16-overflowing encodings queued for k4o_overflow
 constexpr int kK4DoneCounter = 5;              // counters[5]: K4 CTAs finished (its last CTA runs the range-guard fix-up)
 constexpr long kOvfCap = 1 << 18;              // queue capacity (8-column chunks per forward)
@@ -230,6 +231,10 @@ struct mca_weights {
     int32_t* exact_list = nullptr;            // [H, B*n] exact tokens per head
     long long* cert_list = nullptr;           // [B, H, n] Eq. 9 values at an integer boundary (k2c_certify)
     double* cert_cm = nullptr;                // [B, H, n] the score pass's cmax of each flagged entry
+    unsigned* cert_item_cnt = nullptr;        // [B*H] flagged keys per item (k2c)
+    int* cert_slot_j = nullptr;               // [B*H][kCertSlots]
+    double* cert_slot_cm = nullptr;           // [B*H][kCertSlots]
+    long cap_items = 0;
     long long* ovf_list = nullptr;            // [kOvfCap] fp16-overflowing 8-column chunks (bf16 path)
     float* ovf_rows = nullptr;                // [kOvfCap][8] their fp32 values
     void* qk_split = nullptr;                 // fp32 path: q_hi | q_lo | k_hi | k_lo [B, n, H*64] (3xTF32)
@@ -278,6 +283,13 @@ void free_workspace(mca_weights* w) {
     cudaFree(w->cert_list);
     cudaFree(w->cert_cm);
     w->cert_cm = nullptr;
+    cudaFree(w->cert_item_cnt);
+    cudaFree(w->cert_slot_j);
+    cudaFree(w->cert_slot_cm);
+    w->cert_item_cnt = nullptr;
+    w->cert_slot_j = nullptr;
+    w->cert_slot_cm = nullptr;
+    w->cap_items = 0;
     cudaFree(w->ovf_list);
     cudaFree(w->ovf_rows);
     cudaFree(w->qk_split);
@@ -667,7 +679,7 @@ mca_status read_flops(mca_weights* w, int B, int n, bool approx, mca_flops* out,
     out->aggregation = (uint64_t)B * w->heads * 2ull * n * n * w->dh;
     out->samples = approx ? c[3] : 0;
     out->exact_tokens = approx ? c[2] : (uint64_t)th;
-    out->certified = c[kCertCounter];
+    out->certified = c[kCertTotal];
     out->reduction_factor = (double)out->exact_encoding / (double)out->approx_encoding;
     out->total_reduction = (double)(out->exact_encoding + out->aggregation) /
                            (double)(out->approx_encoding + out->aggregation);
@@ -1001,6 +1013,29 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
         cert.count = w->counters + kCertCounter;
         cert.row_done = w->row_done;
         cert.tau_rel = tf32_scores ? kCertTauTf32 : kCertTauBf16;
+        const long items = (long)B * H;
+        if (items > w->cap_items) {   // per-item flag slots
+            if (w->cap_items) MCA_CUDA_TRY(cudaStreamSynchronize(stream));
+            drop_graphs(w);
+            cudaFree(w->cert_item_cnt);
+            cudaFree(w->cert_slot_j);
+            cudaFree(w->cert_slot_cm);
+            w->cert_item_cnt = nullptr;
+            w->cert_slot_j = nullptr;
+            w->cert_slot_cm = nullptr;
+            w->cap_items = 0;
+            if (cudaMalloc(&w->cert_item_cnt, items * sizeof(unsigned)) != cudaSuccess ||
+                cudaMalloc(&w->cert_slot_j, items * kCertSlots * sizeof(int)) != cudaSuccess ||
+                cudaMalloc(&w->cert_slot_cm, items * kCertSlots * sizeof(double)) != cudaSuccess) {
+                cudaGetLastError();
+                return fail(MCA_ERR_ALLOC, "certification slot allocation failed");
+            }
+            w->cap_items = items;
+        }
+        MCA_CUDA_TRY(cudaMemsetAsync(w->cert_item_cnt, 0, items * sizeof(unsigned), stream));
+        cert.item_cnt = w->cert_item_cnt;
+        cert.slot_j = w->cert_slot_j;
+        cert.slot_cm = w->cert_slot_cm;
     }
 
 
@@ -1152,7 +1187,8 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
             c.cmax_out = dbg ? dbg->cmax_out : nullptr;
             c.counters = w->counters;
             c.hist = tile_k3 ? nullptr : w->hist;
-            const int gc = std::min(B * H, sm_count());   // (b, h) items with flags, one CTA each
+            c.cert_total = w->counters + kCertTotal;
+            const int gc = B * H;   // one CTA per (b, h) item; items without flags exit at once
             if (dt == MCA_F32) MCA_CUDA_TRY(launch_pdl(k2c_certify<float>, dim3((unsigned)gc), dim3(kCertThreads), 0, stream, c));
             else MCA_CUDA_TRY(launch_pdl(k2c_certify<__nv_bfloat16>, dim3((unsigned)gc), dim3(kCertThreads), 0, stream, c));
             MCA_LAUNCH_CHECK("k2c_certify");
