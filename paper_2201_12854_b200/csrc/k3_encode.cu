@@ -28,13 +28,17 @@
 //     into L1 when the token starts. Accumulation walks the 16 samples in draw
 //     order: one 16/32-byte shared-memory load of the sampled W_h row and 8 FMAs
 //     per lane per sample.
-// The fp32 path (Acc = double) forms each coefficient exactly as the oracle
-// does, x / (r * p) in binary64, and accumulates in fp64; the bf16 path uses
-// fp32 coefficients x * (1/p) * (1/r) and fp32 accumulation.
+// Both dtypes form fp32 coefficients x * (1/p) * (1/r) and accumulate in fp32
+// in draw order (the fp32 path with FFMA2 on fp32 W_h rows; the oracle's fp64
+// sum differs by ~sqrt(r) * 2^-24 of the row scale, inside the fp32 gate of
+// 1e-5). Acc = double (fp64 coefficients x / (r p), fp64 sums) remains a
+// template option.
 //
 // k3b_encode_exact: exact token-heads (~6% of token-heads, but each costs a
 // full 768-long dot product per output) as a tiled GEMM over K2's per-head
 // exact list: 64 gathered tokens x 64 outputs per tile, K staged 32 at a time.
+#include <type_traits>
+
 #include "mca_common.cuh"
 
 namespace mca_dev {
@@ -76,6 +80,8 @@ struct K3Args {
 
 constexpr int kK3Warps = 32;                          // 1024 threads: one CTA per SM holds W_h once
 constexpr int kK3BlockThreads = kK3Warps * 32;
+constexpr int kK3F32Warps = 16;         // fp32 full-W_h variant: 512 threads
+constexpr int kK3F32GuideBits = 11;     // and a 2048-bucket guide table
 
 template <class Acc>
 struct alignas(16) SamplePair {  // fp32 parity path: one draw, broadcast to its octet through smem
@@ -103,11 +109,16 @@ __device__ __forceinline__ void load4w(const __nv_bfloat16* base, size_t stride,
     v[3] = __uint_as_float(u.y & 0xFFFF0000u);
 }
 
+// An octet's 16 sample pairs, padded to 17 so the four octets of a warp read
+// their pair k from four different bank groups (16 would put all four on the same banks).
+constexpr int kPairStride = 17;
+
 // Shared-memory footprint: sampler tables + the per-warp sample-pair buffers +
 // (optionally) W_h in the staging type WS.
-size_t k3_smem_bytes(int d_in, size_t coef, size_t ws_elem, bool wsmem, int cols = kDh) {
-    const size_t tables = (((size_t)d_in * (8 + coef) + kGuide * 2) + 127) & ~(size_t)127;
-    const size_t pairs = (size_t)kK3Warps * 4 * 16 * 16;   // sizeof(SamplePair<Acc>) = 16 (alignas) for either Acc
+size_t k3_smem_bytes(int d_in, size_t coef, size_t ws_elem, bool wsmem, int cols = kDh, int warps = kK3Warps,
+                     int guide_bits = kGuideBits) {
+    const size_t tables = (((size_t)d_in * (8 + coef) + ((size_t)2 << guide_bits)) + 127) & ~(size_t)127;
+    const size_t pairs = (size_t)warps * 4 * kPairStride * 16;   // sizeof(SamplePair<Acc>) = 16 (alignas) for either Acc
     return tables + pairs + (wsmem ? (size_t)d_in * cols * ws_elem : 0);
 }
 
@@ -119,10 +130,15 @@ size_t k3_smem_bytes(int d_in, size_t coef, size_t ws_elem, bool wsmem, int cols
 // (blockIdx.z = half; both halves draw the same samples), so its fp32 W_h half
 // (d_in x 32) fits in shared memory beside the tables: one 128-byte wavefront
 // per sample (4 fp32 per lane) instead of 256-byte row reads from L2.
-template <class T, class WS, class Acc, bool kWSmem, int kCols = 8>
-__global__ void __launch_bounds__(kK3BlockThreads, 1) k3_encode_sampled(K3Args a) {
+// kWarps / kGBits < defaults (fp32 path at C2): a 512-thread CTA and a coarse
+// guide table (every 2^(kGuideBits - kGBits)-th entry, flags dropped) leave room
+// for the whole fp32 W_h (d_in = 768: 192 KB) in shared memory.
+template <class T, class WS, class Acc, bool kWSmem, int kCols = 8, int kWarps = kK3Warps, int kGBits = kGuideBits>
+__global__ void __launch_bounds__(kWarps * 32, 1) k3_encode_sampled(K3Args a) {
     constexpr int kW = kCols * 8;   // output columns this CTA encodes (64, or 32 for a half)
-    using Coef = typename CoefT<T>::type;
+    constexpr int kThreads = kWarps * 32;
+    constexpr int kG = 1 << kGBits;
+    using Coef = std::conditional_t<sizeof(Acc) == 8, double, float>;   // p(i) (fp64 coefficients) or 1/p(i)
     using Pair = SamplePair<Acc>;
     extern __shared__ __align__(16) unsigned char smem[];
     const int h = blockIdx.y;
@@ -136,20 +152,22 @@ __global__ void __launch_bounds__(kK3BlockThreads, 1) k3_encode_sampled(K3Args a
     Coef* s_coef = reinterpret_cast<Coef*>(s_thr + d_in);
     uint16_t* s_guide = reinterpret_cast<uint16_t*>(s_coef + d_in);
     Pair* s_pairs =
-        reinterpret_cast<Pair*>(smem + ((((size_t)d_in * (8 + sizeof(Coef)) + kGuide * 2) + 127) & ~(size_t)127));
-    WS* s_w = reinterpret_cast<WS*>(s_pairs + kK3Warps * 4 * 16);
-    Pair* my_pairs = s_pairs + (warp * 4 + oct) * 16;
+        reinterpret_cast<Pair*>(smem + ((((size_t)d_in * (8 + sizeof(Coef)) + kG * 2) + 127) & ~(size_t)127));
+    WS* s_w = reinterpret_cast<WS*>(s_pairs + kWarps * 4 * kPairStride);
+    Pair* my_pairs = s_pairs + (warp * 4 + oct) * kPairStride;
 
     const size_t HD = (size_t)heads * kDh;
     const T* wv = reinterpret_cast<const T*>(a.wv);
-    for (int i = tid; i < d_in; i += kK3BlockThreads) {
+    for (int i = tid; i < d_in; i += kThreads) {
         s_thr[i] = a.thr[(size_t)h * d_in + i];
         if constexpr (sizeof(Coef) == 8) s_coef[i] = (Coef)a.probs[(size_t)h * d_in + i];
         else s_coef[i] = (Coef)a.invp[(size_t)h * d_in + i];
     }
-    for (int g = tid; g < kGuide; g += kK3BlockThreads) s_guide[g] = a.guide[(size_t)h * kGuide + g];
+    for (int g = tid; g < kG; g += kThreads)
+        s_guide[g] = kGBits == kGuideBits ? a.guide[(size_t)h * kGuide + g]
+                                          : a.guide[(size_t)h * kGuide + ((size_t)g << (kGuideBits - kGBits))] & kGuideRow;
     if constexpr (kWSmem) {   // W_h (or its column half) -> smem, converted to WS, 8 elements per thread-iteration
-        for (int e = tid; e < d_in * (kW / 8); e += kK3BlockThreads) {
+        for (int e = tid; e < d_in * (kW / 8); e += kThreads) {
             const int i = e / (kW / 8), c8 = (e % (kW / 8)) * 8;
             float v[8];
             load8(wv + (size_t)i * HD + (size_t)h * kDh + half * kW + c8, v);
@@ -167,6 +185,11 @@ __global__ void __launch_bounds__(kK3BlockThreads, 1) k3_encode_sampled(K3Args a
     // lane owns columns [kCols l, kCols l + kCols) of the CTA's kW: one conflict-free
     // 16-byte read per sample (8 bf16 or 4 fp32)
     const int wcol = kCols * l8;
+    // fp32 W_h with 8 columns per lane: lane l8 owns columns [4 l8, 4 l8 + 4) and
+    // [32 + 4 l8, 36 + 4 l8), so each of the octet's two 16-byte reads per sample
+    // covers one contiguous 128-byte half-row (no bank conflicts; [8 l8, 8 l8 + 8)
+    // would put lanes l8 and l8 + 4 on the same banks)
+    constexpr bool kSplitCols = kCols == 8 && sizeof(WS) == 4;
     const int col0 = half * kW + wcol;
     const int nsamp = a.counts[2 * h];
     const int32_t* list = a.samp_list + (size_t)h * a.tokens;
@@ -189,7 +212,7 @@ __global__ void __launch_bounds__(kK3BlockThreads, 1) k3_encode_sampled(K3Args a
             uint64_t m0, m1;
             philox_pair53(a.seed, stream, a.layer, (uint32_t)(base / 2 + l8), &m0, &m1);
             // draws past r resolve to some valid row and are never accumulated
-            sample_index2(s_thr, s_guide, m0, m1, i0, i1);
+            sample_index2<kGBits>(s_thr, s_guide, m0, m1, i0, i1);
             x0 = xrow[i0];
             x1 = xrow[i1];
         };
@@ -210,6 +233,12 @@ __global__ void __launch_bounds__(kK3BlockThreads, 1) k3_encode_sampled(K3Args a
             if constexpr (kCols == 4) {
                 const float4 w4 = *reinterpret_cast<const float4*>(wsrc + (size_t)p.row * wstride + wcol);
                 w[0] = w4.x; w[1] = w4.y; w[2] = w4.z; w[3] = w4.w;
+            } else if constexpr (kSplitCols) {   // two 128-byte half-rows, each one wavefront per octet
+                const float* rw = reinterpret_cast<const float*>(wsrc) + (size_t)p.row * wstride + 4 * l8;
+                const float4 lo4 = *reinterpret_cast<const float4*>(rw);
+                const float4 hi4 = *reinterpret_cast<const float4*>(rw + 32);
+                w[0] = lo4.x; w[1] = lo4.y; w[2] = lo4.z; w[3] = lo4.w;
+                w[4] = hi4.x; w[5] = hi4.y; w[6] = hi4.z; w[7] = hi4.w;
             } else {
                 load8(wsrc + (size_t)p.row * wstride + wcol, w);
             }
@@ -273,6 +302,12 @@ __global__ void __launch_bounds__(kK3BlockThreads, 1) k3_encode_sampled(K3Args a
         float o[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) o[u] = (float)acc[u];
+        if constexpr (kSplitCols) {   // columns [4 l8, 4 l8 + 4) and [32 + 4 l8, 36 + 4 l8)
+            float* orow = reinterpret_cast<float*>(hout) + tok * HD + (size_t)h * kDh + 4 * l8;
+            *reinterpret_cast<float4*>(orow) = make_float4(o[0], o[1], o[2], o[3]);
+            *reinterpret_cast<float4*>(orow + 32) = make_float4(o[4], o[5], o[6], o[7]);
+            return;
+        }
         if constexpr (sizeof(HT) == 2) f16_guard8(a.ovf, (long long)tokh, col0 / 8, o);   // fp16 range guard
         store8(hout + tok * HD + (size_t)h * kDh + col0, o);
     };
@@ -563,23 +598,33 @@ size_t k3_bf16_smem_bytes(int d_in) {
            (size_t)d_in * kDh * 2;
 }
 
-// Exact tokens: tiles of 64 listed tokens x 64 outputs; 256 threads, each 4 x 4.
+// Exact tokens (the fp32 path's fp64 GEMM, and bf16 under MCA_FORCE_SIMT):
+// tiles of 64 listed tokens x 64 outputs, 128 threads, each an 8 x 4 register
+// tile (tokens 16 i + 2 ty + {0, 1}, outputs 32 i + 2 tx + {0, 1}: every 16-byte
+// shared-memory read of a warp covers contiguous bytes, conflict-free), so a
+// k-step costs 6 shared loads per 32 FMAs. The next k-chunk's X and W are
+// loaded into registers while the current one computes.
 template <class T, class Acc>
-__global__ void __launch_bounds__(256) k3b_encode_exact(K3Args a) {
-    constexpr int kTM = 64, kTK = 32;
-    __shared__ Acc xs[kTK][kTM + 4];     // transposed X chunk: xs[k][token]
-    __shared__ Acc ws[kTK][kDh + 4];
+__global__ void __launch_bounds__(128) k3b_encode_exact(K3Args a) {
+    constexpr int kTM = 64, kTK = 32, kThreads = 128;
+    using Acc2 = std::conditional_t<sizeof(Acc) == 8, double2, float2>;
+    __shared__ __align__(16) Acc xs[kTK][kTM];   // transposed X chunk: xs[k][token]
+    __shared__ __align__(16) Acc ws[kTK][kDh];
     __shared__ int toks[kTM];
     const int h = blockIdx.y;
     const int ne = a.counts[2 * h + 1];
     const int tiles = (ne + kTM - 1) / kTM;
-    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;   // outputs 4*tx.., tokens 4*ty..
+    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
     const size_t HD = (size_t)a.heads * kDh;
     const T* x = reinterpret_cast<const T*>(a.x);
     const T* wv = reinterpret_cast<const T*>(a.wv);
     using HT = typename HType<T>::type;
     HT* hout = reinterpret_cast<HT*>(a.h_out);
     const int32_t* list = a.exact_list + (size_t)h * a.tokens;
+    // loader roles: X token tid % 64, k half tid / 64 (16 consecutive k);
+    // W column pair tid % 32, rows 8 (tid / 32) .. + 8 (a warp reads 256 contiguous bytes per row)
+    const int xt = tid & 63, xk = (tid >> 6) * 16;
+    const int wc = 2 * (tid & 31), wr = (tid >> 5) * 8;
     for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
         __syncthreads();
         if (tid < kTM) {
@@ -587,47 +632,63 @@ __global__ void __launch_bounds__(256) k3b_encode_exact(K3Args a) {
             toks[tid] = bj < 0 ? -1 : (bj >> 16) * a.n + (bj & 0xFFFF);
         }
         __syncthreads();
-        Acc acc[4][4];
+        Acc acc[8][4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < 8; ++i)
 #pragma unroll
             for (int jj = 0; jj < 4; ++jj) acc[i][jj] = (Acc)0;
+        const int my_tok = toks[xt];
+        float vx[16], vw[16];
+        auto fetch = [&](int k0) {
+            const int kb = k0 + xk;
+            if (my_tok >= 0 && kb + 16 <= a.d_in) {
+                load8(x + (size_t)my_tok * a.d_in + kb, vx);
+                load8(x + (size_t)my_tok * a.d_in + kb + 8, vx + 8);
+            } else {
+#pragma unroll
+                for (int e = 0; e < 16; ++e)
+                    vx[e] = (my_tok >= 0 && kb + e < a.d_in) ? to_f32(x[(size_t)my_tok * a.d_in + kb + e]) : 0.f;
+            }
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                const int row = k0 + wr + r;
+                const T* src = wv + (size_t)row * HD + (size_t)h * kDh + wc;
+                vw[2 * r] = row < a.d_in ? to_f32(src[0]) : 0.f;
+                vw[2 * r + 1] = row < a.d_in ? to_f32(src[1]) : 0.f;
+            }
+        };
+        fetch(0);
         for (int k0 = 0; k0 < a.d_in; k0 += kTK) {
-            // X chunk: 64 tokens x 32 k (8 consecutive k per thread), W chunk: 32 k x 64 outputs
-            {
-                const int tm = tid >> 2, kq = (tid & 3) * 8;
-                const int tok = toks[tm];
-                float v[8];
-                if (tok >= 0 && k0 + kq + 8 <= a.d_in) {
-                    load8(x + (size_t)tok * a.d_in + k0 + kq, v);
-                } else {
 #pragma unroll
-                    for (int e = 0; e < 8; ++e)
-                        v[e] = (tok >= 0 && k0 + kq + e < a.d_in) ? to_f32(x[(size_t)tok * a.d_in + k0 + kq + e]) : 0.f;
-                }
+            for (int e = 0; e < 16; ++e) xs[xk + e][xt] = (Acc)vx[e];
 #pragma unroll
-                for (int e = 0; e < 8; ++e) xs[kq + e][tm] = (Acc)v[e];
-                const int kr = tid >> 3, c8 = (tid & 7) * 8;
-                float w8[8];
-                if (k0 + kr < a.d_in) load8(wv + (size_t)(k0 + kr) * HD + (size_t)h * kDh + c8, w8);
-                else
-#pragma unroll
-                    for (int e = 0; e < 8; ++e) w8[e] = 0.f;
-#pragma unroll
-                for (int e = 0; e < 8; ++e) ws[kr][c8 + e] = (Acc)w8[e];
+            for (int r = 0; r < 8; ++r) {
+                Acc2 w2;
+                w2.x = (Acc)vw[2 * r];
+                w2.y = (Acc)vw[2 * r + 1];
+                *reinterpret_cast<Acc2*>(&ws[wr + r][wc]) = w2;
             }
             __syncthreads();
-#pragma unroll 8
+            if (k0 + kTK < a.d_in) fetch(k0 + kTK);
+#pragma unroll 4
             for (int kk = 0; kk < kTK; ++kk) {
-                Acc av[4], bv[4];
+                Acc av[8], bv[4];
 #pragma unroll
-                for (int i = 0; i < 4; ++i) av[i] = xs[kk][ty * 4 + i];
+                for (int i = 0; i < 4; ++i) {
+                    const Acc2 t2 = *reinterpret_cast<const Acc2*>(&xs[kk][16 * i + 2 * ty]);
+                    av[2 * i] = t2.x;
+                    av[2 * i + 1] = t2.y;
+                }
 #pragma unroll
-                for (int jj = 0; jj < 4; ++jj) bv[jj] = ws[kk][tx * 4 + jj];
+                for (int i = 0; i < 2; ++i) {
+                    const Acc2 w2 = *reinterpret_cast<const Acc2*>(&ws[kk][32 * i + 2 * tx]);
+                    bv[2 * i] = w2.x;
+                    bv[2 * i + 1] = w2.y;
+                }
 #pragma unroll
-                for (int i = 0; i < 4; ++i)
+                for (int i = 0; i < 8; ++i)
 #pragma unroll
-                    for (int jj = 0; jj < 4; ++jj) acc[i][jj] += av[i] * bv[jj];
+                    for (int jj = 0; jj < 4; ++jj) acc[i][jj] = fma(av[i], bv[jj], acc[i][jj]);
             }
             __syncthreads();
         }
@@ -637,18 +698,18 @@ __global__ void __launch_bounds__(256) k3b_encode_exact(K3Args a) {
             for (int k = 0; k < a.draws_stride; ++k) a.draws_out[tokh * a.draws_stride + k] = -1;
         }
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int tok = toks[ty * 4 + i];
+        for (int i = 0; i < 8; ++i) {
+            const int tok = toks[16 * (i >> 1) + 2 * ty + (i & 1)];
             if (tok < 0) continue;
-            HT* dst = hout + (size_t)tok * HD + (size_t)h * kDh + tx * 4;
+            HT* dst = hout + (size_t)tok * HD + (size_t)h * kDh;
 #pragma unroll
-            for (int jj = 0; jj < 4; ++jj) dst[jj] = (HT)((float)acc[i][jj]);
+            for (int jj = 0; jj < 4; ++jj) dst[32 * (jj >> 1) + 2 * tx + (jj & 1)] = (HT)((float)acc[i][jj]);
         }
     }
 }
 
-template __global__ void k3_encode_sampled<float, float, double, true>(K3Args);
-template __global__ void k3_encode_sampled<float, float, double, false>(K3Args);
+template __global__ void k3_encode_sampled<float, float, float, true>(K3Args);
+template __global__ void k3_encode_sampled<float, float, float, false>(K3Args);
 template __global__ void k3_encode_sampled<__nv_bfloat16, float, float, true>(K3Args);
 template __global__ void k3_encode_sampled<__nv_bfloat16, __nv_bfloat16, float, true>(K3Args);
 template __global__ void k3_encode_sampled<__nv_bfloat16, __nv_bfloat16, float, false>(K3Args);

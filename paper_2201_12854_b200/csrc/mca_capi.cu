@@ -399,7 +399,7 @@ template <class T, class Acc>
 mca_status launch_k3(mca_weights* w, const void* x, int B, int n, long b_offset, uint32_t layer, uint64_t seed,
                      void* hout, int32_t* draws, int draws_stride, mca_stream_t stream, int& launches,
                      bool skip_exact = false) {
-    using Coef = typename CoefT<T>::type;
+    using Coef = float;   // K3's per-row factor: 1/p(i) in fp32 (both dtypes accumulate in fp32)
     K3Args a{};
     a.x = x;
     a.wv = w->w;
@@ -455,6 +455,8 @@ mca_status launch_k3(mca_weights* w, const void* x, int B, int n, long b_offset,
     bool launched = false;
     size_t smem = k3_smem_bytes(w->d_in, sizeof(Coef), sizeof(T), true);
     constexpr size_t kMaxSmem = 220 * 1024;
+    constexpr size_t kMaxSmemOptIn = 227 * 1024;   // sm_100 per-block opt-in maximum
+    int threads = kK3BlockThreads;
     if (sizeof(T) == 2 && k3_bf16_smem_bytes(w->d_in) <= kMaxSmem) {
         smem = k3_bf16_smem_bytes(w->d_in);
         kern = !MCA_K3_SPECIALIZE ? k3_encode_sampled_bf16<0>
@@ -468,7 +470,7 @@ mca_status launch_k3(mca_weights* w, const void* x, int B, int n, long b_offset,
         // draws cost more than the L2 row reads save (0.91 vs 0.79 ms).
         if constexpr (sizeof(T) == 4) {
             smem = k3_smem_bytes(w->d_in, sizeof(Coef), 4, true, kDh / 2);
-            auto kh = k3_encode_sampled<float, float, double, true, 4>;
+            auto kh = k3_encode_sampled<float, float, float, true, 4>;
             MCA_CUDA_TRY(ensure_smem(kh, smem));
             int occ = 0;
             MCA_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kh, kK3BlockThreads, smem));
@@ -483,16 +485,24 @@ mca_status launch_k3(mca_weights* w, const void* x, int B, int n, long b_offset,
         }
     } else if (smem <= kMaxSmem) {
         if constexpr (sizeof(T) == 2) kern = k3_encode_sampled<__nv_bfloat16, __nv_bfloat16, float, true>;
-        else kern = k3_encode_sampled<float, float, double, true>;
+        else kern = k3_encode_sampled<float, float, float, true>;
+    } else if (sizeof(T) == 4 && k3_smem_bytes(w->d_in, sizeof(Coef), 4, true, kDh, kK3F32Warps, kK3F32GuideBits) <=
+                                     kMaxSmemOptIn) {
+        // fp32 at C2 (d_in = 768): the whole fp32 W_h resident beside a coarse
+        // guide table, 512 threads per CTA (conflict-free smem row reads instead of
+        // L1/L2 gathers of 256-byte rows)
+        smem = k3_smem_bytes(w->d_in, sizeof(Coef), 4, true, kDh, kK3F32Warps, kK3F32GuideBits);
+        if constexpr (sizeof(T) == 4) kern = k3_encode_sampled<float, float, float, true, 8, kK3F32Warps, kK3F32GuideBits>;
+        threads = kK3F32Warps * 32;
     } else {
         smem = k3_smem_bytes(w->d_in, sizeof(Coef), sizeof(T), false);
         if constexpr (sizeof(T) == 2) kern = k3_encode_sampled<__nv_bfloat16, __nv_bfloat16, float, false>;
-        else kern = k3_encode_sampled<float, float, double, false>;
+        else kern = k3_encode_sampled<float, float, float, false>;
     }
     if (!launched) {
     MCA_CUDA_TRY(ensure_smem(kern, smem));
     int occ = 0;
-    MCA_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kK3BlockThreads, smem));
+    MCA_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem));
     if (occ < 1) occ = 1;
     int G = sm_count() * occ / w->heads;     // all CTAs resident: no second wave
     const long cap = (a.tokens + 63) / 64;   // at most one CTA per 64 tokens of a head
@@ -504,7 +514,7 @@ mca_status launch_k3(mca_weights* w, const void* x, int B, int n, long b_offset,
     const bool bf16_kern = kern == k3_encode_sampled_bf16<768> || kern == k3_encode_sampled_bf16<1024> ||
                            kern == k3_encode_sampled_bf16<0>;
     if (bf16_kern) MCA_CUDA_TRY(launch_pdl(kern, dim3(G1), dim3(kK3BlockThreads), smem, stream, a));
-    else kern<<<dim3(G, w->heads), kK3BlockThreads, smem, stream>>>(a);
+    else kern<<<dim3(G, w->heads), threads, smem, stream>>>(a);
     MCA_LAUNCH_CHECK("k3_encode_sampled");
     if (bf16_kern) mca_diag::dump_k3s(stream, G1, w->heads);   // diagnostics builds only
     }
@@ -522,11 +532,11 @@ mca_status launch_k3(mca_weights* w, const void* x, int B, int n, long b_offset,
         MCA_LAUNCH_CHECK("k3b_exact_tc");
         mca_diag::dump_k3b(stream);   // diagnostics builds only
     } else {                                  // fp32 parity path: fp64 CUDA-core GEMM
-        int Ge = (2 * sm_count() + w->heads - 1) / w->heads;
+        int Ge = (4 * sm_count() + w->heads - 1) / w->heads;   // 128-thread CTAs, several per SM
         const long ecap = (a.tokens + 63) / 64;
         if (Ge > ecap) Ge = (int)ecap;
         if (Ge < 1) Ge = 1;
-        k3b_encode_exact<T, Acc><<<dim3(Ge, w->heads), 256, 0, stream>>>(a);
+        k3b_encode_exact<T, Acc><<<dim3(Ge, w->heads), 128, 0, stream>>>(a);
         MCA_LAUNCH_CHECK("k3b_encode_exact");
     }
     return MCA_OK;
