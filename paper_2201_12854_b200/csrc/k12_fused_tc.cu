@@ -136,7 +136,7 @@ __global__ void __maxnreg__(72)
     uint64_t* comb_empty = comb_full + 2;        // [2] B has read them
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(comb_empty + 2);
 
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int warp = __shfl_sync(0xffffffffu, (int)threadIdx.x >> 5, 0), lane = threadIdx.x & 31;   // uniform: see k4_apply_tf32
     const int nblk = nt * nt;
     const bool prof0 = MCA_K12_PROF && blockIdx.x == 0;
     griddep_trigger();   // the work-list kernels may launch (they wait for this grid to complete)
@@ -180,6 +180,8 @@ __global__ void __maxnreg__(72)
     // Q_qt K_kt^T into the A buffers; phase 2: S^T = K_kt Q_qt^T into the B
     // buffers. Each stream has its own issuing thread (tcgen05.commit tracks the
     // issuing thread's MMAs), so neither waits on the other's buffer recycling.
+    const uint64_t dbase = sw128_desc(smem_u32(smem), 16, 1024);
+    // Whole-warp MMA streams (one elected lane issues and commits; see tc_common.cuh)
     auto issue = [&](int phase, int li, int u) {
         const int U = li * nblk + u;
         const int qt = u / nt, kt = u - qt * nt, sb = U & 1;
@@ -189,19 +191,18 @@ __global__ void __maxnreg__(72)
         mbar_wait(tile_full + qt, li & 1);
         mbar_wait(tile_full + nt + kt, li & 1);
         tc_fence_after();
-        const uint32_t qa = smem_u32(smem + L.q + qt * kTileBytes);
-        const uint32_t ka = smem_u32(smem + L.k + kt * kTileBytes);
-        const uint32_t a_addr = phase ? ka : qa, b_addr = phase ? qa : ka;
+        const uint64_t dq = desc_add(dbase, L.q + qt * kTileBytes);
+        const uint64_t dk = desc_add(dbase, L.k + kt * kTileBytes);
+        const uint64_t da = phase ? dk : dq, db = phase ? dq : dk;
         const uint32_t d = tmem + (uint32_t)(phase * 2 + sb) * kT;
 #pragma unroll
         for (int kk = 0; kk < kDh / 16; ++kk)
-            umma_f16(d, sw128_desc(a_addr + kk * 32, 16, 1024), sw128_desc(b_addr + kk * 32, 16, 1024), kIdesc,
-                     kk > 0 ? 1u : 0u);
-        umma_commit(full + sb);
-        if (prof0 && phase == 0 && U < 32) g_k12_prof[192 + U] = clock64();
+            umma_f16_w(d, desc_add(da, kk * 32), desc_add(db, kk * 32), kIdesc, kk > 0 ? 1u : 0u);
+        umma_commit_w(full + sb);
+        if (prof0 && lane == 0 && phase == 0 && U < 32) g_k12_prof[192 + U] = clock64();
         uint64_t* tile_empty = phase ? tile_empty2 : tile_empty1;   // this phase's last read of a tile
-        if (kt == nt - 1) umma_commit(tile_empty + qt);
-        if (qt == nt - 1) umma_commit(tile_empty + nt + kt);
+        if (kt == nt - 1) umma_commit_w(tile_empty + qt);
+        if (qt == nt - 1) umma_commit_w(tile_empty + nt + kt);
     };
     if (warp == k12::kThreads / 32 - 1) {
         if (lane == 0) {  // ---------------- TMA: every Q and K tile of each item once
@@ -222,10 +223,9 @@ __global__ void __maxnreg__(72)
                     }
             }
         }
-    } else if (warp < 2) {
-        if (lane == 0)   // ---------------- warp 0: the phase-2 MMA stream; warp 1: phase 1
-            for (int it = blockIdx.x, li = 0; it < a.items; it += gridDim.x, ++li)
-                for (int u = 0; u < nblk; ++u) issue(warp == 0, li, u);
+    } else if (warp < 2) {   // ---------------- warp 0: the phase-2 MMA stream; warp 1: phase 1
+        for (int it = blockIdx.x, li = 0; it < a.items; it += gridDim.x, ++li)
+            for (int u = 0; u < nblk; ++u) issue(warp == 0, li, u);
     } else if (warp < 2 + kAWarps) {
         // ---------------- group A: partial row statistics. Sub-group sub takes the
         // blocks with U & 1 == sub (S buffer sub), 64 columns [64 ch, +64) per warp.

@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(k1tc::kThreads, kTf32 ? 1 : 2)
     const CUtensorMap* tm_b = kMode == kRowStats ? &tm_k : &tm_q;   // streamed blocks
     const CUtensorMap* tm_a2 = kMode == kRowStats ? &tm_q2 : &tm_k2;
     const CUtensorMap* tm_b2 = kMode == kRowStats ? &tm_k2 : &tm_q2;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int warp = __shfl_sync(0xffffffffu, (int)threadIdx.x >> 5, 0), lane = threadIdx.x & 31;   // uniform: see k4_apply_tf32
     const int b = blockIdx.z, h = blockIdx.y, r0 = blockIdx.x * kBM;
     const int nblk = (n + kBN - 1) / kBN;
     const size_t bh = (size_t)b * heads + h;
@@ -138,39 +138,36 @@ __global__ void __launch_bounds__(k1tc::kThreads, kTf32 ? 1 : 2)
                 load_tile(smem + kSmemB + s * kTileBytes, tm_b, tm_b2, b_full + s, i * kBN);
             }
         }
-    } else if (warp == 1) {
-        if (lane == 0) {  // ---------------- MMA issuer
-            const uint32_t a_addr = smem_u32(smem + kSmemA);
-            mbar_wait(a_full, 0);
-            for (int i = 0; i < nblk; ++i) {
-                const int s = i % kStages, sb = i & 1;
-                mbar_wait(b_full + s, (i / kStages) & 1);
-                mbar_wait(s_empty + sb, ((i >> 1) & 1) ^ 1);
-                tc_fence_after();
-                const uint32_t b_addr = smem_u32(smem + kSmemB + s * kTileBytes);
-                if constexpr (!kTf32) {
+    } else if (warp == 1) {   // ---------------- MMA issuer (whole warp; one elected lane issues)
+        const uint64_t da = sw128_desc(smem_u32(smem + kSmemA), 16, 1024);
+        const uint64_t db0 = sw128_desc(smem_u32(smem + kSmemB), 16, 1024);
+        mbar_wait(a_full, 0);
+        for (int i = 0; i < nblk; ++i) {
+            const int s = i % kStages, sb = i & 1;
+            mbar_wait(b_full + s, (i / kStages) & 1);
+            mbar_wait(s_empty + sb, ((i >> 1) & 1) ^ 1);
+            tc_fence_after();
+            const uint64_t db = desc_add(db0, s * kTileBytes);
+            if constexpr (!kTf32) {
 #pragma unroll
-                    for (int kk = 0; kk < kDh / 16; ++kk)
-                        umma_f16(tmem + sb * kBN, sw128_desc(a_addr + kk * 32, 16, 1024),
-                                 sw128_desc(b_addr + kk * 32, 16, 1024), kIdesc, kk > 0 ? 1u : 0u);
-                } else {   // hi.lo + lo.hi + hi.hi, K = 8 fp32 (32 B) per instruction. The small
-                           // products go first: every instruction rounds the fp32 accumulator,
-                           // and only the last eight (hi.hi) do so at the magnitude of S
+                for (int kk = 0; kk < kDh / 16; ++kk)
+                    umma_f16_w(tmem + sb * kBN, desc_add(da, kk * 32), desc_add(db, kk * 32), kIdesc, kk > 0 ? 1u : 0u);
+            } else {   // hi.lo + lo.hi + hi.hi, K = 8 fp32 (32 B) per instruction. The small
+                       // products go first: every instruction rounds the fp32 accumulator,
+                       // and only the last eight (hi.hi) do so at the magnitude of S
 #pragma unroll
-                    for (int pr = 0; pr < 3; ++pr) {
-                        const uint32_t ap = pr == 1 ? Ly::kPartBytes : 0u, bp = pr == 0 ? Ly::kPartBytes : 0u;
+                for (int pr = 0; pr < 3; ++pr) {
+                    const uint32_t ap = pr == 1 ? Ly::kPartBytes : 0u, bp = pr == 0 ? Ly::kPartBytes : 0u;
 #pragma unroll
-                        for (int at = 0; at < 2; ++at)
+                    for (int at = 0; at < 2; ++at)
 #pragma unroll
-                            for (int kk = 0; kk < 4; ++kk)
-                                umma_tf32(tmem + sb * kBN, sw128_desc(a_addr + ap + at * kAtomBytes + kk * 32, 16, 1024),
-                                          sw128_desc(b_addr + bp + at * kAtomBytes + kk * 32, 16, 1024), kIdesc,
-                                          (pr | at | kk) != 0);
-                    }
+                        for (int kk = 0; kk < 4; ++kk)
+                            umma_tf32_w(tmem + sb * kBN, desc_add(da, ap + at * kAtomBytes + kk * 32),
+                                        desc_add(db, bp + at * kAtomBytes + kk * 32), kIdesc, (pr | at | kk) != 0);
                 }
-                umma_commit(s_full + sb);
-                umma_commit(b_empty + s);
             }
+            umma_commit_w(s_full + sb);
+            umma_commit_w(b_empty + s);
         }
     } else {  // ------------------------------- consumers (warps 2..9)
         const int cw = warp - 2;

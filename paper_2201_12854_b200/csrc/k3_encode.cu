@@ -606,7 +606,7 @@ size_t k3_bf16_smem_bytes(int d_in) {
 // loaded into registers while the current one computes.
 template <class T, class Acc>
 __global__ void __launch_bounds__(128) k3b_encode_exact(K3Args a) {
-    constexpr int kTM = 64, kTK = 32, kThreads = 128;
+    constexpr int kTM = 64, kTK = 32;
     using Acc2 = std::conditional_t<sizeof(Acc) == 8, double2, float2>;
     __shared__ __align__(16) Acc xs[kTK][kTM];   // transposed X chunk: xs[k][token]
     __shared__ __align__(16) Acc ws[kTK][kDh];

@@ -64,7 +64,7 @@ __global__ void __launch_bounds__(k3btc::kThreads, 2) k3b_exact_tc(K3Args a) {
     uint64_t* empty = bars + kStages;    // [kStages], MMA commit
     uint64_t* acc_full = bars + 2 * kStages;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 1);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int warp = __shfl_sync(0xffffffffu, (int)threadIdx.x >> 5, 0), lane = threadIdx.x & 31;   // uniform: see k4_apply_tf32
     const int d_in = a.d_in, n = a.n;
     const int nchunks = (d_in + kBK - 1) / kBK;
     const size_t HD = (size_t)a.heads * kDh;

@@ -93,7 +93,7 @@ __global__ void __launch_bounds__(k4tc::kThreads, 2)
     griddep_trigger();
     // Q and K are inputs: their loads and the first S MMAs may run while the
     // encoders drain; lse (score pass) and H~ (encoders) are read after griddep_wait()
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int warp = __shfl_sync(0xffffffffu, (int)threadIdx.x >> 5, 0), lane = threadIdx.x & 31;   // uniform: see k4_apply_tf32
     const int nmt = (n + kBM - 1) / kBM;                   // query tiles per (b, h)
     const int nkb = (n + kBK - 1) / kBK;
     const int ntiles = batch * heads * nmt;
@@ -149,46 +149,45 @@ __global__ void __launch_bounds__(k4tc::kThreads, 2)
                 }
             }
         }
-    } else if (warp == 1) {
-        if (lane == 0) {  // ---------------- MMA issuer
-            auto issue_s = [&](int g) {
-                const int s = g % kStages, sb = g & 1;
-                mbar_wait(k_full + s, (g / kStages) & 1);
-                tc_fence_after();
-                const uint32_t k_addr = smem_u32(smem + kSmemK + s * kTileBytes);
+    } else if (warp == 1) {   // ---------------- MMA issuer (whole warp; one elected lane issues)
+        const uint64_t dk0 = sw128_desc(smem_u32(smem + kSmemK), 16, 1024);
+        const uint64_t dh0 = sw128_desc(smem_u32(smem + kSmemH), kBK * 128, 1024);
+        auto issue_s = [&](int g) {
+            const int s = g % kStages, sb = g & 1;
+            mbar_wait(k_full + s, (g / kStages) & 1);
+            tc_fence_after();
+            const uint64_t dk = desc_add(dk0, s * kTileBytes);
 #pragma unroll
-                for (int kk = 0; kk < kDh / 16; ++kk)
-                    umma_f16_ts(tmem + sb * kBK, tmem + kQCol + kk * 8, sw128_desc(k_addr + kk * 32, 16, 1024),
-                                kIdescS, kk > 0 ? 1u : 0u);
-                umma_commit(s_full + sb);
-                umma_commit(k_empty + s);
-            };
-            auto issue_pv = [&](int g, bool first) {
-                const int s = g % kStages, sb = g & 1;
-                mbar_wait(p_full + sb, (g >> 1) & 1);
-                mbar_wait(h_full + s, (g / kStages) & 1);
-                tc_fence_after();
-                const uint32_t h_addr = smem_u32(smem + kSmemH + s * kTileBytes);
+            for (int kk = 0; kk < kDh / 16; ++kk)
+                umma_f16_ts_w(tmem + sb * kBK, tmem + kQCol + kk * 8, desc_add(dk, kk * 32), kIdescS, kk > 0 ? 1u : 0u);
+            umma_commit_w(s_full + sb);
+            umma_commit_w(k_empty + s);
+        };
+        auto issue_pv = [&](int g, bool first) {
+            const int s = g % kStages, sb = g & 1;
+            mbar_wait(p_full + sb, (g >> 1) & 1);
+            mbar_wait(h_full + s, (g / kStages) & 1);
+            tc_fence_after();
+            const uint64_t dh = desc_add(dh0, s * kTileBytes);
 #pragma unroll
-                for (int kk = 0; kk < kBK / 16; ++kk)
-                    umma_f16_ts(tmem + kOCol, tmem + k4_p_col(sb, kk), sw128_desc(h_addr + kk * 2048, kBK * 128, 1024),
-                                kIdescO, (!first || kk > 0) ? 1u : 0u);
-                umma_commit(h_empty + s);
-            };
-            for (int i = 0; i < my_tiles; ++i) {
-                const int g0 = i * nkb;
-                mbar_wait(q_full, i & 1);
-                tc_fence_after();
-                // S runs two blocks ahead of P.H~ (S(kb+2) goes into the buffer P(kb) just left)
-                issue_s(g0);
-                if (nkb > 1) issue_s(g0 + 1);
-                mbar_wait(o_empty, (i & 1) ^ 1);   // the previous tile's O has been read out
-                for (int kb = 0; kb < nkb; ++kb) {
-                    issue_pv(g0 + kb, kb == 0);
-                    if (kb + 2 < nkb) issue_s(g0 + kb + 2);
-                }
-                umma_commit(o_full);
+            for (int kk = 0; kk < kBK / 16; ++kk)
+                umma_f16_ts_w(tmem + kOCol, tmem + k4_p_col(sb, kk), desc_add(dh, kk * 2048), kIdescO,
+                              (!first || kk > 0) ? 1u : 0u);
+            umma_commit_w(h_empty + s);
+        };
+        for (int i = 0; i < my_tiles; ++i) {
+            const int g0 = i * nkb;
+            mbar_wait(q_full, i & 1);
+            tc_fence_after();
+            // S runs two blocks ahead of P.H~ (S(kb+2) goes into the buffer P(kb) just left)
+            issue_s(g0);
+            if (nkb > 1) issue_s(g0 + 1);
+            mbar_wait(o_empty, (i & 1) ^ 1);   // the previous tile's O has been read out
+            for (int kb = 0; kb < nkb; ++kb) {
+                issue_pv(g0 + kb, kb == 0);
+                if (kb + 2 < nkb) issue_s(g0 + kb + 2);
             }
+            umma_commit_w(o_full);
         }
     } else {  // ------------------------------- Q -> TMEM, softmax, epilogue (warps 2..9)
         const int quad = warp & 3;                 // TMEM lane quadrant this warp may access

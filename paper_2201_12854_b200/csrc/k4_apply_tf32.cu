@@ -5,17 +5,18 @@
 //       left in the workspace, fp32 accumulation in TMEM)
 //   P = 2^(scale log2e S - lse2_i)   (ex2.approx.f32, the row statistics of K1)
 //   O += P . H~ (3xTF32 again: P and H~ split into tf32 hi + lo parts)
-// CTA = (b, h, 128-query tile); 64-key blocks. Operands in 128B-swizzled
-// K-major atoms of 32 fp32 (tc_common.cuh layout):
-//   Q  [128 q x 64 d]  hi | lo, resident                       64 KB
-//   K  [64 keys x 64 d] hi | lo, per block                      32 KB
-//   V  [64 d x 64 keys] hi | lo (H~ transposed per head, k_split_transpose_h)  32 KB
-//   P  [128 q x 64 keys] hi | lo, written by the softmax warps  64 KB
-// TMEM: S (64 columns) and O (64 columns).
+// CTA = (b, h, 128-query tile); 32-key blocks, two stages of every per-block
+// operand. Operands in 128B-swizzled K-major atoms of 32 fp32 (tc_common.cuh):
+//   Q  [128 q x 64 d]  hi | lo, resident                              64 KB
+//   K  [32 keys x 64 d] hi | lo, 2 stages                            2 x 16 KB
+//   V  [64 d x 32 keys] hi | lo (H~ transposed per head, k_split_transpose_h), 2 stages  2 x 16 KB
+//   P  [128 q x 32 keys] hi | lo, written by the softmax warps, 2 stages  2 x 32 KB
+// TMEM: S in two 32-column buffers, O (64 columns).
 // Warp 0: TMA producer; warp 1: TMEM allocator + MMA issuer; warps 2-5:
 // softmax (one query row per thread) and the epilogue.
-// Overlap: K of block kb + 1 loads (and its S MMAs issue) while the softmax
-// warps turn S(kb) into P(kb); V(kb + 1) loads while P(kb) . V(kb) runs.
+// Overlap: the TMA loads of blocks kb + 1 and kb + 2 are in flight, S(kb + 1)
+// is computed while the softmax warps turn S(kb) into P(kb), and P(kb) . V(kb)
+// runs while the softmax warps work on block kb + 1.
 #pragma once
 
 #include "mca_common.cuh"
@@ -23,41 +24,49 @@
 
 namespace mca_dev {
 
+#ifndef MCA_K4TF_EXP
+#define MCA_K4TF_EXP 0   // diagnostics: 1 = softmax stores no P (MMA + TMA only), 2 = no MMAs (softmax + TMA only)
+#endif
 namespace k4tf {
-constexpr int kBM = 128, kBK = 64;
+constexpr int kBM = 128, kBK = 32, kStages = 2;
 constexpr int kThreads = 192;
 constexpr uint32_t kAtom128 = 128 * 128;     // 128 rows x 128 B
 constexpr uint32_t kAtom64 = 64 * 128;       // 64 rows x 128 B
-constexpr uint32_t kQBytes = 2 * 2 * kAtom128;    // 2 parts x 2 atoms = 64 KB
-constexpr uint32_t kKBytes = 2 * 2 * kAtom64;     // 32 KB
-constexpr uint32_t kVBytes = 2 * 2 * kAtom64;     // 32 KB
-constexpr uint32_t kPBytes = 2 * 2 * kAtom128;    // 64 KB
-constexpr uint32_t kSmemQ = 0, kSmemK = kQBytes, kSmemV = kSmemK + kKBytes, kSmemP = kSmemV + kVBytes;
-constexpr uint32_t kSmemBar = kSmemP + kPBytes;
+constexpr uint32_t kAtom32 = 32 * 128;       // 32 rows x 128 B
+constexpr uint32_t kQBytes = 2 * 2 * kAtom128;    // 2 parts x 2 atoms (d) = 64 KB
+constexpr uint32_t kKBytes = 2 * 2 * kAtom32;     // 2 parts x 2 atoms (d) = 16 KB per stage
+constexpr uint32_t kVBytes = 2 * kAtom64;         // 2 parts x 1 atom (keys) = 16 KB per stage
+constexpr uint32_t kPBytes = 2 * kAtom128;        // 2 parts x 1 atom (keys) = 32 KB per stage
+constexpr uint32_t kSmemQ = 0, kSmemK = kQBytes, kSmemV = kSmemK + kStages * kKBytes;
+constexpr uint32_t kSmemP = kSmemV + kStages * kVBytes;
+constexpr uint32_t kSmemBar = kSmemP + kStages * kPBytes;
 constexpr uint32_t kSmemBytes = kSmemBar + 256 + 1024;
-constexpr uint32_t kIdesc = mca_tc::idesc_tf32(kBM, 64);
+constexpr uint32_t kIdescS = mca_tc::idesc_tf32(kBM, kBK);   // S: N = 32 keys
+constexpr uint32_t kIdescO = mca_tc::idesc_tf32(kBM, kDh);   // O: N = 64 dims
 }  // namespace k4tf
 
-// 3xTF32 of one [128 x 64] x [64 x 64]^T product into d: for each of the two
-// 32-wide K atoms, K = 8 per instruction; small products first (see k1_scores_tc)
-__device__ __forceinline__ void umma_3xtf32_k64(uint32_t d, uint32_t a, uint32_t a_part, uint32_t a_atom, uint32_t b,
-                                                uint32_t b_part, uint32_t b_atom, bool accumulate) {
+// 3xTF32 of one [128 x 32 kAtoms] x [N x 32 kAtoms]^T product into d: K = 8 per
+// instruction, small products first (hi.lo, lo.hi, then hi.hi; see k1_scores_tc).
+// Warp-wide: a / b are the descriptors of the hi parts' first atoms.
+template <int kAtoms>
+__device__ __forceinline__ void umma_3xtf32(uint32_t d, uint32_t idesc, uint64_t a, uint32_t a_part, uint32_t a_atom,
+                                            uint64_t b, uint32_t b_part, uint32_t b_atom, bool accumulate) {
     using namespace mca_tc;
+    if (MCA_K4TF_EXP == 2) return;
 #pragma unroll
     for (int pr = 0; pr < 3; ++pr) {
         const uint32_t ap = pr == 1 ? a_part : 0u, bp = pr == 0 ? b_part : 0u;
 #pragma unroll
-        for (int at = 0; at < 2; ++at)
+        for (int at = 0; at < kAtoms; ++at)
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)
-                umma_tf32(d, sw128_desc(a + ap + at * a_atom + kk * 32, 16, 1024),
-                          sw128_desc(b + bp + at * b_atom + kk * 32, 16, 1024), k4tf::kIdesc,
-                          (accumulate || (pr | at | kk) != 0) ? 1u : 0u);
+                umma_tf32_w(d, desc_add(a, ap + at * a_atom + kk * 32), desc_add(b, bp + at * b_atom + kk * 32), idesc,
+                            (accumulate || (pr | at | kk) != 0) ? 1u : 0u);
     }
 }
 
-// maps: tm_qh / tm_ql, tm_kh / tm_kl: [B][n][H*64] fp32 views, box {32, 128} (q) / {32, 64} (k);
-// tm_vh / tm_vl: [B*H][64][n] fp32 (H~ transposed), box {32, 64}.
+// maps: tm_qh / tm_ql: [B][n][H*64] fp32 views, box {32, 128}; tm_kh / tm_kl:
+// box {32, 32}; tm_vh / tm_vl: [B*H][64][n] fp32 (H~ transposed), box {32, 64}.
 __global__ void __launch_bounds__(k4tf::kThreads, 1)
     k4_apply_tf32(const __grid_constant__ CUtensorMap tm_qh, const __grid_constant__ CUtensorMap tm_ql,
                   const __grid_constant__ CUtensorMap tm_kh, const __grid_constant__ CUtensorMap tm_kl,
@@ -67,32 +76,35 @@ __global__ void __launch_bounds__(k4tf::kThreads, 1)
     using namespace mca_tc;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // per stage s: k_full, k_empty, v_full, v_empty, s_full, s_free, p_full, p_free (8 x 2), then q_full, o_full
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kSmemBar);
-    uint64_t* q_full = bars + 0;
-    uint64_t* k_full = bars + 1;
+    uint64_t* k_full = bars + 0;
     uint64_t* k_empty = bars + 2;
-    uint64_t* v_full = bars + 3;
-    uint64_t* v_empty = bars + 4;
-    uint64_t* s_full = bars + 5;
-    uint64_t* s_free = bars + 6;
-    uint64_t* p_full = bars + 7;
-    uint64_t* p_free = bars + 8;
-    uint64_t* o_full = bars + 9;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint64_t* v_full = bars + 4;
+    uint64_t* v_empty = bars + 6;
+    uint64_t* s_full = bars + 8;
+    uint64_t* s_free = bars + 10;
+    uint64_t* p_full = bars + 12;
+    uint64_t* p_free = bars + 14;
+    uint64_t* q_full = bars + 16;
+    uint64_t* o_full = bars + 17;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 18);
+    // warp index through a shuffle: provably warp-uniform, so role branches keep
+    // the MMA descriptors in uniform registers
+    const int warp = __shfl_sync(0xffffffffu, (int)threadIdx.x >> 5, 0), lane = threadIdx.x & 31;
     const int b = blockIdx.z, h = blockIdx.y, i0 = blockIdx.x * kBM;
     const int nblk = (n + kBK - 1) / kBK;
     const size_t bh = (size_t)b * heads + h;
 
     if (threadIdx.x == 0) {
-        for (int i = 0; i < 10; ++i) mbar_init(bars + i, (i == 6 || i == 7) ? 4 : 1);   // s_free, p_full: 4 warps
+        for (int i = 0; i < 18; ++i) mbar_init(bars + i, (i >= 10 && i < 14) ? 4 : 1);   // s_free, p_full: 4 warps
         fence_barrier_init();
     }
     if (warp == 1) tmem_alloc<128>(tmem_slot);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    const uint32_t tmem = *tmem_slot;          // S: columns [0, 64), O: [64, 128)
+    const uint32_t tmem = *tmem_slot;          // S buffers: columns [0, 32), [32, 64); O: [64, 128)
     griddep_trigger();
 
     if (warp == 0) {
@@ -104,48 +116,58 @@ __global__ void __launch_bounds__(k4tf::kThreads, 1)
                     tma_load_3d(smem + kSmemQ + p * 2 * kAtom128 + at * kAtom128, p ? &tm_ql : &tm_qh, q_full,
                                 h * kDh + at * 32, i0, b);
             for (int kb = 0; kb < nblk; ++kb) {
-                mbar_wait(k_empty, (kb & 1) ^ 1);
-                mbar_expect_tx(k_full, kKBytes);
-                for (int p = 0; p < 2; ++p)
-                    for (int at = 0; at < 2; ++at)
-                        tma_load_3d(smem + kSmemK + p * 2 * kAtom64 + at * kAtom64, p ? &tm_kl : &tm_kh, k_full,
-                                    h * kDh + at * 32, kb * kBK, b);
-                mbar_wait(v_empty, (kb & 1) ^ 1);
-                mbar_expect_tx(v_full, kVBytes);
-                for (int p = 0; p < 2; ++p)
-                    for (int at = 0; at < 2; ++at)
-                        tma_load_3d(smem + kSmemV + p * 2 * kAtom64 + at * kAtom64, p ? &tm_vl : &tm_vh, v_full,
-                                    kb * kBK + at * 32, 0, (int)bh);
-            }
-        }
-    } else if (warp == 1) {
-        if (lane == 0) {   // ---------------- MMA issuer
-            const uint32_t sq = smem_u32(smem + kSmemQ), sk = smem_u32(smem + kSmemK);
-            const uint32_t sv = smem_u32(smem + kSmemV), sp = smem_u32(smem + kSmemP);
-            mbar_wait(q_full, 0);
-            mbar_wait(k_full, 0);
-            tc_fence_after();
-            umma_3xtf32_k64(tmem, sq, 2 * kAtom128, kAtom128, sk, 2 * kAtom64, kAtom64, false);   // S(0)
-            umma_commit(s_full);
-            umma_commit(k_empty);
-            for (int kb = 0; kb < nblk; ++kb) {
-                if (kb + 1 < nblk) {   // S(kb + 1) runs while the softmax warps turn S(kb) into P(kb)
-                    mbar_wait(k_full, (kb + 1) & 1);
-                    mbar_wait(s_free, kb & 1);          // S(kb) is in the softmax warps' registers
-                    tc_fence_after();
-                    umma_3xtf32_k64(tmem, sq, 2 * kAtom128, kAtom128, sk, 2 * kAtom64, kAtom64, false);
-                    umma_commit(s_full);
-                    umma_commit(k_empty);
+                const int st = kb & 1;
+                const uint32_t ph = (kb >> 1) & 1;
+                mbar_wait(k_empty + st, ph ^ 1);
+                if (MCA_K4TF_EXP == 3) {   // diagnostics: no K / V loads (MMAs on stale operands)
+                    mbar_arrive(k_full + st);
+                    mbar_wait(v_empty + st, ph ^ 1);
+                    mbar_arrive(v_full + st);
+                    continue;
                 }
-                mbar_wait(p_full, kb & 1);
-                mbar_wait(v_full, kb & 1);
-                tc_fence_after();
-                umma_3xtf32_k64(tmem + 64, sp, 2 * kAtom128, kAtom128, sv, 2 * kAtom64, kAtom64, kb > 0);
-                umma_commit(p_free);
-                umma_commit(v_empty);
+                mbar_expect_tx(k_full + st, kKBytes);
+                for (int p = 0; p < 2; ++p)
+                    for (int at = 0; at < 2; ++at)
+                        tma_load_3d(smem + kSmemK + st * kKBytes + p * 2 * kAtom32 + at * kAtom32, p ? &tm_kl : &tm_kh,
+                                    k_full + st, h * kDh + at * 32, kb * kBK, b);
+                mbar_wait(v_empty + st, ph ^ 1);
+                mbar_expect_tx(v_full + st, kVBytes);
+                for (int p = 0; p < 2; ++p)
+                    tma_load_3d(smem + kSmemV + st * kVBytes + p * kAtom64, p ? &tm_vl : &tm_vh, v_full + st, kb * kBK,
+                                0, (int)bh);
             }
-            umma_commit(o_full);
         }
+    } else if (warp == 1) {   // ---------------- MMA issuer (whole warp; one elected lane issues)
+        const uint64_t dq = sw128_desc(smem_u32(smem + kSmemQ), 16, 1024);
+        const uint64_t dk = sw128_desc(smem_u32(smem + kSmemK), 16, 1024);
+        const uint64_t dv = sw128_desc(smem_u32(smem + kSmemV), 16, 1024);
+        const uint64_t dp = sw128_desc(smem_u32(smem + kSmemP), 16, 1024);
+        auto issue_s = [&](int m) {   // S(m) -> TMEM buffer m & 1
+            const int st = m & 1;
+            const uint32_t ph = (m >> 1) & 1;
+            mbar_wait(k_full + st, ph);
+            mbar_wait(s_free + st, ph ^ 1);         // the softmax warps have read S(m - 2)
+            tc_fence_after();
+            umma_3xtf32<2>(tmem + st * kBK, kIdescS, dq, 2 * kAtom128, kAtom128, desc_add(dk, st * kKBytes),
+                           2 * kAtom32, kAtom32, false);
+            umma_commit_w(s_full + st);
+            umma_commit_w(k_empty + st);
+        };
+        mbar_wait(q_full, 0);
+        issue_s(0);
+        for (int kb = 0; kb < nblk; ++kb) {
+            if (kb + 1 < nblk) issue_s(kb + 1);   // S(kb + 1) runs while the softmax warps turn S(kb) into P(kb)
+            const int st = kb & 1;
+            const uint32_t ph = (kb >> 1) & 1;
+            mbar_wait(p_full + st, ph);
+            mbar_wait(v_full + st, ph);
+            tc_fence_after();
+            umma_3xtf32<1>(tmem + 64, kIdescO, desc_add(dp, st * kPBytes), kAtom128, 0, desc_add(dv, st * kVBytes),
+                           kAtom64, 0, kb > 0);
+            umma_commit_w(p_free + st);
+            umma_commit_w(v_empty + st);
+        }
+        umma_commit_w(o_full);
     } else {   // ------------------------------- softmax + epilogue (warps 2-5)
         const int quad = warp & 3;
         const int r = quad * 32 + lane;                 // TMEM lane = query row of the tile
@@ -153,39 +175,36 @@ __global__ void __launch_bounds__(k4tf::kThreads, 1)
         const float c2 = scale * 1.4426950408889634f;
         const float l2 = (i0 + r < n) ? lse[bh * n + i0 + r] * 1.4426950408889634f : 0.f;
         for (int kb = 0; kb < nblk; ++kb) {
-            mbar_wait(s_full, kb & 1);
+            const int st = kb & 1;
+            const uint32_t ph = (kb >> 1) & 1;
+            mbar_wait(s_full + st, ph);
             tc_fence_after();
-            uint32_t sv[2][32];
-            tmem_ld32(lane_base, sv[0]);
-            tmem_ld32(lane_base + 32, sv[1]);
+            uint32_t sv[32];
+            tmem_ld32(lane_base + st * kBK, sv);
             tmem_ld_wait();
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(s_free);
+            if (lane == 0) mbar_arrive(s_free + st);
             const int valid = min(kBK, n - kb * kBK);
-            mbar_wait(p_free, (kb & 1) ^ 1);            // P(kb - 1) . V has read the P buffer
+            mbar_wait(p_free + st, ph ^ 1);             // P(kb - 2) . V has read this P buffer
+            uint8_t* pb = smem + kSmemP + st * kPBytes;
 #pragma unroll
-            for (int at = 0; at < 2; ++at) {
+            for (int g = 0; g < (MCA_K4TF_EXP == 1 ? 0 : 8); ++g) {               // 16-byte chunk g: keys 4 g ..
+                float hi[4], lo[4];
 #pragma unroll
-                for (int g = 0; g < 8; ++g) {           // 16-byte chunk g of atom at: keys 32 at + 4 g ..
-                    float hi[4], lo[4];
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const int c = at * 32 + g * 4 + e;
-                        const float p = c < valid ? ex2_approx(__fmaf_rn(__uint_as_float(sv[c >> 5][c & 31]), c2, -l2))
-                                                  : 0.f;
-                        hi[e] = __uint_as_float(__float_as_uint(p) & 0xFFFFE000u);
-                        lo[e] = p - hi[e];
-                    }
-                    const uint32_t off = at * kAtom128 + sw128_offset((uint32_t)r, (uint32_t)g * 16);
-                    *reinterpret_cast<float4*>(smem + kSmemP + off) = make_float4(hi[0], hi[1], hi[2], hi[3]);
-                    *reinterpret_cast<float4*>(smem + kSmemP + 2 * kAtom128 + off) =
-                        make_float4(lo[0], lo[1], lo[2], lo[3]);
+                for (int e = 0; e < 4; ++e) {
+                    const int c = g * 4 + e;
+                    const float p = c < valid ? ex2_approx(__fmaf_rn(__uint_as_float(sv[c]), c2, -l2)) : 0.f;
+                    hi[e] = __uint_as_float(__float_as_uint(p) & 0xFFFFE000u);
+                    lo[e] = p - hi[e];
                 }
+                const uint32_t off = sw128_offset((uint32_t)r, (uint32_t)g * 16);
+                *reinterpret_cast<float4*>(pb + off) = make_float4(hi[0], hi[1], hi[2], hi[3]);
+                *reinterpret_cast<float4*>(pb + kAtom128 + off) = make_float4(lo[0], lo[1], lo[2], lo[3]);
             }
             fence_proxy_async_smem();                   // generic-proxy writes -> the tensor core
             __syncwarp();
-            if (lane == 0) mbar_arrive(p_full);
+            if (lane == 0) mbar_arrive(p_full + st);
         }
         // epilogue: O (fp32, exact 3xTF32 accumulation) -> y
         mbar_wait(o_full, 0);

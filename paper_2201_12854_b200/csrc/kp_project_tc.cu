@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(kp::kThreads, 1) kp_project_tc(const __grid_co
     uint64_t* acc_full = bars + 2 * S;   // [2] MMA commit after a tile's last K step
     uint64_t* acc_empty = bars + 2 * S + 2;   // [2] 4 epilogue warps
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 4);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int warp = __shfl_sync(0xffffffffu, (int)threadIdx.x >> 5, 0), lane = threadIdx.x & 31;   // uniform: see k4_apply_tf32
     const int nK = (a.d_in + C::kBK - 1) / C::kBK;
     const int nM = (a.M + kp::kBM - 1) / kp::kBM;
     const int nN = a.nseg * a.HD / BN;
@@ -152,47 +152,45 @@ __global__ void __launch_bounds__(kp::kThreads, 1) kp_project_tc(const __grid_co
                 }
             }
         }
-    } else if (warp == 1) {
-        if (lane == 0) {
-            int s = 0;
-            uint32_t ph = 0;
-            int acc = 0;
-            uint32_t aph = 0;
-            for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-                mbar_wait(acc_empty + acc, aph ^ 1);    // the epilogue drained this accumulator
+    } else if (warp == 1) {   // ---------------- MMA issuer (whole warp; one elected lane issues)
+        const uint64_t d0 = sw128_desc(smem_u32(smem), 16, 1024);
+        int s = 0;
+        uint32_t ph = 0;
+        int acc = 0;
+        uint32_t aph = 0;
+        for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+            mbar_wait(acc_empty + acc, aph ^ 1);    // the epilogue drained this accumulator
+            tc_fence_after();
+            const uint32_t d = tmem + (uint32_t)(acc * BN);
+            for (int kb = 0; kb < nK; ++kb) {
+                mbar_wait(full + s, ph);
                 tc_fence_after();
-                const uint32_t d = tmem + (uint32_t)(acc * BN);
-                for (int kb = 0; kb < nK; ++kb) {
-                    mbar_wait(full + s, ph);
-                    tc_fence_after();
-                    const uint32_t sa = smem_u32(smem + s * C::kStageBytes);
-                    const uint32_t sb = sa + C::kABytes;
-                    if constexpr (kTf32) {   // hi.lo + lo.hi + hi.hi, K = 8 fp32 per instruction
+                const uint64_t da = desc_add(d0, s * C::kStageBytes);
+                const uint64_t db = desc_add(da, C::kABytes);
+                if constexpr (kTf32) {   // hi.lo + lo.hi + hi.hi, K = 8 fp32 per instruction
 #pragma unroll
-                        for (int pr = 0; pr < 3; ++pr) {
-                            const uint32_t ap = pr == 1 ? C::kAPart : 0u, bp = pr == 0 ? C::kBPart : 0u;
-#pragma unroll
-                            for (int kk = 0; kk < 4; ++kk)
-                                umma_tf32(d, sw128_desc(sa + ap + kk * 32, 16, 1024), sw128_desc(sb + bp + kk * 32, 16, 1024),
-                                          C::kIdesc, (kb | pr | kk) != 0);
-                        }
-                    } else {
+                    for (int pr = 0; pr < 3; ++pr) {
+                        const uint32_t ap = pr == 1 ? C::kAPart : 0u, bp = pr == 0 ? C::kBPart : 0u;
 #pragma unroll
                         for (int kk = 0; kk < 4; ++kk)
-                            umma_f16(d, sw128_desc(sa + kk * 32, 16, 1024), sw128_desc(sb + kk * 32, 16, 1024),
-                                     C::kIdesc, (kb | kk) != 0);
+                            umma_tf32_w(d, desc_add(da, ap + kk * 32), desc_add(db, bp + kk * 32), C::kIdesc,
+                                        (kb | pr | kk) != 0);
                     }
-                    umma_commit(empty + s);             // the stage is free once these MMAs read it
-                    if (++s == S) {
-                        s = 0;
-                        ph ^= 1;
-                    }
+                } else {
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk)
+                        umma_f16_w(d, desc_add(da, kk * 32), desc_add(db, kk * 32), C::kIdesc, (kb | kk) != 0);
                 }
-                umma_commit(acc_full + acc);            // the tile's accumulator is complete
-                if (++acc == 2) {
-                    acc = 0;
-                    aph ^= 1;
+                umma_commit_w(empty + s);             // the stage is free once these MMAs read it
+                if (++s == S) {
+                    s = 0;
+                    ph ^= 1;
                 }
+            }
+            umma_commit_w(acc_full + acc);            // the tile's accumulator is complete
+            if (++acc == 2) {
+                acc = 0;
+                aph ^= 1;
             }
         }
     } else {

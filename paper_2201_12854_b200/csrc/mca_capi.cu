@@ -1259,8 +1259,8 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
             };
             if (!make_tmap_f32(&tqh, parts, (uint64_t)H * kDh, n, B, 128) ||
                 !make_tmap_f32(&tql, parts + cnt, (uint64_t)H * kDh, n, B, 128) ||
-                !make_tmap_f32(&tkh, parts + 2 * cnt, (uint64_t)H * kDh, n, B, 64) ||
-                !make_tmap_f32(&tkl, parts + 3 * cnt, (uint64_t)H * kDh, n, B, 64) || !vmap(&tvh, vh) ||
+                !make_tmap_f32(&tkh, parts + 2 * cnt, (uint64_t)H * kDh, n, B, k4tf::kBK) ||
+                !make_tmap_f32(&tkl, parts + 3 * cnt, (uint64_t)H * kDh, n, B, k4tf::kBK) || !vmap(&tvh, vh) ||
                 !vmap(&tvl, vl))
                 return fail(MCA_ERR_CUDA, "cuTensorMapEncodeTiled failed for the K4 tf32 operands");
             MCA_CUDA_TRY(ensure_smem(k4_apply_tf32, k4tf::kSmemBytes));
