@@ -316,7 +316,7 @@ __global__ void k_split_tf32(const float4* __restrict__ src, float4* __restrict_
         c.y = v.y - a.y;
         c.z = v.z - a.z;
         c.w = v.w - a.w;
-        hi[i] = a;
+        if (hi) hi[i] = a;   // nullptr: the caller uses src itself as the hi operand
         lo[i] = c;
     }
 }

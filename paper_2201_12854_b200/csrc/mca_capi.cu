@@ -211,7 +211,7 @@ struct mca_weights {
     void* wqkv_t = nullptr;       // [3*heads*dh][d_in] W_q^T | W_k^T | W_V^T (kp_project_tc's K-major B): bf16, or
                                   // for fp32 the tf32-exact hi parts, with the lo parts in wqkv_t_lo
     void* wqkv_t_lo = nullptr;
-    void* x_split = nullptr;      // fp32 path: x hi | lo [B*n, d_in] (3xTF32 projection A parts)
+    void* x_split = nullptr;      // fp32 path: x - hi(x) [B*n, d_in] (3xTF32 projection lo part; x is the hi part)
     long cap_x = 0;
     bool has_qk_t = false;        // the W_q^T | W_k^T rows are set (mca_set_projections)
     void* qk = nullptr;           // [2][B*n][heads*dh] projected q, k (workspace, grown on demand)
@@ -237,7 +237,7 @@ struct mca_weights {
     long cap_items = 0;
     long long* ovf_list = nullptr;            // [kOvfCap] fp16-overflowing 8-column chunks (bf16 path)
     float* ovf_rows = nullptr;                // [kOvfCap][8] their fp32 values
-    void* qk_split = nullptr;                 // fp32 path: q_hi | q_lo | k_hi | k_lo [B, n, H*64] (3xTF32)
+    void* qk_split = nullptr;                 // fp32 path: q_lo | k_lo [B, n, H*64] (3xTF32; q, k are the hi parts)
     float* vt_split = nullptr;                // fp32 path: H~ transposed hi | lo [B*H][64][n_pad] (K4 3xTF32)
     size_t cap_vt = 0;                        // floats
     long ovf_cap = 0;
@@ -343,7 +343,7 @@ mca_status ensure_workspace(mca_weights* w, long tokens, mca_stream_t stream) {
         cudaMalloc(&w->cert_cm, th * sizeof(double)) != cudaSuccess ||
         cudaMalloc(&w->ovf_list, std::min<long>(8L * (long)th, kOvfCap) * sizeof(long long)) != cudaSuccess ||
         cudaMalloc(&w->ovf_rows, std::min<long>(8L * (long)th, kOvfCap) * 8 * sizeof(float)) != cudaSuccess ||
-        (w->wdt == MCA_F32 && cudaMalloc(&w->qk_split, 4 * th * w->dh * sizeof(float)) != cudaSuccess) ||
+        (w->wdt == MCA_F32 && cudaMalloc(&w->qk_split, 2 * th * w->dh * sizeof(float)) != cudaSuccess) ||
         cudaMalloc(&w->row_done, th * sizeof(uint8_t)) != cudaSuccess) {
         cudaGetLastError();
         free_workspace(w);
@@ -590,19 +590,21 @@ mca_status launch_projection(mca_weights* w, const void* x, long tokens, int seg
             cudaFree(w->x_split);
             w->x_split = nullptr;
             w->cap_x = 0;
-            if (cudaMalloc(&w->x_split, 2 * (size_t)tokens * w->d_in * sizeof(float)) != cudaSuccess) {
+            if (cudaMalloc(&w->x_split, (size_t)tokens * w->d_in * sizeof(float)) != cudaSuccess) {
                 cudaGetLastError();
                 return fail(MCA_ERR_ALLOC, "x split workspace allocation failed");
             }
             w->cap_x = tokens;
         }
         const size_t cnt = (size_t)tokens * w->d_in;
-        float* xh = static_cast<float*>(w->x_split);
-        float* xl = xh + cnt;
+        // kind::tf32 reads the top 19 bits of each fp32 operand (the low 13 are
+        // ignored: measured bitwise equal to the masked hi part), so x itself is
+        // the hi operand and only x - hi(x) is materialised
+        float* xl = static_cast<float*>(w->x_split);
         const unsigned gs = (unsigned)std::min<size_t>((cnt / 4 + 255) / 256, 8 * (size_t)sm_count());
-        k_split_tf32<<<gs, 256, 0, stream>>>((const float4*)x, (float4*)xh, (float4*)xl, cnt / 4);   // d_in % 4 == 0
+        k_split_tf32<<<gs, 256, 0, stream>>>((const float4*)x, nullptr, (float4*)xl, cnt / 4);   // d_in % 4 == 0
         MCA_LAUNCH_CHECK("k_split_tf32");
-        if (!make_tmap_f32(&tx, xh, (uint64_t)w->d_in, (uint64_t)tokens, 1, kp::kBM) ||
+        if (!make_tmap_f32(&tx, x, (uint64_t)w->d_in, (uint64_t)tokens, 1, kp::kBM) ||
             !make_tmap_f32(&tx2, xl, (uint64_t)w->d_in, (uint64_t)tokens, 1, kp::kBM) ||
             !make_tmap_f32(&tw, static_cast<const float*>(w->wqkv_t) + wofs, (uint64_t)w->d_in, (uint64_t)nseg * HD,
                            1, (uint32_t)BN) ||
@@ -1091,18 +1093,19 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
         const dim3 grid((n + kQT - 1) / kQT, H, B);
         if (dt == MCA_F32 && tf32_scores) {   // 3xTF32 tensor-core score passes on split q, k
             const size_t cnt = (size_t)tokens * H * kDh;
-            float* parts = static_cast<float*>(w->qk_split);   // q_hi | q_lo | k_hi | k_lo
+            // q, k are their own hi operands (kind::tf32 ignores the low 13 bits);
+            // the lo parts: q_lo | k_lo
+            float* parts = static_cast<float*>(w->qk_split);
             const unsigned gs = (unsigned)std::min<size_t>((cnt / 4 + 255) / 256, 8 * (size_t)sm_count());
-            k_split_tf32<<<gs, 256, 0, stream>>>((const float4*)q, (float4*)parts, (float4*)(parts + cnt), cnt / 4);
-            k_split_tf32<<<gs, 256, 0, stream>>>((const float4*)k, (float4*)(parts + 2 * cnt), (float4*)(parts + 3 * cnt),
-                                                  cnt / 4);
+            k_split_tf32<<<gs, 256, 0, stream>>>((const float4*)q, nullptr, (float4*)parts, cnt / 4);
+            k_split_tf32<<<gs, 256, 0, stream>>>((const float4*)k, nullptr, (float4*)(parts + cnt), cnt / 4);
             MCA_LAUNCH_CHECK("k_split_tf32");
             ++launches;
             CUtensorMap tqh, tql, tkh, tkl;
-            if (!make_tmap_f32(&tqh, parts, (uint64_t)H * kDh, n, B, 128) ||
-                !make_tmap_f32(&tql, parts + cnt, (uint64_t)H * kDh, n, B, 128) ||
-                !make_tmap_f32(&tkh, parts + 2 * cnt, (uint64_t)H * kDh, n, B, 128) ||
-                !make_tmap_f32(&tkl, parts + 3 * cnt, (uint64_t)H * kDh, n, B, 128))
+            if (!make_tmap_f32(&tqh, q, (uint64_t)H * kDh, n, B, 128) ||
+                !make_tmap_f32(&tql, parts, (uint64_t)H * kDh, n, B, 128) ||
+                !make_tmap_f32(&tkh, k, (uint64_t)H * kDh, n, B, 128) ||
+                !make_tmap_f32(&tkl, parts + cnt, (uint64_t)H * kDh, n, B, 128))
                 return fail(MCA_ERR_CUDA, "cuTensorMapEncodeTiled failed for the q/k tf32 parts");
             MCA_CUDA_TRY(ensure_smem(k1_scores_tc<kRowStats, true>, k1tc::kSmemBytesTf32));
             MCA_CUDA_TRY(ensure_smem(k1_scores_tc<kColMax, true>, k1tc::kSmemBytesTf32));
@@ -1257,10 +1260,10 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
             };
-            if (!make_tmap_f32(&tqh, parts, (uint64_t)H * kDh, n, B, 128) ||
-                !make_tmap_f32(&tql, parts + cnt, (uint64_t)H * kDh, n, B, 128) ||
-                !make_tmap_f32(&tkh, parts + 2 * cnt, (uint64_t)H * kDh, n, B, k4tf::kBK) ||
-                !make_tmap_f32(&tkl, parts + 3 * cnt, (uint64_t)H * kDh, n, B, k4tf::kBK) || !vmap(&tvh, vh) ||
+            if (!make_tmap_f32(&tqh, q, (uint64_t)H * kDh, n, B, 128) ||
+                !make_tmap_f32(&tql, parts, (uint64_t)H * kDh, n, B, 128) ||
+                !make_tmap_f32(&tkh, k, (uint64_t)H * kDh, n, B, k4tf::kBK) ||
+                !make_tmap_f32(&tkl, parts + cnt, (uint64_t)H * kDh, n, B, k4tf::kBK) || !vmap(&tvh, vh) ||
                 !vmap(&tvl, vl))
                 return fail(MCA_ERR_CUDA, "cuTensorMapEncodeTiled failed for the K4 tf32 operands");
             MCA_CUDA_TRY(ensure_smem(k4_apply_tf32, k4tf::kSmemBytes));
