@@ -73,6 +73,7 @@ struct K3Args {
     const int32_t* samp_list;  // [H, tokens]
     const int32_t* exact_list; // [H, tokens]
     const int* counts;         // [H, 2]: sampled, exact
+    long dense_min;            // > 0: k3b_exact_tc exits when sum_h counts[2 h + 1] >= dense_min (the dense GEMM ran)
     int* task_cursor;          // [H]
     long long* prof;           // optional phase clocks (MCA_K3_PROF=1, diagnostics only)
     OvfSink ovf;               // bf16 path: encodings outside fp16's range (mca_common.cuh)

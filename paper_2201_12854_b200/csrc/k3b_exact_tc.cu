@@ -57,6 +57,11 @@ __global__ void __launch_bounds__(k3btc::kThreads, 2) k3b_exact_tc(K3Args a) {
     if (prof && threadIdx.x == 0) g_k3b_prof[1] = clock64();
     const int ne = a.counts[2 * h + 1];
     if ((int)blockIdx.x * kBM >= ne) return;           // uniform early exit, before any barrier / TMEM use
+    if (a.dense_min > 0) {   // the dense X W_V GEMM encoded every exact token-head (kp_project_tc's gate)
+        long ex = 0;
+        for (int hh = 0; hh < a.heads; ++hh) ex += a.counts[2 * hh + 1];
+        if (ex >= a.dense_min) return;
+    }
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kSmemBar);

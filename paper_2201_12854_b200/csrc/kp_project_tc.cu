@@ -78,6 +78,17 @@ struct KpArgs {
     int HD;         // H * 64: segment s = product columns [s HD, (s + 1) HD)
     int nseg;       // 1..3 output segments
     int f16_mask;   // bit s: segment s stored as fp16 (else bf16)
+    // fp16 segments (H~): chunks of 8 values outside fp16's range are zeroed and,
+    // for exact token-heads (exact == nullptr: all of them), queued for the
+    // aggregation's fp32 fix-up (mca_common.cuh f16_guard8); n = tokens per sequence.
+    OvfSink ovf;
+    const uint8_t* exact;   // [B, H, n] or nullptr
+    int n;
+    // Device-side dispatch of the MCA layer's exact encodings (gate != nullptr):
+    // the GEMM runs only when sum_h gate[2 h + 1] >= gate_min (K2's exact counts),
+    // otherwise every CTA exits at once and k3b_exact_tc encodes the listed tokens.
+    const int* gate;
+    long gate_min;
 };
 
 // kTf32: tm_x / tm_w carry the hi parts and tm_x2 / tm_w2 the lo parts.
@@ -101,6 +112,12 @@ __global__ void __launch_bounds__(kp::kThreads, 1) kp_project_tc(const __grid_co
     uint64_t* acc_empty = bars + 2 * S + 2;   // [2] 4 epilogue warps
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 4);
     const int warp = __shfl_sync(0xffffffffu, (int)threadIdx.x >> 5, 0), lane = threadIdx.x & 31;   // uniform: see k4_apply_tf32
+    if (a.gate) {   // the exact fraction decides between this dense GEMM and the gathered one
+        griddep_wait();
+        long ex = 0;
+        for (int hh = 0; hh < a.HD / kDh; ++hh) ex += a.gate[2 * hh + 1];
+        if (ex < a.gate_min) return;
+    }
     const int nK = (a.d_in + C::kBK - 1) / C::kBK;
     const int nM = (a.M + kp::kBM - 1) / kp::kBM;
     const int nN = a.nseg * a.HD / BN;
@@ -232,7 +249,36 @@ __global__ void __launch_bounds__(kp::kThreads, 1) kp_project_tc(const __grid_co
                     for (int g = 0; g < 8; ++g) {        // 16-byte chunk g = columns 8g .. 8g + 7
                         const uint32_t* src = &v[g >> 2][(g & 3) * 8];
                         uint4 u;
-                        if (f16) {
+                        if (f16 && a.ovf.count) {   // fp16 range guard (H~ segments)
+                            float f[8];
+                            bool big = false;
+#pragma unroll
+                            for (int e = 0; e < 8; ++e) {
+                                f[e] = __uint_as_float(src[e]);
+                                big |= f16_overflows(f[e]);
+                            }
+                            const int t = m0 + (int)r;
+                            if (big && t < a.M) {
+                                const int col = oc + c + 8 * g, hh = col / kDh, bb = t / a.n, j = t - bb * a.n;
+                                const long long tokh = ((long long)bb * (a.HD / kDh) + hh) * a.n + j;
+                                if (!a.exact || a.exact[tokh]) {   // sampled token-heads: K3 rewrites the row
+                                    const unsigned long long pos = atomicAdd(a.ovf.count, 1ull);
+                                    if (pos < (unsigned long long)a.ovf.cap) {
+                                        a.ovf.list[pos] = tokh * 8 + ((col % kDh) >> 3);
+#pragma unroll
+                                        for (int e = 0; e < 8; ++e) a.ovf.rows[pos * 8 + e] = f[e];
+                                    }
+                                }
+                            }
+                            if (big) {
+                                u = make_uint4(0u, 0u, 0u, 0u);
+                            } else {
+                                u.x = pack_f16x2(f[0], f[1]);
+                                u.y = pack_f16x2(f[2], f[3]);
+                                u.z = pack_f16x2(f[4], f[5]);
+                                u.w = pack_f16x2(f[6], f[7]);
+                            }
+                        } else if (f16) {
                             u.x = pack_f16x2(__uint_as_float(src[0]), __uint_as_float(src[1]));
                             u.y = pack_f16x2(__uint_as_float(src[2]), __uint_as_float(src[3]));
                             u.z = pack_f16x2(__uint_as_float(src[4]), __uint_as_float(src[5]));

@@ -389,6 +389,19 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
 // | budget histograms [H, d + 1] | list fill counters [H, d + 1]
 size_t zeroed_bytes(int heads, int d_in) { return 64 + (((size_t)heads * 8 + 63) & ~(size_t)63) + 2 * (size_t)heads * (d_in + 1) * 4; }
 
+// Exact-fraction threshold of the dense exact encoding (bf16 MCA layer): at C2 the
+// gathered k3b_exact_tc costs ~2.7 us per 1% of token-heads and the dense X W_V GEMM
+// ~30 us, so the dense GEMM wins above ~12%. MCA_DENSE_EXACT=0 disables it.
+constexpr double kDenseExactFrac = 0.12;
+bool dense_exact_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("MCA_DENSE_EXACT");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+long dense_exact_min(long token_heads) { return std::max(1L, (long)(kDenseExactFrac * (double)token_heads)); }
+
 bool use_k3t(const mca_weights* w) {
     return w->wdt == MCA_BF16 && w->wprime && !force_simt() && tile_k3_requested() && w->d_in % 8 == 0 &&
            k3t::layout(w->d_in).bytes <= 227u * 1024u;
@@ -398,7 +411,7 @@ bool use_k3t(const mca_weights* w) {
 template <class T, class Acc>
 mca_status launch_k3(mca_weights* w, const void* x, int B, int n, long b_offset, uint32_t layer, uint64_t seed,
                      void* hout, int32_t* draws, int draws_stride, mca_stream_t stream, int& launches,
-                     bool skip_exact = false) {
+                     bool skip_exact = false, long dense_min = 0) {
     using Coef = float;   // K3's per-row factor: 1/p(i) in fp32 (both dtypes accumulate in fp32)
     K3Args a{};
     a.x = x;
@@ -423,6 +436,7 @@ mca_status launch_k3(mca_weights* w, const void* x, int B, int n, long b_offset,
     a.samp_list = w->samp_list;
     a.exact_list = w->exact_list;
     a.counts = w->counts;
+    a.dense_min = dense_min;
     a.task_cursor = w->task_cursor;
     a.ovf.count = w->counters + kOvfCounter;
     a.ovf.list = w->ovf_list;
@@ -571,8 +585,10 @@ mca_status launch_lists(mca_weights* w, dim3 grid, int n, long tokens, mca_strea
 // W^T = [W_q^T | W_k^T | W_V^T]: segment s of x W goes to outs[s]. bf16 handles:
 // bf16 outputs, or fp16 when bit s of f16_mask is set. fp32 handles: 3xTF32 on
 // the hi / lo parts of x (split here) and W^T (split at preparation), fp32 outputs.
+// guard: the fp16 range guard / device gate fields of KpArgs (ovf, exact, n, gate,
+// gate_min); the shape fields are filled here.
 mca_status launch_projection(mca_weights* w, const void* x, long tokens, int seg0, int nseg, void* const outs[3],
-                             int f16_mask, mca_stream_t stream, int& launches) {
+                             int f16_mask, mca_stream_t stream, int& launches, const KpArgs* guard = nullptr) {
     const int HD = w->heads * w->dh;
     const bool tf32 = w->wdt == MCA_F32;
     if ((size_t)w->d_in * dtype_size(w->wdt) % 16 != 0)   // TMA: a 16-byte multiple row stride
@@ -629,7 +645,7 @@ mca_status launch_projection(mca_weights* w, const void* x, long tokens, int seg
                                               f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16);
         if (!ok) return fail(MCA_ERR_CUDA, "cuTensorMapEncodeTiled failed for the projection outputs");
     }
-    KpArgs pa{};
+    KpArgs pa = guard ? *guard : KpArgs{};
     pa.M = (int)tokens;
     pa.d_in = w->d_in;
     pa.HD = HD;
@@ -654,6 +670,21 @@ mca_status launch_projection(mca_weights* w, const void* x, long tokens, int seg
     if (ps) return ps;
     MCA_LAUNCH_CHECK("kp_project_tc");
     return MCA_OK;
+}
+
+// The fp16 range guard of a dense H~ segment (all token-heads exact when exact ==
+// nullptr), optionally gated on K2's exact counts (sum >= gate_min).
+KpArgs h_guard(mca_weights* w, int n, const uint8_t* exact, const int* gate, long gate_min) {
+    KpArgs g{};
+    g.ovf.count = w->counters + kOvfCounter;
+    g.ovf.list = w->ovf_list;
+    g.ovf.rows = w->ovf_rows;
+    g.ovf.cap = (int)w->ovf_cap;
+    g.exact = exact;
+    g.n = n;
+    g.gate = gate;
+    g.gate_min = gate_min;
+    return g;
 }
 
 // fp16 range guard's fix-up (k4o_overflow): after the aggregation, add P[:, j] H~_j
@@ -971,6 +1002,8 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
     // above the fp32 contract's 1e-5.
     const bool want_dense_h = !force_simt() && dt == MCA_BF16 && !approx && !budgets_out && !exact_out;
     bool h_dense = false;
+    // counters (incl. the fp16 guard's queue, which the dense H~ GEMM below may fill), cursors, histograms
+    MCA_CUDA_TRY(cudaMemsetAsync(w->zeroed, 0, zeroed_bytes(H, w->d_in), stream));
     if (!q) {   // q = x W_q, k = x W_k (+ H): one tcgen05 GEMM, outputs in the score kernels' layout
         const size_t HD = (size_t)H * w->dh, esz = dtype_size(dt);
         if (tokens > w->cap_qk) {
@@ -986,7 +1019,9 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
             w->cap_qk = tokens;
         }
         void* outs[3] = {w->qk, static_cast<char*>(w->qk) + (size_t)tokens * HD * esz, w->hbuf};
-        if (mca_status ps = launch_projection(w, x, tokens, 0, want_dense_h ? 3 : 2, outs, 0b100, stream, launches))
+        const KpArgs hg = h_guard(w, n, nullptr, nullptr, 0);
+        if (mca_status ps = launch_projection(w, x, tokens, 0, want_dense_h ? 3 : 2, outs, 0b100, stream, launches,
+                                              want_dense_h ? &hg : nullptr))
             return ps;
         h_dense = want_dense_h;
         q = w->qk;
@@ -998,7 +1033,8 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
     }
     if (want_dense_h && !h_dense) {   // given q, k: the H segment alone
         void* outs[3] = {nullptr, nullptr, w->hbuf};
-        if (mca_status ps = launch_projection(w, x, tokens, 2, 1, outs, 0b100, stream, launches)) return ps;
+        const KpArgs hg = h_guard(w, n, nullptr, nullptr, 0);
+        if (mca_status ps = launch_projection(w, x, tokens, 2, 1, outs, 0b100, stream, launches, &hg)) return ps;
         h_dense = true;
     }
     const bool h_done = h_dense && !approx;   // regular mode: no budgets, no encoders
@@ -1008,7 +1044,6 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
 
     if (dt == MCA_F32 || force_simt() || n > k1tc::kMaxN)   // atomicMax column keys (the TC pass writes each once)
         MCA_CUDA_TRY(cudaMemsetAsync(w->colkey, 0, th * sizeof(unsigned long long), stream));
-    MCA_CUDA_TRY(cudaMemsetAsync(w->zeroed, 0, zeroed_bytes(H, w->d_in), stream));   // counters, cursors, histograms
     const bool tile_k3 = dt == MCA_BF16 && use_k3t(w);   // k3t reads budgets directly: no work lists
     // bf16 score passes: Eq. 9 values within kCertTau of an integer boundary are
     // re-derived in binary64 by k2c_certify (the fp32 path's scores are fp64 already)
@@ -1210,6 +1245,16 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
             if (mca_status s = launch_lists(w, grid, n, tokens, stream, launches)) return s;
         }
     }
+    // bf16 MCA layer: when K2 marks at least kDenseExactFrac of the token-heads exact
+    // (small alpha), their encodings come from one dense X W_V GEMM (every row; K3
+    // then rewrites the sampled token-heads' rows) instead of k3b_exact_tc's gathered
+    // tiles. Decided on the device: both kernels read K2's counts, one of them exits.
+    const bool dense_gate = dt == MCA_BF16 && approx && !force_simt() && !tile_k3 && dense_exact_enabled();
+    if (dense_gate) {
+        void* outs[3] = {nullptr, nullptr, w->hbuf};
+        const KpArgs hg = h_guard(w, n, w->exact, w->counts, dense_exact_min(th));
+        if (mca_status ps = launch_projection(w, x, tokens, 2, 1, outs, 0b100, stream, launches, &hg)) return ps;
+    }
     if (w->timing) MCA_CUDA_TRY(cudaEventRecord(w->ev[3], stream));
     // K3: encoding (the dense exact layer's H came out of the projection GEMM)
     if (!h_done) {
@@ -1219,7 +1264,7 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
                            ? launch_k3<float, double>(w, x, B, n, b_offset, layer, seed, w->hbuf, draws, stride,
                                                       stream, launches, h_dense)
                            : launch_k3<__nv_bfloat16, float>(w, x, B, n, b_offset, layer, seed, w->hbuf, draws, stride,
-                                                             stream, launches);
+                                                             stream, launches, false, dense_gate ? dense_exact_min(th) : 0);
         if (s) return s;
     }
     if (w->timing) MCA_CUDA_TRY(cudaEventRecord(w->ev[4], stream));

@@ -700,12 +700,15 @@ def test_bf16_regular_forward_dense(mca, syn, orc, B, n, H, d_in):
     assert out.flops.reduction_factor == 1.0 and out.flops.exact_tokens == B * H * n and out.flops.samples == 0
 
 
-def test_fp16_encoding_range_guard(mca, syn, orc):
+@pytest.mark.parametrize("alpha,mode", [(0.4, "mca"), (0.03, "mca"), (None, "regular")])
+def test_fp16_encoding_range_guard(mca, syn, orc, alpha, mode):
     """bf16 path, H~ stored in fp16: a W_V row of near-zero norm (p ~ 1e-12)
     and outlier tokens whose encodings leave fp16's range (|H~| > 65504, in
     the sampled and the exact branch) must not produce inf / NaN or drop the
     outliers' contribution: the encoders queue those rows in fp32 and
-    k4o_overflow adds P[:, j] H~_j back after K4."""
+    k4o_overflow adds P[:, j] H~_j back after K4. alpha = 0.03
+    takes the dense exact encoding (kp_project_tc's guard, exact rows only);
+    the regular layer's dense H~ uses the same guard."""
     H, n, d_in = 12, 128, 768
     w = syn.make_weights(d_in, H, seed=21)
     w[7, :64] *= 3e-5                                   # p(7) ~ 1e-12 in head 0
@@ -718,13 +721,21 @@ def test_fp16_encoding_range_guard(mca, syn, orc):
     weights = mca.AttentionWeights(w.cuda(), heads=H)
     p, _ = weights.distributions()
     assert 0 < p[0, 7] < 1e-10
-    out = mca.mca_forward(weights, q, k, xb, mca.McaConfig(alpha=0.4), seed=3, return_plan=True)
+    if mode == "regular":
+        y = mca.regular_forward(weights, q, k, xb)
+        torch.cuda.synchronize()
+        assert torch.isfinite(y.float()).all()
+        ref = _oracle(orc, w, q, k, xb, H, mode="regular")
+        assert np.abs(ref.h).max() > 65504
+        assert _row_rel(_np(y), ref.y) <= TOL_Y[torch.bfloat16]
+        return
+    out = mca.mca_forward(weights, q, k, xb, mca.McaConfig(alpha=alpha), seed=3, return_plan=True)
     torch.cuda.synchronize()
     assert torch.isfinite(out.y.float()).all()
     b = out.budgets.cpu().numpy()
     e = out.exact_mask.cpu().numpy().astype(bool)
     assert e[0, :, 5].any() or (~e[0, :, 5]).any()
-    ref = _oracle(orc, w, q, k, xb, H, alpha=0.4, seed=3, budgets_override=b, exact_override=e)
+    ref = _oracle(orc, w, q, k, xb, H, alpha=alpha, seed=3, budgets_override=b, exact_override=e)
     assert np.abs(ref.h).max() > 65504                  # the case is really out of fp16's range
     assert _row_rel(_np(out.y), ref.y) <= TOL_Y[torch.bfloat16]
 
@@ -768,3 +779,50 @@ def test_unaligned_rows_are_refused(mca, syn):
     weights = mca.AttentionWeights(w, heads=H, w_q=wq, w_k=wq)
     x = torch.randn((1, 16, 104)).to(torch.bfloat16).cuda()
     assert torch.isfinite(mca.mca_forward(weights, None, None, x).y.float()).all()
+
+
+_DENSE_SNIPPET = r"""
+import sys, torch
+sys.path.insert(0, {root!r})
+import paper_2201_12854_b200 as mca
+from paper_2201_12854_b200.synthetic import make_weights, make_inputs
+H, n, d_in, B = 12, 256, 768, 2
+w = make_weights(d_in, H, seed=5).to(torch.bfloat16)
+inp = make_inputs(B, n, d_in, H, seed=5)
+q, k, x = (t.to(torch.bfloat16).cuda() for t in (inp.q, inp.k, inp.x))
+weights = mca.AttentionWeights(w.cuda(), heads=H)
+out = mca.mca_forward(weights, q, k, x, mca.McaConfig(alpha={alpha}), seed=11, return_plan=True)
+torch.save(dict(y=out.y.cpu(), e=out.exact_mask.cpu()), {path!r})
+"""
+
+
+@pytest.mark.parametrize("alpha", [0.03, 0.12])
+def test_dense_exact_dispatch(mca, syn, orc, alpha, tmp_path):
+    """Small alpha: K2 marks most token-heads exact and their encodings come from
+    the dense X W_V GEMM (kp_project_tc gated on K2's counts; k3b_exact_tc exits).
+    y and H~ against the oracle with the GPU's plan; and the output equals the
+    gathered path's (MCA_DENSE_EXACT=0, read once per process) bitwise, so the
+    device-side choice cannot break batch-shard invariance."""
+    import subprocess
+    import sys
+    H, n, d_in, B = 12, 256, 768, 2
+    weights, w, q, k, x = _setup(mca, syn, B, n, d_in, H, torch.bfloat16, seed=5)
+    dbg = dict(h_out=torch.zeros_like(q, dtype=torch.float16))
+    out = mca.mca_forward(weights, q, k, x, mca.McaConfig(alpha=alpha), seed=11, return_plan=True, debug=dbg)
+    b = out.budgets.cpu().numpy()
+    e = out.exact_mask.cpu().numpy().astype(bool)
+    frac = float(e.mean())
+    print(f"alpha={alpha}: exact fraction {frac:.3f}")
+    ref = _oracle(orc, w, q, k, x, H, alpha=alpha, seed=11, budgets_override=b, exact_override=e)
+    assert _row_rel(_np(dbg["h_out"]), ref.h) <= TOL_H[torch.bfloat16]
+    assert _row_rel(_np(out.y), ref.y) <= TOL_Y[torch.bfloat16]
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    ys = {}
+    for mode in ("1", "0"):
+        path = str(tmp_path / f"y{mode}.pt")
+        r = subprocess.run([sys.executable, "-c", _DENSE_SNIPPET.format(root=root, alpha=alpha, path=path)],
+                           env=dict(os.environ, MCA_DENSE_EXACT=mode), capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        ys[mode] = torch.load(path)
+    assert torch.equal(ys["1"]["e"], ys["0"]["e"])
+    assert torch.equal(ys["1"]["y"], ys["0"]["y"])
