@@ -230,31 +230,41 @@ __global__ void __launch_bounds__(k4tf::kThreads, 1)
 
 // H~ [B, n, H*64] fp32 -> per head transposed, split: V^T hi / lo [B*H][64][ld]
 // (the K-major B operand of P . H~; ld = n rounded up to 4 for TMA's 16-byte
-// stride rule). grid (ceil(n / 32), H, B), block (32, 8).
-__global__ void k_split_transpose_h(const float* __restrict__ hm, int n, int ld, int heads, float* __restrict__ vh,
-                                    float* __restrict__ vl) {
-    __shared__ float tile[2][32][33];
-    const int j0 = blockIdx.x * 32, h = blockIdx.y, b = blockIdx.z;
+// stride rule). A block moves 64 tokens x 64 dims of one (b, h) with 16-byte
+// loads and stores on both sides (through a padded shared tile).
+// grid (ceil(n / 64), H, B), block 256.
+__global__ void __launch_bounds__(256) k_split_transpose_h(const float* __restrict__ hm, int n, int ld, int heads,
+                                                           float* __restrict__ vh, float* __restrict__ vl) {
+    __shared__ float tile[64][65];   // tile[d][j]
+    const int j0 = blockIdx.x * 64, h = blockIdx.y, b = blockIdx.z, tid = threadIdx.x;
     const size_t HD = (size_t)heads * kDh;
     const size_t bh = (size_t)b * heads + h;
-    for (int half = 0; half < 2; ++half) {                  // dims [32 half, +32)
-        for (int jj = threadIdx.y; jj < 32; jj += 8) {
-            const int j = j0 + jj;
-            tile[half][jj][threadIdx.x] = j < n ? hm[((size_t)b * n + j) * HD + (size_t)h * kDh + half * 32 + threadIdx.x] : 0.f;
-        }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const int e = tid + 256 * u, jj = e >> 4, d4 = (e & 15) * 4;
+        const int j = j0 + jj;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (j < n) v = *reinterpret_cast<const float4*>(hm + ((size_t)b * n + j) * HD + (size_t)h * kDh + d4);
+        tile[d4][jj] = v.x;
+        tile[d4 + 1][jj] = v.y;
+        tile[d4 + 2][jj] = v.z;
+        tile[d4 + 3][jj] = v.w;
     }
     __syncthreads();
-    for (int half = 0; half < 2; ++half) {
-        for (int dd = threadIdx.y; dd < 32; dd += 8) {
-            const int j = j0 + threadIdx.x;
-            if (j < n) {
-                const float v = tile[half][threadIdx.x][dd];
-                const float hi = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
-                const size_t o = (bh * kDh + half * 32 + dd) * (size_t)ld + j;
-                vh[o] = hi;
-                vl[o] = v - hi;
-            }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const int e = tid + 256 * u, d = e >> 4, j4 = (e & 15) * 4;
+        if (j0 + j4 >= ld) continue;
+        float v[4], hi[4], lo[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            v[q] = tile[d][j4 + q];
+            hi[q] = __uint_as_float(__float_as_uint(v[q]) & 0xFFFFE000u);
+            lo[q] = v[q] - hi[q];
         }
+        const size_t o = (bh * kDh + d) * (size_t)ld + j0 + j4;
+        *reinterpret_cast<float4*>(vh + o) = make_float4(hi[0], hi[1], hi[2], hi[3]);
+        *reinterpret_cast<float4*>(vl + o) = make_float4(lo[0], lo[1], lo[2], lo[3]);
     }
 }
 

@@ -89,6 +89,9 @@ struct KpArgs {
     // otherwise every CTA exits at once and k3b_exact_tc encodes the listed tokens.
     const int* gate;
     long gate_min;
+    // 3xTF32: segment s's lo part v - hi(v) also written here (nullptr: not
+    // wanted) -- the score passes' lo operands, so q / k need no split pass
+    float* lo_out[3];
 };
 
 // kTf32: tm_x / tm_w carry the hi parts and tm_x2 / tm_w2 the lo parts.
@@ -240,6 +243,20 @@ __global__ void __launch_bounds__(kp::kThreads, 1) kp_project_tc(const __grid_co
                     for (int g = 0; g < 8; ++g)
                         *reinterpret_cast<uint4*>(st + sw128_offset(r, (uint32_t)g * 16)) =
                             make_uint4(v[4 * g], v[4 * g + 1], v[4 * g + 2], v[4 * g + 3]);
+                    float* lo = a.lo_out[seg];
+                    if (lo && m0 + (int)r < a.M) {   // the row's lo parts: one full 128-byte line per thread
+                        float4* dst = reinterpret_cast<float4*>(lo + (size_t)(m0 + r) * a.HD + oc + c);
+#pragma unroll
+                        for (int g = 0; g < 8; ++g) {
+                            float e[4];
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) {
+                                const uint32_t b = v[4 * g + u];
+                                e[u] = __uint_as_float(b) - __uint_as_float(b & 0xFFFFE000u);
+                            }
+                            dst[g] = make_float4(e[0], e[1], e[2], e[3]);
+                        }
+                    }
                 } else {
                     uint32_t v[2][32];
                     tmem_ld32(lane_base + (uint32_t)(acc * BN + c), v[0]);

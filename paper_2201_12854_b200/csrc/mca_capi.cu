@@ -596,7 +596,8 @@ mca_status launch_projection(mca_weights* w, const void* x, long tokens, int seg
                     "(d_in = %d); pass q and k instead", dtype_size(w->wdt), w->d_in);
     // N tile: the widest of 256 / 128 / 64 that divides H*64 (192 for BERT-base's
     // finer wave quantisation measured 72 us vs 66 for 256: per-tile overheads)
-    const int BN = HD % 256 == 0 ? 256 : HD % 128 == 0 ? 128 : 64;
+    // 3xTF32: 128 (three 64 KB stages instead of two 96 KB ones; measured 291 vs 303 us at C2)
+    const int BN = (HD % 256 == 0 && !tf32) ? 256 : HD % 128 == 0 ? 128 : 64;
     CUtensorMap tx, tw, tx2, tw2, to[3];
     const size_t wofs = (size_t)seg0 * HD * w->d_in;
     if (tf32) {
@@ -1002,6 +1003,7 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
     // above the fp32 contract's 1e-5.
     const bool want_dense_h = !force_simt() && dt == MCA_BF16 && !approx && !budgets_out && !exact_out;
     bool h_dense = false;
+    bool qk_lo_done = false;   // fp32: the projection GEMM wrote q_lo | k_lo
     // counters (incl. the fp16 guard's queue, which the dense H~ GEMM below may fill), cursors, histograms
     MCA_CUDA_TRY(cudaMemsetAsync(w->zeroed, 0, zeroed_bytes(H, w->d_in), stream));
     if (!q) {   // q = x W_q, k = x W_k (+ H): one tcgen05 GEMM, outputs in the score kernels' layout
@@ -1019,9 +1021,14 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
             w->cap_qk = tokens;
         }
         void* outs[3] = {w->qk, static_cast<char*>(w->qk) + (size_t)tokens * HD * esz, w->hbuf};
-        const KpArgs hg = h_guard(w, n, nullptr, nullptr, 0);
+        KpArgs hg = h_guard(w, n, nullptr, nullptr, 0);
+        if (dt == MCA_F32 && w->qk_split) {   // the 3xTF32 score passes' q_lo | k_lo, from the GEMM's epilogue
+            hg.lo_out[0] = static_cast<float*>(w->qk_split);
+            hg.lo_out[1] = static_cast<float*>(w->qk_split) + (size_t)tokens * HD;
+            qk_lo_done = true;
+        }
         if (mca_status ps = launch_projection(w, x, tokens, 0, want_dense_h ? 3 : 2, outs, 0b100, stream, launches,
-                                              want_dense_h ? &hg : nullptr))
+                                              (want_dense_h || qk_lo_done) ? &hg : nullptr))
             return ps;
         h_dense = want_dense_h;
         q = w->qk;
@@ -1132,10 +1139,12 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
             // the lo parts: q_lo | k_lo
             float* parts = static_cast<float*>(w->qk_split);
             const unsigned gs = (unsigned)std::min<size_t>((cnt / 4 + 255) / 256, 8 * (size_t)sm_count());
-            k_split_tf32<<<gs, 256, 0, stream>>>((const float4*)q, nullptr, (float4*)parts, cnt / 4);
-            k_split_tf32<<<gs, 256, 0, stream>>>((const float4*)k, nullptr, (float4*)(parts + cnt), cnt / 4);
-            MCA_LAUNCH_CHECK("k_split_tf32");
-            ++launches;
+            if (!qk_lo_done) {
+                k_split_tf32<<<gs, 256, 0, stream>>>((const float4*)q, nullptr, (float4*)parts, cnt / 4);
+                k_split_tf32<<<gs, 256, 0, stream>>>((const float4*)k, nullptr, (float4*)(parts + cnt), cnt / 4);
+                MCA_LAUNCH_CHECK("k_split_tf32");
+                ++launches;
+            }
             CUtensorMap tqh, tql, tkh, tkl;
             if (!make_tmap_f32(&tqh, q, (uint64_t)H * kDh, n, B, 128) ||
                 !make_tmap_f32(&tql, parts, (uint64_t)H * kDh, n, B, 128) ||
@@ -1288,8 +1297,8 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
             }
             float* vh = w->vt_split;
             float* vl = w->vt_split + need / 2;
-            k_split_transpose_h<<<dim3((n + 31) / 32, H, B), dim3(32, 8), 0, stream>>>((const float*)w->hbuf, n, n_pad,
-                                                                                        H, vh, vl);
+            k_split_transpose_h<<<dim3((n + 63) / 64, H, B), 256, 0, stream>>>((const float*)w->hbuf, n, n_pad, H, vh,
+                                                                                vl);
             MCA_LAUNCH_CHECK("k_split_transpose_h");
             const size_t cnt = (size_t)tokens * H * kDh;
             float* parts = static_cast<float*>(w->qk_split);
