@@ -89,9 +89,11 @@ struct KpArgs {
     // otherwise every CTA exits at once and k3b_exact_tc encodes the listed tokens.
     const int* gate;
     long gate_min;
-    // 3xTF32: segment s's lo part v - hi(v) also written here (nullptr: not
-    // wanted) -- the score passes' lo operands, so q / k need no split pass
-    float* lo_out[3];
+    // 3xTF32, lo_tma != 0: the lo parts v - hi(v) of segments 0 / 1 also go out,
+    // through tm_o2 = a [2][M][HD] map (q_lo | k_lo: the score passes' lo
+    // operands, so q / k need no split pass); each chunk stages hi and lo in the
+    // two staging tiles.
+    int lo_tma;
 };
 
 // kTf32: tm_x / tm_w carry the hi parts and tm_x2 / tm_w2 the lo parts.
@@ -232,7 +234,10 @@ __global__ void __launch_bounds__(kp::kThreads, 1) kp_project_tc(const __grid_co
             tc_fence_after();
 #pragma unroll 1
             for (int c = 0; c < BN; c += C::kOutCols) {
-                if (et == 0) bulk_wait_read<C::kOutBufs - 1>();   // the store that used this buffer has read it
+                if (et == 0) {   // the store that used this buffer has read it (both buffers when lo goes out too)
+                    if (kTf32 && a.lo_tma) bulk_wait_read<0>();
+                    else bulk_wait_read<C::kOutBufs - 1>();
+                }
                 named_bar_sync(1, 128);
                 uint8_t* st = stage_out + ob * C::kOutBytes;
                 if constexpr (kTf32) {                    // 32 fp32 columns: one 128-byte row per thread
@@ -243,18 +248,17 @@ __global__ void __launch_bounds__(kp::kThreads, 1) kp_project_tc(const __grid_co
                     for (int g = 0; g < 8; ++g)
                         *reinterpret_cast<uint4*>(st + sw128_offset(r, (uint32_t)g * 16)) =
                             make_uint4(v[4 * g], v[4 * g + 1], v[4 * g + 2], v[4 * g + 3]);
-                    float* lo = a.lo_out[seg];
-                    if (lo && m0 + (int)r < a.M) {   // the row's lo parts: one full 128-byte line per thread
-                        float4* dst = reinterpret_cast<float4*>(lo + (size_t)(m0 + r) * a.HD + oc + c);
+                    if (a.lo_tma) {   // the lo parts into the other staging tile (both are free: see above)
+                        uint8_t* sl = stage_out + (ob ^ 1) * C::kOutBytes;
 #pragma unroll
                         for (int g = 0; g < 8; ++g) {
-                            float e[4];
+                            uint32_t e[4];
 #pragma unroll
                             for (int u = 0; u < 4; ++u) {
                                 const uint32_t b = v[4 * g + u];
-                                e[u] = __uint_as_float(b) - __uint_as_float(b & 0xFFFFE000u);
+                                e[u] = __float_as_uint(__uint_as_float(b) - __uint_as_float(b & 0xFFFFE000u));
                             }
-                            dst[g] = make_float4(e[0], e[1], e[2], e[3]);
+                            *reinterpret_cast<uint4*>(sl + sw128_offset(r, (uint32_t)g * 16)) = make_uint4(e[0], e[1], e[2], e[3]);
                         }
                     }
                 } else {
@@ -319,8 +323,10 @@ __global__ void __launch_bounds__(kp::kThreads, 1) kp_project_tc(const __grid_co
 #else
                     tma_store_3d(om, st, oc + c, m0, 0);  // rows past M are clipped by the tensor map
 #endif
+                    if (kTf32 && a.lo_tma) tma_store_3d(&tm_o2, stage_out + (ob ^ 1) * C::kOutBytes, oc + c, m0, seg);
                     bulk_commit();
                 }
+                if (kTf32 && a.lo_tma) continue;   // both tiles used: the next chunk waits for both
                 if (++ob == C::kOutBufs) ob = 0;
             }
             tc_fence_before();

@@ -637,7 +637,13 @@ mca_status launch_projection(mca_weights* w, const void* x, long tokens, int seg
         tw2 = tw;
     }
     int mask = 0;
+    const bool lo_tma = tf32 && guard && guard->lo_tma;
     for (int i = 0; i < 3; ++i) {
+        if (lo_tma && i == 2) {   // q_lo | k_lo: [2][tokens][HD], the third map
+            if (!make_tmap_f32(&to[2], outs[2], (uint64_t)HD, (uint64_t)tokens, 2, kp::kBM))
+                return fail(MCA_ERR_CUDA, "cuTensorMapEncodeTiled failed for the lo outputs");
+            continue;
+        }
         const int sg = std::min(seg0 + i, seg0 + nseg - 1);   // unused maps repeat the last segment
         const bool f16 = !tf32 && ((f16_mask >> sg) & 1);
         if (i < nseg && f16) mask |= 1 << i;
@@ -1023,8 +1029,8 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
         void* outs[3] = {w->qk, static_cast<char*>(w->qk) + (size_t)tokens * HD * esz, w->hbuf};
         KpArgs hg = h_guard(w, n, nullptr, nullptr, 0);
         if (dt == MCA_F32 && w->qk_split) {   // the 3xTF32 score passes' q_lo | k_lo, from the GEMM's epilogue
-            hg.lo_out[0] = static_cast<float*>(w->qk_split);
-            hg.lo_out[1] = static_cast<float*>(w->qk_split) + (size_t)tokens * HD;
+            hg.lo_tma = 1;
+            outs[2] = w->qk_split;
             qk_lo_done = true;
         }
         if (mca_status ps = launch_projection(w, x, tokens, 0, want_dense_h ? 3 : 2, outs, 0b100, stream, launches,
