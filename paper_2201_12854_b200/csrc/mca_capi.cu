@@ -37,6 +37,7 @@
 #include "k4_apply_tf32.cu"
 #include "kp_project_tc.cu"
 #include "ka_given_attn.cu"
+#include "ka_aggregate_tc.cu"
 #include "mca_diag.cuh"
 
 #ifndef MCA_K2_FUSED_SCAN
@@ -162,6 +163,19 @@ bool make_tmap_bf16(CUtensorMap* m, const void* base, uint64_t inner, uint64_t r
 
 // 3-D fp32 view [batch][rows][inner] with a {32, box_rows, 1} box (128 bytes) and
 // 128-byte swizzle: the tf32 operand atoms of k1_scores_tc<*, true>.
+// H~ transposed per head, [BH][64][n_pad] fp32 (k_split_transpose_h / k_transpose_h16): box {32 keys, 64 dims}
+bool make_vt_map(CUtensorMap* m, const float* base, int n, int n_pad, long BH) {
+    auto enc = tmap_encoder();
+    if (!enc) return false;
+    cuuint64_t dims[3] = {(cuuint64_t)n, (cuuint64_t)kDh, (cuuint64_t)BH};
+    cuuint64_t strides[2] = {(cuuint64_t)n_pad * 4, (cuuint64_t)kDh * n_pad * 4};
+    cuuint32_t box[3] = {32, 64, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 bool make_tmap_f32(CUtensorMap* m, const void* base, uint64_t inner, uint64_t rows, uint64_t batch, uint32_t box_rows) {
     auto enc = tmap_encoder();
     if (!enc) return false;
@@ -1309,17 +1323,7 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
             const size_t cnt = (size_t)tokens * H * kDh;
             float* parts = static_cast<float*>(w->qk_split);
             CUtensorMap tqh, tql, tkh, tkl, tvh, tvl;
-            auto vmap = [&](CUtensorMap* m, const float* base) {
-                auto enc = tmap_encoder();
-                if (!enc) return false;
-                cuuint64_t dims[3] = {(cuuint64_t)n, (cuuint64_t)kDh, (cuuint64_t)B * H};
-                cuuint64_t strides[2] = {(cuuint64_t)n_pad * 4, (cuuint64_t)kDh * n_pad * 4};
-                cuuint32_t box[3] = {32, 64, 1};
-                cuuint32_t estr[3] = {1, 1, 1};
-                return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box, estr,
-                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-            };
+            auto vmap = [&](CUtensorMap* m, const float* base) { return make_vt_map(m, base, n, n_pad, (long)B * H); };
             if (!make_tmap_f32(&tqh, q, (uint64_t)H * kDh, n, B, 128) ||
                 !make_tmap_f32(&tql, parts, (uint64_t)H * kDh, n, B, 128) ||
                 !make_tmap_f32(&tkh, k, (uint64_t)H * kDh, n, B, k4tf::kBK) ||
@@ -1435,13 +1439,53 @@ mca_status mca_forward_attn(mca_weights* w, const double* attn, const void* x, m
                                  : launch_k3<__nv_bfloat16, float>(w, x, B, n, b_offset, layer, seed, w->hbuf, nullptr,
                                                                    0, stream, launches);
     if (s) return s;
-    const dim3 ga(n, H, B);
-    if (dt == MCA_F32)
-        ka_aggregate<float, float><<<ga, kDh, 0, stream>>>(attn, (const float*)w->hbuf, n, H, (float*)y);
-    else
-        ka_aggregate<__nv_bfloat16, __half><<<ga, kDh, 0, stream>>>(attn, (const __half*)w->hbuf, n, H,
-                                                                   (__nv_bfloat16*)y);
-    MCA_LAUNCH_CHECK("ka_aggregate");
+    if (force_simt()) {   // CUDA cores, fp64 accumulation
+        const dim3 ga(n, H, B);
+        if (dt == MCA_F32)
+            ka_aggregate<float, float><<<ga, kDh, 0, stream>>>(attn, (const float*)w->hbuf, n, H, (float*)y);
+        else
+            ka_aggregate<__nv_bfloat16, __half><<<ga, kDh, 0, stream>>>(attn, (const __half*)w->hbuf, n, H,
+                                                                       (__nv_bfloat16*)y);
+        MCA_LAUNCH_CHECK("ka_aggregate");
+    } else {   // tensor cores: the fp64 dump rounded to fp32, split hi / lo; H~ transposed per head
+        const int n_pad = (n + 3) & ~3;
+        const size_t part = (size_t)B * H * kDh * n_pad;
+        const size_t need = (dt == MCA_F32 ? 2 : 1) * part;
+        if (need > w->cap_vt) {
+            if (w->cap_vt) MCA_CUDA_TRY(cudaStreamSynchronize(stream));
+            drop_graphs(w);
+            cudaFree(w->vt_split);
+            w->vt_split = nullptr;
+            w->cap_vt = 0;
+            if (cudaMalloc(&w->vt_split, need * sizeof(float)) != cudaSuccess) {
+                cudaGetLastError();
+                return fail(MCA_ERR_ALLOC, "H~ transpose workspace allocation failed");
+            }
+            w->cap_vt = need;
+        }
+        float* vh = w->vt_split;
+        float* vl = dt == MCA_F32 ? w->vt_split + part : vh;
+        const dim3 gt((n + 63) / 64, H, B);
+        if (dt == MCA_F32)
+            k_split_transpose_h<<<gt, 256, 0, stream>>>((const float*)w->hbuf, n, n_pad, H, vh, vl);
+        else
+            k_transpose_h16<<<gt, 256, 0, stream>>>((const __half*)w->hbuf, n, n_pad, H, vh);
+        MCA_LAUNCH_CHECK("k_transpose_h");
+        CUtensorMap tvh, tvl;
+        if (!make_vt_map(&tvh, vh, n, n_pad, (long)B * H) || !make_vt_map(&tvl, vl, n, n_pad, (long)B * H))
+            return fail(MCA_ERR_CUDA, "cuTensorMapEncodeTiled failed for H~^T");
+        const dim3 g4((n + katc::kBM - 1) / katc::kBM, H, B);
+        if (dt == MCA_F32) {
+            MCA_CUDA_TRY(ensure_smem(ka_aggregate_tc<true, float>, katc::kSmemBytes));
+            MCA_CUDA_TRY(launch_pdl(ka_aggregate_tc<true, float>, g4, dim3(katc::kThreads), katc::kSmemBytes, stream,
+                                    tvh, tvl, attn, n, H, (float*)y));
+        } else {
+            MCA_CUDA_TRY(ensure_smem(ka_aggregate_tc<false, __nv_bfloat16>, katc::kSmemBytes));
+            MCA_CUDA_TRY(launch_pdl(ka_aggregate_tc<false, __nv_bfloat16>, g4, dim3(katc::kThreads), katc::kSmemBytes,
+                                    stream, tvh, tvl, attn, n, H, (__nv_bfloat16*)y));
+        }
+        MCA_LAUNCH_CHECK("ka_aggregate_tc");
+    }
     if (dt == MCA_BF16)   // encodings outside fp16's range (normally none)
         if (mca_status s2 = launch_overflow_fixup(w, true, nullptr, nullptr, attn, 0.0, B, n, y, stream, launches))
             return s2;
