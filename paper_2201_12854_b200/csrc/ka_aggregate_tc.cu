@@ -8,14 +8,15 @@
 // alone on the bf16 path (fp16 H~ is exact in tf32: A_lo.H + A_hi.H).
 // Bound: HBM, the dump itself (8 B per entry; 1.6 GB at C2's shape).
 //
-// CTA = (128-row tile i0, h, b); 192 threads, ~97 KB of shared memory (two CTAs
+// CTA = (128-row tile i0, h, b); 320 threads, ~97 KB of shared memory (two CTAs
 // per SM):
 //   warp 0      TMA producer: H~^T hi (| lo) of 32-key blocks, 2 stages
 //   warp 1      TMEM allocator (64 columns: O) + MMA issuer (whole warp, elect.sync)
-//   warps 2-5   loaders: warp q reads rows 32 q .. 32 q + 31 of the block, one row
-//               (32 keys, 256 coalesced bytes) per instruction, and writes the
-//               fp32 hi / lo parts into the 128B-swizzled K-major P tile; then the
-//               epilogue (TMEM lane = row).
+//   warps 2-9   loaders: warp w reads 16 rows of the block, one row (32 keys,
+//               256 coalesced bytes) per instruction, the next block's rows in
+//               flight while it writes this block's fp32 hi / lo parts into the
+//               128B-swizzled K-major P tile; warps 2-5 then run the epilogue
+//               (TMEM lane = row).
 #pragma once
 
 #include "mca_common.cuh"
@@ -25,7 +26,8 @@ namespace mca_dev {
 
 namespace katc {
 constexpr int kBM = 128, kBK = 32, kStages = 2;
-constexpr int kThreads = 192;
+constexpr int kLoaders = 8;                    // loader warps: 16 rows each
+constexpr int kThreads = 64 + 32 * kLoaders;   // + TMA warp + MMA warp
 constexpr uint32_t kAtom128 = 128 * 128;   // P: 128 rows x 128 B (32 fp32 keys)
 constexpr uint32_t kAtom64 = 64 * 128;     // H~^T: 64 dims x 128 B (32 fp32 keys)
 constexpr uint32_t kPBytes = 2 * kAtom128;   // hi | lo: 32 KB per stage
@@ -47,7 +49,7 @@ __global__ void __launch_bounds__(katc::kThreads, 2)
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kSmemBar);
     uint64_t* v_full = bars + 0;     // [2] TMA
     uint64_t* v_empty = bars + 2;    // [2] MMA commit
-    uint64_t* p_full = bars + 4;     // [2] 4 loader warps
+    uint64_t* p_full = bars + 4;     // [2] kLoaders loader warps
     uint64_t* p_free = bars + 6;     // [2] MMA commit
     uint64_t* o_full = bars + 8;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 9);
@@ -57,7 +59,7 @@ __global__ void __launch_bounds__(katc::kThreads, 2)
     const size_t bh = (size_t)b * heads + h;
 
     if (threadIdx.x == 0) {
-        for (int i = 0; i < 9; ++i) mbar_init(bars + i, (i >= 4 && i < 6) ? 4 : 1);
+        for (int i = 0; i < 9; ++i) mbar_init(bars + i, (i >= 4 && i < 6) ? kLoaders : 1);
         fence_barrier_init();
     }
     if (warp == 1) tmem_alloc<64>(tmem_slot);
@@ -104,34 +106,45 @@ __global__ void __launch_bounds__(katc::kThreads, 2)
             umma_commit_w(v_empty + st);
         }
         umma_commit_w(o_full);
-    } else {   // ------------------------------- loaders + epilogue (warps 2-5)
-        const int quad = warp & 3;
+    } else {   // ------------------------------- loaders (warps 2-9) + epilogue (warps 2-5)
+        const int lw = warp - 2;                    // rows [16 lw, 16 lw + 16) of the tile
         const double* abase = attn + bh * (size_t)n * n;
+        double v[16];
+        auto fetch = [&](int kb) {
+            const int key = kb * kBK + lane;
+#pragma unroll
+            for (int rr = 0; rr < 16; ++rr) {
+                const int i = i0 + lw * 16 + rr;
+                v[rr] = (i < n && key < n) ? __ldg(abase + (size_t)i * n + key) : 0.0;
+            }
+        };
+        fetch(0);
         for (int kb = 0; kb < nblk; ++kb) {
             const int st = kb & 1;
             const uint32_t ph = (kb >> 1) & 1;
-            const int key = kb * kBK + lane;
-            // 32 rows of this warp, one coalesced 256-byte row per load, all in flight
-            double v[32];
+            float hi[16], lo[16];
 #pragma unroll
-            for (int rr = 0; rr < 32; ++rr) {
-                const int i = i0 + quad * 32 + rr;
-                v[rr] = (i < n && key < n) ? __ldg(abase + (size_t)i * n + key) : 0.0;
+            for (int rr = 0; rr < 16; ++rr) {
+                const float f = __double2float_rn(v[rr]);
+                hi[rr] = __uint_as_float(__float_as_uint(f) & 0xFFFFE000u);
+                lo[rr] = f - hi[rr];
             }
+            if (kb + 1 < nblk) fetch(kb + 1);        // the next block's rows in flight
             mbar_wait(p_free + st, ph ^ 1);          // P(kb - 2) . H~ has read this buffer
             uint8_t* pb = smem + kSmemP + st * kPBytes;
 #pragma unroll
-            for (int rr = 0; rr < 32; ++rr) {
-                const float f = __double2float_rn(v[rr]);
-                const float hi = __uint_as_float(__float_as_uint(f) & 0xFFFFE000u);
-                const uint32_t off = sw128_offset((uint32_t)(quad * 32 + rr), (uint32_t)lane * 4);
-                *reinterpret_cast<float*>(pb + off) = hi;
-                *reinterpret_cast<float*>(pb + kAtom128 + off) = f - hi;
+            for (int rr = 0; rr < 16; ++rr) {
+                const uint32_t off = sw128_offset((uint32_t)(lw * 16 + rr), (uint32_t)lane * 4);
+                *reinterpret_cast<float*>(pb + off) = hi[rr];
+                *reinterpret_cast<float*>(pb + kAtom128 + off) = lo[rr];
             }
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) mbar_arrive(p_full + st);
         }
+        if (warp >= 6) goto done;   // warps 2-5 hold TMEM lane quadrants 0-3 (warp % 4)
+        {
+        const int quad = warp & 3;
         // epilogue: O -> y, TMEM lane = row
         mbar_wait(o_full, 0);
         tc_fence_after();
@@ -162,7 +175,9 @@ __global__ void __launch_bounds__(katc::kThreads, 2)
                 }
             }
         }
+        }
     }
+done:
     tc_fence_before();
     __syncthreads();
     if (warp == 1) tmem_dealloc<64>(tmem);

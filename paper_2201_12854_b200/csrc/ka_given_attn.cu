@@ -14,15 +14,36 @@
 
 namespace mca_dev {
 
-// grid ((n + 255) / 256, B * H), 256 threads: thread = column j (coalesced rows)
-__global__ void ka_colmax(const double* __restrict__ attn, int n, long bh_count, double* __restrict__ cmax) {
+// grid ((n + 31) / 32, B * H), block (32, 8): thread (x, y) = column j = 32 blockIdx.x + x
+// over the rows i = y (mod 8) (a warp reads 256 contiguous bytes per row), then the
+// eight partial maxima of each column meet in shared memory.
+__global__ void __launch_bounds__(256) ka_colmax(const double* __restrict__ attn, int n, long bh_count,
+                                                 double* __restrict__ cmax) {
+    __shared__ double part[8][33];
     const long bh = grid_bh();
-    const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= n || bh >= bh_count) return;
-    const double* a = attn + (size_t)bh * n * n + j;
+    const int j = blockIdx.x * 32 + threadIdx.x;
+    if (bh >= bh_count) return;
     double m = -INFINITY;
-    for (int i = 0; i < n; ++i) m = fmax(m, a[(size_t)i * n]);
-    cmax[(size_t)bh * n + j] = m;
+    if (j < n) {
+        const double* a = attn + (size_t)bh * n * n + j;
+        double m1 = -INFINITY, m2 = -INFINITY, m3 = -INFINITY;
+        int i = threadIdx.y;
+        for (; i + 24 < n; i += 32) {   // four independent loads in flight
+            m = fmax(m, __ldg(a + (size_t)i * n));
+            m1 = fmax(m1, __ldg(a + (size_t)(i + 8) * n));
+            m2 = fmax(m2, __ldg(a + (size_t)(i + 16) * n));
+            m3 = fmax(m3, __ldg(a + (size_t)(i + 24) * n));
+        }
+        for (; i < n; i += 8) m = fmax(m, __ldg(a + (size_t)i * n));
+        m = fmax(fmax(m, m1), fmax(m2, m3));
+    }
+    part[threadIdx.y][threadIdx.x] = m;
+    __syncthreads();
+    if (threadIdx.y == 0 && j < n) {
+#pragma unroll
+        for (int y = 1; y < 8; ++y) m = fmax(m, part[y][threadIdx.x]);
+        cmax[(size_t)bh * n + j] = m;
+    }
 }
 
 // grid (n, H, B), 64 threads: thread = output column c of row i, head h

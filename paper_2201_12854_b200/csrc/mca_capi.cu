@@ -1414,7 +1414,7 @@ mca_status mca_forward_attn(mca_weights* w, const double* attn, const void* x, m
     MCA_CUDA_TRY(cudaMemsetAsync(w->zeroed, 0, zeroed_bytes(H, w->d_in), stream));   // counters, cursors, histograms
     double* cmax = reinterpret_cast<double*>(w->colkey);                             // [B, H, n] scratch
     const dim3 grid = bh_grid((n + 255) / 256, (long)B * H);
-    ka_colmax<<<grid, 256, 0, stream>>>(attn, n, (long)B * H, cmax);
+    ka_colmax<<<bh_grid((n + 31) / 32, (long)B * H), dim3(32, 8), 0, stream>>>(attn, n, (long)B * H, cmax);
     MCA_LAUNCH_CHECK("ka_colmax");
     K2Args a{};
     a.cmax_in = cmax;
