@@ -150,6 +150,16 @@ __device__ __forceinline__ void atomic_max_pos(double* p, double v) {
 
 // Rows [c0, c0 + cnt) of a [n][HD]-strided 64-wide operand -> s_stage (fp32):
 // every thread issues its 16-byte loads at once, so a chunk costs one round trip.
+// Pull the next chunk's rows into L2 while this one is computed (the staging
+// loads are otherwise full DRAM round trips: q / k were written long before).
+template <class T>
+__device__ __forceinline__ void prefetch_rows(const T* __restrict__ base, size_t stride, int c0, int n) {
+    constexpr int kLines = kDh * (int)sizeof(T) / 128;   // 128-byte lines per row
+    const int e = threadIdx.x, r = e / kLines;
+    if (r < kCertStage && c0 + r < n)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(base + (size_t)(c0 + r) * stride + (e % kLines) * (128 / sizeof(T))));
+}
+
 template <class T>
 __device__ __forceinline__ void stage_rows(float (*st)[kDh + 1], const T* __restrict__ base, size_t stride, int c0,
                                            int cnt) {
@@ -180,7 +190,7 @@ __global__ void __launch_bounds__(kCertThreads) k2c_certify(K2cArgs a) {
     __shared__ double s_ct[kCertCands];
     __shared__ int s_rows[kCertCands];
     __shared__ unsigned s_bm[kCertMaxN / 32];        // rows already queued in this batch
-    __shared__ float s_qr[kCertRows][kDh];           // candidate rows of one statistics pass
+    __shared__ double s_qr[kCertRows][kDh];          // candidate rows of one statistics pass (binary64)
     __shared__ double s_mref[kCertRows];
     __shared__ double s_part[kCertThreads / 32][kCertRows];
     __shared__ int s_nkeys, s_ncand, s_nrows, s_slot_next;
@@ -261,6 +271,7 @@ __global__ void __launch_bounds__(kCertThreads) k2c_certify(K2cArgs a) {
             __syncthreads();
             stage_rows(s_stage, Qb, HD, c0, cn);
             __syncthreads();
+            prefetch_rows(Qb, HD, c0 + kCertStage, a.n);
             static_assert(kCertThreads == 2 * kCertStage, "two threads per staged row");
             const int ii = tid % kCertStage, half = tid / kCertStage;
             if (ii < cn) {   // a query row per thread pair, the keys split between the two
@@ -315,7 +326,7 @@ __global__ void __launch_bounds__(kCertThreads) k2c_certify(K2cArgs a) {
             for (int e = tid; e < nr * kDh; e += kCertThreads) {
                 const int r = e / kDh, c = e - r * kDh;
                 const int i = all_rows ? r0 + r : s_rows[r0 + r];
-                s_qr[r][c] = to_f32(Qb[(size_t)i * HD + c]);
+                s_qr[r][c] = (double)to_f32(Qb[(size_t)i * HD + c]);
             }
             if (tid < nr) s_mref[tid] = rowm[all_rows ? r0 + tid : s_rows[r0 + tid]];
             __syncthreads();
@@ -327,19 +338,23 @@ __global__ void __launch_bounds__(kCertThreads) k2c_certify(K2cArgs a) {
                 __syncthreads();
                 stage_rows(s_stage, Kb, HD, c0, cn);
                 __syncthreads();
+                prefetch_rows(Kb, HD, c0 + kCertStage, a.n);
                 const int jj = tid % kCertStage, half = tid / kCertStage;
                 if (jj < cn) {   // a key row per thread pair, the candidate rows split between the two
+                    // rows half, half + 2, ...: each key element converted to binary64 once
+                    double t[kCertRows / 2];
 #pragma unroll
-                    for (int r = 0; r < kCertRows; ++r) {
-                        if ((r & 1) == half && r < nr) {
-                            double t0 = 0.0, t1 = 0.0;
+                    for (int q = 0; q < kCertRows / 2; ++q) t[q] = 0.0;
+#pragma unroll 8
+                    for (int e = 0; e < kDh; ++e) {
+                        const double kd = (double)s_stage[jj][e];
 #pragma unroll
-                            for (int e = 0; e < kDh; e += 2) {
-                                t0 = fma((double)s_stage[jj][e], (double)s_qr[r][e], t0);
-                                t1 = fma((double)s_stage[jj][e + 1], (double)s_qr[r][e + 1], t1);
-                            }
-                            part[r] += exp(a.scale * (t0 + t1) - s_mref[r]);
-                        }
+                        for (int q = 0; q < kCertRows / 2; ++q) t[q] = fma(kd, s_qr[2 * q + half][e], t[q]);
+                    }
+#pragma unroll
+                    for (int q = 0; q < kCertRows / 2; ++q) {   // compile-time indices into part[]
+                        if (half == 0 && 2 * q < nr) part[2 * q] += exp(a.scale * t[q] - s_mref[2 * q]);
+                        if (half == 1 && 2 * q + 1 < nr) part[2 * q + 1] += exp(a.scale * t[q] - s_mref[2 * q + 1]);
                     }
                 }
             }
