@@ -364,6 +364,9 @@ __device__ __forceinline__ void fma2_bf16_f32(float& acc0, float& acc1, uint32_t
 #ifndef MCA_K3S_PROF
 #define MCA_K3S_PROF 0
 #endif
+#ifndef MCA_K3_EXP
+#define MCA_K3_EXP 0   // diagnostics: 1 = draws without accumulation, 2 = accumulation without draws
+#endif
 #ifndef MCA_K3_STEAL
 #define MCA_K3_STEAL 512
 #endif
@@ -471,11 +474,18 @@ __global__ void __launch_bounds__(kK3BlockThreads, 1) k3_encode_sampled_bf16(K3A
         const uint64_t stream = ((uint64_t)(a.b_offset + b) * heads + h) * (uint64_t)n + (uint64_t)j;
         const float inv_r = has ? 1.0f / (float)r : 0.0f;
         auto gen = [&](int base, int& i0, int& i1, unsigned short& x0, unsigned short& x1) {
+#if MCA_K3_EXP == 2   // diagnostics: no draw (fixed rows), accumulate only
+            i0 = (base + 2 * l8 + j) % d_in;
+            i1 = (base + 2 * l8 + 1 + j) % d_in;
+            x0 = 0x3F80;
+            x1 = 0x3F80;
+#else
             uint64_t m0, m1;
             philox_pair53(a.seed, stream, a.layer, (uint32_t)(base / 2 + l8), &m0, &m1);
             sample_index2(s_thr, s_guide, m0, m1, i0, i1);   // draws past r are never accumulated
             x0 = reinterpret_cast<const unsigned short*>(xrow)[i0];
             x1 = reinterpret_cast<const unsigned short*>(xrow)[i1];
+#endif
         };
         auto pack = [&](int i, unsigned short xb) -> PackedPair {
             const float c = __uint_as_float((uint32_t)xb << 16) * s_invp[i] * inv_r;
@@ -486,6 +496,10 @@ __global__ void __launch_bounds__(kK3BlockThreads, 1) k3_encode_sampled_bf16(K3A
 #pragma unroll
         for (int u = 0; u < 8; ++u) acc[u] = 0.f;
         auto accumulate = [&](PackedPair p) {
+            if (MCA_K3_EXP == 1) {   // diagnostics: draws only, no accumulation
+                acc[0] += __uint_as_float(p);
+                return;
+            }
             uint4 w;
             uint32_t addr;
             asm("mad.lo.u32 %0, %1, 16, %2;" : "=r"(addr) : "r"(p & 0xFFFFu), "r"(wbase));   // LOP3 + one IMAD/LEA
