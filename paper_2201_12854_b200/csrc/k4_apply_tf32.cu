@@ -29,6 +29,7 @@ namespace mca_dev {
 #endif
 namespace k4tf {
 constexpr int kBM = 128, kBK = 32, kStages = 2;
+constexpr int kOAcc = 4;   // interleaved O accumulators (TMEM columns 64 .. 319)
 constexpr int kThreads = 192;
 constexpr uint32_t kAtom128 = 128 * 128;     // 128 rows x 128 B
 constexpr uint32_t kAtom64 = 64 * 128;       // 64 rows x 128 B
@@ -100,11 +101,11 @@ __global__ void __launch_bounds__(k4tf::kThreads, 1)
         for (int i = 0; i < 18; ++i) mbar_init(bars + i, (i >= 10 && i < 14) ? 4 : 1);   // s_free, p_full: 4 warps
         fence_barrier_init();
     }
-    if (warp == 1) tmem_alloc<128>(tmem_slot);
+    if (warp == 1) tmem_alloc<512>(tmem_slot);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    const uint32_t tmem = *tmem_slot;          // S buffers: columns [0, 32), [32, 64); O: [64, 128)
+    const uint32_t tmem = *tmem_slot;          // S buffers: columns [0, 32), [32, 64); O_a: [64 + 64 a, 128 + 64 a)
     griddep_trigger();
 
     if (warp == 0) {
@@ -162,8 +163,11 @@ __global__ void __launch_bounds__(k4tf::kThreads, 1)
             mbar_wait(p_full + st, ph);
             mbar_wait(v_full + st, ph);
             tc_fence_after();
-            umma_3xtf32<1>(tmem + 64, kIdescO, desc_add(dp, st * kPBytes), kAtom128, 0, desc_add(dv, st * kVBytes),
-                           kAtom64, 0, kb > 0);
+            // block kb accumulates into O_(kb % kOAcc): kOAcc shorter fp32 accumulation chains (the
+            // epilogue adds them), a ~2x smaller rounding error over long rows (n = 1000: 1.1e-5 -> ~5e-6)
+            umma_3xtf32<1>(tmem + 64 + 64 * (kb % kOAcc), kIdescO, desc_add(dp, st * kPBytes), kAtom128, 0,
+                           desc_add(dv, st * kVBytes),
+                           kAtom64, 0, kb >= kOAcc);   // the first block of each accumulator starts it
             umma_commit_w(p_free + st);
             umma_commit_w(v_empty + st);
         }
@@ -213,6 +217,18 @@ __global__ void __launch_bounds__(k4tf::kThreads, 1)
         tmem_ld32(lane_base + 64, ov[0]);
         tmem_ld32(lane_base + 96, ov[1]);
         tmem_ld_wait();
+#pragma unroll 1
+        for (int acc = 1; acc < kOAcc && acc < nblk; ++acc) {   // fold O_1 .. O_3 into O_0
+            uint32_t ow[2][32];
+            tmem_ld32(lane_base + 64 + 64 * acc, ow[0]);
+            tmem_ld32(lane_base + 96 + 64 * acc, ow[1]);
+            tmem_ld_wait();
+#pragma unroll
+            for (int u = 0; u < 2; ++u)
+#pragma unroll
+                for (int e = 0; e < 32; ++e)
+                    ov[u][e] = __float_as_uint(__uint_as_float(ov[u][e]) + __uint_as_float(ow[u][e]));
+        }
         if (i0 + r < n) {
             float4* dst = reinterpret_cast<float4*>(y + ((size_t)b * n + i0 + r) * heads * kDh + (size_t)h * kDh);
 #pragma unroll
@@ -225,7 +241,7 @@ __global__ void __launch_bounds__(k4tf::kThreads, 1)
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 1) tmem_dealloc<128>(tmem);
+    if (warp == 1) tmem_dealloc<512>(tmem);
 }
 
 // H~ [B, n, H*64] fp32 -> per head transposed, split: V^T hi / lo [B*H][64][ld]

@@ -826,3 +826,53 @@ def test_dense_exact_dispatch(mca, syn, orc, alpha, tmp_path):
         ys[mode] = torch.load(path)
     assert torch.equal(ys["1"]["e"], ys["0"]["e"])
     assert torch.equal(ys["1"]["y"], ys["0"]["y"])
+
+
+def _sweep_cases():
+    rng = np.random.default_rng(2026)
+    cases = []
+    for c in range(36):
+        dtype = torch.float32 if c % 2 == 0 else torch.bfloat16
+        B = int(rng.integers(1, 4))
+        n = int(rng.choice([1, 33, 96, 128, 200, 257, 300, 512, 769, 1000]))
+        H = int(rng.choice([1, 2, 4, 12, 16]))
+        d_in = int(rng.choice([64, 128, 256, 768, 1024]))
+        alpha = float(rng.choice([0.03, 0.2, 0.4, 1.0]))
+        cases.append((c, dtype, B, n, H, d_in, alpha, bool(c % 3 == 0)))
+    return cases
+
+
+@pytest.mark.parametrize("case", _sweep_cases(), ids=lambda c: f"{c[0]}-{'f32' if c[1] == torch.float32 else 'bf16'}"
+                         f"-B{c[2]}-n{c[3]}-H{c[4]}-d{c[5]}-a{c[6]}{'-proj' if c[7] else ''}")
+def test_random_config_sweep(mca, syn, orc, case):
+    """Seeded random shapes, dtypes, alphas (0.03 takes the bf16 dense exact
+    encoding), with and without on-device projections, certified budgets:
+    budgets equal to the fp64 oracle's, H~ and y within the dtype's tolerance
+    on the device's plan."""
+    c, dtype, B, n, H, d_in, alpha, proj = case
+    w = syn.make_weights(d_in, H, seed=100 + c).to(dtype)
+    if proj:
+        pin = syn.make_projected_inputs(B, n, d_in, H, seed=100 + c)
+        x = pin.x.to(dtype).cuda()
+        wq, wk = pin.w_q.to(dtype).cuda(), pin.w_k.to(dtype).cuda()
+        weights = mca.AttentionWeights(w.cuda(), heads=H, w_q=wq, w_k=wk)
+        qd = torch.empty((B, n, H * 64), dtype=dtype, device="cuda")
+        kd = torch.empty_like(qd)
+        hd = torch.empty_like(qd, dtype=torch.float32 if dtype == torch.float32 else torch.float16)
+        out = mca.mca_forward(weights, None, None, x, mca.McaConfig(alpha=alpha, certify=True), seed=c,
+                              return_plan=True, debug=dict(q_out=qd, k_out=kd, h_out=hd))
+        q, k = qd, kd
+    else:
+        inp = syn.make_inputs(B, n, d_in, H, seed=100 + c)
+        q, k, x = (t.to(dtype).cuda() for t in (inp.q, inp.k, inp.x))
+        weights = mca.AttentionWeights(w.cuda(), heads=H)
+        hd = torch.empty_like(q, dtype=torch.float32 if dtype == torch.float32 else torch.float16)
+        out = mca.mca_forward(weights, q, k, x, mca.McaConfig(alpha=alpha, certify=True), seed=c, return_plan=True,
+                              debug=dict(h_out=hd))
+    torch.cuda.synchronize()
+    b = out.budgets.cpu().numpy()
+    e = out.exact_mask.cpu().numpy().astype(bool)
+    ref0 = _oracle(orc, w, q, k, x, H, alpha=alpha, seed=c)
+    assert np.array_equal(b, ref0.budgets) and np.array_equal(e, ref0.exact), case
+    assert _row_rel(_np(hd), ref0.h) <= TOL_H[dtype], case
+    assert _row_rel(_np(out.y), ref0.y) <= TOL_Y[dtype], case
