@@ -25,6 +25,10 @@
 #include "mca_common.cuh"
 #include "tc_common.cuh"
 
+#ifndef MCA_K1_POLY
+#define MCA_K1_POLY 6   // (measured at C4: 0 / 6 / 10 / 14 -> 901 / 818 / 830 / 935 us) pairs of each 64-score chunk whose exp2 runs as an FMA-pipe polynomial (K1a)
+#endif
+
 namespace mca_dev {
 
 namespace k1tc {
@@ -206,10 +210,20 @@ __global__ void __launch_bounds__(k1tc::kThreads, kTf32 ? 1 : 2)
                     const float mn = fmaxf(m2, bmax * c2);
                     float acc0 = 0.f, acc1 = 0.f;
                     if (valid >= 64) {
+                        // MUFU-bound: MCA_K1_POLY of the 32 pairs take the FMA-pipe exp2 (same accuracy)
 #pragma unroll
                         for (int e = 0; e < 64; e += 2) {
-                            acc0 += ex2_approx(__fmaf_rn(__uint_as_float(sv[e >> 5][e & 31]), c2, -mn));
-                            acc1 += ex2_approx(__fmaf_rn(__uint_as_float(sv[(e + 1) >> 5][(e + 1) & 31]), c2, -mn));
+                            if (e < 2 * MCA_K1_POLY) {
+                                const float2 xv = __ffma2_rn(make_float2(__uint_as_float(sv[e >> 5][e & 31]),
+                                                                         __uint_as_float(sv[(e + 1) >> 5][(e + 1) & 31])),
+                                                             make_float2(c2, c2), make_float2(-mn, -mn));
+                                const float2 pv = ex2_poly5x2(xv);
+                                acc0 += pv.x;
+                                acc1 += pv.y;
+                            } else {
+                                acc0 += ex2_approx(__fmaf_rn(__uint_as_float(sv[e >> 5][e & 31]), c2, -mn));
+                                acc1 += ex2_approx(__fmaf_rn(__uint_as_float(sv[(e + 1) >> 5][(e + 1) & 31]), c2, -mn));
+                            }
                         }
                     } else {
 #pragma unroll

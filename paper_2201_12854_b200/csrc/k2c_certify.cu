@@ -106,43 +106,13 @@ struct K2cArgs {
     unsigned long long* cert_total;  // number of re-derived token-heads (FlopsReport.certified)
 };
 
-constexpr int kCertThreads = 128;    // 4 warps; 8 lanes (an octet) per query / key row
+constexpr int kCertThreads = 128;    // 4 warps; a thread pair per staged query / key row
 constexpr int kCertKeys = 32;        // flagged keys of one item processed together
 constexpr int kCertCands = 256;      // (key, query) candidates per batch
 constexpr int kCertRows = 8;         // candidate rows whose statistics one pass over the keys computes
 constexpr int kCertMaxN = 65536;     // bitmap of an item's rows (n <= 65535, mca_forward's limit)
 constexpr int kCertStage = 64;       // rows staged in shared memory per chunk (one L2 round trip each)
 
-// 8 elements [8 l8, 8 l8 + 8) of a 64-wide row, as floats
-template <class T>
-__device__ __forceinline__ void load_oct8(const T* __restrict__ row, int l8, float v[8]) {
-    load8(row + 8 * l8, v);
-}
-// octet sums: lanes 8o .. 8o + 7 hold partials of one dot product (the octet's
-// lanes always run together, so only they take part: octets of one warp may
-// leave a loop at different trip counts). Butterfly order makes the sum
-// identical in all 8 lanes.
-__device__ __forceinline__ unsigned oct_mask() { return 0xFFu << ((threadIdx.x & 31) & 24); }
-__device__ __forceinline__ float oct_sum(float v) {
-    const unsigned m = oct_mask();
-    v += __shfl_xor_sync(m, v, 1);
-    v += __shfl_xor_sync(m, v, 2);
-    v += __shfl_xor_sync(m, v, 4);
-    return v;
-}
-__device__ __forceinline__ double oct_sum(double v) {
-    const unsigned m = oct_mask();
-    v += __shfl_xor_sync(m, v, 1);
-    v += __shfl_xor_sync(m, v, 2);
-    v += __shfl_xor_sync(m, v, 4);
-    return v;
-}
-__device__ __forceinline__ double dot8_exact(const float a[8], const float* __restrict__ b) {
-    double acc = 0.0;
-#pragma unroll
-    for (int e = 0; e < 8; ++e) acc = fma((double)a[e], (double)b[e], acc);
-    return acc;   // a partial: exact products, the octet's sum in binary64 (exact for bf16 inputs)
-}
 // max of positive doubles through their bit patterns (monotone for x >= 0)
 __device__ __forceinline__ void atomic_max_pos(double* p, double v) {
     atomicMax(reinterpret_cast<unsigned long long*>(p), (unsigned long long)__double_as_longlong(v));
@@ -201,8 +171,7 @@ __global__ void __launch_bounds__(kCertThreads) k2c_certify(K2cArgs a) {
     const unsigned cnt = *(volatile const unsigned*)(a.cert.item_cnt + bh);
     if (cnt == 0) return;
     if (threadIdx.x == 0 && a.cert_total) atomicAdd(a.cert_total, (unsigned long long)cnt);
-    const int tid = threadIdx.x, lane = tid & 31, l8 = lane & 7, oct = tid >> 3;   // oct: 0..15
-    constexpr int kOcts = kCertThreads / 8;
+    const int tid = threadIdx.x, lane = tid & 31;
     const long long nflag = (long long)*(volatile const unsigned long long*)a.cert.count;
     const size_t HD = (size_t)a.heads * kDh;
     const int b = bh / a.heads, h = bh - b * a.heads;
@@ -286,17 +255,16 @@ __global__ void __launch_bounds__(kCertThreads) k2c_certify(K2cArgs a) {
                     }
                     const double v = a.scale * (double)(acc0 + acc1) - l;
                     if (v >= s_lcm[f] - (1e-3 + 1e-5 * (fabs(l) + fabs(s_lcm[f])))) {
-                        double t0 = 0.0, t1 = 0.0;
+                        // the same binary64 chain (e = 0 .. 63 in order) as the row pass, so a
+                        // candidate's exp(t - m~) / L is exactly 1 when it is the row's only term
+                        double t = 0.0;
 #pragma unroll
-                        for (int e = 0; e < kDh; e += 2) {
-                            t0 = fma((double)s_stage[ii][e], (double)s_k[f][e], t0);
-                            t1 = fma((double)s_stage[ii][e + 1], (double)s_k[f][e + 1], t1);
-                        }
+                        for (int e = 0; e < kDh; ++e) t = fma((double)s_stage[ii][e], (double)s_k[f][e], t);
                         const int slot = atomicAdd(&s_ncand, 1);
                         if (slot < kCertCands) {
                             s_cf[slot] = f;
                             s_ci[slot] = i;
-                            s_ct[slot] = a.scale * (t0 + t1);
+                            s_ct[slot] = a.scale * t;
                         }
                     }
                 }
@@ -378,13 +346,18 @@ __global__ void __launch_bounds__(kCertThreads) k2c_certify(K2cArgs a) {
         if (all_rows) {
             for (int f = 0; f < nk; ++f) {
                 double best = 0.0;
-                for (int i = oct; i < a.n; i += kOcts) {
-                    float qv[8];
-                    load_oct8(Qb + (size_t)i * HD, l8, qv);
-                    const double t = a.scale * oct_sum(dot8_exact(qv, &s_k[f][8 * l8]));
-                    best = fmax(best, exp(t - rowm[i]) / rowl[i]);
+                for (int i = tid; i < a.n; i += kCertThreads) {   // a query row per thread, the row pass's chain
+                    const T* qi = Qb + (size_t)i * HD;
+                    double t = 0.0;
+                    for (int e0 = 0; e0 < kDh; e0 += 8) {
+                        float qv[8];
+                        load8(qi + e0, qv);
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) t = fma((double)qv[e], (double)s_k[f][e0 + e], t);
+                    }
+                    best = fmax(best, exp(a.scale * t - rowm[i]) / rowl[i]);
                 }
-                if (l8 == 0) atomic_max_pos(&s_best[f], best);
+                atomic_max_pos(&s_best[f], best);
             }
         } else {
             for (int c = tid; c < nc; c += kCertThreads) {

@@ -297,6 +297,26 @@ __device__ __forceinline__ float2 ex2_poly2(float2 x) {
     return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
                        __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
 }
+// 2^x for two fp32 values on the FMA pipe with fp32-grade accuracy: the same
+// split as ex2_poly2 and a degree-5 minimax polynomial for 2^f (max relative
+// error 2.3e-7 after fp32 Horner rounding, like ex2.approx.f32); x >= -126
+// (clamped) keeps the exponent add normal. For MUFU-bound row-statistics loops.
+__device__ __forceinline__ float2 ex2_poly5x2(float2 x) {
+    x.x = fmaxf(x.x, -126.f);
+    x.y = fmaxf(x.y, -126.f);
+    const float2 magic = make_float2(12582912.f, 12582912.f);
+    const float2 t = __fadd2_rn(x, magic);
+    const float2 j = __fadd2_rn(t, make_float2(-12582912.f, -12582912.f));
+    const float2 f = __ffma2_rn(j, make_float2(-1.f, -1.f), x);
+    float2 p = __ffma2_rn(f, make_float2(0.0013276374666020274f, 0.0013276374666020274f),
+                          make_float2(0.00967551488429308f, 0.00967551488429308f));
+    p = __ffma2_rn(f, p, make_float2(0.05550713464617729f, 0.05550713464617729f));
+    p = __ffma2_rn(f, p, make_float2(0.24022120237350464f, 0.24022120237350464f));
+    p = __ffma2_rn(f, p, make_float2(0.6931469440460205f, 0.6931469440460205f));
+    p = __ffma2_rn(f, p, make_float2(1.0000001192092896f, 1.0000001192092896f));
+    return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+                       __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
+}
 __device__ __forceinline__ float ex2_approx(float x) {
     float r;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
