@@ -33,6 +33,8 @@
 // (tests/test_gpu_configs.py, tests/test_gpu_parity.py).
 #pragma once
 
+#include <type_traits>
+
 #include "mca_common.cuh"
 
 namespace mca_dev {
@@ -308,22 +310,30 @@ __global__ void __launch_bounds__(kCertThreads) k2c_certify(K2cArgs a) {
                 __syncthreads();
                 prefetch_rows(Kb, HD, c0 + kCertStage, a.n);
                 const int jj = tid % kCertStage, half = tid / kCertStage;
-                if (jj < cn) {   // a key row per thread pair, the candidate rows split between the two
-                    // rows half, half + 2, ...: each key element converted to binary64 once
-                    double t[kCertRows / 2];
+                // a key row per thread pair, the candidate rows split between the two (rows
+                // half, half + 2, ...); each key element converted to binary64 once; the
+                // per-thread row count kQ is the smallest of 1 / 2 / 4 that covers nr
+                auto rows_pass = [&](auto kq) {
+                    constexpr int kQ = decltype(kq)::value;
+                    double t[kQ];
 #pragma unroll
-                    for (int q = 0; q < kCertRows / 2; ++q) t[q] = 0.0;
+                    for (int q = 0; q < kQ; ++q) t[q] = 0.0;
 #pragma unroll 8
                     for (int e = 0; e < kDh; ++e) {
                         const double kd = (double)s_stage[jj][e];
 #pragma unroll
-                        for (int q = 0; q < kCertRows / 2; ++q) t[q] = fma(kd, s_qr[2 * q + half][e], t[q]);
+                        for (int q = 0; q < kQ; ++q) t[q] = fma(kd, s_qr[2 * q + half][e], t[q]);
                     }
 #pragma unroll
-                    for (int q = 0; q < kCertRows / 2; ++q) {   // compile-time indices into part[]
+                    for (int q = 0; q < kQ; ++q) {   // compile-time indices into part[]
                         if (half == 0 && 2 * q < nr) part[2 * q] += exp(a.scale * t[q] - s_mref[2 * q]);
                         if (half == 1 && 2 * q + 1 < nr) part[2 * q + 1] += exp(a.scale * t[q] - s_mref[2 * q + 1]);
                     }
+                };
+                if (jj < cn) {
+                    if (nr <= 2) rows_pass(std::integral_constant<int, 1>{});
+                    else if (nr <= 4) rows_pass(std::integral_constant<int, 2>{});
+                    else rows_pass(std::integral_constant<int, kCertRows / 2>{});
                 }
             }
 #pragma unroll
