@@ -31,6 +31,13 @@
 #include "mca_common.cuh"
 #include "tc_common.cuh"
 
+#ifndef MCA_K4_STAGES
+#define MCA_K4_STAGES 4
+#endif
+#ifndef MCA_K4_EXP
+#define MCA_K4_EXP 0   // diagnostics: 1 = no exponentials in the softmax warps, 2 = no MMAs
+#endif
+
 namespace mca_dev {
 
 #ifndef MCA_K4_QAHEAD
@@ -44,7 +51,7 @@ namespace mca_dev {
 __device__ long long g_k4_prof[MCA_K4_PROF ? 64 : 1];
 
 namespace k4tc {
-constexpr int kBM = 128, kBK = 64, kStages = 4;      // separate K and H~ rings of kStages each
+constexpr int kBM = 128, kBK = 64, kStages = MCA_K4_STAGES;   // separate K and H~ rings of kStages each
 constexpr int kConsumers = 8;                        // 2 warps per TMEM lane quadrant
 constexpr int kThreads = 64 + kConsumers * 32;
 constexpr uint32_t kTileBytes = kBK * kDh * 2;       // 8 KB: one 64-key K or H~ block
@@ -159,7 +166,8 @@ __global__ void __launch_bounds__(k4tc::kThreads, 2)
             const uint64_t dk = desc_add(dk0, s * kTileBytes);
 #pragma unroll
             for (int kk = 0; kk < kDh / 16; ++kk)
-                umma_f16_ts_w(tmem + sb * kBK, tmem + kQCol + kk * 8, desc_add(dk, kk * 32), kIdescS, kk > 0 ? 1u : 0u);
+                if (MCA_K4_EXP != 2)   // diagnostics: 2 = no MMAs
+                    umma_f16_ts_w(tmem + sb * kBK, tmem + kQCol + kk * 8, desc_add(dk, kk * 32), kIdescS, kk > 0 ? 1u : 0u);
             umma_commit_w(s_full + sb);
             umma_commit_w(k_empty + s);
         };
@@ -171,6 +179,7 @@ __global__ void __launch_bounds__(k4tc::kThreads, 2)
             const uint64_t dh = desc_add(dh0, s * kTileBytes);
 #pragma unroll
             for (int kk = 0; kk < kBK / 16; ++kk)
+                if (MCA_K4_EXP != 2)
                 umma_f16_ts_w(tmem + kOCol, tmem + k4_p_col(sb, kk), desc_add(dh, kk * 2048), kIdescO,
                               (!first || kk > 0) ? 1u : 0u);
             umma_commit_w(h_empty + s);
@@ -257,7 +266,10 @@ __global__ void __launch_bounds__(k4tc::kThreads, 2)
                 // keys past n get 2^-inf = 0
                 uint32_t pk[16];
                 const int valid = n - (kb * kBK + 32 * half);
-                if (valid >= 32) {
+                if (MCA_K4_EXP == 1) {   // diagnostics: no exponentials (P = S bits)
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) pk[e] = sv[2 * e] ^ sv[2 * e + 1];
+                } else if (valid >= 32) {
                     // the MUFU is this loop's bound: kPolyPairs of the 16 pairs take the FMA-pipe exp2
 #pragma unroll
                     for (int e = 0; e < 16; ++e) {
