@@ -36,6 +36,7 @@
 #include "k4_apply_tc.cu"
 #include "k4_apply_tf32.cu"
 #include "kp_project_tc.cu"
+#include "kp_project_pair.cu"
 #include "ka_given_attn.cu"
 #include "ka_aggregate_tc.cu"
 #include "mca_diag.cuh"
@@ -416,6 +417,15 @@ bool dense_exact_enabled() {
 }
 long dense_exact_min(long token_heads) { return std::max(1L, (long)(kDenseExactFrac * (double)token_heads)); }
 
+// MCA_KP_PAIR=0: the single-CTA projection GEMM instead of the CTA-pair one
+bool kp_pair_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("MCA_KP_PAIR");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 bool use_k3t(const mca_weights* w) {
     return w->wdt == MCA_BF16 && w->wprime && !force_simt() && tile_k3_requested() && w->d_in % 8 == 0 &&
            k3t::layout(w->d_in).bytes <= 227u * 1024u;
@@ -674,6 +684,32 @@ mca_status launch_projection(mca_weights* w, const void* x, long tokens, int seg
     pa.f16_mask = mask;
     const long tiles = ((tokens + kp::kBM - 1) / kp::kBM) * ((long)nseg * HD / BN);
     const dim3 grid((unsigned)std::min<long>(tiles, sm_count()));
+    if (!tf32 && BN == 256 && kp_pair_enabled()) {   // CTA pairs: 256 x 256 tiles (kp_project_pair.cu)
+        const long ptiles = ((tokens + 255) / 256) * ((long)nseg * HD / 256);
+        const unsigned pairs = (unsigned)std::max<long>(1, std::min<long>(ptiles, sm_count() / 2));
+        CUtensorMap twp;   // W^T with 128-row boxes: each CTA of the pair loads half of the tile's N
+        if (!make_tmap_bf16(&twp, static_cast<const __nv_bfloat16*>(w->wqkv_t) + wofs, (uint64_t)w->d_in,
+                            (uint64_t)nseg * HD, 1, 128))
+            return fail(MCA_ERR_CUDA, "cuTensorMapEncodeTiled failed for W^T (pair)");
+        MCA_CUDA_TRY(ensure_smem(kp_project_pair, kp2::kSmemBytes));
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(2 * pairs);
+        cfg.blockDim = dim3(kp2::kThreads);
+        cfg.dynamicSmemBytes = kp2::kSmemBytes;
+        cfg.stream = stream;
+        cudaLaunchAttribute at[2];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 2;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[1].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 2;
+        MCA_CUDA_TRY(cudaLaunchKernelEx(&cfg, kp_project_pair, tx, twp, to[0], to[1], to[2], pa));
+        MCA_LAUNCH_CHECK("kp_project_pair");
+        return MCA_OK;
+    }
     auto go = [&](auto kern, uint32_t smem) -> mca_status {
         MCA_CUDA_TRY(ensure_smem(kern, smem));
         MCA_CUDA_TRY(launch_pdl(kern, grid, dim3(kp::kThreads), smem, stream, tx, tw, tx2, tw2, to[0], to[1], to[2], pa));
