@@ -7,8 +7,9 @@
 // memory, and the leader (r = 0) issues M = 256, N = 256 MMAs that read both
 // CTAs' operands and write 128 rows x 256 columns of fp32 into each CTA's TMEM.
 // Per SM and K step that is 32 KB of operands for 512 MMA cycles, against 48 KB
-// in the single-CTA 128 x 256 tile: the single-CTA kernel is bound by what one
-// SM can pull from L2, not by its tensor core (tensor pipe ~60% active).
+// in the single-CTA 128 x 256 tile (tensor pipe ~60% active there). Measured at
+// C2: 60 vs 64 us; 3 / 4 / 6 stages 69.5 / 59.8 / 62.0 us
+// (scripts/kp2_stage_exp.sh).
 //
 //   warp 0      TMA producer of its CTA; every load completes on the LEADER's
 //               full barrier (the leader expects both CTAs' bytes)
@@ -21,10 +22,14 @@
 #include "mca_common.cuh"
 #include "tc_common.cuh"
 
+#ifndef MCA_KP2_STAGES
+#define MCA_KP2_STAGES 4
+#endif
+
 namespace mca_dev {
 
 namespace kp2 {
-constexpr int kBK = 64, kBN = 256, kStages = 4, kOutBufs = 2;
+constexpr int kBK = 64, kBN = 256, kStages = MCA_KP2_STAGES, kOutBufs = 2;
 constexpr int kThreads = 192;
 constexpr uint32_t kABytes = 128 * 128;                       // 16 KB: the CTA's 128 x rows x 64 K
 constexpr uint32_t kBBytes = 128 * 128;                       // 16 KB: the CTA's 128 W^T rows x 64 K
