@@ -29,25 +29,39 @@
 namespace mca_dev {
 
 namespace kp2 {
-constexpr int kBK = 64, kBN = 256, kStages = MCA_KP2_STAGES, kOutBufs = 2;
-constexpr int kThreads = 192;
-constexpr uint32_t kABytes = 128 * 128;                       // 16 KB: the CTA's 128 x rows x 64 K
-constexpr uint32_t kBBytes = 128 * 128;                       // 16 KB: the CTA's 128 W^T rows x 64 K
-constexpr uint32_t kStageBytes = kABytes + kBBytes;
-constexpr uint32_t kSmemOut = kStages * kStageBytes;          // 128 KB
-constexpr uint32_t kOutBytes = 128 * 128;                     // [128 x 64] bf16 staging tile
-constexpr uint32_t kSmemBar = kSmemOut + kOutBufs * kOutBytes;
-constexpr uint32_t kSmemBytes = kSmemBar + 256 + 1024;
-constexpr uint32_t kIdesc = mca_tc::idesc_f16(1, 0, 256, kBN);   // bf16, M = 256 (the pair), N = 256
+// kTf32: 3xTF32 (hi.lo + lo.hi + hi.hi; x and W^T raw as their hi parts, their
+// lo parts from their own maps), 32 fp32 per K step, fp32 outputs staged 32
+// columns at a time, and (KpArgs::lo_tma) the q / k lo parts out through tm_o2.
+template <bool kTf32>
+struct Cfg {
+    static constexpr int kBK = kTf32 ? 32 : 64, kBN = 256;
+    static constexpr int kParts = kTf32 ? 2 : 1;
+    static constexpr int kStages = kTf32 ? 3 : MCA_KP2_STAGES, kOutBufs = 2;
+    static constexpr int kThreads = 192;
+    static constexpr uint32_t kPart = 128 * 128;                  // 16 KB: 128 rows x 128 B
+    static constexpr uint32_t kABytes = kParts * kPart;           // the CTA's 128 x rows
+    static constexpr uint32_t kBBytes = kParts * kPart;           // the CTA's 128 W^T rows
+    static constexpr uint32_t kStageBytes = kABytes + kBBytes;
+    static constexpr uint32_t kSmemOut = kStages * kStageBytes;
+    static constexpr uint32_t kOutBytes = 128 * 128;              // [128 x 128 B] staging tile
+    static constexpr int kOutCols = kTf32 ? 32 : 64;
+    static constexpr uint32_t kSmemBar = kSmemOut + kOutBufs * kOutBytes;
+    static constexpr uint32_t kSmemBytes = kSmemBar + 256 + 1024;
+    static constexpr uint32_t kIdesc = kTf32 ? mca_tc::idesc_tf32(256, kBN) : mca_tc::idesc_f16(1, 0, 256, kBN);
+};
 }  // namespace kp2
 
-__global__ void __launch_bounds__(kp2::kThreads, 1)
+template <bool kTf32>
+__global__ void __launch_bounds__(192, 1)
     kp_project_pair(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_w,
+                    const __grid_constant__ CUtensorMap tm_x2, const __grid_constant__ CUtensorMap tm_w2,
                     const __grid_constant__ CUtensorMap tm_o0, const __grid_constant__ CUtensorMap tm_o1,
                     const __grid_constant__ CUtensorMap tm_o2, KpArgs a) {
     using namespace mca_tc;
-    using namespace kp2;
-    constexpr int S = kStages;
+    using C = kp2::Cfg<kTf32>;
+    constexpr int S = C::kStages, kBK = C::kBK, kBN = C::kBN, kOutBufs = C::kOutBufs;
+    constexpr uint32_t kStageBytes = C::kStageBytes, kABytes = C::kABytes, kSmemOut = C::kSmemOut,
+                       kOutBytes = C::kOutBytes, kSmemBar = C::kSmemBar, kIdesc = C::kIdesc;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kSmemBar);
@@ -105,6 +119,10 @@ __global__ void __launch_bounds__(kp2::kThreads, 1)
                     if (rank == 0) mbar_expect_tx(full + s, 2 * kStageBytes);
                     tma_load_3d_pair(st, &tm_x, full + s, kb * kBK, m0 + 128 * (int)rank, 0);
                     tma_load_3d_pair(st + kABytes, &tm_w, full + s, kb * kBK, n0 + 128 * (int)rank, 0);
+                    if constexpr (kTf32) {
+                        tma_load_3d_pair(st + C::kPart, &tm_x2, full + s, kb * kBK, m0 + 128 * (int)rank, 0);
+                        tma_load_3d_pair(st + kABytes + C::kPart, &tm_w2, full + s, kb * kBK, n0 + 128 * (int)rank, 0);
+                    }
                     if (++s == S) {
                         s = 0;
                         ph ^= 1;
@@ -128,9 +146,20 @@ __global__ void __launch_bounds__(kp2::kThreads, 1)
                     tc_fence_after();
                     const uint64_t da = desc_add(d0, s * kStageBytes);
                     const uint64_t db = desc_add(da, kABytes);
+                    if constexpr (kTf32) {   // hi.lo + lo.hi + hi.hi, K = 8 fp32 per instruction
 #pragma unroll
-                    for (int kk = 0; kk < 4; ++kk)
-                        umma_f16_pair_w(d, desc_add(da, kk * 32), desc_add(db, kk * 32), kIdesc, (kb | kk) != 0);
+                        for (int pr = 0; pr < 3; ++pr) {
+                            const uint32_t ap = pr == 1 ? C::kPart : 0u, bp = pr == 0 ? C::kPart : 0u;
+#pragma unroll
+                            for (int kk = 0; kk < 4; ++kk)
+                                umma_tf32_pair_w(d, desc_add(da, ap + kk * 32), desc_add(db, bp + kk * 32), kIdesc,
+                                                 (kb | pr | kk) != 0);
+                        }
+                    } else {
+#pragma unroll
+                        for (int kk = 0; kk < 4; ++kk)
+                            umma_f16_pair_w(d, desc_add(da, kk * 32), desc_add(db, kk * 32), kIdesc, (kb | kk) != 0);
+                    }
                     umma_commit_pair_w(empty + s);   // the stage is free in both CTAs
                     if (++s == S) {
                         s = 0;
@@ -162,10 +191,44 @@ __global__ void __launch_bounds__(kp2::kThreads, 1)
             mbar_wait(acc_full + acc, aph);
             tc_fence_after();
 #pragma unroll 1
-            for (int c = 0; c < kBN; c += 64) {
-                if (et == 0) bulk_wait_read<kOutBufs - 1>();
+            for (int c = 0; c < kBN; c += C::kOutCols) {
+                if (et == 0) {   // the store that used this buffer has read it (both when lo goes out too)
+                    if (kTf32 && a.lo_tma) bulk_wait_read<0>();
+                    else bulk_wait_read<kOutBufs - 1>();
+                }
                 named_bar_sync(1, 128);
                 uint8_t* st = stage_out + ob * kOutBytes;
+                if constexpr (kTf32) {   // 32 fp32 columns: one 128-byte row per thread (+ its lo parts)
+                    uint32_t v[32];
+                    tmem_ld32(lane_base + (uint32_t)(acc * kBN + c), v);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int g = 0; g < 8; ++g)
+                        *reinterpret_cast<uint4*>(st + sw128_offset(r, (uint32_t)g * 16)) =
+                            make_uint4(v[4 * g], v[4 * g + 1], v[4 * g + 2], v[4 * g + 3]);
+                    if (a.lo_tma) {
+                        uint8_t* sl = stage_out + (ob ^ 1) * kOutBytes;
+#pragma unroll
+                        for (int g = 0; g < 8; ++g) {
+                            uint32_t e[4];
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) {
+                                const uint32_t b = v[4 * g + u];
+                                e[u] = __float_as_uint(__uint_as_float(b) - __uint_as_float(b & 0xFFFFE000u));
+                            }
+                            *reinterpret_cast<uint4*>(sl + sw128_offset(r, (uint32_t)g * 16)) = make_uint4(e[0], e[1], e[2], e[3]);
+                        }
+                    }
+                    fence_proxy_async_smem();
+                    named_bar_sync(1, 128);
+                    if (et == 0) {
+                        tma_store_3d(om, st, oc + c, m0, 0);
+                        if (a.lo_tma) tma_store_3d(&tm_o2, stage_out + (ob ^ 1) * kOutBytes, oc + c, m0, seg);
+                        bulk_commit();
+                    }
+                    if (!a.lo_tma && ++ob == kOutBufs) ob = 0;
+                    continue;
+                }
                 uint32_t v[2][32];
                 tmem_ld32(lane_base + (uint32_t)(acc * kBN + c), v[0]);
                 tmem_ld32(lane_base + (uint32_t)(acc * kBN + c + 32), v[1]);

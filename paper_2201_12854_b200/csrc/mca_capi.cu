@@ -684,18 +684,18 @@ mca_status launch_projection(mca_weights* w, const void* x, long tokens, int seg
     pa.f16_mask = mask;
     const long tiles = ((tokens + kp::kBM - 1) / kp::kBM) * ((long)nseg * HD / BN);
     const dim3 grid((unsigned)std::min<long>(tiles, sm_count()));
-    if (!tf32 && BN == 256 && kp_pair_enabled()) {   // CTA pairs: 256 x 256 tiles (kp_project_pair.cu)
+    if (HD % 256 == 0 && kp_pair_enabled()) {   // a 256-column pair tile never straddles two segments
+        // CTA pairs: 256 x 256 tiles (kp_project_pair.cu); W^T with 128-row boxes
+        // (each CTA of the pair loads half of the tile's N)
         const long ptiles = ((tokens + 255) / 256) * ((long)nseg * HD / 256);
         const unsigned pairs = (unsigned)std::max<long>(1, std::min<long>(ptiles, sm_count() / 2));
-        CUtensorMap twp;   // W^T with 128-row boxes: each CTA of the pair loads half of the tile's N
-        if (!make_tmap_bf16(&twp, static_cast<const __nv_bfloat16*>(w->wqkv_t) + wofs, (uint64_t)w->d_in,
-                            (uint64_t)nseg * HD, 1, 128))
+        CUtensorMap twp = tw;
+        if (!tf32 && !make_tmap_bf16(&twp, static_cast<const __nv_bfloat16*>(w->wqkv_t) + wofs, (uint64_t)w->d_in,
+                                     (uint64_t)nseg * HD, 1, 128))
             return fail(MCA_ERR_CUDA, "cuTensorMapEncodeTiled failed for W^T (pair)");
-        MCA_CUDA_TRY(ensure_smem(kp_project_pair, kp2::kSmemBytes));
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(2 * pairs);
-        cfg.blockDim = dim3(kp2::kThreads);
-        cfg.dynamicSmemBytes = kp2::kSmemBytes;
+        cfg.blockDim = dim3(192);
         cfg.stream = stream;
         cudaLaunchAttribute at[2];
         at[0].id = cudaLaunchAttributeClusterDimension;
@@ -706,7 +706,15 @@ mca_status launch_projection(mca_weights* w, const void* x, long tokens, int seg
         at[1].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = at;
         cfg.numAttrs = 2;
-        MCA_CUDA_TRY(cudaLaunchKernelEx(&cfg, kp_project_pair, tx, twp, to[0], to[1], to[2], pa));
+        if (tf32) {
+            cfg.dynamicSmemBytes = kp2::Cfg<true>::kSmemBytes;
+            MCA_CUDA_TRY(ensure_smem(kp_project_pair<true>, kp2::Cfg<true>::kSmemBytes));
+            MCA_CUDA_TRY(cudaLaunchKernelEx(&cfg, kp_project_pair<true>, tx, twp, tx2, tw2, to[0], to[1], to[2], pa));
+        } else {
+            cfg.dynamicSmemBytes = kp2::Cfg<false>::kSmemBytes;
+            MCA_CUDA_TRY(ensure_smem(kp_project_pair<false>, kp2::Cfg<false>::kSmemBytes));
+            MCA_CUDA_TRY(cudaLaunchKernelEx(&cfg, kp_project_pair<false>, tx, twp, tx2, tw2, to[0], to[1], to[2], pa));
+        }
         MCA_LAUNCH_CHECK("kp_project_pair");
         return MCA_OK;
     }
