@@ -1,4 +1,6 @@
 # K3 bf16 micro-variants A/B on one box: 0 = product, A = __frcp_rn(r), B = count samples per token,
+# (The MCA_K3_FRCP / MCA_K3_CNT_TOKEN switches were removed after this measurement: no gain,
+# DESIGN.md §5. MCA_K3_STEAL remains.)
 # C / D = head-stealing threshold 256 / 1024 list entries (product 512)
 cp paper_2201_12854_b200/lib/libmca_b200.so /tmp/lib30.so
 for rep in 1 2; do for v in 0 A B C D; do
