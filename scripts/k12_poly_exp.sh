@@ -1,4 +1,6 @@
 # K12 FMA-pipe exp2 share: p0 = product (MUFU only), pN = N of 16 pairs per chunk on the polynomial
+# (The MCA_K12_POLY switch and ex2_poly5x2 in k12 were removed after this measurement: slower at
+# every share, DESIGN.md §4. ex2_poly5x2 lives on in K1a, MCA_K1_POLY.)
 cp paper_2201_12854_b200/lib/libmca_b200.so /tmp/libp0.so
 for v in 0 4 6 8; do
   cp /tmp/libp0.so paper_2201_12854_b200/lib/libmca_b200.so
