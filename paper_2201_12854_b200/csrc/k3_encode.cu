@@ -408,7 +408,6 @@ __global__ void __launch_bounds__(kK3BlockThreads, 1) k3_encode_sampled_bf16(K3A
     PackedPair* s_pairs = reinterpret_cast<PackedPair*>(smem + ((((size_t)d_in * 12 + kGuide * 2) + 127) & ~(size_t)127));
     __nv_bfloat16* s_w = reinterpret_cast<__nv_bfloat16*>(s_pairs + kK3Warps * 4 * 16);
     PackedPair* my_pairs = s_pairs + (warp * 4 + oct) * 16;
-    griddep_trigger();
 
     const size_t HD = (size_t)heads * kDh;
     const __nv_bfloat16* wv = reinterpret_cast<const __nv_bfloat16*>(a.wv);
@@ -456,6 +455,7 @@ __global__ void __launch_bounds__(kK3BlockThreads, 1) k3_encode_sampled_bf16(K3A
     }
     __syncthreads();
     griddep_wait();      // W_h and the tables above are weights; the work lists come from the scatter
+    griddep_trigger();   // only now: k3b_exact_tc skips its own wait and relies on the scan being done
     if (MCA_K3S_PROF && threadIdx.x == 0 && cta < 1024) g_k3s_cta[cta][1] = gt_now();
     const int col0 = 8 * l8;
     const int nsamp = a.counts[2 * h];

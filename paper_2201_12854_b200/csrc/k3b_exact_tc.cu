@@ -53,14 +53,24 @@ __global__ void __launch_bounds__(k3btc::kThreads, 2) k3b_exact_tc(K3Args a) {
     const bool prof = MCA_K3B_PROF && blockIdx.x == 0 && blockIdx.y == 0;
     if (prof && threadIdx.x == 0) g_k3b_prof[0] = clock64();
     griddep_trigger();
-    griddep_wait();      // the exact lists (and K3's H~ writes: both encoders write disjoint rows)
+    // No dependency wait up front: the exact lists come from the scan, which completed
+    // before the sampled encoder K3 (the PDL predecessor) let this grid launch (K3
+    // triggers only after its own wait), and the two encoders write disjoint rows of
+    // H~, so these CTAs run in K3's tail. Every CTA waits for K3 before it exits, so
+    // K4 (which waits for this grid) sees all of H~.
     if (prof && threadIdx.x == 0) g_k3b_prof[1] = clock64();
     const int ne = a.counts[2 * h + 1];
-    if ((int)blockIdx.x * kBM >= ne) return;           // uniform early exit, before any barrier / TMEM use
+    if ((int)blockIdx.x * kBM >= ne) {   // uniform early exit, before any barrier / TMEM use
+        griddep_wait();
+        return;
+    }
     if (a.dense_min > 0) {   // the dense X W_V GEMM encoded every exact token-head (kp_project_tc's gate)
         long ex = 0;
         for (int hh = 0; hh < a.heads; ++hh) ex += a.counts[2 * hh + 1];
-        if (ex >= a.dense_min) return;
+        if (ex >= a.dense_min) {
+            griddep_wait();
+            return;
+        }
     }
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -209,6 +219,7 @@ __global__ void __launch_bounds__(k3btc::kThreads, 2) k3b_exact_tc(K3Args a) {
     __syncthreads();
     if (prof && threadIdx.x == 0) g_k3b_prof[41] = clock64();
     if (warp == 4) tmem_dealloc<64>(tmem);
+    griddep_wait();   // K3 has finished too: K4 may read every row of H~
 }
 
 }  // namespace mca_dev
