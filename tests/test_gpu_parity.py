@@ -876,3 +876,43 @@ def test_random_config_sweep(mca, syn, orc, case):
     assert np.array_equal(b, ref0.budgets) and np.array_equal(e, ref0.exact), case
     assert _row_rel(_np(hd), ref0.h) <= TOL_H[dtype], case
     assert _row_rel(_np(out.y), ref0.y) <= TOL_Y[dtype], case
+
+
+_KP_SNIPPET = r"""
+import sys, torch
+sys.path.insert(0, {root!r})
+import paper_2201_12854_b200 as mca
+from paper_2201_12854_b200.synthetic import make_weights, make_projected_inputs
+out = {{}}
+for dt, B, n, H, d_in in ((torch.bfloat16, 2, 300, 12, 768), (torch.float32, 1, 257, 4, 256), (torch.bfloat16, 1, 77, 16, 1024)):
+    w = make_weights(d_in, H, seed=9).to(dt).cuda()
+    pin = make_projected_inputs(B, n, d_in, H, seed=9)
+    wts = mca.AttentionWeights(w, heads=H, w_q=pin.w_q.to(dt).cuda(), w_k=pin.w_k.to(dt).cuda())
+    q = torch.empty((B, n, H * 64), dtype=dt, device="cuda"); k = torch.empty_like(q)
+    r = mca.mca_forward(wts, None, None, pin.x.to(dt).cuda(), mca.McaConfig(alpha=0.4), seed=2, debug=dict(q_out=q, k_out=k))
+    yr = mca.regular_forward(wts, None, None, pin.x.to(dt).cuda()) if dt == torch.bfloat16 else r.y
+    out[str(dt) + str(d_in)] = (q.cpu(), k.cpu(), r.y.cpu(), yr.cpu())
+torch.save(out, {path!r})
+"""
+
+
+def test_projection_pair_vs_single_cta(tmp_path):
+    """The CTA-pair projection GEMM (cta_group::2, default) and the single-CTA
+    one (MCA_KP_PAIR=0, read once per process): q / k agree to fp32 summation
+    order (bf16 outputs: within one rounding; fp32: 1e-6), including the
+    exact layer's three-segment GEMM."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for mode in ("1", "0"):
+        path = str(tmp_path / f"kp{mode}.pt")
+        r = subprocess.run([sys.executable, "-c", _KP_SNIPPET.format(root=root, path=path)],
+                           env=dict(os.environ, MCA_KP_PAIR=mode), capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        res[mode] = torch.load(path)
+    for key in res["1"]:
+        for a, b in zip(res["1"][key], res["0"][key]):
+            a, b = a.double(), b.double()
+            rel = float((a - b).norm() / b.norm().clamp_min(1e-30))
+            assert rel <= (1e-6 if "float32" in key else 4e-3), (key, rel)
