@@ -916,3 +916,23 @@ def test_projection_pair_vs_single_cta(tmp_path):
             a, b = a.double(), b.double()
             rel = float((a - b).norm() / b.norm().clamp_min(1e-30))
             assert rel <= (1e-6 if "float32" in key else 4e-3), (key, rel)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_host_pipeline_x_only(mca, syn, dtype):
+    """HostPipeline with the projections on the device (only x crosses PCIe;
+    fp32: 3xTF32 CTA-pair projection, certified budgets) reproduces the
+    whole-batch forward bitwise, chunk by chunk."""
+    H, n, d_in, B = 12, 128, 768, 4
+    w = syn.make_weights(d_in, H, seed=31).to(dtype)
+    pin = syn.make_projected_inputs(B, n, d_in, H, seed=31)
+    weights = mca.AttentionWeights(w.cuda(), heads=H, w_q=pin.w_q.to(dtype).cuda(), w_k=pin.w_k.to(dtype).cuda())
+    x = pin.x.to(dtype)
+    cfg = mca.McaConfig(alpha=0.4)
+    ref = mca.mca_forward(weights, None, None, x.cuda(), cfg, seed=8, b_offset=1).y.cpu()
+    hx = x.pin_memory()
+    hy = torch.empty((B, n, H * 64), dtype=dtype).pin_memory()
+    pipe = mca.HostPipeline([weights], n, chunk=2, dtype=dtype)
+    pipe.forward(None, None, hx, hy, cfg, seed=8, b_offset=1)
+    torch.cuda.synchronize()
+    assert torch.equal(hy, ref)
