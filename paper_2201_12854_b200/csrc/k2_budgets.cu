@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(256) k2_budgets(K2Args a) {
                 const int i = (int)(0xFFFFFFFFu - (uint32_t)(key & 0xFFFFFFFFull));
                 double s;
                 if (a.colscore) {
-                    s = (double)a.colscore[t];   // tensor-core score: exact bf16 products, fp32 sum
+                    s = (double)a.colscore[t];   // tensor-core score (bf16: exact products, fp32 sum; fp32: 3xTF32)
                 } else {
                     const int b = (int)(bh / a.heads), h = (int)(bh - (long)b * a.heads);
                     const size_t HD = (size_t)a.heads * kDh;

@@ -1261,7 +1261,9 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
         a.row_l = w->row_l;
         a.q = q;
         a.k = k;
-        a.colscore = (dt == MCA_BF16 && !force_simt() && n <= k1tc::kMaxN) ? w->colscore : nullptr;
+        // K1b's winning score: exact bf16 products (bf16), 3xTF32 (fp32: measured
+        // |dcm/cm| <= 1.6e-7 M against the binary64 oracle, tau_tf32 = 3e-6 M)
+        a.colscore = ((dt == MCA_BF16 && !force_simt() && n <= k1tc::kMaxN) || tf32_scores) ? w->colscore : nullptr;
         a.scale = scale;
         a.count = th;
         a.row_len = n;
@@ -1282,7 +1284,7 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
         a.cert = cert;
         if (!fused12) {
             if (a.cmax_in) k2_budgets<kGivenCmax, float><<<grid, 256, 0, stream>>>(a);
-            else if (tf32_scores) k2_budgets<kKeyArgmax, float><<<grid, 256, 0, stream>>>(a);   // fp64 winner re-evaluation
+            else if (tf32_scores) k2_budgets<kKeyArgmax, float><<<grid, 256, 0, stream>>>(a);   // winner score from K1b
             else if (dt == MCA_F32) k2_budgets<kKeyValue, float><<<grid, 256, 0, stream>>>(a);
             else k2_budgets<kKeyArgmax, __nv_bfloat16><<<grid, 256, 0, stream>>>(a);
             MCA_LAUNCH_CHECK("k2_budgets");
