@@ -79,8 +79,8 @@ __host__ __device__ inline Layout layout(int nt, int d) {
     L.lse2 = 2 * nt * kTileBytes;                              // [2][128] f32: -lse2 of a query tile (qt parity)
     L.comb = L.lse2 + 2 * kT * 4;                              // A partials [2][4][128] x 8 B; B maxima [kMaxTiles][2][128] x 4 B
     L.hist = L.comb + 2 * 4 * kT * 8 + 2 * kMaxTiles * kT * 4; // [d + 1] u32 budget histogram
-    L.lmax = L.hist + (uint32_t)(d + 1) * 4;                   // [4] u32: per-warp max |lse| of an item
-    L.bars = (L.lmax + 16 + 15) & ~15u;
+    L.lmax = L.hist + (uint32_t)(d + 1) * 4;                   // [4] u32: per-warp max |lse| of an item; [4] last-unit flag
+    L.bars = (L.lmax + 32 + 15) & ~15u;
     L.bytes = L.bars + 512 + 1024;                             // barriers; + alignment slack
     return L;
 }
@@ -102,7 +102,35 @@ struct K12Args {
     unsigned long long* counters;      // [0] approx cost, [1] sampled draws, [2] exact token-heads
     unsigned int* hist;                // [H, d + 1] (nullable)
     CertSink cert;                     // Eq. 9 values at an integer boundary: deferred to k2c_certify
+    // Work units: items [0, items - tail_items) whole, then each of the last
+    // tail_items items split into tail_parts query-tile ranges (the grid's last
+    // wave). A split item's units merge their per-key maxima and max |lse| into
+    // tail[slot] = [n] ordered-u32 maxima | lse max | unit counter; the last unit
+    // to finish evaluates Eq. 9 and resets the slot to zero for the next launch.
+    int units, tail_items, tail_parts;
+    unsigned* tail;                    // [tail_items][n + 2], zero between launches
 };
+
+namespace k12 {
+struct Unit {
+    int it, q0, q1, slot;   // item, query tiles [q0, q1), split slot (-1: whole item)
+};
+__device__ __forceinline__ Unit unit_of(const K12Args& a, int k, int nt) {
+    const int nfull = a.items - a.tail_items;
+    if (k < nfull) return {k, 0, nt, -1};
+    k -= nfull;
+    const int ti = k / a.tail_parts, p = k - ti * a.tail_parts;
+    return {nfull + ti, p * nt / a.tail_parts, (p + 1) * nt / a.tail_parts, ti};
+}
+// float <-> u32 keys whose unsigned order is the float order (0 is below every float)
+__device__ __forceinline__ unsigned f32_key(float v) {
+    const unsigned b = __float_as_uint(v);
+    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float key_f32(unsigned k) {
+    return __uint_as_float((k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k);
+}
+}  // namespace k12
 
 // Persistent: one CTA per SM walks the items (b, h) = blockIdx.x, + gridDim.x, ...
 // Every stream (TMA, the two MMA issuers, both consumer groups) runs ahead into
@@ -137,7 +165,6 @@ __global__ void __maxnreg__(72)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(comb_empty + 2);
 
     const int warp = __shfl_sync(0xffffffffu, (int)threadIdx.x >> 5, 0), lane = threadIdx.x & 31;   // uniform: see k4_apply_tf32
-    const int nblk = nt * nt;
     const bool prof0 = MCA_K12_PROF && blockIdx.x == 0;
     griddep_trigger();   // the work-list kernels may launch (they wait for this grid to complete)
     if (prof0 && threadIdx.x == 0) g_k12_prof[0] = clock64();
@@ -175,16 +202,16 @@ __global__ void __maxnreg__(72)
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
-    // block u of an item = (qt, kt) = (u / nt, u % nt); U = li * nblk + u counts the
-    // CTA's blocks across items (buffer index and barrier parity). Phase 1: S =
+    // block (qt, kt) of a unit; U counts the CTA's blocks across units (S buffer
+    // index and barrier parity), li its units (tile slot parity: every unit loads
+    // every Q and K tile once). Phase 1: S =
     // Q_qt K_kt^T into the A buffers; phase 2: S^T = K_kt Q_qt^T into the B
     // buffers. Each stream has its own issuing thread (tcgen05.commit tracks the
     // issuing thread's MMAs), so neither waits on the other's buffer recycling.
     const uint64_t dbase = sw128_desc(smem_u32(smem), 16, 1024);
     // Whole-warp MMA streams (one elected lane issues and commits; see tc_common.cuh)
-    auto issue = [&](int phase, int li, int u) {
-        const int U = li * nblk + u;
-        const int qt = u / nt, kt = u - qt * nt, sb = U & 1;
+    auto issue = [&](int phase, int li, int U, int qt, int kt, const Unit& un) {
+        const int sb = U & 1;
         uint64_t* full = phase ? b_full : a_full;
         uint64_t* empty = phase ? b_empty : a_empty;
         mbar_wait(empty + sb, ((U >> 1) & 1) ^ 1);
@@ -202,14 +229,21 @@ __global__ void __maxnreg__(72)
         if (prof0 && lane == 0 && phase == 0 && U < 32) g_k12_prof[192 + U] = clock64();
         uint64_t* tile_empty = phase ? tile_empty2 : tile_empty1;   // this phase's last read of a tile
         if (kt == nt - 1) umma_commit_w(tile_empty + qt);
-        if (qt == nt - 1) umma_commit_w(tile_empty + nt + kt);
+        if (qt == un.q1 - 1) umma_commit_w(tile_empty + nt + kt);
+        if (qt == un.q0 && kt == 0)   // a split unit's other Q tiles: loaded (one load per slot per unit), unused
+            for (int t = 0; t < nt; ++t)
+                if (t < un.q0 || t >= un.q1) {
+                    mbar_wait(tile_full + t, li & 1);   // landed before the slot is released
+                    umma_commit_w(tile_empty + t);
+                }
     };
     if (warp == k12::kThreads / 32 - 1) {
         if (lane == 0) {  // ---------------- TMA: every Q and K tile of each item once
             tma_prefetch(&tm_q);
             tma_prefetch(&tm_k);
             griddep_wait();   // q, k may be the projection GEMM's output
-            for (int it = blockIdx.x, li = 0; it < a.items; it += gridDim.x, ++li) {
+            for (int k = blockIdx.x, li = 0; k < a.units; k += gridDim.x, ++li) {
+                const int it = unit_of(a, k, nt).it;
                 const int b = it / heads, h = it - b * heads;
                 for (int t = 0; t < nt; ++t)
                     for (int op = 0; op < 2; ++op) {   // 0: Q tile t, 1: K tile t
@@ -224,8 +258,11 @@ __global__ void __maxnreg__(72)
             }
         }
     } else if (warp < 2) {   // ---------------- warp 0: the phase-2 MMA stream; warp 1: phase 1
-        for (int it = blockIdx.x, li = 0; it < a.items; it += gridDim.x, ++li)
-            for (int u = 0; u < nblk; ++u) issue(warp == 0, li, u);
+        for (int k = blockIdx.x, li = 0, ub = 0; k < a.units; k += gridDim.x, ++li) {
+            const Unit un = unit_of(a, k, nt);
+            for (int qt = un.q0; qt < un.q1; ++qt)
+                for (int kt = 0; kt < nt; ++kt, ++ub) issue(warp == 0, li, ub, qt, kt, un);
+        }
     } else if (warp < 2 + kAWarps) {
         // ---------------- group A: partial row statistics. Sub-group sub takes the
         // blocks with U & 1 == sub (S buffer sub), 64 columns [64 ch, +64) per warp.
@@ -236,11 +273,12 @@ __global__ void __maxnreg__(72)
         const int row = quad * 32 + lane;          // TMEM lane = query row of the tile
         const uint32_t lane_base = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)sub * kT + (uint32_t)ch * 64u;
         const float c2 = a.scale * 1.4426950408889634f;
-        for (int it = blockIdx.x, li = 0; it < a.items; it += gridDim.x, ++li) {
-            for (int qt = 0; qt < nt; ++qt) {
+        for (int k = blockIdx.x, ub = 0, qb = 0; k < a.units; k += gridDim.x) {
+            const Unit un = unit_of(a, k, nt);
+            for (int qt = un.q0; qt < un.q1; ++qt, ub += nt, ++qb) {
                 float m2 = -INFINITY, l = 0.0f;
                 for (int kt = 0; kt < nt; ++kt) {
-                    const int U = li * nblk + qt * nt + kt;
+                    const int U = ub + kt;
                     if ((U & 1) != sub) continue;
                     mbar_wait(a_full + sub, (U >> 1) & 1);
                     if (prof0 && (gt & 255) == 0 && U < 32) g_k12_prof[96 + U] = clock64();
@@ -296,7 +334,7 @@ __global__ void __maxnreg__(72)
                     if (prof0 && (gt & 255) == 0 && U < 39) g_k12_prof[1 + U] = clock64();
                 }
                 // hand this row's partial (max, sum) to group B
-                const int gq = li * nt + qt;
+                const int gq = qb;
                 mbar_wait(comb_empty + (gq & 1), ((gq >> 1) & 1) ^ 1);
                 combA[((gq & 1) * 4 + part) * kT + row] = make_float2(m2, l);
                 mbar_arrive(comb_full + (gq & 1));
@@ -310,12 +348,13 @@ __global__ void __maxnreg__(72)
         const int row = quad * 32 + lane;          // TMEM lane = key row of the tile
         const uint32_t lane_base = tmem + ((uint32_t)(quad * 32) << 16) + 2u * kT + (uint32_t)half * 64u;
         const float c2 = a.scale * 1.4426950408889634f;
-        for (int it = blockIdx.x, li = 0; it < a.items; it += gridDim.x, ++li) {
-            const int h = it % heads;
+        for (int k = blockIdx.x, ub = 0, qb = 0; k < a.units; k += gridDim.x) {
+            const Unit un = unit_of(a, k, nt);
+            const int it = un.it, h = it % heads;
             const size_t rbase = (size_t)it * n;
-            float lmax = 0.f;                          // max |lse| of the item's queries (certification scale)
-            for (int qt = 0; qt < nt; ++qt) {
-                const int gq = li * nt + qt;
+            float lmax = 0.f;                          // max |lse| of the unit's queries (certification scale)
+            for (int qt = un.q0; qt < un.q1; ++qt, ub += nt, ++qb) {
+                const int gq = qb;
                 float* s_lse2 = s_lse2b + (gq & 1) * kT;
                 mbar_wait(comb_full + (gq & 1), (gq >> 1) & 1);   // acquire: group A's partials of tile qt
                 if (gt < kT) {   // combine the four partials of query row gt
@@ -323,10 +362,15 @@ __global__ void __maxnreg__(72)
                     float mn = cb[0].x;
 #pragma unroll
                     for (int p = 1; p < 4; ++p) mn = fmaxf(mn, cb[p * kT].x);
+                    // canonical order, the even key tiles' partials first: sub-group
+                    // U & 1 took them, and U of (qt, 0) is odd when nt is odd and an
+                    // odd number of query tiles preceded qt on this CTA -- lse then
+                    // does not depend on where the item ran
+                    const int par = (ub & 1) << 1;
                     float lt = 0.f;
 #pragma unroll
                     for (int p = 0; p < 4; ++p) {
-                        const float2 o = cb[p * kT];
+                        const float2 o = cb[(p ^ par) * kT];
                         lt += o.x == -INFINITY ? 0.f : o.y * ex2_approx(o.x - mn);
                     }
                     const int q = qt * kT + gt;
@@ -343,9 +387,9 @@ __global__ void __maxnreg__(72)
                 }
                 named_bar_sync(2, kBThreads);          // -lse2 of tile qt is in smem; the partials are read
                 if (gt == 0) mbar_arrive(comb_empty + (gq & 1));
-                if (prof0 && gt == 0 && li * nt + qt < 32) g_k12_prof[224 + li * nt + qt] = clock64();
+                if (prof0 && gt == 0 && gq < 32) g_k12_prof[224 + gq] = clock64();
                 for (int kt = 0; kt < nt; ++kt) {
-                    const int U = li * nblk + qt * nt + kt, sb = U & 1;
+                    const int U = ub + kt, sb = U & 1;
                     // two running maxima break the dependency chain
                     float m0 = -INFINITY, m1 = -INFINITY;
 #pragma unroll
@@ -375,7 +419,7 @@ __global__ void __maxnreg__(72)
                         }
                     }
                     float* slot = combB + (kt * 2 + half) * kT + row;
-                    *slot = qt == 0 ? fmaxf(m0, m1) : fmaxf(*slot, fmaxf(m0, m1));
+                    *slot = qt == un.q0 ? fmaxf(m0, m1) : fmaxf(*slot, fmaxf(m0, m1));
                     if (prof0 && gt == 0 && U < 39) g_k12_prof[40 + U] = clock64();
                 }
             }
@@ -385,13 +429,35 @@ __global__ void __maxnreg__(72)
                 const unsigned wm = __reduce_max_sync(0xffffffffu, __float_as_uint(lmax));
                 if (lane == 0) s_lmax[gt >> 5] = wm;
             }
-            named_bar_sync(2, kBThreads);          // the running maxima of this item are final
-            const float item_lmax = __uint_as_float(max(max(s_lmax[0], s_lmax[1]), max(s_lmax[2], s_lmax[3])));
+            named_bar_sync(2, kBThreads);          // the running maxima of this unit are final
+            float item_lmax = __uint_as_float(max(max(s_lmax[0], s_lmax[1]), max(s_lmax[2], s_lmax[3])));
+            unsigned* tmax = nullptr;              // split item: the merged maxima
+            if (un.slot >= 0) {
+                tmax = a.tail + (size_t)un.slot * (n + 2);
+                for (int j = gt; j < n; j += kBThreads) {
+                    const int kt = j / kT, r0 = j - kt * kT;
+                    atomicMax(tmax + j, f32_key(fmaxf(combB[(kt * 2) * kT + r0], combB[(kt * 2 + 1) * kT + r0])));
+                }
+                if (gt == 0) atomicMax(tmax + n, __float_as_uint(item_lmax));   // >= 0: u32 order is float order
+                __threadfence();
+                named_bar_sync(2, kBThreads);      // this unit's maxima are visible device-wide
+                if (gt == 0) s_lmax[4] = atomicAdd(tmax + n + 1, 1u) == (unsigned)(a.tail_parts - 1);
+                named_bar_sync(2, kBThreads);
+                if (!s_lmax[4]) continue;          // another unit of the item finishes it
+                __threadfence();
+                item_lmax = __uint_as_float(__ldcg(tmax + n));
+            }
             unsigned long long cost = 0, samples = 0, nexact = 0;
             for (int j = gt; j < n; j += kBThreads) {
                 const int kt = j / kT, r0 = j - kt * kT;
-                // v = t - lse in the log2 domain, maximised over both query halves
-                const float vmax = fmaxf(combB[(kt * 2) * kT + r0], combB[(kt * 2 + 1) * kT + r0]);
+                // v = t - lse in the log2 domain, maximised over both query halves (and the item's units)
+                float vmax;
+                if (tmax) {
+                    vmax = key_f32(__ldcg(tmax + j));
+                    tmax[j] = 0u;
+                } else {
+                    vmax = fmaxf(combB[(kt * 2) * kT + r0], combB[(kt * 2 + 1) * kT + r0]);
+                }
                 const size_t t = rbase + j;
                 if (a.cert.row_done) a.cert.row_done[t] = 0;   // k2c's row-statistics cache
                 int r;
@@ -439,6 +505,10 @@ __global__ void __maxnreg__(72)
                 }
             }
             named_bar_sync(2, kBThreads);          // Eq. 9 has read the maxima and the histogram is complete
+            if (tmax && gt == 0) {
+                tmax[n] = 0u;
+                tmax[n + 1] = 0u;
+            }
             if (use_hist)
                 for (int i = gt; i <= a.d; i += kBThreads) {
                     const unsigned int v = s_hist[i];

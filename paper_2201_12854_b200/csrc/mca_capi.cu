@@ -264,6 +264,7 @@ struct mca_weights {
     unsigned int* cursor = nullptr;           // [H, d_in + 1] scatter cursors
     int* counts = nullptr;                    // [H, 2] sampled / exact token counts
     int* task_cursor = nullptr;               // [2][H] K3 work cursors
+    unsigned* k12_tail = nullptr;             // K12 split items: [SMs][kMaxTiles*128 + 2], zero between launches
     // timing
     bool timing = false;
     cudaEvent_t ev[6] = {};   // stage boundaries: projection | score | budgets | encoding | aggregation
@@ -421,6 +422,15 @@ long dense_exact_min(long token_heads) { return std::max(1L, (long)(kDenseExactF
 bool kp_pair_enabled() {
     static const bool on = [] {
         const char* e = getenv("MCA_KP_PAIR");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+// MCA_K12_SPLIT=0: K12 runs every item whole (no split last wave)
+bool k12_split_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("MCA_K12_SPLIT");
         return !(e && e[0] == '0');
     }();
     return on;
@@ -936,6 +946,7 @@ void mca_weights_free(mca_weights* w) {
     for (auto& g : w->graphs)
         if (g.exec) cudaGraphExecDestroy(g.exec);
     cudaFree(w->zeroed);
+    cudaFree(w->k12_tail);
     cudaFree(w->cursor);
     cudaFree(w->counts);
     for (auto& e : w->ev)
@@ -1189,7 +1200,25 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
         a.hist = tile_k3 ? nullptr : w->hist;
         a.cert = cert;
         a.items = B * H;
-        const int grid = std::min(B * H, sm_count());   // persistent: one CTA per SM
+        // The grid's last wave: split its items into per-query-tile units so the
+        // wave's leftover CTAs share them (C2: 768 items = 5 x 148 + 28 -> the 28
+        // items as 112 one-tile units instead of 28 CTAs running a sixth item).
+        const int sms = sm_count(), nt = (n + k12::kT - 1) / k12::kT;
+        const int rem = a.items % sms;
+        const int parts = rem ? std::min(nt, sms / rem) : 1;
+        a.tail_items = parts > 1 && k12_split_enabled() ? rem : 0;
+        a.tail_parts = a.tail_items ? parts : 1;
+        a.units = a.items - a.tail_items + a.tail_items * a.tail_parts;
+        if (a.tail_items && !w->k12_tail) {
+            const size_t bytes = (size_t)sms * (k12::kMaxTiles * k12::kT + 2) * sizeof(unsigned);
+            if (cudaMalloc(&w->k12_tail, bytes) != cudaSuccess) {
+                cudaGetLastError();
+                return fail(MCA_ERR_ALLOC, "K12 tail scratch allocation failed");
+            }
+            MCA_CUDA_TRY(cudaMemsetAsync(w->k12_tail, 0, bytes, stream));
+        }
+        a.tail = w->k12_tail;
+        const int grid = std::min(a.units, sms);   // persistent: one CTA per SM
         MCA_CUDA_TRY(launch_pdl(k12_fused_tc, dim3((unsigned)grid), dim3(k12::kThreads), smem, stream, tq, tk, a));
         MCA_LAUNCH_CHECK("k12_fused_tc");
         mca_diag::dump_k12(stream, n, grid);   // diagnostics builds only

@@ -470,7 +470,7 @@ def test_bf16_longer_than_tensor_core_score_pass(mca, syn, orc):
     B, n, H, d_in = 1, 4100, 2, 256
     weights, w, q, k, x = _setup(mca, syn, B, n, d_in, H, torch.bfloat16, seed=41)
     cm = torch.zeros((B, H, n), dtype=torch.float64, device="cuda")
-    out = mca.mca_forward(weights, q, k, x, mca.McaConfig(alpha=0.4), seed=3, return_plan=True,
+    out = mca.mca_forward(weights, q, k, x, mca.McaConfig(alpha=0.4), seed=3, return_plan=True, flops=True,
                           debug=dict(cmax_out=cm))
     b = out.budgets.cpu().numpy()
     e = out.exact_mask.cpu().numpy().astype(bool)
@@ -936,3 +936,52 @@ def test_host_pipeline_x_only(mca, syn, dtype):
     pipe.forward(None, None, hx, hy, cfg, seed=8, b_offset=1)
     torch.cuda.synchronize()
     assert torch.equal(hy, ref)
+
+
+_K12_SNIPPET = r"""
+import sys, torch
+sys.path.insert(0, {root!r})
+import paper_2201_12854_b200 as mca
+from paper_2201_12854_b200.synthetic import make_weights, make_projected_inputs
+out = {{}}
+# (B, n, H, d_in): 24 items on 148 SMs (every item split into 4 units), 156 items
+# (8 left over, 3 units each), n = 200 (two tiles, the second padded), C2's 768
+for B, n, H, d_in in ((2, 512, 12, 768), (13, 384, 12, 768), (5, 200, 12, 768), (64, 512, 12, 768)):
+    w = make_weights(d_in, H, seed=19).to(torch.bfloat16).cuda()
+    pin = make_projected_inputs(B, n, d_in, H, seed=19)
+    wts = mca.AttentionWeights(w, heads=H, w_q=pin.w_q.to(torch.bfloat16).cuda(), w_k=pin.w_k.to(torch.bfloat16).cuda())
+    x = pin.x.to(torch.bfloat16).cuda()
+    for cert in (False, True):
+        cm = torch.zeros((B, H, n), dtype=torch.float64, device="cuda")
+        lse = torch.zeros((B, H, n), dtype=torch.float32, device="cuda")
+        r = mca.mca_forward(wts, None, None, x, mca.McaConfig(alpha=0.4, certify=cert), seed=3, return_plan=True, flops=True,
+                            debug=dict(cmax_out=cm, lse_out=lse))
+        out[(B, n, cert)] = (r.y.cpu(), r.budgets.cpu(), r.exact_mask.cpu(), cm.cpu(), lse.cpu(), r.flops.samples,
+                             r.flops.exact_tokens)
+torch.save(out, {path!r})
+"""
+
+
+def test_k12_split_tail_bitwise(tmp_path):
+    """K12 splits the grid's last wave of (b, h) items into query-tile units
+    that merge their column maxima (MCA_K12_SPLIT, read once per process): the
+    outputs, budgets, exact mask, cmax, lse and FLOP counts equal the
+    whole-item kernel's bitwise (max is order-independent), with and without
+    certification."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for mode in ("1", "0"):
+        path = str(tmp_path / f"k12_{mode}.pt")
+        r = subprocess.run([sys.executable, "-c", _K12_SNIPPET.format(root=root, path=path)],
+                           env=dict(os.environ, MCA_K12_SPLIT=mode), capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        res[mode] = torch.load(path)
+    assert res["1"].keys() == res["0"].keys()
+    for key in res["1"]:
+        for i, (a, b) in enumerate(zip(res["1"][key], res["0"][key])):
+            if isinstance(a, torch.Tensor):
+                assert torch.equal(a, b), (key, i)
+            else:
+                assert a == b, (key, i)
