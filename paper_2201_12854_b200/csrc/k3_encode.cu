@@ -164,6 +164,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k3_encode_sampled(K3Args a) {
 
     const size_t HD = (size_t)heads * kDh;
     const T* wv = reinterpret_cast<const T*>(a.wv);
+    griddep_trigger();   // launched after the scan completed: k3b_encode_exact may run beside this grid
     for (int i = tid; i < d_in; i += kThreads) {
         s_thr[i] = a.thr[(size_t)h * d_in + i];
         if constexpr (sizeof(Coef) == 8) s_coef[i] = (Coef)a.probs[(size_t)h * d_in + i];
@@ -618,20 +619,27 @@ size_t k3_bf16_smem_bytes(int d_in) {
            (size_t)d_in * kDh * 2;
 }
 
-// Exact tokens (the fp32 path's fp64 GEMM, and bf16 under MCA_FORCE_SIMT):
+// Exact tokens (the fp32 path's fp64 GEMM, and bf16 under MCA_FORCE_SIMT),
+// concurrent with the sampled encoder (both read only the scan's work lists):
 // tiles of 64 listed tokens x 64 outputs, 128 threads, each an 8 x 4 register
 // tile (tokens 16 i + 2 ty + {0, 1}, outputs 32 i + 2 tx + {0, 1}: every 16-byte
 // shared-memory read of a warp covers contiguous bytes, conflict-free), so a
 // k-step costs 6 shared loads per 32 FMAs. The next k-chunk's X and W are
 // loaded into registers while the current one computes.
-template <class T, class Acc>
+// kNC = 32 (small batches, too few tiles to fill the GPU): each tile's 64
+// outputs are split over two CTAs (blockIdx.z = column half), a 8 x 2 tile per thread.
+template <class T, class Acc, int kNC>
 __global__ void __launch_bounds__(128) k3b_encode_exact(K3Args a) {
     constexpr int kTM = 64, kTK = 32;
+    constexpr int kNJ = kNC / 16;                 // outputs per thread: pairs 32 i + 2 tx
+    constexpr int kWP = kNC / 2;                  // W column pairs per row
+    constexpr int kWR = kTK * kWP / 128;          // W rows per loader thread
     using Acc2 = std::conditional_t<sizeof(Acc) == 8, double2, float2>;
     __shared__ __align__(16) Acc xs[kTK][kTM];   // transposed X chunk: xs[k][token]
-    __shared__ __align__(16) Acc ws[kTK][kDh];
+    __shared__ __align__(16) Acc ws[kTK][kNC];
     __shared__ int toks[kTM];
     const int h = blockIdx.y;
+    const int cbase = kNC == kDh ? 0 : (int)blockIdx.z * kNC;
     const int ne = a.counts[2 * h + 1];
     const int tiles = (ne + kTM - 1) / kTM;
     const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
@@ -642,9 +650,9 @@ __global__ void __launch_bounds__(128) k3b_encode_exact(K3Args a) {
     HT* hout = reinterpret_cast<HT*>(a.h_out);
     const int32_t* list = a.exact_list + (size_t)h * a.tokens;
     // loader roles: X token tid % 64, k half tid / 64 (16 consecutive k);
-    // W column pair tid % 32, rows 8 (tid / 32) .. + 8 (a warp reads 256 contiguous bytes per row)
+    // W column pair tid % kWP, rows kWR (tid / kWP) .. + kWR (contiguous bytes per row)
     const int xt = tid & 63, xk = (tid >> 6) * 16;
-    const int wc = 2 * (tid & 31), wr = (tid >> 5) * 8;
+    const int wc = 2 * (tid % kWP), wr = (tid / kWP) * kWR;
     for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
         __syncthreads();
         if (tid < kTM) {
@@ -652,13 +660,13 @@ __global__ void __launch_bounds__(128) k3b_encode_exact(K3Args a) {
             toks[tid] = bj < 0 ? -1 : (bj >> 16) * a.n + (bj & 0xFFFF);
         }
         __syncthreads();
-        Acc acc[8][4];
+        Acc acc[8][kNJ];
 #pragma unroll
         for (int i = 0; i < 8; ++i)
 #pragma unroll
-            for (int jj = 0; jj < 4; ++jj) acc[i][jj] = (Acc)0;
+            for (int jj = 0; jj < kNJ; ++jj) acc[i][jj] = (Acc)0;
         const int my_tok = toks[xt];
-        float vx[16], vw[16];
+        float vx[16], vw[2 * kWR];
         auto fetch = [&](int k0) {
             const int kb = k0 + xk;
             if (my_tok >= 0 && kb + 16 <= a.d_in) {
@@ -670,9 +678,9 @@ __global__ void __launch_bounds__(128) k3b_encode_exact(K3Args a) {
                     vx[e] = (my_tok >= 0 && kb + e < a.d_in) ? to_f32(x[(size_t)my_tok * a.d_in + kb + e]) : 0.f;
             }
 #pragma unroll
-            for (int r = 0; r < 8; ++r) {
+            for (int r = 0; r < kWR; ++r) {
                 const int row = k0 + wr + r;
-                const T* src = wv + (size_t)row * HD + (size_t)h * kDh + wc;
+                const T* src = wv + (size_t)row * HD + (size_t)h * kDh + cbase + wc;
                 vw[2 * r] = row < a.d_in ? to_f32(src[0]) : 0.f;
                 vw[2 * r + 1] = row < a.d_in ? to_f32(src[1]) : 0.f;
             }
@@ -682,7 +690,7 @@ __global__ void __launch_bounds__(128) k3b_encode_exact(K3Args a) {
 #pragma unroll
             for (int e = 0; e < 16; ++e) xs[xk + e][xt] = (Acc)vx[e];
 #pragma unroll
-            for (int r = 0; r < 8; ++r) {
+            for (int r = 0; r < kWR; ++r) {
                 Acc2 w2;
                 w2.x = (Acc)vw[2 * r];
                 w2.y = (Acc)vw[2 * r + 1];
@@ -692,7 +700,7 @@ __global__ void __launch_bounds__(128) k3b_encode_exact(K3Args a) {
             if (k0 + kTK < a.d_in) fetch(k0 + kTK);
 #pragma unroll 4
             for (int kk = 0; kk < kTK; ++kk) {
-                Acc av[8], bv[4];
+                Acc av[8], bv[kNJ];
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
                     const Acc2 t2 = *reinterpret_cast<const Acc2*>(&xs[kk][16 * i + 2 * ty]);
@@ -700,7 +708,7 @@ __global__ void __launch_bounds__(128) k3b_encode_exact(K3Args a) {
                     av[2 * i + 1] = t2.y;
                 }
 #pragma unroll
-                for (int i = 0; i < 2; ++i) {
+                for (int i = 0; i < kNJ / 2; ++i) {
                     const Acc2 w2 = *reinterpret_cast<const Acc2*>(&ws[kk][32 * i + 2 * tx]);
                     bv[2 * i] = w2.x;
                     bv[2 * i + 1] = w2.y;
@@ -708,11 +716,11 @@ __global__ void __launch_bounds__(128) k3b_encode_exact(K3Args a) {
 #pragma unroll
                 for (int i = 0; i < 8; ++i)
 #pragma unroll
-                    for (int jj = 0; jj < 4; ++jj) acc[i][jj] = fma(av[i], bv[jj], acc[i][jj]);
+                    for (int jj = 0; jj < kNJ; ++jj) acc[i][jj] = fma(av[i], bv[jj], acc[i][jj]);
             }
             __syncthreads();
         }
-        if (a.draws_out && tid < kTM && toks[tid] >= 0) {   // exact token-heads draw nothing
+        if (a.draws_out && cbase == 0 && tid < kTM && toks[tid] >= 0) {   // exact token-heads draw nothing
             const int tok = toks[tid], b = tok / a.n, j = tok - b * a.n;
             const size_t tokh = ((size_t)b * a.heads + h) * a.n + j;
             for (int k = 0; k < a.draws_stride; ++k) a.draws_out[tokh * a.draws_stride + k] = -1;
@@ -721,11 +729,15 @@ __global__ void __launch_bounds__(128) k3b_encode_exact(K3Args a) {
         for (int i = 0; i < 8; ++i) {
             const int tok = toks[16 * (i >> 1) + 2 * ty + (i & 1)];
             if (tok < 0) continue;
-            HT* dst = hout + (size_t)tok * HD + (size_t)h * kDh;
+            HT* dst = hout + (size_t)tok * HD + (size_t)h * kDh + cbase;
 #pragma unroll
-            for (int jj = 0; jj < 4; ++jj) dst[32 * (jj >> 1) + 2 * tx + (jj & 1)] = (HT)((float)acc[i][jj]);
+            for (int jj = 0; jj < kNJ; ++jj) dst[32 * (jj >> 1) + 2 * tx + (jj & 1)] = (HT)((float)acc[i][jj]);
         }
     }
+    // Launched as a programmatic dependent of the sampled encoder, which triggers
+    // at entry: the two run side by side (C1: 24 + 48 CTAs), and this grid
+    // completes only after the encoder did, so the next kernel sees all of H~.
+    griddep_wait();
 }
 
 template __global__ void k3_encode_sampled<float, float, float, true>(K3Args);
@@ -733,7 +745,9 @@ template __global__ void k3_encode_sampled<float, float, float, false>(K3Args);
 template __global__ void k3_encode_sampled<__nv_bfloat16, float, float, true>(K3Args);
 template __global__ void k3_encode_sampled<__nv_bfloat16, __nv_bfloat16, float, true>(K3Args);
 template __global__ void k3_encode_sampled<__nv_bfloat16, __nv_bfloat16, float, false>(K3Args);
-template __global__ void k3b_encode_exact<float, double>(K3Args);
-template __global__ void k3b_encode_exact<__nv_bfloat16, float>(K3Args);
+template __global__ void k3b_encode_exact<float, double, 64>(K3Args);
+template __global__ void k3b_encode_exact<float, double, 32>(K3Args);
+template __global__ void k3b_encode_exact<__nv_bfloat16, float, 64>(K3Args);
+template __global__ void k3b_encode_exact<__nv_bfloat16, float, 32>(K3Args);
 
 }  // namespace mca_dev

@@ -584,7 +584,11 @@ mca_status launch_k3(mca_weights* w, const void* x, int B, int n, long b_offset,
         const long ecap = (a.tokens + 63) / 64;
         if (Ge > ecap) Ge = (int)ecap;
         if (Ge < 1) Ge = 1;
-        k3b_encode_exact<T, Acc><<<dim3(Ge, w->heads), 128, 0, stream>>>(a);
+        // few tiles (C1: 2 per head): split each tile's outputs over two CTAs
+        if ((long)Ge * w->heads * 2 <= 2L * sm_count())
+            MCA_CUDA_TRY(launch_pdl(k3b_encode_exact<T, Acc, 32>, dim3((unsigned)Ge, w->heads, 2), dim3(128), 0, stream, a));
+        else
+            MCA_CUDA_TRY(launch_pdl(k3b_encode_exact<T, Acc, 64>, dim3((unsigned)Ge, w->heads), dim3(128), 0, stream, a));
         MCA_LAUNCH_CHECK("k3b_encode_exact");
     }
     return MCA_OK;
@@ -631,7 +635,11 @@ mca_status launch_projection(mca_weights* w, const void* x, long tokens, int seg
     // N tile: the widest of 256 / 128 / 64 that divides H*64 (192 for BERT-base's
     // finer wave quantisation measured 72 us vs 66 for 256: per-tile overheads)
     // 3xTF32: 128 (three 64 KB stages instead of two 96 KB ones; measured 291 vs 303 us at C2)
-    const int BN = (HD % 256 == 0 && !tf32) ? 256 : HD % 128 == 0 ? 128 : 64;
+    // Small M (C1: one 128-row tile): 128 x 64 tiles on single CTAs when they fit
+    // one wave -- 4x the CTAs of the 256 x 256 pairs on a K loop that is serial
+    // per tile (C1 fp32: 33 -> 9 us)
+    const bool small = HD % 64 == 0 && ((tokens + kp::kBM - 1) / kp::kBM) * ((long)nseg * HD / 64) <= sm_count();
+    const int BN = small ? 64 : (HD % 256 == 0 && !tf32) ? 256 : HD % 128 == 0 ? 128 : 64;
     CUtensorMap tx, tw, tx2, tw2, to[3];
     const size_t wofs = (size_t)seg0 * HD * w->d_in;
     if (tf32) {
@@ -694,7 +702,7 @@ mca_status launch_projection(mca_weights* w, const void* x, long tokens, int seg
     pa.f16_mask = mask;
     const long tiles = ((tokens + kp::kBM - 1) / kp::kBM) * ((long)nseg * HD / BN);
     const dim3 grid((unsigned)std::min<long>(tiles, sm_count()));
-    if (HD % 256 == 0 && kp_pair_enabled()) {   // a 256-column pair tile never straddles two segments
+    if (!small && HD % 256 == 0 && kp_pair_enabled()) {   // a 256-column pair tile never straddles two segments
         // CTA pairs: 256 x 256 tiles (kp_project_pair.cu); W^T with 128-row boxes
         // (each CTA of the pair loads half of the tile's N)
         const long ptiles = ((tokens + 255) / 256) * ((long)nseg * HD / 256);

@@ -884,7 +884,7 @@ sys.path.insert(0, {root!r})
 import paper_2201_12854_b200 as mca
 from paper_2201_12854_b200.synthetic import make_weights, make_projected_inputs
 out = {{}}
-for dt, B, n, H, d_in in ((torch.bfloat16, 2, 300, 12, 768), (torch.float32, 1, 257, 4, 256), (torch.bfloat16, 1, 77, 16, 1024)):
+for dt, B, n, H, d_in in ((torch.bfloat16, 8, 300, 12, 768), (torch.float32, 8, 257, 8, 256), (torch.bfloat16, 8, 77, 16, 1024)):
     w = make_weights(d_in, H, seed=9).to(dt).cuda()
     pin = make_projected_inputs(B, n, d_in, H, seed=9)
     wts = mca.AttentionWeights(w, heads=H, w_q=pin.w_q.to(dt).cuda(), w_k=pin.w_k.to(dt).cuda())
@@ -900,7 +900,8 @@ def test_projection_pair_vs_single_cta(tmp_path):
     """The CTA-pair projection GEMM (cta_group::2, default) and the single-CTA
     one (MCA_KP_PAIR=0, read once per process): q / k agree to fp32 summation
     order (bf16 outputs: within one rounding; fp32: 1e-6), including the
-    exact layer's three-segment GEMM."""
+    exact layer's three-segment GEMM. Shapes with more 128 x 64 tiles than SMs
+    (smaller ones take the single-CTA 128 x 64 tiles in both modes)."""
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
