@@ -327,13 +327,17 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k3_encode_sampled(K3Args a) {
 
     // Warp tasks of 8 consecutive list entries: octet o encodes entries o and 4 + o.
     // Both entries' list / budget loads and row prefetches are issued before the
-    // first is encoded, so the second token's start-up latency is hidden.
+    // first is encoded, so the second token's start-up latency is hidden. A short
+    // list (fewer than two tasks per warp of this head-half) takes 4 per task, so
+    // the longest tokens (the list is budget-descending) run on separate octets
+    // (C1: the critical path was the top token plus the fifth).
+    const int tsz = nsamp < 2 * 8 * kWarps * (int)gridDim.x ? 4 : 8;
     for (;;) {
         int t0 = 0;
-        if (lane == 0) t0 = atomicAdd(a.task_cursor + h + half * heads, 8);   // each half walks the list
+        if (lane == 0) t0 = atomicAdd(a.task_cursor + h + half * heads, tsz);   // each half walks the list
         t0 = __shfl_sync(0xffffffffu, t0, 0);
         if (t0 >= nsamp) break;
-        const int ea = t0 + oct, eb = t0 + 4 + oct;
+        const int ea = t0 + oct, eb = tsz == 8 ? t0 + 4 + oct : nsamp;
         const int bja = ea < nsamp ? list[ea] : -1;
         const int bjb = eb < nsamp ? list[eb] : -1;
         const int ra = bja >= 0 ? a.budgets[((size_t)(bja >> 16) * heads + h) * n + (bja & 0xFFFF)] : 0;
