@@ -1,4 +1,5 @@
-# K4 with / without the next tile's K / H~ L2 prefetch (A/B twice), then the per-block timeline
+# K4 with / without an L2 prefetch of the next tile's K / H~ (A/B twice), then the per-block timeline.
+# Measured 94.7 (prefetch) vs 83.8 us; the prefetch (MCA_K4_L2PF, cp.async.bulk.prefetch.tensor) was removed after it.
 cp paper_2201_12854_b200/lib/libmca_b200.so /tmp/libpf.so
 for rep in 1 2; do for v in pf nopf; do
   if [ $v = pf ]; then cp /tmp/libpf.so paper_2201_12854_b200/lib/libmca_b200.so; else cp paper_2201_12854_b200/lib_exp/libk4nopf.so paper_2201_12854_b200/lib/libmca_b200.so; fi
