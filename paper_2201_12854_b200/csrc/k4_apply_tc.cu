@@ -2,15 +2,17 @@
 // (b, h, 128-query tile) per CTA (matrix.hpp:33-34 `matmul`).
 //
 // A is never materialised. Per 64-key block:
-//   S  = Q K_blk^T                  tcgen05.mma M=128 N=64 K=64, Q and K from smem -> S in TMEM (fp32)
+//   S  = Q K_blk^T                  tcgen05.mma M=128 N=64 K=64, A = Q from TMEM -> S in TMEM (fp32)
 //   P  = 2^(log2e (scale*S - lse))  8 softmax warps, 2 per TMEM lane quadrant
 //                                   (lane = query row), 32 keys each; lse from
 //                                   K1, so no online rescaling; P is written
 //                                   back into TMEM as fp16 over the S columns
 //                                   the warp just read
 //   O += P H~_blk                   tcgen05.mma kind::f16, A = P from TMEM, B = H~ (MN-major smem)
-// K and H~ blocks pass through shared memory (TMA rings), Q tiles through two
-// TMA slots (the tile's and the next one's); P lives in tensor memory.
+// Only K and H~ blocks pass through shared memory (TMA rings); Q and P live in
+// tensor memory, which is what keeps this kernel off the shared-memory
+// bandwidth ceiling (an smem P tile costs a store and a tensor-core read of
+// 16 KB per block, Q another 16 KB read per block).
 // S/P buffers: S(kb) and P(kb) share TMEM columns [64 (kb&1), +64); the
 // issuer puts S(kb+2) into that buffer only after P(kb).H~ was issued (the
 // tensor pipe executes one thread's MMAs in order), and the softmax warps
@@ -18,14 +20,13 @@
 // barriers are needed.
 // Persistent: two CTAs per SM walk tiles t = blockIdx.x + i * gridDim.x. TMEM
 // and barriers are set up once; block numbering continues across tiles, so the
-// K / H~ rings prefetch the next tile while this one computes. O is
-// double-buffered (tile i accumulates into buffer i & 1), so the next tile's
-// P.H~ never waits for the epilogue, and the softmax warps run tile i's
-// epilogue inside tile i + 1, after its second block (C2: 87 -> 83 us).
-// Warp roles (320 threads): warp 0 TMA producers (lane 0: Q and the K ring,
-// lane 16: the H~ ring), warp 1 TMEM allocator + MMA issuer, warps 2-9 softmax
-// and the epilogue. TMEM (256 columns, two CTAs per SM): S/P0 [0,64),
-// S/P1 [64,128), O0 [128,192), O1 [192,256).
+// K / H~ rings prefetch the next tile while this one computes, the next tile's
+// Q is loaded during the last block and its first S MMAs run during this
+// tile's epilogue (O is handed back through o_empty before the next P.H~).
+// Warp roles (320 threads): warp 0 TMA producers (lane 0: K ring, lane 16: H~
+// ring), warp 1 TMEM allocator + single-thread MMA issuer, warps 2-9 load Q
+// into TMEM, then softmax and the epilogue. TMEM (256 columns, two CTAs per
+// SM): S/P0 [0,64), S/P1 [64,128), O [128,192), Q [192,224).
 #include "k4o_overflow.cu"
 #include "mca_common.cuh"
 #include "tc_common.cuh"
@@ -54,15 +55,14 @@ constexpr int kBM = 128, kBK = 64, kStages = MCA_K4_STAGES;   // separate K and 
 constexpr int kConsumers = 8;                        // 2 warps per TMEM lane quadrant
 constexpr int kThreads = 64 + kConsumers * 32;
 constexpr uint32_t kTileBytes = kBK * kDh * 2;       // 8 KB: one 64-key K or H~ block
-constexpr uint32_t kQBytes = kBM * kDh * 2;          // 16 KB: one 128-query Q tile
 constexpr uint32_t kSmemK = 0;                                       // kStages tiles
 constexpr uint32_t kSmemH = kSmemK + kStages * kTileBytes;           // kStages tiles
-constexpr uint32_t kSmemQ = kSmemH + kStages * kTileBytes;           // 2 Q tiles (this tile's, the next one's)
-constexpr uint32_t kSmemBar = kSmemQ + 2 * kQBytes;
+constexpr uint32_t kSmemBar = kSmemH + kStages * kTileBytes;
 constexpr uint32_t kSmemBytes = kSmemBar + 256 + 1024;               // + alignment slack
-constexpr uint32_t kIdescS = mca_tc::idesc_f16(1, 0, kBM, kBK);      // bf16 Q x bf16 K, both K-major in smem
+constexpr uint32_t kIdescS = mca_tc::idesc_f16(1, 0, kBM, kBK);      // bf16 Q (TMEM) x bf16 K, B K-major
 constexpr uint32_t kIdescO = mca_tc::idesc_f16(0, 1, kBM, kDh);      // fp16 P (TMEM) x fp16 H~, B MN-major
-constexpr uint32_t kOCol = 2 * kBK;                                  // O of even / odd tiles: [128,192), [192,256)
+constexpr uint32_t kOCol = 2 * kBK;                                  // O [128,192)
+constexpr uint32_t kQCol = kOCol + kDh;                              // Q [192,224): 64 bf16 per lane
 #ifndef MCA_K4_POLY
 #define MCA_K4_POLY 4
 #endif
@@ -76,7 +76,7 @@ __device__ __forceinline__ uint32_t k4_p_col(int sb, int kk) {
 }
 
 __global__ void __launch_bounds__(k4tc::kThreads, 2)
-    k4_apply_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+    k4_apply_tc(const __nv_bfloat16* __restrict__ q, const __grid_constant__ CUtensorMap tm_k,
                 const __grid_constant__ CUtensorMap tm_h, const float* __restrict__ lse, int n, int heads,
                 int batch, float scale, __nv_bfloat16* __restrict__ y, const K4oArgs oa,
                 unsigned long long* __restrict__ done_ctas) {
@@ -85,17 +85,16 @@ __global__ void __launch_bounds__(k4tc::kThreads, 2)
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kSmemBar);
-    uint64_t* q_full = bars + 0;               // [2] TMA -> issuer: Q tile i is in slot i & 1
-    uint64_t* q_empty = bars + 2;              // [2] issuer -> TMA: tile i's S MMAs completed
-    uint64_t* o_full = bars + 4;               // [2] issuer -> softmax warps: tile i's O (buffer i & 1) is final
-    uint64_t* o_empty = bars + 6;              // [2] softmax warps -> issuer: O buffer read out
-    uint64_t* k_full = bars + 8;               // [kStages]  K ring: freed when S(kb) completes
+    uint64_t* q_full = bars + 0;               // softmax warps -> issuer: the tile's Q is in TMEM
+    uint64_t* o_empty = bars + 1;              // softmax warps -> issuer: the previous tile's O was read out
+    uint64_t* k_full = bars + 2;               // [kStages]  K ring: freed when S(kb) completes
     uint64_t* k_empty = k_full + kStages;      // [kStages]
     uint64_t* h_full = k_empty + kStages;      // [kStages]  H~ ring: freed when P(kb).H~(kb) completes
     uint64_t* h_empty = h_full + kStages;      // [kStages]
     uint64_t* s_full = h_empty + kStages;      // [2]
     uint64_t* p_full = s_full + 2;             // [2]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 4);
+    uint64_t* o_full = s_full + 4;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 5);
 
     if (MCA_K4_PROF && blockIdx.x == 0 && threadIdx.x == 64) g_k4_prof[60] = clock64();
     griddep_trigger();
@@ -115,12 +114,8 @@ __global__ void __launch_bounds__(k4tc::kThreads, 2)
     };
 
     if (threadIdx.x == 0) {
-        for (int i = 0; i < 2; ++i) {
-            mbar_init(q_full + i, 1);
-            mbar_init(q_empty + i, 1);
-            mbar_init(o_full + i, 1);
-            mbar_init(o_empty + i, kConsumers * 32);
-        }
+        mbar_init(q_full, kConsumers * 32);
+        mbar_init(o_empty, kConsumers * 32);
         for (int s = 0; s < kStages; ++s) {
             mbar_init(k_full + s, 1);
             mbar_init(k_empty + s, 1);
@@ -131,6 +126,7 @@ __global__ void __launch_bounds__(k4tc::kThreads, 2)
             mbar_init(s_full + i, 1);
             mbar_init(p_full + i, kConsumers * 32);
         }
+        mbar_init(o_full, 1);
         fence_barrier_init();
     }
     if (warp == 1) tmem_alloc<256>(tmem_slot);
@@ -148,18 +144,10 @@ __global__ void __launch_bounds__(k4tc::kThreads, 2)
             uint64_t* empty = lane == 0 ? k_empty : h_empty;
             const uint32_t base = lane == 0 ? kSmemK : kSmemH;
             tma_prefetch(tm);
-            if (lane == 0) tma_prefetch(&tm_q);
             if (lane == 16) griddep_wait();   // H~ is the encoders' output
             for (int i = 0, g = 0; i < my_tiles; ++i) {
                 int b, h, m0;
                 tile_coords(i, b, h, m0);
-                if (lane == 0) {   // the tile's Q (two slots), in order with its K blocks: its slot frees
-                                   // (tile i - 2's S complete) before the K ring's does
-                    const int slot = i & 1;
-                    mbar_wait(q_empty + slot, ((i >> 1) & 1) ^ 1);
-                    mbar_expect_tx(q_full + slot, kQBytes);
-                    tma_load_3d(smem + kSmemQ + slot * kQBytes, &tm_q, q_full + slot, h * kDh, m0, b);
-                }
                 for (int kb = 0; kb < nkb; ++kb, ++g) {
                     const int s = g % kStages;
                     mbar_wait(empty + s, ((g / kStages) & 1) ^ 1);
@@ -171,21 +159,19 @@ __global__ void __launch_bounds__(k4tc::kThreads, 2)
     } else if (warp == 1) {   // ---------------- MMA issuer (whole warp; one elected lane issues)
         const uint64_t dk0 = sw128_desc(smem_u32(smem + kSmemK), 16, 1024);
         const uint64_t dh0 = sw128_desc(smem_u32(smem + kSmemH), kBK * 128, 1024);
-        const uint64_t dq0 = sw128_desc(smem_u32(smem + kSmemQ), 16, 1024);
-        auto issue_s = [&](int g, int qslot) {
+        auto issue_s = [&](int g) {
             const int s = g % kStages, sb = g & 1;
             mbar_wait(k_full + s, (g / kStages) & 1);
             tc_fence_after();
             const uint64_t dk = desc_add(dk0, s * kTileBytes);
-            const uint64_t dq = desc_add(dq0, qslot * kQBytes);
 #pragma unroll
             for (int kk = 0; kk < kDh / 16; ++kk)
                 if (MCA_K4_EXP != 2)   // diagnostics: 2 = no MMAs
-                    umma_f16_w(tmem + sb * kBK, desc_add(dq, kk * 32), desc_add(dk, kk * 32), kIdescS, kk > 0 ? 1u : 0u);
+                    umma_f16_ts_w(tmem + sb * kBK, tmem + kQCol + kk * 8, desc_add(dk, kk * 32), kIdescS, kk > 0 ? 1u : 0u);
             umma_commit_w(s_full + sb);
             umma_commit_w(k_empty + s);
         };
-        auto issue_pv = [&](int g, bool first, uint32_t ocol) {
+        auto issue_pv = [&](int g, bool first) {
             const int s = g % kStages, sb = g & 1;
             mbar_wait(p_full + sb, (g >> 1) & 1);
             mbar_wait(h_full + s, (g / kStages) & 1);
@@ -194,88 +180,80 @@ __global__ void __launch_bounds__(k4tc::kThreads, 2)
 #pragma unroll
             for (int kk = 0; kk < kBK / 16; ++kk)
                 if (MCA_K4_EXP != 2)
-                umma_f16_ts_w(tmem + ocol, tmem + k4_p_col(sb, kk), desc_add(dh, kk * 2048), kIdescO,
+                umma_f16_ts_w(tmem + kOCol, tmem + k4_p_col(sb, kk), desc_add(dh, kk * 2048), kIdescO,
                               (!first || kk > 0) ? 1u : 0u);
             umma_commit_w(h_empty + s);
         };
         for (int i = 0; i < my_tiles; ++i) {
-            const int g0 = i * nkb, slot = i & 1;
-            mbar_wait(q_full + slot, (i >> 1) & 1);
+            const int g0 = i * nkb;
+            mbar_wait(q_full, i & 1);
             tc_fence_after();
             // S runs two blocks ahead of P.H~ (S(kb+2) goes into the buffer P(kb) just left)
-            issue_s(g0, slot);
-            if (nkb > 1) issue_s(g0 + 1, slot);
-            mbar_wait(o_empty + slot, ((i >> 1) & 1) ^ 1);   // tile i - 2's O (same buffer) was read out
+            issue_s(g0);
+            if (nkb > 1) issue_s(g0 + 1);
+            mbar_wait(o_empty, (i & 1) ^ 1);   // the previous tile's O has been read out
             for (int kb = 0; kb < nkb; ++kb) {
-                issue_pv(g0 + kb, kb == 0, kOCol + (uint32_t)slot * kDh);
-                if (kb + 2 < nkb) issue_s(g0 + kb + 2, slot);
+                issue_pv(g0 + kb, kb == 0);
+                if (kb + 2 < nkb) issue_s(g0 + kb + 2);
             }
-            umma_commit_w(q_empty + slot);   // every S of tile i issued: the slot frees when they complete
-            umma_commit_w(o_full + slot);
+            umma_commit_w(o_full);
         }
-    } else {  // ------------------------------- softmax and epilogue (warps 2..9)
+    } else {  // ------------------------------- Q -> TMEM, softmax, epilogue (warps 2..9)
         const int quad = warp & 3;                 // TMEM lane quadrant this warp may access
-        const int half = (warp - 2) >> 2;          // keys [32*half, 32*half+32) of each block; O columns likewise
+        const int half = (warp - 2) >> 2;          // keys [32*half, 32*half+32) of each block; Q dims likewise
         const int row = quad * 32 + lane;          // query row within the tile
         const uint32_t lane_base = tmem + ((uint32_t)(quad * 32) << 16);
         const float c = scale * 1.4426950408889634f;
         const size_t HD = (size_t)heads * kDh;
         const bool prof = MCA_K4_PROF && blockIdx.x == 0 && warp == 2 && lane == 0;
+        // this thread's 32 Q values (64 bytes) of tile i and its row's lse (log2 domain)
+        uint32_t qv[16];
         float lse_next = 0.f;   // raw: scaled at the next tile's start, so the load overlaps the last block
         bool waited = false;
-        auto load_lse = [&](int i) {
+        auto load_q = [&](int i) {
             int b, h, m0;
             tile_coords(i, b, h, m0);
             const int grow = m0 + row;
             if (i < my_tiles && grow < n) {
+                const uint4* src = reinterpret_cast<const uint4*>(q + ((size_t)b * n + grow) * HD + (size_t)h * kDh + 32 * half);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const uint4 t = __ldg(src + u);
+                    qv[4 * u] = t.x;
+                    qv[4 * u + 1] = t.y;
+                    qv[4 * u + 2] = t.z;
+                    qv[4 * u + 3] = t.w;
+                }
                 if (!waited) {   // lse is the score pass's output
                     griddep_wait();
                     waited = true;
                 }
                 lse_next = lse[((size_t)b * heads + h) * n + grow];
             } else {
+#pragma unroll
+                for (int u = 0; u < 16; ++u) qv[u] = 0u;
                 lse_next = 0.f;
             }
         };
-        // Tile ti's epilogue: O (fp32, buffer ti & 1) -> bf16 -> y, each half 32 columns.
-        // Run inside the next tile (after its second block): O is double-buffered, so
-        // the issuer never waits for it, and by then the last P.H~ has completed.
-        auto epilogue = [&](int ti) {
-            int b, h, m0;
-            tile_coords(ti, b, h, m0);
-            const int grow = m0 + row;
-            mbar_wait(o_full + (ti & 1), (ti >> 1) & 1);
-            if (prof && ti == 0) g_k4_prof[52] = clock64();
-            tc_fence_after();
-            uint32_t ov[32];
-            tmem_ld32(lane_base + kOCol + (uint32_t)(ti & 1) * kDh + half * 32, ov);
-            tmem_ld_wait();
-            if (prof && ti == 0) g_k4_prof[53] = clock64();
+        auto publish_q = [&]() {   // Q registers -> TMEM columns kQCol + [16 half, 16 half + 16)
+            tmem_st16(lane_base + kQCol + 16 * half, qv);
+            tmem_st_wait();
             tc_fence_before();
-            mbar_arrive(o_empty + (ti & 1));
-            if (grow < n) {
-                __nv_bfloat16* dst = y + ((size_t)b * n + grow) * HD + (size_t)h * kDh + half * 32;
-#pragma unroll
-                for (int gq = 0; gq < 4; ++gq) {
-                    uint32_t pk[4];
-#pragma unroll
-                    for (int e = 0; e < 4; ++e)
-                        pk[e] = pack_bf16x2(__uint_as_float(ov[gq * 8 + 2 * e]), __uint_as_float(ov[gq * 8 + 2 * e + 1]));
-                    reinterpret_cast<uint4*>(dst)[gq] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-                }
-            }
+            mbar_arrive(q_full);
         };
-        const int kEpiAt = nkb > 1 ? 1 : 0;   // block of tile i after which tile i - 1's epilogue runs
-        load_lse(0);
+        load_q(0);
+        publish_q();
         for (int i = 0; i < my_tiles; ++i) {
+            int b, h, m0;
+            tile_coords(i, b, h, m0);
+            const int grow = m0 + row;
             const float lse2 = lse_next * 1.4426950408889634f;
             const int g0 = i * nkb;
             if (prof && i == 1) g_k4_prof[0] = clock64();
-            if (prof && i == 1) g_k4_prof[54] = clock64();
             for (int kb = 0; kb < nkb; ++kb) {
                 const int g = g0 + kb, sb = g & 1;
                 if (kb == (nkb > MCA_K4_QAHEAD ? nkb - 1 - MCA_K4_QAHEAD : 0))
-                    load_lse(i + 1);   // next tile's lse in flight during the tile's last blocks
+                    load_q(i + 1);   // next tile's Q (and lse) in flight during the tile's last blocks
                 mbar_wait(s_full + sb, (g >> 1) & 1);
                 if (prof && i == 1 && kb < 16) g_k4_prof[1 + 3 * kb] = clock64();
                 tc_fence_after();
@@ -319,13 +297,32 @@ __global__ void __launch_bounds__(k4tc::kThreads, 2)
                 tc_fence_before();
                 mbar_arrive(p_full + sb);
                 if (prof && i == 1 && kb < 16) g_k4_prof[3 + 3 * kb] = clock64();
-                if (kb == kEpiAt && i > 0) {
-                    epilogue(i - 1);
-                    if (prof && i == 1) g_k4_prof[51] = clock64();
+            }
+            // all of tile i's S are consumed, so Q may be replaced: the issuer starts
+            // tile i+1's S while this tile's epilogue runs
+            if (i + 1 < my_tiles) publish_q();
+            // epilogue: O (fp32, TMEM cols 128..191) -> bf16 -> y; each half writes 32 columns
+            mbar_wait(o_full, i & 1);
+            if (prof && i == 1) g_k4_prof[50] = clock64();
+            tc_fence_after();
+            uint32_t ov[32];
+            tmem_ld32(lane_base + kOCol + half * 32, ov);
+            tmem_ld_wait();
+            tc_fence_before();
+            mbar_arrive(o_empty);
+            if (grow < n) {
+                __nv_bfloat16* dst = y + ((size_t)b * n + grow) * HD + (size_t)h * kDh + half * 32;
+#pragma unroll
+                for (int gq = 0; gq < 4; ++gq) {
+                    uint32_t pk[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e)
+                        pk[e] = pack_bf16x2(__uint_as_float(ov[gq * 8 + 2 * e]), __uint_as_float(ov[gq * 8 + 2 * e + 1]));
+                    reinterpret_cast<uint4*>(dst)[gq] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
                 }
             }
+            if (prof && i == 1) g_k4_prof[51] = clock64();
         }
-        if (my_tiles > 0) epilogue(my_tiles - 1);
     }
     tc_fence_before();
     __syncthreads();

@@ -1425,11 +1425,10 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
                 (const __nv_bfloat16*)q, (const __nv_bfloat16*)k, (const __half*)w->hbuf, w->lse, n, H,
                 (float)scale, (__nv_bfloat16*)y);
         else {
-            CUtensorMap tq4, tk, th;
-            if (!make_tmap_bf16(&tq4, q, (uint64_t)H * kDh, n, B, k4tc::kBM) ||
-                !make_tmap_bf16(&tk, k, (uint64_t)H * kDh, n, B, k4tc::kBK) ||
+            CUtensorMap tk, th;
+            if (!make_tmap_bf16(&tk, k, (uint64_t)H * kDh, n, B, k4tc::kBK) ||
                 !make_tmap_bf16(&th, w->hbuf, (uint64_t)H * kDh, n, B, k4tc::kBK, CU_TENSOR_MAP_DATA_TYPE_FLOAT16))
-                return fail(MCA_ERR_CUDA, "cuTensorMapEncodeTiled failed for q/k/h");
+                return fail(MCA_ERR_CUDA, "cuTensorMapEncodeTiled failed for k/h");
             MCA_CUDA_TRY(ensure_smem(k4_apply_tc, k4tc::kSmemBytes));
             const long tiles = (long)B * H * ((n + k4tc::kBM - 1) / k4tc::kBM);
             const int grid = (int)std::min<long>(tiles, 2L * sm_count());   // persistent: two CTAs per SM
@@ -1446,7 +1445,7 @@ mca_status mca_forward_ex(mca_weights* w, const void* q, const void* k, const vo
             o.heads = H;
             o.y = (__nv_bfloat16*)y;
             MCA_CUDA_TRY(launch_pdl(k4_apply_tc, dim3(grid), dim3(k4tc::kThreads), k4tc::kSmemBytes, stream,
-                                    tq4, tk, th, (const float*)w->lse, n, H, B, (float)scale,
+                                    (const __nv_bfloat16*)q, tk, th, (const float*)w->lse, n, H, B, (float)scale,
                                     (__nv_bfloat16*)y, o, w->counters + kK4DoneCounter));
             mca_diag::dump_k4(stream, n, k4tc::kBK);   // diagnostics builds only
         }

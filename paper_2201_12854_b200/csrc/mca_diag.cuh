@@ -94,7 +94,7 @@ inline void dump_k4(cudaStream_t stream, int n, int block_keys) {
     for (int kb = 0; kb < (n + block_keys - 1) / block_keys && kb < 16; ++kb)
         fprintf(stderr, " kb%d S@%lld P@%lld done@%lld", kb, t[1 + 3 * kb] - t[60], t[2 + 3 * kb] - t[60],
                 t[3 + 3 * kb] - t[60]);
-    fprintf(stderr, " | epilogue of tile 0: O full@%lld O read@%lld end@%lld\n", t[52] - t[60], t[53] - t[60], t[51] - t[60]);
+    fprintf(stderr, " | O@%lld end@%lld\n", t[50] - t[60], t[51] - t[60]);
 }
 #else
 inline void dump_k4(cudaStream_t, int, int) {}
