@@ -268,7 +268,24 @@ __global__ void __launch_bounds__(kScatterThreads) k2_scan_scatter(const int32_t
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     griddep_trigger();
     for (int i = tid; i <= d; i += kScatterThreads) s_cnt[i] = 0;
-    griddep_wait();      // the histograms of the budget pass
+    __syncthreads();     // zeroed before any thread ranks its tokens (ahead of the scan's barrier)
+    griddep_wait();      // the histograms and budgets of the budget pass
+    // this CTA's tokens (positions g of the head's B*n, sequence-major): their
+    // budget loads go out first (overlapping the histogram loads and the scan),
+    // rank within their bin in shared memory, then one global reservation per
+    // non-empty bin after the scan
+    int bin[kScatterPerThread];
+    unsigned int rank[kScatterPerThread];
+#pragma unroll
+    for (int u = 0; u < kScatterPerThread; ++u) {
+        const long g = ((long)blockIdx.x * kScatterPerThread + u) * kScatterThreads + tid;
+        bin[u] = -1;
+        if (g < tokens) {
+            const long b = g / n, j = g - b * n;
+            const long t = (b * heads + h) * n + j;
+            bin[u] = exact[t] ? d : min(budgets[t], d - 1);
+        }
+    }
     const unsigned int* hh = hist + (size_t)h * (d + 1);
     // thread tid owns descending positions [tid * per, +per): bins r = d - 1 - position
     const int nb = d - 1, per = (nb + kScatterThreads - 1) / kScatterThreads;
@@ -284,6 +301,9 @@ __global__ void __launch_bounds__(kScatterThreads) k2_scan_scatter(const int32_t
         if (lane >= off) inc += v;
     }
     if (lane == 31) s_warp[wid] = inc;
+#pragma unroll
+    for (int u = 0; u < kScatterPerThread; ++u)
+        if (bin[u] >= 0) rank[u] = atomicAdd(&s_cnt[bin[u]], 1u);
     __syncthreads();
     unsigned int woff = 0;
     for (int w2 = 0; w2 < wid; ++w2) woff += s_warp[w2];
@@ -300,21 +320,6 @@ __global__ void __launch_bounds__(kScatterThreads) k2_scan_scatter(const int32_t
     if (blockIdx.x == 0 && tid == kScatterThreads - 1) {
         counts[2 * h + 0] = (int)run;           // the last thread's running total: all sampled tokens
         counts[2 * h + 1] = (int)hh[d];
-    }
-    // this CTA's tokens (positions g of the head's B*n, sequence-major): rank within
-    // their bin in shared memory, then one global reservation per non-empty bin
-    int bin[kScatterPerThread];
-    unsigned int rank[kScatterPerThread];
-#pragma unroll
-    for (int u = 0; u < kScatterPerThread; ++u) {
-        const long g = ((long)blockIdx.x * kScatterPerThread + u) * kScatterThreads + tid;
-        bin[u] = -1;
-        if (g < tokens) {
-            const long b = g / n, j = g - b * n;
-            const long t = (b * heads + h) * n + j;
-            bin[u] = exact[t] ? d : min(budgets[t], d - 1);
-            rank[u] = atomicAdd(&s_cnt[bin[u]], 1u);
-        }
     }
     __syncthreads();
     for (int i = tid; i <= d; i += kScatterThreads) {
